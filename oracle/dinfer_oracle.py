@@ -1,0 +1,333 @@
+"""CPU ORACLE for dInfer's denoise-and-commit step (arXiv 2510.08666).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+module.  The product path (``paper_2510_08666_b200``) never imports it and has
+no CPU fallback.  This module shares no code with the CUDA path: it decodes
+bf16 itself, it imports nothing from the package, and the package imports
+nothing from here.
+
+What it is: the plain definition of one iteration of the inner ``while`` loop
+of Algorithm 1 restricted to the decode side: given the
+block's hidden states, it forms the logits, the decoder's credit
+update / fuse (App. B.2), the threshold or hierarchical
+(App. B.1) commit rule, the commit, and iteration
+smoothing (App. A.1).  Everything is float64 numpy on inputs that
+are already bf16-rounded (bf16 -> float64 is exact), written in the paper's
+order and notation.  A library primitive (matmul, argmax, exp, log) is used
+as a step; there is no blocking, fusion or reordering.
+
+Readings of silent / ambiguous passages are the SURVEY.md §8(c) readings
+c1..c20, restated in DESIGN.md "Readings"; each function names the ones it
+takes.
+
+Parity pins: every function is pinned by tests under ``tests/`` (marked
+"not gpu") against worked examples, closed forms, brute force and
+invariants.  Parity unpinned: whether the
+hierarchical run rule (reading c8) is the paper's exact rule (the paper gives
+no worked example), the concrete beta/gamma/alpha values (c6), and raw-vs-
+fused p for smoothing (c13) -- these are readings, not derivations.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+DEC_THRESHOLD = 0
+DEC_HIERARCHICAL = 1
+
+
+# ---------------------------------------------------------------------------
+# bf16 decoding (own copy; the oracle shares no helper with the CUDA path)
+# ---------------------------------------------------------------------------
+def bf16_bits_to_f64(u16: np.ndarray) -> np.ndarray:
+    """bf16 bit patterns (uint16) -> exact float64 values."""
+    u32 = np.asarray(u16, dtype=np.uint16).astype(np.uint32) << np.uint32(16)
+    return u32.view(np.float32).astype(np.float64)
+
+
+# ---------------------------------------------------------------------------
+# Step 1. logits  (Alg. 1 line "logits <- M.Forward"; W_out is the
+# LM head, not tied to W_emb)
+# ---------------------------------------------------------------------------
+def logits(h: np.ndarray, W: np.ndarray) -> np.ndarray:
+    """f[s, v] = sum_k h[s, k] * W[v, k]   (h: [M, H], W: [V, H]) -> [M, V]."""
+    return np.asarray(h, np.float64) @ np.asarray(W, np.float64).T
+
+
+# ---------------------------------------------------------------------------
+# Step 2. softmax statistics  (p = Softmax(f), v* = argmax_v p)
+# ---------------------------------------------------------------------------
+def softmax_stats(f: np.ndarray):
+    """Per row: m = max_v f, v* = lowest argmax (reading c3), lse = log sum exp f,
+    p* = softmax(f)[v*] = exp(f[v*] - lse).   Returns (m, vstar, lse, pstar)."""
+    f = np.asarray(f, np.float64)
+    m = f.max(axis=1)
+    vstar = f.argmax(axis=1)                       # first occurrence = lowest id
+    lse = m + np.log(np.exp(f - m[:, None]).sum(axis=1))
+    pstar = np.exp(f[np.arange(f.shape[0]), vstar] - lse)
+    return m, vstar.astype(np.int64), lse, pstar
+
+
+def softmax(f: np.ndarray) -> np.ndarray:
+    """p = Softmax(f) row-wise, temperature 1 ("without temperature scaling")."""
+    f = np.asarray(f, np.float64)
+    e = np.exp(f - f.max(axis=1, keepdims=True))
+    return e / e.sum(axis=1, keepdims=True)
+
+
+# ---------------------------------------------------------------------------
+# Step 3a. credit update, Eq. (credit-update-top1)
+#   C_t[i, v] = beta * C_{t-1}[i, v] + p(v)^gamma   if v = v*
+#             = beta * C_{t-1}[i, v]                otherwise
+# applied to undecided positions only (reading c7); p and v* are the RAW
+# model distribution's (reading c4).
+# ---------------------------------------------------------------------------
+def credit_update(C: np.ndarray, vstar: np.ndarray, pstar: np.ndarray,
+                  undecided: np.ndarray, beta: float, gamma: float) -> np.ndarray:
+    C = np.array(C, dtype=np.float64, copy=True)
+    for i in range(C.shape[0]):
+        if not undecided[i]:
+            continue                      # decided rows are frozen (c7)
+        C[i, :] = beta * C[i, :]
+        C[i, vstar[i]] += pstar[i] ** gamma
+    return C
+
+
+# ---------------------------------------------------------------------------
+# Step 3b. credit fuse, Eq. (logits-fuse)
+#   f~[i, v] = f[i, v] + alpha * log(1 + C_t[i, v])
+# then p~ = Softmax(f~) replaces p; the committed id is argmax f~ (c5).
+# ---------------------------------------------------------------------------
+def credit_fuse(f: np.ndarray, C: np.ndarray, alpha: float) -> np.ndarray:
+    return np.asarray(f, np.float64) + alpha * np.log1p(np.asarray(C, np.float64))
+
+
+def confidence(ftilde: np.ndarray):
+    """(v~, p~, lse~): argmax of the (fused) logits (lowest id on ties) and its
+    softmax probability."""
+    m, v, lse, p = softmax_stats(ftilde)
+    return v, p, lse
+
+
+# ---------------------------------------------------------------------------
+# Step 4a. threshold decoding (Fast-dLLM), "commits tokens whose
+# confidence exceeds a preset threshold".  Reading c1: strict '>'.
+# Reading c2: if nothing clears, commit the undecided position with the
+# highest confidence (lowest index on ties).
+# ---------------------------------------------------------------------------
+def threshold_decode(ptilde, undecided, tau: float) -> np.ndarray:
+    S = len(undecided)
+    A = np.zeros(S, dtype=bool)
+    for s in range(S):
+        if undecided[s] and ptilde[s] > tau:
+            A[s] = True
+    if not A.any():
+        best = _fallback_argmax(ptilde, undecided)
+        if best is not None:
+            A[best] = True
+    return A
+
+
+def _fallback_argmax(ptilde, undecided):
+    best = None
+    for s in range(len(undecided)):
+        if undecided[s] and (best is None or ptilde[s] > ptilde[best]):
+            best = s                                # strict: lowest s on ties
+    return best
+
+
+def undecided_runs(undecided):
+    """Maximal runs [first, last] of consecutive undecided positions."""
+    runs, s, S = [], 0, len(undecided)
+    while s < S:
+        if undecided[s]:
+            first = s
+            while s + 1 < S and undecided[s + 1]:
+                s += 1
+            runs.append((first, s))
+        s += 1
+    return runs
+
+
+# ---------------------------------------------------------------------------
+# Step 4b. hierarchical decoding, P:119 and App. B.1 P:293-299.
+#   "recursively partitions masked spans into smaller sub-regions ...
+#    attempting to resolve at least one token in each region during every
+#    forward pass whenever confidence permits"; positions near the
+#   centre of each span are preferred.  Hyper-parameters: decoding
+#   threshold 0.92, lower boundary 0.62.
+# Readings c8/c9/c10: (a) commit every undecided s with p~ > theta_hi;
+# (b) sub-regions = maximal runs of undecided positions at step start
+#     (runs_after_hi=True: runs of the positions still undecided after (a),
+#     variant A'); a run with no commit from (a) commits its max-p~ position
+#     (ties: nearest the run centre, then lower index) if p~ > theta_lo;
+# (c) nothing committed at all -> global argmax fallback (c2).
+# The recursion happens across iterations: every commit splits its run.
+# ---------------------------------------------------------------------------
+def hierarchical_decode(ptilde, undecided, theta_hi: float, theta_lo: float,
+                        runs_after_hi: bool = False) -> np.ndarray:
+    S = len(undecided)
+    A = np.zeros(S, dtype=bool)
+    for s in range(S):                                            # (a)
+        if undecided[s] and ptilde[s] > theta_hi:
+            A[s] = True
+    region_mask = [bool(undecided[s]) and not (runs_after_hi and A[s]) for s in range(S)]
+    for first, last in undecided_runs(region_mask):               # (b)
+        if any(A[first:last + 1]):
+            continue
+        best = None
+        for s in range(first, last + 1):
+            if best is None or _hier_better(s, best, ptilde, first, last):
+                best = s
+        if ptilde[best] > theta_lo:
+            A[best] = True
+    if not A.any():                                               # (c)
+        best = _fallback_argmax(ptilde, undecided)
+        if best is not None:
+            A[best] = True
+    return A
+
+
+def _hier_better(s, t, ptilde, first, last) -> bool:
+    """Is position s preferred over t inside run [first, last]?  Higher p~;
+    then nearer the centre (first+last)/2 (compared as |2s-first-last|);
+    then lower index."""
+    if ptilde[s] != ptilde[t]:
+        return ptilde[s] > ptilde[t]
+    ds, dt = abs(2 * s - first - last), abs(2 * t - first - last)
+    if ds != dt:
+        return ds < dt
+    return s < t
+
+
+# ---------------------------------------------------------------------------
+# Step 6. iteration smoothing, App. A.1
+#   p_t[i] = softmax(z_t[i]); Delta e_t[i] = p_t[i] W_emb;
+#   e_{t+1}[i] = e_mask + alpha_t * Delta e_t[i]   (masked positions only)
+# Reading c13: raw softmax; c14: rows still undecided after this step's commit.
+# ---------------------------------------------------------------------------
+def smooth(f_rows: np.ndarray, E: np.ndarray, e_mask: np.ndarray, alpha_t: float) -> np.ndarray:
+    p = softmax(f_rows)
+    delta_e = p @ np.asarray(E, np.float64)
+    return np.asarray(e_mask, np.float64)[None, :] + alpha_t * delta_e
+
+
+def alpha_schedule(alpha_init: float, alpha_growth: float, alpha_preset: float, t: int) -> float:
+    """alpha_t = min(alpha_init + alpha_growth * t, alpha_preset)."""
+    return min(alpha_init + alpha_growth * t, alpha_preset)
+
+
+def tau_schedule(target: float, t: int, decay_steps: int) -> float:
+    """Decode threshold decaying from 1.0 toward `target`; reading c11:
+    linear over `decay_steps` iterations of the block, constant afterwards."""
+    if decay_steps <= 0:
+        return target
+    frac = min(t, decay_steps) / decay_steps
+    return 1.0 - (1.0 - target) * frac
+
+
+# ---------------------------------------------------------------------------
+# The whole step (one iteration of Alg. 1's inner loop, decode side)
+# ---------------------------------------------------------------------------
+@dataclass
+class Params:
+    decoder: int = DEC_THRESHOLD
+    tau: float = 0.9
+    theta_hi: float = 0.92
+    theta_lo: float = 0.62
+    use_credit: bool = False
+    c_alpha: float = 1.0
+    c_beta: float = 0.9
+    c_gamma: float = 0.5
+    use_smooth: bool = False
+    alpha_t: float = 0.1
+    hier_runs_after_hi: bool = False
+
+
+def step(h, W, E, e_mask, mask, tokens, C, params: Params, f=None):
+    """One denoise-and-commit iteration for B batch rows of a block of S.
+
+    h: [B, S, H] float64 (bf16 values); W, E: [V, H]; e_mask: [H];
+    mask: [B, S] bool (True = undecided); tokens: [B, S] int;
+    C: [B, S, V] dense credit table or None (credit off);
+    f (optional): precomputed logits [B, S, V] (reused by shard tests).
+    Returns dict with new tokens / mask / C, committed, stats and smoothed
+    (NaN rows where no smoothed embedding is produced).
+    Order: credit update -> credit fuse -> decode -> commit ->
+    smoothing capture.
+    """
+    B, S, H = h.shape
+    tokens = np.array(tokens, copy=True)
+    mask = np.array(mask, dtype=bool, copy=True)
+    C_new = None if C is None else np.array(C, dtype=np.float64, copy=True)
+    committed = np.zeros((B, S), dtype=bool)
+    out_m = np.zeros((B, S)); out_lse = np.zeros((B, S))
+    out_pt = np.zeros((B, S)); out_vt = np.zeros((B, S), dtype=np.int64)
+    out_vstar = np.zeros((B, S), dtype=np.int64); out_pstar = np.zeros((B, S))
+    smoothed = np.full((B, S, H), np.nan)
+    for b in range(B):
+        fb = logits(h[b], W) if f is None else np.asarray(f[b], np.float64)
+        m, vstar, lse, pstar = softmax_stats(fb)
+        und = mask[b].copy()
+        if params.use_credit:
+            C_new[b] = credit_update(C_new[b], vstar, pstar, und, params.c_beta, params.c_gamma)
+            vt, pt, _ = confidence(credit_fuse(fb, C_new[b], params.c_alpha))
+        else:
+            vt, pt = vstar, pstar
+        if not und.any():
+            A = np.zeros(S, dtype=bool)           # empty row: defined no-op (§8b)
+        elif params.decoder == DEC_THRESHOLD:
+            A = threshold_decode(pt, und, params.tau)
+        else:
+            A = hierarchical_decode(pt, und, params.theta_hi, params.theta_lo,
+                                    params.hier_runs_after_hi)
+        for s in range(S):                         # commit
+            if A[s]:
+                tokens[b, s] = vt[s]
+                mask[b, s] = False
+        committed[b] = A
+        out_m[b], out_lse[b], out_pt[b], out_vt[b] = m, lse, pt, vt
+        out_vstar[b], out_pstar[b] = vstar, pstar
+        if params.use_smooth:
+            still = np.nonzero(mask[b])[0]
+            if len(still):
+                smoothed[b, still] = smooth(fb[still], E, e_mask, params.alpha_t)
+    return dict(tokens=tokens, mask=mask, C=C_new, committed=committed,
+                m=out_m, lse=out_lse, ptilde=out_pt, vtilde=out_vt,
+                vstar=out_vstar, pstar=out_pstar, smoothed=smoothed)
+
+
+# ---------------------------------------------------------------------------
+# Shard-merge mode (vocab split across G ranks).
+# Each shard j reports (m_j, v*_j (global id), l_j = sum_{v in shard} e^{f-m_j},
+# acc_j = sum_{v in shard} e^{f-m_j} E[v]); the merge is the exact identity
+#   m = max_j m_j ; l = sum_j l_j e^{m_j - m} ; acc = sum_j acc_j e^{m_j - m};
+#   v* = v*_j of the maximising shard (lowest id on ties).
+# ---------------------------------------------------------------------------
+def shard_record(f_shard: np.ndarray, v_offset: int, E_shard=None):
+    f_shard = np.asarray(f_shard, np.float64)
+    m = f_shard.max(axis=1)
+    v = f_shard.argmax(axis=1) + v_offset
+    w = np.exp(f_shard - m[:, None])
+    l = w.sum(axis=1)
+    acc = None if E_shard is None else w @ np.asarray(E_shard, np.float64)
+    return dict(m=m, vstar=v, l=l, acc=acc)
+
+
+def merge_records(records):
+    m = np.max(np.stack([r["m"] for r in records]), axis=0)
+    l = np.zeros_like(m)
+    vstar = np.full(m.shape, np.iinfo(np.int64).max, dtype=np.int64)
+    acc = None
+    for r in records:                                  # fixed shard order
+        scale = np.exp(r["m"] - m)
+        l = l + r["l"] * scale
+        hit = r["m"] == m
+        vstar = np.where(hit, np.minimum(vstar, r["vstar"]), vstar)
+        if r["acc"] is not None:
+            acc = (0 if acc is None else acc) + r["acc"] * scale[:, None]
+    lse = m + np.log(l)
+    return dict(m=m, vstar=vstar, l=l, lse=lse, pstar=1.0 / l, acc=acc)
