@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""Benchmark of the fused denoise-and-commit step (dInfer, arXiv 2510.08666).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Workload (BASELINE.json metric: "denoise-step positions/sec and HBM GB/s
+fraction, LLaDA-MoE shape bs1, 1/2/4/8 B200"): configs[2], LLaDA-MoE shape
+H=2048, V=157184, block S=32, batch 1, hierarchical + credit decoding +
+iteration smoothing; the vocabulary is sharded over N GPUs (configs[3]) with
+one NCCL allgather per step.  A step = one dinfer_step (K1 vocab projection +
+stats, K2 smoothing mix, [acc reduce + allgather], K3 select/commit, K4
+smoothing finalize) on the first iteration of a block (all 32 positions
+undecided, fresh credit).  Synthetic seeded weights and planted hidden states
+(paper_2510_08666_b200.synth).  L2 is flushed (256 MiB write) before every
+timed step; inputs (1.29 GB of W + E at N=1) are also larger than L2.
+
+Prints ONE JSON line on rank 0.  --impl reference times the CPU oracle (the
+reference arm of this tier) on the host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "denoise-step positions/sec and HBM GB/s fraction, LLaDA-MoE shape bs1, 1/2/4/8 B200"
+UNIT = "positions/s"
+B, S, H, V, K = 1, 32, 2048, 157184, 32
+WORKLOAD = "LLaDA-MoE shape bs1 block32 hierarchical+credit+smoothing (BASELINE configs[2]; vocab-sharded configs[3] for N>1)"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops", 1590.0)), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, dev_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def report(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ------------------------------------------------------------------ oracle (CPU) arm
+def oracle_run(n_steps: int, n_warm: int, rows: int, budget_s: float | None = None):
+    """Time the CPU oracle (as it stands) on `rows` positions of the workload
+    per step.  Returns (seconds per step list, cores)."""
+    import oracle as O
+    from paper_2510_08666_b200 import synth
+    W = O.bf16_bits_to_f64(synth.make_W(V, H, 1))
+    E = O.bf16_bits_to_f64(synth.make_E(V, H, 2))
+    h = O.bf16_bits_to_f64(synth.planted_hidden(synth.make_W(V, H, 1), S, seed=0))[:rows].reshape(1, rows, H)
+    em = E[synth.mask_id(V)]
+    p = O.Params(decoder=O.DEC_HIERARCHICAL, theta_hi=0.92, theta_lo=0.62, use_credit=True, use_smooth=True,
+                 alpha_t=0.1)
+    times = []
+    for i in range(n_warm + n_steps):
+        mask = np.ones((1, rows), bool)
+        tok = np.full((1, rows), V - 1)
+        C = np.zeros((1, rows, V))
+        t0 = time.perf_counter()
+        O.step(h, W, E, em, mask, tok, C, p)
+        dt = time.perf_counter() - t0
+        if i >= n_warm:
+            times.append(dt)
+        if budget_s is not None and i >= n_warm and sum(times) > budget_s:
+            break
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max((d.get("num_threads", 1) for d in threadpool_info()), default=1)
+    except Exception:
+        cores = os.cpu_count()
+    return times, cores
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    rows = 8  # bounded sample: 8 of the 32 positions per step (cost ~ linear in rows)
+    times, cores = oracle_run(args.steps, args.warmup, rows)
+    sec = sum(times) / len(times)
+    value = rows / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "B": B, "S": S, "H": H, "V": V, "K": K, "decoder": "hierarchical",
+                   "credit": True, "smooth": True, "parallelism": "host cores (numpy fp64 oracle)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{rows} of {S} positions per step, full vocab {V}, fp64 numpy oracle step "
+                                   f"(logits, stats, dense credit, hierarchical, smoothing)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def gpu_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_08666_b200 import Context, build, get_unique_id, make_params, synth
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if rank == 0:
+        build.build()
+    if world > 1:
+        dist.barrier()
+    from paper_2510_08666_b200 import dinfer as _d
+    _d.lib()
+
+    # ---- synthetic inputs: this rank's vocab shard of W and E
+    v0, v1 = synth.shard_range(V, rank, world)
+    Vl = v1 - v0
+    W_u16 = synth.make_W(V, H, 1, rows=(v0, v1))
+    E_u16 = synth.make_E(V, H, 2, rows=(v0, v1))
+    em_u16 = synth.make_E(V, H, 2, rows=(V - 1, V))[0]
+    Wfull_rows = synth.make_W(V, H, 1)  # planted hidden needs W[target] rows (same on every rank)
+    hid_u16 = synth.planted_hidden(Wfull_rows, B * S, seed=0)
+    del Wfull_rows
+
+    def dev_bf16(u):
+        return torch.from_numpy(np.ascontiguousarray(u).view(np.int16)).view(torch.bfloat16).cuda()
+
+    Wd, Ed, emd, hid = dev_bf16(W_u16), dev_bf16(E_u16), dev_bf16(em_u16), dev_bf16(hid_u16)
+    del W_u16, E_u16
+
+    stream = torch.cuda.Stream()
+    nid = None
+    if world > 1:
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(get_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nid = bytes(idt.cpu().numpy().tobytes())
+    ctx = Context(B, S, H, K, V, V_local=Vl, v_offset=v0, world=world, rank=rank, stream=stream.cuda_stream,
+                  nccl_id=nid)
+    p = make_params(decoder="hierarchical", theta_hi=0.92, theta_lo=0.62, use_credit=True, use_smooth=True,
+                    alpha_t=0.1)
+
+    dev = "cuda"
+    M = B * S
+    mask = torch.ones((B, S), dtype=torch.uint8, device=dev)
+    tokens = torch.full((B, S), V - 1, dtype=torch.int32, device=dev)
+    cids = torch.full((B, S, K), -1, dtype=torch.int32, device=dev)
+    cval = torch.zeros((B, S, K), dtype=torch.float32, device=dev)
+    committed = torch.zeros((B, S), dtype=torch.uint8, device=dev)
+    smoothed = torch.zeros((B, S, H), dtype=torch.float32, device=dev)
+    stats = torch.zeros((B, S, 4), dtype=torch.float32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def reset_and_flush():
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
+            mask.fill_(1)
+            tokens.fill_(V - 1)
+            cids.fill_(-1)
+            cval.zero_()
+
+    def one_step():
+        ctx.step(hid, Wd, Ed, emd, mask, tokens, cids, cval, p, committed, smoothed, stats)
+
+    # warm-up
+    for _ in range(args.warmup):
+        reset_and_flush()
+        one_step()
+    ctx.sync()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, L2 flushed before each (outside the events)
+    ctx.set_timing(True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    phase_acc = {}
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    wall0 = time.perf_counter()
+    with sampler:
+        for i in range(args.steps):
+            reset_and_flush()
+            evs[i][0].record(stream)
+            one_step()
+            evs[i][1].record(stream)
+            ph = ctx.get_timing()  # syncs the stream (outside the event pair)
+            for k_, v_ in ph.items():
+                phase_acc[k_] = phase_acc.get(k_, 0.0) + v_
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    if world > 1:
+        dist.barrier()
+    ctx.sync()
+    ctx.set_timing(False)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms = sum(step_ms) / len(step_ms)
+    phases = {k_: v_ / args.steps for k_, v_ in phase_acc.items()}
+    if world > 1:
+        t = torch.tensor([ms] + [phases[k_] for k_ in sorted(phases)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+        for j, k_ in enumerate(sorted(phases)):
+            phases[k_] = float(t[1 + j])
+
+    # ---- e2e: the public host-buffer call (H2D of hidden + state, D2H of state + outputs)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    hid_h = pin(hid_u16.view(np.int16))
+    mask_h, tok_h = pin(np.ones((B, S), np.uint8)), pin(np.full((B, S), V - 1, np.int32))
+    cids_h, cval_h = pin(np.full((B, S, K), -1, np.int32)), pin(np.zeros((B, S, K), np.float32))
+    com_h, sm_h, st_h = pin(np.zeros((B, S), np.uint8)), pin(np.zeros((B, S, H), np.float32)), \
+        pin(np.zeros((B, S, 4), np.float32))
+    h2d = M * H * 2 + M + 4 * M + 8 * M * K
+    d2h = M + 4 * M + M + 8 * M * K + 4 * M * H + 16 * M
+    e2e_steps = max(3, min(args.steps, 50))
+    e2e_ms = []
+    for i in range(args.warmup + e2e_steps):
+        mask_h.fill_(1); tok_h.fill_(V - 1); cids_h.fill_(-1); cval_h.zero_()
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ctx.step_host(hid_h, Wd, Ed, emd, mask_h, tok_h, cids_h, cval_h, p, com_h, sm_h, st_h)
+        e1.record(stream)
+        e1.synchronize()
+        if i >= args.warmup:
+            e2e_ms.append(e0.elapsed_time(e1))
+    e2e = sum(e2e_ms) / len(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = float(t[0])
+    launches = ctx.launches_per_step(p)
+    geom = ctx.geometry()
+
+    if rank == 0:
+        hbm, _, peak_kind = peaks()
+        k1_bytes = Vl * H * 2 + M * H * 2
+        k2_bytes = Vl * H * 2 + M * H * 4
+        k1_ms, k2_ms = phases.get("k1_vocab_proj", 0.0), phases.get("k2_smooth_mix", 0.0)
+        dom, dom_bytes, dom_ms = ("k1_vocab_proj", k1_bytes, k1_ms) if k1_ms >= k2_ms else \
+            ("k2_smooth_mix", k2_bytes, k2_ms)
+        achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+        traffic = ncu_traffic().get(dom)
+        step_bytes = k1_bytes + k2_bytes
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            rows = 8
+            times, cores = oracle_run(100, 1, rows, budget_s=args.cpu_budget)
+            sec = sum(times) / len(times)
+            cpu = {"value": rows / sec, "unit": UNIT, "cores": cores, "kind": "oracle",
+                   "sample": f"{len(times)} oracle steps of {rows} of {S} positions (full vocab {V}, fp64 numpy; "
+                             f"{sum(times):.1f} s of CPU work)"}
+        line = {
+            "metric": METRIC, "value": M / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "B": B, "S": S, "H": H, "V": V, "K": K, "decoder": "hierarchical",
+                       "credit": True, "smooth": True, "vocab_shards": world, "V_local": Vl,
+                       "parallelism": f"vocab-sharded x{world} (NCCL allgather)" if world > 1 else "single GPU",
+                       "l2": "flushed (256 MiB write) before every timed step; inputs > L2"},
+            "e2e": {"value": M / (e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e, "api": "dinfer_step_host"},
+            "gpu_launches": launches * args.steps,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
+                         "algorithmic_bytes_per_launch": dom_bytes, "ms_per_launch": dom_ms},
+            "step_roofline": {"bytes": step_bytes, "achieved_gbs": step_bytes / (ms * 1e-3) / 1e9,
+                              "frac": step_bytes / (ms * 1e-3) / 1e9 / hbm},
+            "phases_ms": phases,
+            "geometry": geom,
+            "clocks": sampler.report(),
+            "wall_s_timed_loop": wall,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    ctx.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return reference_arm(args)
+    return gpu_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,209 @@
+/*
+ * dinfer.h -- C ABI of the B200-native denoise-and-commit step of dInfer
+ * (arXiv 2510.08666).  One call = one iteration of the inner `while` loop of
+ * Algorithm 1 on the decode side:
+ *
+ *   logits = hidden x W_vocab^T            (never materialised in HBM
+ *                                            for the statistics)
+ *   credit update + fuse (App. B.2), threshold or
+ *   hierarchical (App. B.1) commit rule, commit,
+ *   iteration smoothing e_{t+1} = e_mask + alpha_t * softmax(z) W_emb
+ *   (App. A.1) for positions still masked.
+ *
+ * The vocabulary may be sharded over `world` GPUs (contiguous rows of W_vocab
+ * and W_emb); per-rank partial statistics are exchanged with one NCCL
+ * allgather and every rank runs the identical combine, so decode state stays
+ * replicated and bit-identical across ranks.
+ *
+ * Conventions (all entry points):
+ *  - Every pointer is CALLER-OWNED; the library never frees or retains it
+ *    beyond the call.  "device" pointers are CUDA global memory on the ctx's
+ *    device; "host" pointers are ordinary (ideally pinned) host memory.
+ *  - bf16 tensors are passed as `const uint16_t*` holding bf16 bit patterns.
+ *  - Layouts are row-major and dense.  Flattened position index i = b*S + s.
+ *  - Host-side validation is synchronous and has no side effects; on error
+ *    nothing is enqueued.  Device work is asynchronous on the ctx stream, with
+ *    no host synchronisation and no allocation (CUDA-Graph capturable), except
+ *    dinfer_step_host and dinfer_sync which synchronise by definition.
+ *  - Asynchronous faults (CUDA, NCCL, device-checked preconditions such as a
+ *    full credit slot table) surface through dinfer_sync.
+ *  - Readings of the paper's silent points (strict '>' thresholds, lowest-id
+ *    argmax ties, fallback commit, run-based hierarchical rule, raw-softmax
+ *    smoothing, ...) are listed in DESIGN.md "Readings" (c1..c20).
+ */
+#ifndef DINFER_H
+#define DINFER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dinfer_ctx dinfer_ctx;
+
+typedef enum {
+  DINFER_OK = 0,
+  DINFER_ERR_ARG = 1,         /* null / out-of-range argument                      */
+  DINFER_ERR_SHAPE = 2,       /* inconsistent or unsupported shape / alignment     */
+  DINFER_ERR_CUDA = 3,        /* CUDA runtime error                                 */
+  DINFER_ERR_NCCL = 4,        /* NCCL error                                         */
+  DINFER_ERR_NOMEM = 5,       /* device allocation failed                           */
+  DINFER_ERR_UNSUPPORTED = 6, /* feature not available in this ctx / build          */
+  DINFER_ERR_DEVICE = 7       /* device-checked precondition violated (sticky)      */
+} dinfer_status;
+
+enum { DINFER_DEC_THRESHOLD = 0, DINFER_DEC_HIERARCHICAL = 1 };
+
+/* Problem shape, fixed at create time.
+ *   B, S      batch rows and block size; M = B*S positions, 1 <= S <= 1024,
+ *             M <= 256 (the HBM-bound swap-AB path; larger M is UNSUPPORTED).
+ *   H         hidden size, multiple of 128.
+ *   K         credit slots per position, >= 1 (K >= iterations per block is
+ *             enough for an exact credit table).
+ *   V_total   full vocabulary; V_local rows live on this rank starting at
+ *             global id v_offset; V_local % 8 == 0, V_local * world == V_total.
+ *   world, rank   vocab shards (1..8) and this rank.
+ *   smooth_capable  1 to allocate the smoothing workspace (required for
+ *             params.use_smooth).                                              */
+typedef struct {
+  int32_t B, S, H, K;
+  int64_t V_total, V_local, v_offset;
+  int32_t world, rank;
+  int32_t smooth_capable;
+} dinfer_shape;
+
+/* Per-step parameters (host struct, read synchronously).
+ *   decoder      DINFER_DEC_THRESHOLD: commit {undecided s : p~_s > tau}
+ *                (strict '>', reading c1); DINFER_DEC_HIERARCHICAL:
+ *                commit {p~ > theta_hi} plus, for every maximal run of
+ *                undecided positions without such a commit, its best position
+ *                if p~ > theta_lo (readings c8-c10; ties: nearest the
+ *                run centre, then lower index).  Both: if nothing is committed
+ *                in a batch row with undecided positions, commit its max-p~
+ *                position (reading c2).  Thresholds in [0, 1].
+ *   hier_runs_after_hi  0: runs from the mask at step start (reading c8 A);
+ *                1: runs of positions left after the theta_hi commits (A').
+ *   use_credit   credit decoding (App. B.2): C <- beta*C, C[v*] += p*^gamma for
+ *                undecided positions, then f~ = f + c_alpha*log(1+C) and p~, v~
+ *                from softmax(f~).  beta, gamma in (0,1); c_alpha >= 0.
+ *   use_smooth   iteration smoothing with weight alpha_t >= 0.       */
+typedef struct {
+  int32_t decoder;
+  float tau;
+  float theta_hi, theta_lo;
+  int32_t hier_runs_after_hi;
+  int32_t use_credit;
+  float c_alpha, c_beta, c_gamma;
+  int32_t use_smooth;
+  float alpha_t;
+} dinfer_params;
+
+/* 128-byte NCCL unique id for world > 1 (rank 0 calls it and broadcasts). */
+dinfer_status dinfer_get_unique_id(uint8_t out_id[128]);
+
+/* Create a context on the current CUDA device.  `stream` is a cudaStream_t
+ * (NULL = legacy default stream).  `nccl_unique_id`: 128 bytes from
+ * dinfer_get_unique_id (all ranks the same) when world > 1, or NULL: then the
+ * ctx has no communicator and only the split-phase calls
+ * (dinfer_step_local / dinfer_step_combine) work for world > 1.  Allocates the
+ * whole workspace once.  Errors: ARG, SHAPE, UNSUPPORTED, CUDA, NCCL, NOMEM. */
+dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_unique_id,
+                            void* stream, dinfer_ctx** out);
+void dinfer_destroy(dinfer_ctx* ctx);
+dinfer_status dinfer_set_stream(dinfer_ctx* ctx, void* stream);
+
+/* One denoise-and-commit iteration (device pointers, asynchronous).
+ *   hidden      [B,S,H] bf16, identical on every rank.
+ *   W_vocab     [V_local,H] bf16, this rank's rows of the LM head (nn.Linear).
+ *   E           [V_local,H] bf16, this rank's rows of the input embedding
+ *               W_emb; may be NULL iff !use_smooth.
+ *   e_mask      [H] bf16 mask embedding; NULL iff !use_smooth.
+ *   mask        [B,S] uint8 in/out, 1 = undecided; cleared where committed.
+ *   tokens      [B,S] int32 in/out; written only at newly committed positions.
+ *   credit_ids  [B,S,K] int32 in/out, -1 = empty slot; credit_val [B,S,K]
+ *               float in/out.  Only rows undecided at step start change.
+ *               May be NULL iff !use_credit.
+ *   committed   [B,S] uint8 out, 1 = committed by this step.
+ *   smoothed    [B,S,H] float out: e_{t+1} for rows still undecided after the
+ *               commit; other rows untouched.  NULL iff !use_smooth.
+ *   stats       [B,S,4] float out or NULL: (m = max logit, lse = log-sum-exp
+ *               of the raw logits, p~ = confidence used by the decoder,
+ *               v~ = committed/candidate id as int32 bits).
+ * A batch row with no undecided position is a defined no-op (commits
+ * nothing).  world > 1 requires a communicator (else UNSUPPORTED).           */
+dinfer_status dinfer_step(dinfer_ctx* ctx, const uint16_t* hidden, const uint16_t* W_vocab,
+                          const uint16_t* E, const uint16_t* e_mask, uint8_t* mask,
+                          int32_t* tokens, int32_t* credit_ids, float* credit_val,
+                          const dinfer_params* params, uint8_t* committed, float* smoothed,
+                          float* stats);
+
+/* Same step with HOST per-step buffers (weights stay on device): copies
+ * hidden and the decode state host->device, runs dinfer_step, copies the
+ * state and outputs back, and synchronises the stream before returning.    */
+dinfer_status dinfer_step_host(dinfer_ctx* ctx, const uint16_t* hidden_h,
+                               const uint16_t* W_vocab, const uint16_t* E,
+                               const uint16_t* e_mask, uint8_t* mask_h, int32_t* tokens_h,
+                               int32_t* credit_ids_h, float* credit_val_h,
+                               const dinfer_params* params, uint8_t* committed_h,
+                               float* smoothed_h, float* stats_h);
+
+/* Split phases (tests, caller-managed collectives).
+ * dinfer_record_words: number of fp32 words of one rank's record:
+ *   M*(4+K)  statistics: per row (m, v* as int32 bits (global id), l =
+ *            sum_{v in shard} exp(f_v - m), 0, fcred[K] = raw logit of each
+ *            credited token if this rank owns it else -inf)
+ *   + M*H    (use_smooth only) acc[s,:] = sum_{v in shard} exp(f_v - m) E[v,:].
+ * dinfer_step_local writes this rank's record to `record` (device, that many
+ * words).  dinfer_step_combine reads `records` = `world` records back to back
+ * (rank order) and performs the combine / credit / selection / commit /
+ * smoothing exactly as dinfer_step.                                          */
+size_t dinfer_record_words(const dinfer_ctx* ctx, int32_t use_smooth);
+dinfer_status dinfer_step_local(dinfer_ctx* ctx, const uint16_t* hidden, const uint16_t* W_vocab,
+                                const uint16_t* E, const uint8_t* mask, const int32_t* credit_ids,
+                                const dinfer_params* params, float* record);
+dinfer_status dinfer_step_combine(dinfer_ctx* ctx, const float* records, const uint16_t* e_mask,
+                                  uint8_t* mask, int32_t* tokens, int32_t* credit_ids,
+                                  float* credit_val, const dinfer_params* params,
+                                  uint8_t* committed, float* smoothed, float* stats);
+
+/* Block start: empty every credit slot (ids = -1, values = 0). */
+dinfer_status dinfer_credit_reset(dinfer_ctx* ctx, int32_t* credit_ids, float* credit_val);
+
+/* Host schedule helpers.
+ * alpha_t = min(init + growth*t, preset)
+ * tau_t   = 1 - (1 - target)*min(t, decay_steps)/decay_steps,
+ *           i.e. linear decay from 1.0 to target (reading c11);
+ *           decay_steps <= 0 returns target.                                 */
+float dinfer_alpha_schedule(float init, float growth, float preset, int32_t t);
+float dinfer_tau_schedule(float target, int32_t t, int32_t decay_steps);
+
+/* Synchronise the ctx stream and report asynchronous errors (CUDA, NCCL,
+ * sticky device-checked preconditions); clears the sticky device flag.      */
+dinfer_status dinfer_sync(dinfer_ctx* ctx);
+const char* dinfer_strerror(dinfer_status s);
+
+/* Instrumentation.  dinfer_set_timing(ctx, 1) brackets every kernel / the
+ * collective of subsequent steps with CUDA events on the ctx stream;
+ * dinfer_get_timing fills up to n floats with the last step's per-phase
+ * milliseconds in the order [K1 vocab_proj, K2 smooth_mix, K2r acc_reduce,
+ * C1 allgather, K3 select_commit, K4 smooth_finalize] (0 if not run); it
+ * synchronises the stream.  dinfer_launches_per_step: kernels the library
+ * launches for one dinfer_step with these params (collectives excluded).    */
+dinfer_status dinfer_set_timing(dinfer_ctx* ctx, int32_t enable);
+dinfer_status dinfer_get_timing(dinfer_ctx* ctx, float* ms, int32_t n);
+int32_t dinfer_launches_per_step(const dinfer_ctx* ctx, const dinfer_params* params);
+
+/* Geometry actually chosen (for reports): grid sizes and pipeline depth.    */
+typedef struct {
+  int32_t k1_grid, k1_stages, k1_h_resident, k1_smem;
+  int32_t k2_grid, k2_hw, k2_groups, k2_stages, k2_smem;
+  int32_t num_sms;
+} dinfer_geometry;
+dinfer_status dinfer_get_geometry(const dinfer_ctx* ctx, dinfer_geometry* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DINFER_H */

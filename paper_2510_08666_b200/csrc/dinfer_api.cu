@@ -1,0 +1,666 @@
+// dinfer_api.cu -- the C ABI declared in include/dinfer.h: context and
+// workspace management, host-side validation, TMA descriptor encoding, the
+// per-step launch sequence K1 -> K2 -> [K2r -> NCCL allgather] -> K3 -> K4,
+// NCCL communicator ownership, timing instrumentation.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "dinfer.h"
+#include "kernels.h"
+
+#ifdef DINFER_WITH_NCCL
+#include <nccl.h>
+#endif
+
+using namespace dinfer;
+
+namespace {
+
+enum Phase { kPK1 = 0, kPK2, kPK2r, kPC1, kPK3, kPK4, kNumPhases };
+
+constexpr size_t kSmemOptinFallback = 232448;
+
+}  // namespace
+
+struct dinfer_ctx {
+  dinfer_shape shp{};
+  int M = 0, N = 0, dev = 0, num_sms = 0;
+  size_t smem_optin = 0;
+  cudaStream_t stream = nullptr;
+  bool has_comm = false;
+#ifdef DINFER_WITH_NCCL
+  ncclComm_t comm = nullptr;
+#endif
+  // geometry
+  int k1_grid = 0, k1_stages = 0, k1_hres = 0, slab_rows_max = 0;
+  size_t k1_smem = 0;
+  int k2_HW = 0, k2_HS = 0, k2_VG = 0, k2_stages = 0, k2_pstages = 0, k2_nchunks = 0;
+  size_t k2_smem = 0;
+  // workspace (device)
+  float* part1 = nullptr;
+  unsigned* counter = nullptr;
+  int* err = nullptr;
+  float* rec_local = nullptr;
+  float* rec_all = nullptr;
+  float* flog = nullptr;
+  float* part2 = nullptr;
+  float* ml = nullptr;
+  size_t stats_words = 0, full_words = 0;
+  // staging for dinfer_step_host (device)
+  uint16_t* st_hidden = nullptr;
+  uint8_t* st_mask = nullptr;
+  int32_t* st_tokens = nullptr;
+  int32_t* st_cids = nullptr;
+  float* st_cval = nullptr;
+  uint8_t* st_committed = nullptr;
+  float* st_smoothed = nullptr;
+  float* st_stats = nullptr;
+  // tensor-map cache
+  const void* c_w = nullptr;
+  const void* c_h = nullptr;
+  const void* c_e = nullptr;
+  CUtensorMap map_w{}, map_w8{}, map_h{}, map_e{};
+  // timing
+  int timing = 0;
+  cudaEvent_t ev_beg[kNumPhases]{}, ev_end[kNumPhases]{};
+  bool ev_used[kNumPhases]{};
+};
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (fn == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor [outer][inner] row-major, SWIZZLE_128B box [box_outer][box_inner].
+bool encode_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
+               uint32_t box_outer) {
+  auto fn = tmap_encoder();
+  if (fn == nullptr) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+template <typename T>
+dinfer_status dev_alloc(T** p, size_t count) {
+  if (count == 0) {
+    *p = nullptr;
+    return DINFER_OK;
+  }
+  if (cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)) != cudaSuccess) {
+    cudaGetLastError();
+    return DINFER_ERR_NOMEM;
+  }
+  return DINFER_OK;
+}
+
+#define DI_CUDA(call)                                 \
+  do {                                                \
+    cudaError_t e_ = (call);                          \
+    if (e_ != cudaSuccess) return DINFER_ERR_CUDA;    \
+  } while (0)
+
+void ev_begin(dinfer_ctx* c, int ph) {
+  if (c->timing) {
+    cudaEventRecord(c->ev_beg[ph], c->stream);
+    c->ev_used[ph] = true;
+  }
+}
+void ev_finish(dinfer_ctx* c, int ph) {
+  if (c->timing) cudaEventRecord(c->ev_end[ph], c->stream);
+}
+
+dinfer_status check_params(const dinfer_ctx* c, const dinfer_params* p) {
+  if (p == nullptr) return DINFER_ERR_ARG;
+  if (p->decoder != DINFER_DEC_THRESHOLD && p->decoder != DINFER_DEC_HIERARCHICAL) return DINFER_ERR_ARG;
+  auto unit = [](float x) { return x >= 0.f && x <= 1.f; };
+  if (!unit(p->tau) || !unit(p->theta_hi) || !unit(p->theta_lo)) return DINFER_ERR_ARG;
+  if (p->use_credit) {
+    if (!(p->c_beta > 0.f && p->c_beta < 1.f) || !(p->c_gamma > 0.f && p->c_gamma < 1.f) || !(p->c_alpha >= 0.f))
+      return DINFER_ERR_ARG;
+  }
+  if (p->use_smooth) {
+    if (!c->shp.smooth_capable) return DINFER_ERR_UNSUPPORTED;
+    if (!(p->alpha_t >= 0.f)) return DINFER_ERR_ARG;
+  }
+  return DINFER_OK;
+}
+
+dinfer_status ensure_maps(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W, const uint16_t* E) {
+  const uint64_t H = static_cast<uint64_t>(c->shp.H);
+  if (W != c->c_w) {
+    if (!encode_2d(&c->map_w, W, H, static_cast<uint64_t>(c->shp.V_local), kKChunk, kTileRows) ||
+        !encode_2d(&c->map_w8, W, H, static_cast<uint64_t>(c->shp.V_local), kKChunk, kRowGran))
+      return DINFER_ERR_CUDA;
+    c->c_w = W;
+  }
+  if (hidden != c->c_h) {
+    if (!encode_2d(&c->map_h, hidden, H, static_cast<uint64_t>(c->M), kKChunk, static_cast<uint32_t>(c->N)))
+      return DINFER_ERR_CUDA;
+    c->c_h = hidden;
+  }
+  if (E != nullptr && E != c->c_e) {
+    if (!encode_2d(&c->map_e, E, H, static_cast<uint64_t>(c->shp.V_local), 64, kKChunk)) return DINFER_ERR_CUDA;
+    c->c_e = E;
+  }
+  return DINFER_OK;
+}
+
+// K1 (+ K2, + K2r into the record when `reduce_acc`).  `rec` receives the
+// statistics part of this rank's record (and the acc part when reduce_acc).
+dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W, const uint16_t* E,
+                        const uint8_t* mask, const int32_t* credit_ids, const dinfer_params* p, float* rec,
+                        bool reduce_acc) {
+  const bool smooth = p->use_smooth != 0;
+  dinfer_status s = ensure_maps(c, hidden, W, smooth ? E : nullptr);
+  if (s != DINFER_OK) return s;
+  K1Args a{};
+  a.M = c->M;
+  a.N = c->N;
+  a.H = c->shp.H;
+  a.K = c->shp.K;
+  a.V_local = static_cast<int>(c->shp.V_local);
+  a.v_offset = static_cast<int>(c->shp.v_offset);
+  a.num_kc = c->shp.H / kKChunk;
+  a.h_resident = c->k1_hres;
+  a.stages = c->k1_stages;
+  a.slab_rows_max = c->slab_rows_max;
+  a.mask = mask;
+  a.credit_ids = p->use_credit ? credit_ids : nullptr;
+  a.part = c->part1;
+  a.counter = c->counter;
+  a.rec = rec;
+  a.flog = smooth ? c->flog : nullptr;
+  a.err = c->err;
+  ev_begin(c, kPK1);
+  DI_CUDA(launch_k1(c->map_w, c->map_w8, c->map_h, a, c->k1_grid, c->k1_smem, c->stream));
+  ev_finish(c, kPK1);
+  if (smooth) {
+    K2Args b{};
+    b.M = c->M;
+    b.N = c->N;
+    b.H = c->shp.H;
+    b.V_local = static_cast<int>(c->shp.V_local);
+    b.HW = c->k2_HW;
+    b.nsub = c->k2_HW / 128;
+    b.HS = c->k2_HS;
+    b.VG = c->k2_VG;
+    b.nchunks = c->k2_nchunks;
+    b.stages = c->k2_stages;
+    b.pstages = c->k2_pstages;
+    b.flog = c->flog;
+    b.rec = rec;
+    b.rec_stride = kStatWords + c->shp.K;
+    b.part = c->part2;
+    ev_begin(c, kPK2);
+    DI_CUDA(launch_k2(c->map_e, b, c->k2_smem, c->stream));
+    ev_finish(c, kPK2);
+    if (reduce_acc) {
+      ev_begin(c, kPK2r);
+      DI_CUDA(launch_acc_reduce(c->part2, c->k2_VG, c->M * c->shp.H, rec + c->stats_words, c->stream));
+      ev_finish(c, kPK2r);
+    }
+  }
+  return DINFER_OK;
+}
+
+// K3 (+ K4).  `recs` = `world` records spaced `rec_words` apart.  When
+// `acc_from_part2`, K4 sums the VG partials of this (single) rank directly.
+dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, int world, bool acc_from_part2,
+                          const uint16_t* e_mask, uint8_t* mask, int32_t* tokens, int32_t* credit_ids,
+                          float* credit_val, const dinfer_params* p, uint8_t* committed, float* smoothed,
+                          float* stats) {
+  K3Args k{};
+  k.B = c->shp.B;
+  k.S = c->shp.S;
+  k.K = c->shp.K;
+  k.world = world;
+  k.recs = recs;
+  k.rec_words = static_cast<long>(rec_words);
+  k.rec_stride = kStatWords + c->shp.K;
+  k.mask = mask;
+  k.tokens = tokens;
+  k.credit_ids = credit_ids;
+  k.credit_val = credit_val;
+  k.committed = committed;
+  k.stats = stats;
+  k.ml = c->ml;
+  k.decoder = p->decoder;
+  k.runs_after_hi = p->hier_runs_after_hi;
+  k.use_credit = p->use_credit;
+  k.tau = p->tau;
+  k.theta_hi = p->theta_hi;
+  k.theta_lo = p->theta_lo;
+  k.c_alpha = p->c_alpha;
+  k.c_beta = p->c_beta;
+  k.c_gamma = p->c_gamma;
+  k.err = c->err;
+  ev_begin(c, kPK3);
+  DI_CUDA(launch_k3(k, c->stream));
+  ev_finish(c, kPK3);
+  if (p->use_smooth) {
+    K4Args f{};
+    f.M = c->M;
+    f.H = c->shp.H;
+    if (acc_from_part2) {
+      f.acc = c->part2;
+      f.acc_stride = static_cast<long>(c->M) * c->shp.H;
+      f.nparts = c->k2_VG;
+      f.m_part = nullptr;  // all partials are relative to the (only) rank's max
+    } else {
+      f.acc = recs + c->stats_words;
+      f.acc_stride = static_cast<long>(rec_words);
+      f.nparts = world;
+      f.m_part = recs;
+      f.m_stride = static_cast<long>(rec_words);
+      f.m_rowstride = kStatWords + c->shp.K;
+    }
+    f.ml = c->ml;
+    f.mask = mask;
+    f.e_mask = e_mask;
+    f.alpha_t = p->alpha_t;
+    f.out = smoothed;
+    ev_begin(c, kPK4);
+    DI_CUDA(launch_k4(f, c->stream));
+    ev_finish(c, kPK4);
+  }
+  return DINFER_OK;
+}
+
+dinfer_status check_step_ptrs(const dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W, const uint16_t* E,
+                              const uint16_t* e_mask, const uint8_t* mask, const int32_t* tokens,
+                              const int32_t* cids, const float* cval, const dinfer_params* p,
+                              const uint8_t* committed, const float* smoothed) {
+  if (hidden == nullptr || W == nullptr || mask == nullptr || tokens == nullptr || committed == nullptr)
+    return DINFER_ERR_ARG;
+  if (!aligned(hidden, 16) || !aligned(W, 16)) return DINFER_ERR_SHAPE;
+  if (p->use_credit && (cids == nullptr || cval == nullptr)) return DINFER_ERR_ARG;
+  if (p->use_smooth) {
+    if (E == nullptr || e_mask == nullptr || smoothed == nullptr) return DINFER_ERR_ARG;
+    if (!aligned(E, 16) || !aligned(e_mask, 8) || !aligned(smoothed, 16)) return DINFER_ERR_SHAPE;
+  }
+  (void)c;
+  return DINFER_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dinfer_strerror(dinfer_status s) {
+  switch (s) {
+    case DINFER_OK: return "ok";
+    case DINFER_ERR_ARG: return "invalid argument";
+    case DINFER_ERR_SHAPE: return "unsupported or inconsistent shape / alignment";
+    case DINFER_ERR_CUDA: return "CUDA error";
+    case DINFER_ERR_NCCL: return "NCCL error";
+    case DINFER_ERR_NOMEM: return "device allocation failed";
+    case DINFER_ERR_UNSUPPORTED: return "unsupported in this context / build";
+    case DINFER_ERR_DEVICE: return "device-checked precondition violated (credit slots full or entry overflow)";
+  }
+  return "unknown status";
+}
+
+dinfer_status dinfer_get_unique_id(uint8_t out_id[128]) {
+  if (out_id == nullptr) return DINFER_ERR_ARG;
+#ifdef DINFER_WITH_NCCL
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return DINFER_ERR_NCCL;
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  std::memcpy(out_id, &id, 128);
+  return DINFER_OK;
+#else
+  return DINFER_ERR_UNSUPPORTED;
+#endif
+}
+
+float dinfer_alpha_schedule(float init, float growth, float preset, int32_t t) {
+  return std::fmin(init + growth * static_cast<float>(t), preset);
+}
+
+float dinfer_tau_schedule(float target, int32_t t, int32_t decay_steps) {
+  if (decay_steps <= 0) return target;
+  const int tt = t < 0 ? 0 : (t > decay_steps ? decay_steps : t);
+  return 1.0f - (1.0f - target) * static_cast<float>(tt) / static_cast<float>(decay_steps);
+}
+
+void dinfer_destroy(dinfer_ctx* c) {
+  if (c == nullptr) return;
+  cudaStreamSynchronize(c->stream);
+#ifdef DINFER_WITH_NCCL
+  if (c->has_comm) ncclCommDestroy(c->comm);
+#endif
+  void* bufs[] = {c->part1, c->counter, c->err, c->rec_local, c->flog, c->part2, c->ml,
+                  c->st_hidden, c->st_mask, c->st_tokens, c->st_cids, c->st_cval, c->st_committed,
+                  c->st_smoothed, c->st_stats};
+  for (void* b : bufs)
+    if (b != nullptr) cudaFree(b);
+  if (c->rec_all != nullptr && c->rec_all != c->rec_local) cudaFree(c->rec_all);
+  for (int i = 0; i < kNumPhases; ++i) {
+    if (c->ev_beg[i]) cudaEventDestroy(c->ev_beg[i]);
+    if (c->ev_end[i]) cudaEventDestroy(c->ev_end[i]);
+  }
+  delete c;
+}
+
+dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_unique_id, void* stream,
+                            dinfer_ctx** out) {
+  if (shape == nullptr || out == nullptr) return DINFER_ERR_ARG;
+  *out = nullptr;
+  const dinfer_shape& s = *shape;
+  if (s.B < 1 || s.S < 1 || s.S > 1024 || s.K < 1 || s.H < 128) return DINFER_ERR_SHAPE;
+  const long M = static_cast<long>(s.B) * s.S;
+  if (M > 256) return DINFER_ERR_UNSUPPORTED;  // HBM-bound swap-AB path only
+  if (s.H % 128 != 0 || s.H > 16384) return DINFER_ERR_SHAPE;
+  if (s.world < 1 || s.world > 8 || s.rank < 0 || s.rank >= s.world) return DINFER_ERR_SHAPE;
+  if (s.V_local < 8 || s.V_local % 8 != 0 || s.V_local * s.world != s.V_total) return DINFER_ERR_SHAPE;
+  if (s.v_offset < 0 || s.v_offset + s.V_local > s.V_total || s.V_total >= (1LL << 31)) return DINFER_ERR_SHAPE;
+  if (s.K > 32767) return DINFER_ERR_SHAPE;
+
+  dinfer_ctx* c = new (std::nothrow) dinfer_ctx();
+  if (c == nullptr) return DINFER_ERR_NOMEM;
+  c->shp = s;
+  c->M = static_cast<int>(M);
+  c->N = static_cast<int>(((M + 15) / 16) * 16);
+  if (c->N % 32 != 0) c->N += 16;  // epilogue works in 32-column groups
+  c->stream = static_cast<cudaStream_t>(stream);
+  if (cudaGetDevice(&c->dev) != cudaSuccess) { delete c; return DINFER_ERR_CUDA; }
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->dev);
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);
+  c->smem_optin = optin > 0 ? static_cast<size_t>(optin) : kSmemOptinFallback;
+  int cc_major = 0;
+  cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, c->dev);
+  if (cc_major != 10) { delete c; return DINFER_ERR_UNSUPPORTED; }  // sm_100a only
+
+  // ---- K1 geometry: one CTA per SM over equal 8-row-granular vocab slabs
+  const long g8 = s.V_local / kRowGran;
+  c->k1_grid = static_cast<int>(std::min<long>(c->num_sms, std::max<long>(1, (s.V_local + kTileRows - 1) / kTileRows)));
+  c->slab_rows_max = static_cast<int>(kRowGran * ((g8 + c->k1_grid - 1) / c->k1_grid));
+  const bool h_fits = static_cast<long>(c->N) * s.H * 2 <= 128 * 1024;
+  c->k1_hres = 0;
+  c->k1_stages = 0;
+  if (h_fits) {
+    for (int st = 8; st >= 3; --st)
+      if (k1_smem_bytes(c->N, s.H, st, 1, c->slab_rows_max) <= c->smem_optin) {
+        c->k1_hres = 1;
+        c->k1_stages = st;
+        break;
+      }
+  }
+  if (!c->k1_hres) {
+    for (int st = 8; st >= 2; --st)
+      if (k1_smem_bytes(c->N, s.H, st, 0, c->slab_rows_max) <= c->smem_optin) {
+        c->k1_stages = st;
+        break;
+      }
+  }
+  if (c->k1_stages == 0) { delete c; return DINFER_ERR_UNSUPPORTED; }
+  c->k1_smem = k1_smem_bytes(c->N, s.H, c->k1_stages, c->k1_hres, c->slab_rows_max);
+
+  // ---- K2 geometry: hidden slices x vocab groups <= #SMs
+  c->k2_nchunks = static_cast<int>((s.V_local + kKChunk - 1) / kKChunk);
+  c->k2_HW = (s.H % 256 == 0) ? 256 : 128;
+  c->k2_HS = s.H / c->k2_HW;
+  c->k2_VG = std::max(1, std::min(c->num_sms / std::max(1, c->k2_HS), c->k2_nchunks));
+  c->k2_pstages = 4;
+  for (int st = 6; st >= 2; --st)
+    if (k2_smem_bytes(c->N, c->k2_HW, st, c->k2_pstages) <= c->smem_optin) {
+      c->k2_stages = st;
+      break;
+    }
+  c->k2_smem = k2_smem_bytes(c->N, c->k2_HW, std::max(2, c->k2_stages), c->k2_pstages);
+
+  // ---- workspace
+  c->stats_words = static_cast<size_t>(M) * (kStatWords + s.K);
+  c->full_words = c->stats_words + (s.smooth_capable ? static_cast<size_t>(M) * s.H : 0);
+  dinfer_status st = DINFER_OK;
+  auto A = [&](dinfer_status x) { if (st == DINFER_OK) st = x; };
+  A(dev_alloc(&c->part1, static_cast<size_t>(c->k1_grid) * M * 3));
+  A(dev_alloc(&c->counter, 4));
+  A(dev_alloc(&c->err, 4));
+  A(dev_alloc(&c->rec_local, c->full_words));
+  A(dev_alloc(&c->ml, static_cast<size_t>(M) * 2));
+  if (s.world > 1) A(dev_alloc(&c->rec_all, c->full_words * s.world));
+  else c->rec_all = c->rec_local;
+  if (s.smooth_capable) {
+    A(dev_alloc(&c->flog, static_cast<size_t>(M) * s.V_local));
+    A(dev_alloc(&c->part2, static_cast<size_t>(c->k2_VG) * M * s.H));
+  }
+  if (st == DINFER_OK) {
+    if (cudaMemset(c->counter, 0, 16) != cudaSuccess || cudaMemset(c->err, 0, 16) != cudaSuccess ||
+        cudaMemset(c->rec_local, 0, c->full_words * 4) != cudaSuccess)
+      st = DINFER_ERR_CUDA;
+  }
+  for (int i = 0; i < kNumPhases && st == DINFER_OK; ++i) {
+    if (cudaEventCreate(&c->ev_beg[i]) != cudaSuccess || cudaEventCreate(&c->ev_end[i]) != cudaSuccess)
+      st = DINFER_ERR_CUDA;
+  }
+#ifdef DINFER_WITH_NCCL
+  if (st == DINFER_OK && s.world > 1 && nccl_unique_id != nullptr) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, 128);
+    if (ncclCommInitRank(&c->comm, s.world, id, s.rank) != ncclSuccess) st = DINFER_ERR_NCCL;
+    else c->has_comm = true;
+  }
+#else
+  (void)nccl_unique_id;
+#endif
+  if (st != DINFER_OK) {
+    dinfer_destroy(c);
+    return st;
+  }
+  *out = c;
+  return DINFER_OK;
+}
+
+dinfer_status dinfer_set_stream(dinfer_ctx* c, void* stream) {
+  if (c == nullptr) return DINFER_ERR_ARG;
+  c->stream = static_cast<cudaStream_t>(stream);
+  return DINFER_OK;
+}
+
+size_t dinfer_record_words(const dinfer_ctx* c, int32_t use_smooth) {
+  if (c == nullptr) return 0;
+  return use_smooth ? c->full_words : c->stats_words;
+}
+
+dinfer_status dinfer_step(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W, const uint16_t* E,
+                          const uint16_t* e_mask, uint8_t* mask, int32_t* tokens, int32_t* credit_ids,
+                          float* credit_val, const dinfer_params* p, uint8_t* committed, float* smoothed,
+                          float* stats) {
+  if (c == nullptr) return DINFER_ERR_ARG;
+  dinfer_status s = check_params(c, p);
+  if (s != DINFER_OK) return s;
+  s = check_step_ptrs(c, hidden, W, E, e_mask, mask, tokens, credit_ids, credit_val, p, committed, smoothed);
+  if (s != DINFER_OK) return s;
+  const int world = c->shp.world;
+  if (world > 1 && !c->has_comm) return DINFER_ERR_UNSUPPORTED;
+  for (int i = 0; i < kNumPhases; ++i) c->ev_used[i] = false;
+  const bool smooth = p->use_smooth != 0;
+  s = run_local(c, hidden, W, E, mask, credit_ids, p, c->rec_local, /*reduce_acc=*/world > 1);
+  if (s != DINFER_OK) return s;
+  size_t words = smooth ? c->full_words : c->stats_words;
+  if (world > 1) {
+#ifdef DINFER_WITH_NCCL
+    ev_begin(c, kPC1);
+    if (ncclAllGather(c->rec_local, c->rec_all, words, ncclFloat, c->comm, c->stream) != ncclSuccess)
+      return DINFER_ERR_NCCL;
+    ev_finish(c, kPC1);
+#else
+    return DINFER_ERR_UNSUPPORTED;
+#endif
+  }
+  return run_combine(c, c->rec_all, words, world, /*acc_from_part2=*/world == 1, e_mask, mask, tokens, credit_ids,
+                     credit_val, p, committed, smoothed, stats);
+}
+
+dinfer_status dinfer_step_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W, const uint16_t* E,
+                                const uint8_t* mask, const int32_t* credit_ids, const dinfer_params* p,
+                                float* record) {
+  if (c == nullptr || record == nullptr) return DINFER_ERR_ARG;
+  dinfer_status s = check_params(c, p);
+  if (s != DINFER_OK) return s;
+  if (hidden == nullptr || W == nullptr || mask == nullptr) return DINFER_ERR_ARG;
+  if (!aligned(hidden, 16) || !aligned(W, 16) || !aligned(record, 16)) return DINFER_ERR_SHAPE;
+  if (p->use_credit && credit_ids == nullptr) return DINFER_ERR_ARG;
+  if (p->use_smooth && (E == nullptr || !aligned(E, 16))) return DINFER_ERR_ARG;
+  for (int i = 0; i < kNumPhases; ++i) c->ev_used[i] = false;
+  return run_local(c, hidden, W, E, mask, credit_ids, p, record, /*reduce_acc=*/true);
+}
+
+dinfer_status dinfer_step_combine(dinfer_ctx* c, const float* records, const uint16_t* e_mask, uint8_t* mask,
+                                  int32_t* tokens, int32_t* credit_ids, float* credit_val, const dinfer_params* p,
+                                  uint8_t* committed, float* smoothed, float* stats) {
+  if (c == nullptr || records == nullptr) return DINFER_ERR_ARG;
+  dinfer_status s = check_params(c, p);
+  if (s != DINFER_OK) return s;
+  if (mask == nullptr || tokens == nullptr || committed == nullptr) return DINFER_ERR_ARG;
+  if (p->use_credit && (credit_ids == nullptr || credit_val == nullptr)) return DINFER_ERR_ARG;
+  if (p->use_smooth && (e_mask == nullptr || smoothed == nullptr || !aligned(records, 16) ||
+                        !aligned(e_mask, 8) || !aligned(smoothed, 16)))
+    return DINFER_ERR_ARG;
+  const size_t words = p->use_smooth ? c->full_words : c->stats_words;
+  return run_combine(c, records, words, c->shp.world, /*acc_from_part2=*/false, e_mask, mask, tokens, credit_ids,
+                     credit_val, p, committed, smoothed, stats);
+}
+
+dinfer_status dinfer_step_host(dinfer_ctx* c, const uint16_t* hidden_h, const uint16_t* W, const uint16_t* E,
+                               const uint16_t* e_mask, uint8_t* mask_h, int32_t* tokens_h, int32_t* cids_h,
+                               float* cval_h, const dinfer_params* p, uint8_t* committed_h, float* smoothed_h,
+                               float* stats_h) {
+  if (c == nullptr || p == nullptr || hidden_h == nullptr || mask_h == nullptr || tokens_h == nullptr ||
+      committed_h == nullptr)
+    return DINFER_ERR_ARG;
+  if (p->use_credit && (cids_h == nullptr || cval_h == nullptr)) return DINFER_ERR_ARG;
+  if (p->use_smooth && smoothed_h == nullptr) return DINFER_ERR_ARG;
+  const size_t M = static_cast<size_t>(c->M), H = static_cast<size_t>(c->shp.H), K = static_cast<size_t>(c->shp.K);
+  if (c->st_hidden == nullptr) {  // first call: staging buffers (not in the graph-capturable path)
+    dinfer_status st = DINFER_OK;
+    auto A = [&](dinfer_status x) { if (st == DINFER_OK) st = x; };
+    A(dev_alloc(&c->st_hidden, M * H));
+    A(dev_alloc(&c->st_mask, M));
+    A(dev_alloc(&c->st_tokens, M));
+    A(dev_alloc(&c->st_cids, M * K));
+    A(dev_alloc(&c->st_cval, M * K));
+    A(dev_alloc(&c->st_committed, M));
+    A(dev_alloc(&c->st_stats, M * 4));
+    if (c->shp.smooth_capable) A(dev_alloc(&c->st_smoothed, M * H));
+    if (st != DINFER_OK) return st;
+  }
+  cudaStream_t sm = c->stream;
+  DI_CUDA(cudaMemcpyAsync(c->st_hidden, hidden_h, M * H * 2, cudaMemcpyHostToDevice, sm));
+  DI_CUDA(cudaMemcpyAsync(c->st_mask, mask_h, M, cudaMemcpyHostToDevice, sm));
+  DI_CUDA(cudaMemcpyAsync(c->st_tokens, tokens_h, M * 4, cudaMemcpyHostToDevice, sm));
+  if (p->use_credit) {
+    DI_CUDA(cudaMemcpyAsync(c->st_cids, cids_h, M * K * 4, cudaMemcpyHostToDevice, sm));
+    DI_CUDA(cudaMemcpyAsync(c->st_cval, cval_h, M * K * 4, cudaMemcpyHostToDevice, sm));
+  }
+  dinfer_status s = dinfer_step(c, c->st_hidden, W, E, e_mask, c->st_mask, c->st_tokens,
+                                p->use_credit ? c->st_cids : nullptr, p->use_credit ? c->st_cval : nullptr, p,
+                                c->st_committed, p->use_smooth ? c->st_smoothed : nullptr, c->st_stats);
+  if (s != DINFER_OK) return s;
+  DI_CUDA(cudaMemcpyAsync(mask_h, c->st_mask, M, cudaMemcpyDeviceToHost, sm));
+  DI_CUDA(cudaMemcpyAsync(tokens_h, c->st_tokens, M * 4, cudaMemcpyDeviceToHost, sm));
+  DI_CUDA(cudaMemcpyAsync(committed_h, c->st_committed, M, cudaMemcpyDeviceToHost, sm));
+  if (p->use_credit) {
+    DI_CUDA(cudaMemcpyAsync(cids_h, c->st_cids, M * K * 4, cudaMemcpyDeviceToHost, sm));
+    DI_CUDA(cudaMemcpyAsync(cval_h, c->st_cval, M * K * 4, cudaMemcpyDeviceToHost, sm));
+  }
+  if (p->use_smooth) DI_CUDA(cudaMemcpyAsync(smoothed_h, c->st_smoothed, M * H * 4, cudaMemcpyDeviceToHost, sm));
+  if (stats_h != nullptr) DI_CUDA(cudaMemcpyAsync(stats_h, c->st_stats, M * 16, cudaMemcpyDeviceToHost, sm));
+  DI_CUDA(cudaStreamSynchronize(sm));
+  return DINFER_OK;
+}
+
+dinfer_status dinfer_credit_reset(dinfer_ctx* c, int32_t* credit_ids, float* credit_val) {
+  if (c == nullptr || credit_ids == nullptr || credit_val == nullptr) return DINFER_ERR_ARG;
+  const size_t n = static_cast<size_t>(c->M) * c->shp.K;
+  DI_CUDA(cudaMemsetAsync(credit_ids, 0xFF, n * 4, c->stream));  // -1
+  DI_CUDA(cudaMemsetAsync(credit_val, 0, n * 4, c->stream));
+  return DINFER_OK;
+}
+
+dinfer_status dinfer_sync(dinfer_ctx* c) {
+  if (c == nullptr) return DINFER_ERR_ARG;
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return DINFER_ERR_CUDA;
+#ifdef DINFER_WITH_NCCL
+  if (c->has_comm) {
+    ncclResult_t ar = ncclSuccess;
+    if (ncclCommGetAsyncError(c->comm, &ar) != ncclSuccess || ar != ncclSuccess) return DINFER_ERR_NCCL;
+  }
+#endif
+  int flag = 0;
+  if (cudaMemcpy(&flag, c->err, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return DINFER_ERR_CUDA;
+  if (flag != 0) {
+    cudaMemset(c->err, 0, 4);
+    return DINFER_ERR_DEVICE;
+  }
+  return DINFER_OK;
+}
+
+dinfer_status dinfer_set_timing(dinfer_ctx* c, int32_t enable) {
+  if (c == nullptr) return DINFER_ERR_ARG;
+  c->timing = enable ? 1 : 0;
+  return DINFER_OK;
+}
+
+dinfer_status dinfer_get_timing(dinfer_ctx* c, float* ms, int32_t n) {
+  if (c == nullptr || ms == nullptr) return DINFER_ERR_ARG;
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return DINFER_ERR_CUDA;
+  for (int i = 0; i < n && i < kNumPhases; ++i) {
+    ms[i] = 0.f;
+    if (c->timing && c->ev_used[i]) {
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, c->ev_beg[i], c->ev_end[i]) == cudaSuccess) ms[i] = t;
+    }
+  }
+  return DINFER_OK;
+}
+
+int32_t dinfer_launches_per_step(const dinfer_ctx* c, const dinfer_params* p) {
+  if (c == nullptr || p == nullptr) return 0;
+  int n = 2;  // K1, K3
+  if (p->use_smooth) n += 2 + (c->shp.world > 1 ? 1 : 0);
+  return n;
+}
+
+dinfer_status dinfer_get_geometry(const dinfer_ctx* c, dinfer_geometry* g) {
+  if (c == nullptr || g == nullptr) return DINFER_ERR_ARG;
+  g->k1_grid = c->k1_grid;
+  g->k1_stages = c->k1_stages;
+  g->k1_h_resident = c->k1_hres;
+  g->k1_smem = static_cast<int32_t>(c->k1_smem);
+  g->k2_grid = c->k2_HS * c->k2_VG;
+  g->k2_hw = c->k2_HW;
+  g->k2_groups = c->k2_VG;
+  g->k2_stages = c->k2_stages;
+  g->k2_smem = static_cast<int32_t>(c->k2_smem);
+  g->num_sms = c->num_sms;
+  return DINFER_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,395 @@
+// K1 vocab_proj -- LM-head contraction fused with the softmax-statistics
+// epilogue (PAPER.md:95-96 logits; P:278 softmax; P:305 v* = argmax).
+//
+//   logits^T[v, s] = W[v, :] . h[s, :]       (swap-AB: vocab on UMMA M = 128,
+//                                              positions on UMMA N = M_pos)
+// Per (position s) the kernel produces m = max_v f, v* = lowest argmax id,
+// l = sum_v exp(f - m) over this rank's vocab shard; the logits never leave
+// TMEM except (a) the raw value of credited tokens (credit fuse)
+// and (b) -- only when smoothing is on -- an fp32 copy for the smoothing mix
+// (DESIGN.md "K2 v1").
+//
+// Structure (one CTA per SM, persistent over a contiguous vocab slab):
+//   warp 4    TMA producer: W chunks [128 rows x 64 k] (SWIZZLE_128B) into a
+//             `stages`-deep ring; hidden either resident (loaded once) or
+//             streamed with each W chunk.
+//   warp 5    MMA issuer: tcgen05.mma.cta_group::1.kind::f16 128xNx16, fp32
+//             accumulator double-buffered in TMEM (2 x N columns).
+//   warps 0-3 epilogue: tcgen05.ld 32 columns per lane (lane = vocab row),
+//             warp-shuffle reduce-scatter of (m, idx, l) across the 32 rows
+//             (31 pairwise merges per 32x32 block), running merge per column.
+//   End: cross-warp merge -> per-CTA partial -> last CTA merges all partials
+//   in fixed order (deterministic) into the rank record.
+#include <climits>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace dinfer {
+namespace {
+
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = (kEpiWarps + 2) * kWarpThreads;
+constexpr uint32_t kWStageBytes = kTileRows * 128;  // 16 KB
+constexpr int kMaxGroups = 8;                       // N <= 256
+
+__host__ __device__ inline uint32_t tmem_cols_pow2(uint32_t n) {
+  uint32_t c = 32;
+  while (c < n) c <<= 1;
+  return c;
+}
+
+DI float pick32(const float (&x)[32], int j) {
+  float r = 0.f;
+#pragma unroll
+  for (int q = 0; q < 32; ++q) r = (q == j) ? x[q] : r;
+  return r;
+}
+
+// One reduce-scatter level: 2*O values per lane -> O values, merging with the
+// partner lane (lane ^ O).  Lanes with bit O set keep the upper half.
+template <int O>
+DI void rs_level(float* m, int* ix, float* l, bool up) {
+#pragma unroll
+  for (int k = 0; k < O; ++k) {
+    float km = up ? m[k + O] : m[k];
+    int ki = up ? ix[k + O] : ix[k];
+    float kl = up ? l[k + O] : l[k];
+    const float sm = up ? m[k] : m[k + O];
+    const int si = up ? ix[k] : ix[k + O];
+    const float sl = up ? l[k] : l[k + O];
+    const float rm = __shfl_xor_sync(0xffffffffu, sm, O);
+    const int ri = __shfl_xor_sync(0xffffffffu, si, O);
+    const float rl = __shfl_xor_sync(0xffffffffu, sl, O);
+    stat_combine(km, ki, kl, rm, ri, rl);
+    m[k] = km;
+    ix[k] = ki;
+    l[k] = kl;
+  }
+}
+
+DI void named_bar_epi() { asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * kWarpThreads) : "memory"); }
+
+struct Layout {
+  uint32_t h_off, w_off, bar_off, misc_off, head_off, ent_off, red_off, total;
+};
+
+__host__ __device__ inline Layout make_layout(int N, int H, int stages, int h_resident, int slab_rows_max) {
+  Layout L;
+  const uint32_t hchunk = static_cast<uint32_t>(N) * 128u;
+  const uint32_t h_slots = h_resident ? static_cast<uint32_t>(H / kKChunk) : static_cast<uint32_t>(stages);
+  L.h_off = 0;
+  L.w_off = L.h_off + h_slots * hchunk;
+  L.bar_off = L.w_off + static_cast<uint32_t>(stages) * kWStageBytes;
+  L.misc_off = L.bar_off + static_cast<uint32_t>(2 * stages + 5) * 8u;
+  L.head_off = L.misc_off + 16u;
+  L.ent_off = L.head_off + static_cast<uint32_t>(slab_rows_max) * 4u;
+  L.red_off = (L.ent_off + 3u * kMaxCreditEnt * 2u + 15u) & ~15u;
+  L.total = L.red_off + static_cast<uint32_t>(kEpiWarps * N * 3) * 4u;
+  return L;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k1_vocab_proj(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_w8,
+                  const __grid_constant__ CUtensorMap map_h, const K1Args a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const Layout L = make_layout(a.N, a.H, a.stages, a.h_resident, a.slab_rows_max);
+  const int warp = threadIdx.x / kWarpThreads;
+  const int lane = threadIdx.x % kWarpThreads;
+  const int N = a.N;
+  const uint32_t hchunk = static_cast<uint32_t>(N) * 128u;
+
+  uint8_t* h_sm = smem + L.h_off;
+  uint8_t* w_sm = smem + L.w_off;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+  uint64_t* empty = full + a.stages;
+  uint64_t* tfull = empty + a.stages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* hfull = tempty + 2;
+  uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L.misc_off);  // tmem base, last flag, entry count
+  int* head = reinterpret_cast<int*>(smem + L.head_off);
+  int16_t* ent_s = reinterpret_cast<int16_t*>(smem + L.ent_off);
+  int16_t* ent_k = ent_s + kMaxCreditEnt;
+  int16_t* ent_next = ent_k + kMaxCreditEnt;
+  float* red = reinterpret_cast<float*>(smem + L.red_off);
+
+  // Contiguous slab of vocab rows [r0, r1), balanced at 8-row granularity.
+  const long g8 = a.V_local / kRowGran;
+  const int r0 = kRowGran * static_cast<int>(static_cast<long>(blockIdx.x) * g8 / gridDim.x);
+  const int r1 = kRowGran * static_cast<int>(static_cast<long>(blockIdx.x + 1) * g8 / gridDim.x);
+  const int ntiles = (r1 - r0 + kTileRows - 1) / kTileRows;
+  const uint32_t tmem_cols = tmem_cols_pow2(2u * N);
+
+  if (warp == 4 && lane == 0) {
+    prefetch_tmap(&map_w);
+    prefetch_tmap(&map_w8);
+    prefetch_tmap(&map_h);
+    for (int i = 0; i < a.stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], kEpiWarps * kWarpThreads);
+    }
+    mbar_init(hfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc(&misc[0], tmem_cols);
+  if (warp < kEpiWarps) {
+    for (int r = threadIdx.x; r < r1 - r0; r += kEpiWarps * kWarpThreads) head[r] = -1;
+    if (threadIdx.x == 0) misc[2] = 0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  // Credited (position, slot) entries whose token lives in this slab: their
+  // raw logits are captured for the credit fuse.  Rows decided at step start
+  // are frozen (reading c7) and skipped.
+  if (warp < kEpiWarps && a.credit_ids != nullptr) {
+    const int stride = kStatWords + a.K;
+    for (int e = threadIdx.x; e < a.M * a.K; e += kEpiWarps * kWarpThreads) {
+      const int s = e / a.K, k = e - s * a.K;
+      if (!a.mask[s]) continue;
+      const int id = a.credit_ids[e];
+      if (id < 0) continue;
+      const int lv = id - a.v_offset;
+      if (lv < 0 || lv >= a.V_local) {  // owned by another rank
+        if (blockIdx.x == 0) a.rec[s * stride + kStatWords + k] = neg_inf();
+        continue;
+      }
+      if (lv < r0 || lv >= r1) continue;
+      const int slot = static_cast<int>(atomicAdd(&misc[2], 1u));
+      if (slot >= kMaxCreditEnt) {
+        atomicOr(a.err, kErrCreditEntOverflow);
+        continue;
+      }
+      ent_s[slot] = static_cast<int16_t>(s);
+      ent_k[slot] = static_cast<int16_t>(k);
+      ent_next[slot] = static_cast<int16_t>(atomicExch(&head[lv - r0], slot));
+    }
+  }
+  __syncthreads();
+  const uint32_t tmem_base = misc[0];
+
+  if (warp == 4) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first();  // W is streamed exactly once
+      const uint64_t pol_h = policy_evict_last();   // hidden is re-read by every CTA
+      if (a.h_resident) {
+        mbar_expect_tx(hfull, static_cast<uint32_t>(a.num_kc) * hchunk);
+        for (int kc = 0; kc < a.num_kc; ++kc)
+          tma_load_2d(h_sm + kc * hchunk, &map_h, hfull, kc * kKChunk, 0, pol_h);
+      }
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = 0; t < ntiles; ++t) {
+        const int row0 = r0 + t * kTileRows;
+        const int rows = min(kTileRows, r1 - row0);
+        for (int kc = 0; kc < a.num_kc; ++kc) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          const uint32_t bytes = static_cast<uint32_t>(rows) * 128u + (a.h_resident ? 0u : hchunk);
+          mbar_expect_tx(&full[stage], bytes);
+          uint8_t* dst = w_sm + stage * kWStageBytes;
+          if (rows == kTileRows) {
+            tma_load_2d(dst, &map_w, &full[stage], kc * kKChunk, row0, pol_w);
+          } else {  // slab tail: 8-row boxes land at the same swizzled offsets
+            for (int r = 0; r < rows; r += kRowGran)
+              tma_load_2d(dst + r * 128, &map_w8, &full[stage], kc * kKChunk, row0 + r, pol_w);
+          }
+          if (!a.h_resident) tma_load_2d(h_sm + stage * hchunk, &map_h, &full[stage], kc * kKChunk, 0, pol_h);
+          if (++stage == a.stages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16(kTileRows, N, false, false);
+      if (a.h_resident) mbar_wait(hfull, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = 0; t < ntiles; ++t) {
+        const int buf = t & 1;
+        const uint32_t use = static_cast<uint32_t>(t >> 1);
+        mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem_base + static_cast<uint32_t>(buf * N);
+        for (int kc = 0; kc < a.num_kc; ++kc) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(w_sm + stage * kWStageBytes);
+          const uint32_t b_addr = smem_u32(h_sm + (a.h_resident ? kc : stage) * hchunk);
+#pragma unroll
+          for (int k = 0; k < kKChunk / 16; ++k) {
+            mma_bf16(d, sdesc_sw128(a_addr + k * 32, 16, 1024), sdesc_sw128(b_addr + k * 32, 16, 1024), idesc,
+                     (kc | k) != 0);
+          }
+          mma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
+          if (++stage == a.stages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        mma_commit(&tfull[buf]);  // accumulator ready for the epilogue
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int ng = N / 32;
+    float Rm[kMaxGroups];
+    int Ri[kMaxGroups];
+    float Rl[kMaxGroups];
+#pragma unroll
+    for (int g = 0; g < kMaxGroups; ++g) {
+      Rm[g] = neg_inf();
+      Ri[g] = INT_MAX;
+      Rl[g] = 0.f;
+    }
+    const bool up16 = lane & 16, up8 = lane & 8, up4 = lane & 4, up2 = lane & 2, up1 = lane & 1;
+    const int stride = kStatWords + a.K;
+    for (int t = 0; t < ntiles; ++t) {
+      const int buf = t & 1;
+      const uint32_t use = static_cast<uint32_t>(t >> 1);
+      mbar_wait(&tfull[buf], use & 1u);
+      tc_fence_after();
+      const int row0 = r0 + t * kTileRows;
+      const int rows = min(kTileRows, r1 - row0);
+      const int rit = warp * 32 + lane;
+      const bool valid = rit < rows;
+      const int lv = row0 + rit;
+      const int gid = a.v_offset + lv;
+      const int ent0 = valid ? head[lv - r0] : -1;
+#pragma unroll
+      for (int g = 0; g < kMaxGroups; ++g) {
+        if (g < ng) {
+          float x[32];
+          tmem_ld32(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(buf * N + g * 32),
+                    x);
+          if (a.flog != nullptr && valid) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int col = g * 32 + j;
+              if (col < a.M) a.flog[static_cast<long>(col) * a.V_local + lv] = x[j];
+            }
+          }
+          for (int e = ent0; e >= 0; e = ent_next[e]) {
+            const int s = ent_s[e] - g * 32;
+            if (s >= 0 && s < 32) a.rec[(g * 32 + s) * stride + kStatWords + ent_k[e]] = pick32(x, s);
+          }
+          float m[32], l[32];
+          int ix[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            m[j] = valid ? x[j] : neg_inf();
+            ix[j] = valid ? gid : INT_MAX;
+            l[j] = valid ? 1.f : 0.f;
+          }
+          rs_level<16>(m, ix, l, up16);
+          rs_level<8>(m, ix, l, up8);
+          rs_level<4>(m, ix, l, up4);
+          rs_level<2>(m, ix, l, up2);
+          rs_level<1>(m, ix, l, up1);
+          stat_combine(Rm[g], Ri[g], Rl[g], m[0], ix[0], l[0]);  // lane = column g*32+lane
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[buf]);
+    }
+    // cross-warp merge (fixed warp order)
+#pragma unroll
+    for (int g = 0; g < kMaxGroups; ++g) {
+      if (g < ng) {
+        float* r = red + (warp * N + g * 32 + lane) * 3;
+        r[0] = Rm[g];
+        r[1] = __int_as_float(Ri[g]);
+        r[2] = Rl[g];
+      }
+    }
+    named_bar_epi();
+    for (int col = threadIdx.x; col < a.M; col += kEpiWarps * kWarpThreads) {
+      float m = red[col * 3 + 0], l = red[col * 3 + 2];
+      int ix = __float_as_int(red[col * 3 + 1]);
+      for (int w = 1; w < kEpiWarps; ++w) {
+        const float* r = red + (w * N + col) * 3;
+        stat_combine(m, ix, l, r[0], __float_as_int(r[1]), r[2]);
+      }
+      float* p = a.part + (static_cast<long>(blockIdx.x) * a.M + col) * 3;
+      p[0] = m;
+      p[1] = __int_as_float(ix);
+      p[2] = l;
+    }
+    __threadfence();
+    named_bar_epi();
+    if (threadIdx.x == 0) misc[1] = (atomicAdd(a.counter, 1u) == gridDim.x - 1) ? 1u : 0u;
+    named_bar_epi();
+    if (misc[1]) {
+      // Last CTA: merge the per-CTA partials.  tpc threads per column, each
+      // over a strided subset of CTAs, then an in-order shuffle merge.
+      __threadfence();
+      const int nthr = kEpiWarps * kWarpThreads;
+      int tpc = 1;
+      while (tpc * 2 * a.M <= nthr && tpc < 32) tpc *= 2;
+      const int col_per_pass = nthr / tpc;
+      for (int cb = 0; cb < a.M; cb += col_per_pass) {
+        const int col = cb + threadIdx.x / tpc;
+        const int sub = threadIdx.x % tpc;
+        float m = neg_inf(), l = 0.f;
+        int ix = INT_MAX;
+        if (col < a.M) {
+          for (int c = sub; c < static_cast<int>(gridDim.x); c += tpc) {
+            const float* p = a.part + (static_cast<long>(c) * a.M + col) * 3;
+            stat_combine(m, ix, l, __ldcg(p), __float_as_int(__ldcg(p + 1)), __ldcg(p + 2));
+          }
+        }
+        for (int o = 1; o < tpc; o <<= 1) {
+          const float rm = __shfl_down_sync(0xffffffffu, m, o);
+          const int ri = __shfl_down_sync(0xffffffffu, ix, o);
+          const float rl = __shfl_down_sync(0xffffffffu, l, o);
+          if ((sub & (2 * o - 1)) == 0) stat_combine(m, ix, l, rm, ri, rl);
+        }
+        if (col < a.M && sub == 0) {
+          float* r = a.rec + col * stride;
+          r[0] = m;
+          r[1] = __int_as_float(ix);
+          r[2] = l;
+          r[3] = 0.f;
+        }
+      }
+      if (threadIdx.x == 0) *a.counter = 0u;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 5) tmem_dealloc(tmem_base, tmem_cols);
+}
+
+}  // namespace
+
+size_t k1_smem_bytes(int N, int H, int stages, int h_resident, int slab_rows_max) {
+  return make_layout(N, H, stages, h_resident, slab_rows_max).total + 1024;
+}
+
+cudaError_t launch_k1(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
+                      const K1Args& a, int grid, size_t smem, cudaStream_t st) {
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k1_vocab_proj, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  k1_vocab_proj<<<grid, kThreads, smem, st>>>(map_w, map_w8, map_h, a);
+  return cudaGetLastError();
+}
+
+}  // namespace dinfer

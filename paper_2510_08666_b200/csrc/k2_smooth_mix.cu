@@ -1,0 +1,272 @@
+// K2 smooth_mix -- the dense contraction of iteration smoothing
+// (App. A.1):  Delta e_t[i] = p_t[i] W_emb, p_t = softmax(z_t).
+//
+// This kernel accumulates, for each position s and hidden column h,
+//     acc[s, h] = sum_{v in shard} exp(f[s, v] - m_s) * E[v, h]
+// relative to the rank-local max m_s (from K1's record); K3/K4 finish with
+// the cross-rank rescale and the 1/l normalisation.
+//
+// UMMA orientation: D[h, s] (M = 128 hidden columns per sub-tile, N = positions)
+//   A = E^T tile [128 h x 16 v], MN-major straight from E's row-major [V, H]
+//       layout via TMA boxes of [64 h x 64 v] (no transposed copy of E);
+//   B = P^T tile [N s x 16 v], K-major, produced in shared memory by 4 warps
+//       from the fp32 logits: P = exp(f - m) split into bf16 hi + lo
+//       (P = hi + lo to ~2^-17), two MMAs per k-step, so the bf16 operand
+//       rounding stays far below the 2e-3 tolerance.
+// Grid: HS hidden slices x VG vocab groups (<= #SMs); each CTA writes one
+// [M x HW] partial; partials are summed in fixed order downstream.
+#include "common.cuh"
+#include "kernels.h"
+
+#include <cuda_bf16.h>
+
+namespace dinfer {
+namespace {
+
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = (kEpiWarps + 2) * kWarpThreads;
+constexpr uint32_t kEBox = 64u * 64u * 2u;  // [64 h x 64 v] bf16 = 8 KB
+
+__host__ __device__ inline uint32_t tmem_cols_pow2(uint32_t n) {
+  uint32_t c = 32;
+  while (c < n) c <<= 1;
+  return c;
+}
+
+struct Layout {
+  uint32_t e_off, p_off, bar_off, misc_off, m_off, total;
+};
+__host__ __device__ inline Layout make_layout(int N, int HW, int stages, int pstages) {
+  Layout L;
+  const uint32_t e_stage = static_cast<uint32_t>(HW) * 128u;  // HW/64 boxes of 8 KB
+  const uint32_t p_stage = 2u * static_cast<uint32_t>(N) * 128u;
+  L.e_off = 0;
+  L.p_off = L.e_off + static_cast<uint32_t>(stages) * e_stage;
+  L.bar_off = L.p_off + static_cast<uint32_t>(pstages) * p_stage;
+  L.misc_off = L.bar_off + static_cast<uint32_t>(2 * stages + 2 * pstages + 1) * 8u;
+  L.m_off = L.misc_off + 16u;
+  L.total = L.m_off + static_cast<uint32_t>(N) * 4u;
+  return L;
+}
+
+DI uint32_t pack_bf16x2(float lo_elem, float hi_elem) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo_elem, hi_elem);  // .x = first (lower address)
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k2_smooth_mix(const __grid_constant__ CUtensorMap map_e, const K2Args a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const Layout L = make_layout(a.N, a.HW, a.stages, a.pstages);
+  const int warp = threadIdx.x / kWarpThreads;
+  const int lane = threadIdx.x % kWarpThreads;
+  const int N = a.N;
+  const uint32_t e_stage = static_cast<uint32_t>(a.HW) * 128u;
+  const uint32_t p_half = static_cast<uint32_t>(N) * 128u;
+
+  uint8_t* e_sm = smem + L.e_off;
+  uint8_t* p_sm = smem + L.p_off;
+  uint64_t* efull = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+  uint64_t* eempty = efull + a.stages;
+  uint64_t* pfull = eempty + a.stages;
+  uint64_t* pempty = pfull + a.pstages;
+  uint64_t* accfull = pempty + a.pstages;
+  uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L.misc_off);
+  float* m_sm = reinterpret_cast<float*>(smem + L.m_off);
+
+  const int hs = blockIdx.x % a.HS;
+  const int vg = blockIdx.x / a.HS;
+  const int c0 = static_cast<int>(static_cast<long>(vg) * a.nchunks / a.VG);
+  const int c1 = static_cast<int>(static_cast<long>(vg + 1) * a.nchunks / a.VG);
+  const uint32_t tmem_cols = tmem_cols_pow2(static_cast<uint32_t>(a.nsub * N));
+
+  if (warp == 4 && lane == 0) {
+    prefetch_tmap(&map_e);
+    for (int i = 0; i < a.stages; ++i) {
+      mbar_init(&efull[i], 1);
+      mbar_init(&eempty[i], 1);
+    }
+    for (int i = 0; i < a.pstages; ++i) {
+      mbar_init(&pfull[i], kEpiWarps * kWarpThreads);
+      mbar_init(&pempty[i], 1);
+    }
+    mbar_init(accfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc(&misc[0], tmem_cols);
+  if (warp < kEpiWarps) {
+    for (int s = threadIdx.x; s < N; s += kEpiWarps * kWarpThreads)
+      m_sm[s] = (s < a.M) ? a.rec[s * a.rec_stride] : 0.f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = misc[0];
+
+  if (warp == 4) {
+    // ------------------------------------------------------------ TMA: E tiles
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int c = c0; c < c1; ++c) {
+        mbar_wait(&eempty[stage], phase ^ 1u);
+        mbar_expect_tx(&efull[stage], e_stage);
+        for (int b = 0; b < a.HW / 64; ++b)
+          tma_load_2d(e_sm + stage * e_stage + b * kEBox, &map_e, &efull[stage], hs * a.HW + b * 64, c * kKChunk,
+                      pol);
+        if (++stage == a.stages) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0 && c1 > c0) {
+      const uint32_t idesc = idesc_bf16(128, N, /*a MN-major*/ true, /*b K-major*/ false);
+      int es = 0, ps = 0;
+      uint32_t eph = 0, pph = 0;
+      for (int c = c0; c < c1; ++c) {
+        mbar_wait(&efull[es], eph);
+        mbar_wait(&pfull[ps], pph);
+        tc_fence_after();
+        const uint32_t e_addr = smem_u32(e_sm + es * e_stage);
+        const uint32_t phi = smem_u32(p_sm + ps * 2 * p_half);
+        const uint32_t plo = phi + p_half;
+#pragma unroll
+        for (int k = 0; k < kKChunk / 16; ++k) {
+          const uint64_t bhi = sdesc_sw128(phi + k * 32, 16, 1024);
+          const uint64_t blo = sdesc_sw128(plo + k * 32, 16, 1024);
+          for (int sub = 0; sub < a.nsub; ++sub) {
+            // A: [128 h x 16 v] = two 64-h blocks 8 KB apart (LBO), 8-v groups 1 KB apart (SBO)
+            const uint64_t ad = sdesc_sw128(e_addr + sub * 2 * kEBox + k * 16 * 128, kEBox, 1024);
+            const uint32_t d = tmem_base + static_cast<uint32_t>(sub * N);
+            mma_bf16(d, ad, bhi, idesc, (c > c0 || k > 0) ? 1u : 0u);
+            mma_bf16(d, ad, blo, idesc, 1u);
+          }
+        }
+        mma_commit(&eempty[es]);
+        mma_commit(&pempty[ps]);
+        if (++es == a.stages) {
+          es = 0;
+          eph ^= 1u;
+        }
+        if (++ps == a.pstages) {
+          ps = 0;
+          pph ^= 1u;
+        }
+      }
+      mma_commit(accfull);
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ P producers
+    const int tid = threadIdx.x;
+    int ps = 0;
+    uint32_t pph = 0;
+    for (int c = c0; c < c1; ++c) {
+      mbar_wait(&pempty[ps], pph ^ 1u);
+      uint8_t* phi = p_sm + ps * 2 * p_half;
+      uint8_t* plo = phi + p_half;
+      for (int u = tid; u < N * 8; u += kEpiWarps * kWarpThreads) {
+        const int s = u >> 3, cc = u & 7;
+        const int v0 = c * kKChunk + cc * 8;
+        float p[8];
+        if (s < a.M && v0 < a.V_local) {
+          const float4* src = reinterpret_cast<const float4*>(a.flog + static_cast<long>(s) * a.V_local + v0);
+          const float4 q0 = __ldcg(src), q1 = __ldcg(src + 1);
+          const float ms = m_sm[s];
+          p[0] = fexp(q0.x - ms); p[1] = fexp(q0.y - ms); p[2] = fexp(q0.z - ms); p[3] = fexp(q0.w - ms);
+          p[4] = fexp(q1.x - ms); p[5] = fexp(q1.y - ms); p[6] = fexp(q1.z - ms); p[7] = fexp(q1.w - ms);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) p[j] = 0.f;
+        }
+        float r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = p[j] - __bfloat162float(__float2bfloat16_rn(p[j]));
+        const uint4 hi = make_uint4(pack_bf16x2(p[0], p[1]), pack_bf16x2(p[2], p[3]), pack_bf16x2(p[4], p[5]),
+                                    pack_bf16x2(p[6], p[7]));
+        const uint4 lo = make_uint4(pack_bf16x2(r[0], r[1]), pack_bf16x2(r[2], r[3]), pack_bf16x2(r[4], r[5]),
+                                    pack_bf16x2(r[6], r[7]));
+        const uint32_t off = static_cast<uint32_t>(s) * 128u + ((static_cast<uint32_t>(cc) ^ (s & 7u)) << 4);
+        *reinterpret_cast<uint4*>(phi + off) = hi;
+        *reinterpret_cast<uint4*>(plo + off) = lo;
+      }
+      fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05.mma
+      mbar_arrive(&pfull[ps]);
+      if (++ps == a.pstages) {
+        ps = 0;
+        pph ^= 1u;
+      }
+    }
+    // ------------------------------------------------------------ epilogue
+    const int hbase = hs * a.HW;
+    if (c1 > c0) {
+      mbar_wait(accfull, 0);
+      tc_fence_after();
+    }
+    for (int sub = 0; sub < a.nsub; ++sub) {
+      for (int g = 0; g < N / 32; ++g) {
+        float x[32];
+        if (c1 > c0) {
+          tmem_ld32(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(sub * N + g * 32), x);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) x[j] = 0.f;
+        }
+        const int h = hbase + sub * 128 + warp * 32 + lane;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int s = g * 32 + j;
+          if (s < a.M) a.part[(static_cast<long>(vg) * a.M + s) * a.H + h] = x[j];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 5) tmem_dealloc(tmem_base, tmem_cols);
+}
+
+__global__ void acc_reduce_kernel(const float* __restrict__ part, int VG, int MH, float* __restrict__ out) {
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i >= MH) return;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int g = 0; g < VG; ++g) {
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(part + static_cast<long>(g) * MH + i));
+    s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+  }
+  *reinterpret_cast<float4*>(out + i) = s;
+}
+
+}  // namespace
+
+size_t k2_smem_bytes(int N, int HW, int stages, int pstages) {
+  return make_layout(N, HW, stages, pstages).total + 1024;
+}
+
+cudaError_t launch_k2(const CUtensorMap& map_e, const K2Args& a, size_t smem, cudaStream_t st) {
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k2_smooth_mix, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  k2_smooth_mix<<<a.HS * a.VG, kThreads, smem, st>>>(map_e, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_acc_reduce(const float* part, int VG, int MH, float* out, cudaStream_t st) {
+  const int threads = 256;
+  const int blocks = (MH / 4 + threads - 1) / threads;
+  acc_reduce_kernel<<<blocks, threads, 0, st>>>(part, VG, MH, out);
+  return cudaGetLastError();
+}
+
+}  // namespace dinfer

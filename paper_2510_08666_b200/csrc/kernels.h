@@ -1,0 +1,94 @@
+// kernels.h -- internal launch interface between the C-ABI layer (dinfer_api.cu)
+// and the step kernels.  Not part of the public ABI.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dinfer {
+
+constexpr int kWarpThreads = 32;
+constexpr int kKChunk = 64;        // bf16 elements per 128-B swizzled row
+constexpr int kTileRows = 128;     // UMMA M (vocab rows per tile)
+constexpr int kRowGran = 8;        // vocab-row granularity of the K1 partition
+constexpr int kMaxCreditEnt = 1024;  // per-CTA credited (position, slot) entries
+constexpr int kStatWords = 4;      // m, idx, l, pad  (record header per row)
+
+// Device-side sticky error bits (dinfer_sync reads and clears them).
+enum : int { kErrCreditEntOverflow = 1, kErrCreditSlotsFull = 2 };
+
+// ---------------------------------------------------------------- K1
+struct K1Args {
+  int M, N, H, K;          // positions, MMA N (>= M, %16), hidden, credit slots
+  int V_local, v_offset;
+  int num_kc;              // H / 64
+  int h_resident;          // 1: whole hidden block resident in smem
+  int stages;
+  int slab_rows_max;       // max rows of any CTA's slab (credit head table size)
+  const uint8_t* mask;     // [M]
+  const int32_t* credit_ids;  // [M][K] or nullptr
+  float* part;             // [grid][M][3]   per-CTA (m, idx, l)
+  unsigned* counter;       // last-CTA ticket, self-resetting
+  float* rec;              // [M][4+K] rank record (stats part)
+  float* flog;             // [M][V_local] raw logits for K2, or nullptr
+  int* err;
+};
+size_t k1_smem_bytes(int N, int H, int stages, int h_resident, int slab_rows_max);
+cudaError_t launch_k1(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
+                      const K1Args& a, int grid, size_t smem, cudaStream_t st);
+
+// ---------------------------------------------------------------- K2
+struct K2Args {
+  int M, N, H, V_local;
+  int HW, nsub;            // hidden columns per CTA (128 or 256), HW/128
+  int HS, VG;              // H/HW slices, vocab groups
+  int nchunks;             // ceil(V_local / 64)
+  int stages, pstages;
+  const float* flog;       // [M][V_local]
+  const float* rec;        // rank record: m at rec[s*rec_stride]
+  int rec_stride;
+  float* part;             // [VG][M][H]
+};
+size_t k2_smem_bytes(int N, int HW, int stages, int pstages);
+cudaError_t launch_k2(const CUtensorMap& map_e, const K2Args& a, size_t smem, cudaStream_t st);
+
+// sum of VG partials -> one [M][H] block (rank record acc)
+cudaError_t launch_acc_reduce(const float* part, int VG, int MH, float* out, cudaStream_t st);
+
+// ---------------------------------------------------------------- K3
+struct K3Args {
+  int B, S, K, world;
+  const float* recs;       // world records, `rec_words` apart
+  long rec_words;
+  int rec_stride;          // 4 + K
+  uint8_t* mask;
+  int32_t* tokens;
+  int32_t* credit_ids;
+  float* credit_val;
+  uint8_t* committed;
+  float* stats;            // [M][4] or nullptr
+  float* ml;               // [M][2] merged (m, l) for K4
+  int decoder, runs_after_hi, use_credit;
+  float tau, theta_hi, theta_lo, c_alpha, c_beta, c_gamma;
+  int* err;
+};
+cudaError_t launch_k3(const K3Args& a, cudaStream_t st);
+
+// ---------------------------------------------------------------- K4
+struct K4Args {
+  int M, H;
+  const float* acc;        // partial p at acc + p*acc_stride, [M][H] each
+  long acc_stride;
+  int nparts;
+  const float* m_part;     // m of partial p, row s at m_part[p*m_stride + s*m_rowstride]; nullptr = scale 1
+  long m_stride;
+  int m_rowstride;
+  const float* ml;         // [M][2] merged (m, l)
+  const uint8_t* mask;     // [M] after commit
+  const uint16_t* e_mask;  // [H] bf16
+  float alpha_t;
+  float* out;              // [M][H]
+};
+cudaError_t launch_k4(const K4Args& a, cudaStream_t st);
+
+}  // namespace dinfer

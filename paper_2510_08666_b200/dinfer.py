@@ -1,0 +1,203 @@
+"""Thin ctypes binding of libdinfer.so (include/dinfer.h).
+
+Argument marshalling only: every step of the path runs in the library's CUDA
+kernels.  torch tensors are passed by data pointer; torch is used for device
+memory, streams and torch.distributed (plumbing).  There is no CPU fallback:
+if libdinfer.so is missing, importing the binding's entry points raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_float, c_int32, c_int64, c_size_t, c_uint8, c_uint16, c_void_p
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdinfer.so")
+
+DEC_THRESHOLD = 0
+DEC_HIERARCHICAL = 1
+PHASES = ("k1_vocab_proj", "k2_smooth_mix", "k2r_acc_reduce", "c1_allgather", "k3_select_commit",
+          "k4_smooth_finalize")
+
+STATUS = {0: "ok", 1: "ERR_ARG", 2: "ERR_SHAPE", 3: "ERR_CUDA", 4: "ERR_NCCL", 5: "ERR_NOMEM",
+          6: "ERR_UNSUPPORTED", 7: "ERR_DEVICE"}
+
+
+class DInferError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: {STATUS.get(status, status)} ({lib().dinfer_strerror(status).decode()})")
+        self.status = status
+
+
+class Shape(ctypes.Structure):
+    _fields_ = [("B", c_int32), ("S", c_int32), ("H", c_int32), ("K", c_int32), ("V_total", c_int64),
+                ("V_local", c_int64), ("v_offset", c_int64), ("world", c_int32), ("rank", c_int32),
+                ("smooth_capable", c_int32)]
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("decoder", c_int32), ("tau", c_float), ("theta_hi", c_float), ("theta_lo", c_float),
+                ("hier_runs_after_hi", c_int32), ("use_credit", c_int32), ("c_alpha", c_float),
+                ("c_beta", c_float), ("c_gamma", c_float), ("use_smooth", c_int32), ("alpha_t", c_float)]
+
+
+class Geometry(ctypes.Structure):
+    _fields_ = [(n, c_int32) for n in ("k1_grid", "k1_stages", "k1_h_resident", "k1_smem", "k2_grid", "k2_hw",
+                                        "k2_groups", "k2_stages", "k2_smem", "num_sms")]
+
+
+_LIB = None
+
+
+def lib():
+    """Load libdinfer.so (raises if it was not built -- no fallback)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built (python -m paper_2510_08666_b200.build)")
+    L = ctypes.CDLL(LIB_PATH)
+    P, S = c_void_p, c_int32
+    sig = {
+        "dinfer_get_unique_id": (S, [P]),
+        "dinfer_create": (S, [POINTER(Shape), P, P, POINTER(c_void_p)]),
+        "dinfer_destroy": (None, [P]),
+        "dinfer_set_stream": (S, [P, P]),
+        "dinfer_step": (S, [P, P, P, P, P, P, P, P, P, POINTER(Params), P, P, P]),
+        "dinfer_step_host": (S, [P, P, P, P, P, P, P, P, P, POINTER(Params), P, P, P]),
+        "dinfer_record_words": (c_size_t, [P, S]),
+        "dinfer_step_local": (S, [P, P, P, P, P, P, POINTER(Params), P]),
+        "dinfer_step_combine": (S, [P, P, P, P, P, P, P, POINTER(Params), P, P, P]),
+        "dinfer_credit_reset": (S, [P, P, P]),
+        "dinfer_alpha_schedule": (c_float, [c_float, c_float, c_float, S]),
+        "dinfer_tau_schedule": (c_float, [c_float, S, S]),
+        "dinfer_sync": (S, [P]),
+        "dinfer_strerror": (ctypes.c_char_p, [S]),
+        "dinfer_set_timing": (S, [P, S]),
+        "dinfer_get_timing": (S, [P, POINTER(c_float), S]),
+        "dinfer_launches_per_step": (S, [P, POINTER(Params)]),
+        "dinfer_get_geometry": (S, [P, POINTER(Geometry)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype, fn.argtypes = res, args
+    _LIB = L
+    return L
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return c_void_p(t.data_ptr())
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        raise DInferError(status, what)
+
+
+def make_params(decoder=DEC_THRESHOLD, tau=0.9, theta_hi=0.92, theta_lo=0.62, hier_runs_after_hi=False,
+                use_credit=False, c_alpha=1.0, c_beta=0.9, c_gamma=0.5, use_smooth=False, alpha_t=0.1) -> Params:
+    if isinstance(decoder, str):
+        decoder = {"threshold": DEC_THRESHOLD, "hierarchical": DEC_HIERARCHICAL}[decoder]
+    return Params(int(decoder), float(tau), float(theta_hi), float(theta_lo), int(bool(hier_runs_after_hi)),
+                  int(bool(use_credit)), float(c_alpha), float(c_beta), float(c_gamma), int(bool(use_smooth)),
+                  float(alpha_t))
+
+
+def alpha_schedule(init: float, growth: float, preset: float, t: int) -> float:
+    return float(lib().dinfer_alpha_schedule(init, growth, preset, int(t)))
+
+
+def tau_schedule(target: float, t: int, decay_steps: int) -> float:
+    return float(lib().dinfer_tau_schedule(target, int(t), int(decay_steps)))
+
+
+def get_unique_id() -> bytes:
+    buf = (c_uint8 * 128)()
+    _check(lib().dinfer_get_unique_id(buf), "dinfer_get_unique_id")
+    return bytes(buf)
+
+
+class Context:
+    """One dInfer step context (workspace + stream [+ NCCL communicator])."""
+
+    def __init__(self, B: int, S: int, H: int, K: int, V_total: int, V_local: int | None = None,
+                 v_offset: int = 0, world: int = 1, rank: int = 0, smooth_capable: bool = True,
+                 stream=None, nccl_id: bytes | None = None):
+        V_local = V_total // world if V_local is None else V_local
+        self.shape = Shape(B, S, H, K, V_total, V_local, v_offset, world, rank, int(bool(smooth_capable)))
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream().cuda_stream
+        self._stream = stream
+        idbuf = None if nccl_id is None else (c_uint8 * 128).from_buffer_copy(nccl_id)
+        h = c_void_p()
+        _check(lib().dinfer_create(ctypes.byref(self.shape), idbuf, c_void_p(stream), ctypes.byref(h)),
+               "dinfer_create")
+        self._h = h
+
+    # -- lifecycle
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().dinfer_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream):
+        self._stream = stream
+        _check(lib().dinfer_set_stream(self._h, c_void_p(stream)), "dinfer_set_stream")
+
+    # -- the step
+    def step(self, hidden, W, E, e_mask, mask, tokens, credit_ids, credit_val, params: Params, committed,
+             smoothed=None, stats=None):
+        _check(lib().dinfer_step(self._h, _ptr(hidden), _ptr(W), _ptr(E), _ptr(e_mask), _ptr(mask), _ptr(tokens),
+                                 _ptr(credit_ids), _ptr(credit_val), ctypes.byref(params), _ptr(committed),
+                                 _ptr(smoothed), _ptr(stats)), "dinfer_step")
+
+    def step_host(self, hidden_h, W, E, e_mask, mask_h, tokens_h, credit_ids_h, credit_val_h, params: Params,
+                  committed_h, smoothed_h=None, stats_h=None):
+        _check(lib().dinfer_step_host(self._h, _ptr(hidden_h), _ptr(W), _ptr(E), _ptr(e_mask), _ptr(mask_h),
+                                      _ptr(tokens_h), _ptr(credit_ids_h), _ptr(credit_val_h), ctypes.byref(params),
+                                      _ptr(committed_h), _ptr(smoothed_h), _ptr(stats_h)), "dinfer_step_host")
+
+    def record_words(self, use_smooth: bool) -> int:
+        return int(lib().dinfer_record_words(self._h, int(bool(use_smooth))))
+
+    def step_local(self, hidden, W, E, mask, credit_ids, params: Params, record):
+        _check(lib().dinfer_step_local(self._h, _ptr(hidden), _ptr(W), _ptr(E), _ptr(mask), _ptr(credit_ids),
+                                       ctypes.byref(params), _ptr(record)), "dinfer_step_local")
+
+    def step_combine(self, records, e_mask, mask, tokens, credit_ids, credit_val, params: Params, committed,
+                     smoothed=None, stats=None):
+        _check(lib().dinfer_step_combine(self._h, _ptr(records), _ptr(e_mask), _ptr(mask), _ptr(tokens),
+                                         _ptr(credit_ids), _ptr(credit_val), ctypes.byref(params),
+                                         _ptr(committed), _ptr(smoothed), _ptr(stats)), "dinfer_step_combine")
+
+    def credit_reset(self, credit_ids, credit_val):
+        _check(lib().dinfer_credit_reset(self._h, _ptr(credit_ids), _ptr(credit_val)), "dinfer_credit_reset")
+
+    def sync(self):
+        _check(lib().dinfer_sync(self._h), "dinfer_sync")
+
+    # -- instrumentation
+    def set_timing(self, enable: bool):
+        _check(lib().dinfer_set_timing(self._h, int(bool(enable))), "dinfer_set_timing")
+
+    def get_timing(self) -> dict:
+        buf = (c_float * len(PHASES))()
+        _check(lib().dinfer_get_timing(self._h, buf, len(PHASES)), "dinfer_get_timing")
+        return {n: float(v) for n, v in zip(PHASES, buf)}
+
+    def launches_per_step(self, params: Params) -> int:
+        return int(lib().dinfer_launches_per_step(self._h, ctypes.byref(params)))
+
+    def geometry(self) -> dict:
+        g = Geometry()
+        _check(lib().dinfer_get_geometry(self._h, ctypes.byref(g)), "dinfer_get_geometry")
+        return {n: getattr(g, n) for n, _ in Geometry._fields_}

@@ -1,0 +1,79 @@
+"""C-ABI library checks that need no GPU: libdinfer.so loads, exports every
+symbol include/dinfer.h declares, validates shapes synchronously, and its host
+schedule helpers agree with the oracle's schedules."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import oracle as O
+from paper_2510_08666_b200 import build, dinfer
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    build.build()
+    return dinfer.lib()
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "dinfer.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(dinfer_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for must in ("dinfer_create", "dinfer_step", "dinfer_step_host", "dinfer_step_local", "dinfer_step_combine",
+                 "dinfer_credit_reset", "dinfer_alpha_schedule", "dinfer_tau_schedule", "dinfer_sync",
+                 "dinfer_destroy", "dinfer_strerror", "dinfer_get_unique_id"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(L):
+    for name in declared_functions():
+        assert hasattr(L, name), name
+
+
+def test_library_is_sm100a_with_tcgen05_and_tma():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", dinfer.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+    for mnem in ("UTCHMMA", "UTMALDG", "LDTM"):
+        assert mnem in out, mnem
+
+
+def test_schedules_match_oracle(L):
+    for t in range(12):
+        assert dinfer.alpha_schedule(0.1, 0.05, 0.3, t) == pytest.approx(O.alpha_schedule(0.1, 0.05, 0.3, t), abs=1e-7)
+        for D in (0, 1, 4, 7):
+            assert dinfer.tau_schedule(0.8, t, D) == pytest.approx(O.tau_schedule(0.8, t, D), abs=1e-7)
+
+
+def _create(L, **kw):
+    shp = dict(B=1, S=32, H=256, K=8, V_total=1024, V_local=1024, v_offset=0, world=1, rank=0, smooth_capable=1)
+    shp.update(kw)
+    s = dinfer.Shape(*[shp[n] for n, _ in dinfer.Shape._fields_])
+    h = ctypes.c_void_p()
+    return L.dinfer_create(ctypes.byref(s), None, None, ctypes.byref(h))
+
+
+@pytest.mark.parametrize("bad", [dict(H=200), dict(V_local=1020, V_total=1020), dict(S=0), dict(K=0),
+                                 dict(world=2, V_total=1024), dict(rank=1), dict(S=2000)])
+def test_create_rejects_bad_shapes_synchronously(L, bad):
+    assert _create(L, **bad) == 2  # DINFER_ERR_SHAPE, before touching the device
+
+
+def test_create_rejects_large_M(L):
+    assert _create(L, B=64, S=64) == 6  # UNSUPPORTED: M > 256 (compute-bound regime not in this path)
+
+
+def test_null_args(L):
+    assert L.dinfer_create(None, None, None, None) == 1
+    assert L.dinfer_step(None, *([None] * 12)) == 1
+    assert L.dinfer_sync(None) == 1
+    assert L.dinfer_strerror(0) == b"ok"

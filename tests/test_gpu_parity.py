@@ -1,0 +1,231 @@
+"""GPU parity: the CUDA path (via the C ABI) against the fp64 oracle on the
+same seeded, margin-vetted synthetic inputs.  Decisions, ids, mask and credit
+slots bit-exact; m / lse / p~ / smoothed within 2e-3 (north_star)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2510_08666_b200 import synth
+from tests.gpu_harness import GpuState, compare, gpu_params, replay, to_dev_bf16
+from tests.trajectory import vetted_trajectory
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    from paper_2510_08666_b200 import build
+    build.build()
+    return torch
+
+
+_W_CACHE = {}
+
+
+def weights(V, H):
+    key = (V, H)
+    if key not in _W_CACHE:
+        _W_CACHE.clear()
+        _W_CACHE[key] = (synth.make_W(V, H, 1), synth.make_E(V, H, 2))
+    return _W_CACHE[key]
+
+
+def run_trajectory(torch_cuda, V, H, B, S, K, seed, params_fn, use_credit, max_iters=None, **kw):
+    from paper_2510_08666_b200 import Context
+    W, E = weights(V, H)
+    _, _, _, steps = vetted_trajectory(W, E, B, S, seed, params_fn, max_iters=max_iters,
+                                       use_credit_table=use_credit, **kw)
+    ctx = Context(B, S, H, K, V)
+    Wd, Ed = to_dev_bf16(W), to_dev_bf16(E)
+    emd = to_dev_bf16(E[synth.mask_id(V)])
+    replay(ctx, Wd, Ed, emd, steps, B, S, H, K, V)
+    ctx.close()
+    return steps
+
+
+def thr_params(tau=0.9):
+    return lambda t: O.Params(decoder=O.DEC_THRESHOLD, tau=tau)
+
+
+def hier_credit_smooth(t):
+    return O.Params(decoder=O.DEC_HIERARCHICAL, theta_hi=O.tau_schedule(0.92, t, 4), theta_lo=0.62,
+                    use_credit=True, use_smooth=True, alpha_t=O.alpha_schedule(0.1, 0.05, 0.3, t))
+
+
+# ---------------------------------------------------------------- tiny config (BASELINE configs[0])
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_tiny_threshold_block(torch_cuda, seed):
+    steps = run_trajectory(torch_cuda, 1024, 256, 1, 32, 32, seed, thr_params(0.9), False)
+    assert not steps[-1]["result"]["mask"].any()
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_tiny_hier_credit_smooth_block(torch_cuda, seed):
+    run_trajectory(torch_cuda, 1024, 256, 2, 32, 32, seed, hier_credit_smooth, True)
+
+
+@pytest.mark.parametrize("seed", [3, 4])
+def test_tiny_threshold_credit_smooth_variants(torch_cuda, seed):
+    pf = lambda t: O.Params(decoder=O.DEC_THRESHOLD, tau=O.tau_schedule(0.8, t, 4), use_credit=True,
+                            c_alpha=0.7, c_beta=0.8, c_gamma=0.4, use_smooth=True, alpha_t=0.3)
+    run_trajectory(torch_cuda, 1024, 256, 2, 32, 32, seed, pf, True)
+    pf2 = lambda t: O.Params(decoder=O.DEC_HIERARCHICAL, theta_hi=0.92, theta_lo=0.62, hier_runs_after_hi=True)
+    run_trajectory(torch_cuda, 1024, 256, 1, 32, 32, seed, pf2, False)
+
+
+# ---------------------------------------------------------------- ragged / edge shapes
+def test_ragged_tail_and_odd_shapes(torch_cuda):
+    """V = 1000 (slab tails of 8-row boxes), S = 20 (N padding), H = 384
+    (128-wide smoothing slices), B = 3."""
+    run_trajectory(torch_cuda, 1000, 384, 3, 20, 24, 5, hier_credit_smooth, True)
+
+
+def test_max_M_256(torch_cuda):
+    run_trajectory(torch_cuda, 2048, 128, 8, 32, 8, 6, thr_params(0.9), False, max_iters=3)
+
+
+def test_S64_block(torch_cuda):
+    run_trajectory(torch_cuda, 4096, 256, 2, 64, 64, 7, hier_credit_smooth, True, max_iters=6)
+
+
+def test_empty_rows_are_noops(torch_cuda):
+    import torch
+    from paper_2510_08666_b200 import Context
+    V, H, B, S, K = 1024, 256, 2, 32, 4
+    W, E = weights(V, H)
+    ctx = Context(B, S, H, K, V)
+    st = GpuState(B, S, H, K, synth.mask_id(V))
+    st.mask[1].zero_()
+    st.tokens[1] = torch.arange(S, dtype=torch.int32, device="cuda")
+    h = synth.planted_hidden(W, B * S, seed=3)
+    p = gpu_params(O.Params(decoder=O.DEC_HIERARCHICAL, use_credit=True, use_smooth=True))
+    st.smoothed.fill_(7.0)
+    ctx.step(to_dev_bf16(h), to_dev_bf16(W), to_dev_bf16(E), to_dev_bf16(E[V - 1]), st.mask, st.tokens, st.cids,
+             st.cval, p, st.committed, st.smoothed, st.stats)
+    ctx.sync()
+    out = st.snapshot()
+    assert not out["committed"][1].any() and out["committed"][0].sum() >= 1
+    assert np.array_equal(out["tokens"][1], np.arange(S))
+    assert (out["cids"][1] == -1).all()
+    assert np.all(out["smoothed"][1] == 7.0)
+
+
+def test_determinism_repeat(torch_cuda):
+    import torch
+    from paper_2510_08666_b200 import Context
+    V, H, B, S, K = 4096, 512, 1, 32, 8
+    W, E = weights(V, H)
+    ctx = Context(B, S, H, K, V)
+    h = to_dev_bf16(synth.planted_hidden(W, B * S, seed=9))
+    Wd, Ed, emd = to_dev_bf16(W), to_dev_bf16(E), to_dev_bf16(E[V - 1])
+    p = gpu_params(O.Params(decoder=O.DEC_HIERARCHICAL, use_credit=True, use_smooth=True))
+    ref = None
+    for _ in range(20):
+        st = GpuState(B, S, H, K, synth.mask_id(V))
+        ctx.step(h, Wd, Ed, emd, st.mask, st.tokens, st.cids, st.cval, p, st.committed, st.smoothed, st.stats)
+        torch.cuda.synchronize()
+        out = st.snapshot()
+        if ref is None:
+            ref = out
+        for k in ("committed", "tokens", "cids", "cval", "m", "lse", "ptilde"):
+            assert np.array_equal(out[k], ref[k]), k
+        assert np.array_equal(np.nan_to_num(out["smoothed"]), np.nan_to_num(ref["smoothed"]))
+
+
+# ---------------------------------------------------------------- split phases / vocab sharding on one GPU
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_sharded_split_phase_matches_oracle(torch_cuda, G):
+    """Emulate G vocab shards on one GPU: one context per rank (no NCCL),
+    dinfer_step_local per shard, records concatenated in rank order,
+    dinfer_step_combine on the result -- the exact data flow of the NCCL
+    allgather path.  Compared with the unsharded oracle."""
+    import torch
+    from paper_2510_08666_b200 import Context
+    V, H, B, S, K = 2048, 256, 2, 32, 32
+    W, E = weights(V, H)
+    _, _, _, steps = vetted_trajectory(W, E, B, S, 11, hier_credit_smooth, use_credit_table=True)
+    Vl = V // G
+    ctxs = [Context(B, S, H, K, V, V_local=Vl, v_offset=r * Vl, world=G, rank=r) for r in range(G)]
+    Wd = [to_dev_bf16(W[r * Vl:(r + 1) * Vl]) for r in range(G)]
+    Ed = [to_dev_bf16(E[r * Vl:(r + 1) * Vl]) for r in range(G)]
+    emd = to_dev_bf16(E[synth.mask_id(V)])
+    words = ctxs[0].record_words(True)
+    recs = torch.zeros((G, words), dtype=torch.float32, device="cuda")
+    st = GpuState(B, S, H, K, synth.mask_id(V))
+    for t, step in enumerate(steps):
+        p = step["params"]
+        gp = gpu_params(p)
+        hid = to_dev_bf16(step["h"].reshape(B * S, H))
+        for r in range(G):
+            ctxs[r].step_local(hid, Wd[r], Ed[r], st.mask, st.cids, gp, recs[r])
+        ctxs[0].step_combine(recs, emd, st.mask, st.tokens, st.cids, st.cval, gp, st.committed, st.smoothed,
+                             st.stats)
+        torch.cuda.synchronize()
+        ctxs[0].sync()
+        compare(st.snapshot(), step["result"], step["mask"], p, where=f"G={G} iter {t}")
+
+
+def test_step_host_matches_device_step(torch_cuda):
+    import torch
+    from paper_2510_08666_b200 import Context
+    V, H, B, S, K = 2048, 256, 1, 32, 8
+    W, E = weights(V, H)
+    h = synth.planted_hidden(W, B * S, seed=12)
+    p = gpu_params(O.Params(decoder=O.DEC_HIERARCHICAL, use_credit=True, use_smooth=True, alpha_t=0.2))
+    Wd, Ed, emd = to_dev_bf16(W), to_dev_bf16(E), to_dev_bf16(E[V - 1])
+    ctx = Context(B, S, H, K, V)
+    st = GpuState(B, S, H, K, V - 1)
+    ctx.step(to_dev_bf16(h), Wd, Ed, emd, st.mask, st.tokens, st.cids, st.cval, p, st.committed, st.smoothed,
+             st.stats)
+    torch.cuda.synchronize()
+    dev = st.snapshot()
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    hh = pin(h.view(np.int16))
+    mask, tok = pin(np.ones((B, S), np.uint8)), pin(np.full((B, S), V - 1, np.int32))
+    cids, cval = pin(np.full((B, S, K), -1, np.int32)), pin(np.zeros((B, S, K), np.float32))
+    com, sm, sts = pin(np.zeros((B, S), np.uint8)), pin(np.full((B, S, H), np.nan, np.float32)), \
+        pin(np.zeros((B, S, 4), np.float32))
+    ctx.step_host(hh, Wd, Ed, emd, mask, tok, cids, cval, p, com, sm, sts)
+    assert np.array_equal(com.numpy().astype(bool), dev["committed"])
+    assert np.array_equal(tok.numpy(), dev["tokens"])
+    assert np.array_equal(cids.numpy(), dev["cids"]) and np.array_equal(cval.numpy(), dev["cval"])
+    still = mask.numpy().astype(bool)
+    assert np.array_equal(sm.numpy()[still], dev["smoothed"][still])
+
+
+def test_credit_slot_overflow_is_reported(torch_cuda):
+    """K = 1 slot cannot hold two different tokens: the device flag surfaces
+    as DINFER_ERR_DEVICE through dinfer_sync."""
+    import torch
+    from paper_2510_08666_b200 import Context, DInferError
+    V, H, B, S, K = 1024, 256, 1, 32, 1
+    W, E = weights(V, H)
+    ctx = Context(B, S, H, K, V)
+    st = GpuState(B, S, H, K, V - 1)
+    st.cids.fill_(V - 5)  # every slot occupied by a token that is never the argmax
+    st.cval.fill_(0.5)
+    p = gpu_params(O.Params(decoder=O.DEC_THRESHOLD, tau=0.99, use_credit=True))
+    h = synth.planted_hidden(W, B * S, seed=13)
+    ctx.step(to_dev_bf16(h), to_dev_bf16(W), None, None, st.mask, st.tokens, st.cids, st.cval, p, st.committed,
+             None, st.stats)
+    with pytest.raises(DInferError) as ei:
+        ctx.sync()
+    assert ei.value.status == 7
+    ctx.sync()  # sticky flag cleared
+
+
+# ---------------------------------------------------------------- full paper shapes
+@pytest.mark.slow
+def test_moe_shape_hier_credit_smooth(torch_cuda):
+    """LLaDA-MoE shape (BASELINE configs[2]): H=2048, V=157184, block 32, bs1,
+    hierarchical + credit + smoothing; the first 4 iterations of a block."""
+    run_trajectory(torch_cuda, 157184, 2048, 1, 32, 32, 0, hier_credit_smooth, True, max_iters=4)
+
+
+@pytest.mark.slow
+def test_8b_shape_threshold(torch_cuda):
+    """LLaDA-8B shape (BASELINE configs[1]): H=4096 (hidden streamed with W),
+    V=126464, block 32, bs1, threshold decoding; 3 iterations."""
+    run_trajectory(torch_cuda, 126464, 4096, 1, 32, 32, 1, thr_params(0.9), False, max_iters=3)
