@@ -201,11 +201,8 @@ def gpu_arm(args):
     stream = torch.cuda.Stream()
     nid = None
     if world > 1:
-        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(get_unique_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        nid = bytes(idt.cpu().numpy().tobytes())
+        from paper_2510_08666_b200.dist import broadcast_unique_id
+        nid = broadcast_unique_id("cuda")
     ctx = Context(B, S, H, K, V, V_local=Vl, v_offset=v0, world=world, rank=rank, stream=stream.cuda_stream,
                   nccl_id=nid)
     p = make_params(decoder="hierarchical", theta_hi=0.92, theta_lo=0.62, use_credit=True, use_smooth=True,
@@ -240,9 +237,12 @@ def gpu_arm(args):
     ctx.sync()
     torch.cuda.synchronize()
 
-    # ---- timed region: K steps, L2 flushed before each (outside the events)
-    ctx.set_timing(True)
+    # ---- timed region: K steps, L2 flushed before each (outside the events).
+    # Loop A (headline): plain steps.  Loop B: the same K steps with the
+    # library's per-kernel events on (these serialise the PDL overlap between
+    # kernels, so B's per-kernel times are upper bounds) -> roofline per kernel.
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    evb = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     phase_acc = {}
     if world > 1:
         dist.barrier()
@@ -255,24 +255,32 @@ def gpu_arm(args):
             evs[i][0].record(stream)
             one_step()
             evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+        ctx.set_timing(True)
+        for i in range(args.steps):
+            reset_and_flush()
+            evb[i][0].record(stream)
+            one_step()
+            evb[i][1].record(stream)
             ph = ctx.get_timing()  # syncs the stream (outside the event pair)
             for k_, v_ in ph.items():
                 phase_acc[k_] = phase_acc.get(k_, 0.0) + v_
+        ctx.set_timing(False)
     torch.cuda.synchronize()
-    wall = time.perf_counter() - wall0
     if world > 1:
         dist.barrier()
     ctx.sync()
-    ctx.set_timing(False)
     step_ms = [a.elapsed_time(b) for a, b in evs]
     ms = sum(step_ms) / len(step_ms)
+    ms_b = sum(a.elapsed_time(b) for a, b in evb) / len(evb)
     phases = {k_: v_ / args.steps for k_, v_ in phase_acc.items()}
     if world > 1:
-        t = torch.tensor([ms] + [phases[k_] for k_ in sorted(phases)], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms, ms_b] + [phases[k_] for k_ in sorted(phases)], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t[0])
+        ms, ms_b = float(t[0]), float(t[1])
         for j, k_ in enumerate(sorted(phases)):
-            phases[k_] = float(t[1 + j])
+            phases[k_] = float(t[2 + j])
 
     # ---- e2e: the public host-buffer call (H2D of hidden + state, D2H of state + outputs)
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
@@ -339,6 +347,8 @@ def gpu_arm(args):
             "step_roofline": {"bytes": step_bytes, "achieved_gbs": step_bytes / (ms * 1e-3) / 1e9,
                               "frac": step_bytes / (ms * 1e-3) / 1e9 / hbm},
             "phases_ms": phases,
+            "ms_per_step_with_kernel_events": ms_b,
+            "ms_per_step_min": min(step_ms), "ms_per_step_max": max(step_ms),
             "geometry": geom,
             "clocks": sampler.report(),
             "wall_s_timed_loop": wall,

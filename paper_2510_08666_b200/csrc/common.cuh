@@ -54,6 +54,15 @@ DI void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch: a kernel launched with programmatic stream
+// serialization may start (prologue, barrier init, TMEM alloc, independent
+// prefetch) while its predecessor drains; grid_dep_wait() blocks until the
+// predecessor grid has completed and its memory is visible.  Both are no-ops
+// for a normally launched kernel.
+DI void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+DI void grid_dep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- TMA
 DI void prefetch_tmap(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
@@ -76,6 +85,17 @@ DI void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, in
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
+
+// 1-D bulk copy global -> shared (async proxy), completes on `bar`.
+DI void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// Order prior generic-proxy global accesses (made visible by other CTAs'
+// release fences) before subsequent async-proxy (TMA / bulk) global reads.
+DI void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
 // ---------------------------------------------------------------- tcgen05
 DI void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {  // whole warp

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -66,9 +67,10 @@ struct dinfer_ctx {
   const void* c_w = nullptr;
   const void* c_h = nullptr;
   const void* c_e = nullptr;
-  CUtensorMap map_w{}, map_w8{}, map_h{}, map_e{};
+  CUtensorMap map_w{}, map_w8{}, map_h{}, map_e{}, map_f{};
   // timing
   int timing = 0;
+  bool pdl = true;  // programmatic dependent launch between the step's kernels
   cudaEvent_t ev_beg[kNumPhases]{}, ev_end[kNumPhases]{};
   bool ev_used[kNumPhases]{};
 };
@@ -98,6 +100,21 @@ bool encode_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
   cuuint32_t es[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// 2-D fp32 tensor [outer][inner] row-major, no swizzle (K2's logits chunks).
+bool encode_2d_f32(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                   uint32_t box_outer) {
+  auto fn = tmap_encoder();
+  if (fn == nullptr) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 4};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -196,7 +213,7 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
   a.flog = smooth ? c->flog : nullptr;
   a.err = c->err;
   ev_begin(c, kPK1);
-  DI_CUDA(launch_k1(c->map_w, c->map_w8, c->map_h, a, c->k1_grid, c->k1_smem, c->stream));
+  DI_CUDA(launch_k1(c->map_w, c->map_w8, c->map_h, a, c->k1_grid, c->k1_smem, c->stream, c->pdl));
   ev_finish(c, kPK1);
   if (smooth) {
     K2Args b{};
@@ -216,11 +233,11 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
     b.rec_stride = kStatWords + c->shp.K;
     b.part = c->part2;
     ev_begin(c, kPK2);
-    DI_CUDA(launch_k2(c->map_e, b, c->k2_smem, c->stream));
+    DI_CUDA(launch_k2(c->map_e, c->map_f, b, c->k2_smem, c->stream, c->pdl));
     ev_finish(c, kPK2);
     if (reduce_acc) {
       ev_begin(c, kPK2r);
-      DI_CUDA(launch_acc_reduce(c->part2, c->k2_VG, c->M * c->shp.H, rec + c->stats_words, c->stream));
+      DI_CUDA(launch_acc_reduce(c->part2, c->k2_VG, c->M * c->shp.H, rec + c->stats_words, c->stream, c->pdl));
       ev_finish(c, kPK2r);
     }
   }
@@ -259,7 +276,7 @@ dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, in
   k.c_gamma = p->c_gamma;
   k.err = c->err;
   ev_begin(c, kPK3);
-  DI_CUDA(launch_k3(k, c->stream));
+  DI_CUDA(launch_k3(k, c->stream, c->pdl));
   ev_finish(c, kPK3);
   if (p->use_smooth) {
     K4Args f{};
@@ -284,7 +301,7 @@ dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, in
     f.alpha_t = p->alpha_t;
     f.out = smoothed;
     ev_begin(c, kPK4);
-    DI_CUDA(launch_k4(f, c->stream));
+    DI_CUDA(launch_k4(f, c->stream, c->pdl));
     ev_finish(c, kPK4);
   }
   return DINFER_OK;
@@ -423,10 +440,18 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
 
   // ---- K2 geometry: hidden slices x vocab groups <= #SMs
   c->k2_nchunks = static_cast<int>((s.V_local + kKChunk - 1) / kKChunk);
-  c->k2_HW = (s.H % 256 == 0) ? 256 : 128;
+  // Widest hidden slice that divides H: 512 columns per CTA give 1 KB
+  // contiguous E row segments per TMA chunk and HS x VG = 4 x 37 = 148 CTAs
+  // at H = 2048 (measured: K2 131 us vs 165 us with 256-wide slices).
+  c->k2_HW = (s.H % 512 == 0) ? 512 : ((s.H % 256 == 0) ? 256 : 128);
+  if (const char* e = std::getenv("DINFER_K2_HW")) {  // tuning override: 128 / 256 / 512
+    const int hw = std::atoi(e);
+    if ((hw == 128 || hw == 256 || hw == 512) && s.H % hw == 0) c->k2_HW = hw;
+  }
+  if (const char* e = std::getenv("DINFER_PDL")) c->pdl = std::atoi(e) != 0;
   c->k2_HS = s.H / c->k2_HW;
   c->k2_VG = std::max(1, std::min(c->num_sms / std::max(1, c->k2_HS), c->k2_nchunks));
-  c->k2_pstages = 4;
+  c->k2_pstages = 3;
   for (int st = 6; st >= 2; --st)
     if (k2_smem_bytes(c->N, c->k2_HW, st, c->k2_pstages) <= c->smem_optin) {
       c->k2_stages = st;
@@ -439,7 +464,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
   c->full_words = c->stats_words + (s.smooth_capable ? static_cast<size_t>(M) * s.H : 0);
   dinfer_status st = DINFER_OK;
   auto A = [&](dinfer_status x) { if (st == DINFER_OK) st = x; };
-  A(dev_alloc(&c->part1, static_cast<size_t>(c->k1_grid) * M * 3));
+  A(dev_alloc(&c->part1, static_cast<size_t>(c->k1_grid) * M * 4));
   A(dev_alloc(&c->counter, 4));
   A(dev_alloc(&c->err, 4));
   A(dev_alloc(&c->rec_local, c->full_words));
@@ -455,6 +480,10 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
         cudaMemset(c->rec_local, 0, c->full_words * 4) != cudaSuccess)
       st = DINFER_ERR_CUDA;
   }
+  if (st == DINFER_OK && s.smooth_capable &&
+      !encode_2d_f32(&c->map_f, c->flog, static_cast<uint64_t>(s.V_local), static_cast<uint64_t>(M), kKChunk,
+                     static_cast<uint32_t>(c->N)))
+    st = DINFER_ERR_CUDA;
   for (int i = 0; i < kNumPhases && st == DINFER_OK; ++i) {
     if (cudaEventCreate(&c->ev_beg[i]) != cudaSuccess || cudaEventCreate(&c->ev_end[i]) != cudaSuccess)
       st = DINFER_ERR_CUDA;

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + a.stages;
   uint64_t* tfull = empty + a.stages;
   uint64_t* tempty = tfull + 2;
-  uint64_t* hfull = tempty + 2;
+  uint64_t* mfull = tempty + 2;  // last-CTA bulk load of the partials
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L.misc_off);  // tmem base, last flag, entry count
   int* head = reinterpret_cast<int*>(smem + L.head_off);
   int16_t* ent_s = reinterpret_cast<int16_t*>(smem + L.ent_off);
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], kEpiWarps * kWarpThreads);
     }
-    mbar_init(hfull, 1);
+    mbar_init(mfull, 1);
     fence_mbar_init();
   }
   if (warp == 5) tmem_alloc(&misc[0], tmem_cols);
@@ -144,46 +144,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-
-  // Credited (position, slot) entries whose token lives in this slab: their
-  // raw logits are captured for the credit fuse.  Rows decided at step start
-  // are frozen (reading c7) and skipped.
-  if (warp < kEpiWarps && a.credit_ids != nullptr) {
-    const int stride = kStatWords + a.K;
-    for (int e = threadIdx.x; e < a.M * a.K; e += kEpiWarps * kWarpThreads) {
-      const int s = e / a.K, k = e - s * a.K;
-      if (!a.mask[s]) continue;
-      const int id = a.credit_ids[e];
-      if (id < 0) continue;
-      const int lv = id - a.v_offset;
-      if (lv < 0 || lv >= a.V_local) {  // owned by another rank
-        if (blockIdx.x == 0) a.rec[s * stride + kStatWords + k] = neg_inf();
-        continue;
-      }
-      if (lv < r0 || lv >= r1) continue;
-      const int slot = static_cast<int>(atomicAdd(&misc[2], 1u));
-      if (slot >= kMaxCreditEnt) {
-        atomicOr(a.err, kErrCreditEntOverflow);
-        continue;
-      }
-      ent_s[slot] = static_cast<int16_t>(s);
-      ent_k[slot] = static_cast<int16_t>(k);
-      ent_next[slot] = static_cast<int16_t>(atomicExch(&head[lv - r0], slot));
-    }
-  }
-  __syncthreads();
   const uint32_t tmem_base = misc[0];
+  // The next kernel (K2 / K3) may be scheduled onto SMs as they free up.
+  grid_dep_launch_dependents();
 
   if (warp == 4) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
+      grid_dep_wait();  // hidden may be produced by the preceding kernel
       const uint64_t pol_w = policy_evict_first();  // W is streamed exactly once
       const uint64_t pol_h = policy_evict_last();   // hidden is re-read by every CTA
-      if (a.h_resident) {
-        mbar_expect_tx(hfull, static_cast<uint32_t>(a.num_kc) * hchunk);
-        for (int kc = 0; kc < a.num_kc; ++kc)
-          tma_load_2d(h_sm + kc * hchunk, &map_h, hfull, kc * kKChunk, 0, pol_h);
-      }
       int stage = 0;
       uint32_t phase = 0;
       for (int t = 0; t < ntiles; ++t) {
@@ -191,7 +161,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int rows = min(kTileRows, r1 - row0);
         for (int kc = 0; kc < a.num_kc; ++kc) {
           mbar_wait(&empty[stage], phase ^ 1u);
-          const uint32_t bytes = static_cast<uint32_t>(rows) * 128u + (a.h_resident ? 0u : hchunk);
+          // hidden chunk kc rides with W chunk kc: every stage when streamed,
+          // only tile 0 when resident (it then stays in slot kc).
+          const bool with_h = !a.h_resident || t == 0;
+          const uint32_t bytes = static_cast<uint32_t>(rows) * 128u + (with_h ? hchunk : 0u);
           mbar_expect_tx(&full[stage], bytes);
           uint8_t* dst = w_sm + stage * kWStageBytes;
           if (rows == kTileRows) {
@@ -200,7 +173,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int r = 0; r < rows; r += kRowGran)
               tma_load_2d(dst + r * 128, &map_w8, &full[stage], kc * kKChunk, row0 + r, pol_w);
           }
-          if (!a.h_resident) tma_load_2d(h_sm + stage * hchunk, &map_h, &full[stage], kc * kKChunk, 0, pol_h);
+          if (with_h)
+            tma_load_2d(h_sm + (a.h_resident ? kc : stage) * hchunk, &map_h, &full[stage], kc * kKChunk, 0, pol_h);
           if (++stage == a.stages) {
             stage = 0;
             phase ^= 1u;
@@ -213,7 +187,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16(kTileRows, N, false, false);
-      if (a.h_resident) mbar_wait(hfull, 0);
       int stage = 0;
       uint32_t phase = 0;
       for (int t = 0; t < ntiles; ++t) {
@@ -244,6 +217,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {
     // ------------------------------------------------------------ epilogue
+    // Credited (position, slot) entries whose token lives in this slab: their
+    // raw logits are captured for the credit fuse.  Rows decided at step start
+    // are frozen (reading c7) and skipped.  Runs while the first W chunks fly.
+    grid_dep_wait();  // mask / credit ids of the previous step's commit visible
+    if (a.credit_ids != nullptr) {
+      const int stride = kStatWords + a.K;
+      for (int e = threadIdx.x; e < a.M * a.K; e += kEpiWarps * kWarpThreads) {
+        const int s = e / a.K, k = e - s * a.K;
+        if (!a.mask[s]) continue;
+        const int id = a.credit_ids[e];
+        if (id < 0) continue;
+        const int lv = id - a.v_offset;
+        if (lv < 0 || lv >= a.V_local) {  // owned by another rank
+          if (blockIdx.x == 0) a.rec[s * stride + kStatWords + k] = neg_inf();
+          continue;
+        }
+        if (lv < r0 || lv >= r1) continue;
+        const int slot = static_cast<int>(atomicAdd(&misc[2], 1u));
+        if (slot >= kMaxCreditEnt) {
+          atomicOr(a.err, kErrCreditEntOverflow);
+          continue;
+        }
+        ent_s[slot] = static_cast<int16_t>(s);
+        ent_k[slot] = static_cast<int16_t>(k);
+        ent_next[slot] = static_cast<int16_t>(atomicExch(&head[lv - r0], slot));
+      }
+    }
+    named_bar_epi();
     const int ng = N / 32;
     float Rm[kMaxGroups];
     int Ri[kMaxGroups];
@@ -322,32 +323,46 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float* r = red + (w * N + col) * 3;
         stat_combine(m, ix, l, r[0], __float_as_int(r[1]), r[2]);
       }
-      float* p = a.part + (static_cast<long>(blockIdx.x) * a.M + col) * 3;
-      p[0] = m;
-      p[1] = __int_as_float(ix);
-      p[2] = l;
+      // partials are column-major [M][grid] so a column range is contiguous
+      reinterpret_cast<float4*>(a.part)[static_cast<long>(col) * gridDim.x + blockIdx.x] =
+          make_float4(m, __int_as_float(ix), l, 0.f);
     }
     __threadfence();
     named_bar_epi();
     if (threadIdx.x == 0) misc[1] = (atomicAdd(a.counter, 1u) == gridDim.x - 1) ? 1u : 0u;
     named_bar_epi();
     if (misc[1]) {
-      // Last CTA: merge the per-CTA partials.  tpc threads per column, each
-      // over a strided subset of CTAs, then an in-order shuffle merge.
+      // Last CTA: bulk-copy the partials (column slabs) into the now idle
+      // operand region of shared memory, then merge each column with tpc
+      // threads in a fixed order (deterministic).
       __threadfence();
+      fence_proxy_async_global();
       const int nthr = kEpiWarps * kWarpThreads;
+      const int G = static_cast<int>(gridDim.x);
+      const int cols_fit = max(1, static_cast<int>(L.bar_off / (static_cast<uint32_t>(G) * 16u)));
       int tpc = 1;
       while (tpc * 2 * a.M <= nthr && tpc < 32) tpc *= 2;
-      const int col_per_pass = nthr / tpc;
+      const int col_per_pass = min(nthr / tpc, cols_fit);
+      const float4* ps = reinterpret_cast<const float4*>(smem);
+      uint32_t mphase = 0;
       for (int cb = 0; cb < a.M; cb += col_per_pass) {
-        const int col = cb + threadIdx.x / tpc;
+        const int ncols = min(col_per_pass, a.M - cb);
+        if (threadIdx.x == 0) {
+          fence_proxy_async();  // previous pass's generic smem reads before the async overwrite
+          const uint32_t bytes = static_cast<uint32_t>(ncols * G) * 16u;
+          mbar_expect_tx(mfull, bytes);
+          bulk_load(smem, reinterpret_cast<const float4*>(a.part) + static_cast<long>(cb) * G, bytes, mfull);
+        }
+        mbar_wait(mfull, mphase);
+        mphase ^= 1u;
+        const int lc = threadIdx.x / tpc;
         const int sub = threadIdx.x % tpc;
         float m = neg_inf(), l = 0.f;
         int ix = INT_MAX;
-        if (col < a.M) {
-          for (int c = sub; c < static_cast<int>(gridDim.x); c += tpc) {
-            const float* p = a.part + (static_cast<long>(c) * a.M + col) * 3;
-            stat_combine(m, ix, l, __ldcg(p), __float_as_int(__ldcg(p + 1)), __ldcg(p + 2));
+        if (lc < ncols) {
+          for (int c = sub; c < G; c += tpc) {
+            const float4 p = ps[lc * G + c];
+            stat_combine(m, ix, l, p.x, __float_as_int(p.y), p.z);
           }
         }
         for (int o = 1; o < tpc; o <<= 1) {
@@ -356,13 +371,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float rl = __shfl_down_sync(0xffffffffu, l, o);
           if ((sub & (2 * o - 1)) == 0) stat_combine(m, ix, l, rm, ri, rl);
         }
-        if (col < a.M && sub == 0) {
-          float* r = a.rec + col * stride;
+        if (lc < ncols && sub == 0) {
+          float* r = a.rec + (cb + lc) * stride;
           r[0] = m;
           r[1] = __int_as_float(ix);
           r[2] = l;
           r[3] = 0.f;
         }
+        named_bar_epi();  // smem slab free for the next pass
       }
       if (threadIdx.x == 0) *a.counter = 0u;
     }
@@ -380,7 +396,7 @@ size_t k1_smem_bytes(int N, int H, int stages, int h_resident, int slab_rows_max
 }
 
 cudaError_t launch_k1(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
-                      const K1Args& a, int grid, size_t smem, cudaStream_t st) {
+                      const K1Args& a, int grid, size_t smem, cudaStream_t st, bool pdl) {
   static size_t configured = 0;
   if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(k1_vocab_proj, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -388,8 +404,7 @@ cudaError_t launch_k1(const CUtensorMap& map_w, const CUtensorMap& map_w8, const
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  k1_vocab_proj<<<grid, kThreads, smem, st>>>(map_w, map_w8, map_h, a);
-  return cudaGetLastError();
+  return launch_ex(k1_vocab_proj, dim3(grid), dim3(kThreads), smem, st, pdl, map_w, map_w8, map_h, a);
 }
 
 }  // namespace dinfer

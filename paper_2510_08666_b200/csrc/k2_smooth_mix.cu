@@ -38,7 +38,8 @@ struct Layout {
 };
 __host__ __device__ inline Layout make_layout(int N, int HW, int stages, int pstages) {
   Layout L;
-  const uint32_t e_stage = static_cast<uint32_t>(HW) * 128u;  // HW/64 boxes of 8 KB
+  // E boxes (HW/64 x 8 KB) + the fp32 logits chunk [N x 64] (no swizzle)
+  const uint32_t e_stage = static_cast<uint32_t>(HW) * 128u + static_cast<uint32_t>(N) * 256u;
   const uint32_t p_stage = 2u * static_cast<uint32_t>(N) * 128u;
   L.e_off = 0;
   L.p_off = L.e_off + static_cast<uint32_t>(stages) * e_stage;
@@ -55,14 +56,16 @@ DI uint32_t pack_bf16x2(float lo_elem, float hi_elem) {
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    k2_smooth_mix(const __grid_constant__ CUtensorMap map_e, const K2Args a) {
+    k2_smooth_mix(const __grid_constant__ CUtensorMap map_e, const __grid_constant__ CUtensorMap map_f,
+                  const K2Args a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const Layout L = make_layout(a.N, a.HW, a.stages, a.pstages);
   const int warp = threadIdx.x / kWarpThreads;
   const int lane = threadIdx.x % kWarpThreads;
   const int N = a.N;
-  const uint32_t e_stage = static_cast<uint32_t>(a.HW) * 128u;
+  const uint32_t e_bytes = static_cast<uint32_t>(a.HW) * 128u;
+  const uint32_t e_stage = e_bytes + static_cast<uint32_t>(N) * 256u;
   const uint32_t p_half = static_cast<uint32_t>(N) * 128u;
 
   uint8_t* e_sm = smem + L.e_off;
@@ -83,6 +86,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 4 && lane == 0) {
     prefetch_tmap(&map_e);
+    prefetch_tmap(&map_f);
     for (int i = 0; i < a.stages; ++i) {
       mbar_init(&efull[i], 1);
       mbar_init(&eempty[i], 1);
@@ -95,27 +99,39 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_mbar_init();
   }
   if (warp == 5) tmem_alloc(&misc[0], tmem_cols);
-  if (warp < kEpiWarps) {
-    for (int s = threadIdx.x; s < N; s += kEpiWarps * kWarpThreads)
-      m_sm[s] = (s < a.M) ? a.rec[s * a.rec_stride] : 0.f;
-  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = misc[0];
+  grid_dep_launch_dependents();
 
   if (warp == 4) {
     // ------------------------------------------------------------ TMA: E tiles
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int c = c0; c < c1; ++c) {
+      const uint64_t pol_f = policy_evict_last();  // re-read by the other hidden slices
+      // Prologue: the first `npre` E tiles do not depend on K1 -- issue them
+      // before waiting for K1 (PDL), so E streaming overlaps K1's tail.
+      const int npre = min(a.stages, c1 - c0);
+      for (int j = 0; j < npre; ++j) {
+        mbar_expect_tx(&efull[j], e_stage);
+        for (int b = 0; b < a.HW / 64; ++b)
+          tma_load_2d(e_sm + j * e_stage + b * kEBox, &map_e, &efull[j], hs * a.HW + b * 64, (c0 + j) * kKChunk,
+                      pol);
+      }
+      grid_dep_wait();  // K1's logits (flog) visible
+      for (int j = 0; j < npre; ++j)
+        tma_load_2d(e_sm + j * e_stage + e_bytes, &map_f, &efull[j], (c0 + j) * kKChunk, 0, pol_f);
+      int stage = npre % a.stages;
+      uint32_t phase = (npre == a.stages) ? 1u : 0u;
+      for (int c = c0 + npre; c < c1; ++c) {
         mbar_wait(&eempty[stage], phase ^ 1u);
         mbar_expect_tx(&efull[stage], e_stage);
         for (int b = 0; b < a.HW / 64; ++b)
           tma_load_2d(e_sm + stage * e_stage + b * kEBox, &map_e, &efull[stage], hs * a.HW + b * 64, c * kKChunk,
                       pol);
+        // logits chunk f[0:N, c*64 : c*64+64] (rows >= M and columns >= V_local zero-filled)
+        tma_load_2d(e_sm + stage * e_stage + e_bytes, &map_f, &efull[stage], c * kKChunk, 0, pol_f);
         if (++stage == a.stages) {
           stage = 0;
           phase ^= 1u;
@@ -165,9 +181,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ------------------------------------------------------------ P producers
     const int tid = threadIdx.x;
-    int ps = 0;
-    uint32_t pph = 0;
+    grid_dep_wait();  // K1's record (m per row) visible
+    for (int s = tid; s < N; s += kEpiWarps * kWarpThreads) m_sm[s] = (s < a.M) ? a.rec[s * a.rec_stride] : 0.f;
+    asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * kWarpThreads) : "memory");
+    int ps = 0, es = 0;
+    uint32_t pph = 0, eph = 0;
     for (int c = c0; c < c1; ++c) {
+      mbar_wait(&efull[es], eph);  // logits chunk landed (with the E tile)
+      const float* f_sm = reinterpret_cast<const float*>(e_sm + es * e_stage + e_bytes);
+      if (++es == a.stages) {
+        es = 0;
+        eph ^= 1u;
+      }
       mbar_wait(&pempty[ps], pph ^ 1u);
       uint8_t* phi = p_sm + ps * 2 * p_half;
       uint8_t* plo = phi + p_half;
@@ -176,8 +201,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int v0 = c * kKChunk + cc * 8;
         float p[8];
         if (s < a.M && v0 < a.V_local) {
-          const float4* src = reinterpret_cast<const float4*>(a.flog + static_cast<long>(s) * a.V_local + v0);
-          const float4 q0 = __ldcg(src), q1 = __ldcg(src + 1);
+          const float4* src = reinterpret_cast<const float4*>(f_sm + s * kKChunk + cc * 8);
+          const float4 q0 = src[0], q1 = src[1];
           const float ms = m_sm[s];
           p[0] = fexp(q0.x - ms); p[1] = fexp(q0.y - ms); p[2] = fexp(q0.z - ms); p[3] = fexp(q0.w - ms);
           p[4] = fexp(q1.x - ms); p[5] = fexp(q1.y - ms); p[6] = fexp(q1.z - ms); p[7] = fexp(q1.w - ms);
@@ -234,6 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 __global__ void acc_reduce_kernel(const float* __restrict__ part, int VG, int MH, float* __restrict__ out) {
+  grid_dep_wait();
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (i >= MH) return;
   float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -250,7 +276,8 @@ size_t k2_smem_bytes(int N, int HW, int stages, int pstages) {
   return make_layout(N, HW, stages, pstages).total + 1024;
 }
 
-cudaError_t launch_k2(const CUtensorMap& map_e, const K2Args& a, size_t smem, cudaStream_t st) {
+cudaError_t launch_k2(const CUtensorMap& map_e, const CUtensorMap& map_f, const K2Args& a, size_t smem,
+                      cudaStream_t st, bool pdl) {
   static size_t configured = 0;
   if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(k2_smooth_mix, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -258,15 +285,13 @@ cudaError_t launch_k2(const CUtensorMap& map_e, const K2Args& a, size_t smem, cu
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  k2_smooth_mix<<<a.HS * a.VG, kThreads, smem, st>>>(map_e, a);
-  return cudaGetLastError();
+  return launch_ex(k2_smooth_mix, dim3(a.HS * a.VG), dim3(kThreads), smem, st, pdl, map_e, map_f, a);
 }
 
-cudaError_t launch_acc_reduce(const float* part, int VG, int MH, float* out, cudaStream_t st) {
+cudaError_t launch_acc_reduce(const float* part, int VG, int MH, float* out, cudaStream_t st, bool pdl) {
   const int threads = 256;
   const int blocks = (MH / 4 + threads - 1) / threads;
-  acc_reduce_kernel<<<blocks, threads, 0, st>>>(part, VG, MH, out);
-  return cudaGetLastError();
+  return launch_ex(acc_reduce_kernel, dim3(blocks), dim3(threads), 0, st, pdl, part, VG, MH, out);
 }
 
 }  // namespace dinfer

@@ -2,15 +2,19 @@
 // threshold / hierarchical selection, commit.  K4 smooth_finalize -- the
 // iteration-smoothing output e_{t+1} for positions still masked.
 //
-// K3: one CTA per batch row, one thread per position (S <= 1024).
+// K3: one CTA per batch row.  Phase 1 is warp-per-position / lane-per-slot:
 //   combine   m = max_r m_r, v* = v*_r of the maximiser (lowest id on ties),
-//             l = sum_r l_r e^{m_r - m}; lse = m + ln l; p* = 1/l
+//             l = sum_r l_r e^{m_r - m} in rank order; lse = m + ln l; p* = 1/l
+//
 //   credit    undecided rows: C <- beta*C; C[v*] += p*^gamma  (Eq. credit-update,
 //             P:306-313) on K sparse slots (exactly the dense table: untouched
-//             tokens have C = 0); fuse f~ = f + alpha ln(1+C) (Eq. logits-fuse,
-//             P:317-322); only credited tokens change, so
+//             tokens have C = 0); hit / first-empty slot found by warp ballots;
+//             fuse f~ = f + alpha ln(1+C) (Eq. logits-fuse); only
+//             credited tokens change, so
 //             lse~ = m + ln(l + sum_{cred} e^{f_v - m}((1+C_v)^alpha - 1)),
-//             v~ = argmax_{cred u {v*}} f~, p~ = e^{f~_{v~} - lse~}.
+//             v~ = argmax_{cred u {v*}} f~ (lowest id on ties), p~ = e^{f~_{v~} - lse~}
+//             (warp-shuffle reductions in a fixed order).
+// Phase 2 is thread-per-position:
 //   select    threshold (strict '>', fallback max) or hierarchical
 //             (maximal runs of undecided positions; per run the
 //             best position, ties nearest the run centre then lower index,
@@ -18,6 +22,7 @@
 //   commit    tokens[s] = v~, mask[s] = 0, committed[s] = 1
 // K4: e_{t+1}[s,:] = e_mask + alpha_t * (sum_p acc_p[s,:] e^{m_p - m}) / l
 //     for rows still undecided (App. A.1).
+#include <algorithm>
 #include <climits>
 
 #include "common.cuh"
@@ -29,6 +34,7 @@ namespace dinfer {
 namespace {
 
 constexpr int kMaxS = 1024;
+constexpr int kK3Threads = 1024;
 
 DI int run_first(const uint32_t* words, int s) {
   int w = s >> 5;
@@ -50,107 +56,156 @@ DI int run_last(const uint32_t* words, int s, int nwords) {
   return (w << 5) + __ffs(z) - 2;
 }
 
-__global__ void k3_select_commit(const K3Args a) {
-  __shared__ uint32_t s_und[kMaxS / 32];
+// argmax with the lowest id on ties, over (value, id) pairs of a warp
+DI void warp_argmax(float& v, int& id) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, id, o);
+    if (ov > v || (ov == v && oi < id)) {
+      v = ov;
+      id = oi;
+    }
+  }
+}
+DI float warp_sum(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+__global__ void __launch_bounds__(kK3Threads) k3_select_commit(const K3Args a) {
   __shared__ uint32_t s_reg[kMaxS / 32];
   __shared__ int s_runA[kMaxS];
   __shared__ unsigned long long s_runkey[kMaxS];
+  __shared__ float s_pt[kMaxS];
+  __shared__ int s_vt[kMaxS];
+  __shared__ uint8_t s_und[kMaxS];
   __shared__ unsigned long long s_best;
 
-  const int b = blockIdx.x;
-  const int s = threadIdx.x;
-  const int nwords = blockDim.x / 32;
-  const bool valid = s < a.S;
-  const int i = b * a.S + s;
-  const int lane = s & 31, warp = s >> 5;
-  const float thr_primary = (a.decoder == 0) ? a.tau : a.theta_hi;
+  grid_dep_wait();  // K1 / K2 / allgather results visible
+  grid_dep_launch_dependents();
 
-  bool und = false;
-  float pt = 0.f;
-  int vt = 0;
-  if (valid) {
-    und = a.mask[i] != 0;
-    // ---- combine the `world` records (fixed rank order)
-    const float* r0 = a.recs + static_cast<long>(i) * a.rec_stride;
-    float m = r0[0], l = r0[2];
-    int vstar = __float_as_int(r0[1]);
-    for (int r = 1; r < a.world; ++r) {
-      const float* rr = a.recs + r * a.rec_words + static_cast<long>(i) * a.rec_stride;
-      stat_combine(m, vstar, l, rr[0], __float_as_int(rr[1]), rr[2]);
+  const int b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+
+  // ------------------------------------------------------------ phase 1
+  for (int s = warp; s < a.S; s += nwarps) {
+    const int i = b * a.S + s;
+    const long roff = static_cast<long>(i) * a.rec_stride;
+    float m = neg_inf(), l = 0.f;
+    int vstar = INT_MAX;
+    if (lane < a.world) {
+      const float* rr = a.recs + lane * a.rec_words + roff;
+      m = rr[0];
+      vstar = __float_as_int(rr[1]);
+      l = rr[2];
     }
+    {  // merge ranks 1..world-1 into lane 0 in rank order, then broadcast
+      float m0 = m, l0 = l;
+      int v0 = vstar;
+      for (int r = 1; r < a.world; ++r) {
+        const float mr = __shfl_sync(0xffffffffu, m, r);
+        const int vr = __shfl_sync(0xffffffffu, vstar, r);
+        const float lr = __shfl_sync(0xffffffffu, l, r);
+        stat_combine(m0, v0, l0, mr, vr, lr);
+      }
+      m = __shfl_sync(0xffffffffu, m0, 0);
+      vstar = __shfl_sync(0xffffffffu, v0, 0);
+      l = __shfl_sync(0xffffffffu, l0, 0);
+    }
+    const bool und = a.mask[i] != 0;
     const float lse = m + logf(l);
     const float pstar = 1.0f / l;
-    vt = vstar;
-    pt = pstar;
+    int vt = vstar;
+    float pt = pstar;
     if (a.use_credit && und) {
-      int32_t* ids = a.credit_ids + static_cast<long>(i) * a.K;
-      float* vals = a.credit_val + static_cast<long>(i) * a.K;
+      const long cbase = static_cast<long>(i) * a.K;
       const float gain = powf(pstar, a.c_gamma);
+      // pass 1: decay, locate the slot of v* (or the first empty one)
       int hit = -1, empty = -1;
-      for (int k = 0; k < a.K; ++k) {
-        const int id = ids[k];
-        if (id < 0) {
-          if (empty < 0) empty = k;
-          continue;
+      for (int k0 = 0; k0 < a.K; k0 += 32) {
+        const int k = k0 + lane;
+        const int id = (k < a.K) ? a.credit_ids[cbase + k] : INT_MAX;
+        if (k < a.K && id >= 0) a.credit_val[cbase + k] = a.c_beta * a.credit_val[cbase + k];
+        const unsigned hb = __ballot_sync(0xffffffffu, k < a.K && id == vstar);
+        const unsigned eb = __ballot_sync(0xffffffffu, k < a.K && id < 0);
+        if (hit < 0 && hb) hit = k0 + __ffs(hb) - 1;
+        if (empty < 0 && eb) empty = k0 + __ffs(eb) - 1;
+      }
+      __syncwarp();  // decayed values visible to lane 0
+      if (lane == 0) {
+        if (hit >= 0) {
+          a.credit_val[cbase + hit] += gain;
+        } else if (empty >= 0) {
+          a.credit_ids[cbase + empty] = vstar;
+          a.credit_val[cbase + empty] = gain;
+        } else {
+          atomicOr(a.err, kErrCreditSlotsFull);
         }
-        vals[k] = a.c_beta * vals[k];
-        if (id == vstar) hit = k;
       }
-      if (hit >= 0) {
-        vals[hit] += gain;
-      } else if (empty >= 0) {
-        ids[empty] = vstar;
-        vals[empty] = gain;
-      } else {
-        atomicOr(a.err, kErrCreditSlotsFull);
-      }
-      // fuse over credited tokens (v* included)
+      __syncwarp();
+      // pass 2: fuse over credited tokens (v* included)
       float best = m, extra = 0.f;
       int best_id = vstar;
-      for (int k = 0; k < a.K; ++k) {
-        const int id = ids[k];
-        if (id < 0) continue;
-        float fk;
-        if (id == vstar) {
-          fk = m;
-        } else {
-          fk = a.recs[static_cast<long>(i) * a.rec_stride + kStatWords + k];
-          for (int r = 1; r < a.world; ++r)
-            fk = fmaxf(fk, a.recs[r * a.rec_words + static_cast<long>(i) * a.rec_stride + kStatWords + k]);
-        }
-        const float lc = log1pf(vals[k]);
-        const float ft = fk + a.c_alpha * lc;
-        extra += expf(fk - m) * expm1f(a.c_alpha * lc);
-        if (ft > best || (ft == best && id < best_id)) {
-          best = ft;
-          best_id = id;
+      for (int k0 = 0; k0 < a.K; k0 += 32) {
+        const int k = k0 + lane;
+        const int id = (k < a.K) ? a.credit_ids[cbase + k] : -1;
+        if (id >= 0) {
+          float fk = m;
+          if (id != vstar) {
+            fk = a.recs[roff + kStatWords + k];
+            for (int r = 1; r < a.world; ++r) fk = fmaxf(fk, a.recs[r * a.rec_words + roff + kStatWords + k]);
+          }
+          const float lc = log1pf(a.credit_val[cbase + k]);
+          const float ft = fk + a.c_alpha * lc;
+          extra += expf(fk - m) * expm1f(a.c_alpha * lc);
+          if (ft > best || (ft == best && id < best_id)) {
+            best = ft;
+            best_id = id;
+          }
         }
       }
+      extra = warp_sum(extra);
+      warp_argmax(best, best_id);
       const float lse_t = m + logf(l + extra);
       vt = best_id;
       pt = expf(best - lse_t);
     }
-    if (a.stats != nullptr) {
-      float* st = a.stats + static_cast<long>(i) * 4;
-      st[0] = m;
-      st[1] = lse;
-      st[2] = pt;
-      st[3] = __int_as_float(vt);
+    if (lane == 0) {
+      if (a.stats != nullptr) {
+        float* st = a.stats + static_cast<long>(i) * 4;
+        st[0] = m;
+        st[1] = lse;
+        st[2] = pt;
+        st[3] = __int_as_float(vt);
+      }
+      a.ml[2 * i] = m;
+      a.ml[2 * i + 1] = l;
+      s_pt[s] = pt;
+      s_vt[s] = vt;
+      s_und[s] = und ? 1 : 0;
     }
-    a.ml[2 * i] = m;
-    a.ml[2 * i + 1] = l;
   }
+  __syncthreads();
 
-  // ---- selection
+  // ------------------------------------------------------------ phase 2: selection
+  const int s = threadIdx.x;
+  const bool valid = s < a.S;
+  const int nwords = (a.S + 31) / 32;
+  const bool und = valid && s_und[s];
+  const float pt = valid ? s_pt[s] : 0.f;
+  const float thr_primary = (a.decoder == 0) ? a.tau : a.theta_hi;
   bool A = und && pt > thr_primary;
-  const unsigned ub = __ballot_sync(0xffffffffu, und);
-  if (lane == 0) s_und[warp] = ub;
   if (a.decoder == 1) {
     const bool region = und && !(a.runs_after_hi && A);
     const unsigned rb = __ballot_sync(0xffffffffu, region);
-    if (lane == 0) s_reg[warp] = rb;
-    s_runA[s] = 0;
-    s_runkey[s] = 0ull;
+    if (lane == 0 && warp < nwords) s_reg[warp] = rb;
+    if (valid) {
+      s_runA[s] = 0;
+      s_runkey[s] = 0ull;
+    }
     __syncthreads();
     int first = 0, last = 0;
     unsigned long long key = 0ull;
@@ -170,25 +225,27 @@ __global__ void k3_select_commit(const K3Args a) {
   const int anyA = __syncthreads_or(A);
   if (!anyA) {  // fallback: the undecided position with max p~ (lowest index on ties)
     if (und) {
-      const unsigned long long key =
-          (static_cast<unsigned long long>(__float_as_uint(pt)) << 32) | static_cast<unsigned long long>(0xFFFFFFFFu - s);
+      const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(pt)) << 32) |
+                                     static_cast<unsigned long long>(0xFFFFFFFFu - s);
       atomicMax(&s_best, key);
     }
     __syncthreads();
     A = und && s_best != 0ull && static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(s_best & 0xFFFFFFFFull)) == s;
   }
 
-  // ---- commit
+  // ------------------------------------------------------------ commit
   if (valid) {
+    const int i = b * a.S + s;
     a.committed[i] = A ? 1 : 0;
     if (A) {
-      a.tokens[i] = vt;
+      a.tokens[i] = s_vt[s];
       a.mask[i] = 0;
     }
   }
 }
 
-__global__ void k4_smooth_finalize(const K4Args a) {
+__global__ void __launch_bounds__(256) k4_smooth_finalize(const K4Args a) {
+  grid_dep_wait();  // K3's mask / (m, l) and K2's partials visible
   const int h4 = a.H / 4;
   const long t = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= static_cast<long>(a.M) * h4) return;
@@ -197,14 +254,27 @@ __global__ void k4_smooth_finalize(const K4Args a) {
   if (!a.mask[s]) return;  // only rows still masked get e_{t+1}
   const float m = a.ml[2 * s], l = a.ml[2 * s + 1];
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int p = 0; p < a.nparts; ++p) {
-    const float4 v =
-        __ldcg(reinterpret_cast<const float4*>(a.acc + p * a.acc_stride + static_cast<long>(s) * a.H + h));
-    const float sc = (a.m_part == nullptr) ? 1.f : __expf(a.m_part[p * a.m_stride + static_cast<long>(s) * a.m_rowstride] - m);
-    acc.x = fmaf(v.x, sc, acc.x);
-    acc.y = fmaf(v.y, sc, acc.y);
-    acc.z = fmaf(v.z, sc, acc.z);
-    acc.w = fmaf(v.w, sc, acc.w);
+  const float* src = a.acc + static_cast<long>(s) * a.H + h;
+  constexpr int kBatch = 8;  // independent loads in flight per thread
+  for (int p0 = 0; p0 < a.nparts; p0 += kBatch) {
+    float4 v[kBatch];
+    float sc[kBatch];
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int p = p0 + j;
+      v[j] = (p < a.nparts) ? __ldcg(reinterpret_cast<const float4*>(src + p * a.acc_stride))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+      sc[j] = (a.m_part == nullptr || p >= a.nparts)
+                  ? 1.f
+                  : expf(a.m_part[p * a.m_stride + static_cast<long>(s) * a.m_rowstride] - m);
+    }
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {  // fixed summation order
+      acc.x = fmaf(v[j].x, sc[j], acc.x);
+      acc.y = fmaf(v[j].y, sc[j], acc.y);
+      acc.z = fmaf(v[j].z, sc[j], acc.z);
+      acc.w = fmaf(v[j].w, sc[j], acc.w);
+    }
   }
   const float w = a.alpha_t / l;
   const uint2 em = *reinterpret_cast<const uint2*>(a.e_mask + h);
@@ -220,18 +290,23 @@ __global__ void k4_smooth_finalize(const K4Args a) {
 
 }  // namespace
 
-cudaError_t launch_k3(const K3Args& a, cudaStream_t st) {
-  const int threads = ((a.S + 31) / 32) * 32;
-  k3_select_commit<<<a.B, threads, 0, st>>>(a);
-  return cudaGetLastError();
+cudaError_t launch_k3(const K3Args& a, cudaStream_t st, bool pdl) {
+  static bool configured = false;
+  if (!configured) {  // same smem carveout as K1/K2 (no L1/smem reconfiguration between kernels)
+    cudaError_t e = cudaFuncSetAttribute(k3_select_commit, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k4_smooth_finalize, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  return launch_ex(k3_select_commit, dim3(a.B), dim3(kK3Threads), 0, st, pdl, a);
 }
 
-cudaError_t launch_k4(const K4Args& a, cudaStream_t st) {
+cudaError_t launch_k4(const K4Args& a, cudaStream_t st, bool pdl) {
   const long n = static_cast<long>(a.M) * (a.H / 4);
-  const int threads = 256;
+  const int threads = 128;
   const int blocks = static_cast<int>((n + threads - 1) / threads);
-  k4_smooth_finalize<<<blocks, threads, 0, st>>>(a);
-  return cudaGetLastError();
+  return launch_ex(k4_smooth_finalize, dim3(blocks), dim3(threads), 0, st, pdl, a);
 }
 
 }  // namespace dinfer

@@ -14,6 +14,23 @@ constexpr int kRowGran = 8;        // vocab-row granularity of the K1 partition
 constexpr int kMaxCreditEnt = 1024;  // per-CTA credited (position, slot) entries
 constexpr int kStatWords = 4;      // m, idx, l, pad  (record header per row)
 
+// Launch helper: optional programmatic dependent launch (PDL) attribute.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+                      Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // Device-side sticky error bits (dinfer_sync reads and clears them).
 enum : int { kErrCreditEntOverflow = 1, kErrCreditSlotsFull = 2 };
 
@@ -27,7 +44,7 @@ struct K1Args {
   int slab_rows_max;       // max rows of any CTA's slab (credit head table size)
   const uint8_t* mask;     // [M]
   const int32_t* credit_ids;  // [M][K] or nullptr
-  float* part;             // [grid][M][3]   per-CTA (m, idx, l)
+  float* part;             // [M][grid] float4 per-CTA (m, idx, l, 0), column-major
   unsigned* counter;       // last-CTA ticket, self-resetting
   float* rec;              // [M][4+K] rank record (stats part)
   float* flog;             // [M][V_local] raw logits for K2, or nullptr
@@ -35,7 +52,7 @@ struct K1Args {
 };
 size_t k1_smem_bytes(int N, int H, int stages, int h_resident, int slab_rows_max);
 cudaError_t launch_k1(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
-                      const K1Args& a, int grid, size_t smem, cudaStream_t st);
+                      const K1Args& a, int grid, size_t smem, cudaStream_t st, bool pdl);
 
 // ---------------------------------------------------------------- K2
 struct K2Args {
@@ -50,10 +67,11 @@ struct K2Args {
   float* part;             // [VG][M][H]
 };
 size_t k2_smem_bytes(int N, int HW, int stages, int pstages);
-cudaError_t launch_k2(const CUtensorMap& map_e, const K2Args& a, size_t smem, cudaStream_t st);
+cudaError_t launch_k2(const CUtensorMap& map_e, const CUtensorMap& map_f, const K2Args& a, size_t smem,
+                      cudaStream_t st, bool pdl);
 
 // sum of VG partials -> one [M][H] block (rank record acc)
-cudaError_t launch_acc_reduce(const float* part, int VG, int MH, float* out, cudaStream_t st);
+cudaError_t launch_acc_reduce(const float* part, int VG, int MH, float* out, cudaStream_t st, bool pdl);
 
 // ---------------------------------------------------------------- K3
 struct K3Args {
@@ -72,7 +90,7 @@ struct K3Args {
   float tau, theta_hi, theta_lo, c_alpha, c_beta, c_gamma;
   int* err;
 };
-cudaError_t launch_k3(const K3Args& a, cudaStream_t st);
+cudaError_t launch_k3(const K3Args& a, cudaStream_t st, bool pdl);
 
 // ---------------------------------------------------------------- K4
 struct K4Args {
@@ -89,6 +107,6 @@ struct K4Args {
   float alpha_t;
   float* out;              // [M][H]
 };
-cudaError_t launch_k4(const K4Args& a, cudaStream_t st);
+cudaError_t launch_k4(const K4Args& a, cudaStream_t st, bool pdl);
 
 }  // namespace dinfer

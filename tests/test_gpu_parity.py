@@ -82,6 +82,19 @@ def test_ragged_tail_and_odd_shapes(torch_cuda):
     run_trajectory(torch_cuda, 1000, 384, 3, 20, 24, 5, hier_credit_smooth, True)
 
 
+@pytest.mark.parametrize("hw", ["128", "256", "512"])
+def test_k2_slice_widths(torch_cuda, monkeypatch, hw):
+    """The smoothing mix gives the same result for every hidden-slice width
+    (DINFER_K2_HW tuning override): H = 1024, V = 4096."""
+    monkeypatch.setenv("DINFER_K2_HW", hw)
+    run_trajectory(torch_cuda, 4096, 1024, 1, 32, 32, 8, hier_credit_smooth, True, max_iters=4)
+
+
+def test_without_pdl(torch_cuda, monkeypatch):
+    monkeypatch.setenv("DINFER_PDL", "0")
+    run_trajectory(torch_cuda, 2048, 512, 2, 32, 32, 9, hier_credit_smooth, True, max_iters=4)
+
+
 def test_max_M_256(torch_cuda):
     run_trajectory(torch_cuda, 2048, 128, 8, 32, 8, 6, thr_params(0.9), False, max_iters=3)
 
