@@ -183,6 +183,9 @@ float dinfer_tau_schedule(float target, int32_t t, int32_t decay_steps);
  * sticky device-checked preconditions); clears the sticky device flag.      */
 dinfer_status dinfer_sync(dinfer_ctx* ctx);
 const char* dinfer_strerror(dinfer_status s);
+/* Detail of the most recent CUDA/NCCL failure on the calling thread
+ * ("<call>: <error string>"), or "" -- diagnostics only.                    */
+const char* dinfer_last_error(void);
 
 /* Instrumentation.  dinfer_set_timing(ctx, 1) brackets every kernel / the
  * collective of subsequent steps with CUDA events on the ctx stream;

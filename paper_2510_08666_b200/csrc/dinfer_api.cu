@@ -134,10 +134,17 @@ dinfer_status dev_alloc(T** p, size_t count) {
   return DINFER_OK;
 }
 
-#define DI_CUDA(call)                                 \
-  do {                                                \
-    cudaError_t e_ = (call);                          \
-    if (e_ != cudaSuccess) return DINFER_ERR_CUDA;    \
+thread_local char g_last_error[256] = "";
+
+void note_error(const char* where, const char* what) { std::snprintf(g_last_error, sizeof(g_last_error), "%s: %s", where, what); }
+
+#define DI_CUDA(call)                                     \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) {                              \
+      note_error(#call, cudaGetErrorString(e_));          \
+      return DINFER_ERR_CUDA;                             \
+    }                                                     \
   } while (0)
 
 void ev_begin(dinfer_ctx* c, int ph) {
@@ -327,6 +334,8 @@ dinfer_status check_step_ptrs(const dinfer_ctx* c, const uint16_t* hidden, const
 
 extern "C" {
 
+const char* dinfer_last_error(void) { return g_last_error; }
+
 const char* dinfer_strerror(dinfer_status s) {
   switch (s) {
     case DINFER_OK: return "ok";
@@ -417,47 +426,46 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
   const long g8 = s.V_local / kRowGran;
   c->k1_grid = static_cast<int>(std::min<long>(c->num_sms, std::max<long>(1, (s.V_local + kTileRows - 1) / kTileRows)));
   c->slab_rows_max = static_cast<int>(kRowGran * ((g8 + c->k1_grid - 1) / c->k1_grid));
-  const bool h_fits = static_cast<long>(c->N) * s.H * 2 <= 128 * 1024;
-  c->k1_hres = 0;
-  c->k1_stages = 0;
-  if (h_fits) {
-    for (int st = 8; st >= 3; --st)
-      if (k1_smem_bytes(c->N, s.H, st, 1, c->slab_rows_max) <= c->smem_optin) {
-        c->k1_hres = 1;
-        c->k1_stages = st;
-        break;
-      }
-  }
-  if (!c->k1_hres) {
-    for (int st = 8; st >= 2; --st)
-      if (k1_smem_bytes(c->N, s.H, st, 0, c->slab_rows_max) <= c->smem_optin) {
-        c->k1_stages = st;
-        break;
-      }
-  }
+  // Hidden block resident in smem (loaded once) or streamed from L2 with every
+  // W stage.  Residency only pays if it still leaves >= 4 W stages: at MoE
+  // shape it leaves 2 (measured 144 us) against 5 streamed stages (134 us).
+  int st_res = 0, st_str = 0;
+  if (static_cast<long>(c->N) * s.H * 2 <= 160 * 1024)
+    for (int st = 8; st >= 2 && st_res == 0; --st)
+      if (k1_smem_bytes(c->N, s.H, st, 1, c->slab_rows_max) <= c->smem_optin) st_res = st;
+  for (int st = 8; st >= 2 && st_str == 0; --st)
+    if (k1_smem_bytes(c->N, s.H, st, 0, c->slab_rows_max) <= c->smem_optin) st_str = st;
+  bool use_res = st_res >= 4 || (st_res > 0 && st_str == 0);
+  if (const char* e = std::getenv("DINFER_K1_HRES")) use_res = (std::atoi(e) != 0 && st_res > 0) || st_str == 0;
+  c->k1_hres = use_res ? 1 : 0;
+  c->k1_stages = use_res ? st_res : st_str;
   if (c->k1_stages == 0) { delete c; return DINFER_ERR_UNSUPPORTED; }
   c->k1_smem = k1_smem_bytes(c->N, s.H, c->k1_stages, c->k1_hres, c->slab_rows_max);
 
-  // ---- K2 geometry: hidden slices x vocab groups <= #SMs
+  // ---- K2 geometry: hidden slices x vocab groups <= #SMs.  Prefer the widest
+  // hidden slice that divides H (512 columns: 1 KB contiguous E row segments,
+  // 4 x 37 = 148 CTAs at H = 2048; measured 131 us vs 165 us with 256), then
+  // the deepest E ring (>= 2 stages) with logits/P rings of >= 2 stages.
   c->k2_nchunks = static_cast<int>((s.V_local + kKChunk - 1) / kKChunk);
-  // Widest hidden slice that divides H: 512 columns per CTA give 1 KB
-  // contiguous E row segments per TMA chunk and HS x VG = 4 x 37 = 148 CTAs
-  // at H = 2048 (measured: K2 131 us vs 165 us with 256-wide slices).
-  c->k2_HW = (s.H % 512 == 0) ? 512 : ((s.H % 256 == 0) ? 256 : 128);
-  if (const char* e = std::getenv("DINFER_K2_HW")) {  // tuning override: 128 / 256 / 512
-    const int hw = std::atoi(e);
-    if ((hw == 128 || hw == 256 || hw == 512) && s.H % hw == 0) c->k2_HW = hw;
+  int hw_pref = 512;
+  if (const char* e = std::getenv("DINFER_K2_HW")) hw_pref = std::atoi(e);  // tuning override: 128 / 256 / 512
+  c->k2_stages = 0;
+  for (int hw = 512; hw >= 128 && c->k2_stages == 0; hw /= 2) {
+    if (hw > hw_pref || s.H % hw != 0) continue;
+    for (int pst = 4; pst >= 1 && c->k2_stages == 0; --pst)  // depth 1 only for very large M
+      for (int st = 6; st >= 2; --st)
+        if (k2_smem_bytes(c->N, hw, st, pst) <= c->smem_optin) {
+          c->k2_HW = hw;
+          c->k2_pstages = pst;
+          c->k2_stages = st;
+          break;
+        }
   }
-  if (const char* e = std::getenv("DINFER_PDL")) c->pdl = std::atoi(e) != 0;
+  if (c->k2_stages == 0) { delete c; return DINFER_ERR_UNSUPPORTED; }
   c->k2_HS = s.H / c->k2_HW;
   c->k2_VG = std::max(1, std::min(c->num_sms / std::max(1, c->k2_HS), c->k2_nchunks));
-  c->k2_pstages = 3;
-  for (int st = 6; st >= 2; --st)
-    if (k2_smem_bytes(c->N, c->k2_HW, st, c->k2_pstages) <= c->smem_optin) {
-      c->k2_stages = st;
-      break;
-    }
-  c->k2_smem = k2_smem_bytes(c->N, c->k2_HW, std::max(2, c->k2_stages), c->k2_pstages);
+  c->k2_smem = k2_smem_bytes(c->N, c->k2_HW, c->k2_stages, c->k2_pstages);
+  if (const char* e = std::getenv("DINFER_PDL")) c->pdl = std::atoi(e) != 0;
 
   // ---- workspace
   c->stats_words = static_cast<size_t>(M) * (kStatWords + s.K);

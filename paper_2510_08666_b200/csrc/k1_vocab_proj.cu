@@ -30,7 +30,13 @@ namespace {
 
 constexpr int kEpiWarps = 4;
 constexpr int kThreads = (kEpiWarps + 2) * kWarpThreads;
-constexpr uint32_t kWStageBytes = kTileRows * 128;  // 16 KB
+// A pipeline stage carries two adjacent K-chunks of W (2 x [128 rows x 64 k]
+// = 32 KB, 256 contiguous bytes per row): single 16 KB boxes cap TMA
+// streaming at ~4.7 TB/s on B200, adjacent pairs reach ~5.6 TB/s
+// (tools/hbm_stream.cu, profiles/).
+constexpr int kChunksPerStage = 2;
+constexpr uint32_t kChunkBytes = kTileRows * 128;                 // 16 KB
+constexpr uint32_t kWStageBytes = kChunksPerStage * kChunkBytes;  // 32 KB
 constexpr int kMaxGroups = 8;                       // N <= 256
 
 __host__ __device__ inline uint32_t tmem_cols_pow2(uint32_t n) {
@@ -77,7 +83,8 @@ struct Layout {
 __host__ __device__ inline Layout make_layout(int N, int H, int stages, int h_resident, int slab_rows_max) {
   Layout L;
   const uint32_t hchunk = static_cast<uint32_t>(N) * 128u;
-  const uint32_t h_slots = h_resident ? static_cast<uint32_t>(H / kKChunk) : static_cast<uint32_t>(stages);
+  const uint32_t h_slots =
+      h_resident ? static_cast<uint32_t>(H / kKChunk) : static_cast<uint32_t>(stages * kChunksPerStage);
   L.h_off = 0;
   L.w_off = L.h_off + h_slots * hchunk;
   L.bar_off = L.w_off + static_cast<uint32_t>(stages) * kWStageBytes;
@@ -159,22 +166,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = 0; t < ntiles; ++t) {
         const int row0 = r0 + t * kTileRows;
         const int rows = min(kTileRows, r1 - row0);
-        for (int kc = 0; kc < a.num_kc; ++kc) {
+        for (int kc0 = 0; kc0 < a.num_kc; kc0 += kChunksPerStage) {
           mbar_wait(&empty[stage], phase ^ 1u);
           // hidden chunk kc rides with W chunk kc: every stage when streamed,
           // only tile 0 when resident (it then stays in slot kc).
           const bool with_h = !a.h_resident || t == 0;
-          const uint32_t bytes = static_cast<uint32_t>(rows) * 128u + (with_h ? hchunk : 0u);
+          const uint32_t bytes =
+              kChunksPerStage * (static_cast<uint32_t>(rows) * 128u + (with_h ? hchunk : 0u));
           mbar_expect_tx(&full[stage], bytes);
-          uint8_t* dst = w_sm + stage * kWStageBytes;
-          if (rows == kTileRows) {
-            tma_load_2d(dst, &map_w, &full[stage], kc * kKChunk, row0, pol_w);
-          } else {  // slab tail: 8-row boxes land at the same swizzled offsets
-            for (int r = 0; r < rows; r += kRowGran)
-              tma_load_2d(dst + r * 128, &map_w8, &full[stage], kc * kKChunk, row0 + r, pol_w);
+#pragma unroll
+          for (int j = 0; j < kChunksPerStage; ++j) {
+            const int kc = kc0 + j;
+            uint8_t* dst = w_sm + stage * kWStageBytes + j * kChunkBytes;
+            if (rows == kTileRows) {
+              tma_load_2d(dst, &map_w, &full[stage], kc * kKChunk, row0, pol_w);
+            } else {  // slab tail: 8-row boxes land at the same swizzled offsets
+              for (int r = 0; r < rows; r += kRowGran)
+                tma_load_2d(dst + r * 128, &map_w8, &full[stage], kc * kKChunk, row0 + r, pol_w);
+            }
+            if (with_h)
+              tma_load_2d(h_sm + (a.h_resident ? kc : stage * kChunksPerStage + j) * hchunk, &map_h, &full[stage],
+                          kc * kKChunk, 0, pol_h);
           }
-          if (with_h)
-            tma_load_2d(h_sm + (a.h_resident ? kc : stage) * hchunk, &map_h, &full[stage], kc * kKChunk, 0, pol_h);
           if (++stage == a.stages) {
             stage = 0;
             phase ^= 1u;
@@ -195,15 +208,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t d = tmem_base + static_cast<uint32_t>(buf * N);
-        for (int kc = 0; kc < a.num_kc; ++kc) {
+        for (int kc0 = 0; kc0 < a.num_kc; kc0 += kChunksPerStage) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(w_sm + stage * kWStageBytes);
-          const uint32_t b_addr = smem_u32(h_sm + (a.h_resident ? kc : stage) * hchunk);
 #pragma unroll
-          for (int k = 0; k < kKChunk / 16; ++k) {
-            mma_bf16(d, sdesc_sw128(a_addr + k * 32, 16, 1024), sdesc_sw128(b_addr + k * 32, 16, 1024), idesc,
-                     (kc | k) != 0);
+          for (int j = 0; j < kChunksPerStage; ++j) {
+            const int kc = kc0 + j;
+            const uint32_t a_addr = smem_u32(w_sm + stage * kWStageBytes + j * kChunkBytes);
+            const uint32_t b_addr = smem_u32(h_sm + (a.h_resident ? kc : stage * kChunksPerStage + j) * hchunk);
+#pragma unroll
+            for (int k = 0; k < kKChunk / 16; ++k) {
+              mma_bf16(d, sdesc_sw128(a_addr + k * 32, 16, 1024), sdesc_sw128(b_addr + k * 32, 16, 1024), idesc,
+                       (kc | k) != 0);
+            }
           }
           mma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
           if (++stage == a.stages) {

@@ -13,6 +13,10 @@
 //       from the fp32 logits: P = exp(f - m) split into bf16 hi + lo
 //       (P = hi + lo to ~2^-17), two MMAs per k-step, so the bf16 operand
 //       rounding stays far below the 2e-3 tolerance.
+// Three rings: E tiles (HW/64 boxes per 64-v chunk, 1 KB contiguous per E row
+// at HW = 512), logits chunks [N x 64] fp32 (from L2), and P tiles.  The
+// logits ring runs ahead of the E ring, so an E stage is held only for its
+// load and its MMAs.
 // Grid: HS hidden slices x VG vocab groups (<= #SMs); each CTA writes one
 // [M x HW] partial; partials are summed in fixed order downstream.
 #include "common.cuh"
@@ -24,8 +28,8 @@ namespace dinfer {
 namespace {
 
 constexpr int kEpiWarps = 4;
-constexpr int kThreads = (kEpiWarps + 2) * kWarpThreads;
-constexpr uint32_t kEBox = 64u * 64u * 2u;  // [64 h x 64 v] bf16 = 8 KB
+constexpr int kThreads = (kEpiWarps + 3) * kWarpThreads;  // + E TMA, MMA, logits TMA
+constexpr uint32_t kEBox = 64u * 64u * 2u;                // [64 h x 64 v] bf16 = 8 KB
 
 __host__ __device__ inline uint32_t tmem_cols_pow2(uint32_t n) {
   uint32_t c = 32;
@@ -34,17 +38,18 @@ __host__ __device__ inline uint32_t tmem_cols_pow2(uint32_t n) {
 }
 
 struct Layout {
-  uint32_t e_off, p_off, bar_off, misc_off, m_off, total;
+  uint32_t e_off, f_off, p_off, bar_off, misc_off, m_off, total;
 };
 __host__ __device__ inline Layout make_layout(int N, int HW, int stages, int pstages) {
   Layout L;
-  // E boxes (HW/64 x 8 KB) + the fp32 logits chunk [N x 64] (no swizzle)
-  const uint32_t e_stage = static_cast<uint32_t>(HW) * 128u + static_cast<uint32_t>(N) * 256u;
-  const uint32_t p_stage = 2u * static_cast<uint32_t>(N) * 128u;
+  const uint32_t e_stage = static_cast<uint32_t>(HW) * 128u;     // HW/64 boxes of 8 KB
+  const uint32_t f_stage = static_cast<uint32_t>(N) * 256u;      // [N x 64] fp32
+  const uint32_t p_stage = 2u * static_cast<uint32_t>(N) * 128u;  // hi + lo [N x 64] bf16
   L.e_off = 0;
-  L.p_off = L.e_off + static_cast<uint32_t>(stages) * e_stage;
+  L.f_off = L.e_off + static_cast<uint32_t>(stages) * e_stage;
+  L.p_off = L.f_off + static_cast<uint32_t>(pstages) * f_stage;
   L.bar_off = L.p_off + static_cast<uint32_t>(pstages) * p_stage;
-  L.misc_off = L.bar_off + static_cast<uint32_t>(2 * stages + 2 * pstages + 1) * 8u;
+  L.misc_off = L.bar_off + static_cast<uint32_t>(2 * stages + 4 * pstages + 1) * 8u;
   L.m_off = L.misc_off + 16u;
   L.total = L.m_off + static_cast<uint32_t>(N) * 4u;
   return L;
@@ -53,6 +58,13 @@ __host__ __device__ inline Layout make_layout(int N, int HW, int stages, int pst
 DI uint32_t pack_bf16x2(float lo_elem, float hi_elem) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(lo_elem, hi_elem);  // .x = first (lower address)
   return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+DI void advance(int& stage, uint32_t& phase, int n) {
+  if (++stage == n) {
+    stage = 0;
+    phase ^= 1u;
+  }
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -64,15 +76,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x / kWarpThreads;
   const int lane = threadIdx.x % kWarpThreads;
   const int N = a.N;
-  const uint32_t e_bytes = static_cast<uint32_t>(a.HW) * 128u;
-  const uint32_t e_stage = e_bytes + static_cast<uint32_t>(N) * 256u;
+  const uint32_t e_stage = static_cast<uint32_t>(a.HW) * 128u;
+  const uint32_t f_stage = static_cast<uint32_t>(N) * 256u;
   const uint32_t p_half = static_cast<uint32_t>(N) * 128u;
 
   uint8_t* e_sm = smem + L.e_off;
+  uint8_t* f_sm = smem + L.f_off;
   uint8_t* p_sm = smem + L.p_off;
   uint64_t* efull = reinterpret_cast<uint64_t*>(smem + L.bar_off);
   uint64_t* eempty = efull + a.stages;
-  uint64_t* pfull = eempty + a.stages;
+  uint64_t* ffull = eempty + a.stages;
+  uint64_t* fempty = ffull + a.pstages;
+  uint64_t* pfull = fempty + a.pstages;
   uint64_t* pempty = pfull + a.pstages;
   uint64_t* accfull = pempty + a.pstages;
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L.misc_off);
@@ -92,6 +107,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&eempty[i], 1);
     }
     for (int i = 0; i < a.pstages; ++i) {
+      mbar_init(&ffull[i], 1);
+      mbar_init(&fempty[i], kEpiWarps * kWarpThreads);
       mbar_init(&pfull[i], kEpiWarps * kWarpThreads);
       mbar_init(&pempty[i], 1);
     }
@@ -107,35 +124,35 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 4) {
     // ------------------------------------------------------------ TMA: E tiles
+    // E does not depend on K1: streaming starts before the PDL wait, so it
+    // overlaps K1's tail.
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      const uint64_t pol_f = policy_evict_last();  // re-read by the other hidden slices
-      // Prologue: the first `npre` E tiles do not depend on K1 -- issue them
-      // before waiting for K1 (PDL), so E streaming overlaps K1's tail.
-      const int npre = min(a.stages, c1 - c0);
-      for (int j = 0; j < npre; ++j) {
-        mbar_expect_tx(&efull[j], e_stage);
-        for (int b = 0; b < a.HW / 64; ++b)
-          tma_load_2d(e_sm + j * e_stage + b * kEBox, &map_e, &efull[j], hs * a.HW + b * 64, (c0 + j) * kKChunk,
-                      pol);
-      }
-      grid_dep_wait();  // K1's logits (flog) visible
-      for (int j = 0; j < npre; ++j)
-        tma_load_2d(e_sm + j * e_stage + e_bytes, &map_f, &efull[j], (c0 + j) * kKChunk, 0, pol_f);
-      int stage = npre % a.stages;
-      uint32_t phase = (npre == a.stages) ? 1u : 0u;
-      for (int c = c0 + npre; c < c1; ++c) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int c = c0; c < c1; ++c) {
         mbar_wait(&eempty[stage], phase ^ 1u);
         mbar_expect_tx(&efull[stage], e_stage);
         for (int b = 0; b < a.HW / 64; ++b)
           tma_load_2d(e_sm + stage * e_stage + b * kEBox, &map_e, &efull[stage], hs * a.HW + b * 64, c * kKChunk,
                       pol);
-        // logits chunk f[0:N, c*64 : c*64+64] (rows >= M and columns >= V_local zero-filled)
-        tma_load_2d(e_sm + stage * e_stage + e_bytes, &map_f, &efull[stage], c * kKChunk, 0, pol_f);
-        if (++stage == a.stages) {
-          stage = 0;
-          phase ^= 1u;
-        }
+        advance(stage, phase, a.stages);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 6) {
+    // ------------------------------------------------------------ TMA: logits chunks
+    if (lane == 0) {
+      grid_dep_wait();  // K1's logits (flog) visible
+      const uint64_t pol = policy_evict_last();  // re-read by the other hidden slices
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int c = c0; c < c1; ++c) {
+        mbar_wait(&fempty[stage], phase ^ 1u);
+        mbar_expect_tx(&ffull[stage], f_stage);
+        // f[0:N, c*64 : c*64+64]; rows >= M and columns >= V_local zero-filled
+        tma_load_2d(f_sm + stage * f_stage, &map_f, &ffull[stage], c * kKChunk, 0, pol);
+        advance(stage, phase, a.pstages);
       }
     }
     __syncwarp();
@@ -146,8 +163,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int es = 0, ps = 0;
       uint32_t eph = 0, pph = 0;
       for (int c = c0; c < c1; ++c) {
-        mbar_wait(&efull[es], eph);
         mbar_wait(&pfull[ps], pph);
+        mbar_wait(&efull[es], eph);
         tc_fence_after();
         const uint32_t e_addr = smem_u32(e_sm + es * e_stage);
         const uint32_t phi = smem_u32(p_sm + ps * 2 * p_half);
@@ -166,14 +183,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_commit(&eempty[es]);
         mma_commit(&pempty[ps]);
-        if (++es == a.stages) {
-          es = 0;
-          eph ^= 1u;
-        }
-        if (++ps == a.pstages) {
-          ps = 0;
-          pph ^= 1u;
-        }
+        advance(es, eph, a.stages);
+        advance(ps, pph, a.pstages);
       }
       mma_commit(accfull);
     }
@@ -184,16 +195,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     grid_dep_wait();  // K1's record (m per row) visible
     for (int s = tid; s < N; s += kEpiWarps * kWarpThreads) m_sm[s] = (s < a.M) ? a.rec[s * a.rec_stride] : 0.f;
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * kWarpThreads) : "memory");
-    int ps = 0, es = 0;
-    uint32_t pph = 0, eph = 0;
+    int ps = 0;
+    uint32_t pph = 0;
     for (int c = c0; c < c1; ++c) {
-      mbar_wait(&efull[es], eph);  // logits chunk landed (with the E tile)
-      const float* f_sm = reinterpret_cast<const float*>(e_sm + es * e_stage + e_bytes);
-      if (++es == a.stages) {
-        es = 0;
-        eph ^= 1u;
-      }
+      mbar_wait(&ffull[ps], pph);  // logits chunk landed
       mbar_wait(&pempty[ps], pph ^ 1u);
+      const float* fch = reinterpret_cast<const float*>(f_sm + ps * f_stage);
       uint8_t* phi = p_sm + ps * 2 * p_half;
       uint8_t* plo = phi + p_half;
       for (int u = tid; u < N * 8; u += kEpiWarps * kWarpThreads) {
@@ -201,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int v0 = c * kKChunk + cc * 8;
         float p[8];
         if (s < a.M && v0 < a.V_local) {
-          const float4* src = reinterpret_cast<const float4*>(f_sm + s * kKChunk + cc * 8);
+          const float4* src = reinterpret_cast<const float4*>(fch + s * kKChunk + cc * 8);
           const float4 q0 = src[0], q1 = src[1];
           const float ms = m_sm[s];
           p[0] = fexp(q0.x - ms); p[1] = fexp(q0.y - ms); p[2] = fexp(q0.z - ms); p[3] = fexp(q0.w - ms);
@@ -221,12 +228,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         *reinterpret_cast<uint4*>(phi + off) = hi;
         *reinterpret_cast<uint4*>(plo + off) = lo;
       }
-      fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05.mma
+      mbar_arrive(&fempty[ps]);  // logits chunk consumed
+      fence_proxy_async();       // generic-proxy smem writes -> visible to tcgen05.mma
       mbar_arrive(&pfull[ps]);
-      if (++ps == a.pstages) {
-        ps = 0;
-        pph ^= 1u;
-      }
+      advance(ps, pph, a.pstages);
     }
     // ------------------------------------------------------------ epilogue
     const int hbase = hs * a.HW;

@@ -244,39 +244,55 @@ __global__ void __launch_bounds__(kK3Threads) k3_select_commit(const K3Args a) {
   }
 }
 
-__global__ void __launch_bounds__(256) k4_smooth_finalize(const K4Args a) {
+// 256 threads = 32 float4 columns x 8 partial groups: each thread sums a
+// strided subset of the partials, the 8 groups are then combined in a fixed
+// order through shared memory (deterministic; ~nparts/8 loads in flight per
+// thread instead of nparts dependent rounds).
+constexpr int kK4Cols = 32, kK4Groups = 8;
+__global__ void __launch_bounds__(kK4Cols * kK4Groups) k4_smooth_finalize(const K4Args a) {
+  __shared__ float4 red[kK4Groups][kK4Cols];
   grid_dep_wait();  // K3's mask / (m, l) and K2's partials visible
   const int h4 = a.H / 4;
-  const long t = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= static_cast<long>(a.M) * h4) return;
-  const int s = static_cast<int>(t / h4);
-  const int h = static_cast<int>(t - static_cast<long>(s) * h4) * 4;
-  if (!a.mask[s]) return;  // only rows still masked get e_{t+1}
-  const float m = a.ml[2 * s], l = a.ml[2 * s + 1];
+  const int cl = threadIdx.x % kK4Cols, grp = threadIdx.x / kK4Cols;
+  const long t = static_cast<long>(blockIdx.x) * kK4Cols + cl;
+  const bool in = t < static_cast<long>(a.M) * h4;
+  const int s = in ? static_cast<int>(t / h4) : 0;
+  const int h = in ? static_cast<int>(t - static_cast<long>(s) * h4) * 4 : 0;
+  const bool active = in && a.mask[s] != 0;  // only rows still masked get e_{t+1}
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  const float* src = a.acc + static_cast<long>(s) * a.H + h;
-  constexpr int kBatch = 8;  // independent loads in flight per thread
-  for (int p0 = 0; p0 < a.nparts; p0 += kBatch) {
-    float4 v[kBatch];
-    float sc[kBatch];
+  if (active) {
+    const float m = a.ml[2 * s];
+    const float* src = a.acc + static_cast<long>(s) * a.H + h;
+    constexpr int kBatch = 8;
+    for (int p0 = grp; p0 < a.nparts; p0 += kBatch * kK4Groups) {
+      float4 v[kBatch];
+      float sc[kBatch];
 #pragma unroll
-    for (int j = 0; j < kBatch; ++j) {
-      const int p = p0 + j;
-      v[j] = (p < a.nparts) ? __ldcg(reinterpret_cast<const float4*>(src + p * a.acc_stride))
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-      sc[j] = (a.m_part == nullptr || p >= a.nparts)
-                  ? 1.f
-                  : expf(a.m_part[p * a.m_stride + static_cast<long>(s) * a.m_rowstride] - m);
-    }
+      for (int j = 0; j < kBatch; ++j) {
+        const int p = p0 + j * kK4Groups;
+        v[j] = (p < a.nparts) ? __ldcg(reinterpret_cast<const float4*>(src + p * a.acc_stride))
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+        sc[j] = (a.m_part == nullptr || p >= a.nparts)
+                    ? 1.f
+                    : expf(a.m_part[p * a.m_stride + static_cast<long>(s) * a.m_rowstride] - m);
+      }
 #pragma unroll
-    for (int j = 0; j < kBatch; ++j) {  // fixed summation order
-      acc.x = fmaf(v[j].x, sc[j], acc.x);
-      acc.y = fmaf(v[j].y, sc[j], acc.y);
-      acc.z = fmaf(v[j].z, sc[j], acc.z);
-      acc.w = fmaf(v[j].w, sc[j], acc.w);
+      for (int j = 0; j < kBatch; ++j) {  // fixed summation order
+        acc.x = fmaf(v[j].x, sc[j], acc.x);
+        acc.y = fmaf(v[j].y, sc[j], acc.y);
+        acc.z = fmaf(v[j].z, sc[j], acc.z);
+        acc.w = fmaf(v[j].w, sc[j], acc.w);
+      }
     }
   }
-  const float w = a.alpha_t / l;
+  red[grp][cl] = acc;
+  __syncthreads();
+  if (grp != 0 || !active) return;
+  for (int g = 1; g < kK4Groups; ++g) {
+    const float4 r = red[g][cl];
+    acc.x += r.x; acc.y += r.y; acc.z += r.z; acc.w += r.w;
+  }
+  const float w = a.alpha_t / a.ml[2 * s + 1];
   const uint2 em = *reinterpret_cast<const uint2*>(a.e_mask + h);
   const __nv_bfloat162 e01 = *reinterpret_cast<const __nv_bfloat162*>(&em.x);
   const __nv_bfloat162 e23 = *reinterpret_cast<const __nv_bfloat162*>(&em.y);
@@ -304,9 +320,8 @@ cudaError_t launch_k3(const K3Args& a, cudaStream_t st, bool pdl) {
 
 cudaError_t launch_k4(const K4Args& a, cudaStream_t st, bool pdl) {
   const long n = static_cast<long>(a.M) * (a.H / 4);
-  const int threads = 128;
-  const int blocks = static_cast<int>((n + threads - 1) / threads);
-  return launch_ex(k4_smooth_finalize, dim3(blocks), dim3(threads), 0, st, pdl, a);
+  const int blocks = static_cast<int>((n + kK4Cols - 1) / kK4Cols);
+  return launch_ex(k4_smooth_finalize, dim3(blocks), dim3(kK4Cols * kK4Groups), 0, st, pdl, a);
 }
 
 }  // namespace dinfer

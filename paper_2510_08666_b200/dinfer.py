@@ -25,7 +25,9 @@ STATUS = {0: "ok", 1: "ERR_ARG", 2: "ERR_SHAPE", 3: "ERR_CUDA", 4: "ERR_NCCL", 5
 
 class DInferError(RuntimeError):
     def __init__(self, status: int, what: str):
-        super().__init__(f"{what}: {STATUS.get(status, status)} ({lib().dinfer_strerror(status).decode()})")
+        detail = lib().dinfer_last_error().decode() if status in (3, 4) else ""
+        super().__init__(f"{what}: {STATUS.get(status, status)} ({lib().dinfer_strerror(status).decode()})"
+                         + (f" [{detail}]" if detail else ""))
         self.status = status
 
 
@@ -73,6 +75,7 @@ def lib():
         "dinfer_tau_schedule": (c_float, [c_float, S, S]),
         "dinfer_sync": (S, [P]),
         "dinfer_strerror": (ctypes.c_char_p, [S]),
+        "dinfer_last_error": (ctypes.c_char_p, []),
         "dinfer_set_timing": (S, [P, S]),
         "dinfer_get_timing": (S, [P, POINTER(c_float), S]),
         "dinfer_launches_per_step": (S, [P, POINTER(Params)]),

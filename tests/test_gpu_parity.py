@@ -90,6 +90,13 @@ def test_k2_slice_widths(torch_cuda, monkeypatch, hw):
     run_trajectory(torch_cuda, 4096, 1024, 1, 32, 32, 8, hier_credit_smooth, True, max_iters=4)
 
 
+@pytest.mark.parametrize("hres", ["0", "1"])
+def test_k1_hidden_resident_or_streamed(torch_cuda, monkeypatch, hres):
+    """K1 with the hidden block resident in smem or streamed with every W stage."""
+    monkeypatch.setenv("DINFER_K1_HRES", hres)
+    run_trajectory(torch_cuda, 3000, 512, 2, 32, 32, 10, hier_credit_smooth, True, max_iters=4)
+
+
 def test_without_pdl(torch_cuda, monkeypatch):
     monkeypatch.setenv("DINFER_PDL", "0")
     run_trajectory(torch_cuda, 2048, 512, 2, 32, 32, 9, hier_credit_smooth, True, max_iters=4)
