@@ -198,6 +198,13 @@ dinfer_status dinfer_set_timing(dinfer_ctx* ctx, int32_t enable);
 dinfer_status dinfer_get_timing(dinfer_ctx* ctx, float* ms, int32_t n);
 int32_t dinfer_launches_per_step(const dinfer_ctx* ctx, const dinfer_params* params);
 
+/* Per-CTA kernel timelines (diagnostics).  Only when the process sets
+ * DINFER_TRACE=1 before dinfer_create: K1 then K2 CTAs, 4 %globaltimer
+ * nanosecond stamps each (start, first operand stage ready, main loop done,
+ * exit) of the most recent step.  Returns the number of words (out == NULL:
+ * the number available), 0 if tracing is off.                               */
+int32_t dinfer_get_trace(dinfer_ctx* ctx, uint64_t* out, int32_t n);
+
 /* Geometry actually chosen (for reports): grid sizes and pipeline depth.    */
 typedef struct {
   int32_t k1_grid, k1_stages, k1_h_resident, k1_smem;

@@ -54,6 +54,12 @@ DI void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+DI uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // ---------------------------------------------------------------- PDL
 // Programmatic dependent launch: a kernel launched with programmatic stream
 // serialization may start (prologue, barrier init, TMEM alloc, independent

@@ -53,6 +53,7 @@ struct dinfer_ctx {
   float* flog = nullptr;
   float* part2 = nullptr;
   float* ml = nullptr;
+  unsigned long long* trace = nullptr;  // DINFER_TRACE=1: [K1 grid + K2 grid][4] globaltimer ns
   size_t stats_words = 0, full_words = 0;
   // staging for dinfer_step_host (device)
   uint16_t* st_hidden = nullptr;
@@ -219,6 +220,7 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
   a.rec = rec;
   a.flog = smooth ? c->flog : nullptr;
   a.err = c->err;
+  a.trace = c->trace;
   ev_begin(c, kPK1);
   DI_CUDA(launch_k1(c->map_w, c->map_w8, c->map_h, a, c->k1_grid, c->k1_smem, c->stream, c->pdl));
   ev_finish(c, kPK1);
@@ -239,6 +241,7 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
     b.rec = rec;
     b.rec_stride = kStatWords + c->shp.K;
     b.part = c->part2;
+    b.trace = c->trace == nullptr ? nullptr : c->trace + 4 * c->k1_grid;
     ev_begin(c, kPK2);
     DI_CUDA(launch_k2(c->map_e, c->map_f, b, c->k2_smem, c->stream, c->pdl));
     ev_finish(c, kPK2);
@@ -379,7 +382,7 @@ void dinfer_destroy(dinfer_ctx* c) {
 #ifdef DINFER_WITH_NCCL
   if (c->has_comm) ncclCommDestroy(c->comm);
 #endif
-  void* bufs[] = {c->part1, c->counter, c->err, c->rec_local, c->flog, c->part2, c->ml,
+  void* bufs[] = {c->part1, c->counter, c->err, c->rec_local, c->flog, c->part2, c->ml, c->trace,
                   c->st_hidden, c->st_mask, c->st_tokens, c->st_cids, c->st_cval, c->st_committed,
                   c->st_smoothed, c->st_stats};
   for (void* b : bufs)
@@ -483,6 +486,8 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
     A(dev_alloc(&c->flog, static_cast<size_t>(M) * s.V_local));
     A(dev_alloc(&c->part2, static_cast<size_t>(c->k2_VG) * M * s.H));
   }
+  if (std::getenv("DINFER_TRACE") != nullptr && std::atoi(std::getenv("DINFER_TRACE")) != 0)
+    A(dev_alloc(&c->trace, static_cast<size_t>(4) * (c->k1_grid + c->k2_HS * c->k2_VG)));
   if (st == DINFER_OK) {
     if (cudaMemset(c->counter, 0, 16) != cudaSuccess || cudaMemset(c->err, 0, 16) != cudaSuccess ||
         cudaMemset(c->rec_local, 0, c->full_words * 4) != cudaSuccess)
@@ -676,6 +681,16 @@ dinfer_status dinfer_get_timing(dinfer_ctx* c, float* ms, int32_t n) {
     }
   }
   return DINFER_OK;
+}
+
+int32_t dinfer_get_trace(dinfer_ctx* c, uint64_t* out, int32_t n) {
+  if (c == nullptr || c->trace == nullptr) return 0;
+  const int total = 4 * (c->k1_grid + c->k2_HS * c->k2_VG);
+  if (out == nullptr) return total;
+  cudaStreamSynchronize(c->stream);
+  const int k = n < total ? n : total;
+  if (cudaMemcpy(out, c->trace, static_cast<size_t>(k) * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  return k;
 }
 
 int32_t dinfer_launches_per_step(const dinfer_ctx* c, const dinfer_params* p) {

@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int ntiles = (r1 - r0 + kTileRows - 1) / kTileRows;
   const uint32_t tmem_cols = tmem_cols_pow2(2u * N);
 
+  if (a.trace != nullptr && threadIdx.x == 0) a.trace[blockIdx.x * 4 + 0] = globaltimer_ns();
   if (warp == 4 && lane == 0) {
     prefetch_tmap(&map_w);
     prefetch_tmap(&map_w8);
@@ -211,6 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kc0 = 0; kc0 < a.num_kc; kc0 += kChunksPerStage) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
+          if (a.trace != nullptr && t == 0 && kc0 == 0) a.trace[blockIdx.x * 4 + 1] = globaltimer_ns();
 #pragma unroll
           for (int j = 0; j < kChunksPerStage; ++j) {
             const int kc = kc0 + j;
@@ -322,6 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&tempty[buf]);
     }
+    if (a.trace != nullptr && threadIdx.x == 0) a.trace[blockIdx.x * 4 + 2] = globaltimer_ns();
     // cross-warp merge (fixed warp order)
 #pragma unroll
     for (int g = 0; g < kMaxGroups; ++g) {
@@ -404,6 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 5) tmem_dealloc(tmem_base, tmem_cols);
+  if (a.trace != nullptr && threadIdx.x == 0) a.trace[blockIdx.x * 4 + 3] = globaltimer_ns();
 }
 
 }  // namespace

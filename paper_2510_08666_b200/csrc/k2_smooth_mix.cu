@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int c1 = static_cast<int>(static_cast<long>(vg + 1) * a.nchunks / a.VG);
   const uint32_t tmem_cols = tmem_cols_pow2(static_cast<uint32_t>(a.nsub * N));
 
+  if (a.trace != nullptr && threadIdx.x == 0) a.trace[blockIdx.x * 4 + 0] = globaltimer_ns();
   if (warp == 4 && lane == 0) {
     prefetch_tmap(&map_e);
     prefetch_tmap(&map_f);
@@ -166,6 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&pfull[ps], pph);
         mbar_wait(&efull[es], eph);
         tc_fence_after();
+        if (a.trace != nullptr && c == c0) a.trace[blockIdx.x * 4 + 1] = globaltimer_ns();
         const uint32_t e_addr = smem_u32(e_sm + es * e_stage);
         const uint32_t phi = smem_u32(p_sm + ps * 2 * p_half);
         const uint32_t plo = phi + p_half;
@@ -187,6 +189,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         advance(ps, pph, a.pstages);
       }
       mma_commit(accfull);
+      if (a.trace != nullptr) {
+        mbar_wait(accfull, 0);
+        a.trace[blockIdx.x * 4 + 2] = globaltimer_ns();
+      }
     }
     __syncwarp();
   } else {
@@ -261,6 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 5) tmem_dealloc(tmem_base, tmem_cols);
+  if (a.trace != nullptr && threadIdx.x == 0) a.trace[blockIdx.x * 4 + 3] = globaltimer_ns();
 }
 
 __global__ void acc_reduce_kernel(const float* __restrict__ part, int VG, int MH, float* __restrict__ out) {

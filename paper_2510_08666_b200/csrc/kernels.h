@@ -49,6 +49,7 @@ struct K1Args {
   float* rec;              // [M][4+K] rank record (stats part)
   float* flog;             // [M][V_local] raw logits for K2, or nullptr
   int* err;
+  unsigned long long* trace;  // optional [grid][4] globaltimer ns: start, first W stage, last tile done, exit
 };
 size_t k1_smem_bytes(int N, int H, int stages, int h_resident, int slab_rows_max);
 cudaError_t launch_k1(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
@@ -65,6 +66,7 @@ struct K2Args {
   const float* rec;        // rank record: m at rec[s*rec_stride]
   int rec_stride;
   float* part;             // [VG][M][H]
+  unsigned long long* trace;  // optional [grid][4] globaltimer ns: start, first E stage, MMAs done, exit
 };
 size_t k2_smem_bytes(int N, int HW, int stages, int pstages);
 cudaError_t launch_k2(const CUtensorMap& map_e, const CUtensorMap& map_f, const K2Args& a, size_t smem,

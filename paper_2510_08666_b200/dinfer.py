@@ -80,6 +80,7 @@ def lib():
         "dinfer_get_timing": (S, [P, POINTER(c_float), S]),
         "dinfer_launches_per_step": (S, [P, POINTER(Params)]),
         "dinfer_get_geometry": (S, [P, POINTER(Geometry)]),
+        "dinfer_get_trace": (S, [P, P, S]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -199,6 +200,19 @@ class Context:
 
     def launches_per_step(self, params: Params) -> int:
         return int(lib().dinfer_launches_per_step(self._h, ctypes.byref(params)))
+
+    def trace(self):
+        """Per-CTA globaltimer stamps of the last step (DINFER_TRACE=1), as
+        (k1 [grid,4], k2 [grid,4]) numpy arrays in ns, or None."""
+        import numpy as np
+        n = int(lib().dinfer_get_trace(self._h, None, 0))
+        if n == 0:
+            return None
+        buf = np.zeros(n, dtype=np.uint64)
+        lib().dinfer_get_trace(self._h, c_void_p(buf.ctypes.data), n)
+        g = self.geometry()
+        k1 = buf[:4 * g["k1_grid"]].reshape(-1, 4)
+        return k1, buf[4 * g["k1_grid"]:].reshape(-1, 4)
 
     def geometry(self) -> dict:
         g = Geometry()

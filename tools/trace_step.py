@@ -1,0 +1,57 @@
+"""Per-CTA timelines of K1 and K2 for one MoE step (DINFER_TRACE=1).
+  python tools/trace_step.py [--config moe|8b]"""
+import os
+import sys
+
+os.environ["DINFER_TRACE"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2510_08666_b200 import Context, make_params, synth  # noqa: E402
+
+H, V = (4096, 126464) if "8b" in sys.argv else (2048, 157184)
+smooth = "8b" not in sys.argv
+B, S, K = 1, 32, 32
+dev = lambda u: torch.from_numpy(np.ascontiguousarray(u).view(np.int16)).view(torch.bfloat16).cuda()
+W = synth.make_W(V, H, 1)
+h = dev(synth.planted_hidden(W, B * S, seed=0))
+Wd = dev(W)
+del W
+Ed = dev(synth.make_E(V, H, 2)) if smooth else None
+em = dev(synth.make_E(V, H, 2, rows=(V - 1, V))[0]) if smooth else None
+ctx = Context(B, S, H, K, V, smooth_capable=smooth)
+p = make_params(decoder="hierarchical", use_credit=True, use_smooth=smooth)
+mask = torch.ones((B, S), dtype=torch.uint8, device="cuda")
+tok = torch.full((B, S), V - 1, dtype=torch.int32, device="cuda")
+cids = torch.full((B, S, K), -1, dtype=torch.int32, device="cuda")
+cval = torch.zeros((B, S, K), dtype=torch.float32, device="cuda")
+com = torch.zeros((B, S), dtype=torch.uint8, device="cuda")
+sm = torch.zeros((B, S, H), dtype=torch.float32, device="cuda") if smooth else None
+st = torch.zeros((B, S, 4), dtype=torch.float32, device="cuda")
+flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+for it in range(4):
+    flush.fill_(1.0)
+    mask.fill_(1)
+    cids.fill_(-1)
+    ctx.step(h, Wd, Ed, em, mask, tok, cids, cval, p, com, sm, st)
+    torch.cuda.synchronize()
+k1, k2 = ctx.trace()
+t0 = int(k1[:, 0].min())
+us = lambda a: (a.astype(np.int64) - t0) / 1e3
+
+
+def row(name, a):
+    a = us(a)
+    print(f"  {name:22s} min {a.min():7.1f}  p10 {np.percentile(a, 10):7.1f}  med {np.median(a):7.1f}  "
+          f"p90 {np.percentile(a, 90):7.1f}  max {a.max():7.1f} us")
+
+
+print("K1 (148 CTAs), us from first K1 CTA start:")
+for i, n in enumerate(["start", "first W stage", "last tile done", "exit"]):
+    row(n, k1[:, i])
+if smooth:
+    print("K2:")
+    for i, n in enumerate(["start", "first MMA (E+P)", "MMAs done", "exit"]):
+        row(n, k2[:, i])
+    print(f"  step span: {us(k2[:, 3]).max():.1f} us (K1 start -> last K2 CTA exit)")
