@@ -35,8 +35,28 @@ sys.path.insert(0, ROOT)
 
 METRIC = "denoise-step positions/sec and HBM GB/s fraction, LLaDA-MoE shape bs1, 1/2/4/8 B200"
 UNIT = "positions/s"
-B, S, H, V, K = 1, 32, 2048, 157184, 32
-WORKLOAD = "LLaDA-MoE shape bs1 block32 hierarchical+credit+smoothing (BASELINE configs[2]; vocab-sharded configs[3] for N>1)"
+# BASELINE.json configs.  The default (the metric's workload) is "moe".
+CONFIGS = {
+    "moe": dict(B=1, S=32, H=2048, V=157184, K=32, decoder="hierarchical", credit=True, smooth=True,
+                workload="LLaDA-MoE shape bs1 block32 hierarchical+credit+smoothing (BASELINE configs[2]; "
+                         "vocab-sharded configs[3] for N>1)"),
+    "8b": dict(B=1, S=32, H=4096, V=126464, K=32, decoder="threshold", credit=False, smooth=False,
+               workload="LLaDA-8B shape bs1 block32 threshold decoding (BASELINE configs[1])"),
+    "8b-bs64": dict(B=64, S=64, H=4096, V=126464, K=8, decoder="threshold", credit=False, smooth=False,
+                    workload="LLaDA-8B shape bs64 block64 threshold decoding, compute-bound (BASELINE configs[4])"),
+    "tiny": dict(B=1, S=32, H=256, V=1024, K=32, decoder="threshold", credit=False, smooth=False,
+                 workload="tiny synthetic block32 hidden256 vocab1024 threshold 0.9 (BASELINE configs[0])"),
+}
+B = S = H = V = K = None
+CFG = None
+WORKLOAD = None
+
+
+def set_config(name):
+    global B, S, H, V, K, CFG, WORKLOAD
+    CFG = CONFIGS[name]
+    B, S, H, V, K = CFG["B"], CFG["S"], CFG["H"], CFG["V"], CFG["K"]
+    WORKLOAD = CFG["workload"]
 
 
 def peaks():
@@ -46,6 +66,14 @@ def peaks():
         return float(d["hbm_gbs"]), float(d.get("bf16_tflops", 1590.0)), "measured"
     except Exception:
         return 6650.0, 1590.0, "fallback"
+
+
+def peaks_sustained():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["bf16_tflops_sustained"])
+    except Exception:
+        return 1400.0
 
 
 def ncu_traffic():
@@ -113,17 +141,20 @@ def oracle_run(n_steps: int, n_warm: int, rows: int, budget_s: float | None = No
     per step.  Returns (seconds per step list, cores)."""
     import oracle as O
     from paper_2510_08666_b200 import synth
-    W = O.bf16_bits_to_f64(synth.make_W(V, H, 1))
-    E = O.bf16_bits_to_f64(synth.make_E(V, H, 2))
-    h = O.bf16_bits_to_f64(synth.planted_hidden(synth.make_W(V, H, 1), S, seed=0))[:rows].reshape(1, rows, H)
-    em = E[synth.mask_id(V)]
-    p = O.Params(decoder=O.DEC_HIERARCHICAL, theta_hi=0.92, theta_lo=0.62, use_credit=True, use_smooth=True,
+    W_u16 = synth.make_W(V, H, 1)
+    W = O.bf16_bits_to_f64(W_u16)
+    E = O.bf16_bits_to_f64(synth.make_E(V, H, 2)) if CFG["smooth"] else W[:1]
+    h = O.bf16_bits_to_f64(synth.planted_hidden(W_u16, S, seed=0))[:rows].reshape(1, rows, H)
+    del W_u16
+    em = E[synth.mask_id(V)] if CFG["smooth"] else None
+    p = O.Params(decoder=O.DEC_HIERARCHICAL if CFG["decoder"] == "hierarchical" else O.DEC_THRESHOLD,
+                 tau=0.9, theta_hi=0.92, theta_lo=0.62, use_credit=CFG["credit"], use_smooth=CFG["smooth"],
                  alpha_t=0.1)
     times = []
     for i in range(n_warm + n_steps):
         mask = np.ones((1, rows), bool)
         tok = np.full((1, rows), V - 1)
-        C = np.zeros((1, rows, V))
+        C = np.zeros((1, rows, V)) if CFG["credit"] else None
         t0 = time.perf_counter()
         O.step(h, W, E, em, mask, tok, C, p)
         dt = time.perf_counter() - t0
@@ -151,11 +182,12 @@ def reference_arm(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "B": B, "S": S, "H": H, "V": V, "K": K, "decoder": "hierarchical",
-                   "credit": True, "smooth": True, "parallelism": "host cores (numpy fp64 oracle)"},
+        "config": {"workload": WORKLOAD, "name": args.config, "B": B, "S": S, "H": H, "V": V, "K": K,
+                   "decoder": CFG["decoder"], "credit": CFG["credit"], "smooth": CFG["smooth"],
+                   "parallelism": "host cores (numpy fp64 oracle)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"{rows} of {S} positions per step, full vocab {V}, fp64 numpy oracle step "
-                                   f"(logits, stats, dense credit, hierarchical, smoothing)"},
+                         "sample": f"{rows} of {B * S} positions per step, full vocab {V}, fp64 numpy oracle step "
+                                   f"({CFG['decoder']}, credit={CFG['credit']}, smoothing={CFG['smooth']})"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -185,18 +217,19 @@ def gpu_arm(args):
     # ---- synthetic inputs: this rank's vocab shard of W and E
     v0, v1 = synth.shard_range(V, rank, world)
     Vl = v1 - v0
+    smooth, credit = CFG["smooth"], CFG["credit"]
     W_u16 = synth.make_W(V, H, 1, rows=(v0, v1))
-    E_u16 = synth.make_E(V, H, 2, rows=(v0, v1))
-    em_u16 = synth.make_E(V, H, 2, rows=(V - 1, V))[0]
-    Wfull_rows = synth.make_W(V, H, 1)  # planted hidden needs W[target] rows (same on every rank)
+    Wfull_rows = synth.make_W(V, H, 1) if world > 1 else W_u16  # planted hidden needs W[target] rows
     hid_u16 = synth.planted_hidden(Wfull_rows, B * S, seed=0)
     del Wfull_rows
 
     def dev_bf16(u):
         return torch.from_numpy(np.ascontiguousarray(u).view(np.int16)).view(torch.bfloat16).cuda()
 
-    Wd, Ed, emd, hid = dev_bf16(W_u16), dev_bf16(E_u16), dev_bf16(em_u16), dev_bf16(hid_u16)
-    del W_u16, E_u16
+    Wd, hid = dev_bf16(W_u16), dev_bf16(hid_u16)
+    Ed = dev_bf16(synth.make_E(V, H, 2, rows=(v0, v1))) if smooth else None
+    emd = dev_bf16(synth.make_E(V, H, 2, rows=(V - 1, V))[0]) if smooth else None
+    del W_u16
 
     stream = torch.cuda.Stream()
     nid = None
@@ -204,9 +237,9 @@ def gpu_arm(args):
         from paper_2510_08666_b200.dist import broadcast_unique_id
         nid = broadcast_unique_id("cuda")
     ctx = Context(B, S, H, K, V, V_local=Vl, v_offset=v0, world=world, rank=rank, stream=stream.cuda_stream,
-                  nccl_id=nid)
-    p = make_params(decoder="hierarchical", theta_hi=0.92, theta_lo=0.62, use_credit=True, use_smooth=True,
-                    alpha_t=0.1)
+                  nccl_id=nid, smooth_capable=smooth)
+    p = make_params(decoder=CFG["decoder"], tau=0.9, theta_hi=0.92, theta_lo=0.62, use_credit=credit,
+                    use_smooth=smooth, alpha_t=0.1)
 
     dev = "cuda"
     M = B * S
@@ -215,7 +248,7 @@ def gpu_arm(args):
     cids = torch.full((B, S, K), -1, dtype=torch.int32, device=dev)
     cval = torch.zeros((B, S, K), dtype=torch.float32, device=dev)
     committed = torch.zeros((B, S), dtype=torch.uint8, device=dev)
-    smoothed = torch.zeros((B, S, H), dtype=torch.float32, device=dev)
+    smoothed = torch.zeros((B, S, H), dtype=torch.float32, device=dev) if smooth else None
     stats = torch.zeros((B, S, 4), dtype=torch.float32, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
@@ -228,7 +261,8 @@ def gpu_arm(args):
             cval.zero_()
 
     def one_step():
-        ctx.step(hid, Wd, Ed, emd, mask, tokens, cids, cval, p, committed, smoothed, stats)
+        ctx.step(hid, Wd, Ed, emd, mask, tokens, cids if credit else None, cval if credit else None, p, committed,
+                 smoothed, stats)
 
     # warm-up
     for _ in range(args.warmup):
@@ -287,10 +321,10 @@ def gpu_arm(args):
     hid_h = pin(hid_u16.view(np.int16))
     mask_h, tok_h = pin(np.ones((B, S), np.uint8)), pin(np.full((B, S), V - 1, np.int32))
     cids_h, cval_h = pin(np.full((B, S, K), -1, np.int32)), pin(np.zeros((B, S, K), np.float32))
-    com_h, sm_h, st_h = pin(np.zeros((B, S), np.uint8)), pin(np.zeros((B, S, H), np.float32)), \
-        pin(np.zeros((B, S, 4), np.float32))
-    h2d = M * H * 2 + M + 4 * M + 8 * M * K
-    d2h = M + 4 * M + M + 8 * M * K + 4 * M * H + 16 * M
+    com_h, st_h = pin(np.zeros((B, S), np.uint8)), pin(np.zeros((B, S, 4), np.float32))
+    sm_h = pin(np.zeros((B, S, H), np.float32)) if smooth else None
+    h2d = M * H * 2 + M + 4 * M + (8 * M * K if credit else 0)
+    d2h = M + 4 * M + M + (8 * M * K if credit else 0) + (4 * M * H if smooth else 0) + 16 * M
     e2e_steps = max(3, min(args.steps, 50))
     e2e_ms = []
     for i in range(args.warmup + e2e_steps):
@@ -299,7 +333,8 @@ def gpu_arm(args):
             flush.fill_(1.0)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        ctx.step_host(hid_h, Wd, Ed, emd, mask_h, tok_h, cids_h, cval_h, p, com_h, sm_h, st_h)
+        ctx.step_host(hid_h, Wd, Ed, emd, mask_h, tok_h, cids_h if credit else None, cval_h if credit else None, p,
+                      com_h, sm_h, st_h)
         e1.record(stream)
         e1.synchronize()
         if i >= args.warmup:
@@ -313,38 +348,49 @@ def gpu_arm(args):
     geom = ctx.geometry()
 
     if rank == 0:
-        hbm, _, peak_kind = peaks()
+        hbm, tflops, peak_kind = peaks()
+        tflops_sus = peaks_sustained()
         k1_bytes = Vl * H * 2 + M * H * 2
-        k2_bytes = Vl * H * 2 + M * H * 4
+        k2_bytes = (Vl * H * 2 + M * H * 4) if smooth else 0
         k1_ms, k2_ms = phases.get("k1_vocab_proj", 0.0), phases.get("k2_smooth_mix", 0.0)
         dom, dom_bytes, dom_ms = ("k1_vocab_proj", k1_bytes, k1_ms) if k1_ms >= k2_ms else \
             ("k2_smooth_mix", k2_bytes, k2_ms)
-        achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
-        traffic = ncu_traffic().get(dom)
+        traffic = ncu_traffic().get(dom if M <= 256 else "k1b_vocab_proj_dense")
         step_bytes = k1_bytes + k2_bytes
+        if M > 256:  # compute-bound regime (BASELINE configs[4]): tensor roofline of K1b
+            flops = 2.0 * M * H * Vl
+            achieved = flops / (dom_ms * 1e-3) / 1e12
+            roof = {"bound": "tensor", "kernel": "k1b_vocab_proj_dense", "achieved": achieved, "peak": tflops_sus,
+                    "unit": "TFLOP/s", "frac": achieved / tflops_sus, "traffic": traffic, "peak_kind":
+                    peak_kind + " sustained (kernel timed inside a ms-long step)", "burst_peak": tflops,
+                    "algorithmic_flops_per_launch": flops, "ms_per_launch": dom_ms}
+        else:
+            achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+            roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                    "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
+                    "algorithmic_bytes_per_launch": dom_bytes, "ms_per_launch": dom_ms}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             rows = 8
             times, cores = oracle_run(100, 1, rows, budget_s=args.cpu_budget)
             sec = sum(times) / len(times)
             cpu = {"value": rows / sec, "unit": UNIT, "cores": cores, "kind": "oracle",
-                   "sample": f"{len(times)} oracle steps of {rows} of {S} positions (full vocab {V}, fp64 numpy; "
+                   "sample": f"{len(times)} oracle steps of {rows} of {B * S} positions (full vocab {V}, fp64 numpy; "
                              f"{sum(times):.1f} s of CPU work)"}
         line = {
             "metric": METRIC, "value": M / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "B": B, "S": S, "H": H, "V": V, "K": K, "decoder": "hierarchical",
-                       "credit": True, "smooth": True, "vocab_shards": world, "V_local": Vl,
+            "config": {"workload": WORKLOAD, "name": args.config, "B": B, "S": S, "H": H, "V": V, "K": K,
+                       "decoder": CFG["decoder"], "credit": credit, "smooth": smooth, "vocab_shards": world,
+                       "V_local": Vl,
                        "parallelism": f"vocab-sharded x{world} (NCCL allgather)" if world > 1 else "single GPU",
                        "l2": "flushed (256 MiB write) before every timed step; inputs > L2"},
             "e2e": {"value": M / (e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e, "api": "dinfer_step_host"},
             "gpu_launches": launches * args.steps,
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
-                         "algorithmic_bytes_per_launch": dom_bytes, "ms_per_launch": dom_ms},
-            "step_roofline": {"bytes": step_bytes, "achieved_gbs": step_bytes / (ms * 1e-3) / 1e9,
+            "roofline": roof,
+            "step_roofline": None if M > 256 else {"bytes": step_bytes, "achieved_gbs": step_bytes / (ms * 1e-3) / 1e9,
                               "frac": step_bytes / (ms * 1e-3) / 1e9 / hbm},
             "phases_ms": phases,
             "ms_per_step_with_kernel_events": ms_b,
@@ -370,7 +416,9 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--config", default="moe", choices=sorted(CONFIGS))
     args = ap.parse_args()
+    set_config(args.config)
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

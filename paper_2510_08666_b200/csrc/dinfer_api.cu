@@ -41,6 +41,9 @@ struct dinfer_ctx {
 #endif
   // geometry
   int k1_grid = 0, k1_stages = 0, k1_hres = 0, slab_rows_max = 0;
+  bool dense = false;  // M > 256: compute-bound K1b path (no smoothing / credit)
+  int kb_grid = 0, kb_stages = 0, kb_VG = 0;
+  size_t kb_smem = 0;
   size_t k1_smem = 0;
   int k2_HW = 0, k2_HS = 0, k2_VG = 0, k2_stages = 0, k2_pstages = 0, k2_nchunks = 0;
   size_t k2_smem = 0;
@@ -259,7 +262,7 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
 dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, int world, bool acc_from_part2,
                           const uint16_t* e_mask, uint8_t* mask, int32_t* tokens, int32_t* credit_ids,
                           float* credit_val, const dinfer_params* p, uint8_t* committed, float* smoothed,
-                          float* stats) {
+                          float* stats, int rec_stride = -1) {
   K3Args k{};
   k.B = c->shp.B;
   k.S = c->shp.S;
@@ -267,7 +270,7 @@ dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, in
   k.world = world;
   k.recs = recs;
   k.rec_words = static_cast<long>(rec_words);
-  k.rec_stride = kStatWords + c->shp.K;
+  k.rec_stride = rec_stride > 0 ? rec_stride : kStatWords + c->shp.K;
   k.mask = mask;
   k.tokens = tokens;
   k.credit_ids = credit_ids;
@@ -402,7 +405,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
   const dinfer_shape& s = *shape;
   if (s.B < 1 || s.S < 1 || s.S > 1024 || s.K < 1 || s.H < 128) return DINFER_ERR_SHAPE;
   const long M = static_cast<long>(s.B) * s.S;
-  if (M > 256) return DINFER_ERR_UNSUPPORTED;  // HBM-bound swap-AB path only
+  if (M > 256 && (s.smooth_capable || M > (1L << 20))) return DINFER_ERR_UNSUPPORTED;  // dense path: stats only
   if (s.H % 128 != 0 || s.H > 16384) return DINFER_ERR_SHAPE;
   if (s.world < 1 || s.world > 8 || s.rank < 0 || s.rank >= s.world) return DINFER_ERR_SHAPE;
   if (s.V_local < 8 || s.V_local % 8 != 0 || s.V_local * s.world != s.V_total) return DINFER_ERR_SHAPE;
@@ -425,57 +428,72 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
   cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, c->dev);
   if (cc_major != 10) { delete c; return DINFER_ERR_UNSUPPORTED; }  // sm_100a only
 
-  // ---- K1 geometry: one CTA per SM over equal 8-row-granular vocab slabs
-  const long g8 = s.V_local / kRowGran;
-  c->k1_grid = static_cast<int>(std::min<long>(c->num_sms, std::max<long>(1, (s.V_local + kTileRows - 1) / kTileRows)));
-  c->slab_rows_max = static_cast<int>(kRowGran * ((g8 + c->k1_grid - 1) / c->k1_grid));
-  // Hidden block resident in smem (loaded once) or streamed from L2 with every
-  // W stage.  Residency only pays if it still leaves >= 4 W stages: at MoE
-  // shape it leaves 2 (measured 144 us) against 5 streamed stages (134 us).
-  int st_res = 0, st_str = 0;
-  if (static_cast<long>(c->N) * s.H * 2 <= 160 * 1024)
-    for (int st = 8; st >= 2 && st_res == 0; --st)
-      if (k1_smem_bytes(c->N, s.H, st, 1, c->slab_rows_max) <= c->smem_optin) st_res = st;
-  for (int st = 8; st >= 2 && st_str == 0; --st)
-    if (k1_smem_bytes(c->N, s.H, st, 0, c->slab_rows_max) <= c->smem_optin) st_str = st;
-  bool use_res = st_res >= 4 || (st_res > 0 && st_str == 0);
-  if (const char* e = std::getenv("DINFER_K1_HRES")) use_res = (std::atoi(e) != 0 && st_res > 0) || st_str == 0;
-  c->k1_hres = use_res ? 1 : 0;
-  c->k1_stages = use_res ? st_res : st_str;
-  if (c->k1_stages == 0) { delete c; return DINFER_ERR_UNSUPPORTED; }
-  c->k1_smem = k1_smem_bytes(c->N, s.H, c->k1_stages, c->k1_hres, c->slab_rows_max);
-
-  // ---- K2 geometry: hidden slices x vocab groups <= #SMs.  Prefer the widest
-  // hidden slice that divides H (512 columns: 1 KB contiguous E row segments,
-  // 4 x 37 = 148 CTAs at H = 2048; measured 131 us vs 165 us with 256), then
-  // the deepest E ring (>= 2 stages) with logits/P rings of >= 2 stages.
-  c->k2_nchunks = static_cast<int>((s.V_local + kKChunk - 1) / kKChunk);
-  int hw_pref = 512;
-  if (const char* e = std::getenv("DINFER_K2_HW")) hw_pref = std::atoi(e);  // tuning override: 128 / 256 / 512
-  c->k2_stages = 0;
-  for (int hw = 512; hw >= 128 && c->k2_stages == 0; hw /= 2) {
-    if (hw > hw_pref || s.H % hw != 0) continue;
-    for (int pst = 4; pst >= 1 && c->k2_stages == 0; --pst)  // depth 1 only for very large M
-      for (int st = 6; st >= 2; --st)
-        if (k2_smem_bytes(c->N, hw, st, pst) <= c->smem_optin) {
-          c->k2_HW = hw;
-          c->k2_pstages = pst;
-          c->k2_stages = st;
-          break;
-        }
+  if (M > 256) {
+    // ---- K1b geometry (compute-bound): units = 256-position blocks x vocab
+    // groups, one wave of persistent CTAs
+    c->dense = true;
+    if (s.world != 1) { delete c; return DINFER_ERR_UNSUPPORTED; }
+    const int nmb = static_cast<int>((M + 255) / 256);
+    const int nblocks = static_cast<int>((s.V_local + 255) / 256);
+    c->kb_VG = std::max(1, std::min(std::min(c->num_sms / nmb, nblocks), 32));
+    c->kb_grid = std::min(c->num_sms, nmb * c->kb_VG);
+    for (int st = 4; st >= 2 && c->kb_stages == 0; --st)
+      if (k1b_smem_bytes(st) <= c->smem_optin) c->kb_stages = st;
+    c->kb_smem = k1b_smem_bytes(c->kb_stages);
   }
-  if (c->k2_stages == 0) { delete c; return DINFER_ERR_UNSUPPORTED; }
-  c->k2_HS = s.H / c->k2_HW;
-  c->k2_VG = std::max(1, std::min(c->num_sms / std::max(1, c->k2_HS), c->k2_nchunks));
-  c->k2_smem = k2_smem_bytes(c->N, c->k2_HW, c->k2_stages, c->k2_pstages);
-  if (const char* e = std::getenv("DINFER_PDL")) c->pdl = std::atoi(e) != 0;
+  if (!c->dense) {
+    // ---- K1 geometry: one CTA per SM over equal 8-row-granular vocab slabs
+    const long g8 = s.V_local / kRowGran;
+    c->k1_grid = static_cast<int>(std::min<long>(c->num_sms, std::max<long>(1, (s.V_local + kTileRows - 1) / kTileRows)));
+    c->slab_rows_max = static_cast<int>(kRowGran * ((g8 + c->k1_grid - 1) / c->k1_grid));
+    // Hidden block resident in smem (loaded once) or streamed from L2 with every
+    // W stage.  Residency only pays if it still leaves >= 4 W stages: at MoE
+    // shape it leaves 2 (measured 144 us) against 5 streamed stages (134 us).
+    int st_res = 0, st_str = 0;
+    if (static_cast<long>(c->N) * s.H * 2 <= 160 * 1024)
+      for (int st = 8; st >= 2 && st_res == 0; --st)
+        if (k1_smem_bytes(c->N, s.H, st, 1, c->slab_rows_max) <= c->smem_optin) st_res = st;
+    for (int st = 8; st >= 2 && st_str == 0; --st)
+      if (k1_smem_bytes(c->N, s.H, st, 0, c->slab_rows_max) <= c->smem_optin) st_str = st;
+    bool use_res = st_res >= 4 || (st_res > 0 && st_str == 0);
+    if (const char* e = std::getenv("DINFER_K1_HRES")) use_res = (std::atoi(e) != 0 && st_res > 0) || st_str == 0;
+    c->k1_hres = use_res ? 1 : 0;
+    c->k1_stages = use_res ? st_res : st_str;
+    if (c->k1_stages == 0) { delete c; return DINFER_ERR_UNSUPPORTED; }
+    c->k1_smem = k1_smem_bytes(c->N, s.H, c->k1_stages, c->k1_hres, c->slab_rows_max);
+
+    // ---- K2 geometry: hidden slices x vocab groups <= #SMs.  Prefer the widest
+    // hidden slice that divides H (512 columns: 1 KB contiguous E row segments,
+    // 4 x 37 = 148 CTAs at H = 2048; measured 131 us vs 165 us with 256), then
+    // the deepest E ring (>= 2 stages) with logits/P rings of >= 2 stages.
+    c->k2_nchunks = static_cast<int>((s.V_local + kKChunk - 1) / kKChunk);
+    int hw_pref = 512;
+    if (const char* e = std::getenv("DINFER_K2_HW")) hw_pref = std::atoi(e);  // tuning override: 128 / 256 / 512
+    c->k2_stages = 0;
+    for (int hw = 512; hw >= 128 && c->k2_stages == 0; hw /= 2) {
+      if (hw > hw_pref || s.H % hw != 0) continue;
+      for (int pst = 4; pst >= 1 && c->k2_stages == 0; --pst)  // depth 1 only for very large M
+        for (int st = 6; st >= 2; --st)
+          if (k2_smem_bytes(c->N, hw, st, pst) <= c->smem_optin) {
+            c->k2_HW = hw;
+            c->k2_pstages = pst;
+            c->k2_stages = st;
+            break;
+          }
+    }
+    if (c->k2_stages == 0) { delete c; return DINFER_ERR_UNSUPPORTED; }
+    c->k2_HS = s.H / c->k2_HW;
+    c->k2_VG = std::max(1, std::min(c->num_sms / std::max(1, c->k2_HS), c->k2_nchunks));
+    c->k2_smem = k2_smem_bytes(c->N, c->k2_HW, c->k2_stages, c->k2_pstages);
+    if (const char* e = std::getenv("DINFER_PDL")) c->pdl = std::atoi(e) != 0;
+  }
 
   // ---- workspace
   c->stats_words = static_cast<size_t>(M) * (kStatWords + s.K);
   c->full_words = c->stats_words + (s.smooth_capable ? static_cast<size_t>(M) * s.H : 0);
   dinfer_status st = DINFER_OK;
   auto A = [&](dinfer_status x) { if (st == DINFER_OK) st = x; };
-  A(dev_alloc(&c->part1, static_cast<size_t>(c->k1_grid) * M * 4));
+  A(dev_alloc(&c->part1, static_cast<size_t>(c->dense ? c->kb_VG : c->k1_grid) * M * 4));
   A(dev_alloc(&c->counter, 4));
   A(dev_alloc(&c->err, 4));
   A(dev_alloc(&c->rec_local, c->full_words));
@@ -542,6 +560,34 @@ dinfer_status dinfer_step(dinfer_ctx* c, const uint16_t* hidden, const uint16_t*
   const int world = c->shp.world;
   if (world > 1 && !c->has_comm) return DINFER_ERR_UNSUPPORTED;
   for (int i = 0; i < kNumPhases; ++i) c->ev_used[i] = false;
+  if (c->dense) {
+    // compute-bound path: K1b writes one record row per (vocab group,
+    // position); K3 combines the groups like ranks
+    if (p->use_credit || p->use_smooth) return DINFER_ERR_UNSUPPORTED;
+    const uint64_t H = static_cast<uint64_t>(c->shp.H);
+    if (W != c->c_w) {
+      if (!encode_2d(&c->map_w, W, H, static_cast<uint64_t>(c->shp.V_local), kKChunk, kTileRows))
+        return DINFER_ERR_CUDA;
+      c->c_w = W;
+    }
+    if (hidden != c->c_h) {
+      if (!encode_2d(&c->map_h, hidden, H, static_cast<uint64_t>(c->M), kKChunk, kTileRows)) return DINFER_ERR_CUDA;
+      c->c_h = hidden;
+    }
+    K1bArgs kb{};
+    kb.M = c->M;
+    kb.H = c->shp.H;
+    kb.V_local = static_cast<int>(c->shp.V_local);
+    kb.v_offset = static_cast<int>(c->shp.v_offset);
+    kb.VG = c->kb_VG;
+    kb.stages = c->kb_stages;
+    kb.part = c->part1;
+    ev_begin(c, kPK1);
+    DI_CUDA(launch_k1b(c->map_h, c->map_w, kb, c->kb_grid, c->kb_smem, c->stream, c->pdl));
+    ev_finish(c, kPK1);
+    return run_combine(c, c->part1, static_cast<size_t>(c->M) * 4, c->kb_VG, false, e_mask, mask, tokens,
+                       credit_ids, credit_val, p, committed, smoothed, stats, /*rec_stride=*/4);
+  }
   const bool smooth = p->use_smooth != 0;
   s = run_local(c, hidden, W, E, mask, credit_ids, p, c->rec_local, /*reduce_acc=*/world > 1);
   if (s != DINFER_OK) return s;
@@ -564,6 +610,7 @@ dinfer_status dinfer_step_local(dinfer_ctx* c, const uint16_t* hidden, const uin
                                 const uint8_t* mask, const int32_t* credit_ids, const dinfer_params* p,
                                 float* record) {
   if (c == nullptr || record == nullptr) return DINFER_ERR_ARG;
+  if (c->dense) return DINFER_ERR_UNSUPPORTED;
   dinfer_status s = check_params(c, p);
   if (s != DINFER_OK) return s;
   if (hidden == nullptr || W == nullptr || mask == nullptr) return DINFER_ERR_ARG;
@@ -578,6 +625,7 @@ dinfer_status dinfer_step_combine(dinfer_ctx* c, const float* records, const uin
                                   int32_t* tokens, int32_t* credit_ids, float* credit_val, const dinfer_params* p,
                                   uint8_t* committed, float* smoothed, float* stats) {
   if (c == nullptr || records == nullptr) return DINFER_ERR_ARG;
+  if (c->dense) return DINFER_ERR_UNSUPPORTED;
   dinfer_status s = check_params(c, p);
   if (s != DINFER_OK) return s;
   if (mask == nullptr || tokens == nullptr || committed == nullptr) return DINFER_ERR_ARG;
@@ -695,6 +743,7 @@ int32_t dinfer_get_trace(dinfer_ctx* c, uint64_t* out, int32_t n) {
 
 int32_t dinfer_launches_per_step(const dinfer_ctx* c, const dinfer_params* p) {
   if (c == nullptr || p == nullptr) return 0;
+  if (c->dense) return 2;  // K1b, K3
   int n = 2;  // K1, K3
   if (p->use_smooth) n += 2 + (c->shp.world > 1 ? 1 : 0);
   return n;
@@ -702,7 +751,7 @@ int32_t dinfer_launches_per_step(const dinfer_ctx* c, const dinfer_params* p) {
 
 dinfer_status dinfer_get_geometry(const dinfer_ctx* c, dinfer_geometry* g) {
   if (c == nullptr || g == nullptr) return DINFER_ERR_ARG;
-  g->k1_grid = c->k1_grid;
+  g->k1_grid = c->dense ? c->kb_grid : c->k1_grid;
   g->k1_stages = c->k1_stages;
   g->k1_h_resident = c->k1_hres;
   g->k1_smem = static_cast<int32_t>(c->k1_smem);

@@ -55,6 +55,17 @@ size_t k1_smem_bytes(int N, int H, int stages, int h_resident, int slab_rows_max
 cudaError_t launch_k1(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
                       const K1Args& a, int grid, size_t smem, cudaStream_t st, bool pdl);
 
+// ---------------------------------------------------------------- K1b (M > 256)
+struct K1bArgs {
+  int M, H, V_local, v_offset;
+  int VG;                  // vocab groups (record rows per position)
+  int stages;
+  float* part;             // [VG][M] float4 (m, v* bits, l, 0) -- K3 reads it as VG "ranks"
+};
+size_t k1b_smem_bytes(int stages);
+cudaError_t launch_k1b(const CUtensorMap& map_h, const CUtensorMap& map_w, const K1bArgs& a, int grid, size_t smem,
+                       cudaStream_t st, bool pdl);
+
 // ---------------------------------------------------------------- K2
 struct K2Args {
   int M, N, H, V_local;

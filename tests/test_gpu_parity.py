@@ -37,7 +37,7 @@ def run_trajectory(torch_cuda, V, H, B, S, K, seed, params_fn, use_credit, max_i
     W, E = weights(V, H)
     _, _, _, steps = vetted_trajectory(W, E, B, S, seed, params_fn, max_iters=max_iters,
                                        use_credit_table=use_credit, **kw)
-    ctx = Context(B, S, H, K, V)
+    ctx = Context(B, S, H, K, V, smooth_capable=B * S <= 256)  # M > 256: dense stats-only path
     Wd, Ed = to_dev_bf16(W), to_dev_bf16(E)
     emd = to_dev_bf16(E[synth.mask_id(V)])
     replay(ctx, Wd, Ed, emd, steps, B, S, H, K, V)
@@ -249,3 +249,66 @@ def test_8b_shape_threshold(torch_cuda):
     """LLaDA-8B shape (BASELINE configs[1]): H=4096 (hidden streamed with W),
     V=126464, block 32, bs1, threshold decoding; 3 iterations."""
     run_trajectory(torch_cuda, 126464, 4096, 1, 32, 32, 1, thr_params(0.9), False, max_iters=3)
+
+
+# ---------------------------------------------------------------- compute-bound path (M > 256, K1b)
+def test_dense_path_threshold_and_hier(torch_cuda):
+    """M = 512 positions (B=4 x S=128) -> the dense K1b path; whole trajectory."""
+    run_trajectory(torch_cuda, 4096, 256, 4, 128, 8, 21, thr_params(0.9), False, max_iters=5)
+    pf = lambda t: O.Params(decoder=O.DEC_HIERARCHICAL, theta_hi=O.tau_schedule(0.92, t, 4), theta_lo=0.62)
+    run_trajectory(torch_cuda, 4096, 256, 4, 128, 8, 22, pf, False, max_iters=5)
+
+
+def test_dense_path_ragged(torch_cuda):
+    """M = 300 (partial 256-position block), V = 1000 (partial vocab block), H = 384."""
+    run_trajectory(torch_cuda, 1000, 384, 3, 100, 8, 23, thr_params(0.85), False, max_iters=4)
+
+
+def test_dense_path_rejects_credit_and_smoothing(torch_cuda):
+    from paper_2510_08666_b200 import Context, DInferError
+    with pytest.raises(DInferError):
+        Context(4, 128, 256, 8, 4096, smooth_capable=True)  # smoothing workspace not offered for M > 256
+    ctx = Context(4, 128, 256, 8, 4096, smooth_capable=False)
+    W, E = weights(4096, 256)
+    st = GpuState(4, 128, 256, 8, 4095)
+    h = to_dev_bf16(synth.planted_hidden(W, 512, seed=1))
+    with pytest.raises(DInferError) as ei:
+        ctx.step(h, to_dev_bf16(W), None, None, st.mask, st.tokens, st.cids, st.cval,
+                 gpu_params(O.Params(use_credit=True)), st.committed, None, st.stats)
+    assert ei.value.status == 6
+
+
+@pytest.mark.slow
+def test_8b_bs64_block64_sampled_rows(torch_cuda):
+    """LLaDA-8B shape bs64 x block 64 (BASELINE configs[4]): the GPU runs all
+    64 batch rows (M = 4096); two batch rows are margin-vetted trajectories
+    checked against the oracle (selection is per batch row), the rest are
+    planted filler."""
+    import torch
+    from paper_2510_08666_b200 import Context
+    V, H, B, S, K = 126464, 4096, 64, 64, 8
+    W, _ = weights(V, H)
+    Wd = to_dev_bf16(W)
+    sample = {5: 31, 40: 32}  # batch row -> trajectory seed
+    trajs = {}
+    for b, seed in sample.items():
+        _, _, _, steps = vetted_trajectory(W, W[:8], 1, S, seed, thr_params(0.9), max_iters=2)
+        trajs[b] = steps
+    filler = synth.planted_hidden(W, B * S, seed=33).reshape(B, S, H)
+    ctx = Context(B, S, H, K, V, smooth_capable=False)
+    st = GpuState(B, S, H, K, synth.mask_id(V))
+    for t in range(2):
+        h = filler.copy()
+        for b in sample:
+            h[b] = trajs[b][t]["h"][0]
+        p = trajs[5][t]["params"]
+        ctx.step(to_dev_bf16(h.reshape(B * S, H)), Wd, None, None, st.mask, st.tokens, None, None, gpu_params(p),
+                 st.committed, None, st.stats)
+        torch.cuda.synchronize()
+        ctx.sync()
+        out = st.snapshot()
+        for b in sample:
+            gold = trajs[b][t]["result"]
+            one = {k: (v[b:b + 1] if isinstance(v, np.ndarray) and v.ndim >= 1 and v.shape[0] == B else v)
+                   for k, v in out.items()}
+            compare(one, gold, trajs[b][t]["mask"], p, where=f"row {b} iter {t}")

@@ -61,7 +61,7 @@ def vetted_trajectory(W_u16, E_u16, B, S, seed, params_fn, max_iters=None,
     M = B * S
     W64 = O.bf16_bits_to_f64(W_u16)
     E64 = O.bf16_bits_to_f64(E_u16)
-    em64 = E64[synth.mask_id(V)]
+    em64 = E64[synth.mask_id(V)] if E64.shape[0] == V else E64[0]  # e_mask only used with smoothing
     sch = synth.PlantedSchedule(M, V, H, seed, ramp=ramp, flip_prob=flip_prob)
     mask = np.ones((B, S), bool)
     tokens = np.full((B, S), synth.mask_id(V), dtype=np.int64)

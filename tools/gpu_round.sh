@@ -10,8 +10,11 @@ python - "$1" <<'PY'
 import json, sys
 d = json.load(open(sys.argv[1]))
 ph = {k.split('_')[0]: round(v * 1000, 1) for k, v in d["phases_ms"].items() if v}
-print(f"  step {d['ms_per_step']*1000:.1f} us  {d['value']:.0f} pos/s  step-roofline {d['step_roofline']['frac']:.3f}"
-      f"  kernels(us) {ph}  e2e {d['e2e']['ms_per_step']*1000:.1f} us  clocks {d['clocks']['sm_mhz']} {d['clocks']['reasons']}")
+sr = d.get("step_roofline") or {}
+r = d["roofline"]
+print(f"  [{d['config'].get('name')}] step {d['ms_per_step']*1000:.1f} us  {d['value']:.0f} pos/s  step-roofline {sr.get('frac', 0):.3f}"
+      f"  {r['kernel']} {r['achieved']:.0f} {r['unit']} ({r['frac']:.3f})  kernels(us) {ph}  e2e {d['e2e']['ms_per_step']*1000:.1f} us"
+      f"  clocks {d['clocks']['sm_mhz']} {d['clocks']['reasons']}")
 PY
 }
 for v in "default" "$@"; do
