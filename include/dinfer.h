@@ -199,9 +199,9 @@ dinfer_status dinfer_get_timing(dinfer_ctx* ctx, float* ms, int32_t n);
 int32_t dinfer_launches_per_step(const dinfer_ctx* ctx, const dinfer_params* params);
 
 /* Per-CTA kernel timelines (diagnostics).  Only when the process sets
- * DINFER_TRACE=1 before dinfer_create: K1 then K2 CTAs, 4 %globaltimer
- * nanosecond stamps each (start, first operand stage ready, main loop done,
- * exit) of the most recent step.  Returns the number of words (out == NULL:
+ * DINFER_TRACE=1 before dinfer_create: K1 then K2 CTAs, 5 words each: 4
+ * %globaltimer nanosecond stamps (start, first operand stage ready, main loop
+ * done, exit) and the SM id, of the most recent step.  Returns the number of words (out == NULL:
  * the number available), 0 if tracing is off.                               */
 int32_t dinfer_get_trace(dinfer_ctx* ctx, uint64_t* out, int32_t n);
 

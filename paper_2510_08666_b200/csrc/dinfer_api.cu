@@ -56,6 +56,10 @@ struct dinfer_ctx {
   float* flog = nullptr;
   float* part2 = nullptr;
   float* ml = nullptr;
+  float* mref = nullptr;          // [k2_VG][M] per-vocab-group reference max (K2 -> K4 / record finalize)
+  unsigned* grp_cnt = nullptr;    // [k2_VG] K1 slabs done per vocab group (self-resetting)
+  unsigned* grp_pass = nullptr;   // [k2_VG]
+  int k1_VG = 1, k1_SPG = 1;      // K1 slab partition: vocab groups x slabs per group
   unsigned long long* trace = nullptr;  // DINFER_TRACE=1: [K1 grid + K2 grid][4] globaltimer ns
   size_t stats_words = 0, full_words = 0;
   // staging for dinfer_step_host (device)
@@ -218,8 +222,11 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
   a.slab_rows_max = c->slab_rows_max;
   a.mask = mask;
   a.credit_ids = p->use_credit ? credit_ids : nullptr;
+  a.VG = c->k1_VG;
+  a.SPG = c->k1_SPG;
+  a.nchunks = static_cast<int>((c->shp.V_local + kKChunk - 1) / kKChunk);
   a.part = c->part1;
-  a.counter = c->counter;
+  a.grp_cnt = smooth ? c->grp_cnt : nullptr;  // K2 consumes the group counts
   a.rec = rec;
   a.flog = smooth ? c->flog : nullptr;
   a.err = c->err;
@@ -241,18 +248,33 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
     b.stages = c->k2_stages;
     b.pstages = c->k2_pstages;
     b.flog = c->flog;
-    b.rec = rec;
-    b.rec_stride = kStatWords + c->shp.K;
+    b.part1 = reinterpret_cast<const float4*>(c->part1);
+    b.grid1 = c->k1_grid;
+    b.SPG = c->k1_SPG;
+    b.grp_cnt = c->grp_cnt;
+    b.grp_pass = c->grp_pass;
+    b.mref = c->mref;
     b.part = c->part2;
-    b.trace = c->trace == nullptr ? nullptr : c->trace + 4 * c->k1_grid;
+    b.trace = c->trace == nullptr ? nullptr : c->trace + 5 * c->k1_grid;
     ev_begin(c, kPK2);
     DI_CUDA(launch_k2(c->map_e, c->map_f, b, c->k2_smem, c->stream, c->pdl));
     ev_finish(c, kPK2);
-    if (reduce_acc) {
-      ev_begin(c, kPK2r);
-      DI_CUDA(launch_acc_reduce(c->part2, c->k2_VG, c->M * c->shp.H, rec + c->stats_words, c->stream, c->pdl));
-      ev_finish(c, kPK2r);
-    }
+  }
+  if (reduce_acc) {  // the rank record (sharded / split-phase): stats (+ acc) finalize
+    RecArgs r{};
+    r.M = c->M;
+    r.H = c->shp.H;
+    r.grid1 = c->k1_grid;
+    r.VG = c->k2_VG;
+    r.rec_stride = kStatWords + c->shp.K;
+    r.part1 = reinterpret_cast<const float4*>(c->part1);
+    r.part2 = smooth ? c->part2 : nullptr;
+    r.mref = c->mref;
+    r.rec = rec;
+    r.rec_acc = rec + c->stats_words;
+    ev_begin(c, kPK2r);
+    DI_CUDA(launch_rec_finalize(r, c->stream, c->pdl));
+    ev_finish(c, kPK2r);
   }
   return DINFER_OK;
 }
@@ -268,6 +290,8 @@ dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, in
   k.S = c->shp.S;
   k.K = c->shp.K;
   k.world = world;
+  k.part1 = acc_from_part2 ? reinterpret_cast<const float4*>(c->part1) : nullptr;  // single-rank dinfer_step
+  k.grid1 = c->k1_grid;
   k.recs = recs;
   k.rec_words = static_cast<long>(rec_words);
   k.rec_stride = rec_stride > 0 ? rec_stride : kStatWords + c->shp.K;
@@ -299,7 +323,9 @@ dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, in
       f.acc = c->part2;
       f.acc_stride = static_cast<long>(c->M) * c->shp.H;
       f.nparts = c->k2_VG;
-      f.m_part = nullptr;  // all partials are relative to the (only) rank's max
+      f.m_part = c->mref;  // partial g is relative to its vocab group's max m_g
+      f.m_stride = c->M;
+      f.m_rowstride = 1;
     } else {
       f.acc = recs + c->stats_words;
       f.acc_stride = static_cast<long>(rec_words);
@@ -385,7 +411,8 @@ void dinfer_destroy(dinfer_ctx* c) {
 #ifdef DINFER_WITH_NCCL
   if (c->has_comm) ncclCommDestroy(c->comm);
 #endif
-  void* bufs[] = {c->part1, c->counter, c->err, c->rec_local, c->flog, c->part2, c->ml, c->trace,
+  void* bufs[] = {c->part1, c->counter, c->err, c->rec_local, c->flog, c->part2, c->ml, c->trace, c->mref,
+                  c->grp_cnt, c->grp_pass,
                   c->st_hidden, c->st_mask, c->st_tokens, c->st_cids, c->st_cval, c->st_committed,
                   c->st_smoothed, c->st_stats};
   for (void* b : bufs)
@@ -442,26 +469,6 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
     c->kb_smem = k1b_smem_bytes(c->kb_stages);
   }
   if (!c->dense) {
-    // ---- K1 geometry: one CTA per SM over equal 8-row-granular vocab slabs
-    const long g8 = s.V_local / kRowGran;
-    c->k1_grid = static_cast<int>(std::min<long>(c->num_sms, std::max<long>(1, (s.V_local + kTileRows - 1) / kTileRows)));
-    c->slab_rows_max = static_cast<int>(kRowGran * ((g8 + c->k1_grid - 1) / c->k1_grid));
-    // Hidden block resident in smem (loaded once) or streamed from L2 with every
-    // W stage.  Residency only pays if it still leaves >= 4 W stages: at MoE
-    // shape it leaves 2 (measured 144 us) against 5 streamed stages (134 us).
-    int st_res = 0, st_str = 0;
-    if (static_cast<long>(c->N) * s.H * 2 <= 160 * 1024)
-      for (int st = 8; st >= 2 && st_res == 0; --st)
-        if (k1_smem_bytes(c->N, s.H, st, 1, c->slab_rows_max) <= c->smem_optin) st_res = st;
-    for (int st = 8; st >= 2 && st_str == 0; --st)
-      if (k1_smem_bytes(c->N, s.H, st, 0, c->slab_rows_max) <= c->smem_optin) st_str = st;
-    bool use_res = st_res >= 4 || (st_res > 0 && st_str == 0);
-    if (const char* e = std::getenv("DINFER_K1_HRES")) use_res = (std::atoi(e) != 0 && st_res > 0) || st_str == 0;
-    c->k1_hres = use_res ? 1 : 0;
-    c->k1_stages = use_res ? st_res : st_str;
-    if (c->k1_stages == 0) { delete c; return DINFER_ERR_UNSUPPORTED; }
-    c->k1_smem = k1_smem_bytes(c->N, s.H, c->k1_stages, c->k1_hres, c->slab_rows_max);
-
     // ---- K2 geometry: hidden slices x vocab groups <= #SMs.  Prefer the widest
     // hidden slice that divides H (512 columns: 1 KB contiguous E row segments,
     // 4 x 37 = 148 CTAs at H = 2048; measured 131 us vs 165 us with 256), then
@@ -485,6 +492,47 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
     c->k2_HS = s.H / c->k2_HW;
     c->k2_VG = std::max(1, std::min(c->num_sms / std::max(1, c->k2_HS), c->k2_nchunks));
     c->k2_smem = k2_smem_bytes(c->N, c->k2_HW, c->k2_stages, c->k2_pstages);
+    // ---- K1 geometry: one CTA per SM over contiguous vocab slabs.  With the
+    // smoothing workspace the slabs nest in K2's vocab groups (SPG slabs per
+    // group, group boundaries on 64-row chunks) so a K2 CTA depends only on
+    // its group's slabs; each slab is balanced at 8-row granularity.
+    const int nch = static_cast<int>((s.V_local + kKChunk - 1) / kKChunk);
+    if (s.smooth_capable) {
+      c->k1_VG = c->k2_VG;
+      const long grp_rows = (s.V_local + c->k1_VG - 1) / c->k1_VG;
+      c->k1_SPG = static_cast<int>(std::max<long>(1, std::min<long>(c->num_sms / c->k1_VG,
+                                                                    (grp_rows + kTileRows - 1) / kTileRows)));
+    } else {
+      c->k1_VG = 1;
+      c->k1_SPG = static_cast<int>(std::min<long>(c->num_sms, std::max<long>(1, (s.V_local + kTileRows - 1) / kTileRows)));
+    }
+    c->k1_grid = c->k1_VG * c->k1_SPG;
+    c->slab_rows_max = 0;
+    for (int g = 0; g < c->k1_VG; ++g) {  // same arithmetic as the kernel
+      const long rg0 = static_cast<long>(kKChunk) * (static_cast<long>(g) * nch / c->k1_VG);
+      const long rg1 = std::min<long>(s.V_local, static_cast<long>(kKChunk) * (static_cast<long>(g + 1) * nch / c->k1_VG));
+      const long n8 = (rg1 - rg0) / kRowGran;
+      for (int q = 0; q < c->k1_SPG; ++q) {
+        const long rows = kRowGran * ((q + 1) * n8 / c->k1_SPG - q * n8 / c->k1_SPG);
+        c->slab_rows_max = std::max<int>(c->slab_rows_max, static_cast<int>(rows));
+      }
+    }
+    // Hidden block resident in smem (loaded once) or streamed from L2 with every
+    // W stage.  Residency only pays if it still leaves >= 4 W stages: at MoE
+    // shape it leaves 2 (measured 144 us) against 5 streamed stages (134 us).
+    int st_res = 0, st_str = 0;
+    if (static_cast<long>(c->N) * s.H * 2 <= 160 * 1024)
+      for (int st = 8; st >= 2 && st_res == 0; --st)
+        if (k1_smem_bytes(c->N, s.H, st, 1, c->slab_rows_max) <= c->smem_optin) st_res = st;
+    for (int st = 8; st >= 2 && st_str == 0; --st)
+      if (k1_smem_bytes(c->N, s.H, st, 0, c->slab_rows_max) <= c->smem_optin) st_str = st;
+    bool use_res = st_res >= 4 || (st_res > 0 && st_str == 0);
+    if (const char* e = std::getenv("DINFER_K1_HRES")) use_res = (std::atoi(e) != 0 && st_res > 0) || st_str == 0;
+    c->k1_hres = use_res ? 1 : 0;
+    c->k1_stages = use_res ? st_res : st_str;
+    if (c->k1_stages == 0) { delete c; return DINFER_ERR_UNSUPPORTED; }
+    c->k1_smem = k1_smem_bytes(c->N, s.H, c->k1_stages, c->k1_hres, c->slab_rows_max);
+
     if (const char* e = std::getenv("DINFER_PDL")) c->pdl = std::atoi(e) != 0;
   }
 
@@ -503,10 +551,16 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
   if (s.smooth_capable) {
     A(dev_alloc(&c->flog, static_cast<size_t>(M) * s.V_local));
     A(dev_alloc(&c->part2, static_cast<size_t>(c->k2_VG) * M * s.H));
+    A(dev_alloc(&c->mref, static_cast<size_t>(c->k2_VG) * M));
+    A(dev_alloc(&c->grp_cnt, static_cast<size_t>(c->k2_VG)));
+    A(dev_alloc(&c->grp_pass, static_cast<size_t>(c->k2_VG)));
   }
   if (std::getenv("DINFER_TRACE") != nullptr && std::atoi(std::getenv("DINFER_TRACE")) != 0)
-    A(dev_alloc(&c->trace, static_cast<size_t>(4) * (c->k1_grid + c->k2_HS * c->k2_VG)));
+    A(dev_alloc(&c->trace, static_cast<size_t>(5) * (c->k1_grid + c->k2_HS * c->k2_VG)));
   if (st == DINFER_OK) {
+    if (c->grp_cnt != nullptr && (cudaMemset(c->grp_cnt, 0, 4 * c->k2_VG) != cudaSuccess ||
+                                  cudaMemset(c->grp_pass, 0, 4 * c->k2_VG) != cudaSuccess))
+      st = DINFER_ERR_CUDA;
     if (cudaMemset(c->counter, 0, 16) != cudaSuccess || cudaMemset(c->err, 0, 16) != cudaSuccess ||
         cudaMemset(c->rec_local, 0, c->full_words * 4) != cudaSuccess)
       st = DINFER_ERR_CUDA;
@@ -733,7 +787,7 @@ dinfer_status dinfer_get_timing(dinfer_ctx* c, float* ms, int32_t n) {
 
 int32_t dinfer_get_trace(dinfer_ctx* c, uint64_t* out, int32_t n) {
   if (c == nullptr || c->trace == nullptr) return 0;
-  const int total = 4 * (c->k1_grid + c->k2_HS * c->k2_VG);
+  const int total = 5 * (c->k1_grid + c->k2_HS * c->k2_VG);
   if (out == nullptr) return total;
   cudaStreamSynchronize(c->stream);
   const int k = n < total ? n : total;

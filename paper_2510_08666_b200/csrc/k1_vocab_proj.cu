@@ -18,8 +18,9 @@
 //   warps 0-3 epilogue: tcgen05.ld 32 columns per lane (lane = vocab row),
 //             warp-shuffle reduce-scatter of (m, idx, l) across the 32 rows
 //             (31 pairwise merges per 32x32 block), running merge per column.
-//   End: cross-warp merge -> per-CTA partial -> last CTA merges all partials
-//   in fixed order (deterministic) into the rank record.
+//   End: cross-warp merge -> per-CTA partial (m, idx, l) per position, and a
+//   release-ordered increment of the slab's vocab-group counter (K2 waits on
+//   it).  Partials are merged downstream in a fixed order (deterministic).
 #include <climits>
 
 #include "common.cuh"
@@ -113,7 +114,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + a.stages;
   uint64_t* tfull = empty + a.stages;
   uint64_t* tempty = tfull + 2;
-  uint64_t* mfull = tempty + 2;  // last-CTA bulk load of the partials
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L.misc_off);  // tmem base, last flag, entry count
   int* head = reinterpret_cast<int*>(smem + L.head_off);
   int16_t* ent_s = reinterpret_cast<int16_t*>(smem + L.ent_off);
@@ -121,14 +121,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   int16_t* ent_next = ent_k + kMaxCreditEnt;
   float* red = reinterpret_cast<float*>(smem + L.red_off);
 
-  // Contiguous slab of vocab rows [r0, r1), balanced at 8-row granularity.
-  const long g8 = a.V_local / kRowGran;
-  const int r0 = kRowGran * static_cast<int>(static_cast<long>(blockIdx.x) * g8 / gridDim.x);
-  const int r1 = kRowGran * static_cast<int>(static_cast<long>(blockIdx.x + 1) * g8 / gridDim.x);
+  // Contiguous slab of vocab rows [r0, r1): the vocabulary is cut into VG
+  // groups on 64-row chunk boundaries (K2's vocab groups) and each group into
+  // SPG slabs balanced at 8-row granularity; slab = blockIdx.x.
+  const int grp = blockIdx.x / a.SPG, q = blockIdx.x - grp * a.SPG;
+  const int rg0 = kKChunk * static_cast<int>(static_cast<long>(grp) * a.nchunks / a.VG);
+  const int rg1 = min(a.V_local, kKChunk * static_cast<int>(static_cast<long>(grp + 1) * a.nchunks / a.VG));
+  const int n8 = (rg1 - rg0) / kRowGran;
+  const int r0 = rg0 + kRowGran * static_cast<int>(static_cast<long>(q) * n8 / a.SPG);
+  const int r1 = rg0 + kRowGran * static_cast<int>(static_cast<long>(q + 1) * n8 / a.SPG);
   const int ntiles = (r1 - r0 + kTileRows - 1) / kTileRows;
   const uint32_t tmem_cols = tmem_cols_pow2(2u * N);
 
-  if (a.trace != nullptr && threadIdx.x == 0) a.trace[blockIdx.x * 4 + 0] = globaltimer_ns();
+  if (a.trace != nullptr && threadIdx.x == 0) { a.trace[blockIdx.x * 5 + 0] = globaltimer_ns(); uint32_t sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm)); a.trace[blockIdx.x * 5 + 4] = sm; }
   if (warp == 4 && lane == 0) {
     prefetch_tmap(&map_w);
     prefetch_tmap(&map_w8);
@@ -141,7 +146,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], kEpiWarps * kWarpThreads);
     }
-    mbar_init(mfull, 1);
     fence_mbar_init();
   }
   if (warp == 5) tmem_alloc(&misc[0], tmem_cols);
@@ -212,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kc0 = 0; kc0 < a.num_kc; kc0 += kChunksPerStage) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          if (a.trace != nullptr && t == 0 && kc0 == 0) a.trace[blockIdx.x * 4 + 1] = globaltimer_ns();
+          if (a.trace != nullptr && t == 0 && kc0 == 0) a.trace[blockIdx.x * 5 + 1] = globaltimer_ns();
 #pragma unroll
           for (int j = 0; j < kChunksPerStage; ++j) {
             const int kc = kc0 + j;
@@ -324,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&tempty[buf]);
     }
-    if (a.trace != nullptr && threadIdx.x == 0) a.trace[blockIdx.x * 4 + 2] = globaltimer_ns();
+    if (a.trace != nullptr && threadIdx.x == 0) a.trace[blockIdx.x * 5 + 2] = globaltimer_ns();
     // cross-warp merge (fixed warp order)
 #pragma unroll
     for (int g = 0; g < kMaxGroups; ++g) {
@@ -347,67 +351,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       reinterpret_cast<float4*>(a.part)[static_cast<long>(col) * gridDim.x + blockIdx.x] =
           make_float4(m, __int_as_float(ix), l, 0.f);
     }
+    // Publish: this slab's logits (flog), captured credited logits and
+    // partial statistics are complete -> count it towards its vocab group, so
+    // K2's CTAs for that group can start without waiting for the whole grid.
+    // The per-CTA partials are merged downstream (K2 needs only the group
+    // max, K3 merges all slabs in a fixed order), off K1's critical path.
     __threadfence();
     named_bar_epi();
-    if (threadIdx.x == 0) misc[1] = (atomicAdd(a.counter, 1u) == gridDim.x - 1) ? 1u : 0u;
-    named_bar_epi();
-    if (misc[1]) {
-      // Last CTA: bulk-copy the partials (column slabs) into the now idle
-      // operand region of shared memory, then merge each column with tpc
-      // threads in a fixed order (deterministic).
+    if (threadIdx.x == 0 && a.grp_cnt != nullptr) {
       __threadfence();
-      fence_proxy_async_global();
-      const int nthr = kEpiWarps * kWarpThreads;
-      const int G = static_cast<int>(gridDim.x);
-      const int cols_fit = max(1, static_cast<int>(L.bar_off / (static_cast<uint32_t>(G) * 16u)));
-      int tpc = 1;
-      while (tpc * 2 * a.M <= nthr && tpc < 32) tpc *= 2;
-      const int col_per_pass = min(nthr / tpc, cols_fit);
-      const float4* ps = reinterpret_cast<const float4*>(smem);
-      uint32_t mphase = 0;
-      for (int cb = 0; cb < a.M; cb += col_per_pass) {
-        const int ncols = min(col_per_pass, a.M - cb);
-        if (threadIdx.x == 0) {
-          fence_proxy_async();  // previous pass's generic smem reads before the async overwrite
-          const uint32_t bytes = static_cast<uint32_t>(ncols * G) * 16u;
-          mbar_expect_tx(mfull, bytes);
-          bulk_load(smem, reinterpret_cast<const float4*>(a.part) + static_cast<long>(cb) * G, bytes, mfull);
-        }
-        mbar_wait(mfull, mphase);
-        mphase ^= 1u;
-        const int lc = threadIdx.x / tpc;
-        const int sub = threadIdx.x % tpc;
-        float m = neg_inf(), l = 0.f;
-        int ix = INT_MAX;
-        if (lc < ncols) {
-          for (int c = sub; c < G; c += tpc) {
-            const float4 p = ps[lc * G + c];
-            stat_combine(m, ix, l, p.x, __float_as_int(p.y), p.z);
-          }
-        }
-        for (int o = 1; o < tpc; o <<= 1) {
-          const float rm = __shfl_down_sync(0xffffffffu, m, o);
-          const int ri = __shfl_down_sync(0xffffffffu, ix, o);
-          const float rl = __shfl_down_sync(0xffffffffu, l, o);
-          if ((sub & (2 * o - 1)) == 0) stat_combine(m, ix, l, rm, ri, rl);
-        }
-        if (lc < ncols && sub == 0) {
-          float* r = a.rec + (cb + lc) * stride;
-          r[0] = m;
-          r[1] = __int_as_float(ix);
-          r[2] = l;
-          r[3] = 0.f;
-        }
-        named_bar_epi();  // smem slab free for the next pass
-      }
-      if (threadIdx.x == 0) *a.counter = 0u;
+      atomicAdd(&a.grp_cnt[grp], 1u);
     }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 5) tmem_dealloc(tmem_base, tmem_cols);
-  if (a.trace != nullptr && threadIdx.x == 0) a.trace[blockIdx.x * 4 + 3] = globaltimer_ns();
+  if (a.trace != nullptr && threadIdx.x == 0) a.trace[blockIdx.x * 5 + 3] = globaltimer_ns();
 }
 
 }  // namespace

@@ -49,7 +49,7 @@ __host__ __device__ inline Layout make_layout(int N, int HW, int stages, int pst
   L.f_off = L.e_off + static_cast<uint32_t>(stages) * e_stage;
   L.p_off = L.f_off + static_cast<uint32_t>(pstages) * f_stage;
   L.bar_off = L.p_off + static_cast<uint32_t>(pstages) * p_stage;
-  L.misc_off = L.bar_off + static_cast<uint32_t>(2 * stages + 4 * pstages + 1) * 8u;
+  L.misc_off = L.bar_off + static_cast<uint32_t>(2 * stages + 4 * pstages + 2) * 8u;
   L.m_off = L.misc_off + 16u;
   L.total = L.m_off + static_cast<uint32_t>(N) * 4u;
   return L;
@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* pfull = fempty + a.pstages;
   uint64_t* pempty = pfull + a.pstages;
   uint64_t* accfull = pempty + a.pstages;
+  uint64_t* ready = accfull + 1;  // this CTA's vocab group of K1 slabs is complete
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L.misc_off);
   float* m_sm = reinterpret_cast<float*>(smem + L.m_off);
 
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int c1 = static_cast<int>(static_cast<long>(vg + 1) * a.nchunks / a.VG);
   const uint32_t tmem_cols = tmem_cols_pow2(static_cast<uint32_t>(a.nsub * N));
 
-  if (a.trace != nullptr && threadIdx.x == 0) a.trace[blockIdx.x * 4 + 0] = globaltimer_ns();
+  if (a.trace != nullptr && threadIdx.x == 0) { a.trace[blockIdx.x * 5 + 0] = globaltimer_ns(); uint32_t sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm)); a.trace[blockIdx.x * 5 + 4] = sm; }
   if (warp == 4 && lane == 0) {
     prefetch_tmap(&map_e);
     prefetch_tmap(&map_f);
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&pempty[i], 1);
     }
     mbar_init(accfull, 1);
+    mbar_init(ready, 1);
     fence_mbar_init();
   }
   if (warp == 5) tmem_alloc(&misc[0], tmem_cols);
@@ -144,7 +146,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 6) {
     // ------------------------------------------------------------ TMA: logits chunks
     if (lane == 0) {
-      grid_dep_wait();  // K1's logits (flog) visible
+      // Wait for the K1 slabs of this vocab group only (not the whole K1
+      // grid): their logits, partial statistics and group count are published
+      // with release ordering.  The last of the HS CTAs of the group resets
+      // the counters for the next step.
+      const volatile unsigned* cnt = a.grp_cnt + vg;
+      uint32_t spins = 0;
+      while (*cnt < static_cast<unsigned>(a.SPG)) {
+        __nanosleep(64);
+        if (++spins > (1u << 26)) __trap();
+      }
+      __threadfence();
+      if (atomicAdd(a.grp_pass + vg, 1u) == static_cast<unsigned>(a.HS - 1)) {
+        a.grp_cnt[vg] = 0u;
+        a.grp_pass[vg] = 0u;
+      }
+      fence_proxy_async_global();  // generic-proxy writes of K1 -> TMA reads below
+      mbar_arrive(ready);
       const uint64_t pol = policy_evict_last();  // re-read by the other hidden slices
       int stage = 0;
       uint32_t phase = 0;
@@ -167,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&pfull[ps], pph);
         mbar_wait(&efull[es], eph);
         tc_fence_after();
-        if (a.trace != nullptr && c == c0) a.trace[blockIdx.x * 4 + 1] = globaltimer_ns();
+        if (a.trace != nullptr && c == c0) a.trace[blockIdx.x * 5 + 1] = globaltimer_ns();
         const uint32_t e_addr = smem_u32(e_sm + es * e_stage);
         const uint32_t phi = smem_u32(p_sm + ps * 2 * p_half);
         const uint32_t plo = phi + p_half;
@@ -191,15 +209,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       mma_commit(accfull);
       if (a.trace != nullptr) {
         mbar_wait(accfull, 0);
-        a.trace[blockIdx.x * 4 + 2] = globaltimer_ns();
+        a.trace[blockIdx.x * 5 + 2] = globaltimer_ns();
       }
     }
     __syncwarp();
   } else {
     // ------------------------------------------------------------ P producers
+    // Reference max of this vocab group: m_g[s] = max over its K1 slabs of the
+    // partial maxima (exact max of the group's logits).  P = exp(f - m_g); the
+    // partial accumulator is relative to m_g, K4 rescales with exp(m_g - m).
     const int tid = threadIdx.x;
-    grid_dep_wait();  // K1's record (m per row) visible
-    for (int s = tid; s < N; s += kEpiWarps * kWarpThreads) m_sm[s] = (s < a.M) ? a.rec[s * a.rec_stride] : 0.f;
+    mbar_wait(ready, 0);
+    __threadfence();
+    for (int s = tid; s < N; s += kEpiWarps * kWarpThreads) {
+      float mg = 0.f;
+      if (s < a.M) {
+        mg = neg_inf();
+        const float4* ps = a.part1 + static_cast<long>(s) * a.grid1 + vg * a.SPG;
+        for (int q = 0; q < a.SPG; ++q) mg = fmaxf(mg, __ldcg(&ps[q].x));
+        if (hs == 0) a.mref[static_cast<long>(vg) * a.M + s] = mg;
+      }
+      m_sm[s] = mg;
+    }
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * kWarpThreads) : "memory");
     int ps = 0;
     uint32_t pph = 0;
@@ -267,19 +298,59 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 5) tmem_dealloc(tmem_base, tmem_cols);
-  if (a.trace != nullptr && threadIdx.x == 0) a.trace[blockIdx.x * 4 + 3] = globaltimer_ns();
+  if (a.trace != nullptr && threadIdx.x == 0) a.trace[blockIdx.x * 5 + 3] = globaltimer_ns();
 }
 
-__global__ void acc_reduce_kernel(const float* __restrict__ part, int VG, int MH, float* __restrict__ out) {
+// Rank record finalize (vocab-sharded / split-phase path only).  Block b < M:
+// one warp merges position b's K1 slab partials in a fixed order into the
+// record's (m, v*, l).  Blocks >= M (when part2): rec_acc[s, h..h+3] =
+// sum_g part2[g][s, h..] * e^{m_g - m_rank}, with m_rank recomputed from the
+// group maxima (identical to the merged m: the groups tile the shard).
+__global__ void rec_finalize_kernel(const RecArgs a) {
   grid_dep_wait();
-  const int i = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  if (i >= MH) return;
-  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int g = 0; g < VG; ++g) {
-    const float4 v = __ldcg(reinterpret_cast<const float4*>(part + static_cast<long>(g) * MH + i));
-    s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+  if (static_cast<int>(blockIdx.x) < a.M) {
+    if (threadIdx.x >= 32) return;
+    const int s = blockIdx.x, lane = threadIdx.x;
+    float m = neg_inf(), l = 0.f;
+    int ix = 0x7fffffff;
+    for (int j = lane; j < a.grid1; j += 32) {
+      const float4 p = __ldcg(a.part1 + static_cast<long>(s) * a.grid1 + j);
+      stat_combine(m, ix, l, p.x, __float_as_int(p.y), p.z);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float rm = __shfl_xor_sync(0xffffffffu, m, o);
+      const int ri = __shfl_xor_sync(0xffffffffu, ix, o);
+      const float rl = __shfl_xor_sync(0xffffffffu, l, o);
+      stat_combine(m, ix, l, rm, ri, rl);
+    }
+    if (lane == 0) {
+      float* r = a.rec + static_cast<long>(s) * a.rec_stride;
+      r[0] = m;
+      r[1] = __int_as_float(ix);
+      r[2] = l;
+      r[3] = 0.f;
+    }
+    return;
   }
-  *reinterpret_cast<float4*>(out + i) = s;
+  if (a.part2 == nullptr) return;
+  const long t = static_cast<long>(blockIdx.x - a.M) * blockDim.x + threadIdx.x;
+  const int h4 = a.H / 4;
+  if (t >= static_cast<long>(a.M) * h4) return;
+  const int s = static_cast<int>(t / h4);
+  const int h = static_cast<int>(t - static_cast<long>(s) * h4) * 4;
+  float mr = neg_inf();
+  for (int g = 0; g < a.VG; ++g) mr = fmaxf(mr, a.mref[static_cast<long>(g) * a.M + s]);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int g = 0; g < a.VG; ++g) {
+    const float sc = expf(a.mref[static_cast<long>(g) * a.M + s] - mr);
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(a.part2 + (static_cast<long>(g) * a.M + s) * a.H + h));
+    acc.x = fmaf(v.x, sc, acc.x);
+    acc.y = fmaf(v.y, sc, acc.y);
+    acc.z = fmaf(v.z, sc, acc.z);
+    acc.w = fmaf(v.w, sc, acc.w);
+  }
+  *reinterpret_cast<float4*>(a.rec_acc + static_cast<long>(s) * a.H + h) = acc;
 }
 
 }  // namespace
@@ -300,10 +371,10 @@ cudaError_t launch_k2(const CUtensorMap& map_e, const CUtensorMap& map_f, const 
   return launch_ex(k2_smooth_mix, dim3(a.HS * a.VG), dim3(kThreads), smem, st, pdl, map_e, map_f, a);
 }
 
-cudaError_t launch_acc_reduce(const float* part, int VG, int MH, float* out, cudaStream_t st, bool pdl) {
+cudaError_t launch_rec_finalize(const RecArgs& a, cudaStream_t st, bool pdl) {
   const int threads = 256;
-  const int blocks = (MH / 4 + threads - 1) / threads;
-  return launch_ex(acc_reduce_kernel, dim3(blocks), dim3(threads), 0, st, pdl, part, VG, MH, out);
+  const int acc_blocks = a.part2 == nullptr ? 0 : (a.M * (a.H / 4) + threads - 1) / threads;
+  return launch_ex(rec_finalize_kernel, dim3(a.M + acc_blocks), dim3(threads), 0, st, pdl, a);
 }
 
 }  // namespace dinfer

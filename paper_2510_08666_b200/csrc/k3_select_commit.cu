@@ -96,13 +96,30 @@ __global__ void __launch_bounds__(kK3Threads) k3_select_commit(const K3Args a) {
     const long roff = static_cast<long>(i) * a.rec_stride;
     float m = neg_inf(), l = 0.f;
     int vstar = INT_MAX;
-    if (lane < a.world) {
-      const float* rr = a.recs + lane * a.rec_words + roff;
-      m = rr[0];
-      vstar = __float_as_int(rr[1]);
-      l = rr[2];
+    if (a.part1 != nullptr) {
+      // single rank: merge K1's per-slab partials (lanes stride the slabs,
+      // then an xor butterfly; stat_combine is commutative bit for bit, so
+      // every lane holds the identical, deterministic result)
+      for (int j = lane; j < a.grid1; j += 32) {
+        const float4 p = __ldcg(a.part1 + static_cast<long>(i) * a.grid1 + j);
+        stat_combine(m, vstar, l, p.x, __float_as_int(p.y), p.z);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float rm = __shfl_xor_sync(0xffffffffu, m, o);
+        const int rv = __shfl_xor_sync(0xffffffffu, vstar, o);
+        const float rl = __shfl_xor_sync(0xffffffffu, l, o);
+        stat_combine(m, vstar, l, rm, rv, rl);
+      }
+    } else {
+      if (lane < a.world) {
+        const float* rr = a.recs + lane * a.rec_words + roff;
+        m = rr[0];
+        vstar = __float_as_int(rr[1]);
+        l = rr[2];
+      }
     }
-    {  // merge ranks 1..world-1 into lane 0 in rank order, then broadcast
+    if (a.part1 == nullptr) {  // merge ranks 1..world-1 into lane 0 in rank order, then broadcast
       float m0 = m, l0 = l;
       int v0 = vstar;
       for (int r = 1; r < a.world; ++r) {

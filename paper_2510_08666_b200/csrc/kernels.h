@@ -44,12 +44,13 @@ struct K1Args {
   int slab_rows_max;       // max rows of any CTA's slab (credit head table size)
   const uint8_t* mask;     // [M]
   const int32_t* credit_ids;  // [M][K] or nullptr
+  int VG, SPG, nchunks;     // vocab groups (64-row chunk aligned) x slabs per group = grid
   float* part;             // [M][grid] float4 per-CTA (m, idx, l, 0), column-major
-  unsigned* counter;       // last-CTA ticket, self-resetting
-  float* rec;              // [M][4+K] rank record (stats part)
+  unsigned* grp_cnt;       // [VG] slabs completed per group (K2 waits, resets), or nullptr
+  float* rec;              // [M][4+K] rank record: only fcred (captured credited logits) is written
   float* flog;             // [M][V_local] raw logits for K2, or nullptr
   int* err;
-  unsigned long long* trace;  // optional [grid][4] globaltimer ns: start, first W stage, last tile done, exit
+  unsigned long long* trace;  // optional [grid][5]: globaltimer ns start, first W stage, last tile done, exit; smid
 };
 size_t k1_smem_bytes(int N, int H, int stages, int h_resident, int slab_rows_max);
 cudaError_t launch_k1(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
@@ -74,22 +75,37 @@ struct K2Args {
   int nchunks;             // ceil(V_local / 64)
   int stages, pstages;
   const float* flog;       // [M][V_local]
-  const float* rec;        // rank record: m at rec[s*rec_stride]
-  int rec_stride;
+  const float4* part1;     // K1 partials [M][grid1]
+  int grid1, SPG;          // K1 slabs, slabs per vocab group
+  unsigned* grp_cnt;       // [VG] K1 slabs done per group
+  unsigned* grp_pass;      // [VG] K2 CTAs past the wait (the last resets both)
+  float* mref;             // [VG][M] out: per-group reference max m_g (acc is relative to it)
   float* part;             // [VG][M][H]
-  unsigned long long* trace;  // optional [grid][4] globaltimer ns: start, first E stage, MMAs done, exit
+  unsigned long long* trace;  // optional [grid][5]: globaltimer ns start, first E stage, MMAs done, exit; smid
 };
 size_t k2_smem_bytes(int N, int HW, int stages, int pstages);
 cudaError_t launch_k2(const CUtensorMap& map_e, const CUtensorMap& map_f, const K2Args& a, size_t smem,
                       cudaStream_t st, bool pdl);
 
-// sum of VG partials -> one [M][H] block (rank record acc)
-cudaError_t launch_acc_reduce(const float* part, int VG, int MH, float* out, cudaStream_t st, bool pdl);
+// Rank record finalize (sharded / split-phase path):
+//   stats: rec[s] = merge of K1's per-slab partials (fixed order);
+//   acc (if part2): rec_acc[s,:] = sum_g part2[g][s,:] * e^{m_g - m_rank}.
+struct RecArgs {
+  int M, H, grid1, VG, rec_stride;
+  const float4* part1;
+  const float* part2;      // [VG][M][H] or nullptr
+  const float* mref;       // [VG][M]
+  float* rec;              // stats rows
+  float* rec_acc;          // [M][H]
+};
+cudaError_t launch_rec_finalize(const RecArgs& a, cudaStream_t st, bool pdl);
 
 // ---------------------------------------------------------------- K3
 struct K3Args {
   int B, S, K, world;
-  const float* recs;       // world records, `rec_words` apart
+  const float4* part1;     // G = 1: K1 per-slab partials [M][grid1] (stats merged here), else nullptr
+  int grid1;
+  const float* recs;       // world records, `rec_words` apart (stats used when part1 == nullptr; fcred always)
   long rec_words;
   int rec_stride;          // 4 + K
   uint8_t* mask;

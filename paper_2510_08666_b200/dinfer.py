@@ -203,7 +203,7 @@ class Context:
 
     def trace(self):
         """Per-CTA globaltimer stamps of the last step (DINFER_TRACE=1), as
-        (k1 [grid,4], k2 [grid,4]) numpy arrays in ns, or None."""
+        (k1 [grid,5], k2 [grid,5]) numpy arrays (4 stamps in ns + SM id), or None."""
         import numpy as np
         n = int(lib().dinfer_get_trace(self._h, None, 0))
         if n == 0:
@@ -211,8 +211,8 @@ class Context:
         buf = np.zeros(n, dtype=np.uint64)
         lib().dinfer_get_trace(self._h, c_void_p(buf.ctypes.data), n)
         g = self.geometry()
-        k1 = buf[:4 * g["k1_grid"]].reshape(-1, 4)
-        return k1, buf[4 * g["k1_grid"]:].reshape(-1, 4)
+        k1 = buf[:5 * g["k1_grid"]].reshape(-1, 5)
+        return k1, buf[5 * g["k1_grid"]:].reshape(-1, 5)
 
     def geometry(self) -> dict:
         g = Geometry()

@@ -30,13 +30,15 @@ com = torch.zeros((B, S), dtype=torch.uint8, device="cuda")
 sm = torch.zeros((B, S, H), dtype=torch.float32, device="cuda") if smooth else None
 st = torch.zeros((B, S, 4), dtype=torch.float32, device="cuda")
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
-for it in range(4):
+runs = []
+for it in range(6):
     flush.fill_(1.0)
     mask.fill_(1)
     cids.fill_(-1)
     ctx.step(h, Wd, Ed, em, mask, tok, cids, cval, p, com, sm, st)
     torch.cuda.synchronize()
-k1, k2 = ctx.trace()
+    runs.append(tuple(x.copy() for x in ctx.trace()))
+k1, k2 = runs[-1]
 t0 = int(k1[:, 0].min())
 us = lambda a: (a.astype(np.int64) - t0) / 1e3
 
@@ -55,3 +57,20 @@ if smooth:
     for i, n in enumerate(["start", "first MMA (E+P)", "MMAs done", "exit"]):
         row(n, k2[:, i])
     print(f"  step span: {us(k2[:, 3]).max():.1f} us (K1 start -> last K2 CTA exit)")
+
+# Systematic or random?  Per-SM K1 main-loop duration across repeated steps.
+if len(runs) > 2:
+    dur = {}
+    for r1, _ in runs[1:]:
+        for row in r1:
+            dur.setdefault(int(row[4]), []).append((int(row[2]) - int(row[1])) / 1e3)
+    sms = sorted(dur)
+    d = np.array([dur[s_] for s_ in sms if len(dur[s_]) == len(runs) - 1])
+    if len(d):
+        mean = d.mean(axis=1)
+        corr = np.corrcoef(d[:, 0], d[:, 1])[0, 1] if d.shape[1] > 1 else float("nan")
+        print(f"K1 per-SM main-loop us over {d.shape[1]} steps: spread of per-SM means {mean.min():.1f}..{mean.max():.1f}, "
+              f"step-to-step correlation {corr:.2f}")
+        order = np.argsort(mean)
+        print("  slowest SMs:", [(sms[i], round(float(mean[i]), 1)) for i in order[-6:]])
+        print("  fastest SMs:", [(sms[i], round(float(mean[i]), 1)) for i in order[:6]])
