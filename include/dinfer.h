@@ -126,8 +126,10 @@ dinfer_status dinfer_set_stream(dinfer_ctx* ctx, void* stream);
  *               float in/out.  Only rows undecided at step start change.
  *               May be NULL iff !use_credit.
  *   committed   [B,S] uint8 out, 1 = committed by this step.
- *   smoothed    [B,S,H] float out: e_{t+1} for rows still undecided after the
- *               commit; other rows untouched.  NULL iff !use_smooth.
+ *   smoothed    [B,S,H] float out: e_{t+1} for every row undecided at
+ *               step start; it is meaningful for the rows still undecided
+ *               after the commit (the caller feeds only those back).
+ *               Rows decided at step start are untouched.  NULL iff !use_smooth.
  *   stats       [B,S,4] float out or NULL: (m = max logit, lse = log-sum-exp
  *               of the raw logits, p~ = confidence used by the decoder,
  *               v~ = committed/candidate id as int32 bits).
@@ -190,8 +192,9 @@ const char* dinfer_last_error(void);
 /* Instrumentation.  dinfer_set_timing(ctx, 1) brackets every kernel / the
  * collective of subsequent steps with CUDA events on the ctx stream;
  * dinfer_get_timing fills up to n floats with the last step's per-phase
- * milliseconds in the order [K1 vocab_proj, K2 smooth_mix, K2r acc_reduce,
- * C1 allgather, K3 select_commit, K4 smooth_finalize] (0 if not run); it
+ * milliseconds in the order [K1 vocab_proj (or K1b), K2 smooth_mix, record
+ * finalize (sharded / split-phase), C1 allgather, K34 select_commit +
+ * smooth_finalize, unused] (0 if not run); it
  * synchronises the stream.  dinfer_launches_per_step: kernels the library
  * launches for one dinfer_step with these params (collectives excluded).    */
 dinfer_status dinfer_set_timing(dinfer_ctx* ctx, int32_t enable);

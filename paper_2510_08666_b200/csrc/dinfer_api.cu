@@ -56,6 +56,7 @@ struct dinfer_ctx {
   float* flog = nullptr;
   float* part2 = nullptr;
   float* ml = nullptr;
+  uint8_t* mask_snap = nullptr;   // [M] step-start mask (K1 -> smoothing blocks of K34)
   float* mref = nullptr;          // [k2_VG][M] per-vocab-group reference max (K2 -> K4 / record finalize)
   unsigned* grp_cnt = nullptr;    // [k2_VG] K1 slabs done per vocab group (self-resetting)
   unsigned* grp_pass = nullptr;   // [k2_VG]
@@ -229,6 +230,7 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
   a.grp_cnt = smooth ? c->grp_cnt : nullptr;  // K2 consumes the group counts
   a.rec = rec;
   a.flog = smooth ? c->flog : nullptr;
+  a.mask_snap = smooth ? c->mask_snap : nullptr;
   a.err = c->err;
   a.trace = c->trace;
   ev_begin(c, kPK1);
@@ -312,11 +314,8 @@ dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, in
   k.c_beta = p->c_beta;
   k.c_gamma = p->c_gamma;
   k.err = c->err;
-  ev_begin(c, kPK3);
-  DI_CUDA(launch_k3(k, c->stream, c->pdl));
-  ev_finish(c, kPK3);
+  K4Args f{};
   if (p->use_smooth) {
-    K4Args f{};
     f.M = c->M;
     f.H = c->shp.H;
     if (acc_from_part2) {
@@ -334,15 +333,14 @@ dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, in
       f.m_stride = static_cast<long>(rec_words);
       f.m_rowstride = kStatWords + c->shp.K;
     }
-    f.ml = c->ml;
-    f.mask = mask;
+    f.mask_start = c->mask_snap;
     f.e_mask = e_mask;
     f.alpha_t = p->alpha_t;
     f.out = smoothed;
-    ev_begin(c, kPK4);
-    DI_CUDA(launch_k4(f, c->stream, c->pdl));
-    ev_finish(c, kPK4);
   }
+  ev_begin(c, kPK3);
+  DI_CUDA(launch_k34(k, p->use_smooth ? &f : nullptr, c->stream, c->pdl));
+  ev_finish(c, kPK3);
   return DINFER_OK;
 }
 
@@ -412,6 +410,7 @@ void dinfer_destroy(dinfer_ctx* c) {
   if (c->has_comm) ncclCommDestroy(c->comm);
 #endif
   void* bufs[] = {c->part1, c->counter, c->err, c->rec_local, c->flog, c->part2, c->ml, c->trace, c->mref,
+                  c->mask_snap,
                   c->grp_cnt, c->grp_pass,
                   c->st_hidden, c->st_mask, c->st_tokens, c->st_cids, c->st_cval, c->st_committed,
                   c->st_smoothed, c->st_stats};
@@ -546,6 +545,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
   A(dev_alloc(&c->err, 4));
   A(dev_alloc(&c->rec_local, c->full_words));
   A(dev_alloc(&c->ml, static_cast<size_t>(M) * 2));
+  A(dev_alloc(&c->mask_snap, static_cast<size_t>(M)));
   if (s.world > 1) A(dev_alloc(&c->rec_all, c->full_words * s.world));
   else c->rec_all = c->rec_local;
   if (s.smooth_capable) {
@@ -688,6 +688,7 @@ dinfer_status dinfer_step_combine(dinfer_ctx* c, const float* records, const uin
                         !aligned(e_mask, 8) || !aligned(smoothed, 16)))
     return DINFER_ERR_ARG;
   const size_t words = p->use_smooth ? c->full_words : c->stats_words;
+  if (p->use_smooth) DI_CUDA(cudaMemcpyAsync(c->mask_snap, mask, c->M, cudaMemcpyDeviceToDevice, c->stream));
   return run_combine(c, records, words, c->shp.world, /*acc_from_part2=*/false, e_mask, mask, tokens, credit_ids,
                      credit_val, p, committed, smoothed, stats);
 }
@@ -798,8 +799,9 @@ int32_t dinfer_get_trace(dinfer_ctx* c, uint64_t* out, int32_t n) {
 int32_t dinfer_launches_per_step(const dinfer_ctx* c, const dinfer_params* p) {
   if (c == nullptr || p == nullptr) return 0;
   if (c->dense) return 2;  // K1b, K3
-  int n = 2;  // K1, K3
-  if (p->use_smooth) n += 2 + (c->shp.world > 1 ? 1 : 0);
+  int n = 2;  // K1, K34
+  if (p->use_smooth) n += 1 + (c->shp.world > 1 ? 1 : 0);  // K2 (+ record finalize)
+  else if (c->shp.world > 1) n += 1;                         // record finalize
   return n;
 }
 

@@ -244,6 +244,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // raw logits are captured for the credit fuse.  Rows decided at step start
     // are frozen (reading c7) and skipped.  Runs while the first W chunks fly.
     grid_dep_wait();  // mask / credit ids of the previous step's commit visible
+    if (a.mask_snap != nullptr && blockIdx.x == 0)
+      for (int s = threadIdx.x; s < a.M; s += kEpiWarps * kWarpThreads) a.mask_snap[s] = a.mask[s];
     if (a.credit_ids != nullptr) {
       const int stride = kStatWords + a.K;
       for (int e = threadIdx.x; e < a.M * a.K; e += kEpiWarps * kWarpThreads) {

@@ -74,7 +74,51 @@ DI float warp_sum(float x) {
   return x;
 }
 
-__global__ void __launch_bounds__(kK3Threads) k3_select_commit(const K3Args a) {
+// Warp-collective: merged statistics (m, v*, l) of position i, from K1's
+// per-slab partials (single rank) or from the `world` records (rank order).
+// Every lane returns the identical, deterministic result.
+DI void row_stats(const K3Args& a, int i, int lane, float& m, int& vstar, float& l) {
+  m = neg_inf();
+  l = 0.f;
+  vstar = INT_MAX;
+  if (a.part1 != nullptr) {
+    // lanes stride the slabs, then an xor butterfly (stat_combine is
+    // commutative bit for bit, so all lanes agree)
+    for (int j = lane; j < a.grid1; j += 32) {
+      const float4 p = __ldcg(a.part1 + static_cast<long>(i) * a.grid1 + j);
+      stat_combine(m, vstar, l, p.x, __float_as_int(p.y), p.z);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float rm = __shfl_xor_sync(0xffffffffu, m, o);
+      const int rv = __shfl_xor_sync(0xffffffffu, vstar, o);
+      const float rl = __shfl_xor_sync(0xffffffffu, l, o);
+      stat_combine(m, vstar, l, rm, rv, rl);
+    }
+    return;
+  }
+  const long roff = static_cast<long>(i) * a.rec_stride;
+  if (lane < a.world) {
+    const float* rr = a.recs + lane * a.rec_words + roff;
+    m = rr[0];
+    vstar = __float_as_int(rr[1]);
+    l = rr[2];
+  }
+  float m0 = m, l0 = l;  // merge ranks 1..world-1 into lane 0 in rank order, then broadcast
+  int v0 = vstar;
+  for (int r = 1; r < a.world; ++r) {
+    const float mr = __shfl_sync(0xffffffffu, m, r);
+    const int vr = __shfl_sync(0xffffffffu, vstar, r);
+    const float lr = __shfl_sync(0xffffffffu, l, r);
+    stat_combine(m0, v0, l0, mr, vr, lr);
+  }
+  m = __shfl_sync(0xffffffffu, m0, 0);
+  vstar = __shfl_sync(0xffffffffu, v0, 0);
+  l = __shfl_sync(0xffffffffu, l0, 0);
+}
+
+// Selection block for batch row b (blockDim = kK3Threads).
+DI void select_block(const K3Args& a, int b) {
   __shared__ uint32_t s_reg[kMaxS / 32];
   __shared__ int s_runA[kMaxS];
   __shared__ unsigned long long s_runkey[kMaxS];
@@ -83,10 +127,6 @@ __global__ void __launch_bounds__(kK3Threads) k3_select_commit(const K3Args a) {
   __shared__ uint8_t s_und[kMaxS];
   __shared__ unsigned long long s_best;
 
-  grid_dep_wait();  // K1 / K2 / allgather results visible
-  grid_dep_launch_dependents();
-
-  const int b = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
 
@@ -94,44 +134,9 @@ __global__ void __launch_bounds__(kK3Threads) k3_select_commit(const K3Args a) {
   for (int s = warp; s < a.S; s += nwarps) {
     const int i = b * a.S + s;
     const long roff = static_cast<long>(i) * a.rec_stride;
-    float m = neg_inf(), l = 0.f;
-    int vstar = INT_MAX;
-    if (a.part1 != nullptr) {
-      // single rank: merge K1's per-slab partials (lanes stride the slabs,
-      // then an xor butterfly; stat_combine is commutative bit for bit, so
-      // every lane holds the identical, deterministic result)
-      for (int j = lane; j < a.grid1; j += 32) {
-        const float4 p = __ldcg(a.part1 + static_cast<long>(i) * a.grid1 + j);
-        stat_combine(m, vstar, l, p.x, __float_as_int(p.y), p.z);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float rm = __shfl_xor_sync(0xffffffffu, m, o);
-        const int rv = __shfl_xor_sync(0xffffffffu, vstar, o);
-        const float rl = __shfl_xor_sync(0xffffffffu, l, o);
-        stat_combine(m, vstar, l, rm, rv, rl);
-      }
-    } else {
-      if (lane < a.world) {
-        const float* rr = a.recs + lane * a.rec_words + roff;
-        m = rr[0];
-        vstar = __float_as_int(rr[1]);
-        l = rr[2];
-      }
-    }
-    if (a.part1 == nullptr) {  // merge ranks 1..world-1 into lane 0 in rank order, then broadcast
-      float m0 = m, l0 = l;
-      int v0 = vstar;
-      for (int r = 1; r < a.world; ++r) {
-        const float mr = __shfl_sync(0xffffffffu, m, r);
-        const int vr = __shfl_sync(0xffffffffu, vstar, r);
-        const float lr = __shfl_sync(0xffffffffu, l, r);
-        stat_combine(m0, v0, l0, mr, vr, lr);
-      }
-      m = __shfl_sync(0xffffffffu, m0, 0);
-      vstar = __shfl_sync(0xffffffffu, v0, 0);
-      l = __shfl_sync(0xffffffffu, l0, 0);
-    }
+    float m, l;
+    int vstar;
+    row_stats(a, i, lane, m, vstar, l);
     const bool und = a.mask[i] != 0;
     const float lse = m + logf(l);
     const float pstar = 1.0f / l;
@@ -261,55 +266,84 @@ __global__ void __launch_bounds__(kK3Threads) k3_select_commit(const K3Args a) {
   }
 }
 
-// 256 threads = 32 float4 columns x 8 partial groups: each thread sums a
-// strided subset of the partials, the 8 groups are then combined in a fixed
-// order through shared memory (deterministic; ~nparts/8 loads in flight per
-// thread instead of nparts dependent rounds).
-constexpr int kK4Cols = 32, kK4Groups = 8;
-__global__ void __launch_bounds__(kK4Cols * kK4Groups) k4_smooth_finalize(const K4Args a) {
-  __shared__ float4 red[kK4Groups][kK4Cols];
-  grid_dep_wait();  // K3's mask / (m, l) and K2's partials visible
-  const int h4 = a.H / 4;
-  const int cl = threadIdx.x % kK4Cols, grp = threadIdx.x / kK4Cols;
-  const long t = static_cast<long>(blockIdx.x) * kK4Cols + cl;
-  const bool in = t < static_cast<long>(a.M) * h4;
-  const int s = in ? static_cast<int>(t / h4) : 0;
-  const int h = in ? static_cast<int>(t - static_cast<long>(s) * h4) * 4 : 0;
-  const bool active = in && a.mask[s] != 0;  // only rows still masked get e_{t+1}
+// Smoothing block: 1024 threads = 128 float4 columns x 8 partial groups, i.e.
+// 512 consecutive elements of the [M, H] output.  Each thread loads a strided
+// subset of the nparts partials (issued before the statistics merge so both
+// latencies overlap), the 8 groups are combined in a fixed order through
+// shared memory (deterministic).  The block merges the statistics (m, l) of
+// the rows it covers itself (one warp per row), so it does not wait for the
+// selection; rows undecided at step START are written (e_{t+1} matters for
+// those still undecided after the commit).
+constexpr int kSmCols = 128, kSmGroups = 8, kSmBatch = 8;
+DI void smooth_block(const K3Args& a3, const K4Args& a, int blk) {
+  __shared__ float s_m[4], s_w[4];
+  __shared__ float4 red[kSmGroups][kSmCols];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cl = threadIdx.x % kSmCols, grp = threadIdx.x / kSmCols;
+  const long e0 = static_cast<long>(blk) * kSmCols * 4;
+  const long total = static_cast<long>(a.M) * a.H;
+  const int s0 = static_cast<int>(e0 / a.H);
+  const int s1 = static_cast<int>((min(e0 + kSmCols * 4, total) - 1) / a.H);
+  const long e = e0 + static_cast<long>(cl) * 4;
+  const bool in = e < total;
+  const int s = in ? static_cast<int>(e / a.H) : s0;
+  const int h = in ? static_cast<int>(e - static_cast<long>(s) * a.H) : 0;
+  const bool active = in && a.mask_start[s] != 0;
+  const float* src = a.acc + static_cast<long>(s) * a.H + h;
+  // first batch of partials in flight before the statistics merge
+  float4 v[kSmBatch];
+  float mp[kSmBatch];
+#pragma unroll
+  for (int j = 0; j < kSmBatch; ++j) {
+    const int p = grp + j * kSmGroups;
+    const bool ok = active && p < a.nparts;
+    v[j] = ok ? __ldcg(reinterpret_cast<const float4*>(src + p * a.acc_stride)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    mp[j] = ok ? a.m_part[p * a.m_stride + static_cast<long>(s) * a.m_rowstride] : 0.f;
+  }
+  if (warp <= s1 - s0) {
+    float m, l;
+    int vs;
+    row_stats(a3, s0 + warp, lane, m, vs, l);
+    if (lane == 0) {
+      s_m[warp] = m;
+      s_w[warp] = a.alpha_t / l;
+    }
+  }
+  __syncthreads();
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if (active) {
-    const float m = a.ml[2 * s];
-    const float* src = a.acc + static_cast<long>(s) * a.H + h;
-    constexpr int kBatch = 8;
-    for (int p0 = grp; p0 < a.nparts; p0 += kBatch * kK4Groups) {
-      float4 v[kBatch];
-      float sc[kBatch];
+    const float m = s_m[s - s0];
+    for (int p0 = 0;; p0 += kSmBatch * kSmGroups) {
 #pragma unroll
-      for (int j = 0; j < kBatch; ++j) {
-        const int p = p0 + j * kK4Groups;
-        v[j] = (p < a.nparts) ? __ldcg(reinterpret_cast<const float4*>(src + p * a.acc_stride))
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
-        sc[j] = (a.m_part == nullptr || p >= a.nparts)
-                    ? 1.f
-                    : expf(a.m_part[p * a.m_stride + static_cast<long>(s) * a.m_rowstride] - m);
+      for (int j = 0; j < kSmBatch; ++j) {  // fixed summation order
+        const int p = grp + p0 + j * kSmGroups;
+        const float sc = (p < a.nparts) ? expf(mp[j] - m) : 0.f;
+        acc.x = fmaf(v[j].x, sc, acc.x);
+        acc.y = fmaf(v[j].y, sc, acc.y);
+        acc.z = fmaf(v[j].z, sc, acc.z);
+        acc.w = fmaf(v[j].w, sc, acc.w);
       }
+      if (grp + p0 + kSmBatch * kSmGroups >= a.nparts) break;
 #pragma unroll
-      for (int j = 0; j < kBatch; ++j) {  // fixed summation order
-        acc.x = fmaf(v[j].x, sc[j], acc.x);
-        acc.y = fmaf(v[j].y, sc[j], acc.y);
-        acc.z = fmaf(v[j].z, sc[j], acc.z);
-        acc.w = fmaf(v[j].w, sc[j], acc.w);
+      for (int j = 0; j < kSmBatch; ++j) {
+        const int p = grp + p0 + kSmBatch * kSmGroups + j * kSmGroups;
+        const bool ok = p < a.nparts;
+        v[j] = ok ? __ldcg(reinterpret_cast<const float4*>(src + p * a.acc_stride)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        mp[j] = ok ? a.m_part[p * a.m_stride + static_cast<long>(s) * a.m_rowstride] : 0.f;
       }
     }
   }
   red[grp][cl] = acc;
   __syncthreads();
   if (grp != 0 || !active) return;
-  for (int g = 1; g < kK4Groups; ++g) {
+  for (int g = 1; g < kSmGroups; ++g) {
     const float4 r = red[g][cl];
-    acc.x += r.x; acc.y += r.y; acc.z += r.z; acc.w += r.w;
+    acc.x += r.x;
+    acc.y += r.y;
+    acc.z += r.z;
+    acc.w += r.w;
   }
-  const float w = a.alpha_t / a.ml[2 * s + 1];
+  const float w = s_w[s - s0];
   const uint2 em = *reinterpret_cast<const uint2*>(a.e_mask + h);
   const __nv_bfloat162 e01 = *reinterpret_cast<const __nv_bfloat162*>(&em.x);
   const __nv_bfloat162 e23 = *reinterpret_cast<const __nv_bfloat162*>(&em.y);
@@ -318,27 +352,38 @@ __global__ void __launch_bounds__(kK4Cols * kK4Groups) k4_smooth_finalize(const 
   o.y = fmaf(w, acc.y, __high2float(e01));
   o.z = fmaf(w, acc.z, __low2float(e23));
   o.w = fmaf(w, acc.w, __high2float(e23));
-  *reinterpret_cast<float4*>(a.out + static_cast<long>(s) * a.H + h) = o;
+  *reinterpret_cast<float4*>(a.out + e) = o;
+}
+
+// K3+K4 in one launch: blocks [0, B) select/commit batch rows, blocks >= B
+// (only with smoothing) write the smoothed embeddings.  Both read only what
+// K1 / K2 / the allgather produced (plus the step-start mask snapshot).
+__global__ void __launch_bounds__(kK3Threads) k34_select_smooth(const K3Args a3, const K4Args a4) {
+  grid_dep_wait();  // K1 / K2 / allgather results visible
+  grid_dep_launch_dependents();
+  if (static_cast<int>(blockIdx.x) < a3.B) {
+    select_block(a3, blockIdx.x);
+  } else {
+    smooth_block(a3, a4, blockIdx.x - a3.B);
+  }
 }
 
 }  // namespace
 
-cudaError_t launch_k3(const K3Args& a, cudaStream_t st, bool pdl) {
+cudaError_t launch_k34(const K3Args& a3, const K4Args* a4, cudaStream_t st, bool pdl) {
   static bool configured = false;
   if (!configured) {  // same smem carveout as K1/K2 (no L1/smem reconfiguration between kernels)
-    cudaError_t e = cudaFuncSetAttribute(k3_select_commit, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k4_smooth_finalize, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaError_t e = cudaFuncSetAttribute(k34_select_smooth, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  return launch_ex(k3_select_commit, dim3(a.B), dim3(kK3Threads), 0, st, pdl, a);
-}
-
-cudaError_t launch_k4(const K4Args& a, cudaStream_t st, bool pdl) {
-  const long n = static_cast<long>(a.M) * (a.H / 4);
-  const int blocks = static_cast<int>((n + kK4Cols - 1) / kK4Cols);
-  return launch_ex(k4_smooth_finalize, dim3(blocks), dim3(kK4Cols * kK4Groups), 0, st, pdl, a);
+  int nsm = 0;
+  K4Args f{};
+  if (a4 != nullptr) {
+    f = *a4;
+    nsm = static_cast<int>((static_cast<long>(f.M) * f.H / 4 + kSmCols - 1) / kSmCols);
+  }
+  return launch_ex(k34_select_smooth, dim3(a3.B + nsm), dim3(kK3Threads), 0, st, pdl, a3, f);
 }
 
 }  // namespace dinfer

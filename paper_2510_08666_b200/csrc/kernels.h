@@ -49,6 +49,7 @@ struct K1Args {
   unsigned* grp_cnt;       // [VG] slabs completed per group (K2 waits, resets), or nullptr
   float* rec;              // [M][4+K] rank record: only fcred (captured credited logits) is written
   float* flog;             // [M][V_local] raw logits for K2, or nullptr
+  uint8_t* mask_snap;      // [M] copy of the step-start mask (written by CTA 0), or nullptr
   int* err;
   unsigned long long* trace;  // optional [grid][5]: globaltimer ns start, first W stage, last tile done, exit; smid
 };
@@ -119,7 +120,7 @@ struct K3Args {
   float tau, theta_hi, theta_lo, c_alpha, c_beta, c_gamma;
   int* err;
 };
-cudaError_t launch_k3(const K3Args& a, cudaStream_t st, bool pdl);
+
 
 // ---------------------------------------------------------------- K4
 struct K4Args {
@@ -130,12 +131,12 @@ struct K4Args {
   const float* m_part;     // m of partial p, row s at m_part[p*m_stride + s*m_rowstride]; nullptr = scale 1
   long m_stride;
   int m_rowstride;
-  const float* ml;         // [M][2] merged (m, l)
-  const uint8_t* mask;     // [M] after commit
+  const uint8_t* mask_start;  // [M] mask at step start (snapshot; the selection blocks rewrite `mask`)
   const uint16_t* e_mask;  // [H] bf16
   float alpha_t;
   float* out;              // [M][H]
 };
-cudaError_t launch_k4(const K4Args& a, cudaStream_t st, bool pdl);
+// K3 + K4 in one launch (a4 == nullptr: selection only)
+cudaError_t launch_k34(const K3Args& a3, const K4Args* a4, cudaStream_t st, bool pdl);
 
 }  // namespace dinfer

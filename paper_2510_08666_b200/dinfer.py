@@ -16,8 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libdinfer.so")
 
 DEC_THRESHOLD = 0
 DEC_HIERARCHICAL = 1
-PHASES = ("k1_vocab_proj", "k2_smooth_mix", "k2r_acc_reduce", "c1_allgather", "k3_select_commit",
-          "k4_smooth_finalize")
+PHASES = ("k1_vocab_proj", "k2_smooth_mix", "rec_finalize", "c1_allgather", "k34_select_smooth", "unused")
 
 STATUS = {0: "ok", 1: "ERR_ARG", 2: "ERR_SHAPE", 3: "ERR_CUDA", 4: "ERR_NCCL", 5: "ERR_NOMEM",
           6: "ERR_UNSUPPORTED", 7: "ERR_DEVICE"}
