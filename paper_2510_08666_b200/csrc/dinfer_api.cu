@@ -65,13 +65,9 @@ struct dinfer_ctx {
   size_t stats_words = 0, full_words = 0;
   // staging for dinfer_step_host (device)
   uint16_t* st_hidden = nullptr;
-  uint8_t* st_mask = nullptr;
-  int32_t* st_tokens = nullptr;
-  int32_t* st_cids = nullptr;
-  float* st_cval = nullptr;
-  uint8_t* st_committed = nullptr;
+  uint8_t* st_block = nullptr;  // device: mask | tokens | credit ids | credit vals | committed | stats
+  uint8_t* st_host = nullptr;   // pinned host mirror of st_block
   float* st_smoothed = nullptr;
-  float* st_stats = nullptr;
   // tensor-map cache
   const void* c_w = nullptr;
   const void* c_h = nullptr;
@@ -412,11 +408,11 @@ void dinfer_destroy(dinfer_ctx* c) {
   void* bufs[] = {c->part1, c->counter, c->err, c->rec_local, c->flog, c->part2, c->ml, c->trace, c->mref,
                   c->mask_snap,
                   c->grp_cnt, c->grp_pass,
-                  c->st_hidden, c->st_mask, c->st_tokens, c->st_cids, c->st_cval, c->st_committed,
-                  c->st_smoothed, c->st_stats};
+                  c->st_hidden, c->st_block, c->st_smoothed};
   for (void* b : bufs)
     if (b != nullptr) cudaFree(b);
   if (c->rec_all != nullptr && c->rec_all != c->rec_local) cudaFree(c->rec_all);
+  if (c->st_host != nullptr) cudaFreeHost(c->st_host);
   for (int i = 0; i < kNumPhases; ++i) {
     if (c->ev_beg[i]) cudaEventDestroy(c->ev_beg[i]);
     if (c->ev_end[i]) cudaEventDestroy(c->ev_end[i]);
@@ -703,41 +699,54 @@ dinfer_status dinfer_step_host(dinfer_ctx* c, const uint16_t* hidden_h, const ui
   if (p->use_credit && (cids_h == nullptr || cval_h == nullptr)) return DINFER_ERR_ARG;
   if (p->use_smooth && smoothed_h == nullptr) return DINFER_ERR_ARG;
   const size_t M = static_cast<size_t>(c->M), H = static_cast<size_t>(c->shp.H), K = static_cast<size_t>(c->shp.K);
-  if (c->st_hidden == nullptr) {  // first call: staging buffers (not in the graph-capturable path)
+  // One device block + one pinned host mirror for the small per-step state, so
+  // the step moves it with one H2D and one D2H copy (hidden and smoothed go
+  // directly between the caller's buffers and the device).
+  auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+  const size_t o_mask = 0, o_tok = al(M), o_cid = o_tok + 4 * M, o_cval = o_cid + 4 * M * K,
+               o_com = o_cval + 4 * M * K, o_stats = al(o_com + M), total = o_stats + 16 * M;
+  if (c->st_hidden == nullptr) {  // first call (not in the graph-capturable path)
     dinfer_status st = DINFER_OK;
     auto A = [&](dinfer_status x) { if (st == DINFER_OK) st = x; };
     A(dev_alloc(&c->st_hidden, M * H));
-    A(dev_alloc(&c->st_mask, M));
-    A(dev_alloc(&c->st_tokens, M));
-    A(dev_alloc(&c->st_cids, M * K));
-    A(dev_alloc(&c->st_cval, M * K));
-    A(dev_alloc(&c->st_committed, M));
-    A(dev_alloc(&c->st_stats, M * 4));
+    A(dev_alloc(&c->st_block, total));
     if (c->shp.smooth_capable) A(dev_alloc(&c->st_smoothed, M * H));
+    if (st == DINFER_OK && cudaMallocHost(reinterpret_cast<void**>(&c->st_host), total) != cudaSuccess)
+      st = DINFER_ERR_NOMEM;
     if (st != DINFER_OK) return st;
+  }
+  uint8_t* d = c->st_block;
+  uint8_t* hs = c->st_host;
+  std::memcpy(hs + o_mask, mask_h, M);
+  std::memcpy(hs + o_tok, tokens_h, 4 * M);
+  if (p->use_credit) {
+    std::memcpy(hs + o_cid, cids_h, 4 * M * K);
+    std::memcpy(hs + o_cval, cval_h, 4 * M * K);
   }
   cudaStream_t sm = c->stream;
   DI_CUDA(cudaMemcpyAsync(c->st_hidden, hidden_h, M * H * 2, cudaMemcpyHostToDevice, sm));
-  DI_CUDA(cudaMemcpyAsync(c->st_mask, mask_h, M, cudaMemcpyHostToDevice, sm));
-  DI_CUDA(cudaMemcpyAsync(c->st_tokens, tokens_h, M * 4, cudaMemcpyHostToDevice, sm));
-  if (p->use_credit) {
-    DI_CUDA(cudaMemcpyAsync(c->st_cids, cids_h, M * K * 4, cudaMemcpyHostToDevice, sm));
-    DI_CUDA(cudaMemcpyAsync(c->st_cval, cval_h, M * K * 4, cudaMemcpyHostToDevice, sm));
-  }
-  dinfer_status s = dinfer_step(c, c->st_hidden, W, E, e_mask, c->st_mask, c->st_tokens,
-                                p->use_credit ? c->st_cids : nullptr, p->use_credit ? c->st_cval : nullptr, p,
-                                c->st_committed, p->use_smooth ? c->st_smoothed : nullptr, c->st_stats);
+  DI_CUDA(cudaMemcpyAsync(d, hs, p->use_credit ? o_com : o_cid, cudaMemcpyHostToDevice, sm));
+  auto* dmask = d + o_mask;
+  auto* dtok = reinterpret_cast<int32_t*>(d + o_tok);
+  auto* dcid = reinterpret_cast<int32_t*>(d + o_cid);
+  auto* dcval = reinterpret_cast<float*>(d + o_cval);
+  auto* dcom = d + o_com;
+  auto* dstats = reinterpret_cast<float*>(d + o_stats);
+  dinfer_status s = dinfer_step(c, c->st_hidden, W, E, e_mask, dmask, dtok, p->use_credit ? dcid : nullptr,
+                                p->use_credit ? dcval : nullptr, p, dcom, p->use_smooth ? c->st_smoothed : nullptr,
+                                dstats);
   if (s != DINFER_OK) return s;
-  DI_CUDA(cudaMemcpyAsync(mask_h, c->st_mask, M, cudaMemcpyDeviceToHost, sm));
-  DI_CUDA(cudaMemcpyAsync(tokens_h, c->st_tokens, M * 4, cudaMemcpyDeviceToHost, sm));
-  DI_CUDA(cudaMemcpyAsync(committed_h, c->st_committed, M, cudaMemcpyDeviceToHost, sm));
-  if (p->use_credit) {
-    DI_CUDA(cudaMemcpyAsync(cids_h, c->st_cids, M * K * 4, cudaMemcpyDeviceToHost, sm));
-    DI_CUDA(cudaMemcpyAsync(cval_h, c->st_cval, M * K * 4, cudaMemcpyDeviceToHost, sm));
-  }
+  DI_CUDA(cudaMemcpyAsync(hs, d, total, cudaMemcpyDeviceToHost, sm));
   if (p->use_smooth) DI_CUDA(cudaMemcpyAsync(smoothed_h, c->st_smoothed, M * H * 4, cudaMemcpyDeviceToHost, sm));
-  if (stats_h != nullptr) DI_CUDA(cudaMemcpyAsync(stats_h, c->st_stats, M * 16, cudaMemcpyDeviceToHost, sm));
   DI_CUDA(cudaStreamSynchronize(sm));
+  std::memcpy(mask_h, hs + o_mask, M);
+  std::memcpy(tokens_h, hs + o_tok, 4 * M);
+  std::memcpy(committed_h, hs + o_com, M);
+  if (p->use_credit) {
+    std::memcpy(cids_h, hs + o_cid, 4 * M * K);
+    std::memcpy(cval_h, hs + o_cval, 4 * M * K);
+  }
+  if (stats_h != nullptr) std::memcpy(stats_h, hs + o_stats, 16 * M);
   return DINFER_OK;
 }
 
