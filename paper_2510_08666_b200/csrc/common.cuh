@@ -173,6 +173,19 @@ DI uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) 
   return d;
 }
 
+// Same descriptor with an explicit layout type (2 = SWIZZLE_128B,
+// 4 = SWIZZLE_64B, 6 = SWIZZLE_32B).  K-major SWIZZLE_64B: 64-B rows,
+// 8-row atoms of 512 B (SBO = 512).
+DI uint64_t sdesc_swz(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes, uint32_t layout) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= 1ull << 46;
+  d |= static_cast<uint64_t>(layout & 7u) << 61;
+  return d;
+}
+
 // Instruction descriptor, kind::f16: A = B = bf16, D = fp32.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn_major, bool b_mn_major) {
   return (1u << 4)                                   // D format fp32

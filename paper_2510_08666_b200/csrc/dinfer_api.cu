@@ -45,7 +45,7 @@ struct dinfer_ctx {
   int kb_grid = 0, kb_stages = 0, kb_VG = 0;
   size_t kb_smem = 0;
   size_t k1_smem = 0;
-  int k2_HW = 0, k2_HS = 0, k2_VG = 0, k2_stages = 0, k2_pstages = 0, k2_nchunks = 0;
+  int k2_HW = 0, k2_HS = 0, k2_VG = 0, k2_stages = 0, k2_pstages = 0, k2_nchunks = 0, k2_KV = 64;
   size_t k2_smem = 0;
   // workspace (device)
   float* part1 = nullptr;
@@ -192,7 +192,8 @@ dinfer_status ensure_maps(dinfer_ctx* c, const uint16_t* hidden, const uint16_t*
     c->c_h = hidden;
   }
   if (E != nullptr && E != c->c_e) {
-    if (!encode_2d(&c->map_e, E, H, static_cast<uint64_t>(c->shp.V_local), 64, kKChunk)) return DINFER_ERR_CUDA;
+    if (!encode_2d(&c->map_e, E, H, static_cast<uint64_t>(c->shp.V_local), 64, static_cast<uint32_t>(c->k2_KV)))
+      return DINFER_ERR_CUDA;
     c->c_e = E;
   }
   return DINFER_OK;
@@ -221,7 +222,8 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
   a.credit_ids = p->use_credit ? credit_ids : nullptr;
   a.VG = c->k1_VG;
   a.SPG = c->k1_SPG;
-  a.nchunks = static_cast<int>((c->shp.V_local + kKChunk - 1) / kKChunk);
+  a.nchunks = static_cast<int>((c->shp.V_local + c->k2_KV - 1) / c->k2_KV);
+  a.chunk_rows = c->k2_KV;
   a.part = c->part1;
   a.grp_cnt = smooth ? c->grp_cnt : nullptr;  // K2 consumes the group counts
   a.rec = rec;
@@ -243,6 +245,7 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
     b.HS = c->k2_HS;
     b.VG = c->k2_VG;
     b.nchunks = c->k2_nchunks;
+    b.KV = c->k2_KV;
     b.stages = c->k2_stages;
     b.pstages = c->k2_pstages;
     b.flog = c->flog;
@@ -468,30 +471,35 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
     // hidden slice that divides H (512 columns: 1 KB contiguous E row segments,
     // 4 x 37 = 148 CTAs at H = 2048; measured 131 us vs 165 us with 256), then
     // the deepest E ring (>= 2 stages) with logits/P rings of >= 2 stages.
-    c->k2_nchunks = static_cast<int>((s.V_local + kKChunk - 1) / kKChunk);
-    int hw_pref = 512;
-    if (const char* e = std::getenv("DINFER_K2_HW")) hw_pref = std::atoi(e);  // tuning override: 128 / 256 / 512
+    // Slices of 1024 columns (2 KB contiguous per E row) use 32-row vocab
+    // chunks (64 KB E stages, SWIZZLE_64B P tiles); narrower slices 64-row
+    // chunks.  The accumulator (HW/128 x N columns) must fit the 512-column TMEM.
+    int hw_pref = 1024;
+    if (const char* e = std::getenv("DINFER_K2_HW")) hw_pref = std::atoi(e);  // tuning override: 128 .. 1024
     c->k2_stages = 0;
-    for (int hw = 512; hw >= 128 && c->k2_stages == 0; hw /= 2) {
-      if (hw > hw_pref || s.H % hw != 0) continue;
+    for (int hw = 1024; hw >= 128 && c->k2_stages == 0; hw /= 2) {
+      if (hw > hw_pref || s.H % hw != 0 || (hw / 128) * c->N > 512) continue;
+      const int kv = hw == 1024 ? 32 : 64;
       for (int pst = 4; pst >= 1 && c->k2_stages == 0; --pst)  // depth 1 only for very large M
         for (int st = 6; st >= 2; --st)
-          if (k2_smem_bytes(c->N, hw, st, pst) <= c->smem_optin) {
+          if (k2_smem_bytes(c->N, hw, kv, st, pst) <= c->smem_optin) {
             c->k2_HW = hw;
+            c->k2_KV = kv;
             c->k2_pstages = pst;
             c->k2_stages = st;
             break;
           }
     }
+    c->k2_nchunks = static_cast<int>((s.V_local + c->k2_KV - 1) / c->k2_KV);
     if (c->k2_stages == 0) { delete c; return DINFER_ERR_UNSUPPORTED; }
     c->k2_HS = s.H / c->k2_HW;
     c->k2_VG = std::max(1, std::min(c->num_sms / std::max(1, c->k2_HS), c->k2_nchunks));
-    c->k2_smem = k2_smem_bytes(c->N, c->k2_HW, c->k2_stages, c->k2_pstages);
+    c->k2_smem = k2_smem_bytes(c->N, c->k2_HW, c->k2_KV, c->k2_stages, c->k2_pstages);
     // ---- K1 geometry: one CTA per SM over contiguous vocab slabs.  With the
     // smoothing workspace the slabs nest in K2's vocab groups (SPG slabs per
     // group, group boundaries on 64-row chunks) so a K2 CTA depends only on
     // its group's slabs; each slab is balanced at 8-row granularity.
-    const int nch = static_cast<int>((s.V_local + kKChunk - 1) / kKChunk);
+    const int nch = static_cast<int>((s.V_local + c->k2_KV - 1) / c->k2_KV);
     if (s.smooth_capable) {
       c->k1_VG = c->k2_VG;
       const long grp_rows = (s.V_local + c->k1_VG - 1) / c->k1_VG;
@@ -504,8 +512,8 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
     c->k1_grid = c->k1_VG * c->k1_SPG;
     c->slab_rows_max = 0;
     for (int g = 0; g < c->k1_VG; ++g) {  // same arithmetic as the kernel
-      const long rg0 = static_cast<long>(kKChunk) * (static_cast<long>(g) * nch / c->k1_VG);
-      const long rg1 = std::min<long>(s.V_local, static_cast<long>(kKChunk) * (static_cast<long>(g + 1) * nch / c->k1_VG));
+      const long rg0 = static_cast<long>(c->k2_KV) * (static_cast<long>(g) * nch / c->k1_VG);
+      const long rg1 = std::min<long>(s.V_local, static_cast<long>(c->k2_KV) * (static_cast<long>(g + 1) * nch / c->k1_VG));
       const long n8 = (rg1 - rg0) / kRowGran;
       for (int q = 0; q < c->k1_SPG; ++q) {
         const long rows = kRowGran * ((q + 1) * n8 / c->k1_SPG - q * n8 / c->k1_SPG);
@@ -562,7 +570,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
       st = DINFER_ERR_CUDA;
   }
   if (st == DINFER_OK && s.smooth_capable &&
-      !encode_2d_f32(&c->map_f, c->flog, static_cast<uint64_t>(s.V_local), static_cast<uint64_t>(M), kKChunk,
+      !encode_2d_f32(&c->map_f, c->flog, static_cast<uint64_t>(s.V_local), static_cast<uint64_t>(M), c->k2_KV,
                      static_cast<uint32_t>(c->N)))
     st = DINFER_ERR_CUDA;
   for (int i = 0; i < kNumPhases && st == DINFER_OK; ++i) {

@@ -125,8 +125,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // groups on 64-row chunk boundaries (K2's vocab groups) and each group into
   // SPG slabs balanced at 8-row granularity; slab = blockIdx.x.
   const int grp = blockIdx.x / a.SPG, q = blockIdx.x - grp * a.SPG;
-  const int rg0 = kKChunk * static_cast<int>(static_cast<long>(grp) * a.nchunks / a.VG);
-  const int rg1 = min(a.V_local, kKChunk * static_cast<int>(static_cast<long>(grp + 1) * a.nchunks / a.VG));
+  const int rg0 = a.chunk_rows * static_cast<int>(static_cast<long>(grp) * a.nchunks / a.VG);
+  const int rg1 = min(a.V_local, a.chunk_rows * static_cast<int>(static_cast<long>(grp + 1) * a.nchunks / a.VG));
   const int n8 = (rg1 - rg0) / kRowGran;
   const int r0 = rg0 + kRowGran * static_cast<int>(static_cast<long>(q) * n8 / a.SPG);
   const int r1 = rg0 + kRowGran * static_cast<int>(static_cast<long>(q + 1) * n8 / a.SPG);

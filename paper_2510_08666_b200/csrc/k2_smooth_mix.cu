@@ -29,7 +29,6 @@ namespace {
 
 constexpr int kEpiWarps = 4;
 constexpr int kThreads = (kEpiWarps + 3) * kWarpThreads;  // + E TMA, MMA, logits TMA
-constexpr uint32_t kEBox = 64u * 64u * 2u;                // [64 h x 64 v] bf16 = 8 KB
 
 __host__ __device__ inline uint32_t tmem_cols_pow2(uint32_t n) {
   uint32_t c = 32;
@@ -40,11 +39,11 @@ __host__ __device__ inline uint32_t tmem_cols_pow2(uint32_t n) {
 struct Layout {
   uint32_t e_off, f_off, p_off, bar_off, misc_off, m_off, total;
 };
-__host__ __device__ inline Layout make_layout(int N, int HW, int stages, int pstages) {
+__host__ __device__ inline Layout make_layout(int N, int HW, int KV, int stages, int pstages) {
   Layout L;
-  const uint32_t e_stage = static_cast<uint32_t>(HW) * 128u;     // HW/64 boxes of 8 KB
-  const uint32_t f_stage = static_cast<uint32_t>(N) * 256u;      // [N x 64] fp32
-  const uint32_t p_stage = 2u * static_cast<uint32_t>(N) * 128u;  // hi + lo [N x 64] bf16
+  const uint32_t e_stage = static_cast<uint32_t>(HW * KV) * 2u;      // HW/64 boxes of [64 h x KV v]
+  const uint32_t f_stage = static_cast<uint32_t>(N * KV) * 4u;       // [N x KV] fp32
+  const uint32_t p_stage = 2u * static_cast<uint32_t>(N * KV) * 2u;  // hi + lo [N x KV] bf16
   L.e_off = 0;
   L.f_off = L.e_off + static_cast<uint32_t>(stages) * e_stage;
   L.p_off = L.f_off + static_cast<uint32_t>(pstages) * f_stage;
@@ -72,13 +71,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const K2Args a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const Layout L = make_layout(a.N, a.HW, a.stages, a.pstages);
+  const Layout L = make_layout(a.N, a.HW, a.KV, a.stages, a.pstages);
   const int warp = threadIdx.x / kWarpThreads;
   const int lane = threadIdx.x % kWarpThreads;
   const int N = a.N;
-  const uint32_t e_stage = static_cast<uint32_t>(a.HW) * 128u;
-  const uint32_t f_stage = static_cast<uint32_t>(N) * 256u;
-  const uint32_t p_half = static_cast<uint32_t>(N) * 128u;
+  const int KV = a.KV;                          // vocab rows per chunk: 64 (P in SW128) or 32 (SW64)
+  const uint32_t ebox = 128u * static_cast<uint32_t>(KV);   // [64 h x KV v] bf16
+  const uint32_t e_stage = static_cast<uint32_t>(a.HW) * 2u * static_cast<uint32_t>(KV);
+  const uint32_t f_stage = static_cast<uint32_t>(N * KV) * 4u;
+  const uint32_t p_row = 2u * static_cast<uint32_t>(KV);    // bytes per P row (128 or 64)
+  const uint32_t p_half = static_cast<uint32_t>(N) * p_row;
 
   uint8_t* e_sm = smem + L.e_off;
   uint8_t* f_sm = smem + L.f_off;
@@ -137,8 +139,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&eempty[stage], phase ^ 1u);
         mbar_expect_tx(&efull[stage], e_stage);
         for (int b = 0; b < a.HW / 64; ++b)
-          tma_load_2d(e_sm + stage * e_stage + b * kEBox, &map_e, &efull[stage], hs * a.HW + b * 64, c * kKChunk,
-                      pol);
+          tma_load_2d(e_sm + stage * e_stage + b * ebox, &map_e, &efull[stage], hs * a.HW + b * 64, c * KV, pol);
         advance(stage, phase, a.stages);
       }
     }
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&fempty[stage], phase ^ 1u);
         mbar_expect_tx(&ffull[stage], f_stage);
         // f[0:N, c*64 : c*64+64]; rows >= M and columns >= V_local zero-filled
-        tma_load_2d(f_sm + stage * f_stage, &map_f, &ffull[stage], c * kKChunk, 0, pol);
+        tma_load_2d(f_sm + stage * f_stage, &map_f, &ffull[stage], c * KV, 0, pol);
         advance(stage, phase, a.pstages);
       }
     }
@@ -189,13 +190,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t e_addr = smem_u32(e_sm + es * e_stage);
         const uint32_t phi = smem_u32(p_sm + ps * 2 * p_half);
         const uint32_t plo = phi + p_half;
-#pragma unroll
-        for (int k = 0; k < kKChunk / 16; ++k) {
-          const uint64_t bhi = sdesc_sw128(phi + k * 32, 16, 1024);
-          const uint64_t blo = sdesc_sw128(plo + k * 32, 16, 1024);
+        const uint32_t play = (KV == 64) ? 2u : 4u, psbo = 8u * p_row;  // SW128 / SW64 K-major
+        for (int k = 0; k < KV / 16; ++k) {
+          const uint64_t bhi = sdesc_swz(phi + k * 32, 16, psbo, play);
+          const uint64_t blo = sdesc_swz(plo + k * 32, 16, psbo, play);
           for (int sub = 0; sub < a.nsub; ++sub) {
             // A: [128 h x 16 v] = two 64-h blocks 8 KB apart (LBO), 8-v groups 1 KB apart (SBO)
-            const uint64_t ad = sdesc_sw128(e_addr + sub * 2 * kEBox + k * 16 * 128, kEBox, 1024);
+            const uint64_t ad = sdesc_sw128(e_addr + sub * 2 * ebox + k * 16 * 128, ebox, 1024);
             const uint32_t d = tmem_base + static_cast<uint32_t>(sub * N);
             mma_bf16(d, ad, bhi, idesc, (c > c0 || k > 0) ? 1u : 0u);
             mma_bf16(d, ad, blo, idesc, 1u);
@@ -240,12 +241,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float* fch = reinterpret_cast<const float*>(f_sm + ps * f_stage);
       uint8_t* phi = p_sm + ps * 2 * p_half;
       uint8_t* plo = phi + p_half;
-      for (int u = tid; u < N * 8; u += kEpiWarps * kWarpThreads) {
-        const int s = u >> 3, cc = u & 7;
-        const int v0 = c * kKChunk + cc * 8;
+      const int cpr = KV / 8;  // 16-B chunks per P row
+      for (int u = tid; u < N * cpr; u += kEpiWarps * kWarpThreads) {
+        const int s = u / cpr, cc = u - s * cpr;
+        const int v0 = c * KV + cc * 8;
         float p[8];
         if (s < a.M && v0 < a.V_local) {
-          const float4* src = reinterpret_cast<const float4*>(fch + s * kKChunk + cc * 8);
+          const float4* src = reinterpret_cast<const float4*>(fch + s * KV + cc * 8);
           const float4 q0 = src[0], q1 = src[1];
           const float ms = m_sm[s];
           p[0] = fexp(q0.x - ms); p[1] = fexp(q0.y - ms); p[2] = fexp(q0.z - ms); p[3] = fexp(q0.w - ms);
@@ -261,7 +263,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     pack_bf16x2(p[6], p[7]));
         const uint4 lo = make_uint4(pack_bf16x2(r[0], r[1]), pack_bf16x2(r[2], r[3]), pack_bf16x2(r[4], r[5]),
                                     pack_bf16x2(r[6], r[7]));
-        const uint32_t off = static_cast<uint32_t>(s) * 128u + ((static_cast<uint32_t>(cc) ^ (s & 7u)) << 4);
+        // manual swizzle = the TMA/UMMA pattern: 16-B chunk index XOR address bits [7,10) (SW128) / [7,9) (SW64)
+        const uint32_t swz = (KV == 64) ? (s & 7u) : ((s >> 1) & 3u);
+        const uint32_t off = static_cast<uint32_t>(s) * p_row + ((static_cast<uint32_t>(cc) ^ swz) << 4);
         *reinterpret_cast<uint4*>(phi + off) = hi;
         *reinterpret_cast<uint4*>(plo + off) = lo;
       }
@@ -276,6 +280,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(accfull, 0);
       tc_fence_after();
     }
+    // TMEM [128 h lanes x 32 s] -> smem tile [32 s][128 h] (the idle E ring)
+    // -> coalesced float4 rows of the [M][H] partial.
+    float* tile = reinterpret_cast<float*>(e_sm);
     for (int sub = 0; sub < a.nsub; ++sub) {
       for (int g = 0; g < N / 32; ++g) {
         float x[32];
@@ -285,12 +292,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) x[j] = 0.f;
         }
-        const int h = hbase + sub * 128 + warp * 32 + lane;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int s = g * 32 + j;
-          if (s < a.M) a.part[(static_cast<long>(vg) * a.M + s) * a.H + h] = x[j];
+        for (int j = 0; j < 32; ++j) tile[j * 128 + warp * 32 + lane] = x[j];
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * kWarpThreads) : "memory");
+        for (int q = threadIdx.x; q < 32 * 32; q += kEpiWarps * kWarpThreads) {
+          const int row = q >> 5, c4 = q & 31;
+          const int s = g * 32 + row;
+          if (s < a.M)
+            *reinterpret_cast<float4*>(a.part + (static_cast<long>(vg) * a.M + s) * a.H + hbase + sub * 128 + c4 * 4) =
+                *reinterpret_cast<const float4*>(tile + row * 128 + c4 * 4);
         }
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * kWarpThreads) : "memory");
       }
     }
   }
@@ -355,8 +367,8 @@ __global__ void rec_finalize_kernel(const RecArgs a) {
 
 }  // namespace
 
-size_t k2_smem_bytes(int N, int HW, int stages, int pstages) {
-  return make_layout(N, HW, stages, pstages).total + 1024;
+size_t k2_smem_bytes(int N, int HW, int KV, int stages, int pstages) {
+  return make_layout(N, HW, KV, stages, pstages).total + 1024;
 }
 
 cudaError_t launch_k2(const CUtensorMap& map_e, const CUtensorMap& map_f, const K2Args& a, size_t smem,

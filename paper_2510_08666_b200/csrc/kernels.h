@@ -44,7 +44,8 @@ struct K1Args {
   int slab_rows_max;       // max rows of any CTA's slab (credit head table size)
   const uint8_t* mask;     // [M]
   const int32_t* credit_ids;  // [M][K] or nullptr
-  int VG, SPG, nchunks;     // vocab groups (64-row chunk aligned) x slabs per group = grid
+  int VG, SPG, nchunks;     // vocab groups (K2-chunk aligned) x slabs per group = grid
+  int chunk_rows;          // K2 chunk rows (group boundaries are multiples of it)
   float* part;             // [M][grid] float4 per-CTA (m, idx, l, 0), column-major
   unsigned* grp_cnt;       // [VG] slabs completed per group (K2 waits, resets), or nullptr
   float* rec;              // [M][4+K] rank record: only fcred (captured credited logits) is written
@@ -71,9 +72,10 @@ cudaError_t launch_k1b(const CUtensorMap& map_h, const CUtensorMap& map_w, const
 // ---------------------------------------------------------------- K2
 struct K2Args {
   int M, N, H, V_local;
-  int HW, nsub;            // hidden columns per CTA (128 or 256), HW/128
+  int HW, nsub;            // hidden columns per CTA (128 .. 1024), HW/128
+  int KV;                  // vocab rows per chunk: 64 (P tile SW128) or 32 (SW64, for HW = 1024)
   int HS, VG;              // H/HW slices, vocab groups
-  int nchunks;             // ceil(V_local / 64)
+  int nchunks;             // ceil(V_local / KV)
   int stages, pstages;
   const float* flog;       // [M][V_local]
   const float4* part1;     // K1 partials [M][grid1]
@@ -84,7 +86,7 @@ struct K2Args {
   float* part;             // [VG][M][H]
   unsigned long long* trace;  // optional [grid][5]: globaltimer ns start, first E stage, MMAs done, exit; smid
 };
-size_t k2_smem_bytes(int N, int HW, int stages, int pstages);
+size_t k2_smem_bytes(int N, int HW, int KV, int stages, int pstages);
 cudaError_t launch_k2(const CUtensorMap& map_e, const CUtensorMap& map_f, const K2Args& a, size_t smem,
                       cudaStream_t st, bool pdl);
 

@@ -82,7 +82,7 @@ def test_ragged_tail_and_odd_shapes(torch_cuda):
     run_trajectory(torch_cuda, 1000, 384, 3, 20, 24, 5, hier_credit_smooth, True)
 
 
-@pytest.mark.parametrize("hw", ["128", "256", "512"])
+@pytest.mark.parametrize("hw", ["128", "256", "512", "1024"])
 def test_k2_slice_widths(torch_cuda, monkeypatch, hw):
     """The smoothing mix gives the same result for every hidden-slice width
     (DINFER_K2_HW tuning override): H = 1024, V = 4096."""
