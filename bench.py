@@ -323,8 +323,12 @@ def gpu_arm(args):
     cids_h, cval_h = pin(np.full((B, S, K), -1, np.int32)), pin(np.zeros((B, S, K), np.float32))
     com_h, st_h = pin(np.zeros((B, S), np.uint8)), pin(np.zeros((B, S, 4), np.float32))
     sm_h = pin(np.zeros((B, S, H), np.float32)) if smooth else None
-    h2d = M * H * 2 + M + 4 * M + (8 * M * K if credit else 0)
-    d2h = M + 4 * M + M + (8 * M * K if credit else 0) + (4 * M * H if smooth else 0) + 16 * M
+    # dinfer_step_host's packed state block (include/dinfer.h): params(32 B) | mask | tokens |
+    # credit ids | credit values | committed | stats; uploaded up to `committed`, read back whole
+    al = lambda x: (x + 15) & ~15
+    o_com = al(32 + M) + 4 * M + 8 * M * K
+    h2d = M * H * 2 + o_com
+    d2h = al(o_com + M) + 16 * M + (4 * M * H if smooth else 0)
     e2e_steps = max(3, min(args.steps, 50))
     e2e_ms = []
     for i in range(args.warmup + e2e_steps):

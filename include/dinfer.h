@@ -143,7 +143,19 @@ dinfer_status dinfer_step(dinfer_ctx* ctx, const uint16_t* hidden, const uint16_
 
 /* Same step with HOST per-step buffers (weights stay on device): copies
  * hidden and the decode state host->device, runs dinfer_step, copies the
- * state and outputs back, and synchronises the stream before returning.    */
+ * state and outputs back, and synchronises the stream before returning.
+ * Transfers: hidden (M*H*2 B) directly from hidden_h; the small state (the
+ * numeric params, mask, tokens, credit table) packed through one pinned
+ * staging block into one H2D copy; one D2H copy of the packed state +
+ * committed + stats; smoothed (M*H*4 B) directly into smoothed_h.
+ * On a single-rank ctx with timing off, the whole sequence (copies and
+ * kernels) is captured once into a CUDA graph and replayed; the numeric
+ * params (tau, theta_*, c_*, alpha_t) are read on device from the packed
+ * block, so schedules never force a re-capture. A change of any pointer
+ * argument or of decoder / hier_runs_after_hi / use_credit / use_smooth /
+ * stats_h nullness re-captures. Buffers the graph cannot capture (pageable
+ * host memory) run the same sequence un-captured. hidden_h and smoothed_h
+ * may be pageable; pinned buffers avoid a staging copy inside the driver. */
 dinfer_status dinfer_step_host(dinfer_ctx* ctx, const uint16_t* hidden_h,
                                const uint16_t* W_vocab, const uint16_t* E,
                                const uint16_t* e_mask, uint8_t* mask_h, int32_t* tokens_h,

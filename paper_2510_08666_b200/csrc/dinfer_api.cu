@@ -68,6 +68,13 @@ struct dinfer_ctx {
   uint8_t* st_block = nullptr;  // device: mask | tokens | credit ids | credit vals | committed | stats
   uint8_t* st_host = nullptr;   // pinned host mirror of st_block
   float* st_smoothed = nullptr;
+  // dinfer_step_host replays a captured CUDA graph of its whole sequence
+  cudaGraphExec_t host_graph = nullptr;
+  uint64_t host_graph_key[12] = {};
+  bool host_graph_failed = false;
+  cudaStream_t cap_stream = nullptr;  // private capture stream
+  bool host_graph_ok = true;           // env DINFER_HOST_GRAPH=0 disables the graph (measurement)
+  const float* pdev_active = nullptr;  // device params the kernels read (set while capturing)
   // tensor-map cache
   const void* c_w = nullptr;
   const void* c_h = nullptr;
@@ -312,6 +319,7 @@ dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, in
   k.c_alpha = p->c_alpha;
   k.c_beta = p->c_beta;
   k.c_gamma = p->c_gamma;
+  k.pdev = c->pdev_active;
   k.err = c->err;
   K4Args f{};
   if (p->use_smooth) {
@@ -416,6 +424,8 @@ void dinfer_destroy(dinfer_ctx* c) {
     if (b != nullptr) cudaFree(b);
   if (c->rec_all != nullptr && c->rec_all != c->rec_local) cudaFree(c->rec_all);
   if (c->st_host != nullptr) cudaFreeHost(c->st_host);
+  if (c->host_graph != nullptr) cudaGraphExecDestroy(c->host_graph);
+  if (c->cap_stream != nullptr) cudaStreamDestroy(c->cap_stream);
   for (int i = 0; i < kNumPhases; ++i) {
     if (c->ev_beg[i]) cudaEventDestroy(c->ev_beg[i]);
     if (c->ev_end[i]) cudaEventDestroy(c->ev_end[i]);
@@ -538,6 +548,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
 
     if (const char* e = std::getenv("DINFER_PDL")) c->pdl = std::atoi(e) != 0;
   }
+  if (const char* e = std::getenv("DINFER_HOST_GRAPH")) c->host_graph_ok = std::atoi(e) != 0;
 
   // ---- workspace
   c->stats_words = static_cast<size_t>(M) * (kStatWords + s.K);
@@ -711,7 +722,7 @@ dinfer_status dinfer_step_host(dinfer_ctx* c, const uint16_t* hidden_h, const ui
   // the step moves it with one H2D and one D2H copy (hidden and smoothed go
   // directly between the caller's buffers and the device).
   auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
-  const size_t o_mask = 0, o_tok = al(M), o_cid = o_tok + 4 * M, o_cval = o_cid + 4 * M * K,
+  const size_t o_par = 0, o_mask = 32, o_tok = al(o_mask + M), o_cid = o_tok + 4 * M, o_cval = o_cid + 4 * M * K,
                o_com = o_cval + 4 * M * K, o_stats = al(o_com + M), total = o_stats + 16 * M;
   if (c->st_hidden == nullptr) {  // first call (not in the graph-capturable path)
     dinfer_status st = DINFER_OK;
@@ -723,8 +734,13 @@ dinfer_status dinfer_step_host(dinfer_ctx* c, const uint16_t* hidden_h, const ui
       st = DINFER_ERR_NOMEM;
     if (st != DINFER_OK) return st;
   }
+  dinfer_status s = check_params(c, p);
+  if (s != DINFER_OK) return s;
   uint8_t* d = c->st_block;
   uint8_t* hs = c->st_host;
+  // per-step numeric parameters travel with the packed state (the graph reads them on device)
+  const float par[8] = {p->tau, p->theta_hi, p->theta_lo, p->c_alpha, p->c_beta, p->c_gamma, p->alpha_t, 0.f};
+  std::memcpy(hs + o_par, par, sizeof(par));
   std::memcpy(hs + o_mask, mask_h, M);
   std::memcpy(hs + o_tok, tokens_h, 4 * M);
   if (p->use_credit) {
@@ -732,20 +748,73 @@ dinfer_status dinfer_step_host(dinfer_ctx* c, const uint16_t* hidden_h, const ui
     std::memcpy(hs + o_cval, cval_h, 4 * M * K);
   }
   cudaStream_t sm = c->stream;
-  DI_CUDA(cudaMemcpyAsync(c->st_hidden, hidden_h, M * H * 2, cudaMemcpyHostToDevice, sm));
-  DI_CUDA(cudaMemcpyAsync(d, hs, p->use_credit ? o_com : o_cid, cudaMemcpyHostToDevice, sm));
-  auto* dmask = d + o_mask;
-  auto* dtok = reinterpret_cast<int32_t*>(d + o_tok);
-  auto* dcid = reinterpret_cast<int32_t*>(d + o_cid);
-  auto* dcval = reinterpret_cast<float*>(d + o_cval);
-  auto* dcom = d + o_com;
-  auto* dstats = reinterpret_cast<float*>(d + o_stats);
-  dinfer_status s = dinfer_step(c, c->st_hidden, W, E, e_mask, dmask, dtok, p->use_credit ? dcid : nullptr,
-                                p->use_credit ? dcval : nullptr, p, dcom, p->use_smooth ? c->st_smoothed : nullptr,
-                                dstats);
-  if (s != DINFER_OK) return s;
-  DI_CUDA(cudaMemcpyAsync(hs, d, total, cudaMemcpyDeviceToHost, sm));
-  if (p->use_smooth) DI_CUDA(cudaMemcpyAsync(smoothed_h, c->st_smoothed, M * H * 4, cudaMemcpyDeviceToHost, sm));
+  // graph key: everything baked into the captured sequence (pointers + structural flags)
+  const uint64_t key[12] = {reinterpret_cast<uint64_t>(hidden_h), reinterpret_cast<uint64_t>(W),
+                            reinterpret_cast<uint64_t>(E),        reinterpret_cast<uint64_t>(e_mask),
+                            reinterpret_cast<uint64_t>(smoothed_h), static_cast<uint64_t>(p->decoder),
+                            static_cast<uint64_t>(p->hier_runs_after_hi), static_cast<uint64_t>(p->use_credit),
+                            static_cast<uint64_t>(p->use_smooth), static_cast<uint64_t>(c->timing),
+                            static_cast<uint64_t>(stats_h != nullptr), 1};
+  // timing events / NCCL: plain enqueue; a key whose capture failed (e.g. pageable
+  // host buffers) also stays on the plain path
+  const bool same_key = std::memcmp(key, c->host_graph_key, sizeof(key)) == 0;
+  bool use_graph = !c->timing && c->shp.world == 1 && !(same_key && c->host_graph_failed) && c->host_graph_ok;
+  if (use_graph && (c->host_graph == nullptr || !same_key)) {
+    if (c->host_graph != nullptr) {
+      cudaGraphExecDestroy(c->host_graph);
+      c->host_graph = nullptr;
+    }
+    cudaGraph_t g = nullptr;
+    // capture on a private stream (the legacy default stream cannot be
+    // captured); the graph is launched on the ctx stream below
+    if (c->cap_stream == nullptr) DI_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+    const cudaStream_t user_stream = c->stream;
+    sm = c->cap_stream;
+    DI_CUDA(cudaStreamBeginCapture(sm, cudaStreamCaptureModeRelaxed));
+    c->stream = sm;
+    c->pdev_active = reinterpret_cast<const float*>(d + o_par);
+    bool ok = cudaMemcpyAsync(c->st_hidden, hidden_h, M * H * 2, cudaMemcpyHostToDevice, sm) == cudaSuccess &&
+              cudaMemcpyAsync(d, hs, o_com, cudaMemcpyHostToDevice, sm) == cudaSuccess;
+    dinfer_status st = DINFER_OK;
+    if (ok)
+      st = dinfer_step(c, c->st_hidden, W, E, e_mask, d + o_mask, reinterpret_cast<int32_t*>(d + o_tok),
+                       p->use_credit ? reinterpret_cast<int32_t*>(d + o_cid) : nullptr,
+                       p->use_credit ? reinterpret_cast<float*>(d + o_cval) : nullptr, p, d + o_com,
+                       p->use_smooth ? c->st_smoothed : nullptr, reinterpret_cast<float*>(d + o_stats));
+    c->pdev_active = nullptr;
+    ok = ok && st == DINFER_OK && cudaMemcpyAsync(hs, d, total, cudaMemcpyDeviceToHost, sm) == cudaSuccess;
+    if (ok && p->use_smooth)
+      ok = cudaMemcpyAsync(smoothed_h, c->st_smoothed, M * H * 4, cudaMemcpyDeviceToHost, sm) == cudaSuccess;
+    const cudaError_t ee = cudaStreamEndCapture(sm, &g);
+    c->stream = sm = user_stream;
+    if (st != DINFER_OK && st != DINFER_ERR_CUDA) {  // argument / shape error: report it, nothing ran
+      if (g != nullptr) cudaGraphDestroy(g);
+      cudaGetLastError();
+      return st;
+    }
+    std::memcpy(c->host_graph_key, key, sizeof(key));
+    c->host_graph_failed = !ok || ee != cudaSuccess || g == nullptr ||
+                           cudaGraphInstantiate(&c->host_graph, g, 0) != cudaSuccess;
+    if (g != nullptr) cudaGraphDestroy(g);
+    if (c->host_graph_failed) {
+      c->host_graph = nullptr;
+      cudaGetLastError();
+      use_graph = false;
+    }
+  }
+  if (use_graph) {
+    DI_CUDA(cudaGraphLaunch(c->host_graph, sm));
+  } else {
+    DI_CUDA(cudaMemcpyAsync(c->st_hidden, hidden_h, M * H * 2, cudaMemcpyHostToDevice, sm));
+    DI_CUDA(cudaMemcpyAsync(d, hs, p->use_credit ? o_com : o_cid, cudaMemcpyHostToDevice, sm));
+    s = dinfer_step(c, c->st_hidden, W, E, e_mask, d + o_mask, reinterpret_cast<int32_t*>(d + o_tok),
+                    p->use_credit ? reinterpret_cast<int32_t*>(d + o_cid) : nullptr,
+                    p->use_credit ? reinterpret_cast<float*>(d + o_cval) : nullptr, p, d + o_com,
+                    p->use_smooth ? c->st_smoothed : nullptr, reinterpret_cast<float*>(d + o_stats));
+    if (s != DINFER_OK) return s;
+    DI_CUDA(cudaMemcpyAsync(hs, d, total, cudaMemcpyDeviceToHost, sm));
+    if (p->use_smooth) DI_CUDA(cudaMemcpyAsync(smoothed_h, c->st_smoothed, M * H * 4, cudaMemcpyDeviceToHost, sm));
+  }
   DI_CUDA(cudaStreamSynchronize(sm));
   std::memcpy(mask_h, hs + o_mask, M);
   std::memcpy(tokens_h, hs + o_tok, 4 * M);

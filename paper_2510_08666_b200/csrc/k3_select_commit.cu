@@ -358,9 +358,20 @@ DI void smooth_block(const K3Args& a3, const K4Args& a, int blk) {
 // K3+K4 in one launch: blocks [0, B) select/commit batch rows, blocks >= B
 // (only with smoothing) write the smoothed embeddings.  Both read only what
 // K1 / K2 / the allgather produced (plus the step-start mask snapshot).
-__global__ void __launch_bounds__(kK3Threads) k34_select_smooth(const K3Args a3, const K4Args a4) {
+__global__ void __launch_bounds__(kK3Threads) k34_select_smooth(const K3Args a3in, const K4Args a4in) {
   grid_dep_wait();  // K1 / K2 / allgather results visible
   grid_dep_launch_dependents();
+  K3Args a3 = a3in;
+  K4Args a4 = a4in;
+  if (a3.pdev != nullptr) {  // per-step numeric parameters from device memory (graph replay)
+    a3.tau = a3.pdev[0];
+    a3.theta_hi = a3.pdev[1];
+    a3.theta_lo = a3.pdev[2];
+    a3.c_alpha = a3.pdev[3];
+    a3.c_beta = a3.pdev[4];
+    a3.c_gamma = a3.pdev[5];
+    a4.alpha_t = a3.pdev[6];
+  }
   if (static_cast<int>(blockIdx.x) < a3.B) {
     select_block(a3, blockIdx.x);
   } else {

@@ -120,6 +120,9 @@ struct K3Args {
   float* ml;               // [M][2] merged (m, l) for K4
   int decoder, runs_after_hi, use_credit;
   float tau, theta_hi, theta_lo, c_alpha, c_beta, c_gamma;
+  const float* pdev;       // optional device copy of the numeric params [tau, theta_hi, theta_lo,
+                           // c_alpha, c_beta, c_gamma, alpha_t] (overrides the values above; lets a
+                           // captured CUDA graph run with per-step schedules)
   int* err;
 };
 

@@ -215,6 +215,45 @@ def test_step_host_matches_device_step(torch_cuda):
     assert np.array_equal(sm.numpy()[still], dev["smoothed"][still])
 
 
+@pytest.mark.parametrize("pinned", [True, False])
+def test_step_host_graph_replay_follows_schedules(torch_cuda, pinned):
+    """dinfer_step_host replays one captured CUDA graph across iterations; the
+    per-step tau / alpha_t (linear schedules, App. A.1 / B.1) reach the kernels
+    through the packed state upload. Each iteration must equal the device
+    step run with the same parameters. Pageable buffers take the plain path."""
+    import torch
+    from paper_2510_08666_b200 import Context, make_params
+    V, H, B, S, K = 2048, 256, 1, 32, 8
+    W, E = weights(V, H)
+    Wd, Ed, emd = to_dev_bf16(W), to_dev_bf16(E), to_dev_bf16(E[V - 1])
+    ctx_d, ctx_h = Context(B, S, H, K, V), Context(B, S, H, K, V)
+    st = GpuState(B, S, H, K, V - 1)
+    wrap = (lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()) if pinned else \
+        (lambda a: torch.from_numpy(np.ascontiguousarray(a)))
+    mask, tok = wrap(np.ones((B, S), np.uint8)), wrap(np.full((B, S), V - 1, np.int32))
+    cids, cval = wrap(np.full((B, S, K), -1, np.int32)), wrap(np.zeros((B, S, K), np.float32))
+    com, sts = wrap(np.zeros((B, S), np.uint8)), wrap(np.zeros((B, S, 4), np.float32))
+    sm = wrap(np.full((B, S, H), np.nan, np.float32))
+    for t in range(4):
+        h = synth.planted_hidden(W, B * S, seed=40 + t, t=t)
+        p = make_params(decoder="hierarchical" if t < 3 else "threshold", tau=0.9 - 0.1 * t, theta_hi=0.8,
+                        theta_lo=0.3 - 0.05 * t, use_credit=True, c_alpha=0.5 + 0.1 * t, c_beta=0.9,
+                        c_gamma=0.3 + 0.15 * t, use_smooth=True, alpha_t=0.1 * (t + 1))
+        ctx_d.step(to_dev_bf16(h), Wd, Ed, emd, st.mask, st.tokens, st.cids, st.cval, p, st.committed,
+                   st.smoothed, st.stats)
+        torch.cuda.synchronize()
+        dev = st.snapshot()
+        hh = wrap(h.view(np.int16))
+        was = mask.numpy().astype(bool).copy()
+        ctx_h.step_host(hh, Wd, Ed, emd, mask, tok, cids, cval, p, com, sm, sts)
+        assert np.array_equal(mask.numpy().astype(bool), dev["mask"]), t
+        assert np.array_equal(com.numpy().astype(bool), dev["committed"]), t
+        assert np.array_equal(tok.numpy(), dev["tokens"]), t
+        assert np.array_equal(cids.numpy(), dev["cids"]) and np.array_equal(cval.numpy(), dev["cval"]), t
+        assert np.array_equal(sts.numpy(), st.stats.cpu().numpy()), t
+        assert np.array_equal(sm.numpy()[was], dev["smoothed"][was]), t
+
+
 def test_credit_slot_overflow_is_reported(torch_cuda):
     """K = 1 slot cannot hold two different tokens: the device flag surfaces
     as DINFER_ERR_DEVICE through dinfer_sync."""
