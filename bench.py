@@ -54,7 +54,7 @@ WORKLOAD = None
 
 def set_config(name):
     global B, S, H, V, K, CFG, WORKLOAD
-    CFG = CONFIGS[name]
+    CFG = dict(CONFIGS[name], name=name)
     B, S, H, V, K = CFG["B"], CFG["S"], CFG["H"], CFG["V"], CFG["K"]
     WORKLOAD = CFG["workload"]
 
@@ -359,7 +359,7 @@ def gpu_arm(args):
         k1_ms, k2_ms = phases.get("k1_vocab_proj", 0.0), phases.get("k2_smooth_mix", 0.0)
         dom, dom_bytes, dom_ms = ("k1_vocab_proj", k1_bytes, k1_ms) if k1_ms >= k2_ms else \
             ("k2_smooth_mix", k2_bytes, k2_ms)
-        traffic = ncu_traffic().get(dom if M <= 256 else "k1b_vocab_proj_dense")
+        traffic = ncu_traffic().get(f"{CFG['name']}/" + (dom if M <= 256 else "k1b_vocab_proj_dense"))
         step_bytes = k1_bytes + k2_bytes
         if M > 256:  # compute-bound regime (BASELINE configs[4]): tensor roofline of K1b
             flops = 2.0 * M * H * Vl

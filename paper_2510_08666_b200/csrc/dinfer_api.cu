@@ -294,6 +294,7 @@ dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, in
                           float* credit_val, const dinfer_params* p, uint8_t* committed, float* smoothed,
                           float* stats, int rec_stride = -1) {
   K3Args k{};
+  k.trace = c->trace == nullptr ? nullptr : c->trace + 5 * (c->k1_grid + c->k2_HS * c->k2_VG);
   k.B = c->shp.B;
   k.S = c->shp.S;
   k.K = c->shp.K;
@@ -571,7 +572,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
     A(dev_alloc(&c->grp_pass, static_cast<size_t>(c->k2_VG)));
   }
   if (std::getenv("DINFER_TRACE") != nullptr && std::atoi(std::getenv("DINFER_TRACE")) != 0)
-    A(dev_alloc(&c->trace, static_cast<size_t>(5) * (c->k1_grid + c->k2_HS * c->k2_VG)));
+    A(dev_alloc(&c->trace, static_cast<size_t>(5) * (c->k1_grid + c->k2_HS * c->k2_VG + kTraceK34)));
   if (st == DINFER_OK) {
     if (c->grp_cnt != nullptr && (cudaMemset(c->grp_cnt, 0, 4 * c->k2_VG) != cudaSuccess ||
                                   cudaMemset(c->grp_pass, 0, 4 * c->k2_VG) != cudaSuccess))
@@ -874,7 +875,7 @@ dinfer_status dinfer_get_timing(dinfer_ctx* c, float* ms, int32_t n) {
 
 int32_t dinfer_get_trace(dinfer_ctx* c, uint64_t* out, int32_t n) {
   if (c == nullptr || c->trace == nullptr) return 0;
-  const int total = 5 * (c->k1_grid + c->k2_HS * c->k2_VG);
+  const int total = 5 * (c->k1_grid + c->k2_HS * c->k2_VG + kTraceK34);
   if (out == nullptr) return total;
   cudaStreamSynchronize(c->stream);
   const int k = n < total ? n : total;

@@ -34,7 +34,10 @@ namespace dinfer {
 namespace {
 
 constexpr int kMaxS = 1024;
-constexpr int kK3Threads = 1024;
+// 512 threads: the kernel needs ~110 registers (1024 threads would cap it at
+// 64 and spill to local memory, each spill a dependent L1/L2 round trip)
+constexpr int kK3Threads = 512;
+constexpr int kPer = kMaxS / kK3Threads;  // positions per thread in the selection
 
 DI int run_first(const uint32_t* words, int s) {
   int w = s >> 5;
@@ -83,10 +86,20 @@ DI void row_stats(const K3Args& a, int i, int lane, float& m, int& vstar, float&
   vstar = INT_MAX;
   if (a.part1 != nullptr) {
     // lanes stride the slabs, then an xor butterfly (stat_combine is
-    // commutative bit for bit, so all lanes agree)
-    for (int j = lane; j < a.grid1; j += 32) {
-      const float4 p = __ldcg(a.part1 + static_cast<long>(i) * a.grid1 + j);
-      stat_combine(m, vstar, l, p.x, __float_as_int(p.y), p.z);
+    // commutative bit for bit, so all lanes agree).  Up to 8 loads per lane
+    // are issued before the first combine (one L2 round trip, not eight).
+    constexpr int kU = 8;
+    const float4* src = a.part1 + static_cast<long>(i) * a.grid1;
+    for (int j0 = 0; j0 < a.grid1; j0 += 32 * kU) {
+      float4 p[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int j = j0 + lane + 32 * u;
+        if (j < a.grid1) p[u] = __ldcg(src + j);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (j0 + lane + 32 * u < a.grid1) stat_combine(m, vstar, l, p[u].x, __float_as_int(p[u].y), p[u].z);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -118,7 +131,7 @@ DI void row_stats(const K3Args& a, int i, int lane, float& m, int& vstar, float&
 }
 
 // Selection block for batch row b (blockDim = kK3Threads).
-DI void select_block(const K3Args& a, int b) {
+DI void select_block(const K3Args& a, int b, unsigned long long* tr) {
   __shared__ uint32_t s_reg[kMaxS / 32];
   __shared__ int s_runA[kMaxS];
   __shared__ unsigned long long s_runkey[kMaxS];
@@ -134,16 +147,65 @@ DI void select_block(const K3Args& a, int b) {
   for (int s = warp; s < a.S; s += nwarps) {
     const int i = b * a.S + s;
     const long roff = static_cast<long>(i) * a.rec_stride;
+    const long cbase = static_cast<long>(i) * a.K;
+    // state loads issued before the statistics merge (independent round trips)
+    const bool und = a.mask[i] != 0;
+    const bool fast = a.use_credit && a.K <= 32;  // slot k in lane k, kept in registers
+    const bool slot = fast && lane < a.K;
+    int cid = slot ? a.credit_ids[cbase + lane] : -1;
+    float cv = slot ? a.credit_val[cbase + lane] : 0.f;
+    float fc = 0.f;  // raw logit of the credited token (max over ranks: -inf where not owned)
+    if (slot) {
+      fc = a.recs[roff + kStatWords + lane];
+      for (int r = 1; r < a.world; ++r) fc = fmaxf(fc, a.recs[r * a.rec_words + roff + kStatWords + lane]);
+    }
     float m, l;
     int vstar;
     row_stats(a, i, lane, m, vstar, l);
-    const bool und = a.mask[i] != 0;
     const float lse = m + logf(l);
     const float pstar = 1.0f / l;
     int vt = vstar;
     float pt = pstar;
-    if (a.use_credit && und) {
-      const long cbase = static_cast<long>(i) * a.K;
+    if (fast && und) {
+      const float gain = powf(pstar, a.c_gamma);
+      // decay, then add the gain to v*'s slot (or claim the first empty one)
+      if (cid >= 0) cv = a.c_beta * cv;
+      const unsigned hb = __ballot_sync(0xffffffffu, slot && cid == vstar);
+      const unsigned eb = __ballot_sync(0xffffffffu, slot && cid < 0);
+      const int hit = hb ? __ffs(hb) - 1 : -1, empty = eb ? __ffs(eb) - 1 : -1;
+      if (hit >= 0) {
+        if (lane == hit) cv += gain;
+      } else if (empty >= 0) {
+        if (lane == empty) {
+          cid = vstar;
+          cv = gain;
+        }
+      } else if (lane == 0) {
+        atomicOr(a.err, kErrCreditSlotsFull);
+      }
+      if (slot) {
+        a.credit_ids[cbase + lane] = cid;
+        a.credit_val[cbase + lane] = cv;
+      }
+      // fuse over credited tokens (v* included)
+      float best = m, extra = 0.f;
+      int best_id = vstar;
+      if (cid >= 0) {
+        const float fk = (cid == vstar) ? m : fc;
+        const float lc = log1pf(cv);
+        const float ft = fk + a.c_alpha * lc;
+        extra = expf(fk - m) * expm1f(a.c_alpha * lc);
+        if (ft > best || (ft == best && cid < best_id)) {
+          best = ft;
+          best_id = cid;
+        }
+      }
+      extra = warp_sum(extra);
+      warp_argmax(best, best_id);
+      const float lse_t = m + logf(l + extra);
+      vt = best_id;
+      pt = expf(best - lse_t);
+    } else if (a.use_credit && und) {  // K > 32: slots strided over the lanes
       const float gain = powf(pstar, a.c_gamma);
       // pass 1: decay, locate the slot of v* (or the first empty one)
       int hit = -1, empty = -1;
@@ -211,71 +273,104 @@ DI void select_block(const K3Args& a, int b) {
     }
   }
   __syncthreads();
+  if (tr != nullptr) tr[2] = globaltimer_ns();
 
   // ------------------------------------------------------------ phase 2: selection
-  const int s = threadIdx.x;
-  const bool valid = s < a.S;
+  // position s = threadIdx.x + q * kK3Threads (q < kPer); its ballot word is warp + q * nwarps
   const int nwords = (a.S + 31) / 32;
-  const bool und = valid && s_und[s];
-  const float pt = valid ? s_pt[s] : 0.f;
   const float thr_primary = (a.decoder == 0) ? a.tau : a.theta_hi;
-  bool A = und && pt > thr_primary;
-  if (a.decoder == 1) {
-    const bool region = und && !(a.runs_after_hi && A);
-    const unsigned rb = __ballot_sync(0xffffffffu, region);
-    if (lane == 0 && warp < nwords) s_reg[warp] = rb;
-    if (valid) {
-      s_runA[s] = 0;
-      s_runkey[s] = 0ull;
-    }
-    __syncthreads();
-    int first = 0, last = 0;
-    unsigned long long key = 0ull;
-    if (region) {
-      first = run_first(s_reg, s);
-      last = run_last(s_reg, s, nwords);
-      if (A) atomicOr(&s_runA[first], 1);
-      const int dist = abs(2 * s - first - last);
-      key = (static_cast<unsigned long long>(__float_as_uint(pt)) << 32) |
-            (static_cast<unsigned long long>(0xFFFF - dist) << 16) | static_cast<unsigned long long>(0xFFFF - s);
-      atomicMax(&s_runkey[first], key);
-    }
-    __syncthreads();
-    if (region && !s_runA[first] && s_runkey[first] == key && pt > a.theta_lo) A = true;
+  bool A[kPer], und[kPer], region[kPer];
+  float pt[kPer];
+  int first[kPer];
+  unsigned long long key[kPer];
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int s = threadIdx.x + q * kK3Threads;
+    const bool valid = s < a.S;
+    und[q] = valid && s_und[s];
+    pt[q] = valid ? s_pt[s] : 0.f;
+    A[q] = und[q] && pt[q] > thr_primary;
+    region[q] = false;
+    first[q] = 0;
+    key[q] = 0ull;
   }
-  if (s == 0) s_best = 0ull;
-  const int anyA = __syncthreads_or(A);
-  if (!anyA) {  // fallback: the undecided position with max p~ (lowest index on ties)
-    if (und) {
-      const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(pt)) << 32) |
-                                     static_cast<unsigned long long>(0xFFFFFFFFu - s);
-      atomicMax(&s_best, key);
+  if (a.decoder == 1) {
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int s = threadIdx.x + q * kK3Threads;
+      region[q] = und[q] && !(a.runs_after_hi && A[q]);
+      const unsigned rb = __ballot_sync(0xffffffffu, region[q]);
+      if (lane == 0 && warp + q * nwarps < nwords) s_reg[warp + q * nwarps] = rb;
+      if (s < a.S) {
+        s_runA[s] = 0;
+        s_runkey[s] = 0ull;
+      }
     }
     __syncthreads();
-    A = und && s_best != 0ull && static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(s_best & 0xFFFFFFFFull)) == s;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      if (!region[q]) continue;
+      const int s = threadIdx.x + q * kK3Threads;
+      first[q] = run_first(s_reg, s);
+      const int last = run_last(s_reg, s, nwords);
+      if (A[q]) atomicOr(&s_runA[first[q]], 1);
+      const int dist = abs(2 * s - first[q] - last);
+      key[q] = (static_cast<unsigned long long>(__float_as_uint(pt[q])) << 32) |
+               (static_cast<unsigned long long>(0xFFFF - dist) << 16) | static_cast<unsigned long long>(0xFFFF - s);
+      atomicMax(&s_runkey[first[q]], key[q]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kPer; ++q)
+      if (region[q] && !s_runA[first[q]] && s_runkey[first[q]] == key[q] && pt[q] > a.theta_lo) A[q] = true;
+  }
+  if (threadIdx.x == 0) s_best = 0ull;
+  bool mine = false;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) mine = mine || A[q];
+  const int anyA = __syncthreads_or(mine);
+  if (!anyA) {  // fallback: the undecided position with max p~ (lowest index on ties)
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int s = threadIdx.x + q * kK3Threads;
+      if (und[q])
+        atomicMax(&s_best, (static_cast<unsigned long long>(__float_as_uint(pt[q])) << 32) |
+                               static_cast<unsigned long long>(0xFFFFFFFFu - s));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int s = threadIdx.x + q * kK3Threads;
+      A[q] = und[q] && s_best != 0ull &&
+             static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(s_best & 0xFFFFFFFFull)) == s;
+    }
   }
 
   // ------------------------------------------------------------ commit
-  if (valid) {
-    const int i = b * a.S + s;
-    a.committed[i] = A ? 1 : 0;
-    if (A) {
-      a.tokens[i] = s_vt[s];
-      a.mask[i] = 0;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int s = threadIdx.x + q * kK3Threads;
+    if (s < a.S) {
+      const int i = b * a.S + s;
+      a.committed[i] = A[q] ? 1 : 0;
+      if (A[q]) {
+        a.tokens[i] = s_vt[s];
+        a.mask[i] = 0;
+      }
     }
   }
 }
 
-// Smoothing block: 1024 threads = 128 float4 columns x 8 partial groups, i.e.
-// 512 consecutive elements of the [M, H] output.  Each thread loads a strided
+// Smoothing block: 512 threads = 64 float4 columns x 8 partial groups, i.e.
+// 256 consecutive elements of the [M, H] output.  Each thread loads a strided
 // subset of the nparts partials (issued before the statistics merge so both
 // latencies overlap), the 8 groups are combined in a fixed order through
 // shared memory (deterministic).  The block merges the statistics (m, l) of
 // the rows it covers itself (one warp per row), so it does not wait for the
 // selection; rows undecided at step START are written (e_{t+1} matters for
 // those still undecided after the commit).
-constexpr int kSmCols = 128, kSmGroups = 8, kSmBatch = 8;
-DI void smooth_block(const K3Args& a3, const K4Args& a, int blk) {
+constexpr int kSmCols = 64, kSmGroups = 8, kSmBatch = 8;
+DI void smooth_block(const K3Args& a3, const K4Args& a, int blk, unsigned long long* tr) {
   __shared__ float s_m[4], s_w[4];
   __shared__ float4 red[kSmGroups][kSmCols];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -310,6 +405,7 @@ DI void smooth_block(const K3Args& a3, const K4Args& a, int blk) {
     }
   }
   __syncthreads();
+  if (tr != nullptr) tr[2] = globaltimer_ns();
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if (active) {
     const float m = s_m[s - s0];
@@ -359,7 +455,16 @@ DI void smooth_block(const K3Args& a3, const K4Args& a, int blk) {
 // (only with smoothing) write the smoothed embeddings.  Both read only what
 // K1 / K2 / the allgather produced (plus the step-start mask snapshot).
 __global__ void __launch_bounds__(kK3Threads) k34_select_smooth(const K3Args a3in, const K4Args a4in) {
+  unsigned long long* tr =
+      (a3in.trace != nullptr && threadIdx.x == 0 && blockIdx.x < kTraceK34) ? a3in.trace + blockIdx.x * 5 : nullptr;
+  if (tr != nullptr) {
+    tr[0] = globaltimer_ns();
+    uint32_t sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    tr[4] = sm;
+  }
   grid_dep_wait();  // K1 / K2 / allgather results visible
+  if (tr != nullptr) tr[1] = globaltimer_ns();
   grid_dep_launch_dependents();
   K3Args a3 = a3in;
   K4Args a4 = a4in;
@@ -373,10 +478,11 @@ __global__ void __launch_bounds__(kK3Threads) k34_select_smooth(const K3Args a3i
     a4.alpha_t = a3.pdev[6];
   }
   if (static_cast<int>(blockIdx.x) < a3.B) {
-    select_block(a3, blockIdx.x);
+    select_block(a3, blockIdx.x, tr);
   } else {
-    smooth_block(a3, a4, blockIdx.x - a3.B);
+    smooth_block(a3, a4, blockIdx.x - a3.B, tr);
   }
+  if (tr != nullptr) tr[3] = globaltimer_ns();
 }
 
 }  // namespace

@@ -12,7 +12,8 @@ constexpr int kKChunk = 64;        // bf16 elements per 128-B swizzled row
 constexpr int kTileRows = 128;     // UMMA M (vocab rows per tile)
 constexpr int kRowGran = 8;        // vocab-row granularity of the K1 partition
 constexpr int kMaxCreditEnt = 1024;  // per-CTA credited (position, slot) entries
-constexpr int kStatWords = 4;      // m, idx, l, pad  (record header per row)
+constexpr int kStatWords = 4;
+constexpr int kTraceK34 = 64;  // K34 blocks traced (DINFER_TRACE)      // m, idx, l, pad  (record header per row)
 
 // Launch helper: optional programmatic dependent launch (PDL) attribute.
 template <typename... KArgs, typename... Args>
@@ -120,6 +121,7 @@ struct K3Args {
   float* ml;               // [M][2] merged (m, l) for K4
   int decoder, runs_after_hi, use_credit;
   float tau, theta_hi, theta_lo, c_alpha, c_beta, c_gamma;
+  unsigned long long* trace;  // DINFER_TRACE: blocks < kTraceK34 stamp [entry, deps, phase1, end, smid]
   const float* pdev;       // optional device copy of the numeric params [tau, theta_hi, theta_lo,
                            // c_alpha, c_beta, c_gamma, alpha_t] (overrides the values above; lets a
                            // captured CUDA graph run with per-step schedules)

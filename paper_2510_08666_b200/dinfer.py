@@ -202,7 +202,8 @@ class Context:
 
     def trace(self):
         """Per-CTA globaltimer stamps of the last step (DINFER_TRACE=1), as
-        (k1 [grid,5], k2 [grid,5]) numpy arrays (4 stamps in ns + SM id), or None."""
+        (k1 [grid,5], k2 [grid,5], k34 [64,5]) numpy arrays (4 stamps in ns + SM id; K34
+        blocks that did not run stay 0), or None."""
         import numpy as np
         n = int(lib().dinfer_get_trace(self._h, None, 0))
         if n == 0:
@@ -211,7 +212,8 @@ class Context:
         lib().dinfer_get_trace(self._h, c_void_p(buf.ctypes.data), n)
         g = self.geometry()
         k1 = buf[:5 * g["k1_grid"]].reshape(-1, 5)
-        return k1, buf[5 * g["k1_grid"]:].reshape(-1, 5)
+        rest = buf[5 * g["k1_grid"]:].reshape(-1, 5)
+        return k1, rest[:-64], rest[-64:]  # K1, K2, K34 (first 64 blocks)
 
     def geometry(self) -> dict:
         g = Geometry()

@@ -47,6 +47,19 @@ def test_library_is_sm100a_with_tcgen05_and_tma():
         assert mnem in out, mnem
 
 
+def test_kernels_do_not_spill():
+    """Every kernel keeps its state in registers: no local-memory stack (a
+    spill is a dependent L1/L2 round trip on the latency-bound K34 path)."""
+    import re
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-res-usage", dinfer.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    funcs = re.findall(r"Function (\S+):\n\s*REG:(\d+) STACK:(\d+) SHARED:\d+ LOCAL:(\d+)", out)
+    assert len(funcs) >= 5, out[:500]
+    for name, reg, stack, local in funcs:
+        assert int(stack) == 0 and int(local) == 0, (name, reg, stack, local)
+
+
 def test_schedules_match_oracle(L):
     for t in range(12):
         assert dinfer.alpha_schedule(0.1, 0.05, 0.3, t) == pytest.approx(O.alpha_schedule(0.1, 0.05, 0.3, t), abs=1e-7)

@@ -2,7 +2,10 @@
 DRAM bytes (-> profiles/ncu_traffic.json, read by bench.py), throughput,
 tensor-pipe activity, SM activity and the top stall-sampled SASS lines.
 
-  python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r1_ncu_summary.md
+  python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r1_ncu_summary.md [config]
+
+With `config`, the traffic entries are keyed "config/kernel" (bench.py looks
+up its own config's entry).
 """
 import csv
 import io
@@ -41,12 +44,14 @@ def to_bytes(v, unit):
 
 
 def to_us(v, unit):
-    mult = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "us": 1.0, "ns": 1e-3}.get(unit, 1.0)
+    mult = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "us": 1.0, "ns": 1e-3, "ms": 1e3,
+            "second": 1e6, "s": 1e6}.get(unit, 1.0)
     return float(v.replace(",", "")) * mult
 
 
 def main():
     rep, out_md = sys.argv[1], sys.argv[2]
+    cfg = sys.argv[3] + "/" if len(sys.argv) > 3 else ""
     hdr, units, rows = raw(rep)
     col = {h: i for i, h in enumerate(hdr)}
     per = {}
@@ -99,8 +104,13 @@ def main():
     with open(out_md, "w") as fh:
         fh.write("\n".join(lines) + "\n")
     tj = os.path.join(os.path.dirname(out_md) or ".", "ncu_traffic.json")
+    old = {}
+    if os.path.exists(tj):
+        with open(tj) as fh:
+            old = json.load(fh)
+    old.update({cfg + k: int(v) for k, v in traffic.items()})  # merge: one report per config
     with open(tj, "w") as fh:
-        json.dump({k: int(v) for k, v in traffic.items()}, fh, indent=1)
+        json.dump(old, fh, indent=1, sort_keys=True)
     print("\n".join(lines))
 
 

@@ -1,5 +1,5 @@
-"""Per-CTA timelines of K1 and K2 for one MoE step (DINFER_TRACE=1).
-  python tools/trace_step.py [--config moe|8b]"""
+"""Per-CTA timelines of K1, K2 and K34 for one step (DINFER_TRACE=1).
+  python tools/trace_step.py [8b|tiny]"""
 import os
 import sys
 
@@ -10,8 +10,8 @@ import torch  # noqa: E402
 
 from paper_2510_08666_b200 import Context, make_params, synth  # noqa: E402
 
-H, V = (4096, 126464) if "8b" in sys.argv else (2048, 157184)
-smooth = "8b" not in sys.argv
+H, V = (4096, 126464) if "8b" in sys.argv else (256, 1024) if "tiny" in sys.argv else (2048, 157184)
+smooth = "8b" not in sys.argv and "tiny" not in sys.argv
 B, S, K = 1, 32, 32
 dev = lambda u: torch.from_numpy(np.ascontiguousarray(u).view(np.int16)).view(torch.bfloat16).cuda()
 W = synth.make_W(V, H, 1)
@@ -38,7 +38,8 @@ for it in range(6):
     ctx.step(h, Wd, Ed, em, mask, tok, cids, cval, p, com, sm, st)
     torch.cuda.synchronize()
     runs.append(tuple(x.copy() for x in ctx.trace()))
-k1, k2 = runs[-1]
+k1, k2, k34 = runs[-1]
+k34 = k34[k34[:, 0] > 0]
 t0 = int(k1[:, 0].min())
 us = lambda a: (a.astype(np.int64) - t0) / 1e3
 
@@ -57,11 +58,15 @@ if smooth:
     for i, n in enumerate(["start", "first MMA (E+P)", "MMAs done", "exit"]):
         row(n, k2[:, i])
     print(f"  step span: {us(k2[:, 3]).max():.1f} us (K1 start -> last K2 CTA exit)")
+print(f"K34 ({len(k34)} traced blocks; block 0 = selection):")
+for i, n in enumerate(["start", "deps visible", "stats merged", "exit"]):
+    row(n, k34[:, i])
+print("  selection block:", [round(float(x), 1) for x in us(k34[0, :4])])
 
 # Systematic or random?  Per-SM K1 main-loop duration across repeated steps.
 if len(runs) > 2:
     dur = {}
-    for r1, _ in runs[1:]:
+    for r1, _, _ in runs[1:]:
         for row in r1:
             dur.setdefault(int(row[4]), []).append((int(row[2]) - int(row[1])) / 1e3)
     sms = sorted(dur)
