@@ -56,6 +56,8 @@ struct dinfer_ctx {
   float* flog = nullptr;
   float* part2 = nullptr;
   float* ml = nullptr;
+  float4* sel = nullptr;    // K34 phase-1 -> phase-2 exchange [M]
+  int* row_cnt = nullptr;   // [B] K34 arrival counters
   uint8_t* mask_snap = nullptr;   // [M] step-start mask (K1 -> smoothing blocks of K34)
   float* mref = nullptr;          // [k2_VG][M] per-vocab-group reference max (K2 -> K4 / record finalize)
   unsigned* grp_cnt = nullptr;    // [k2_VG] K1 slabs done per vocab group (self-resetting)
@@ -311,6 +313,8 @@ dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, in
   k.committed = committed;
   k.stats = stats;
   k.ml = c->ml;
+  k.sel = c->sel;
+  k.row_cnt = c->row_cnt;
   k.decoder = p->decoder;
   k.runs_after_hi = p->hier_runs_after_hi;
   k.use_credit = p->use_credit;
@@ -417,7 +421,8 @@ void dinfer_destroy(dinfer_ctx* c) {
 #ifdef DINFER_WITH_NCCL
   if (c->has_comm) ncclCommDestroy(c->comm);
 #endif
-  void* bufs[] = {c->part1, c->counter, c->err, c->rec_local, c->flog, c->part2, c->ml, c->trace, c->mref,
+  void* bufs[] = {c->part1, c->counter, c->err, c->rec_local, c->flog, c->part2, c->ml, c->sel, c->row_cnt, c->trace,
+                  c->mref,
                   c->mask_snap,
                   c->grp_cnt, c->grp_pass,
                   c->st_hidden, c->st_block, c->st_smoothed};
@@ -561,6 +566,8 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
   A(dev_alloc(&c->err, 4));
   A(dev_alloc(&c->rec_local, c->full_words));
   A(dev_alloc(&c->ml, static_cast<size_t>(M) * 2));
+  A(dev_alloc(&c->sel, static_cast<size_t>(M)));
+  A(dev_alloc(&c->row_cnt, static_cast<size_t>(s.B)));
   A(dev_alloc(&c->mask_snap, static_cast<size_t>(M)));
   if (s.world > 1) A(dev_alloc(&c->rec_all, c->full_words * s.world));
   else c->rec_all = c->rec_local;
@@ -578,6 +585,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
                                   cudaMemset(c->grp_pass, 0, 4 * c->k2_VG) != cudaSuccess))
       st = DINFER_ERR_CUDA;
     if (cudaMemset(c->counter, 0, 16) != cudaSuccess || cudaMemset(c->err, 0, 16) != cudaSuccess ||
+        cudaMemset(c->row_cnt, 0, 4 * static_cast<size_t>(s.B)) != cudaSuccess ||
         cudaMemset(c->rec_local, 0, c->full_words * 4) != cudaSuccess)
       st = DINFER_ERR_CUDA;
   }

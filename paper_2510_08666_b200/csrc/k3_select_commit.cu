@@ -130,8 +130,15 @@ DI void row_stats(const K3Args& a, int i, int lane, float& m, int& vstar, float&
   l = __shfl_sync(0xffffffffu, l0, 0);
 }
 
-// Selection block for batch row b (blockDim = kK3Threads).
-DI void select_block(const K3Args& a, int b, unsigned long long* tr) {
+// Selection CTAs: phase 1 is spread over ceil(S / kSelPos) CTAs per batch
+// row (one warp per position: the per-position chain is latency- and
+// issue-bound, so fewer warps per SM finish sooner); each writes its
+// positions' (p~, v~, undecided) to `sel`, and the last CTA of the row to
+// arrive (counter, release/acquire fences) runs phase 2 over the whole row.
+constexpr int kSelPos = 8;
+DI int sel_ctas_per_row(int S) { return (S + kSelPos - 1) / kSelPos; }
+
+DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
   __shared__ uint32_t s_reg[kMaxS / 32];
   __shared__ int s_runA[kMaxS];
   __shared__ unsigned long long s_runkey[kMaxS];
@@ -139,12 +146,16 @@ DI void select_block(const K3Args& a, int b, unsigned long long* tr) {
   __shared__ int s_vt[kMaxS];
   __shared__ uint8_t s_und[kMaxS];
   __shared__ unsigned long long s_best;
+  __shared__ int s_last;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
+  const int cps = sel_ctas_per_row(a.S);
+  const int b = c / cps, chunk = c - b * cps;
 
   // ------------------------------------------------------------ phase 1
-  for (int s = warp; s < a.S; s += nwarps) {
+  if (warp < kSelPos && chunk * kSelPos + warp < a.S) {
+    const int s = chunk * kSelPos + warp;
     const int i = b * a.S + s;
     const long roff = static_cast<long>(i) * a.rec_stride;
     const long cbase = static_cast<long>(i) * a.K;
@@ -162,12 +173,12 @@ DI void select_block(const K3Args& a, int b, unsigned long long* tr) {
     float m, l;
     int vstar;
     row_stats(a, i, lane, m, vstar, l);
-    const float lse = m + logf(l);
-    const float pstar = 1.0f / l;
+    const float lse = m + __logf(l);
+    const float pstar = __frcp_rn(l);  // == 1.0f / l (correctly rounded), no slow path
     int vt = vstar;
     float pt = pstar;
     if (fast && und) {
-      const float gain = powf(pstar, a.c_gamma);
+      const float gain = ex2(a.c_gamma * __log2f(pstar));  // p*^gamma
       // decay, then add the gain to v*'s slot (or claim the first empty one)
       if (cid >= 0) cv = a.c_beta * cv;
       const unsigned hb = __ballot_sync(0xffffffffu, slot && cid == vstar);
@@ -192,9 +203,9 @@ DI void select_block(const K3Args& a, int b, unsigned long long* tr) {
       int best_id = vstar;
       if (cid >= 0) {
         const float fk = (cid == vstar) ? m : fc;
-        const float lc = log1pf(cv);
+        const float lc = __logf(1.f + cv);
         const float ft = fk + a.c_alpha * lc;
-        extra = expf(fk - m) * expm1f(a.c_alpha * lc);
+        extra = __expf(fk - m) * (__expf(a.c_alpha * lc) - 1.f);
         if (ft > best || (ft == best && cid < best_id)) {
           best = ft;
           best_id = cid;
@@ -202,11 +213,11 @@ DI void select_block(const K3Args& a, int b, unsigned long long* tr) {
       }
       extra = warp_sum(extra);
       warp_argmax(best, best_id);
-      const float lse_t = m + logf(l + extra);
+      const float lse_t = m + __logf(l + extra);
       vt = best_id;
-      pt = expf(best - lse_t);
+      pt = __expf(best - lse_t);
     } else if (a.use_credit && und) {  // K > 32: slots strided over the lanes
-      const float gain = powf(pstar, a.c_gamma);
+      const float gain = ex2(a.c_gamma * __log2f(pstar));  // p*^gamma
       // pass 1: decay, locate the slot of v* (or the first empty one)
       int hit = -1, empty = -1;
       for (int k0 = 0; k0 < a.K; k0 += 32) {
@@ -242,9 +253,9 @@ DI void select_block(const K3Args& a, int b, unsigned long long* tr) {
             fk = a.recs[roff + kStatWords + k];
             for (int r = 1; r < a.world; ++r) fk = fmaxf(fk, a.recs[r * a.rec_words + roff + kStatWords + k]);
           }
-          const float lc = log1pf(a.credit_val[cbase + k]);
+          const float lc = __logf(1.f + a.credit_val[cbase + k]);
           const float ft = fk + a.c_alpha * lc;
-          extra += expf(fk - m) * expm1f(a.c_alpha * lc);
+          extra += __expf(fk - m) * (__expf(a.c_alpha * lc) - 1.f);
           if (ft > best || (ft == best && id < best_id)) {
             best = ft;
             best_id = id;
@@ -253,9 +264,9 @@ DI void select_block(const K3Args& a, int b, unsigned long long* tr) {
       }
       extra = warp_sum(extra);
       warp_argmax(best, best_id);
-      const float lse_t = m + logf(l + extra);
+      const float lse_t = m + __logf(l + extra);
       vt = best_id;
-      pt = expf(best - lse_t);
+      pt = __expf(best - lse_t);
     }
     if (lane == 0) {
       if (a.stats != nullptr) {
@@ -267,9 +278,40 @@ DI void select_block(const K3Args& a, int b, unsigned long long* tr) {
       }
       a.ml[2 * i] = m;
       a.ml[2 * i + 1] = l;
-      s_pt[s] = pt;
-      s_vt[s] = vt;
-      s_und[s] = und ? 1 : 0;
+      if (cps == 1) {
+        s_pt[s] = pt;
+        s_vt[s] = vt;
+        s_und[s] = und ? 1 : 0;
+      } else {
+        a.sel[i] = make_float4(pt, __int_as_float(vt), und ? 1.f : 0.f, 0.f);
+        __threadfence();  // release: this position before the arrival below
+      }
+    }
+  }
+  if (cps > 1) {  // last CTA of the row to arrive runs phase 2
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int prev = atomicAdd(a.row_cnt + b, 1);
+      s_last = prev == cps - 1;
+      if (s_last) {
+        __threadfence();  // acquire: the other CTAs' positions
+        a.row_cnt[b] = 0;  // all arrived: reset for the next step
+      }
+    }
+    __syncthreads();
+    if (!s_last) {
+      if (tr != nullptr) tr[2] = globaltimer_ns();
+      return;
+    }
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int s = threadIdx.x + q * kK3Threads;
+      if (s < a.S) {
+        const float4 v = __ldcg(a.sel + static_cast<long>(b) * a.S + s);
+        s_pt[s] = v.x;
+        s_vt[s] = __float_as_int(v.y);
+        s_und[s] = v.z != 0.f;
+      }
     }
   }
   __syncthreads();
@@ -413,7 +455,7 @@ DI void smooth_block(const K3Args& a3, const K4Args& a, int blk, unsigned long l
 #pragma unroll
       for (int j = 0; j < kSmBatch; ++j) {  // fixed summation order
         const int p = grp + p0 + j * kSmGroups;
-        const float sc = (p < a.nparts) ? expf(mp[j] - m) : 0.f;
+        const float sc = (p < a.nparts) ? __expf(mp[j] - m) : 0.f;
         acc.x = fmaf(v[j].x, sc, acc.x);
         acc.y = fmaf(v[j].y, sc, acc.y);
         acc.z = fmaf(v[j].z, sc, acc.z);
@@ -477,10 +519,11 @@ __global__ void __launch_bounds__(kK3Threads) k34_select_smooth(const K3Args a3i
     a3.c_gamma = a3.pdev[5];
     a4.alpha_t = a3.pdev[6];
   }
-  if (static_cast<int>(blockIdx.x) < a3.B) {
+  const int nsel = a3.B * sel_ctas_per_row(a3.S);
+  if (static_cast<int>(blockIdx.x) < nsel) {
     select_block(a3, blockIdx.x, tr);
   } else {
-    smooth_block(a3, a4, blockIdx.x - a3.B, tr);
+    smooth_block(a3, a4, blockIdx.x - nsel, tr);
   }
   if (tr != nullptr) tr[3] = globaltimer_ns();
 }
@@ -500,7 +543,8 @@ cudaError_t launch_k34(const K3Args& a3, const K4Args* a4, cudaStream_t st, bool
     f = *a4;
     nsm = static_cast<int>((static_cast<long>(f.M) * f.H / 4 + kSmCols - 1) / kSmCols);
   }
-  return launch_ex(k34_select_smooth, dim3(a3.B + nsm), dim3(kK3Threads), 0, st, pdl, a3, f);
+  return launch_ex(k34_select_smooth, dim3(a3.B * ((a3.S + kSelPos - 1) / kSelPos) + nsm), dim3(kK3Threads), 0, st,
+                   pdl, a3, f);
 }
 
 }  // namespace dinfer

@@ -119,6 +119,8 @@ struct K3Args {
   uint8_t* committed;
   float* stats;            // [M][4] or nullptr
   float* ml;               // [M][2] merged (m, l) for K4
+  float4* sel;             // [M] per-position (p~, v~ bits, undecided, 0) from the phase-1 CTAs
+  int* row_cnt;            // [B] phase-1 CTAs arrived per batch row (zero between steps)
   int decoder, runs_after_hi, use_credit;
   float tau, theta_hi, theta_lo, c_alpha, c_beta, c_gamma;
   unsigned long long* trace;  // DINFER_TRACE: blocks < kTraceK34 stamp [entry, deps, phase1, end, smid]

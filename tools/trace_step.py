@@ -58,10 +58,11 @@ if smooth:
     for i, n in enumerate(["start", "first MMA (E+P)", "MMAs done", "exit"]):
         row(n, k2[:, i])
     print(f"  step span: {us(k2[:, 3]).max():.1f} us (K1 start -> last K2 CTA exit)")
-print(f"K34 ({len(k34)} traced blocks; block 0 = selection):")
+print(f"K34 ({len(k34)} traced blocks; the first B*ceil(S/8) are selection CTAs):")
 for i, n in enumerate(["start", "deps visible", "stats merged", "exit"]):
     row(n, k34[:, i])
-print("  selection block:", [round(float(x), 1) for x in us(k34[0, :4])])
+for j in range(4):
+    print(f"  selection CTA {j}:", [round(float(x), 1) for x in us(k34[j, :4])])
 
 # Systematic or random?  Per-SM K1 main-loop duration across repeated steps.
 if len(runs) > 2:
