@@ -331,3 +331,116 @@ def merge_records(records):
             acc = (0 if acc is None else acc) + r["acc"] * scale[:, None]
     lse = m + np.log(l)
     return dict(m=m, vstar=vstar, l=l, lse=lse, pstar=1.0 / l, acc=acc)
+
+
+# ---------------------------------------------------------------------------
+# The blockwise generation loop (Algorithm 1) around step(),
+# with the schedules (App. A.1), per-block credit reset
+# and EOS early termination.  SURVEY §8(f) row f1.
+#
+# Readings:
+#   c11/c12  tau_t / alpha_t restart at t = 0 in every block; tau_t drives tau
+#            (threshold) or theta_hi (hierarchical), theta_lo stays fixed.
+#   c21      blocks are [prompt_len + k*S, prompt_len + (k+1)*S), left to
+#            right; all B rows decode the same block in lockstep (a row with
+#            no undecided position is a no-op, §8(b)); the block ends when no
+#            row has an undecided position.  Positions of the generation
+#            region that are not mask_id at block start count as decided.
+#   c22      early termination: when row b's block contains eos_id after the
+#            block completes, row b is finished -- every later block of row b
+#            is filled with eos_id ("fills all remaining blocks with
+#            EOS"); the block in which EOS appeared is decoded to completion
+#            (P:174 makes the *remaining blocks* redundant, not the current
+#            one).  The loop halts when every row is finished or the blocks
+#            run out.
+#   c23      T_b = number of generated tokens before the first eos_id of row
+#            b, gen_len if none; F = number of forwards (iterations)
+#            the loop ran -- shared by the B rows, which step in lockstep.
+#   The model forward is outside the method's hot path: iteration n (global,
+#   0-based) uses the hidden block hidden_of(n) supplied by the caller.
+# ---------------------------------------------------------------------------
+@dataclass
+class GenConfig:
+    prompt_len: int
+    S: int
+    mask_id: int
+    eos_id: int
+    early_termination: bool = True
+    tau_target: float = 0.9      # decays from 1.0, reading c11
+    tau_decay_steps: int = 0     # 0 = constant tau_target
+    alpha_init: float = 0.1      # alpha_t = min(init + growth*t, preset)
+    alpha_growth: float = 0.05
+    alpha_preset: float = 0.3
+    max_forwards: int = 1 << 30
+
+
+def iteration_params(base: Params, cfg: GenConfig, t: int) -> Params:
+    """The step parameters of block-local iteration t (schedules, c11/c12)."""
+    p = Params(**vars(base))
+    thr = tau_schedule(cfg.tau_target, t, cfg.tau_decay_steps)
+    if p.decoder == DEC_THRESHOLD:
+        p.tau = thr
+    else:
+        p.theta_hi = thr
+    if p.use_smooth:
+        p.alpha_t = alpha_schedule(cfg.alpha_init, cfg.alpha_growth, cfg.alpha_preset, t)
+    return p
+
+
+def generate(hidden_of, W, E, e_mask, X0, cfg: GenConfig, base: Params, dense_credit=True, trace=None):
+    """Run Algorithm 1's block loop on token rows X0 [B, L].
+
+    hidden_of(n, tokens_blk, mask_blk) -> [B, S, H] float64 hidden states of
+    global iteration n (the model stand-in).  Returns dict(X, F, T,
+    truncated).  `trace`, when a list, receives per-iteration dicts (block,
+    t, params, state before, step result)."""
+    X = np.array(X0, dtype=np.int64, copy=True)
+    B, L = X.shape
+    S, P = cfg.S, cfg.prompt_len
+    gen_len = L - P
+    assert gen_len > 0 and gen_len % S == 0
+    V = W.shape[0]
+    nblocks = gen_len // S
+    done = np.zeros(B, dtype=bool)
+    F = 0
+    truncated = False
+    for k in range(nblocks):
+        lo, hi = P + k * S, P + (k + 1) * S
+        tokens = X[:, lo:hi].copy()
+        for b in range(B):
+            if done[b]:
+                tokens[b][tokens[b] == cfg.mask_id] = cfg.eos_id     # c22: EOS fill
+        mask = tokens == cfg.mask_id
+        C = np.zeros((B, S, V)) if (base.use_credit and dense_credit) else None  # P:327 reset
+        t = 0
+        while mask.any():
+            if F >= cfg.max_forwards:
+                truncated = True
+                break
+            p = iteration_params(base, cfg, t)
+            h = hidden_of(F, tokens, mask)
+            res = step(h, W, E, e_mask, mask, tokens, C, p)
+            if trace is not None:
+                trace.append(dict(block=k, t=t, params=p, mask=mask.copy(), tokens=tokens.copy(),
+                                  C=None if C is None else C.copy(), h=h, result=res))
+            tokens, mask = res["tokens"], res["mask"]
+            if C is not None:
+                C = res["C"]
+            F += 1
+            t += 1
+        X[:, lo:hi] = tokens
+        if truncated:
+            break
+        if cfg.early_termination:
+            done |= (tokens == cfg.eos_id).any(axis=1)
+            if done.all():
+                for b in range(B):                                   # c22: fill the rest
+                    rest = X[b, hi:]
+                    rest[rest == cfg.mask_id] = cfg.eos_id
+                break
+    T = np.full(B, gen_len, dtype=np.int64)
+    for b in range(B):
+        e = np.nonzero(X[b, P:] == cfg.eos_id)[0]
+        if len(e):
+            T[b] = e[0]
+    return dict(X=X, F=F, T=T, truncated=truncated)
