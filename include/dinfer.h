@@ -193,6 +193,57 @@ dinfer_status dinfer_credit_reset(dinfer_ctx* ctx, int32_t* credit_ids, float* c
 float dinfer_alpha_schedule(float init, float growth, float preset, int32_t t);
 float dinfer_tau_schedule(float target, int32_t t, int32_t decay_steps);
 
+/* ---------------------------------------------------------------------------
+ * Device-resident blockwise generation loop (Algorithm 1).
+ *
+ * dinfer_generate runs the block loop over the generation region
+ * [prompt_len, L) of the token rows X [B][L] (device int32, in/out; mask_id
+ * marks undecided positions), S positions per block, left to right, all B
+ * rows in lockstep:
+ *   for each block: credit table reset, t = 0;
+ *     while any position of the block is undecided:
+ *       hidden  <- the model's hidden states of this iteration (see below)
+ *       params  <- tau_t (drives tau, or theta_hi for the hierarchical
+ *                  decoder; reading c11), alpha_t, rest from `base`
+ *       dinfer_step on the block; t += 1; F += 1
+ *     early termination (reading c22): a row whose completed block
+ *     holds eos_id is finished; its later blocks are filled with eos_id; the
+ *     loop halts once every row is finished.
+ * The whole loop is ONE CUDA graph (a conditional WHILE node around
+ * {hidden, step kernels, bookkeeping kernel}) launched on the ctx stream: no
+ * host synchronisation or data-dependent host control inside a generation.
+ * Asynchronous like dinfer_step; results land in X and `out` (device int32
+ * [B+2]: T_b = generated tokens before the first eos_id of row b (
+ * gen_len if none), then F = forwards run, then 1 if max_forwards stopped
+ * the loop early).  The graph is built on the first call and re-used while
+ * the pointers and the configuration are unchanged.
+ *
+ * The model forward is not part of this library.  Its stand-in here is a
+ * hidden-state source: iteration n (0-based, global) uses
+ * hidden_src + min(n, hidden_iters-1)*B*S*H (bf16 [B][S][H] blocks, device),
+ * copied into the step's hidden buffer -- the point where a real model's
+ * captured forward is inserted.
+ *
+ * Constraints: (L - prompt_len) % S == 0 and > 0; ctx shape B, S as created;
+ * world == 1; B <= 1024; mask_id, eos_id in [0, V_total).  `base` supplies the
+ * decoder, theta_lo, credit constants and use_smooth/use_credit; its tau /
+ * theta_hi / alpha_t are replaced per iteration by the schedules.
+ * Smoothed embeddings of the last iteration stay in ctx-owned memory.      */
+typedef struct {
+  int32_t L;                 /* tokens per row (prompt + generation)          */
+  int32_t prompt_len;        /* fixed input positions [0, prompt_len)         */
+  int32_t mask_id, eos_id;
+  int32_t early_termination;
+  float tau_target;          /* tau_t = dinfer_tau_schedule(tau_target, t, tau_decay_steps) */
+  int32_t tau_decay_steps;
+  float alpha_init, alpha_growth, alpha_preset; /* alpha_t (used with smoothing) */
+  int32_t max_forwards;      /* safety bound on F (>= 1)                        */
+} dinfer_gen_config;
+
+dinfer_status dinfer_generate(dinfer_ctx* ctx, const dinfer_gen_config* cfg, const dinfer_params* base,
+                              const uint16_t* W_vocab, const uint16_t* E, const uint16_t* e_mask,
+                              const uint16_t* hidden_src, int64_t hidden_iters, int32_t* X, int32_t* out);
+
 /* Synchronise the ctx stream and report asynchronous errors (CUDA, NCCL,
  * sticky device-checked preconditions); clears the sticky device flag.      */
 dinfer_status dinfer_sync(dinfer_ctx* ctx);

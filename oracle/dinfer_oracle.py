@@ -390,10 +390,11 @@ def iteration_params(base: Params, cfg: GenConfig, t: int) -> Params:
 def generate(hidden_of, W, E, e_mask, X0, cfg: GenConfig, base: Params, dense_credit=True, trace=None):
     """Run Algorithm 1's block loop on token rows X0 [B, L].
 
-    hidden_of(n, tokens_blk, mask_blk) -> [B, S, H] float64 hidden states of
-    global iteration n (the model stand-in).  Returns dict(X, F, T,
-    truncated).  `trace`, when a list, receives per-iteration dicts (block,
-    t, params, state before, step result)."""
+    hidden_of(n, state) -> [B, S, H] float64 hidden states of global
+    iteration n (the model stand-in); state = dict(block, t, tokens, mask, C,
+    params) before the step.  Returns dict(X, F, T, truncated).  `trace`,
+    when a list, receives per-iteration dicts (block, t, params, state
+    before, step result)."""
     X = np.array(X0, dtype=np.int64, copy=True)
     B, L = X.shape
     S, P = cfg.S, cfg.prompt_len
@@ -418,7 +419,7 @@ def generate(hidden_of, W, E, e_mask, X0, cfg: GenConfig, base: Params, dense_cr
                 truncated = True
                 break
             p = iteration_params(base, cfg, t)
-            h = hidden_of(F, tokens, mask)
+            h = hidden_of(F, dict(block=k, t=t, tokens=tokens, mask=mask, C=C, params=p))
             res = step(h, W, E, e_mask, mask, tokens, C, p)
             if trace is not None:
                 trace.append(dict(block=k, t=t, params=p, mask=mask.copy(), tokens=tokens.copy(),

@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "dinfer.h"
 #include "kernels.h"
@@ -75,6 +76,20 @@ struct dinfer_ctx {
   uint64_t host_graph_key[12] = {};
   bool host_graph_failed = false;
   cudaStream_t cap_stream = nullptr;  // private capture stream
+  // dinfer_generate: block-local state, loop state and the cached loop graph
+  uint8_t* g_mask = nullptr;
+  int32_t* g_tok = nullptr;
+  int32_t* g_cids = nullptr;
+  float* g_cval = nullptr;
+  uint8_t* g_com = nullptr;
+  float* g_sm = nullptr;
+  float* g_pdev = nullptr;
+  int* g_st = nullptr;
+  uint16_t* g_hbuf = nullptr;
+  cudaGraphExec_t gen_exec = nullptr;
+  uint64_t gen_key[10] = {};
+  dinfer_gen_config gen_cfg{};
+  dinfer_params gen_base{};
   bool host_graph_ok = true;           // env DINFER_HOST_GRAPH=0 disables the graph (measurement)
   const float* pdev_active = nullptr;  // device params the kernels read (set while capturing)
   // tensor-map cache
@@ -425,12 +440,14 @@ void dinfer_destroy(dinfer_ctx* c) {
                   c->mref,
                   c->mask_snap,
                   c->grp_cnt, c->grp_pass,
-                  c->st_hidden, c->st_block, c->st_smoothed};
+                  c->st_hidden, c->st_block, c->st_smoothed,
+                  c->g_mask, c->g_tok, c->g_cids, c->g_cval, c->g_com, c->g_sm, c->g_pdev, c->g_st, c->g_hbuf};
   for (void* b : bufs)
     if (b != nullptr) cudaFree(b);
   if (c->rec_all != nullptr && c->rec_all != c->rec_local) cudaFree(c->rec_all);
   if (c->st_host != nullptr) cudaFreeHost(c->st_host);
   if (c->host_graph != nullptr) cudaGraphExecDestroy(c->host_graph);
+  if (c->gen_exec != nullptr) cudaGraphExecDestroy(c->gen_exec);
   if (c->cap_stream != nullptr) cudaStreamDestroy(c->cap_stream);
   for (int i = 0; i < kNumPhases; ++i) {
     if (c->ev_beg[i]) cudaEventDestroy(c->ev_beg[i]);
@@ -833,6 +850,169 @@ dinfer_status dinfer_step_host(dinfer_ctx* c, const uint16_t* hidden_h, const ui
     std::memcpy(cval_h, hs + o_cval, 4 * M * K);
   }
   if (stats_h != nullptr) std::memcpy(stats_h, hs + o_stats, 16 * M);
+  return DINFER_OK;
+}
+
+// ---------------------------------------------------------------- generation loop
+namespace {
+
+// Build the loop graph: gen_init -> WHILE { hidden stand-in -> step -> gen_control }.
+dinfer_status build_gen_graph(dinfer_ctx* c, const GenArgs& ga, const uint16_t* W, const uint16_t* E,
+                              const uint16_t* e_mask, const dinfer_params* base, bool pdl, cudaGraphExec_t* exec) {
+  cudaGraph_t g = nullptr;
+  DI_CUDA(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  auto fail = [&](const char* where, cudaError_t e) {
+    note_error(where, cudaGetErrorString(e));
+    cudaGetLastError();
+    if (g != nullptr) cudaGraphDestroy(g);
+    return DINFER_ERR_CUDA;
+  };
+  cudaError_t e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+  if (e != cudaSuccess) return fail("cudaGraphConditionalHandleCreate", e);
+  if (c->cap_stream == nullptr) DI_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  cudaStream_t cs = c->cap_stream;
+  if ((e = cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)) != cudaSuccess)
+    return fail("cudaStreamBeginCaptureToGraph(init)", e);
+  cudaError_t le = launch_gen_init(ga, h, cs);
+  cudaGraph_t gg = g;
+  e = cudaStreamEndCapture(cs, &gg);
+  if (le != cudaSuccess) return fail("gen_init capture", le);
+  if (e != cudaSuccess) return fail("cudaStreamEndCapture(init)", e);
+  size_t n = 0;
+  cudaGraphGetNodes(g, nullptr, &n);
+  std::vector<cudaGraphNode_t> nodes(n);
+  cudaGraphGetNodes(g, nodes.data(), &n);
+  cudaGraphNodeParams np{};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t cn;
+  if ((e = cudaGraphAddNode(&cn, g, nodes.data(), n, &np)) != cudaSuccess) return fail("cudaGraphAddNode(while)", e);
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  if ((e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)) != cudaSuccess)
+    return fail("cudaStreamBeginCaptureToGraph(body)", e);
+  const cudaStream_t user_stream = c->stream;
+  const bool user_pdl = c->pdl, user_timing = c->timing;
+  c->stream = cs;
+  c->pdl = pdl;
+  c->timing = false;
+  c->pdev_active = ga.pdev;
+  le = launch_gen_hidden(ga, c->num_sms, cs);
+  dinfer_status st = DINFER_OK;
+  if (le == cudaSuccess)
+    st = dinfer_step(c, ga.hbuf, W, E, e_mask, ga.mask, ga.tokens, base->use_credit ? ga.cids : nullptr,
+                     base->use_credit ? ga.cval : nullptr, base, c->g_com, base->use_smooth ? c->g_sm : nullptr,
+                     nullptr);
+  if (le == cudaSuccess && st == DINFER_OK) le = launch_gen_control(ga, h, cs);
+  c->stream = user_stream;
+  c->pdl = user_pdl;
+  c->timing = user_timing;
+  c->pdev_active = nullptr;
+  cudaGraph_t bb = body;
+  e = cudaStreamEndCapture(cs, &bb);
+  if (st != DINFER_OK) {
+    cudaGetLastError();
+    cudaGraphDestroy(g);
+    return st;
+  }
+  if (le != cudaSuccess) return fail("loop body capture", le);
+  if (e != cudaSuccess) return fail("cudaStreamEndCapture(body)", e);
+  if ((e = cudaGraphInstantiate(exec, g, 0)) != cudaSuccess) return fail("cudaGraphInstantiate(loop)", e);
+  cudaGraphDestroy(g);
+  return DINFER_OK;
+}
+
+}  // namespace
+
+dinfer_status dinfer_generate(dinfer_ctx* c, const dinfer_gen_config* cfg, const dinfer_params* base,
+                              const uint16_t* W, const uint16_t* E, const uint16_t* e_mask,
+                              const uint16_t* hidden_src, int64_t hidden_iters, int32_t* X, int32_t* out) {
+  if (c == nullptr || cfg == nullptr || base == nullptr || W == nullptr || hidden_src == nullptr || X == nullptr ||
+      out == nullptr || hidden_iters < 1)
+    return DINFER_ERR_ARG;
+  if (c->shp.world != 1) return DINFER_ERR_UNSUPPORTED;
+  dinfer_status s = check_params(c, base);
+  if (s != DINFER_OK) return s;
+  const int B = c->shp.B, S = c->shp.S, K = c->shp.K, M = c->M;
+  const long H = c->shp.H;
+  if (cfg->prompt_len < 0 || cfg->L <= cfg->prompt_len || (cfg->L - cfg->prompt_len) % S != 0 || B > 1024)
+    return DINFER_ERR_SHAPE;
+  if (cfg->mask_id < 0 || cfg->mask_id >= c->shp.V_total || cfg->eos_id < 0 || cfg->eos_id >= c->shp.V_total ||
+      cfg->mask_id == cfg->eos_id || cfg->max_forwards < 1 || !(cfg->tau_target >= 0.f && cfg->tau_target <= 1.f))
+    return DINFER_ERR_ARG;
+  if (base->use_smooth && (E == nullptr || e_mask == nullptr)) return DINFER_ERR_ARG;
+  if (!aligned(hidden_src, 16) || !aligned(W, 16)) return DINFER_ERR_SHAPE;
+  if (c->g_st == nullptr) {  // first call: block-local state, loop state, hidden buffer
+    dinfer_status st = DINFER_OK;
+    auto A = [&](dinfer_status x) { if (st == DINFER_OK) st = x; };
+    A(dev_alloc(&c->g_mask, static_cast<size_t>(M)));
+    A(dev_alloc(&c->g_tok, static_cast<size_t>(M)));
+    A(dev_alloc(&c->g_cids, static_cast<size_t>(M) * K));
+    A(dev_alloc(&c->g_cval, static_cast<size_t>(M) * K));
+    A(dev_alloc(&c->g_com, static_cast<size_t>(M)));
+    if (c->shp.smooth_capable) A(dev_alloc(&c->g_sm, static_cast<size_t>(M) * H));
+    A(dev_alloc(&c->g_pdev, 8));
+    A(dev_alloc(&c->g_st, static_cast<size_t>(4 + B)));
+    A(dev_alloc(&c->g_hbuf, static_cast<size_t>(M) * H));
+    if (st != DINFER_OK) return st;
+  }
+  const uint64_t key[10] = {reinterpret_cast<uint64_t>(X), reinterpret_cast<uint64_t>(W),
+                            reinterpret_cast<uint64_t>(E), reinterpret_cast<uint64_t>(e_mask),
+                            reinterpret_cast<uint64_t>(hidden_src), static_cast<uint64_t>(hidden_iters),
+                            reinterpret_cast<uint64_t>(out), reinterpret_cast<uint64_t>(c->stream), 0, 0};
+  const bool same = c->gen_exec != nullptr && std::memcmp(key, c->gen_key, sizeof(key)) == 0 &&
+                    std::memcmp(cfg, &c->gen_cfg, sizeof(*cfg)) == 0 && std::memcmp(base, &c->gen_base, sizeof(*base)) == 0;
+  if (!same) {
+    if (c->gen_exec != nullptr) {
+      cudaGraphExecDestroy(c->gen_exec);
+      c->gen_exec = nullptr;
+    }
+    GenArgs ga{};
+    ga.B = B;
+    ga.S = S;
+    ga.L = cfg->L;
+    ga.P = cfg->prompt_len;
+    ga.K = K;
+    ga.nblocks = (cfg->L - cfg->prompt_len) / S;
+    ga.mask_id = cfg->mask_id;
+    ga.eos_id = cfg->eos_id;
+    ga.early = cfg->early_termination != 0;
+    ga.decoder = base->decoder;
+    ga.use_smooth = base->use_smooth != 0;
+    ga.use_credit = base->use_credit != 0;
+    ga.max_forwards = cfg->max_forwards;
+    ga.tau_target = cfg->tau_target;
+    ga.tau_decay = cfg->tau_decay_steps;
+    ga.a_init = cfg->alpha_init;
+    ga.a_growth = cfg->alpha_growth;
+    ga.a_preset = cfg->alpha_preset;
+    const float bp[8] = {base->tau, base->theta_hi, base->theta_lo, base->c_alpha, base->c_beta, base->c_gamma,
+                         base->alpha_t, 0.f};
+    std::memcpy(ga.base, bp, sizeof(bp));
+    ga.X = X;
+    ga.mask = c->g_mask;
+    ga.tokens = c->g_tok;
+    ga.cids = c->g_cids;
+    ga.cval = c->g_cval;
+    ga.pdev = c->g_pdev;
+    ga.st = c->g_st;
+    ga.out = out;
+    ga.hsrc = hidden_src;
+    ga.hsrc_iters = hidden_iters;
+    ga.MH = static_cast<long>(M) * H;
+    ga.hbuf = c->g_hbuf;
+    cudaGraphExec_t ex = nullptr;
+    s = build_gen_graph(c, ga, W, E, e_mask, base, c->pdl, &ex);
+    if (s == DINFER_ERR_CUDA && c->pdl) s = build_gen_graph(c, ga, W, E, e_mask, base, false, &ex);
+    if (s != DINFER_OK) return s;
+    c->gen_exec = ex;
+    std::memcpy(c->gen_key, key, sizeof(key));
+    c->gen_cfg = *cfg;
+    c->gen_base = *base;
+  }
+  DI_CUDA(cudaGraphLaunch(c->gen_exec, c->stream));
   return DINFER_OK;
 }
 

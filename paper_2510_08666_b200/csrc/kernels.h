@@ -148,4 +148,28 @@ struct K4Args {
 // K3 + K4 in one launch (a4 == nullptr: selection only)
 cudaError_t launch_k34(const K3Args& a3, const K4Args* a4, cudaStream_t st, bool pdl);
 
+// ---------------------------------------------------------------- generation loop (gen_loop.cu)
+struct GenArgs {
+  int B, S, L, P, K, nblocks;   // rows, block size, row length, prompt length, credit slots
+  int mask_id, eos_id, early, decoder, use_smooth, use_credit, max_forwards;
+  float tau_target;
+  int tau_decay;
+  float a_init, a_growth, a_preset;
+  float base[8];                // step params [tau, theta_hi, theta_lo, c_alpha, c_beta, c_gamma, alpha_t, 0]
+  int32_t* X;                   // [B][L] token rows (caller's, in/out)
+  uint8_t* mask;                // block-local state the step runs on: [B][S]
+  int32_t* tokens;              // [B][S]
+  int32_t* cids;                // [B][S][K]
+  float* cval;                  // [B][S][K]
+  float* pdev;                  // [8] per-iteration step params (read by K34)
+  int* st;                      // [4 + B]: block, t, F, truncated, row_done[B]
+  int32_t* out;                 // [B + 2]: T[b], F, truncated (caller's)
+  const uint16_t* hsrc;         // model stand-in: [hsrc_iters][M][H] bf16
+  long hsrc_iters, MH;
+  uint16_t* hbuf;               // [M][H] the step's hidden input
+};
+cudaError_t launch_gen_init(const GenArgs& a, cudaGraphConditionalHandle h, cudaStream_t st);
+cudaError_t launch_gen_control(const GenArgs& a, cudaGraphConditionalHandle h, cudaStream_t st);
+cudaError_t launch_gen_hidden(const GenArgs& a, int grid, cudaStream_t st);
+
 }  // namespace dinfer

@@ -42,6 +42,21 @@ class Params(ctypes.Structure):
                 ("c_beta", c_float), ("c_gamma", c_float), ("use_smooth", c_int32), ("alpha_t", c_float)]
 
 
+class GenConfig(ctypes.Structure):
+    """dinfer_gen_config (include/dinfer.h): the block loop of Algorithm 1."""
+    _fields_ = [("L", c_int32), ("prompt_len", c_int32), ("mask_id", c_int32), ("eos_id", c_int32),
+                ("early_termination", c_int32), ("tau_target", c_float), ("tau_decay_steps", c_int32),
+                ("alpha_init", c_float), ("alpha_growth", c_float), ("alpha_preset", c_float),
+                ("max_forwards", c_int32)]
+
+
+def make_gen_config(L, prompt_len, mask_id, eos_id, early_termination=True, tau_target=0.9, tau_decay_steps=0,
+                    alpha_init=0.1, alpha_growth=0.05, alpha_preset=0.3, max_forwards=1 << 30) -> GenConfig:
+    return GenConfig(int(L), int(prompt_len), int(mask_id), int(eos_id), int(bool(early_termination)),
+                     float(tau_target), int(tau_decay_steps), float(alpha_init), float(alpha_growth),
+                     float(alpha_preset), int(max_forwards))
+
+
 class Geometry(ctypes.Structure):
     _fields_ = [(n, c_int32) for n in ("k1_grid", "k1_stages", "k1_h_resident", "k1_smem", "k2_grid", "k2_hw",
                                         "k2_groups", "k2_stages", "k2_smem", "num_sms")]
@@ -80,6 +95,7 @@ def lib():
         "dinfer_launches_per_step": (S, [P, POINTER(Params)]),
         "dinfer_get_geometry": (S, [P, POINTER(Geometry)]),
         "dinfer_get_trace": (S, [P, P, S]),
+        "dinfer_generate": (S, [P, POINTER(GenConfig), POINTER(Params), P, P, P, P, c_int64, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -168,6 +184,14 @@ class Context:
         _check(lib().dinfer_step_host(self._h, _ptr(hidden_h), _ptr(W), _ptr(E), _ptr(e_mask), _ptr(mask_h),
                                       _ptr(tokens_h), _ptr(credit_ids_h), _ptr(credit_val_h), ctypes.byref(params),
                                       _ptr(committed_h), _ptr(smoothed_h), _ptr(stats_h)), "dinfer_step_host")
+
+    def generate(self, cfg: GenConfig, base: Params, W, E, e_mask, hidden_src, X, out):
+        """Device-resident block loop (Alg. 1) over X [B, L] int32; hidden_src
+        [iters, B*S, H] bf16 is the model stand-in; out int32 [B + 2] receives
+        T_b, F, truncated.  Asynchronous on the ctx stream."""
+        iters = int(hidden_src.shape[0])
+        _check(lib().dinfer_generate(self._h, ctypes.byref(cfg), ctypes.byref(base), _ptr(W), _ptr(E), _ptr(e_mask),
+                                     _ptr(hidden_src), iters, _ptr(X), _ptr(out)), "dinfer_generate")
 
     def record_words(self, use_smooth: bool) -> int:
         return int(lib().dinfer_record_words(self._h, int(bool(use_smooth))))

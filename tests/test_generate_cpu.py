@@ -43,7 +43,7 @@ def test_sequential_degeneration_one_commit_per_step():
     rng = np.random.default_rng(1)
     tgt = rng.integers(0, V - 2, size=(B, S))
     cfg = O.GenConfig(prompt_len=P, S=S, mask_id=MASK, eos_id=EOS, tau_target=1.0)
-    out = O.generate(lambda n, tok, m: _saturated(W, tgt, amp=8.0 + 0.1 * n), W64, None, None,
+    out = O.generate(lambda n, st: _saturated(W, tgt, amp=8.0 + 0.1 * n), W64, None, None,
                      _X0(B, P, nb), cfg, O.Params(decoder=O.DEC_THRESHOLD, tau=1.0))
     assert out["F"] == nb * S
     assert not (out["X"] == MASK).any()
@@ -58,7 +58,7 @@ def test_saturated_confidence_one_forward_per_block():
     tgts = rng.integers(0, V - 2, size=(nb, B, S))
     cfg = O.GenConfig(prompt_len=P, S=S, mask_id=MASK, eos_id=EOS, tau_target=0.9)
     X0 = _X0(B, P, nb)
-    out = O.generate(lambda n, tok, m: _saturated(W, tgts[n]), W64, None, None, X0, cfg,
+    out = O.generate(lambda n, st: _saturated(W, tgts[n]), W64, None, None, X0, cfg,
                      O.Params(decoder=O.DEC_THRESHOLD, tau=0.9))
     assert out["F"] == nb
     assert np.array_equal(out["X"][:, :P], X0[:, :P])            # prompt untouched
@@ -75,7 +75,7 @@ def _eos_run(early, B=1):
     tgts[1, 0, 7] = EOS                      # row 0 emits EOS in block 1 at offset 7
     cfg = O.GenConfig(prompt_len=P, S=S, mask_id=MASK, eos_id=EOS, tau_target=0.9,
                       early_termination=early)
-    out = O.generate(lambda n, tok, m: _saturated(W, tgts[min(n, nb - 1)]), W64, None, None,
+    out = O.generate(lambda n, st: _saturated(W, tgts[min(n, nb - 1)]), W64, None, None,
                      _X0(B, P, nb), cfg, O.Params(decoder=O.DEC_THRESHOLD, tau=0.9))
     return out, P, nb
 
@@ -136,7 +136,7 @@ def test_credit_table_resets_at_every_block():
     sch = [synth.PlantedSchedule(B * S, V, H, seed=10 + k) for k in range(nb)]
     hid = {}
 
-    def hidden_of(n, tok, m):
+    def hidden_of(n, st):
         if n not in hid:
             k = 0 if n < 3 else 1
             tgt, a = sch[k].targets_and_amplitudes(n)

@@ -99,3 +99,61 @@ def vetted_trajectory(W_u16, E_u16, B, S, seed, params_fn, max_iters=None,
             C = res["C"]
         t += 1
     return W64, E64, em64, steps
+
+
+def vetted_generation(W_u16, E_u16, B, S, nblocks, prompt_len, seed, base: O.Params, cfg: O.GenConfig,
+                      eos_at=(), ramp=2.5, flip_prob=0.1, max_rounds=400):
+    """A whole blockwise generation (Alg. 1) driven by planted hidden states,
+    every iteration vetted against the decision margins (c19) on the oracle's
+    carried state.  Block k draws from PlantedSchedule(seed*100 + k); eos_at =
+    [(row, block, offset)] plants eos_id as that position's target.
+    Returns (hidden [F, B*S, H] u16, X0 [B, L], oracle result)."""
+    V, H = W_u16.shape
+    M = B * S
+    W64 = O.bf16_bits_to_f64(W_u16)
+    E64 = O.bf16_bits_to_f64(E_u16)
+    em64 = E64[cfg.mask_id]
+    rng = np.random.default_rng(np.random.SeedSequence([seed, 4242]))
+    L = prompt_len + nblocks * S
+    X0 = np.full((B, L), cfg.mask_id, dtype=np.int64)
+    X0[:, :prompt_len] = rng.integers(0, V - 2, size=(B, prompt_len))
+    schedules = {}
+    hidden = []
+
+    def hidden_of(n, st):
+        k, t = st["block"], st["t"]
+        if k not in schedules:
+            sch = synth.PlantedSchedule(M, V, H, seed * 100 + k, ramp=ramp, flip_prob=flip_prob)
+            for (r, blk, off) in eos_at:
+                if blk == k:
+                    sch.tgt[r * S + off] = cfg.eos_id
+            schedules[k] = sch
+        sch = schedules[k]
+        p, mask, tokens, C = st["params"], st["mask"], st["tokens"], st["C"]
+        tgt, a = sch.targets_and_amplitudes(t)
+        h = sch.hidden(W_u16[tgt], a).reshape(B, S, H)
+        redraws = np.zeros(M, dtype=int)
+        for _round in range(max_rounds):
+            h64 = O.bf16_bits_to_f64(h)
+            f = np.stack([O.logits(h64[b], W64) for b in range(B)])
+            res = O.step(h64, W64, E64, em64, mask, tokens, C, p, f=f)
+            bad = _offenders(f, res, res["C"] if p.use_credit else None, mask, p)
+            if not bad:
+                break
+            rows = np.array(sorted(bad))
+            redraws[rows] += 1
+            base_rows = rows[redraws[rows] % 25 == 0]
+            if len(base_rows):
+                sch.redraw_base(base_rows)
+                a[base_rows] = sch.a0[base_rows] + sch.ramp * np.maximum(0, t - sch.onset[base_rows]) + 0.5
+            hf = h.reshape(M, H)
+            hf[rows] = sch.hidden(W_u16[tgt[rows]], a[rows])
+            h = hf.reshape(B, S, H)
+        else:
+            raise RuntimeError("vetting did not converge")
+        assert n == len(hidden)
+        hidden.append(h.reshape(M, H).copy())
+        return O.bf16_bits_to_f64(h)
+
+    out = O.generate(hidden_of, W64, E64, em64, X0, cfg, base)
+    return np.stack(hidden), X0, out
