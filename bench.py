@@ -357,8 +357,11 @@ def gpu_arm(args):
         k1_bytes = Vl * H * 2 + M * H * 2
         k2_bytes = (Vl * H * 2 + M * H * 4) if smooth else 0
         k1_ms, k2_ms = phases.get("k1_vocab_proj", 0.0), phases.get("k2_smooth_mix", 0.0)
-        dom, dom_bytes, dom_ms = ("k1_vocab_proj", k1_bytes, k1_ms) if k1_ms >= k2_ms else \
-            ("k2_smooth_mix", k2_bytes, k2_ms)
+        if smooth and geom.get("fused"):  # K12: W and E streams in one kernel (timed in the K1 phase slot)
+            dom, dom_bytes, dom_ms = "k12_proj_smooth", k1_bytes + k2_bytes, k1_ms
+        else:
+            dom, dom_bytes, dom_ms = ("k1_vocab_proj", k1_bytes, k1_ms) if k1_ms >= k2_ms else \
+                ("k2_smooth_mix", k2_bytes, k2_ms)
         traffic = ncu_traffic().get(f"{CFG['name']}/" + (dom if M <= 256 else "k1b_vocab_proj_dense"))
         step_bytes = k1_bytes + k2_bytes
         if M > 256:  # compute-bound regime (BASELINE configs[4]): tensor roofline of K1b

@@ -276,6 +276,9 @@ typedef struct {
   int32_t k1_grid, k1_stages, k1_h_resident, k1_smem;
   int32_t k2_grid, k2_hw, k2_groups, k2_stages, k2_smem;
   int32_t num_sms;
+  int32_t fused;       /* 1: smoothing steps run K1+K2 as one kernel (K12); its
+                          E phase is described by k2_hw / k2_groups / k2_stages */
+  int32_t fused_smem;
 } dinfer_geometry;
 dinfer_status dinfer_get_geometry(const dinfer_ctx* ctx, dinfer_geometry* out);
 

@@ -51,6 +51,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd += ["-Xptxas", "-v"]
     if inc:
         cmd += ["-DDINFER_WITH_NCCL", "-I", inc]
+    cmd += os.environ.get("DINFER_EXTRA_NVCC", "").split()  # diagnostics, e.g. -DDINFER_DEBUG_HANG
     cmd += sources()
     tmp = LIB + ".tmp"
     cmd += ["-o", tmp]

@@ -5,6 +5,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #define DI __device__ __forceinline__
 
@@ -50,7 +51,14 @@ DI void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t spins = 0;
   while (!mbar_try_wait(a, parity)) {
+#ifdef DINFER_DEBUG_HANG
+    if (++spins > (1u << 26)) {
+      printf("mbar hang: block %d thread %d bar smem+%u parity %u\n", blockIdx.x, threadIdx.x, a, parity);
+      __trap();
+    }
+#else
     if (++spins > (1u << 26)) __trap();
+#endif
   }
 }
 

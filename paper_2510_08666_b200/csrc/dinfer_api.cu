@@ -48,6 +48,12 @@ struct dinfer_ctx {
   size_t k1_smem = 0;
   int k2_HW = 0, k2_HS = 0, k2_VG = 0, k2_stages = 0, k2_pstages = 0, k2_nchunks = 0, k2_KV = 64;
   size_t k2_smem = 0;
+  // K12 (K1 + K2 fused, smoothing steps with N <= 64): the k2_* fields then
+  // describe its E phase (HW, HS, VG, KV = 16) and k1_VG x k1_SPG its slabs
+  bool fused = false;
+  int* probe_h = nullptr;  // DINFER_K12_PROBE: mapped pinned host progress words
+  int f_stages = 0, f_pstages = 0;
+  size_t f_smem = 0;
   // workspace (device)
   float* part1 = nullptr;
   unsigned* counter = nullptr;
@@ -255,10 +261,56 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
   a.mask_snap = smooth ? c->mask_snap : nullptr;
   a.err = c->err;
   a.trace = c->trace;
-  ev_begin(c, kPK1);
-  DI_CUDA(launch_k1(c->map_w, c->map_w8, c->map_h, a, c->k1_grid, c->k1_smem, c->stream, c->pdl));
-  ev_finish(c, kPK1);
-  if (smooth) {
+  if (smooth && c->fused) {
+    // K12: the vocab slab partition at 16-row chunk granularity (nchunks /
+    // chunk_rows), the E phase over the slab's vocab group
+    a.stages = c->f_stages;
+    a.nchunks = c->k2_nchunks;
+    a.chunk_rows = kChunkRows12;
+    K2Args b{};
+    b.M = c->M;
+    b.N = c->N;
+    b.H = c->shp.H;
+    b.V_local = static_cast<int>(c->shp.V_local);
+    b.HW = c->k2_HW;
+    b.nsub = c->k2_HW / 128;
+    b.HS = c->k2_HS;
+    b.VG = c->k2_VG;
+    b.nchunks = c->k2_nchunks;
+    b.KV = kChunkRows12;
+    b.stages = c->f_stages;
+    b.pstages = c->f_pstages;
+    b.flog = c->flog;
+    b.part1 = reinterpret_cast<const float4*>(c->part1);
+    b.grid1 = c->k1_grid;
+    b.SPG = c->k1_SPG;
+    b.grp_cnt = c->grp_cnt;
+    b.grp_pass = c->grp_pass;
+    b.mref = c->mref;
+    b.part = c->part2;
+    b.trace = c->trace == nullptr ? nullptr : c->trace + 5 * c->k1_grid;
+    if (std::getenv("DINFER_K12_PROBE") != nullptr) {
+      if (c->probe_h == nullptr) {
+        void* hp = nullptr;
+        if (cudaHostAlloc(&hp, 64 * 4 * 1024, cudaHostAllocMapped) == cudaSuccess) {
+          std::memset(hp, 0xff, 64 * 4 * 1024);
+          c->probe_h = static_cast<int*>(hp);
+        }
+      }
+      void* dp = nullptr;
+      if (c->probe_h != nullptr && cudaHostGetDevicePointer(&dp, c->probe_h, 0) == cudaSuccess)
+        b.probe = static_cast<volatile int*>(dp);
+    }
+    ev_begin(c, kPK1);
+    DI_CUDA(launch_k12(c->map_w, c->map_w8, c->map_h, c->map_e, c->map_f, a, b, c->k1_grid, c->f_smem, c->stream,
+                       c->pdl));
+    ev_finish(c, kPK1);
+  } else {
+    ev_begin(c, kPK1);
+    DI_CUDA(launch_k1(c->map_w, c->map_w8, c->map_h, a, c->k1_grid, c->k1_smem, c->stream, c->pdl));
+    ev_finish(c, kPK1);
+  }
+  if (smooth && !c->fused) {
     K2Args b{};
     b.M = c->M;
     b.N = c->N;
@@ -509,7 +561,52 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
     // chunks.  The accumulator (HW/128 x N columns) must fit the 512-column TMEM.
     int hw_pref = 1024;
     if (const char* e = std::getenv("DINFER_K2_HW")) hw_pref = std::atoi(e);  // tuning override: 128 .. 1024
-    c->k2_stages = 0;
+    bool want_fused = s.smooth_capable && c->N <= 64;
+    if (const char* e = std::getenv("DINFER_FUSED")) want_fused = want_fused && std::atoi(e) != 0;
+    if (want_fused) {
+      // ---- K12 geometry: hidden slices of HW columns (the widest power of two
+      // <= 1024 dividing H whose accumulator set, HW/128 x N columns, fits half
+      // the TMEM), HS = H/HW slabs per vocab group, VG groups of 16-row chunks.
+      int hw = 0;
+      for (int w = 1024; w >= 128 && hw == 0; w /= 2)
+        if (w <= hw_pref && s.H % w == 0 && (w / 128) * c->N <= 256) hw = w;
+      const int nch = static_cast<int>((s.V_local + kChunkRows12 - 1) / kChunkRows12);
+      const int HS = hw > 0 ? s.H / hw : 0;
+      if (hw > 0 && HS <= c->num_sms) {
+        const int VG = std::max(1, std::min(c->num_sms / HS, nch));
+        int srm = 0;  // largest slab (16-row chunk granularity, same arithmetic as the kernel)
+        for (int g = 0; g < VG; ++g) {
+          const long g0 = static_cast<long>(g) * nch / VG, g1 = static_cast<long>(g + 1) * nch / VG;
+          for (int q = 0; q < HS; ++q) {
+            const long a0 = g0 + q * (g1 - g0) / HS, a1 = g0 + (q + 1) * (g1 - g0) / HS;
+            srm = std::max<int>(srm, static_cast<int>((a1 - a0) * kChunkRows12));
+          }
+        }
+        int st_max = 6, pst_max = 4;  // tuning overrides (measurement only)
+        if (const char* e = std::getenv("DINFER_K12_STAGES")) st_max = std::max(3, std::atoi(e));
+        if (const char* e = std::getenv("DINFER_K12_PSTAGES")) pst_max = std::max(2, std::atoi(e));
+        for (int st = st_max; st >= 3 && c->f_stages == 0; --st)
+          for (int pst = pst_max; pst >= 2; --pst)
+            if (k12_smem_bytes(c->N, hw, st, pst, srm) <= c->smem_optin) {
+              c->f_stages = st;
+              c->f_pstages = pst;
+              break;
+            }
+        if (c->f_stages > 0) {
+          c->fused = true;
+          c->k2_HW = hw;
+          c->k2_KV = kChunkRows12;
+          c->k2_HS = HS;
+          c->k2_VG = VG;
+          c->k2_nchunks = nch;
+          c->k2_stages = c->f_stages;
+          c->k2_pstages = c->f_pstages;
+          c->f_smem = k12_smem_bytes(c->N, hw, c->f_stages, c->f_pstages, srm);
+          c->slab_rows_max = srm;
+        }
+      }
+    }
+    if (!c->fused) c->k2_stages = 0;
     for (int hw = 1024; hw >= 128 && c->k2_stages == 0; hw /= 2) {
       if (hw > hw_pref || s.H % hw != 0 || (hw / 128) * c->N > 512) continue;
       const int kv = hw == 1024 ? 32 : 64;
@@ -523,17 +620,22 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
             break;
           }
     }
-    c->k2_nchunks = static_cast<int>((s.V_local + c->k2_KV - 1) / c->k2_KV);
     if (c->k2_stages == 0) { delete c; return DINFER_ERR_UNSUPPORTED; }
-    c->k2_HS = s.H / c->k2_HW;
-    c->k2_VG = std::max(1, std::min(c->num_sms / std::max(1, c->k2_HS), c->k2_nchunks));
-    c->k2_smem = k2_smem_bytes(c->N, c->k2_HW, c->k2_KV, c->k2_stages, c->k2_pstages);
+    if (!c->fused) {
+      c->k2_nchunks = static_cast<int>((s.V_local + c->k2_KV - 1) / c->k2_KV);
+      c->k2_HS = s.H / c->k2_HW;
+      c->k2_VG = std::max(1, std::min(c->num_sms / std::max(1, c->k2_HS), c->k2_nchunks));
+      c->k2_smem = k2_smem_bytes(c->N, c->k2_HW, c->k2_KV, c->k2_stages, c->k2_pstages);
+    }
     // ---- K1 geometry: one CTA per SM over contiguous vocab slabs.  With the
     // smoothing workspace the slabs nest in K2's vocab groups (SPG slabs per
     // group, group boundaries on 64-row chunks) so a K2 CTA depends only on
     // its group's slabs; each slab is balanced at 8-row granularity.
     const int nch = static_cast<int>((s.V_local + c->k2_KV - 1) / c->k2_KV);
-    if (s.smooth_capable) {
+    if (c->fused) {  // K1-only steps use the same groups x slabs as K12
+      c->k1_VG = c->k2_VG;
+      c->k1_SPG = c->k2_HS;
+    } else if (s.smooth_capable) {
       c->k1_VG = c->k2_VG;
       const long grp_rows = (s.V_local + c->k1_VG - 1) / c->k1_VG;
       c->k1_SPG = static_cast<int>(std::max<long>(1, std::min<long>(c->num_sms / c->k1_VG,
@@ -543,7 +645,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
       c->k1_SPG = static_cast<int>(std::min<long>(c->num_sms, std::max<long>(1, (s.V_local + kTileRows - 1) / kTileRows)));
     }
     c->k1_grid = c->k1_VG * c->k1_SPG;
-    c->slab_rows_max = 0;
+    if (!c->fused) c->slab_rows_max = 0;
     for (int g = 0; g < c->k1_VG; ++g) {  // same arithmetic as the kernel
       const long rg0 = static_cast<long>(c->k2_KV) * (static_cast<long>(g) * nch / c->k1_VG);
       const long rg1 = std::min<long>(s.V_local, static_cast<long>(c->k2_KV) * (static_cast<long>(g + 1) * nch / c->k1_VG));
@@ -568,6 +670,16 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
     c->k1_stages = use_res ? st_res : st_str;
     if (c->k1_stages == 0) { delete c; return DINFER_ERR_UNSUPPORTED; }
     c->k1_smem = k1_smem_bytes(c->N, s.H, c->k1_stages, c->k1_hres, c->slab_rows_max);
+    if (c->fused) {  // the head table covers the larger of the K1 / K12 slabs
+      while (k12_smem_bytes(c->N, c->k2_HW, c->f_stages, c->f_pstages, c->slab_rows_max) > c->smem_optin) {
+        if (c->f_pstages > 2) --c->f_pstages;
+        else if (c->f_stages > 3) --c->f_stages;
+        else { delete c; return DINFER_ERR_UNSUPPORTED; }
+      }
+      c->k2_stages = c->f_stages;
+      c->k2_pstages = c->f_pstages;
+      c->f_smem = k12_smem_bytes(c->N, c->k2_HW, c->f_stages, c->f_pstages, c->slab_rows_max);
+    }
 
     if (const char* e = std::getenv("DINFER_PDL")) c->pdl = std::atoi(e) != 0;
   }
@@ -1071,11 +1183,14 @@ int32_t dinfer_get_trace(dinfer_ctx* c, uint64_t* out, int32_t n) {
   return k;
 }
 
+/* diagnostics: the K12 progress words (DINFER_K12_PROBE), readable after a fault */
+const int* dinfer_debug_probe(const dinfer_ctx* c) { return c == nullptr ? nullptr : c->probe_h; }
+
 int32_t dinfer_launches_per_step(const dinfer_ctx* c, const dinfer_params* p) {
   if (c == nullptr || p == nullptr) return 0;
   if (c->dense) return 2;  // K1b, K3
-  int n = 2;  // K1, K34
-  if (p->use_smooth) n += 1 + (c->shp.world > 1 ? 1 : 0);  // K2 (+ record finalize)
+  int n = 2;  // K1 (or K12), K34
+  if (p->use_smooth) n += (c->fused ? 0 : 1) + (c->shp.world > 1 ? 1 : 0);  // K2 (+ record finalize)
   else if (c->shp.world > 1) n += 1;                         // record finalize
   return n;
 }
@@ -1092,6 +1207,8 @@ dinfer_status dinfer_get_geometry(const dinfer_ctx* c, dinfer_geometry* g) {
   g->k2_stages = c->k2_stages;
   g->k2_smem = static_cast<int32_t>(c->k2_smem);
   g->num_sms = c->num_sms;
+  g->fused = c->fused ? 1 : 0;
+  g->fused_smem = static_cast<int32_t>(c->f_smem);
   return DINFER_OK;
 }
 

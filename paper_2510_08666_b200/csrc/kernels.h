@@ -13,7 +13,8 @@ constexpr int kTileRows = 128;     // UMMA M (vocab rows per tile)
 constexpr int kRowGran = 8;        // vocab-row granularity of the K1 partition
 constexpr int kMaxCreditEnt = 1024;  // per-CTA credited (position, slot) entries
 constexpr int kStatWords = 4;
-constexpr int kTraceK34 = 64;  // K34 blocks traced (DINFER_TRACE)      // m, idx, l, pad  (record header per row)
+constexpr int kTraceK34 = 64;     // K34 blocks traced (DINFER_TRACE)
+constexpr int kChunkRows12 = 32;  // K12: vocab rows per E chunk (two UMMA K steps)
 
 // Launch helper: optional programmatic dependent launch (PDL) attribute.
 template <typename... KArgs, typename... Args>
@@ -86,10 +87,20 @@ struct K2Args {
   float* mref;             // [VG][M] out: per-group reference max m_g (acc is relative to it)
   float* part;             // [VG][M][H]
   unsigned long long* trace;  // optional [grid][5]: globaltimer ns start, first E stage, MMAs done, exit; smid
+  volatile int* probe;     // K12 diagnostics (env DINFER_K12_PROBE): [grid][8] progress words in mapped host memory
 };
 size_t k2_smem_bytes(int N, int HW, int KV, int stages, int pstages);
 cudaError_t launch_k2(const CUtensorMap& map_e, const CUtensorMap& map_f, const K2Args& a, size_t smem,
                       cudaStream_t st, bool pdl);
+
+// ---------------------------------------------------------------- K12 (K1 + K2 fused, N <= 64)
+// Uses K1Args (W phase; VG x SPG slabs at 16-row chunk granularity,
+// nchunks / chunk_rows in 16-row chunks) and K2Args (E phase; HS == SPG
+// hidden slices of HW columns, pstages logits / P ring depth; stages unused).
+size_t k12_smem_bytes(int N, int HW, int stages, int pstages, int slab_rows_max);
+cudaError_t launch_k12(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
+                       const CUtensorMap& map_e, const CUtensorMap& map_f, const K1Args& a, const K2Args& b, int grid,
+                       size_t smem, cudaStream_t st, bool pdl);
 
 // Rank record finalize (sharded / split-phase path):
 //   stats: rec[s] = merge of K1's per-slab partials (fixed order);

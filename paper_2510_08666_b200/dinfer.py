@@ -59,7 +59,8 @@ def make_gen_config(L, prompt_len, mask_id, eos_id, early_termination=True, tau_
 
 class Geometry(ctypes.Structure):
     _fields_ = [(n, c_int32) for n in ("k1_grid", "k1_stages", "k1_h_resident", "k1_smem", "k2_grid", "k2_hw",
-                                        "k2_groups", "k2_stages", "k2_smem", "num_sms")]
+                                        "k2_groups", "k2_stages", "k2_smem", "num_sms", "fused",
+                                        "fused_smem")]
 
 
 _LIB = None

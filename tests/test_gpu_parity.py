@@ -97,6 +97,25 @@ def test_k1_hidden_resident_or_streamed(torch_cuda, monkeypatch, hres):
     run_trajectory(torch_cuda, 3000, 512, 2, 32, 32, 10, hier_credit_smooth, True, max_iters=4)
 
 
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_fused_and_two_kernel_smoothing_paths(torch_cuda, monkeypatch, fused):
+    """Smoothing steps run K12 (K1 + K2 in one kernel, N <= 64) or the two-kernel
+    K1 -> K2 path (DINFER_FUSED=0); both must match the oracle: ragged vocab /
+    odd shapes (V = 1000, H = 384, B = 3, S = 20), HS = 2 groups (H = 2048, the
+    other-slab accumulator set in use), N = 64 (B = 2, S = 32)."""
+    from paper_2510_08666_b200 import Context
+    monkeypatch.setenv("DINFER_FUSED", fused)
+    ctx = Context(1, 32, 2048, 32, 4096, smooth_capable=True)
+    g = ctx.geometry()
+    ctx.close()
+    assert g["fused"] == int(fused)
+    if fused == "1":
+        assert g["k2_hw"] == 1024 and g["k1_grid"] == 2 * g["k2_groups"]
+    run_trajectory(torch_cuda, 1000, 384, 3, 20, 24, 5, hier_credit_smooth, True, max_iters=5)
+    run_trajectory(torch_cuda, 4096, 2048, 1, 32, 32, 11, hier_credit_smooth, True, max_iters=4)
+    run_trajectory(torch_cuda, 2048, 1024, 2, 32, 32, 12, hier_credit_smooth, True, max_iters=3)
+
+
 def test_without_pdl(torch_cuda, monkeypatch):
     monkeypatch.setenv("DINFER_PDL", "0")
     run_trajectory(torch_cuda, 2048, 512, 2, 32, 32, 9, hier_credit_smooth, True, max_iters=4)
@@ -279,7 +298,12 @@ def test_credit_slot_overflow_is_reported(torch_cuda):
 @pytest.mark.slow
 def test_moe_shape_hier_credit_smooth(torch_cuda):
     """LLaDA-MoE shape (BASELINE configs[2]): H=2048, V=157184, block 32, bs1,
-    hierarchical + credit + smoothing; the first 4 iterations of a block."""
+    hierarchical + credit + smoothing; the first 4 iterations of a block, in
+    the launch configuration bench.py times (K12 fused, 148 CTAs)."""
+    from paper_2510_08666_b200 import Context
+    ctx = Context(1, 32, 2048, 32, 157184, smooth_capable=True)
+    assert ctx.geometry()["fused"] == 1
+    ctx.close()
     run_trajectory(torch_cuda, 157184, 2048, 1, 32, 32, 0, hier_credit_smooth, True, max_iters=4)
 
 

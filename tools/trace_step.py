@@ -58,6 +58,13 @@ if smooth:
     for i, n in enumerate(["start", "first MMA (E+P)", "MMAs done", "exit"]):
         row(n, k2[:, i])
     print(f"  step span: {us(k2[:, 3]).max():.1f} us (K1 start -> last K2 CTA exit)")
+    g = ctx.geometry()
+    if g.get("fused"):
+        e_bytes = V * H * 2 / len(k2)
+        dur = (k2[:, 2].astype(np.int64) - k2[:, 1].astype(np.int64)) / 1e3
+        wdur = (k1[:, 2].astype(np.int64) - k1[:, 1].astype(np.int64)) / 1e3
+        print(f"  K12 per-CTA W phase {np.median(wdur):.1f} us (med), E phase {np.median(dur):.1f} us (med) -> "
+              f"E {e_bytes / np.median(dur) / 1e3 * len(k2) / 1e3:.2f} TB/s aggregate at the median; geometry {g}")
 print(f"K34 ({len(k34)} traced blocks; the first B*ceil(S/8) are selection CTAs):")
 for i, n in enumerate(["start", "deps visible", "stats merged", "exit"]):
     row(n, k34[:, i])
