@@ -141,6 +141,20 @@ dinfer_status dinfer_step(dinfer_ctx* ctx, const uint16_t* hidden, const uint16_
                           const dinfer_params* params, uint8_t* committed, float* smoothed,
                           float* stats);
 
+/* dinfer_step plus the next iteration's model input (Fig. 3 /
+ * PAPER.md:152): emb [B,S,H] bf16 device out,
+ *   emb[s] = W_emb[tokens[s]]   for every position decided after this step
+ *            (decided earlier, or committed now: its new token's row),
+ *   emb[s] = bf16(e_{t+1}[s])   for positions still masked (= smoothed[s]).
+ * Written by the same K34 launch (no extra kernel).  Requires use_smooth,
+ * world == 1 (the embedding rows of committed tokens live on one rank) and
+ * M <= 256; else UNSUPPORTED.  emb must be 16-byte aligned.                 */
+dinfer_status dinfer_step_embed(dinfer_ctx* ctx, const uint16_t* hidden, const uint16_t* W_vocab,
+                                const uint16_t* E, const uint16_t* e_mask, uint8_t* mask,
+                                int32_t* tokens, int32_t* credit_ids, float* credit_val,
+                                const dinfer_params* params, uint8_t* committed, float* smoothed,
+                                float* stats, uint16_t* emb);
+
 /* Same step with HOST per-step buffers (weights stay on device): copies
  * hidden and the decode state host->device, runs dinfer_step, copies the
  * state and outputs back, and synchronises the stream before returning.

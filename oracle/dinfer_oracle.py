@@ -215,6 +215,29 @@ def smooth(f_rows: np.ndarray, E: np.ndarray, e_mask: np.ndarray, alpha_t: float
     return np.asarray(e_mask, np.float64)[None, :] + alpha_t * delta_e
 
 
+# ---------------------------------------------------------------------------
+# Next iteration's model input (Fig. 3 / P:152):
+# the embedding the model reads at iteration t+1 for each position of the
+# block.  Decided positions feed their token's row of the input embedding
+# W_emb (the ordinary lookup); positions still masked feed e_{t+1}, the
+# smoothed embedding -- "iteration smoothing ... only on masked positions"
+# (P:275), "retains logit-weighted embeddings" for the next iteration.
+# Reading c24: without smoothing a masked position would feed e_mask; this
+# output is defined for smoothing steps only (the CUDA path requires it).
+# ---------------------------------------------------------------------------
+def next_input_embedding(E: np.ndarray, tokens: np.ndarray, mask: np.ndarray,
+                         smoothed: np.ndarray) -> np.ndarray:
+    """tokens, mask: [B, S] after this step's commit; smoothed: [B, S, H]
+    (e_{t+1}, valid where mask).  Returns [B, S, H] float64."""
+    E = np.asarray(E, np.float64)
+    B, S = tokens.shape
+    out = np.empty((B, S, E.shape[1]))
+    for b in range(B):
+        for s in range(S):
+            out[b, s] = smoothed[b, s] if mask[b, s] else E[tokens[b, s]]
+    return out
+
+
 def alpha_schedule(alpha_init: float, alpha_growth: float, alpha_preset: float, t: int) -> float:
     """alpha_t = min(alpha_init + alpha_growth * t, alpha_preset)   (P:281)."""
     return min(alpha_init + alpha_growth * t, alpha_preset)

@@ -65,6 +65,7 @@ struct dinfer_ctx {
   float* ml = nullptr;
   float4* sel = nullptr;    // K34 phase-1 -> phase-2 exchange [M]
   int* row_cnt = nullptr;   // [B] K34 arrival counters
+  int* rowdone = nullptr;   // [M] K34 smoothing blocks done per row (next-input embedding handoff)
   uint8_t* mask_snap = nullptr;   // [M] step-start mask (K1 -> smoothing blocks of K34)
   float* mref = nullptr;          // [k2_VG][M] per-vocab-group reference max (K2 -> K4 / record finalize)
   unsigned* grp_cnt = nullptr;    // [k2_VG] K1 slabs done per vocab group (self-resetting)
@@ -361,8 +362,12 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
 dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, int world, bool acc_from_part2,
                           const uint16_t* e_mask, uint8_t* mask, int32_t* tokens, int32_t* credit_ids,
                           float* credit_val, const dinfer_params* p, uint8_t* committed, float* smoothed,
-                          float* stats, int rec_stride = -1) {
+                          float* stats, int rec_stride = -1, const uint16_t* E = nullptr, uint16_t* emb = nullptr) {
   K3Args k{};
+  k.H = c->shp.H;
+  k.E = E;
+  k.emb = emb;
+  k.rowdone = c->rowdone;
   k.trace = c->trace == nullptr ? nullptr : c->trace + 5 * (c->k1_grid + c->k2_HS * c->k2_VG);
   k.B = c->shp.B;
   k.S = c->shp.S;
@@ -414,6 +419,10 @@ dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, in
     }
     f.mask_start = c->mask_snap;
     f.e_mask = e_mask;
+    f.E = E;
+    f.emb = emb;
+    f.tokens = tokens;
+    f.rowdone = c->rowdone;
     f.alpha_t = p->alpha_t;
     f.out = smoothed;
   }
@@ -490,7 +499,7 @@ void dinfer_destroy(dinfer_ctx* c) {
 #endif
   void* bufs[] = {c->part1, c->counter, c->err, c->rec_local, c->flog, c->part2, c->ml, c->sel, c->row_cnt, c->trace,
                   c->mref,
-                  c->mask_snap,
+                  c->mask_snap, c->rowdone,
                   c->grp_cnt, c->grp_pass,
                   c->st_hidden, c->st_block, c->st_smoothed,
                   c->g_mask, c->g_tok, c->g_cids, c->g_cval, c->g_com, c->g_sm, c->g_pdev, c->g_st, c->g_hbuf};
@@ -498,6 +507,7 @@ void dinfer_destroy(dinfer_ctx* c) {
     if (b != nullptr) cudaFree(b);
   if (c->rec_all != nullptr && c->rec_all != c->rec_local) cudaFree(c->rec_all);
   if (c->st_host != nullptr) cudaFreeHost(c->st_host);
+  if (c->probe_h != nullptr) cudaFreeHost(c->probe_h);
   if (c->host_graph != nullptr) cudaGraphExecDestroy(c->host_graph);
   if (c->gen_exec != nullptr) cudaGraphExecDestroy(c->gen_exec);
   if (c->cap_stream != nullptr) cudaStreamDestroy(c->cap_stream);
@@ -561,8 +571,12 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
     // chunks.  The accumulator (HW/128 x N columns) must fit the 512-column TMEM.
     int hw_pref = 1024;
     if (const char* e = std::getenv("DINFER_K2_HW")) hw_pref = std::atoi(e);  // tuning override: 128 .. 1024
-    bool want_fused = s.smooth_capable && c->N <= 64;
-    if (const char* e = std::getenv("DINFER_FUSED")) want_fused = want_fused && std::atoi(e) != 0;
+    // K12 for smoothing steps with N <= 64.  DINFER_FUSED: 0 never, 1 (default)
+    // when the vocabulary fills the machine (>= one 32-row chunk per CTA --
+    // small vocabularies are latency-bound and run faster as K1 -> K2), 2 always.
+    int fused_mode = 1;
+    if (const char* e = std::getenv("DINFER_FUSED")) fused_mode = std::atoi(e);
+    const bool want_fused = s.smooth_capable && c->N <= 64 && fused_mode != 0;
     if (want_fused) {
       // ---- K12 geometry: hidden slices of HW columns (the widest power of two
       // <= 1024 dividing H whose accumulator set, HW/128 x N columns, fits half
@@ -572,7 +586,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
         if (w <= hw_pref && s.H % w == 0 && (w / 128) * c->N <= 256) hw = w;
       const int nch = static_cast<int>((s.V_local + kChunkRows12 - 1) / kChunkRows12);
       const int HS = hw > 0 ? s.H / hw : 0;
-      if (hw > 0 && HS <= c->num_sms) {
+      if (hw > 0 && HS <= c->num_sms && (fused_mode == 2 || nch >= c->num_sms / HS)) {
         const int VG = std::max(1, std::min(c->num_sms / HS, nch));
         int srm = 0;  // largest slab (16-row chunk granularity, same arithmetic as the kernel)
         for (int g = 0; g < VG; ++g) {
@@ -697,6 +711,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
   A(dev_alloc(&c->ml, static_cast<size_t>(M) * 2));
   A(dev_alloc(&c->sel, static_cast<size_t>(M)));
   A(dev_alloc(&c->row_cnt, static_cast<size_t>(s.B)));
+  A(dev_alloc(&c->rowdone, static_cast<size_t>(M)));
   A(dev_alloc(&c->mask_snap, static_cast<size_t>(M)));
   if (s.world > 1) A(dev_alloc(&c->rec_all, c->full_words * s.world));
   else c->rec_all = c->rec_local;
@@ -715,6 +730,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
       st = DINFER_ERR_CUDA;
     if (cudaMemset(c->counter, 0, 16) != cudaSuccess || cudaMemset(c->err, 0, 16) != cudaSuccess ||
         cudaMemset(c->row_cnt, 0, 4 * static_cast<size_t>(s.B)) != cudaSuccess ||
+        cudaMemset(c->rowdone, 0, 4 * static_cast<size_t>(M)) != cudaSuccess ||
         cudaMemset(c->rec_local, 0, c->full_words * 4) != cudaSuccess)
       st = DINFER_ERR_CUDA;
   }
@@ -755,10 +771,11 @@ size_t dinfer_record_words(const dinfer_ctx* c, int32_t use_smooth) {
   return use_smooth ? c->full_words : c->stats_words;
 }
 
-dinfer_status dinfer_step(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W, const uint16_t* E,
-                          const uint16_t* e_mask, uint8_t* mask, int32_t* tokens, int32_t* credit_ids,
-                          float* credit_val, const dinfer_params* p, uint8_t* committed, float* smoothed,
-                          float* stats) {
+namespace {
+dinfer_status step_impl(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W, const uint16_t* E,
+                        const uint16_t* e_mask, uint8_t* mask, int32_t* tokens, int32_t* credit_ids,
+                        float* credit_val, const dinfer_params* p, uint8_t* committed, float* smoothed,
+                        float* stats, uint16_t* emb) {
   if (c == nullptr) return DINFER_ERR_ARG;
   dinfer_status s = check_params(c, p);
   if (s != DINFER_OK) return s;
@@ -810,7 +827,27 @@ dinfer_status dinfer_step(dinfer_ctx* c, const uint16_t* hidden, const uint16_t*
 #endif
   }
   return run_combine(c, c->rec_all, words, world, /*acc_from_part2=*/world == 1, e_mask, mask, tokens, credit_ids,
-                     credit_val, p, committed, smoothed, stats);
+                     credit_val, p, committed, smoothed, stats, -1, E, emb);
+}
+}  // namespace
+
+dinfer_status dinfer_step(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W, const uint16_t* E,
+                          const uint16_t* e_mask, uint8_t* mask, int32_t* tokens, int32_t* credit_ids,
+                          float* credit_val, const dinfer_params* p, uint8_t* committed, float* smoothed,
+                          float* stats) {
+  return step_impl(c, hidden, W, E, e_mask, mask, tokens, credit_ids, credit_val, p, committed, smoothed, stats,
+                   nullptr);
+}
+
+dinfer_status dinfer_step_embed(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W, const uint16_t* E,
+                                const uint16_t* e_mask, uint8_t* mask, int32_t* tokens, int32_t* credit_ids,
+                                float* credit_val, const dinfer_params* p, uint8_t* committed, float* smoothed,
+                                float* stats, uint16_t* emb) {
+  if (c == nullptr || p == nullptr) return DINFER_ERR_ARG;
+  if (emb == nullptr) return DINFER_ERR_ARG;
+  if (!aligned(emb, 16)) return DINFER_ERR_SHAPE;
+  if (!p->use_smooth || c->shp.world != 1 || c->dense) return DINFER_ERR_UNSUPPORTED;
+  return step_impl(c, hidden, W, E, e_mask, mask, tokens, credit_ids, credit_val, p, committed, smoothed, stats, emb);
 }
 
 dinfer_status dinfer_step_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W, const uint16_t* E,

@@ -136,6 +136,8 @@ DI void row_stats(const K3Args& a, int i, int lane, float& m, int& vstar, float&
 // positions' (p~, v~, undecided) to `sel`, and the last CTA of the row to
 // arrive (counter, release/acquire fences) runs phase 2 over the whole row.
 constexpr int kSelPos = 8;
+// smoothing blocks: 64 float4 columns x 8 partial groups (256 consecutive elements)
+constexpr int kSmCols = 64, kSmGroups = 8, kSmBatch = 8;
 DI int sel_ctas_per_row(int S) { return (S + kSelPos - 1) / kSelPos; }
 
 DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
@@ -395,12 +397,43 @@ DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
     if (s < a.S) {
       const int i = b * a.S + s;
       a.committed[i] = A[q] ? 1 : 0;
+      s_und[s] = A[q] ? 1 : 0;  // reused below: committed by this step
       if (A[q]) {
         a.tokens[i] = s_vt[s];
         a.mask[i] = 0;
       }
     }
   }
+  if (a.emb == nullptr) return;
+  // ------------------------------------------------------------ next-iteration input embedding (f2)
+  // The smoothing blocks wrote every row of this batch row (E[token] for rows
+  // decided at step start, bf16(e_{t+1}) for the others); once all of them
+  // have counted in, the rows committed by this step are overwritten with
+  // their new token's embedding row E[v~] (smoothing feeds only
+  // positions that stay masked).
+  constexpr int kSmElems = kSmCols * 4;
+  for (int s = threadIdx.x; s < a.S; s += blockDim.x) {
+    const long i = static_cast<long>(b) * a.S + s;
+    const int need = static_cast<int>(((i + 1) * a.H - 1) / kSmElems - (i * a.H) / kSmElems + 1);
+    const volatile int* cnt = a.rowdone + i;
+    uint32_t spins = 0;
+    while (*cnt < need) {
+      __nanosleep(32);
+      if (++spins > (1u << 26)) __trap();
+    }
+  }
+  __syncthreads();
+  __threadfence();
+  const int h8 = a.H / 8;
+  for (int u = threadIdx.x; u < a.S * h8; u += blockDim.x) {
+    const int s = u / h8, c8 = u - s * h8;
+    if (s_und[s]) {
+      const long i = static_cast<long>(b) * a.S + s;
+      *reinterpret_cast<uint4*>(a.emb + i * a.H + c8 * 8) =
+          *reinterpret_cast<const uint4*>(a.E + static_cast<long>(s_vt[s]) * a.H + c8 * 8);
+    }
+  }
+  for (int s = threadIdx.x; s < a.S; s += blockDim.x) a.rowdone[static_cast<long>(b) * a.S + s] = 0;
 }
 
 // Smoothing block: 512 threads = 64 float4 columns x 8 partial groups, i.e.
@@ -411,7 +444,6 @@ DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
 // the rows it covers itself (one warp per row), so it does not wait for the
 // selection; rows undecided at step START are written (e_{t+1} matters for
 // those still undecided after the commit).
-constexpr int kSmCols = 64, kSmGroups = 8, kSmBatch = 8;
 DI void smooth_block(const K3Args& a3, const K4Args& a, int blk, unsigned long long* tr) {
   __shared__ float s_m[4], s_w[4];
   __shared__ float4 red[kSmGroups][kSmCols];
@@ -473,24 +505,42 @@ DI void smooth_block(const K3Args& a3, const K4Args& a, int blk, unsigned long l
   }
   red[grp][cl] = acc;
   __syncthreads();
-  if (grp != 0 || !active) return;
-  for (int g = 1; g < kSmGroups; ++g) {
-    const float4 r = red[g][cl];
-    acc.x += r.x;
-    acc.y += r.y;
-    acc.z += r.z;
-    acc.w += r.w;
+  if (grp == 0 && active) {
+    for (int g = 1; g < kSmGroups; ++g) {
+      const float4 r = red[g][cl];
+      acc.x += r.x;
+      acc.y += r.y;
+      acc.z += r.z;
+      acc.w += r.w;
+    }
+    const float w = s_w[s - s0];
+    const uint2 em = *reinterpret_cast<const uint2*>(a.e_mask + h);
+    const __nv_bfloat162 e01 = *reinterpret_cast<const __nv_bfloat162*>(&em.x);
+    const __nv_bfloat162 e23 = *reinterpret_cast<const __nv_bfloat162*>(&em.y);
+    float4 o;
+    o.x = fmaf(w, acc.x, __low2float(e01));
+    o.y = fmaf(w, acc.y, __high2float(e01));
+    o.z = fmaf(w, acc.z, __low2float(e23));
+    o.w = fmaf(w, acc.w, __high2float(e23));
+    *reinterpret_cast<float4*>(a.out + e) = o;
+    if (a.emb != nullptr) {  // next-iteration input of a (possibly) still-masked row: bf16(e_{t+1})
+      const __nv_bfloat162 o01 = __floats2bfloat162_rn(o.x, o.y), o23 = __floats2bfloat162_rn(o.z, o.w);
+      uint2 ob;
+      ob.x = *reinterpret_cast<const uint32_t*>(&o01);
+      ob.y = *reinterpret_cast<const uint32_t*>(&o23);
+      *reinterpret_cast<uint2*>(a.emb + e) = ob;
+    }
+  } else if (grp == 0 && in && a.emb != nullptr) {  // decided at step start: its token's embedding row
+    const long tok = a.tokens[s];
+    *reinterpret_cast<uint2*>(a.emb + e) = *reinterpret_cast<const uint2*>(a.E + tok * a.H + h);
   }
-  const float w = s_w[s - s0];
-  const uint2 em = *reinterpret_cast<const uint2*>(a.e_mask + h);
-  const __nv_bfloat162 e01 = *reinterpret_cast<const __nv_bfloat162*>(&em.x);
-  const __nv_bfloat162 e23 = *reinterpret_cast<const __nv_bfloat162*>(&em.y);
-  float4 o;
-  o.x = fmaf(w, acc.x, __low2float(e01));
-  o.y = fmaf(w, acc.y, __high2float(e01));
-  o.z = fmaf(w, acc.z, __low2float(e23));
-  o.w = fmaf(w, acc.w, __high2float(e23));
-  *reinterpret_cast<float4*>(a.out + e) = o;
+  if (a.emb != nullptr) {  // count this block's rows as written (the selection block waits for them)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      for (int r = s0; r <= s1; ++r) atomicAdd(a.rowdone + r, 1);
+    }
+  }
 }
 
 // K3+K4 in one launch: blocks [0, B) select/commit batch rows, blocks >= B

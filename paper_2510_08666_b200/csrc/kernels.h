@@ -135,6 +135,10 @@ struct K3Args {
   int decoder, runs_after_hi, use_credit;
   float tau, theta_hi, theta_lo, c_alpha, c_beta, c_gamma;
   unsigned long long* trace;  // DINFER_TRACE: blocks < kTraceK34 stamp [entry, deps, phase1, end, smid]
+  int H;
+  const uint16_t* E;       // [V_local][H] bf16 (next-input embedding of committed rows) or nullptr
+  uint16_t* emb;           // [M][H] bf16 next-iteration input embedding (f2) or nullptr
+  int* rowdone;            // [M] smoothing blocks done per row (phase 2 waits, then resets)
   const float* pdev;       // optional device copy of the numeric params [tau, theta_hi, theta_lo,
                            // c_alpha, c_beta, c_gamma, alpha_t] (overrides the values above; lets a
                            // captured CUDA graph run with per-step schedules)
@@ -155,6 +159,12 @@ struct K4Args {
   const uint16_t* e_mask;  // [H] bf16
   float alpha_t;
   float* out;              // [M][H]
+  const uint16_t* E;       // [V_local][H] bf16, with emb
+  uint16_t* emb;           // [M][H] bf16 next-iteration input embedding or nullptr: E[token] for rows
+                           // decided at step start, bf16(e_{t+1}) for the others (committed rows are
+                           // then overwritten with E[v~] by the selection block)
+  const int32_t* tokens;   // [M] (rows decided at step start are stable during the step)
+  int* rowdone;            // [M]
 };
 // K3 + K4 in one launch (a4 == nullptr: selection only)
 cudaError_t launch_k34(const K3Args& a3, const K4Args* a4, cudaStream_t st, bool pdl);

@@ -82,6 +82,7 @@ def lib():
         "dinfer_set_stream": (S, [P, P]),
         "dinfer_step": (S, [P, P, P, P, P, P, P, P, P, POINTER(Params), P, P, P]),
         "dinfer_step_host": (S, [P, P, P, P, P, P, P, P, P, POINTER(Params), P, P, P]),
+        "dinfer_step_embed": (S, [P, P, P, P, P, P, P, P, P, POINTER(Params), P, P, P, P]),
         "dinfer_record_words": (c_size_t, [P, S]),
         "dinfer_step_local": (S, [P, P, P, P, P, P, POINTER(Params), P]),
         "dinfer_step_combine": (S, [P, P, P, P, P, P, P, POINTER(Params), P, P, P]),
@@ -179,6 +180,13 @@ class Context:
         _check(lib().dinfer_step(self._h, _ptr(hidden), _ptr(W), _ptr(E), _ptr(e_mask), _ptr(mask), _ptr(tokens),
                                  _ptr(credit_ids), _ptr(credit_val), ctypes.byref(params), _ptr(committed),
                                  _ptr(smoothed), _ptr(stats)), "dinfer_step")
+
+    def step_embed(self, hidden, W, E, e_mask, mask, tokens, credit_ids, credit_val, params: Params, committed,
+                   smoothed, stats, emb):
+        """dinfer_step + the next iteration's bf16 input embedding `emb` [B,S,H]."""
+        _check(lib().dinfer_step_embed(self._h, _ptr(hidden), _ptr(W), _ptr(E), _ptr(e_mask), _ptr(mask),
+                                       _ptr(tokens), _ptr(credit_ids), _ptr(credit_val), ctypes.byref(params),
+                                       _ptr(committed), _ptr(smoothed), _ptr(stats), _ptr(emb)), "dinfer_step_embed")
 
     def step_host(self, hidden_h, W, E, e_mask, mask_h, tokens_h, credit_ids_h, credit_val_h, params: Params,
                   committed_h, smoothed_h=None, stats_h=None):

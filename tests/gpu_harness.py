@@ -88,22 +88,64 @@ def compare(out, gold, mask_before, params: O.Params, where=""):
                 assert rel <= TOL_REL, f"smoothed normwise rel {rel:.3g} b{b} s{s} {where}"
 
 
-def replay(ctx, W_dev, E_dev, em_dev, steps, B, S, H, K, V, on_step=None):
+TOL_EMB_REL = TOL_REL + 2.0 ** -9  # bf16 model input: + one bf16 rounding (DESIGN.md c24)
+
+
+def bf16_round_bits(x):
+    """fp32 -> bf16 bit patterns, round to nearest even (test-side reference)."""
+    u = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    return r
+
+
+def compare_embed(emb_bits, out, gold, E_bits, where=""):
+    """Next-iteration input (f2): decided rows are W_emb[token] bit for bit;
+    masked rows are bf16(e_{t+1}) -- the GPU's own fp32 smoothed row rounded
+    to nearest (bit-exact) and within TOL_EMB_REL of the oracle's fp64 row."""
+    B, S = gold["mask"].shape
+    oracle_emb = O.next_input_embedding(O.bf16_bits_to_f64(E_bits), gold["tokens"], gold["mask"], gold["smoothed"])
+    for b in range(B):
+        for s in range(S):
+            if not gold["mask"][b, s]:
+                np.testing.assert_array_equal(emb_bits[b, s], E_bits[gold["tokens"][b, s]],
+                                              err_msg=f"emb decided row b{b} s{s} {where}")
+            else:
+                np.testing.assert_array_equal(emb_bits[b, s], bf16_round_bits(out["smoothed"][b, s]),
+                                              err_msg=f"emb masked row = bf16(smoothed) b{b} s{s} {where}")
+                got = O.bf16_bits_to_f64(emb_bits[b, s])
+                ref = oracle_emb[b, s]
+                rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+                assert rel <= TOL_EMB_REL, f"emb normwise rel {rel:.3g} b{b} s{s} {where}"
+
+
+def replay(ctx, W_dev, E_dev, em_dev, steps, B, S, H, K, V, on_step=None, E_bits=None):
     """Feed every vetted iteration's hidden states to the CUDA path, carrying
-    the GPU's OWN decode state, and compare with the oracle's golden result."""
+    the GPU's OWN decode state, and compare with the oracle's golden result.
+    With E_bits (host bf16 [V, H]) the step also writes the next-iteration
+    input embedding (dinfer_step_embed), checked by compare_embed."""
     import torch
     from paper_2510_08666_b200 import synth
     st = GpuState(B, S, H, K, synth.mask_id(V))
+    emb = None
+    if E_bits is not None:
+        emb = torch.full((B, S, H), -1, dtype=torch.int16, device="cuda")
     for t, step in enumerate(steps):
         p = step["params"]
         hid = to_dev_bf16(step["h"].reshape(B * S, H))
-        ctx.step(hid, W_dev, E_dev if p.use_smooth else None, em_dev if p.use_smooth else None, st.mask, st.tokens,
-                 st.cids if p.use_credit else None, st.cval if p.use_credit else None, gpu_params(p),
-                 st.committed, st.smoothed if p.use_smooth else None, st.stats)
+        args = (hid, W_dev, E_dev if p.use_smooth else None, em_dev if p.use_smooth else None, st.mask, st.tokens,
+                st.cids if p.use_credit else None, st.cval if p.use_credit else None, gpu_params(p),
+                st.committed, st.smoothed if p.use_smooth else None, st.stats)
+        if emb is not None:
+            emb.fill_(-1)  # 0xFFFF (NaN) everywhere: every row must be written
+            ctx.step_embed(*args, emb)
+        else:
+            ctx.step(*args)
         torch.cuda.synchronize()
         ctx.sync()
         out = st.snapshot()
         compare(out, step["result"], step["mask"], p, where=f"iter {t}")
+        if emb is not None:
+            compare_embed(emb.cpu().numpy().view(np.uint16), out, step["result"], E_bits, where=f"iter {t}")
         if on_step is not None:
             on_step(t, out)
     return st

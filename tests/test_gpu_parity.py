@@ -32,7 +32,7 @@ def weights(V, H):
     return _W_CACHE[key]
 
 
-def run_trajectory(torch_cuda, V, H, B, S, K, seed, params_fn, use_credit, max_iters=None, **kw):
+def run_trajectory(torch_cuda, V, H, B, S, K, seed, params_fn, use_credit, max_iters=None, embed=False, **kw):
     from paper_2510_08666_b200 import Context
     W, E = weights(V, H)
     _, _, _, steps = vetted_trajectory(W, E, B, S, seed, params_fn, max_iters=max_iters,
@@ -40,7 +40,7 @@ def run_trajectory(torch_cuda, V, H, B, S, K, seed, params_fn, use_credit, max_i
     ctx = Context(B, S, H, K, V, smooth_capable=B * S <= 256)  # M > 256: dense stats-only path
     Wd, Ed = to_dev_bf16(W), to_dev_bf16(E)
     emd = to_dev_bf16(E[synth.mask_id(V)])
-    replay(ctx, Wd, Ed, emd, steps, B, S, H, K, V)
+    replay(ctx, Wd, Ed, emd, steps, B, S, H, K, V, E_bits=E if embed else None)
     ctx.close()
     return steps
 
@@ -97,10 +97,11 @@ def test_k1_hidden_resident_or_streamed(torch_cuda, monkeypatch, hres):
     run_trajectory(torch_cuda, 3000, 512, 2, 32, 32, 10, hier_credit_smooth, True, max_iters=4)
 
 
-@pytest.mark.parametrize("fused", ["0", "1"])
+@pytest.mark.parametrize("fused", ["0", "2"])
 def test_fused_and_two_kernel_smoothing_paths(torch_cuda, monkeypatch, fused):
-    """Smoothing steps run K12 (K1 + K2 in one kernel, N <= 64) or the two-kernel
-    K1 -> K2 path (DINFER_FUSED=0); both must match the oracle: ragged vocab /
+    """Smoothing steps run K12 (K1 + K2 in one kernel, N <= 64; DINFER_FUSED=2
+    forces it even for vocabularies too small to fill the machine) or the
+    two-kernel K1 -> K2 path (DINFER_FUSED=0); both must match the oracle: ragged vocab /
     odd shapes (V = 1000, H = 384, B = 3, S = 20), HS = 2 groups (H = 2048, the
     other-slab accumulator set in use), N = 64 (B = 2, S = 32)."""
     from paper_2510_08666_b200 import Context
@@ -108,12 +109,40 @@ def test_fused_and_two_kernel_smoothing_paths(torch_cuda, monkeypatch, fused):
     ctx = Context(1, 32, 2048, 32, 4096, smooth_capable=True)
     g = ctx.geometry()
     ctx.close()
-    assert g["fused"] == int(fused)
-    if fused == "1":
+    assert g["fused"] == (fused != "0")
+    if fused != "0":
         assert g["k2_hw"] == 1024 and g["k1_grid"] == 2 * g["k2_groups"]
     run_trajectory(torch_cuda, 1000, 384, 3, 20, 24, 5, hier_credit_smooth, True, max_iters=5)
     run_trajectory(torch_cuda, 4096, 2048, 1, 32, 32, 11, hier_credit_smooth, True, max_iters=4)
     run_trajectory(torch_cuda, 2048, 1024, 2, 32, 32, 12, hier_credit_smooth, True, max_iters=3)
+
+
+@pytest.mark.parametrize("fused", ["0", "2"])
+def test_next_input_embedding(torch_cuda, monkeypatch, fused):
+    """f2: dinfer_step_embed writes the next iteration's bf16 model input in
+    the same K34 launch -- W_emb[token] for decided rows (bit-exact), bf16 of
+    e_{t+1} for masked rows -- over whole trajectories (tiny B = 2, ragged
+    V = 1000 / H = 384 / S = 20, and H = 2048 with two hidden slices)."""
+    monkeypatch.setenv("DINFER_FUSED", fused)
+    run_trajectory(torch_cuda, 1024, 256, 2, 32, 32, 0, hier_credit_smooth, True, embed=True)
+    run_trajectory(torch_cuda, 1000, 384, 3, 20, 24, 5, hier_credit_smooth, True, max_iters=5, embed=True)
+    run_trajectory(torch_cuda, 4096, 2048, 1, 32, 32, 11, hier_credit_smooth, True, max_iters=4, embed=True)
+
+
+def test_next_input_embedding_rejects_unsupported(torch_cuda):
+    from paper_2510_08666_b200 import Context, DInferError
+    import torch
+    V, H, B, S, K = 1024, 256, 1, 32, 8
+    W, E = weights(V, H)
+    ctx = Context(B, S, H, K, V, smooth_capable=True)
+    st = GpuState(B, S, H, K, synth.mask_id(V))
+    emb = torch.zeros((B, S, H), dtype=torch.int16, device="cuda")
+    h = to_dev_bf16(synth.planted_hidden(W, B * S, seed=1))
+    with pytest.raises(DInferError) as ei:  # no smoothing -> no e_{t+1} to feed
+        ctx.step_embed(h, to_dev_bf16(W), to_dev_bf16(E), to_dev_bf16(E[V - 1]), st.mask, st.tokens, None, None,
+                       gpu_params(O.Params()), st.committed, None, st.stats, emb)
+    assert ei.value.status == 6
+    ctx.close()
 
 
 def test_without_pdl(torch_cuda, monkeypatch):

@@ -362,6 +362,44 @@ def test_smoothing_sm1_vector_and_convexity():
     assert np.all(de <= E.max(axis=0) + 1e-12) and np.all(de >= E.min(axis=0) - 1e-12)
 
 
+# ------------------------------------------------------------ next-iteration input (f2)
+def test_next_input_embedding_rows():
+    """Decided rows are the ordinary embedding lookup (numpy fancy indexing as
+    the independent reference), masked rows are e_{t+1}; a fully decided block
+    is exactly the plain lookup."""
+    rng = np.random.default_rng(21)
+    V, H, B, S = 50, 6, 2, 9
+    E = rng.standard_normal((V, H)); tok = rng.integers(0, V, (B, S)); mask = rng.random((B, S)) < 0.5
+    sm = rng.standard_normal((B, S, H))
+    out = O.next_input_embedding(E, tok, mask, sm)
+    np.testing.assert_array_equal(out, np.where(mask[..., None], sm, E[tok]))
+    np.testing.assert_array_equal(O.next_input_embedding(E, tok, np.zeros((B, S), bool), sm), E[tok])
+
+
+def test_next_input_embedding_after_step_and_onehot_limit():
+    """Through a whole oracle step: with alpha_t = 0 every still-masked row is
+    e_mask exactly and every committed row is W_emb[committed id]; the
+    decided-row embedding is the one-hot limit of the smoothed one
+    (alpha = 1, e_mask = 0, all mass on the committed token)."""
+    rng = np.random.default_rng(22)
+    V, H, B, S = 64, 8, 1, 12
+    W = rng.standard_normal((V, H)); E = rng.standard_normal((V, H)); em = rng.standard_normal(H)
+    h = rng.standard_normal((B, S, H)) * 2
+    mask = np.ones((B, S), bool); tok = np.full((B, S), V - 1)
+    res = O.step(h, W, E, em, mask, tok, None, O.Params(tau=0.3, use_smooth=True, alpha_t=0.0))
+    out = O.next_input_embedding(E, res["tokens"], res["mask"], res["smoothed"])
+    assert res["committed"].any() and res["mask"].any()
+    for s in range(S):
+        if res["mask"][0, s]:
+            np.testing.assert_array_equal(out[0, s], em)
+        else:
+            v = res["tokens"][0, s]
+            assert v == np.argmax(h[0, s] @ W.T)
+            np.testing.assert_array_equal(out[0, s], E[v])
+            f = np.full((1, V), -1e9); f[0, v] = 0.0
+            np.testing.assert_allclose(O.smooth(f, E, np.zeros(H), 1.0)[0], out[0, s], atol=1e-9)
+
+
 # ------------------------------------------------------------ schedules
 def test_schedules_spec_examples_and_monotone():
     g = _gold("spec_worked_examples.json")

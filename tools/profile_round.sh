@@ -13,9 +13,13 @@ done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches_bench.csv \
   python bench.py --steps 5 --warmup 3 > gpurun_out/${TAG}_launches_bench.out 2>&1; echo "ncu launches rc=$?"
 # 3) one --set full capture per kernel (steady-state launches of the step loop)
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k1_vocab|k2_smooth|k34_select" \
-  --launch-skip 6 -c 3 -f -o gpurun_out/${TAG}_full_moe python tools/step_loop.py --steps 4 > gpurun_out/${TAG}_full_moe.out 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k12_proj|k34_select" \
+  --launch-skip 4 -c 2 -f -o gpurun_out/${TAG}_full_moe python tools/step_loop.py --steps 4 > gpurun_out/${TAG}_full_moe.out 2>&1
 echo "ncu full moe rc=$?"
+DINFER_FUSED=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k1_vocab|k2_smooth" \
+  --launch-skip 6 -c 2 -f -o gpurun_out/${TAG}_full_moe_unfused python tools/step_loop.py --steps 4 \
+  > gpurun_out/${TAG}_full_moe_unfused.out 2>&1
+echo "ncu full moe unfused rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k1_vocab|k34_select" \
   --launch-skip 4 -c 2 -f -o gpurun_out/${TAG}_full_8b python tools/step_loop.py --config 8b --no-smooth --steps 4 \
   > gpurun_out/${TAG}_full_8b.out 2>&1
