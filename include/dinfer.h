@@ -88,7 +88,12 @@ typedef struct {
  *   use_credit   credit decoding (App. B.2): C <- beta*C, C[v*] += p*^gamma for
  *                undecided positions, then f~ = f + c_alpha*log(1+C) and p~, v~
  *                from softmax(f~).  beta, gamma in (0,1); c_alpha >= 0.
- *   use_smooth   iteration smoothing with weight alpha_t >= 0.       */
+ *   use_smooth   iteration smoothing with weight alpha_t >= 0.
+ *   smooth_credit_fused  0: smooth with the raw softmax(z) (reading
+ *                c13); 1: with the distribution the decoder decided on,
+ *                softmax(f + c_alpha ln(1 + C)) -- exact, via the
+ *                credited tokens' correction.  Requires use_credit,
+ *                use_smooth, K <= 32 and world == 1 (else UNSUPPORTED).      */
 typedef struct {
   int32_t decoder;
   float tau;
@@ -98,6 +103,7 @@ typedef struct {
   float c_alpha, c_beta, c_gamma;
   int32_t use_smooth;
   float alpha_t;
+  int32_t smooth_credit_fused;
 } dinfer_params;
 
 /* 128-byte NCCL unique id for world > 1 (rank 0 calls it and broadcasts). */

@@ -216,6 +216,20 @@ def smooth(f_rows: np.ndarray, E: np.ndarray, e_mask: np.ndarray, alpha_t: float
 
 
 # ---------------------------------------------------------------------------
+# Credit-fused smoothing variant (the alternative of
+# reading c13): the expected embedding under the distribution the decoder
+# actually decides on, p~ = softmax(f~) with f~ = f + alpha * ln(1 + C)
+# (Eq. logits-fuse), instead of the raw softmax(z) of P:278.
+#   e_{t+1} = e_mask + alpha_t * softmax(f + c_alpha ln(1 + C)) W_emb
+# C is the credit table after this iteration's update (the one the decision
+# used).  c_alpha = 0 or C = 0 reduce it to smooth().
+# ---------------------------------------------------------------------------
+def smooth_credit_fused(f_rows: np.ndarray, C_rows: np.ndarray, E: np.ndarray, e_mask: np.ndarray,
+                        alpha_t: float, c_alpha: float) -> np.ndarray:
+    return smooth(credit_fuse(f_rows, C_rows, c_alpha), E, e_mask, alpha_t)
+
+
+# ---------------------------------------------------------------------------
 # Next iteration's model input (Fig. 3 / P:152):
 # the embedding the model reads at iteration t+1 for each position of the
 # block.  Decided positions feed their token's row of the input embedding
@@ -268,6 +282,7 @@ class Params:
     use_smooth: bool = False
     alpha_t: float = 0.1
     hier_runs_after_hi: bool = False
+    smooth_credit_fused: bool = False   # f4: smooth with softmax(f~) instead of softmax(f)
 
 
 def step(h, W, E, e_mask, mask, tokens, C, params: Params, f=None):
@@ -317,7 +332,11 @@ def step(h, W, E, e_mask, mask, tokens, C, params: Params, f=None):
         if params.use_smooth:
             still = np.nonzero(mask[b])[0]
             if len(still):
-                smoothed[b, still] = smooth(fb[still], E, e_mask, params.alpha_t)
+                if params.smooth_credit_fused and params.use_credit:
+                    smoothed[b, still] = smooth_credit_fused(fb[still], C_new[b][still], E, e_mask,
+                                                             params.alpha_t, params.c_alpha)
+                else:
+                    smoothed[b, still] = smooth(fb[still], E, e_mask, params.alpha_t)
     return dict(tokens=tokens, mask=mask, C=C_new, committed=committed,
                 m=out_m, lse=out_lse, ptilde=out_pt, vtilde=out_vt,
                 vstar=out_vstar, pstar=out_pstar, smoothed=smoothed)

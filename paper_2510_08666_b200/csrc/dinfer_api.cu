@@ -67,6 +67,8 @@ struct dinfer_ctx {
   int* row_cnt = nullptr;   // [B] K34 arrival counters
   int* rowdone = nullptr;   // [M] K34 smoothing blocks done per row (next-input embedding handoff)
   uint8_t* mask_snap = nullptr;   // [M] step-start mask (K1 -> smoothing blocks of K34)
+  int32_t* cids_snap = nullptr;   // [M][K] step-start credit slots (credit-fused smoothing, f4)
+  float* cval_snap = nullptr;
   float* mref = nullptr;          // [k2_VG][M] per-vocab-group reference max (K2 -> K4 / record finalize)
   unsigned* grp_cnt = nullptr;    // [k2_VG] K1 slabs done per vocab group (self-resetting)
   unsigned* grp_pass = nullptr;   // [k2_VG]
@@ -206,6 +208,8 @@ dinfer_status check_params(const dinfer_ctx* c, const dinfer_params* p) {
     if (!c->shp.smooth_capable) return DINFER_ERR_UNSUPPORTED;
     if (!(p->alpha_t >= 0.f)) return DINFER_ERR_ARG;
   }
+  if (p->smooth_credit_fused && (!p->use_credit || !p->use_smooth || c->shp.K > 32 || c->shp.world != 1))
+    return DINFER_ERR_UNSUPPORTED;
   return DINFER_OK;
 }
 
@@ -234,7 +238,7 @@ dinfer_status ensure_maps(dinfer_ctx* c, const uint16_t* hidden, const uint16_t*
 // statistics part of this rank's record (and the acc part when reduce_acc).
 dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W, const uint16_t* E,
                         const uint8_t* mask, const int32_t* credit_ids, const dinfer_params* p, float* rec,
-                        bool reduce_acc) {
+                        bool reduce_acc, const float* credit_val = nullptr) {
   const bool smooth = p->use_smooth != 0;
   dinfer_status s = ensure_maps(c, hidden, W, smooth ? E : nullptr);
   if (s != DINFER_OK) return s;
@@ -260,6 +264,12 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
   a.rec = rec;
   a.flog = smooth ? c->flog : nullptr;
   a.mask_snap = smooth ? c->mask_snap : nullptr;
+  a.credit_val = nullptr;
+  if (smooth && p->smooth_credit_fused) {  // f4: the smoothing blocks recompute this step's credit update
+    a.cids_snap = c->cids_snap;
+    a.cval_snap = c->cval_snap;
+    a.credit_val = credit_val;
+  }
   a.err = c->err;
   a.trace = c->trace;
   if (smooth && c->fused) {
@@ -423,6 +433,11 @@ dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, in
     f.emb = emb;
     f.tokens = tokens;
     f.rowdone = c->rowdone;
+    if (p->smooth_credit_fused) {
+      f.cids0 = c->cids_snap;
+      f.cval0 = c->cval_snap;
+      f.E = E;
+    }
     f.alpha_t = p->alpha_t;
     f.out = smoothed;
   }
@@ -499,7 +514,7 @@ void dinfer_destroy(dinfer_ctx* c) {
 #endif
   void* bufs[] = {c->part1, c->counter, c->err, c->rec_local, c->flog, c->part2, c->ml, c->sel, c->row_cnt, c->trace,
                   c->mref,
-                  c->mask_snap, c->rowdone,
+                  c->mask_snap, c->rowdone, c->cids_snap, c->cval_snap,
                   c->grp_cnt, c->grp_pass,
                   c->st_hidden, c->st_block, c->st_smoothed,
                   c->g_mask, c->g_tok, c->g_cids, c->g_cval, c->g_com, c->g_sm, c->g_pdev, c->g_st, c->g_hbuf};
@@ -713,6 +728,10 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
   A(dev_alloc(&c->row_cnt, static_cast<size_t>(s.B)));
   A(dev_alloc(&c->rowdone, static_cast<size_t>(M)));
   A(dev_alloc(&c->mask_snap, static_cast<size_t>(M)));
+  if (s.smooth_capable) {
+    A(dev_alloc(&c->cids_snap, static_cast<size_t>(M) * s.K));
+    A(dev_alloc(&c->cval_snap, static_cast<size_t>(M) * s.K));
+  }
   if (s.world > 1) A(dev_alloc(&c->rec_all, c->full_words * s.world));
   else c->rec_all = c->rec_local;
   if (s.smooth_capable) {
@@ -813,7 +832,7 @@ dinfer_status step_impl(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
                        credit_ids, credit_val, p, committed, smoothed, stats, /*rec_stride=*/4);
   }
   const bool smooth = p->use_smooth != 0;
-  s = run_local(c, hidden, W, E, mask, credit_ids, p, c->rec_local, /*reduce_acc=*/world > 1);
+  s = run_local(c, hidden, W, E, mask, credit_ids, p, c->rec_local, /*reduce_acc=*/world > 1, credit_val);
   if (s != DINFER_OK) return s;
   size_t words = smooth ? c->full_words : c->stats_words;
   if (world > 1) {
@@ -853,6 +872,7 @@ dinfer_status dinfer_step_embed(dinfer_ctx* c, const uint16_t* hidden, const uin
 dinfer_status dinfer_step_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W, const uint16_t* E,
                                 const uint8_t* mask, const int32_t* credit_ids, const dinfer_params* p,
                                 float* record) {
+  if (p != nullptr && p->smooth_credit_fused) return DINFER_ERR_UNSUPPORTED;  // needs the fused step's snapshot
   if (c == nullptr || record == nullptr) return DINFER_ERR_ARG;
   if (c->dense) return DINFER_ERR_UNSUPPORTED;
   dinfer_status s = check_params(c, p);
@@ -868,6 +888,7 @@ dinfer_status dinfer_step_local(dinfer_ctx* c, const uint16_t* hidden, const uin
 dinfer_status dinfer_step_combine(dinfer_ctx* c, const float* records, const uint16_t* e_mask, uint8_t* mask,
                                   int32_t* tokens, int32_t* credit_ids, float* credit_val, const dinfer_params* p,
                                   uint8_t* committed, float* smoothed, float* stats) {
+  if (p != nullptr && p->smooth_credit_fused) return DINFER_ERR_UNSUPPORTED;
   if (c == nullptr || records == nullptr) return DINFER_ERR_ARG;
   if (c->dense) return DINFER_ERR_UNSUPPORTED;
   dinfer_status s = check_params(c, p);
@@ -929,7 +950,8 @@ dinfer_status dinfer_step_host(dinfer_ctx* c, const uint16_t* hidden_h, const ui
                             reinterpret_cast<uint64_t>(smoothed_h), static_cast<uint64_t>(p->decoder),
                             static_cast<uint64_t>(p->hier_runs_after_hi), static_cast<uint64_t>(p->use_credit),
                             static_cast<uint64_t>(p->use_smooth), static_cast<uint64_t>(c->timing),
-                            static_cast<uint64_t>(stats_h != nullptr), 1};
+                            static_cast<uint64_t>(stats_h != nullptr),
+                            static_cast<uint64_t>(p->smooth_credit_fused) + 1};
   // timing events / NCCL: plain enqueue; a key whose capture failed (e.g. pageable
   // host buffers) also stays on the plain path
   const bool same_key = std::memcmp(key, c->host_graph_key, sizeof(key)) == 0;

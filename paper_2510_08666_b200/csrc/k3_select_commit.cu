@@ -77,6 +77,41 @@ DI float warp_sum(float x) {
   return x;
 }
 
+// Credit update (Eq. credit-update) on the K <= 32 slots of one
+// undecided position, slot k in lane k (warp-collective): every credited slot
+// decays by beta, then v*'s slot gains p*^gamma (or v* claims the first empty
+// slot).  Returns true if v* had no slot and none was free.  Shared by the
+// selection blocks and (credit-fused smoothing) the smoothing blocks, so both
+// see bit-identical credit values.
+DI bool credit_update_slots(float beta, float gamma, bool slot, int vstar, float pstar, int& cid, float& cv) {
+  const float gain = ex2(gamma * __log2f(pstar));  // p*^gamma
+  if (cid >= 0) cv = beta * cv;
+  const int lane = threadIdx.x & 31;
+  const unsigned hb = __ballot_sync(0xffffffffu, slot && cid == vstar);
+  const unsigned eb = __ballot_sync(0xffffffffu, slot && cid < 0);
+  const int hit = hb ? __ffs(hb) - 1 : -1, empty = eb ? __ffs(eb) - 1 : -1;
+  if (hit >= 0) {
+    if (lane == hit) cv += gain;
+  } else if (empty >= 0) {
+    if (lane == empty) {
+      cid = vstar;
+      cv = gain;
+    }
+  }
+  return hit < 0 && empty < 0;
+}
+
+// Fuse of one credited slot (Eq. logits-fuse): ft = f_k + alpha
+// ln(1 + C_k) (f_k = m for v*, else the captured raw logit fc); returns the
+// slot's share of the fused partition function relative to e^m,
+// w_k = e^{f_k - m}((1 + C_k)^alpha - 1) (non-credited tokens are unchanged).
+DI float credit_fuse_slot(float alpha, int cid, float cv, int vstar, float m, float fc, float& ft) {
+  const float fk = (cid == vstar) ? m : fc;
+  const float lc = __logf(1.f + cv);
+  ft = fk + alpha * lc;
+  return __expf(fk - m) * (__expf(alpha * lc) - 1.f);
+}
+
 // Warp-collective: merged statistics (m, v*, l) of position i, from K1's
 // per-slab partials (single rank) or from the `world` records (rank order).
 // Every lane returns the identical, deterministic result.
@@ -180,22 +215,8 @@ DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
     int vt = vstar;
     float pt = pstar;
     if (fast && und) {
-      const float gain = ex2(a.c_gamma * __log2f(pstar));  // p*^gamma
-      // decay, then add the gain to v*'s slot (or claim the first empty one)
-      if (cid >= 0) cv = a.c_beta * cv;
-      const unsigned hb = __ballot_sync(0xffffffffu, slot && cid == vstar);
-      const unsigned eb = __ballot_sync(0xffffffffu, slot && cid < 0);
-      const int hit = hb ? __ffs(hb) - 1 : -1, empty = eb ? __ffs(eb) - 1 : -1;
-      if (hit >= 0) {
-        if (lane == hit) cv += gain;
-      } else if (empty >= 0) {
-        if (lane == empty) {
-          cid = vstar;
-          cv = gain;
-        }
-      } else if (lane == 0) {
+      if (credit_update_slots(a.c_beta, a.c_gamma, slot, vstar, pstar, cid, cv) && lane == 0)
         atomicOr(a.err, kErrCreditSlotsFull);
-      }
       if (slot) {
         a.credit_ids[cbase + lane] = cid;
         a.credit_val[cbase + lane] = cv;
@@ -204,10 +225,8 @@ DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
       float best = m, extra = 0.f;
       int best_id = vstar;
       if (cid >= 0) {
-        const float fk = (cid == vstar) ? m : fc;
-        const float lc = __logf(1.f + cv);
-        const float ft = fk + a.c_alpha * lc;
-        extra = __expf(fk - m) * (__expf(a.c_alpha * lc) - 1.f);
+        float ft;
+        extra = credit_fuse_slot(a.c_alpha, cid, cv, vstar, m, fc, ft);
         if (ft > best || (ft == best && cid < best_id)) {
           best = ft;
           best_id = cid;
@@ -446,6 +465,8 @@ DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
 // those still undecided after the commit).
 DI void smooth_block(const K3Args& a3, const K4Args& a, int blk, unsigned long long* tr) {
   __shared__ float s_m[4], s_w[4];
+  __shared__ float s_cw[4][32];  // credit-fused smoothing: per-slot weights w_k and ids
+  __shared__ int s_cid[4][32];
   __shared__ float4 red[kSmGroups][kSmCols];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cl = threadIdx.x % kSmCols, grp = threadIdx.x / kSmCols;
@@ -472,10 +493,31 @@ DI void smooth_block(const K3Args& a3, const K4Args& a, int blk, unsigned long l
   if (warp <= s1 - s0) {
     float m, l;
     int vs;
-    row_stats(a3, s0 + warp, lane, m, vs, l);
+    const int i = s0 + warp;
+    row_stats(a3, i, lane, m, vs, l);
+    float extra = 0.f;
+    if (a.cids0 != nullptr && a.mask_start[i]) {
+      // credit-fused smoothing (f4): this step's credit update recomputed from
+      // the step-start snapshot with the selection's own helpers, then
+      // p~ = softmax(f~) = (e^{f-m} + w_v [v credited]) / (l + sum w)
+      const bool slot = lane < a3.K;
+      const long cb = static_cast<long>(i) * a3.K;
+      int cid = slot ? a.cids0[cb + lane] : -1;
+      float cv = slot ? a.cval0[cb + lane] : 0.f;
+      const float fc = slot ? a3.recs[static_cast<long>(i) * a3.rec_stride + kStatWords + lane] : 0.f;
+      credit_update_slots(a3.c_beta, a3.c_gamma, slot, vs, __frcp_rn(l), cid, cv);
+      float w = 0.f;
+      if (cid >= 0) {
+        float ft;
+        w = credit_fuse_slot(a3.c_alpha, cid, cv, vs, m, fc, ft);
+      }
+      s_cw[warp][lane] = w;
+      s_cid[warp][lane] = cid;
+      extra = warp_sum(w);
+    }
     if (lane == 0) {
       s_m[warp] = m;
-      s_w[warp] = a.alpha_t / l;
+      s_w[warp] = a.alpha_t / (l + extra);
     }
   }
   __syncthreads();
@@ -512,6 +554,21 @@ DI void smooth_block(const K3Args& a3, const K4Args& a, int blk, unsigned long l
       acc.y += r.y;
       acc.z += r.z;
       acc.w += r.w;
+    }
+    if (a.cids0 != nullptr) {  // + sum_k w_k E[id_k, h..h+3] over the row's credited tokens
+      const int rr = s - s0;
+      for (int k = 0; k < a3.K; ++k) {
+        const int id = s_cid[rr][k];
+        if (id < 0) continue;
+        const float wk = s_cw[rr][k];
+        const uint2 ev = *reinterpret_cast<const uint2*>(a.E + static_cast<long>(id) * a.H + h);
+        const __nv_bfloat162 e01 = *reinterpret_cast<const __nv_bfloat162*>(&ev.x);
+        const __nv_bfloat162 e23 = *reinterpret_cast<const __nv_bfloat162*>(&ev.y);
+        acc.x = fmaf(wk, __low2float(e01), acc.x);
+        acc.y = fmaf(wk, __high2float(e01), acc.y);
+        acc.z = fmaf(wk, __low2float(e23), acc.z);
+        acc.w = fmaf(wk, __high2float(e23), acc.w);
+      }
     }
     const float w = s_w[s - s0];
     const uint2 em = *reinterpret_cast<const uint2*>(a.e_mask + h);

@@ -53,6 +53,9 @@ struct K1Args {
   float* rec;              // [M][4+K] rank record: only fcred (captured credited logits) is written
   float* flog;             // [M][V_local] raw logits for K2, or nullptr
   uint8_t* mask_snap;      // [M] copy of the step-start mask (written by CTA 0), or nullptr
+  int32_t* cids_snap;      // [M][K] copy of the step-start credit slots (f4), or nullptr
+  float* cval_snap;
+  const float* credit_val; // [M][K] (read for the snapshot)
   int* err;
   unsigned long long* trace;  // optional [grid][5]: globaltimer ns start, first W stage, last tile done, exit; smid
 };
@@ -165,6 +168,8 @@ struct K4Args {
                            // then overwritten with E[v~] by the selection block)
   const int32_t* tokens;   // [M] (rows decided at step start are stable during the step)
   int* rowdone;            // [M]
+  const int32_t* cids0;    // credit-fused smoothing (f4): step-start credit snapshot [M][K], or nullptr
+  const float* cval0;
 };
 // K3 + K4 in one launch (a4 == nullptr: selection only)
 cudaError_t launch_k34(const K3Args& a3, const K4Args* a4, cudaStream_t st, bool pdl);

@@ -39,7 +39,8 @@ class Shape(ctypes.Structure):
 class Params(ctypes.Structure):
     _fields_ = [("decoder", c_int32), ("tau", c_float), ("theta_hi", c_float), ("theta_lo", c_float),
                 ("hier_runs_after_hi", c_int32), ("use_credit", c_int32), ("c_alpha", c_float),
-                ("c_beta", c_float), ("c_gamma", c_float), ("use_smooth", c_int32), ("alpha_t", c_float)]
+                ("c_beta", c_float), ("c_gamma", c_float), ("use_smooth", c_int32), ("alpha_t", c_float),
+                ("smooth_credit_fused", c_int32)]
 
 
 class GenConfig(ctypes.Structure):
@@ -118,12 +119,13 @@ def _check(status: int, what: str):
 
 
 def make_params(decoder=DEC_THRESHOLD, tau=0.9, theta_hi=0.92, theta_lo=0.62, hier_runs_after_hi=False,
-                use_credit=False, c_alpha=1.0, c_beta=0.9, c_gamma=0.5, use_smooth=False, alpha_t=0.1) -> Params:
+                use_credit=False, c_alpha=1.0, c_beta=0.9, c_gamma=0.5, use_smooth=False, alpha_t=0.1,
+                smooth_credit_fused=False) -> Params:
     if isinstance(decoder, str):
         decoder = {"threshold": DEC_THRESHOLD, "hierarchical": DEC_HIERARCHICAL}[decoder]
     return Params(int(decoder), float(tau), float(theta_hi), float(theta_lo), int(bool(hier_runs_after_hi)),
                   int(bool(use_credit)), float(c_alpha), float(c_beta), float(c_gamma), int(bool(use_smooth)),
-                  float(alpha_t))
+                  float(alpha_t), int(bool(smooth_credit_fused)))
 
 
 def alpha_schedule(init: float, growth: float, preset: float, t: int) -> float:

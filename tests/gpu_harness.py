@@ -47,7 +47,8 @@ def gpu_params(p: O.Params):
     from paper_2510_08666_b200 import make_params
     return make_params(decoder=p.decoder, tau=p.tau, theta_hi=p.theta_hi, theta_lo=p.theta_lo,
                        hier_runs_after_hi=p.hier_runs_after_hi, use_credit=p.use_credit, c_alpha=p.c_alpha,
-                       c_beta=p.c_beta, c_gamma=p.c_gamma, use_smooth=p.use_smooth, alpha_t=p.alpha_t)
+                       c_beta=p.c_beta, c_gamma=p.c_gamma, use_smooth=p.use_smooth, alpha_t=p.alpha_t,
+                       smooth_credit_fused=p.smooth_credit_fused)
 
 
 def compare(out, gold, mask_before, params: O.Params, where=""):

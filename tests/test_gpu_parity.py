@@ -129,6 +129,38 @@ def test_next_input_embedding(torch_cuda, monkeypatch, fused):
     run_trajectory(torch_cuda, 4096, 2048, 1, 32, 32, 11, hier_credit_smooth, True, max_iters=4, embed=True)
 
 
+def hier_credit_fused_smooth(t):
+    p = hier_credit_smooth(t)
+    p.c_alpha = 2.0
+    p.smooth_credit_fused = True
+    return p
+
+
+@pytest.mark.parametrize("fused", ["0", "2"])
+def test_credit_fused_smoothing(torch_cuda, monkeypatch, fused):
+    """f4: smoothing with softmax(f + c_alpha ln(1 + C)) (the distribution the
+    decoder decided on) instead of the raw softmax, on both smoothing paths and
+    together with the next-iteration input; the test also checks that the two
+    variants differ well beyond the tolerance on these trajectories."""
+    monkeypatch.setenv("DINFER_FUSED", fused)
+    steps = run_trajectory(torch_cuda, 1024, 256, 2, 32, 32, 1, hier_credit_fused_smooth, True)
+    run_trajectory(torch_cuda, 1000, 384, 3, 20, 24, 5, hier_credit_fused_smooth, True, max_iters=5, embed=True)
+    run_trajectory(torch_cuda, 4096, 2048, 1, 32, 32, 11, hier_credit_fused_smooth, True, max_iters=4)
+    W, E = weights(1024, 256)
+    em = O.bf16_bits_to_f64(E[synth.mask_id(1024)])
+    worst = 0.0
+    for st in steps:
+        p_raw = O.Params(**{**vars(st["params"]), "smooth_credit_fused": False})
+        raw = O.step(O.bf16_bits_to_f64(st["h"]), O.bf16_bits_to_f64(W), O.bf16_bits_to_f64(E), em, st["mask"], st["tokens"], st["C"],
+                     p_raw)["smoothed"]
+        fz = st["result"]["smoothed"]
+        ok = ~np.isnan(raw[..., 0])
+        if ok.any():
+            d = np.linalg.norm(raw[ok] - fz[ok], axis=-1) / np.linalg.norm(fz[ok], axis=-1)
+            worst = max(worst, float(d.max()))
+    assert worst > 10 * 2e-3, f"fused and raw smoothing indistinguishable here ({worst:.3g})"
+
+
 def test_next_input_embedding_rejects_unsupported(torch_cuda):
     from paper_2510_08666_b200 import Context, DInferError
     import torch
@@ -141,6 +173,10 @@ def test_next_input_embedding_rejects_unsupported(torch_cuda):
     with pytest.raises(DInferError) as ei:  # no smoothing -> no e_{t+1} to feed
         ctx.step_embed(h, to_dev_bf16(W), to_dev_bf16(E), to_dev_bf16(E[V - 1]), st.mask, st.tokens, None, None,
                        gpu_params(O.Params()), st.committed, None, st.stats, emb)
+    assert ei.value.status == 6
+    with pytest.raises(DInferError) as ei:  # credit-fused smoothing without credit
+        ctx.step(h, to_dev_bf16(W), to_dev_bf16(E), to_dev_bf16(E[V - 1]), st.mask, st.tokens, None, None,
+                 gpu_params(O.Params(use_smooth=True, smooth_credit_fused=True)), st.committed, st.smoothed, st.stats)
     assert ei.value.status == 6
     ctx.close()
 

@@ -362,6 +362,61 @@ def test_smoothing_sm1_vector_and_convexity():
     assert np.all(de <= E.max(axis=0) + 1e-12) and np.all(de >= E.min(axis=0) - 1e-12)
 
 
+# ------------------------------------------------------------ credit-fused smoothing (f4)
+def test_smooth_credit_fused_reductions_and_shortcut():
+    """c_alpha = 0 and C = 0 reduce to raw smoothing; the credited-token
+    shortcut (raw partial sums plus a correction over credited tokens only,
+    the form the GPU computes) equals the dense definition; pure-Python brute
+    force on a 5-token vocabulary."""
+    rng = np.random.default_rng(31)
+    V, H, R = 40, 5, 4
+    f = rng.standard_normal((R, V)) * 3; E = rng.standard_normal((V, H)); em = rng.standard_normal(H)
+    C = np.zeros((R, V))
+    for r in range(R):
+        C[r, rng.choice(V, 3, replace=False)] = rng.random(3) * 2
+    np.testing.assert_allclose(O.smooth_credit_fused(f, C, E, em, 0.3, 0.0), O.smooth(f, E, em, 0.3), rtol=1e-13)
+    np.testing.assert_allclose(O.smooth_credit_fused(f, np.zeros_like(C), E, em, 0.3, 1.3), O.smooth(f, E, em, 0.3),
+                               rtol=1e-13)
+    a = 0.8
+    for r in range(R):
+        m = f[r].max()
+        acc = np.exp(f[r] - m) @ E
+        l = np.exp(f[r] - m).sum()
+        cred = np.nonzero(C[r])[0]
+        w = np.exp(f[r, cred] - m) * ((1 + C[r, cred]) ** a - 1)
+        short = em + 0.2 * (acc + w @ E[cred]) / (l + w.sum())
+        np.testing.assert_allclose(O.smooth_credit_fused(f[r:r + 1], C[r:r + 1], E, em, 0.2, a)[0], short,
+                                   rtol=1e-12)
+    f5 = [1.0, 0.5, -0.2, 2.0, 0.0]; C5 = [0.0, 1.5, 0.0, 0.0, 0.7]; E5 = [[1, 2], [0, 1], [3, -1], [-2, 0], [1, 1]]
+    ft = [f5[v] + 0.6 * math.log(1 + C5[v]) for v in range(5)]
+    z = math.fsum(math.exp(x) for x in ft)
+    de = [math.fsum(math.exp(ft[v]) / z * E5[v][k] for v in range(5)) for k in range(2)]
+    got = O.smooth_credit_fused(np.array([f5]), np.array([C5]), np.array(E5, float), np.zeros(2), 1.0, 0.6)[0]
+    np.testing.assert_allclose(got, de, rtol=1e-13)
+
+
+def test_step_credit_fused_smoothing_uses_updated_credit():
+    """Through a whole step: the fused variant smooths with the credit table
+    AFTER this step's update (the one the decision used), and equals the raw
+    variant when c_alpha = 0."""
+    rng = np.random.default_rng(32)
+    V, H, B, S = 48, 6, 1, 8
+    W = rng.standard_normal((V, H)); E = rng.standard_normal((V, H)); em = rng.standard_normal(H)
+    h = rng.standard_normal((B, S, H))
+    mask = np.ones((B, S), bool); tok = np.full((B, S), V - 1)
+    C = np.zeros((B, S, V)); C[0, :, 3] = 0.5; C[0, :, 7] = 1.2
+    p = O.Params(tau=0.99, use_credit=True, c_alpha=0.9, use_smooth=True, alpha_t=0.25, smooth_credit_fused=True)
+    res = O.step(h, W, E, em, mask, tok, C, p)
+    f = O.logits(h[0], W)
+    for s in np.nonzero(res["mask"][0])[0]:
+        want = O.smooth(O.credit_fuse(f[s:s + 1], res["C"][0, s:s + 1], 0.9), E, em, 0.25)[0]
+        np.testing.assert_allclose(res["smoothed"][0, s], want, rtol=1e-12)
+    p0 = O.Params(**{**vars(p), "c_alpha": 0.0})
+    r0 = O.step(h, W, E, em, mask, tok, C, p0)
+    r1 = O.step(h, W, E, em, mask, tok, C, O.Params(**{**vars(p0), "smooth_credit_fused": False}))
+    np.testing.assert_allclose(r0["smoothed"], r1["smoothed"], rtol=1e-13, equal_nan=True)
+
+
 # ------------------------------------------------------------ next-iteration input (f2; P:152, P:275)
 def test_next_input_embedding_rows():
     """Decided rows are the ordinary embedding lookup (numpy fancy indexing as
