@@ -487,3 +487,70 @@ def generate(hidden_of, W, E, e_mask, X0, cfg: GenConfig, base: Params, dense_cr
         if len(e):
             T[b] = e[0]
     return dict(X=X, F=F, T=T, truncated=truncated)
+
+
+# ---------------------------------------------------------------------------
+# Vicinity KV-cache refresh (SURVEY §8(f) row f3; §2.3 P:125-133, App. D
+# P:368) on a synthetic single bidirectional attention layer -- the KV-cache
+# manager of Algorithm 1 (K.ShouldUpdate / K.Update, P:84, P:91-92).
+#
+# Readings (DESIGN.md):
+#   c25  refresh region (SPEC S:376): for block [start, end), iteration t of
+#        the block: all positions [0, L) while t < warmup_times (S:409), else
+#        [start - prefix_look, end + after_look) clipped to [0, L) (P:133
+#        "recomputed for both masked tokens and their immediate neighbors";
+#        looks 16, warmup 4, P:368).  The region is also the forward's query
+#        region (S:410); positions outside it keep their cached K/V (stale).
+#        A block's completion triggers a full refresh (P:133 "once a block is
+#        fully decoded, a full cache update ensures global consistency").
+#   c26  the layer: q = x Wq^T, k = x Wk^T, v = x Wv^T (nn.Linear layout
+#        [out, in]); n_heads = H / d_head; per head o = softmax(q K^T /
+#        sqrt(d_head)) V over all L cached positions (bidirectional: no mask).
+#   c27  storage precision: q and the cached k, v are stored in bf16
+#        (round to nearest even) as a bf16 model would; accumulation in fp64
+#        here (fp32 on the GPU).
+# ---------------------------------------------------------------------------
+def refresh_region(L: int, start: int, end: int, t: int, prefix_look: int, after_look: int,
+                   warmup_times: int, full: bool = False):
+    """[lo, hi) of positions whose K/V (and queries) this forward recomputes."""
+    if full or t < warmup_times:
+        return 0, L
+    return max(0, start - prefix_look), min(L, end + after_look)
+
+
+def round_bf16(x: np.ndarray) -> np.ndarray:
+    """float64 -> nearest bf16 value (ties to even), returned as float64.
+    bf16 keeps 8 significand bits: x = m 2^e with m in [0.5, 1) (frexp), so
+    the bf16 value is round(m 2^8) 2^(e-8) (np.round ties to even).  Normal
+    range only (the layer's values are far from bf16 under/overflow)."""
+    m, e = np.frexp(np.asarray(x, np.float64))
+    return np.round(m * 256.0) * np.exp2(e - 8.0)
+
+
+def attention(Q: np.ndarray, K: np.ndarray, V: np.ndarray, n_heads: int) -> np.ndarray:
+    """Bidirectional multi-head attention: Q [R, H], K, V [L, H] -> [R, H]."""
+    R, H = Q.shape
+    d = H // n_heads
+    out = np.empty((R, H))
+    for hh in range(n_heads):
+        sl = slice(hh * d, (hh + 1) * d)
+        s = Q[:, sl] @ K[:, sl].T / math.sqrt(d)
+        out[:, sl] = softmax(s) @ V[:, sl]
+    return out
+
+
+def vicinity_step(X, Wq, Wk, Wv, Kc, Vc, start: int, end: int, t: int, n_heads: int,
+                  prefix_look: int = 16, after_look: int = 16, warmup_times: int = 4, full: bool = False):
+    """One forward of the attention layer under vicinity refresh.
+    X: [L, H] layer input (all positions, this iteration); Kc, Vc: [L, H]
+    cached keys / values (bf16 values as float64).  Returns dict(lo, hi, O
+    [hi-lo, H] for the query rows lo..hi-1, K, V = updated caches)."""
+    L = X.shape[0]
+    lo, hi = refresh_region(L, start, end, t, prefix_look, after_look, warmup_times, full)
+    X = np.asarray(X, np.float64)
+    K = np.array(Kc, np.float64, copy=True)
+    Vn = np.array(Vc, np.float64, copy=True)
+    K[lo:hi] = round_bf16(X[lo:hi] @ np.asarray(Wk, np.float64).T)      # K.Update on the region
+    Vn[lo:hi] = round_bf16(X[lo:hi] @ np.asarray(Wv, np.float64).T)
+    Q = round_bf16(X[lo:hi] @ np.asarray(Wq, np.float64).T)
+    return dict(lo=lo, hi=hi, O=attention(Q, K, Vn, n_heads), K=K, V=Vn)

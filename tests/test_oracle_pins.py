@@ -519,3 +519,80 @@ def test_step_empty_row_is_noop():
     r = O.step(rng.standard_normal((1, 5, 4)), W, W, W[0], np.zeros((1, 5), bool),
                np.arange(5)[None, :], None, O.Params())
     assert not r["committed"].any() and np.array_equal(r["tokens"], np.arange(5)[None, :])
+
+
+# ------------------------------------------------------------ vicinity KV-cache refresh (f3)
+def test_refresh_region_spec_examples():
+    """SPEC S:379-381: block [64,128), looks 16 after warmup -> [48,144);
+    step 0 with warmup 4 -> everything; clipping at both ends; a block's
+    completion (full) -> everything."""
+    L = 256
+    assert O.refresh_region(L, 64, 128, 4, 16, 16, 4) == (48, 144)
+    assert O.refresh_region(L, 64, 128, 0, 16, 16, 4) == (0, L)
+    assert O.refresh_region(L, 64, 128, 3, 16, 16, 4) == (0, L)
+    assert O.refresh_region(L, 0, 32, 9, 16, 16, 4) == (0, 48)
+    assert O.refresh_region(L, 224, 256, 9, 16, 16, 4) == (208, 256)
+    assert O.refresh_region(L, 64, 128, 9, 16, 16, 4, full=True) == (0, L)
+
+
+def test_round_bf16_against_bit_patterns():
+    """Round-to-nearest-even to 8 significand bits: exact bf16 values are fixed
+    points; midpoints go to the even neighbour; bf16 bit decoding agrees."""
+    vals = O.bf16_bits_to_f64(np.arange(0x3f00, 0x4100, dtype=np.uint16))
+    np.testing.assert_array_equal(O.round_bf16(vals), vals)
+    assert O.round_bf16(np.array([1.0 + 2 ** -8]))[0] == 1.0                 # tie -> even (1.0)
+    assert O.round_bf16(np.array([1.0 + 3 * 2 ** -8]))[0] == 1.0 + 2 ** -6   # tie -> even (1 + 2^-6)
+    assert O.round_bf16(np.array([1.0 + 2 ** -8 + 1e-12]))[0] == 1.0 + 2 ** -7
+    assert O.round_bf16(np.array([-3.0]))[0] == -3.0
+
+
+def test_attention_brute_force_and_closed_forms():
+    """Pure-Python softmax attention on 2 heads; K = 0 gives the mean of V per
+    head (uniform weights); one key gives that key's V row."""
+    rng = np.random.default_rng(41)
+    R, L, H, nh = 3, 5, 4, 2
+    Q = rng.standard_normal((R, H)); K = rng.standard_normal((L, H)); V = rng.standard_normal((L, H))
+    out = O.attention(Q, K, V, nh)
+    d = H // nh
+    for r in range(R):
+        for hh in range(nh):
+            sc = [math.fsum(Q[r, hh * d + j] * K[k, hh * d + j] for j in range(d)) / math.sqrt(d) for k in range(L)]
+            z = math.fsum(math.exp(x) for x in sc)
+            for j in range(d):
+                want = math.fsum(math.exp(sc[k]) / z * V[k, hh * d + j] for k in range(L))
+                assert abs(out[r, hh * d + j] - want) < 1e-12
+    np.testing.assert_allclose(O.attention(Q, np.zeros((L, H)), V, nh), np.tile(V.mean(axis=0), (R, 1)), rtol=1e-13)
+    np.testing.assert_allclose(O.attention(Q, K[:1], V[:1], nh), np.tile(V[0], (R, 1)), rtol=1e-13)
+
+
+def _layer(rng, L, H):
+    W = [rng.standard_normal((H, H)) / math.sqrt(H) for _ in range(3)]
+    return [O.round_bf16(w) for w in W]
+
+
+def test_vicinity_exactness_limit_and_staleness():
+    """Looks covering the whole sequence degenerate to a full recompute
+    (bitwise in the oracle); otherwise rows outside the region keep
+    their stale K/V exactly while the region's rows are recomputed from the
+    current input; a full refresh makes the forward equal the no-cache one."""
+    rng = np.random.default_rng(42)
+    L, H, nh = 48, 16, 2
+    Wq, Wk, Wv = _layer(rng, L, H)
+    X0 = O.round_bf16(rng.standard_normal((L, H)))
+    full = O.vicinity_step(X0, Wq, Wk, Wv, np.zeros((L, H)), np.zeros((L, H)), 16, 24, 0, nh, full=True)
+    X1 = X0.copy(); X1[16:24] = O.round_bf16(rng.standard_normal((8, H)))   # the block's inputs evolve
+    X1[35:40] = O.round_bf16(rng.standard_normal((5, H)))                    # and some far rows (stale keys)
+    nocache = O.vicinity_step(X1, Wq, Wk, Wv, full["K"], full["V"], 16, 24, 9, nh, full=True)
+    wide = O.vicinity_step(X1, Wq, Wk, Wv, full["K"], full["V"], 16, 24, 9, nh, prefix_look=L, after_look=L)
+    np.testing.assert_array_equal(wide["O"], nocache["O"])
+    np.testing.assert_array_equal(wide["K"], nocache["K"])
+    vic = O.vicinity_step(X1, Wq, Wk, Wv, full["K"], full["V"], 16, 24, 9, nh, prefix_look=4, after_look=4)
+    assert (vic["lo"], vic["hi"]) == (12, 28)
+    np.testing.assert_array_equal(vic["K"][:12], full["K"][:12])             # stale outside the region
+    np.testing.assert_array_equal(vic["V"][28:], full["V"][28:])
+    np.testing.assert_array_equal(vic["K"][12:28], nocache["K"][12:28])      # fresh inside
+    # queries are the region's rows; they differ from the no-cache forward through the stale keys only
+    assert vic["O"].shape == (16, H)
+    assert np.abs(vic["O"] - nocache["O"][12:28]).max() > 1e-6
+    np.testing.assert_array_equal(vic["K"][35:40], full["K"][35:40])
+    np.testing.assert_array_equal(O.attention(O.round_bf16(X1[12:28] @ Wq.T), vic["K"], vic["V"], nh), vic["O"])
