@@ -264,6 +264,43 @@ dinfer_status dinfer_generate(dinfer_ctx* ctx, const dinfer_gen_config* cfg, con
                               const uint16_t* W_vocab, const uint16_t* E, const uint16_t* e_mask,
                               const uint16_t* hidden_src, int64_t hidden_iters, int32_t* X, int32_t* out);
 
+/* ---------------------------------------------------------------------------
+ * Vicinity KV-cache refresh (§2.3, App. D
+ * P:368) on a synthetic single bidirectional attention layer: the KV-cache
+ * manager of Algorithm 1 (K.ShouldUpdate / K.Update).
+ *
+ * Shape: L positions, hidden H = n_heads * d_head (d_head must be 128),
+ * prefix_look / after_look (16 / 16 in the paper) and warmup_times (4).
+ * Refresh region of a forward (readings c25-c27): for block [start, end) at
+ * block-local iteration t, [0, L) while t < warmup_times or when `full`
+ * (a completed block's full refresh), else
+ * [start - prefix_look, end + after_look) clipped to [0, L).
+ *
+ * dinfer_kv_step (device pointers, asynchronous on the kv stream):
+ *   X        [L,H] bf16 layer input of every position (this iteration)
+ *   Wq/Wk/Wv [H,H] bf16 projections, nn.Linear layout [out, in]
+ *   Kc, Vc   [L,H] bf16 caller-owned caches, updated IN PLACE on the region
+ *            (bf16 of the fp32-accumulated projection); other rows untouched
+ *   out      [L,H] fp32: rows [lo, hi) receive the attention output of the
+ *            region's queries (q = bf16(x Wq^T)) over all L cached positions,
+ *            per head softmax(q k^T / sqrt(d_head)) v; other rows untouched
+ *   lo_hi    optional HOST int32[2] receiving the region.
+ * The projections run on cuBLAS (plain GEMMs); the attention on this
+ * library's kernels.  Errors: ARG (null / bad block), SHAPE (alignment).    */
+typedef struct dinfer_kv dinfer_kv;
+typedef struct {
+  int32_t L, H, d_head;
+  int32_t prefix_look, after_look, warmup_times;
+} dinfer_kv_shape;
+dinfer_status dinfer_kv_create(const dinfer_kv_shape* shape, void* stream, dinfer_kv** out);
+void dinfer_kv_destroy(dinfer_kv* kv);
+/* host helper: the refresh region [lo, hi) (returns hi - lo, -1 on null args) */
+int32_t dinfer_kv_region(const dinfer_kv_shape* shape, int32_t start, int32_t end, int32_t t, int32_t full,
+                         int32_t* lo, int32_t* hi);
+dinfer_status dinfer_kv_step(dinfer_kv* kv, const uint16_t* X, const uint16_t* Wq, const uint16_t* Wk,
+                             const uint16_t* Wv, uint16_t* Kc, uint16_t* Vc, int32_t start, int32_t end,
+                             int32_t t, int32_t full, float* out, int32_t* lo_hi);
+
 /* Synchronise the ctx stream and report asynchronous errors (CUDA, NCCL,
  * sticky device-checked preconditions); clears the sticky device flag.      */
 dinfer_status dinfer_sync(dinfer_ctx* ctx);

@@ -5,4 +5,4 @@ in include/dinfer.h); `dinfer` is its thin ctypes binding.  `synth` holds the
 seeded synthetic input generators (no method arithmetic).
 """
 from .dinfer import (DEC_HIERARCHICAL, DEC_THRESHOLD, Context, DInferError, GenConfig, Params,  # noqa: F401
-                     alpha_schedule, get_unique_id, lib, make_gen_config, make_params, tau_schedule)
+                     VicinityKV, alpha_schedule, get_unique_id, lib, make_gen_config, make_params, tau_schedule)

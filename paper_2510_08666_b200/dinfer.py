@@ -64,6 +64,11 @@ class Geometry(ctypes.Structure):
                                         "fused_smem")]
 
 
+class KvShape(ctypes.Structure):
+    """dinfer_kv_shape (include/dinfer.h): vicinity KV-cache refresh layer."""
+    _fields_ = [(n, c_int32) for n in ("L", "H", "d_head", "prefix_look", "after_look", "warmup_times")]
+
+
 _LIB = None
 
 
@@ -99,6 +104,10 @@ def lib():
         "dinfer_get_geometry": (S, [P, POINTER(Geometry)]),
         "dinfer_get_trace": (S, [P, P, S]),
         "dinfer_generate": (S, [P, POINTER(GenConfig), POINTER(Params), P, P, P, P, c_int64, P, P]),
+        "dinfer_kv_create": (S, [POINTER(KvShape), P, POINTER(c_void_p)]),
+        "dinfer_kv_destroy": (None, [P]),
+        "dinfer_kv_region": (S, [POINTER(KvShape), S, S, S, S, POINTER(c_int32), POINTER(c_int32)]),
+        "dinfer_kv_step": (S, [P, P, P, P, P, P, P, S, S, S, S, P, POINTER(c_int32)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -254,3 +263,38 @@ class Context:
         g = Geometry()
         _check(lib().dinfer_get_geometry(self._h, ctypes.byref(g)), "dinfer_get_geometry")
         return {n: getattr(g, n) for n, _ in Geometry._fields_}
+
+
+class VicinityKV:
+    """Vicinity KV-cache refresh on a synthetic attention layer (dinfer_kv_*):
+    marshalling only."""
+
+    def __init__(self, L, H, d_head=128, prefix_look=16, after_look=16, warmup_times=4, stream=None):
+        self.shape = KvShape(L, H, d_head, prefix_look, after_look, warmup_times)
+        h = c_void_p()
+        _check(lib().dinfer_kv_create(ctypes.byref(self.shape), c_void_p(stream) if stream else None,
+                                      ctypes.byref(h)), "dinfer_kv_create")
+        self._h = h
+
+    def region(self, start, end, t, full=False):
+        lo, hi = c_int32(), c_int32()
+        lib().dinfer_kv_region(ctypes.byref(self.shape), start, end, t, int(bool(full)), ctypes.byref(lo),
+                               ctypes.byref(hi))
+        return lo.value, hi.value
+
+    def step(self, X, Wq, Wk, Wv, Kc, Vc, start, end, t, out, full=False):
+        lohi = (c_int32 * 2)()
+        _check(lib().dinfer_kv_step(self._h, _ptr(X), _ptr(Wq), _ptr(Wk), _ptr(Wv), _ptr(Kc), _ptr(Vc), start, end,
+                                    t, int(bool(full)), _ptr(out), lohi), "dinfer_kv_step")
+        return lohi[0], lohi[1]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().dinfer_kv_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

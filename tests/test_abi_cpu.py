@@ -5,6 +5,7 @@ import ctypes
 import os
 import re
 
+import numpy as np
 import pytest
 
 import oracle as O
@@ -90,3 +91,21 @@ def test_null_args(L):
     assert L.dinfer_step(None, *([None] * 12)) == 1
     assert L.dinfer_sync(None) == 1
     assert L.dinfer_strerror(0) == b"ok"
+
+
+def test_kv_region_helper_matches_oracle(L):
+    """The host refresh-region helper of the vicinity KV cache (f3) against the
+    oracle's refresh_region, incl. warmup, clipping and full refresh."""
+    import ctypes
+    from paper_2510_08666_b200.dinfer import KvShape
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        Ls = int(rng.integers(32, 400))
+        pre, aft, warm = (int(x) for x in rng.integers(0, 40, 3))
+        start = int(rng.integers(0, Ls - 1)); end = int(rng.integers(start + 1, Ls + 1))
+        t = int(rng.integers(0, 8)); full = bool(rng.random() < 0.2)
+        s = KvShape(Ls, 256, 128, pre, aft, warm % 6)
+        lo, hi = ctypes.c_int32(), ctypes.c_int32()
+        n = L.dinfer_kv_region(ctypes.byref(s), start, end, t, int(full), ctypes.byref(lo), ctypes.byref(hi))
+        want = O.refresh_region(Ls, start, end, t, pre, aft, warm % 6, full)
+        assert (lo.value, hi.value) == want and n == want[1] - want[0]
