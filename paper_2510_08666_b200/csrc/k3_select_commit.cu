@@ -171,8 +171,9 @@ DI void row_stats(const K3Args& a, int i, int lane, float& m, int& vstar, float&
 // positions' (p~, v~, undecided) to `sel`, and the last CTA of the row to
 // arrive (counter, release/acquire fences) runs phase 2 over the whole row.
 constexpr int kSelPos = 8;
-// smoothing blocks: 64 float4 columns x 8 partial groups (256 consecutive elements)
-constexpr int kSmCols = 64, kSmGroups = 8, kSmBatch = 8;
+// smoothing blocks: 128 float4 columns x 4 partial groups (512 consecutive elements; one
+// wave of <= 144 blocks at the MoE shape)
+constexpr int kSmCols = 128, kSmGroups = 4, kSmBatch = 8;
 DI int sel_ctas_per_row(int S) { return (S + kSelPos - 1) / kSelPos; }
 
 DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
@@ -455,8 +456,8 @@ DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
   for (int s = threadIdx.x; s < a.S; s += blockDim.x) a.rowdone[static_cast<long>(b) * a.S + s] = 0;
 }
 
-// Smoothing block: 512 threads = 64 float4 columns x 8 partial groups, i.e.
-// 256 consecutive elements of the [M, H] output.  Each thread loads a strided
+// Smoothing block: 512 threads = 128 float4 columns x 4 partial groups, i.e.
+// 512 consecutive elements of the [M, H] output.  Each thread loads a strided
 // subset of the nparts partials (issued before the statistics merge so both
 // latencies overlap), the 8 groups are combined in a fixed order through
 // shared memory (deterministic).  The block merges the statistics (m, l) of
@@ -464,9 +465,9 @@ DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
 // selection; rows undecided at step START are written (e_{t+1} matters for
 // those still undecided after the commit).
 DI void smooth_block(const K3Args& a3, const K4Args& a, int blk, unsigned long long* tr) {
-  __shared__ float s_m[4], s_w[4];
-  __shared__ float s_cw[4][32];  // credit-fused smoothing: per-slot weights w_k and ids
-  __shared__ int s_cid[4][32];
+  __shared__ float s_m[8], s_w[8];
+  __shared__ float s_cw[8][32];  // credit-fused smoothing: per-slot weights w_k and ids
+  __shared__ int s_cid[8][32];
   __shared__ float4 red[kSmGroups][kSmCols];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cl = threadIdx.x % kSmCols, grp = threadIdx.x / kSmCols;
