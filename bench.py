@@ -204,9 +204,17 @@ def gpu_arm(args):
     rank, world, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # BENCH_SAME_DEVICE=1 (test hook): every rank on cuda:0 with a gloo process
+    # group, so the N > 1 code path can run on a one-GPU box (--exchange p2p)
+    same_dev = os.environ.get("BENCH_SAME_DEVICE") == "1"
+    if same_dev:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if rank == 0:
         build.build()
     if world > 1:
@@ -233,11 +241,35 @@ def gpu_arm(args):
 
     stream = torch.cuda.Stream()
     nid = None
-    if world > 1:
+    if world > 1 and args.exchange != "p2p":  # the NCCL communicator (allgather / fallback)
         from paper_2510_08666_b200.dist import broadcast_unique_id
-        nid = broadcast_unique_id("cuda")
+        nid = broadcast_unique_id("cpu" if same_dev else "cuda")
     ctx = Context(B, S, H, K, V, V_local=Vl, v_offset=v0, world=world, rank=rank, stream=stream.cuda_stream,
                   nccl_id=nid, smooth_capable=smooth)
+    exchange = "none"
+    if world > 1:
+        # the product's exchange: records pushed into every rank's gather buffer by
+        # the record-finalize kernel over NVLink P2P (CUDA IPC handles shared via
+        # torch.distributed); the NCCL allgather stays as the fallback / --exchange nccl
+        exchange = "nccl"
+        if args.exchange in ("auto", "p2p"):
+            from paper_2510_08666_b200 import DInferError
+            handles = [None] * world
+            dist.all_gather_object(handles, ctx.exchange_handle())
+            try:
+                ctx.exchange_open(b"".join(handles))
+                ok = 1
+            except DInferError as e:
+                if args.exchange == "p2p":
+                    raise
+                print(f"[bench] peer-memory exchange unavailable ({e}); using the NCCL allgather", file=sys.stderr)
+                ok = 0
+            flag = torch.tensor([ok], dtype=torch.int32, device="cpu" if same_dev else "cuda")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag[0]) == 1:
+                exchange = "p2p"
+            elif ok:
+                raise SystemExit("peer-memory exchange opened on some ranks only")
     p = make_params(decoder=CFG["decoder"], tau=0.9, theta_hi=0.92, theta_lo=0.62, use_credit=credit,
                     use_smooth=smooth, alpha_t=0.1)
 
@@ -310,7 +342,8 @@ def gpu_arm(args):
     ms_b = sum(a.elapsed_time(b) for a, b in evb) / len(evb)
     phases = {k_: v_ / args.steps for k_, v_ in phase_acc.items()}
     if world > 1:
-        t = torch.tensor([ms, ms_b] + [phases[k_] for k_ in sorted(phases)], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms, ms_b] + [phases[k_] for k_ in sorted(phases)], dtype=torch.float64,
+                         device="cpu" if same_dev else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, ms_b = float(t[0]), float(t[1])
         for j, k_ in enumerate(sorted(phases)):
@@ -345,7 +378,7 @@ def gpu_arm(args):
             e2e_ms.append(e0.elapsed_time(e1))
     e2e = sum(e2e_ms) / len(e2e_ms)
     if world > 1:
-        t = torch.tensor([e2e], dtype=torch.float64, device=dev)
+        t = torch.tensor([e2e], dtype=torch.float64, device="cpu" if same_dev else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = float(t[0])
     launches = ctx.launches_per_step(p)
@@ -391,7 +424,10 @@ def gpu_arm(args):
             "config": {"workload": WORKLOAD, "name": args.config, "B": B, "S": S, "H": H, "V": V, "K": K,
                        "decoder": CFG["decoder"], "credit": credit, "smooth": smooth, "vocab_shards": world,
                        "V_local": Vl,
-                       "parallelism": f"vocab-sharded x{world} (NCCL allgather)" if world > 1 else "single GPU",
+                       "parallelism": (f"vocab-sharded x{world} ("
+                                       + ("in-kernel peer-memory record exchange" if exchange == "p2p"
+                                          else "NCCL allgather") + ")") if world > 1 else "single GPU",
+                       "exchange": exchange,
                        "l2": "flushed (256 MiB write) before every timed step; inputs > L2"},
             "e2e": {"value": M / (e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e, "api": "dinfer_step_host"},
@@ -424,6 +460,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--config", default="moe", choices=sorted(CONFIGS))
+    ap.add_argument("--exchange", default="auto", choices=["auto", "p2p", "nccl"],
+                    help="N>1 record exchange: peer memory (auto: if every rank can open it) or NCCL allgather")
     args = ap.parse_args()
     set_config(args.config)
     if args.warmup < 3:

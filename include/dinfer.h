@@ -183,6 +183,20 @@ dinfer_status dinfer_step_host(dinfer_ctx* ctx, const uint16_t* hidden_h,
                                const dinfer_params* params, uint8_t* committed_h,
                                float* smoothed_h, float* stats_h);
 
+/* Peer-memory exchange of the per-rank records (world > 1),
+ * replacing the NCCL allgather: the record finalize kernel stores this rank's
+ * record straight into every rank's gather buffer over NVLink P2P (slot
+ * [epoch & 1][rank], double-buffered so a rank one step ahead never
+ * overwrites a slot a slower rank still reads) and raises a per-rank flag
+ * (epoch + 1) on every peer; the select/commit kernel waits for all flags of
+ * its epoch and advances the epoch -- no host synchronisation, graph safe.
+ * dinfer_exchange_handle: this ctx's gather buffer as a 64-byte CUDA IPC
+ * handle.  dinfer_exchange_open: `handles` = world handles back to back in
+ * rank order (all ranks); after it, dinfer_step exchanges through peer memory
+ * (no communicator needed).  Errors: ARG, UNSUPPORTED (world == 1), CUDA.  */
+dinfer_status dinfer_exchange_handle(dinfer_ctx* ctx, uint8_t out_handle[64]);
+dinfer_status dinfer_exchange_open(dinfer_ctx* ctx, const uint8_t* handles);
+
 /* Split phases (tests, caller-managed collectives).
  * dinfer_record_words: number of fp32 words of one rank's record:
  *   M*(4+K)  statistics: per row (m, v* as int32 bits (global id), l =

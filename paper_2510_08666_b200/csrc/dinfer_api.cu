@@ -48,6 +48,14 @@ struct dinfer_ctx {
   size_t k1_smem = 0;
   int k2_HW = 0, k2_HS = 0, k2_VG = 0, k2_stages = 0, k2_pstages = 0, k2_nchunks = 0, k2_KV = 64;
   size_t k2_smem = 0;
+  // peer-memory exchange (world > 1): gather buffer [2 slots][world][full_words]
+  // + flags [2][world] (IPC-shared), local control words, opened peer buffers
+  float* xbuf = nullptr;
+  unsigned* xctl = nullptr;
+  float** d_peers = nullptr;
+  float* peer_host[8] = {};
+  bool p2p = false;
+  long xslot = 0, xflags_off = 0;
   // K12 (K1 + K2 fused, smoothing steps with N <= 64): the k2_* fields then
   // describe its E phase (HW, HS, VG, KV = 16) and k1_VG x k1_SPG its slabs
   bool fused = false;
@@ -360,6 +368,15 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
     r.mref = c->mref;
     r.rec = rec;
     r.rec_acc = rec + c->stats_words;
+    r.K = c->shp.K;
+    if (c->p2p && rec == c->rec_local) {  // dinfer_step: push the record into every rank's gather buffer
+      r.peers = c->d_peers;
+      r.world = c->shp.world;
+      r.rank = c->shp.rank;
+      r.rec_words = static_cast<long>(c->full_words);
+      r.flags_off = c->xflags_off;
+      r.ctl = c->xctl;
+    }
     ev_begin(c, kPK2r);
     DI_CUDA(launch_rec_finalize(r, c->stream, c->pdl));
     ev_finish(c, kPK2r);
@@ -408,6 +425,11 @@ dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, in
   k.c_gamma = p->c_gamma;
   k.pdev = c->pdev_active;
   k.err = c->err;
+  if (c->p2p && recs == c->xbuf) {
+    k.xflags = reinterpret_cast<const unsigned*>(c->xbuf + c->xflags_off);
+    k.xctl = c->xctl;
+    k.xslot = c->xslot;
+  }
   K4Args f{};
   if (p->use_smooth) {
     f.M = c->M;
@@ -509,12 +531,14 @@ float dinfer_tau_schedule(float target, int32_t t, int32_t decay_steps) {
 void dinfer_destroy(dinfer_ctx* c) {
   if (c == nullptr) return;
   cudaStreamSynchronize(c->stream);
+  for (int j = 0; j < 8; ++j)
+    if (c->peer_host[j] != nullptr && c->peer_host[j] != c->xbuf) cudaIpcCloseMemHandle(c->peer_host[j]);
 #ifdef DINFER_WITH_NCCL
   if (c->has_comm) ncclCommDestroy(c->comm);
 #endif
   void* bufs[] = {c->part1, c->counter, c->err, c->rec_local, c->flog, c->part2, c->ml, c->sel, c->row_cnt, c->trace,
                   c->mref,
-                  c->mask_snap, c->rowdone, c->cids_snap, c->cval_snap,
+                  c->mask_snap, c->rowdone, c->cids_snap, c->cval_snap, c->xbuf, c->xctl, c->d_peers,
                   c->grp_cnt, c->grp_pass,
                   c->st_hidden, c->st_block, c->st_smoothed,
                   c->g_mask, c->g_tok, c->g_cids, c->g_cval, c->g_com, c->g_sm, c->g_pdev, c->g_st, c->g_hbuf};
@@ -732,8 +756,16 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
     A(dev_alloc(&c->cids_snap, static_cast<size_t>(M) * s.K));
     A(dev_alloc(&c->cval_snap, static_cast<size_t>(M) * s.K));
   }
-  if (s.world > 1) A(dev_alloc(&c->rec_all, c->full_words * s.world));
-  else c->rec_all = c->rec_local;
+  if (s.world > 1) {
+    A(dev_alloc(&c->rec_all, c->full_words * s.world));
+    c->xslot = static_cast<long>(c->full_words) * s.world;
+    c->xflags_off = 2 * c->xslot;
+    A(dev_alloc(&c->xbuf, static_cast<size_t>(c->xflags_off) + 2 * s.world + 4));
+    A(dev_alloc(&c->xctl, 4));
+    A(dev_alloc(&c->d_peers, 8));
+  } else {
+    c->rec_all = c->rec_local;
+  }
   if (s.smooth_capable) {
     A(dev_alloc(&c->flog, static_cast<size_t>(M) * s.V_local));
     A(dev_alloc(&c->part2, static_cast<size_t>(c->k2_VG) * M * s.H));
@@ -750,6 +782,9 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
     if (cudaMemset(c->counter, 0, 16) != cudaSuccess || cudaMemset(c->err, 0, 16) != cudaSuccess ||
         cudaMemset(c->row_cnt, 0, 4 * static_cast<size_t>(s.B)) != cudaSuccess ||
         cudaMemset(c->rowdone, 0, 4 * static_cast<size_t>(M)) != cudaSuccess ||
+        (c->xbuf != nullptr && cudaMemset(c->xbuf, 0, 4 * (static_cast<size_t>(c->xflags_off) + 2 * s.world + 4)) !=
+                                   cudaSuccess) ||
+        (c->xctl != nullptr && cudaMemset(c->xctl, 0, 16) != cudaSuccess) ||
         cudaMemset(c->rec_local, 0, c->full_words * 4) != cudaSuccess)
       st = DINFER_ERR_CUDA;
   }
@@ -785,6 +820,45 @@ dinfer_status dinfer_set_stream(dinfer_ctx* c, void* stream) {
   return DINFER_OK;
 }
 
+dinfer_status dinfer_exchange_handle(dinfer_ctx* c, uint8_t out_handle[64]) {
+  if (c == nullptr || out_handle == nullptr) return DINFER_ERR_ARG;
+  if (c->shp.world < 2 || c->xbuf == nullptr) return DINFER_ERR_UNSUPPORTED;
+  cudaIpcMemHandle_t h;
+  DI_CUDA(cudaIpcGetMemHandle(&h, c->xbuf));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(out_handle, &h, 64);
+  return DINFER_OK;
+}
+
+dinfer_status dinfer_exchange_open(dinfer_ctx* c, const uint8_t* handles) {
+  if (c == nullptr || handles == nullptr) return DINFER_ERR_ARG;
+  if (c->shp.world < 2 || c->xbuf == nullptr) return DINFER_ERR_UNSUPPORTED;
+  if (c->p2p) return DINFER_ERR_ARG;  // already open
+  const int W = c->shp.world;
+  for (int j = 0; j < W; ++j) {
+    if (j == c->shp.rank) {
+      c->peer_host[j] = c->xbuf;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles + 64 * j, 64);
+    void* p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      note_error("cudaIpcOpenMemHandle", cudaGetErrorString(e));
+      cudaGetLastError();
+      for (int k = 0; k < j; ++k)
+        if (c->peer_host[k] != nullptr && c->peer_host[k] != c->xbuf) cudaIpcCloseMemHandle(c->peer_host[k]);
+      for (int k = 0; k < 8; ++k) c->peer_host[k] = nullptr;
+      return DINFER_ERR_CUDA;
+    }
+    c->peer_host[j] = static_cast<float*>(p);
+  }
+  DI_CUDA(cudaMemcpy(c->d_peers, c->peer_host, sizeof(float*) * 8, cudaMemcpyHostToDevice));
+  c->p2p = true;
+  return DINFER_OK;
+}
+
 size_t dinfer_record_words(const dinfer_ctx* c, int32_t use_smooth) {
   if (c == nullptr) return 0;
   return use_smooth ? c->full_words : c->stats_words;
@@ -801,7 +875,7 @@ dinfer_status step_impl(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
   s = check_step_ptrs(c, hidden, W, E, e_mask, mask, tokens, credit_ids, credit_val, p, committed, smoothed);
   if (s != DINFER_OK) return s;
   const int world = c->shp.world;
-  if (world > 1 && !c->has_comm) return DINFER_ERR_UNSUPPORTED;
+  if (world > 1 && !c->has_comm && !c->p2p) return DINFER_ERR_UNSUPPORTED;
   for (int i = 0; i < kNumPhases; ++i) c->ev_used[i] = false;
   if (c->dense) {
     // compute-bound path: K1b writes one record row per (vocab group,
@@ -835,6 +909,10 @@ dinfer_status step_impl(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
   s = run_local(c, hidden, W, E, mask, credit_ids, p, c->rec_local, /*reduce_acc=*/world > 1, credit_val);
   if (s != DINFER_OK) return s;
   size_t words = smooth ? c->full_words : c->stats_words;
+  if (world > 1 && c->p2p) {  // the record finalize pushed every rank's record over peer memory
+    return run_combine(c, c->xbuf, c->full_words, world, /*acc_from_part2=*/false, e_mask, mask, tokens, credit_ids,
+                       credit_val, p, committed, smoothed, stats, -1, E, emb);
+  }
   if (world > 1) {
 #ifdef DINFER_WITH_NCCL
     ev_begin(c, kPC1);

@@ -318,51 +318,99 @@ __global__ void __launch_bounds__(kThreads, 1)
 // record's (m, v*, l).  Blocks >= M (when part2): rec_acc[s, h..h+3] =
 // sum_g part2[g][s, h..] * e^{m_g - m_rank}, with m_rank recomputed from the
 // group maxima (identical to the merged m: the groups tile the shard).
+// Store one record word (or float4) locally and, with the peer exchange, into
+// every rank's gather buffer (NVLink P2P stores).
+DI void rec_put(const RecArgs& a, long word, float v, unsigned par) {
+  if (a.peers == nullptr) return;
+  const long off = (static_cast<long>(par) * a.world + a.rank) * a.rec_words + word;
+  for (int j = 0; j < a.world; ++j) a.peers[j][off] = v;
+}
+DI void rec_put4(const RecArgs& a, long word, float4 v, unsigned par) {
+  if (a.peers == nullptr) return;
+  const long off = (static_cast<long>(par) * a.world + a.rank) * a.rec_words + word;
+  for (int j = 0; j < a.world; ++j) *reinterpret_cast<float4*>(a.peers[j] + off) = v;
+}
+
 __global__ void rec_finalize_kernel(const RecArgs a) {
   grid_dep_wait();
+  const unsigned epoch = (a.peers != nullptr) ? *reinterpret_cast<volatile unsigned*>(a.ctl) : 0u;
+  const unsigned par = epoch & 1u;
   if (static_cast<int>(blockIdx.x) < a.M) {
-    if (threadIdx.x >= 32) return;
-    const int s = blockIdx.x, lane = threadIdx.x;
-    float m = neg_inf(), l = 0.f;
-    int ix = 0x7fffffff;
-    for (int j = lane; j < a.grid1; j += 32) {
-      const float4 p = __ldcg(a.part1 + static_cast<long>(s) * a.grid1 + j);
-      stat_combine(m, ix, l, p.x, __float_as_int(p.y), p.z);
-    }
+    if (threadIdx.x < 32) {
+      const int s = blockIdx.x, lane = threadIdx.x;
+      float m = neg_inf(), l = 0.f;
+      int ix = 0x7fffffff;
+      for (int j = lane; j < a.grid1; j += 32) {
+        const float4 p = __ldcg(a.part1 + static_cast<long>(s) * a.grid1 + j);
+        stat_combine(m, ix, l, p.x, __float_as_int(p.y), p.z);
+      }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float rm = __shfl_xor_sync(0xffffffffu, m, o);
-      const int ri = __shfl_xor_sync(0xffffffffu, ix, o);
-      const float rl = __shfl_xor_sync(0xffffffffu, l, o);
-      stat_combine(m, ix, l, rm, ri, rl);
+      for (int o = 16; o > 0; o >>= 1) {
+        const float rm = __shfl_xor_sync(0xffffffffu, m, o);
+        const int ri = __shfl_xor_sync(0xffffffffu, ix, o);
+        const float rl = __shfl_xor_sync(0xffffffffu, l, o);
+        stat_combine(m, ix, l, rm, ri, rl);
+      }
+      const long row = static_cast<long>(s) * a.rec_stride;
+      if (lane == 0) {
+        float* r = a.rec + row;
+        r[0] = m;
+        r[1] = __int_as_float(ix);
+        r[2] = l;
+        r[3] = 0.f;
+        rec_put(a, row, m, par);
+        rec_put(a, row + 1, __int_as_float(ix), par);
+        rec_put(a, row + 2, l, par);
+        rec_put(a, row + 3, 0.f, par);
+      }
+      // the captured credited logits (K1 wrote them into the local record)
+      for (int k = lane; k < a.K && a.peers != nullptr; k += 32)
+        rec_put(a, row + kStatWords + k, __ldcg(a.rec + row + kStatWords + k), par);
     }
-    if (lane == 0) {
-      float* r = a.rec + static_cast<long>(s) * a.rec_stride;
-      r[0] = m;
-      r[1] = __int_as_float(ix);
-      r[2] = l;
-      r[3] = 0.f;
+  } else if (a.part2 != nullptr) {
+    const long t = static_cast<long>(blockIdx.x - a.M) * blockDim.x + threadIdx.x;
+    const int h4 = a.H / 4;
+    if (t < static_cast<long>(a.M) * h4) {
+      const int s = static_cast<int>(t / h4);
+      const int h = static_cast<int>(t - static_cast<long>(s) * h4) * 4;
+      float mr = neg_inf();
+      for (int g = 0; g < a.VG; ++g) mr = fmaxf(mr, a.mref[static_cast<long>(g) * a.M + s]);
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int g = 0; g < a.VG; ++g) {
+        const float sc = expf(a.mref[static_cast<long>(g) * a.M + s] - mr);
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(a.part2 + (static_cast<long>(g) * a.M + s) * a.H + h));
+        acc.x = fmaf(v.x, sc, acc.x);
+        acc.y = fmaf(v.y, sc, acc.y);
+        acc.z = fmaf(v.z, sc, acc.z);
+        acc.w = fmaf(v.w, sc, acc.w);
+      }
+      *reinterpret_cast<float4*>(a.rec_acc + static_cast<long>(s) * a.H + h) = acc;
+      const long w = (a.rec_acc - a.rec) + static_cast<long>(s) * a.H + h;
+      if (((a.rec_acc - a.rec) | a.rec_words) % 4 == 0) {
+        rec_put4(a, w, acc, par);
+      } else {
+        rec_put(a, w, acc.x, par);
+        rec_put(a, w + 1, acc.y, par);
+        rec_put(a, w + 2, acc.z, par);
+        rec_put(a, w + 3, acc.w, par);
+      }
     }
-    return;
   }
-  if (a.part2 == nullptr) return;
-  const long t = static_cast<long>(blockIdx.x - a.M) * blockDim.x + threadIdx.x;
-  const int h4 = a.H / 4;
-  if (t >= static_cast<long>(a.M) * h4) return;
-  const int s = static_cast<int>(t / h4);
-  const int h = static_cast<int>(t - static_cast<long>(s) * h4) * 4;
-  float mr = neg_inf();
-  for (int g = 0; g < a.VG; ++g) mr = fmaxf(mr, a.mref[static_cast<long>(g) * a.M + s]);
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int g = 0; g < a.VG; ++g) {
-    const float sc = expf(a.mref[static_cast<long>(g) * a.M + s] - mr);
-    const float4 v = __ldcg(reinterpret_cast<const float4*>(a.part2 + (static_cast<long>(g) * a.M + s) * a.H + h));
-    acc.x = fmaf(v.x, sc, acc.x);
-    acc.y = fmaf(v.y, sc, acc.y);
-    acc.z = fmaf(v.z, sc, acc.z);
-    acc.w = fmaf(v.w, sc, acc.w);
+  if (a.peers == nullptr) return;
+  // completion: every block's peer stores are system-visible before its count;
+  // the last block raises this rank's flag on every peer (release)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    if (atomicAdd(a.ctl + 1, 1u) == gridDim.x - 1) {
+      a.ctl[1] = 0u;
+      __threadfence_system();
+      for (int j = 0; j < a.world; ++j) {
+        unsigned* f = reinterpret_cast<unsigned*>(a.peers[j] + a.flags_off) + par * a.world + a.rank;
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch + 1u) : "memory");
+      }
+    }
   }
-  *reinterpret_cast<float4*>(a.rec_acc + static_cast<long>(s) * a.H + h) = acc;
 }
 
 }  // namespace
@@ -385,7 +433,7 @@ cudaError_t launch_k2(const CUtensorMap& map_e, const CUtensorMap& map_f, const 
 
 cudaError_t launch_rec_finalize(const RecArgs& a, cudaStream_t st, bool pdl) {
   const int threads = 256;
-  const int acc_blocks = a.part2 == nullptr ? 0 : (a.M * (a.H / 4) + threads - 1) / threads;
+  const int acc_blocks = a.part2 == nullptr ? 0 : (a.M * (a.H / 4) + threads - 1) / threads;  // 0: stats only
   return launch_ex(rec_finalize_kernel, dim3(a.M + acc_blocks), dim3(threads), 0, st, pdl, a);
 }
 

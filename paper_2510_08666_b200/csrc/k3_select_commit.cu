@@ -618,6 +618,28 @@ __global__ void __launch_bounds__(kK3Threads) k34_select_smooth(const K3Args a3i
   grid_dep_launch_dependents();
   K3Args a3 = a3in;
   K4Args a4 = a4in;
+  unsigned epoch = 0;
+  if (a3.xflags != nullptr) {
+    // peer-memory exchange: every rank's record of this epoch has landed in
+    // slot (epoch & 1) of the local gather buffer once its flag reads epoch + 1
+    epoch = *reinterpret_cast<volatile unsigned*>(a3.xctl);
+    const unsigned par = epoch & 1u;
+    if (static_cast<int>(threadIdx.x) < a3.world) {
+      const unsigned* f = a3.xflags + par * a3.world + threadIdx.x;
+      uint32_t spins = 0;
+      for (;;) {
+        unsigned v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if (v == epoch + 1u) break;
+        __nanosleep(64);
+        if (++spins > (1u << 26)) __trap();
+      }
+    }
+    __syncthreads();
+    a3.recs += par * a3.xslot;
+    a4.acc += par * a3.xslot;
+    a4.m_part += par * a3.xslot;
+  }
   if (a3.pdev != nullptr) {  // per-step numeric parameters from device memory (graph replay)
     a3.tau = a3.pdev[0];
     a3.theta_hi = a3.pdev[1];
@@ -634,6 +656,16 @@ __global__ void __launch_bounds__(kK3Threads) k34_select_smooth(const K3Args a3i
     smooth_block(a3, a4, blockIdx.x - nsel, tr);
   }
   if (tr != nullptr) tr[3] = globaltimer_ns();
+  if (a3.xflags != nullptr) {  // the last block advances the exchange epoch
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(a3.xctl + 2, 1u) == gridDim.x - 1) {
+        a3.xctl[2] = 0u;
+        a3.xctl[0] = epoch + 1u;
+      }
+    }
+  }
 }
 
 }  // namespace

@@ -115,6 +115,15 @@ struct RecArgs {
   const float* mref;       // [VG][M]
   float* rec;              // stats rows
   float* rec_acc;          // [M][H]
+  // Peer-memory exchange (world > 1, dinfer_exchange_open): the record is ALSO
+  // written straight into every rank's gather buffer (slot [epoch & 1][rank]),
+  // then the last block raises this rank's flag (= epoch + 1) on every peer.
+  float* const* peers;     // [world] device pointers to the ranks' gather buffers, or nullptr
+  int world, rank;
+  long rec_words;          // words of one rank's record
+  long flags_off;          // word offset of the flags [2][world] in a gather buffer
+  unsigned* ctl;           // local control words: [0] epoch, [1] finished blocks of this kernel
+  int K;                   // credit slots (fcred words per stats row, copied from `rec`)
 };
 cudaError_t launch_rec_finalize(const RecArgs& a, cudaStream_t st, bool pdl);
 
@@ -142,6 +151,13 @@ struct K3Args {
   const uint16_t* E;       // [V_local][H] bf16 (next-input embedding of committed rows) or nullptr
   uint16_t* emb;           // [M][H] bf16 next-iteration input embedding (f2) or nullptr
   int* rowdone;            // [M] smoothing blocks done per row (phase 2 waits, then resets)
+  // Peer-memory exchange: recs / K4 acc point at slot 0 of the local gather
+  // buffer; the kernel waits until every rank's flag for this epoch is up,
+  // offsets them to slot (epoch & 1) (xslot words), and its last block
+  // advances the epoch.
+  const unsigned* xflags;  // [2][world] in the local gather buffer, or nullptr
+  unsigned* xctl;          // [0] epoch, [2] finished K34 blocks
+  long xslot;
   const float* pdev;       // optional device copy of the numeric params [tau, theta_hi, theta_lo,
                            // c_alpha, c_beta, c_gamma, alpha_t] (overrides the values above; lets a
                            // captured CUDA graph run with per-step schedules)

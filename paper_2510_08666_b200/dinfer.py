@@ -104,6 +104,8 @@ def lib():
         "dinfer_get_geometry": (S, [P, POINTER(Geometry)]),
         "dinfer_get_trace": (S, [P, P, S]),
         "dinfer_generate": (S, [P, POINTER(GenConfig), POINTER(Params), P, P, P, P, c_int64, P, P]),
+        "dinfer_exchange_handle": (S, [P, P]),
+        "dinfer_exchange_open": (S, [P, P]),
         "dinfer_kv_create": (S, [POINTER(KvShape), P, POINTER(c_void_p)]),
         "dinfer_kv_destroy": (None, [P]),
         "dinfer_kv_region": (S, [POINTER(KvShape), S, S, S, S, POINTER(c_int32), POINTER(c_int32)]),
@@ -191,6 +193,18 @@ class Context:
         _check(lib().dinfer_step(self._h, _ptr(hidden), _ptr(W), _ptr(E), _ptr(e_mask), _ptr(mask), _ptr(tokens),
                                  _ptr(credit_ids), _ptr(credit_val), ctypes.byref(params), _ptr(committed),
                                  _ptr(smoothed), _ptr(stats)), "dinfer_step")
+
+    def exchange_handle(self) -> bytes:
+        """64-byte CUDA IPC handle of this rank's gather buffer (peer-memory exchange)."""
+        buf = (ctypes.c_uint8 * 64)()
+        _check(lib().dinfer_exchange_handle(self._h, buf), "dinfer_exchange_handle")
+        return bytes(buf)
+
+    def exchange_open(self, handles: bytes):
+        """Open every rank's gather buffer (world x 64 bytes, rank order): dinfer_step
+        then exchanges the records over peer memory instead of NCCL."""
+        buf = (ctypes.c_uint8 * len(handles)).from_buffer_copy(handles)
+        _check(lib().dinfer_exchange_open(self._h, buf), "dinfer_exchange_open")
 
     def step_embed(self, hidden, W, E, e_mask, mask, tokens, credit_ids, credit_val, params: Params, committed,
                    smoothed, stats, emb):
