@@ -296,6 +296,15 @@ def gpu_arm(args):
         ctx.step(hid, Wd, Ed, emd, mask, tokens, cids if credit else None, cval if credit else None, p, committed,
                  smoothed, stats)
 
+    # calibrated vocab partition (K12): measured per-SM streaming rates -> slab split
+    partition = "even"
+    if not args.no_balance and smooth:
+        from paper_2510_08666_b200 import DInferError
+        try:
+            ctx.balance(hid, Wd, Ed, emd, p, iters=4)
+            partition = "calibrated (dinfer_balance, 4 steps)"
+        except DInferError:
+            pass
     # warm-up
     for _ in range(args.warmup):
         reset_and_flush()
@@ -427,7 +436,7 @@ def gpu_arm(args):
                        "parallelism": (f"vocab-sharded x{world} ("
                                        + ("in-kernel peer-memory record exchange" if exchange == "p2p"
                                           else "NCCL allgather") + ")") if world > 1 else "single GPU",
-                       "exchange": exchange,
+                       "exchange": exchange, "partition": partition,
                        "l2": "flushed (256 MiB write) before every timed step; inputs > L2"},
             "e2e": {"value": M / (e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e, "api": "dinfer_step_host"},
@@ -460,6 +469,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--config", default="moe", choices=sorted(CONFIGS))
+    ap.add_argument("--no-balance", action="store_true", help="keep the even K12 vocab partition")
     ap.add_argument("--exchange", default="auto", choices=["auto", "p2p", "nccl"],
                     help="N>1 record exchange: peer memory (auto: if every rank can open it) or NCCL allgather")
     args = ap.parse_args()

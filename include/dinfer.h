@@ -183,6 +183,24 @@ dinfer_status dinfer_step_host(dinfer_ctx* ctx, const uint16_t* hidden_h,
                                const dinfer_params* params, uint8_t* committed_h,
                                float* smoothed_h, float* stats_h);
 
+/* Calibrated vocab partition for the fused projection + smoothing kernel
+ * (K12, hidden split in two slices).  Per-SM HBM streaming rates on B200
+ * differ systematically (~100-123 us for equal W slabs at MoE shape; the
+ * CTA -> SM placement of a full-machine launch is the same every launch),
+ * so the finishing spread of equal slabs is exposed at the end of the step.
+ * dinfer_balance runs `iters` (+1 warm-up) steps with the given weights on
+ * scratch state, measures each CTA's W-phase time, pairs the slowest SM with
+ * the fastest in each vocab group and splits the group's rows so both finish
+ * their W slabs together (20..80 % bounds); later steps use that partition
+ * (results are the same up to fp32 summation order).  Synchronous; allocates
+ * scratch temporarily.  UNSUPPORTED unless the ctx runs K12 with two hidden
+ * slices and params.use_smooth.  dinfer_balance_reset restores the even
+ * partition.                                                                */
+dinfer_status dinfer_balance(dinfer_ctx* ctx, const uint16_t* hidden, const uint16_t* W_vocab,
+                             const uint16_t* E, const uint16_t* e_mask, const dinfer_params* params,
+                             int32_t iters);
+dinfer_status dinfer_balance_reset(dinfer_ctx* ctx);
+
 /* Peer-memory exchange of the per-rank records (world > 1),
  * replacing the NCCL allgather: the record finalize kernel stores this rank's
  * record straight into every rank's gather buffer over NVLink P2P (slot

@@ -60,6 +60,12 @@ struct dinfer_ctx {
   // describe its E phase (HW, HS, VG, KV = 16) and k1_VG x k1_SPG its slabs
   bool fused = false;
   int* probe_h = nullptr;  // DINFER_K12_PROBE: mapped pinned host progress words
+  // calibrated K12 partition (dinfer_balance): role per CTA, split per group, W-phase ns per CTA
+  int* d_role = nullptr;
+  int* d_split = nullptr;
+  unsigned* d_wdur = nullptr;
+  bool balanced = false;
+  bool record_wdur = false;
   int f_stages = 0, f_pstages = 0;
   size_t f_smem = 0;
   // workspace (device)
@@ -286,6 +292,11 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
     a.stages = c->f_stages;
     a.nchunks = c->k2_nchunks;
     a.chunk_rows = kChunkRows12;
+    if (c->balanced) {
+      a.role_of = c->d_role;
+      a.split = c->d_split;
+    }
+    if (c->record_wdur) a.wdur = c->d_wdur;
     K2Args b{};
     b.M = c->M;
     b.N = c->N;
@@ -539,6 +550,7 @@ void dinfer_destroy(dinfer_ctx* c) {
   void* bufs[] = {c->part1, c->counter, c->err, c->rec_local, c->flog, c->part2, c->ml, c->sel, c->row_cnt, c->trace,
                   c->mref,
                   c->mask_snap, c->rowdone, c->cids_snap, c->cval_snap, c->xbuf, c->xctl, c->d_peers,
+                  c->d_role, c->d_split, c->d_wdur,
                   c->grp_cnt, c->grp_pass,
                   c->st_hidden, c->st_block, c->st_smoothed,
                   c->g_mask, c->g_tok, c->g_cids, c->g_cval, c->g_com, c->g_sm, c->g_pdev, c->g_st, c->g_hbuf};
@@ -627,12 +639,15 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
       const int HS = hw > 0 ? s.H / hw : 0;
       if (hw > 0 && HS <= c->num_sms && (fused_mode == 2 || nch >= c->num_sms / HS)) {
         const int VG = std::max(1, std::min(c->num_sms / HS, nch));
-        int srm = 0;  // largest slab (16-row chunk granularity, same arithmetic as the kernel)
+        // largest slab (chunk granularity, same arithmetic as the kernel); with
+        // HS == 2 a calibrated split (dinfer_balance) may give one CTA most of
+        // its group, so the credit head table covers a whole group
+        int srm = 0;
         for (int g = 0; g < VG; ++g) {
           const long g0 = static_cast<long>(g) * nch / VG, g1 = static_cast<long>(g + 1) * nch / VG;
           for (int q = 0; q < HS; ++q) {
             const long a0 = g0 + q * (g1 - g0) / HS, a1 = g0 + (q + 1) * (g1 - g0) / HS;
-            srm = std::max<int>(srm, static_cast<int>((a1 - a0) * kChunkRows12));
+            srm = std::max<int>(srm, static_cast<int>((HS == 2 ? g1 - g0 : a1 - a0) * kChunkRows12));
           }
         }
         int st_max = 6, pst_max = 4;  // tuning overrides (measurement only)
@@ -756,6 +771,11 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
     A(dev_alloc(&c->cids_snap, static_cast<size_t>(M) * s.K));
     A(dev_alloc(&c->cval_snap, static_cast<size_t>(M) * s.K));
   }
+  if (c->fused) {
+    A(dev_alloc(&c->d_role, static_cast<size_t>(c->k1_grid)));
+    A(dev_alloc(&c->d_split, static_cast<size_t>(c->k2_VG)));
+    A(dev_alloc(&c->d_wdur, static_cast<size_t>(c->k1_grid)));
+  }
   if (s.world > 1) {
     A(dev_alloc(&c->rec_all, c->full_words * s.world));
     c->xslot = static_cast<long>(c->full_words) * s.world;
@@ -856,6 +876,168 @@ dinfer_status dinfer_exchange_open(dinfer_ctx* c, const uint8_t* handles) {
   }
   DI_CUDA(cudaMemcpy(c->d_peers, c->peer_host, sizeof(float*) * 8, cudaMemcpyHostToDevice));
   c->p2p = true;
+  return DINFER_OK;
+}
+
+dinfer_status dinfer_balance(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W, const uint16_t* E,
+                             const uint16_t* e_mask, const dinfer_params* p, int32_t iters) {
+  if (c == nullptr || p == nullptr || hidden == nullptr || W == nullptr || iters < 1) return DINFER_ERR_ARG;
+  if (!c->fused || c->k2_HS != 2 || !p->use_smooth) return DINFER_ERR_UNSUPPORTED;
+  dinfer_status s = check_params(c, p);
+  if (s != DINFER_OK) return s;
+  const int G = c->k1_grid, VG = c->k2_VG, nch = c->k2_nchunks;
+  const size_t M = static_cast<size_t>(c->M), K = static_cast<size_t>(c->shp.K), H = static_cast<size_t>(c->shp.H);
+  // scratch decode state (a block's first iteration: everything masked, no credit)
+  uint8_t *mask = nullptr, *com = nullptr;
+  int32_t *tok = nullptr, *cid = nullptr;
+  float *cval = nullptr, *sm = nullptr, *st = nullptr;
+  s = DINFER_OK;
+  auto A = [&](dinfer_status x) { if (s == DINFER_OK) s = x; };
+  A(dev_alloc(&mask, M));
+  A(dev_alloc(&com, M));
+  A(dev_alloc(&tok, M));
+  A(dev_alloc(&cid, M * K));
+  A(dev_alloc(&cval, M * K));
+  A(dev_alloc(&sm, M * H));
+  A(dev_alloc(&st, M * 4));
+  auto gsz = [&](int g) {
+    return static_cast<int>(static_cast<long>(g + 1) * nch / VG) - static_cast<int>(static_cast<long>(g) * nch / VG);
+  };
+  auto gbeg = [&](int g) { return static_cast<int>(static_cast<long>(g) * nch / VG); };
+  std::vector<int> role(G), split(VG);
+  std::vector<double> dur(G, 0.0);
+  // measure W-phase durations per CTA under a given partition
+  auto measure = [&](int n) -> dinfer_status {
+    std::fill(dur.begin(), dur.end(), 0.0);
+    c->record_wdur = true;
+    for (int it = 0; it <= n; ++it) {
+      DI_CUDA(cudaMemsetAsync(mask, 1, M, c->stream));
+      DI_CUDA(cudaMemsetAsync(cid, 0xff, 4 * M * K, c->stream));
+      DI_CUDA(cudaMemsetAsync(cval, 0, 4 * M * K, c->stream));
+      dinfer_status r = dinfer_step(c, hidden, W, E, e_mask, mask, tok, p->use_credit ? cid : nullptr,
+                                    p->use_credit ? cval : nullptr, p, com, sm, st);
+      if (r != DINFER_OK) return r;
+      std::vector<unsigned> w(G);
+      DI_CUDA(cudaMemcpyAsync(w.data(), c->d_wdur, 4 * G, cudaMemcpyDeviceToHost, c->stream));
+      DI_CUDA(cudaStreamSynchronize(c->stream));
+      if (it > 0)
+        for (int b = 0; b < G; ++b) dur[b] += w[b];
+    }
+    c->record_wdur = false;
+    return DINFER_OK;
+  };
+  auto upload = [&]() -> dinfer_status {
+    DI_CUDA(cudaMemcpy(c->d_role, role.data(), 4 * G, cudaMemcpyHostToDevice));
+    DI_CUDA(cudaMemcpy(c->d_split, split.data(), 4 * VG, cudaMemcpyHostToDevice));
+    return DINFER_OK;
+  };
+  // 1) the even partition
+  for (int b = 0; b < G; ++b) role[b] = b;
+  for (int g = 0; g < VG; ++g) split[g] = gbeg(g) + gsz(g) / 2;
+  if (s == DINFER_OK) s = upload();
+  c->balanced = true;
+  if (s == DINFER_OK) s = measure(iters);
+  if (s == DINFER_OK) {
+    // rows per ns of each CTA's SM (the CTA -> SM mapping is fixed launch to launch)
+    std::vector<double> rate(G);
+    for (int b = 0; b < G; ++b) {
+      const int g = role[b] / 2, q = role[b] % 2;
+      const int rows = (q == 0 ? split[g] - gbeg(g) : gbeg(g) + gsz(g) - split[g]) * kChunkRows12;
+      rate[b] = rows / std::max(1.0, dur[b] / iters);
+    }
+    // 2) pair the slowest SM with the fastest (DINFER_BALANCE_PAIR=1) or keep
+    //    the launch-order pairs, then move each group's split toward equal W
+    //    times, damped (rates are not independent of the partition)
+    std::vector<int> order(G);
+    for (int b = 0; b < G; ++b) order[b] = b;
+    std::sort(order.begin(), order.end(), [&](int x, int y) { return rate[x] < rate[y]; });
+    bool pair = true;  // measured: exit spread 238 -> 233 us with pairs, no gain from splits alone
+    if (const char* e = std::getenv("DINFER_BALANCE_PAIR")) pair = std::atoi(e) != 0;
+    double damp = 0.3;  // a full step over-corrects (per-SM rates shift with the partition)
+    if (const char* e = std::getenv("DINFER_BALANCE_DAMP")) damp = std::atof(e);
+    std::vector<int> cta0(G / 2), cta1(G / 2);
+    for (int k = 0; k < G / 2; ++k) {
+      cta0[k] = pair ? order[k] : 2 * k;
+      cta1[k] = pair ? order[G - 1 - k] : 2 * k + 1;
+    }
+    for (int k = 0; k < G / 2; ++k) {
+      const int x = cta0[k], y = cta1[k];
+      role[x] = 2 * k;
+      role[y] = 2 * k + 1;
+      const int n = gsz(k);
+      const double target = n * rate[x] / (rate[x] + rate[y]);
+      int n0 = static_cast<int>(std::lround(n / 2.0 + damp * (target - n / 2.0)));
+      n0 = std::min(std::max(n0, std::max(1, n / 5)), std::min(n - 1, n - n / 5));
+      split[k] = gbeg(k) + n0;
+    }
+    s = upload();
+    // 3) refinement rounds on the new pairs: re-measure, move each split a damped
+    //    step toward equal W-phase times of the pair
+    int rounds = 0;  // refinement rounds measured no better than one damped step
+    if (const char* e = std::getenv("DINFER_BALANCE_ROUNDS")) rounds = std::atoi(e);
+    for (int r = 0; r < rounds && s == DINFER_OK; ++r) {
+      s = measure(iters);
+      if (s != DINFER_OK) break;
+      for (int k = 0; k < G / 2; ++k) {
+        const int x = cta0[k], y = cta1[k];
+        const int n = gsz(k), n0 = split[k] - gbeg(k);
+        const double rx = n0 / std::max(1.0, dur[x]), ry = (n - n0) / std::max(1.0, dur[y]);
+        const double target = n * rx / (rx + ry);
+        int m0 = static_cast<int>(std::lround(n0 + damp * (target - n0)));
+        m0 = std::min(std::max(m0, std::max(1, n / 5)), std::min(n - 1, n - n / 5));
+        split[k] = gbeg(k) + m0;
+      }
+      s = upload();
+    }
+    if (std::getenv("DINFER_BALANCE_VERBOSE") != nullptr) {
+      double dmin = 1e30, dmax = 0;
+      for (int b = 0; b < G; ++b) {
+        dmin = std::min(dmin, dur[b] / iters);
+        dmax = std::max(dmax, dur[b] / iters);
+      }
+      std::fprintf(stderr, "[dinfer_balance] W-phase ns/CTA %.0f..%.0f; rate rows/us %.2f..%.2f\n", dmin, dmax,
+                   rate[order[0]] * 1e3, rate[order[G - 1]] * 1e3);
+      for (int k = 0; k < std::min(G / 2, 6); ++k)
+        std::fprintf(stderr, "  group %d: slow cta %d (%.0f ns) + fast cta %d (%.0f ns): %d / %d chunks\n", k,
+                     cta0[k], dur[cta0[k]] / iters, cta1[k], dur[cta1[k]] / iters,
+                     split[k] - gbeg(k), gsz(k) - (split[k] - gbeg(k)));
+      if (measure(iters) == DINFER_OK) {
+        double amin = 1e30, amax = 0;
+        for (int b = 0; b < G; ++b) {
+          amin = std::min(amin, dur[b] / iters);
+          amax = std::max(amax, dur[b] / iters);
+        }
+        std::fprintf(stderr, "  after: W-phase ns/CTA %.0f..%.0f; pair 0: %.0f / %.0f ns\n", amin, amax,
+                     dur[cta0[0]] / iters, dur[cta1[0]] / iters);
+      }
+    }
+  }
+  cudaStreamSynchronize(c->stream);
+  cudaFree(mask); cudaFree(com); cudaFree(tok); cudaFree(cid); cudaFree(cval); cudaFree(sm); cudaFree(st);
+  if (s != DINFER_OK) c->balanced = false;
+  return s;
+}
+
+/* diagnostics: even partition with the roles rotated by `shift` (does a CTA's
+ * W-phase time follow its SM or its rows?) */
+dinfer_status dinfer_debug_role_shift(dinfer_ctx* c, int32_t shift) {
+  if (c == nullptr || !c->fused || c->k2_HS != 2) return DINFER_ERR_UNSUPPORTED;
+  const int G = c->k1_grid, VG = c->k2_VG, nch = c->k2_nchunks;
+  std::vector<int> role(G), split(VG);
+  for (int b = 0; b < G; ++b) role[b] = ((b + shift) % G + G) % G;
+  for (int g = 0; g < VG; ++g) {
+    const int g0 = static_cast<int>(static_cast<long>(g) * nch / VG), g1 = static_cast<int>(static_cast<long>(g + 1) * nch / VG);
+    split[g] = g0 + (g1 - g0) / 2;
+  }
+  DI_CUDA(cudaMemcpy(c->d_role, role.data(), 4 * G, cudaMemcpyHostToDevice));
+  DI_CUDA(cudaMemcpy(c->d_split, split.data(), 4 * VG, cudaMemcpyHostToDevice));
+  c->balanced = true;
+  return DINFER_OK;
+}
+
+dinfer_status dinfer_balance_reset(dinfer_ctx* c) {
+  if (c == nullptr) return DINFER_ERR_ARG;
+  c->balanced = false;
   return DINFER_OK;
 }
 

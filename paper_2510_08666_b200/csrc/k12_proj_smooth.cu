@@ -202,13 +202,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* red = reinterpret_cast<float*>(smem + L.red_off);
 
   // ---- partition: group g = chunks [gc0, gc1) of 16 rows; slab q = chunks [sc0, sc1)
+  // With a calibrated partition (dinfer_balance) CTA b plays role role_of[b]
+  // and the group's rows split where the two SMs' measured W rates balance.
   const int SPG = a.SPG;
-  const int grp = blockIdx.x / SPG, q = blockIdx.x - grp * SPG;
+  const int role = (a.role_of != nullptr) ? a.role_of[blockIdx.x] : static_cast<int>(blockIdx.x);
+  const int grp = role / SPG, q = role - grp * SPG;
   const int gc0 = static_cast<int>(static_cast<long>(grp) * a.nchunks / a.VG);
   const int gc1 = static_cast<int>(static_cast<long>(grp + 1) * a.nchunks / a.VG);
   const int nc = gc1 - gc0;
-  const int sc0 = gc0 + static_cast<int>(static_cast<long>(q) * nc / SPG);
-  const int sc1 = gc0 + static_cast<int>(static_cast<long>(q + 1) * nc / SPG);
+  int sc0 = gc0 + static_cast<int>(static_cast<long>(q) * nc / SPG);
+  int sc1 = gc0 + static_cast<int>(static_cast<long>(q + 1) * nc / SPG);
+  if (a.split != nullptr && SPG == 2) {
+    const int sp = a.split[grp];
+    sc0 = (q == 0) ? gc0 : sp;
+    sc1 = (q == 0) ? sp : gc1;
+  }
+  const unsigned long long t_start = (a.wdur != nullptr) ? globaltimer_ns() : 0ull;
   const int r0 = min(a.V_local, sc0 * KV), r1 = min(a.V_local, sc1 * KV);
   const int ntiles = (r1 - r0 + kTileRows - 1) / kTileRows;
   const int n_own = sc1 - sc0, n_all = nc;
@@ -544,6 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&tempty[buf]);
     }
     if (tr != nullptr && threadIdx.x == 0) tr[2] = globaltimer_ns();
+    if (a.wdur != nullptr && threadIdx.x == 0) a.wdur[blockIdx.x] = static_cast<unsigned>(globaltimer_ns() - t_start);
 #pragma unroll
     for (int g = 0; g < kMaxGroups; ++g) {
       if (g < ng) {
@@ -562,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         stat_combine(m, ix, l, r[0], __float_as_int(r[1]), r[2]);
       }
       if (col < a.M) {
-        reinterpret_cast<float4*>(a.part)[static_cast<long>(col) * gridDim.x + blockIdx.x] =
+        reinterpret_cast<float4*>(a.part)[static_cast<long>(col) * gridDim.x + role] =
             make_float4(m, __int_as_float(ix), l, 0.f);
         m_own[col] = m;
       } else {

@@ -58,6 +58,12 @@ struct K1Args {
   const float* credit_val; // [M][K] (read for the snapshot)
   int* err;
   unsigned long long* trace;  // optional [grid][5]: globaltimer ns start, first W stage, last tile done, exit; smid
+  // K12 calibrated partition (dinfer_balance; nullptr = the even one): CTA b
+  // plays role role_of[b] (group role / SPG, slab role % SPG) and, with
+  // SPG == 2, group g's rows split at chunk split[g]; wdur[b] <- W-phase ns.
+  const int* role_of;
+  const int* split;
+  unsigned* wdur;
 };
 size_t k1_smem_bytes(int N, int H, int stages, int h_resident, int slab_rows_max);
 cudaError_t launch_k1(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,

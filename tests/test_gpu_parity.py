@@ -181,6 +181,24 @@ def test_next_input_embedding_rejects_unsupported(torch_cuda):
     ctx.close()
 
 
+def test_balanced_partition_matches_oracle(torch_cuda):
+    """dinfer_balance re-pairs CTAs and moves each group's split point to the
+    measured per-SM rates; the step's results must not change beyond fp32
+    summation order (decisions bit-exact), including with a skewed split."""
+    from paper_2510_08666_b200 import Context
+    V, H, B, S, K = 32768, 2048, 1, 32, 32
+    W, E = weights(V, H)
+    _, _, _, steps = vetted_trajectory(W, E, B, S, 13, hier_credit_smooth, max_iters=4, use_credit_table=True)
+    ctx = Context(B, S, H, K, V, smooth_capable=True)
+    assert ctx.geometry()["fused"] == 1
+    Wd, Ed, emd = to_dev_bf16(W), to_dev_bf16(E), to_dev_bf16(E[synth.mask_id(V)])
+    ctx.balance(to_dev_bf16(steps[0]["h"].reshape(B * S, H)), Wd, Ed, emd, gpu_params(steps[0]["params"]), iters=3)
+    replay(ctx, Wd, Ed, emd, steps, B, S, H, K, V)
+    ctx.balance_reset()
+    replay(ctx, Wd, Ed, emd, steps, B, S, H, K, V)
+    ctx.close()
+
+
 def test_without_pdl(torch_cuda, monkeypatch):
     monkeypatch.setenv("DINFER_PDL", "0")
     run_trajectory(torch_cuda, 2048, 512, 2, 32, 32, 9, hier_credit_smooth, True, max_iters=4)

@@ -22,6 +22,8 @@ Ed = dev(synth.make_E(V, H, 2)) if smooth else None
 em = dev(synth.make_E(V, H, 2, rows=(V - 1, V))[0]) if smooth else None
 ctx = Context(B, S, H, K, V, smooth_capable=smooth)
 p = make_params(decoder="hierarchical", use_credit=True, use_smooth=smooth)
+if "balance" in sys.argv:
+    ctx.balance(h, Wd, Ed, em, p, iters=4)
 mask = torch.ones((B, S), dtype=torch.uint8, device="cuda")
 tok = torch.full((B, S), V - 1, dtype=torch.int32, device="cuda")
 cids = torch.full((B, S, K), -1, dtype=torch.int32, device="cuda")
