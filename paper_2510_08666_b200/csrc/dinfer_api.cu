@@ -879,6 +879,37 @@ dinfer_status dinfer_exchange_open(dinfer_ctx* c, const uint8_t* handles) {
   return DINFER_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// Calibration steps run after dirtying the L2 (a write of 2x its size), the
+// state a preceding model forward leaves it in: the per-SM streaming rates
+// differ much more with dirty lines to write back (measured K1 W phase at 8B
+// shape: 166-177 us back to back, 172-194 us after such a write).  (A rate-
+// proportional K1 slab split for stats-only steps was measured too: no gain
+// beyond noise at damping 0.3-1.5, so only K12 is calibrated.)
+struct L2Dirty {
+  void* buf = nullptr;
+  size_t bytes = 0;
+  explicit L2Dirty(int dev) {
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    bytes = static_cast<size_t>(std::max(l2, 1 << 20)) * 2;
+    if (cudaMalloc(&buf, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      buf = nullptr;
+    }
+  }
+  void apply(cudaStream_t st) const {
+    if (buf != nullptr) cudaMemsetAsync(buf, 0x5a, bytes, st);
+  }
+  ~L2Dirty() { cudaFree(buf); }
+};
+
+}  // namespace
+
+extern "C" {
+
 dinfer_status dinfer_balance(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W, const uint16_t* E,
                              const uint16_t* e_mask, const dinfer_params* p, int32_t iters) {
   if (c == nullptr || p == nullptr || hidden == nullptr || W == nullptr || iters < 1) return DINFER_ERR_ARG;
@@ -907,10 +938,12 @@ dinfer_status dinfer_balance(dinfer_ctx* c, const uint16_t* hidden, const uint16
   std::vector<int> role(G), split(VG);
   std::vector<double> dur(G, 0.0);
   // measure W-phase durations per CTA under a given partition
+  const L2Dirty dirty(c->dev);
   auto measure = [&](int n) -> dinfer_status {
     std::fill(dur.begin(), dur.end(), 0.0);
     c->record_wdur = true;
     for (int it = 0; it <= n; ++it) {
+      dirty.apply(c->stream);
       DI_CUDA(cudaMemsetAsync(mask, 1, M, c->stream));
       DI_CUDA(cudaMemsetAsync(cid, 0xff, 4 * M * K, c->stream));
       DI_CUDA(cudaMemsetAsync(cval, 0, 4 * M * K, c->stream));
