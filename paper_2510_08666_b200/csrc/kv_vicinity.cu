@@ -22,6 +22,7 @@
 // attention's 64 x L x H x 4 flop run on CUDA cores.
 #include <cublas_v2.h>
 #include <cuda_bf16.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -229,6 +230,183 @@ __global__ void kv_attention_merge(const AttnArgs a) {
   a.out[static_cast<long>(a.lo + r) * a.H + col] = num / den;
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core attention (tcgen05): CTA = (head, 128-query tile, 256-key tile).
+//   S = Q K^T      UMMA M=128 (queries) x N=256 (keys) x K=128 (d), both
+//                  operands K-major SW128 straight from the row-major Q / cache
+//                  (TMA boxes [128|256 rows x 64 d]); S in TMEM columns 0-255
+//   P = exp2((S - m) log2e / sqrt(d)) per query row (thread = row, tcgen05.ld),
+//                  masked beyond L; bf16 into a K-major SW128 smem tile (the K
+//                  tile's bytes, consumed by then)
+//   O = P V        UMMA M=128 x N=128 (d) x K=256 (keys): V is the MN-major B
+//                  operand taken straight from the row-major cache (boxes
+//                  [64 d x 256 keys], LBO between the two 64-d blocks)
+// and the (m, l, O) partial of the key tile goes to the same split merge.
+// ---------------------------------------------------------------------------
+constexpr int kTQ = 128, kTK = 256;
+constexpr uint32_t kQBlk = kTQ * 128;    // [128 rows x 64 d] bf16 = 16 KB
+constexpr uint32_t kKBlk = kTK * 128;    // [256 rows x 64 d] bf16 = 32 KB
+constexpr uint32_t kPBlk = kTQ * 128;    // [128 q x 64 keys] bf16 = 16 KB
+constexpr size_t kTcSmem = 2 * kQBlk + 2 * kKBlk + 2 * kKBlk + 64 + 1024;
+
+struct TcArgs {
+  int L, H, R;
+  float* opart;  // [nkt][R][H]
+  float* mpart;  // [nkt][nheads][R]  base-2 max of the scaled scores
+  float* lpart;
+};
+
+__global__ void __launch_bounds__(128, 1)
+    kv_attention_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                    const __grid_constant__ CUtensorMap map_v, const TcArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                  // 2 d-blocks
+  uint8_t* sK = sQ + 2 * kQBlk;        // 2 d-blocks; reused for P (4 key-blocks of 16 KB)
+  uint8_t* sV = sK + 2 * kKBlk;        // 2 d-blocks, [256 keys x 64 d] each
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + 2 * kKBlk);  // full, sdone, odone
+  uint32_t* misc = reinterpret_cast<uint32_t*>(bar + 4);
+  const int head = blockIdx.x, q0 = blockIdx.y * kTQ, kt = blockIdx.z, k0 = kt * kTK;
+  const int nheads = a.H / kD;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&map_q);
+    prefetch_tmap(&map_k);
+    prefetch_tmap(&map_v);
+    for (int i = 0; i < 3; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(&misc[0], 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = misc[0];
+  const uint32_t tS = tmem, tO = tmem + 256;
+  if (threadIdx.x == 0) {
+    const uint64_t pol = policy_evict_normal();
+    mbar_expect_tx(&bar[0], 2 * kQBlk + 4 * kKBlk);
+    for (int j = 0; j < 2; ++j) {
+      tma_load_2d(sQ + j * kQBlk, &map_q, &bar[0], head * kD + 64 * j, q0, pol);
+      tma_load_2d(sK + j * kKBlk, &map_k, &bar[0], head * kD + 64 * j, k0, pol);
+      tma_load_2d(sV + j * kKBlk, &map_v, &bar[0], head * kD + 64 * j, k0, pol);
+    }
+    mbar_wait(&bar[0], 0);
+    tc_fence_after();
+    const uint32_t idesc_s = idesc_bf16(kTQ, kTK, false, false);
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        mma_bf16(tS, sdesc_sw128(smem_u32(sQ + j * kQBlk) + k * 32, 16, 1024),
+                 sdesc_sw128(smem_u32(sK + j * kKBlk) + k * 32, 16, 1024), idesc_s, (j | k) != 0);
+    mma_commit(&bar[1]);
+  }
+  __syncwarp();
+  // ---- softmax: thread = query row (TMEM lane), 256 key columns
+  mbar_wait(&bar[1], 0);
+  tc_fence_after();
+  const int row = warp * 32 + lane;
+  const uint32_t lrow = tS + (static_cast<uint32_t>(warp * 32) << 16);
+  const float sc = kLog2e * rsqrtf(static_cast<float>(kD));
+  float m = neg_inf();
+  for (int c = 0; c < kTK / 32; ++c) {
+    float x[32];
+    tmem_ld32(lrow + c * 32, x);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (k0 + c * 32 + j < a.L) m = fmaxf(m, x[j]);
+  }
+  const float ms = m * sc;  // base-2 max of the scaled scores
+  float l = 0.f;
+  for (int c = 0; c < kTK / 32; ++c) {
+    float x[32];
+    tmem_ld32(lrow + c * 32, x);
+    uint32_t pk[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int kk = k0 + c * 32 + 2 * j;
+      const float p0 = (kk < a.L) ? ex2(fmaf(x[2 * j], sc, -ms)) : 0.f;
+      const float p1 = (kk + 1 < a.L) ? ex2(fmaf(x[2 * j + 1], sc, -ms)) : 0.f;
+      l += p0 + p1;
+      const __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+      pk[j] = *reinterpret_cast<const uint32_t*>(&b2);
+    }
+    // keys c*32 .. c*32+31 -> key block (c / 2), 16-B chunks ((c % 2) * 4 + u) of this row, SW128
+    uint8_t* blk = sK + (c / 2) * kPBlk + row * 128;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t chunk = static_cast<uint32_t>((c % 2) * 4 + u) ^ static_cast<uint32_t>(row & 7);
+      *reinterpret_cast<uint4*>(blk + chunk * 16) = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+    }
+  }
+  fence_proxy_async();  // P (generic smem writes) -> visible to tcgen05.mma
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    // O[128 q x 128 d] = P[128 q x 256 keys] V[256 keys x 128 d]; V MN-major:
+    // 128-B rows of 64 d per key, 8-key atoms 1 KB apart (SBO), the two 64-d
+    // blocks kKBlk apart (LBO)
+    const uint32_t idesc_o = idesc_bf16(kTQ, kD, false, /*b MN-major*/ true);
+#pragma unroll
+    for (int kb = 0; kb < kTK / 64; ++kb)
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        mma_bf16(tO, sdesc_sw128(smem_u32(sK + kb * kPBlk) + k * 32, 16, 1024),
+                 sdesc_sw128(smem_u32(sV) + (kb * 64 + k * 16) * 128, kKBlk, 1024), idesc_o, (kb | k) != 0);
+    mma_commit(&bar[2]);
+  }
+  __syncwarp();
+  mbar_wait(&bar[2], 0);
+  tc_fence_after();
+  const uint32_t orow = tO + (static_cast<uint32_t>(warp * 32) << 16);
+  const bool valid = q0 + row < a.R;
+  float* op = a.opart + (static_cast<long>(kt) * a.R + q0 + row) * a.H + head * kD;
+  for (int c = 0; c < kD / 32; ++c) {
+    float x[32];
+    tmem_ld32(orow + c * 32, x);
+    if (valid) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(op + c * 32 + j) = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
+    }
+  }
+  if (valid) {
+    const long mi = (static_cast<long>(kt) * nheads + head) * a.R + q0 + row;
+    a.mpart[mi] = ms;
+    a.lpart[mi] = l;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 kv_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (fn == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// [outer][inner] bf16 row-major, SWIZZLE_128B boxes [box_outer][64]
+bool kv_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_outer) {
+  auto fn = kv_encoder();
+  if (fn == nullptr) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {64, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 }  // namespace dinfer
 
@@ -244,6 +422,10 @@ struct dinfer_kv {
   float* mpart = nullptr;
   float* lpart = nullptr;
   size_t part_rows = 0;   // capacity of opart in rows of H
+  bool tc = true;         // tcgen05 attention (DINFER_KV_TC=0: the CUDA-core kernel)
+  CUtensorMap map_q{}, map_k{}, map_v{};
+  const void* c_k = nullptr;
+  const void* c_v = nullptr;
 };
 
 extern "C" {
@@ -279,6 +461,12 @@ dinfer_status dinfer_kv_create(const dinfer_kv_shape* s, void* stream, dinfer_kv
   bool ok = cudaMalloc(&c->Q, LH * 2) == cudaSuccess && cudaMalloc(&c->opart, c->part_rows * s->H * 4) == cudaSuccess &&
             cudaMalloc(&c->mpart, nml * 4) == cudaSuccess && cudaMalloc(&c->lpart, nml * 4) == cudaSuccess;
   if (ok) ok = cublasCreate(&c->blas) == CUBLAS_STATUS_SUCCESS;
+  if (const char* e = std::getenv("DINFER_KV_TC")) c->tc = std::atoi(e) != 0;
+  if (ok && c->tc) {
+    ok = kv_map(&c->map_q, c->Q, static_cast<uint64_t>(s->H), static_cast<uint64_t>(s->L), kTQ) &&
+         cudaFuncSetAttribute(kv_attention_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(kTcSmem)) == cudaSuccess;
+  }
   if (ok) ok = cudaFuncSetAttribute(kv_attention, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kAttnSmem)) == cudaSuccess;
   if (!ok) {
@@ -333,6 +521,40 @@ dinfer_status dinfer_kv_step(dinfer_kv* c, const uint16_t* X, const uint16_t* Wq
       return DINFER_ERR_CUDA;
   }
   // ---- attention over all L cached positions
+  if (c->tc) {
+    if (Kc != c->c_k) {
+      if (!kv_map(&c->map_k, Kc, H, L, kTK)) return DINFER_ERR_CUDA;
+      c->c_k = Kc;
+    }
+    if (Vc != c->c_v) {
+      if (!kv_map(&c->map_v, Vc, H, L, kTK)) return DINFER_ERR_CUDA;
+      c->c_v = Vc;
+    }
+    const int nh = H / kD, nkt = (L + kTK - 1) / kTK, nqt = (R + kTQ - 1) / kTQ;
+    if (static_cast<size_t>(nkt) * R > c->part_rows) return DINFER_ERR_SHAPE;
+    TcArgs t{};
+    t.L = L;
+    t.H = H;
+    t.R = R;
+    t.opart = c->opart;
+    t.mpart = c->mpart;
+    t.lpart = c->lpart;
+    kv_attention_tc<<<dim3(nh, nqt, nkt), 128, kTcSmem, c->stream>>>(c->map_q, c->map_k, c->map_v, t);
+    AttnArgs m{};
+    m.L = L;
+    m.H = H;
+    m.R = R;
+    m.lo = lo;
+    m.nsplit = nkt;
+    m.opart = c->opart;
+    m.mpart = c->mpart;
+    m.lpart = c->lpart;
+    m.out = out;
+    const long n = static_cast<long>(R) * H;
+    kv_attention_merge<<<static_cast<unsigned>((n + 255) / 256), 256, 0, c->stream>>>(m);
+    if (cudaGetLastError() != cudaSuccess) return DINFER_ERR_CUDA;
+    return DINFER_OK;
+  }
   const int nheads = H / kD, qtiles = (R + kQT - 1) / kQT;
   // about one CTA per SM: each split re-reads the query tile and writes a partial
   int nsplit = std::max(1, (c->num_sms + nheads * qtiles - 1) / (nheads * qtiles));
