@@ -209,25 +209,33 @@ __global__ void __launch_bounds__(kAThreads) kv_attention(const AttnArgs a) {
   }
 }
 
-// out[lo + r][head*128 + c] = sum_s O_s 2^{m_s - m} / sum_s l_s 2^{m_s - m}
-// (splits merged in index order: deterministic).
+// out[lo + r][head*128 + c..c+3] = sum_s O_s 2^{m_s - m} / sum_s l_s 2^{m_s - m}
+// (splits merged in index order: deterministic), one float4 per thread.
 __global__ void kv_attention_merge(const AttnArgs a) {
   const long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= static_cast<long>(a.R) * a.H) return;
-  const int r = static_cast<int>(e / a.H), col = static_cast<int>(e - static_cast<long>(r) * a.H);
+  const int h4 = a.H / 4;
+  if (e >= static_cast<long>(a.R) * h4) return;
+  const int r = static_cast<int>(e / h4), col = static_cast<int>(e - static_cast<long>(r) * h4) * 4;
   const int head = col / kD, nheads = a.H / kD;
   float m = neg_inf();
-  for (int s = 0; s < a.nsplit; ++s) m = fmaxf(m, a.mpart[(static_cast<long>(s) * nheads + head) * a.R + r]);
-  float num = 0.f, den = 0.f;
+  for (int s = 0; s < a.nsplit; ++s) m = fmaxf(m, __ldcg(a.mpart + (static_cast<long>(s) * nheads + head) * a.R + r));
+  float den = 0.f;
+  float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int s = 0; s < a.nsplit; ++s) {
     const long mi = (static_cast<long>(s) * nheads + head) * a.R + r;
-    const float ms = a.mpart[mi];
+    const float ms = __ldcg(a.mpart + mi);
     if (ms == neg_inf()) continue;  // a split with no keys
     const float w = ex2(ms - m);
-    num = fmaf(a.opart[(static_cast<long>(s) * a.R + r) * a.H + col], w, num);
-    den = fmaf(a.lpart[mi], w, den);
+    const float4 o = __ldcg(reinterpret_cast<const float4*>(a.opart + (static_cast<long>(s) * a.R + r) * a.H + col));
+    num.x = fmaf(o.x, w, num.x);
+    num.y = fmaf(o.y, w, num.y);
+    num.z = fmaf(o.z, w, num.z);
+    num.w = fmaf(o.w, w, num.w);
+    den = fmaf(__ldcg(a.lpart + mi), w, den);
   }
-  a.out[static_cast<long>(a.lo + r) * a.H + col] = num / den;
+  const float inv = 1.f / den;
+  *reinterpret_cast<float4*>(a.out + static_cast<long>(a.lo + r) * a.H + col) =
+      make_float4(num.x * inv, num.y * inv, num.z * inv, num.w * inv);
 }
 
 // ---------------------------------------------------------------------------
@@ -250,10 +258,12 @@ constexpr uint32_t kPBlk = kTQ * 128;    // [128 q x 64 keys] bf16 = 16 KB
 constexpr size_t kTcSmem = 2 * kQBlk + 2 * kKBlk + 2 * kKBlk + 64 + 1024;
 
 struct TcArgs {
-  int L, H, R;
+  int L, H, R, lo, nkt;
   float* opart;  // [nkt][R][H]
   float* mpart;  // [nkt][nheads][R]  base-2 max of the scaled scores
   float* lpart;
+  int* cnt;      // [nheads][query tiles] key tiles done (the last one merges; self-resetting)
+  float* out;    // [L][H] rows lo..lo+R-1
 };
 
 __global__ void __launch_bounds__(128, 1)
@@ -382,6 +392,13 @@ __global__ void __launch_bounds__(128, 1)
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
+// Pointer arrays of the three projections (one batched GEMM).
+__global__ void kv_set_ptrs(const void** d, const void* a0, const void* a1, const void* a2, const void* b0,
+                            void* c0, void* c1, void* c2) {
+  const void* v[9] = {a0, a1, a2, b0, b0, b0, c0, c1, c2};
+  if (threadIdx.x < 9) d[threadIdx.x] = v[threadIdx.x];
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 kv_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (fn == nullptr) {
@@ -426,6 +443,8 @@ struct dinfer_kv {
   CUtensorMap map_q{}, map_k{}, map_v{};
   const void* c_k = nullptr;
   const void* c_v = nullptr;
+  int* cnt = nullptr;          // [nheads][query tiles] merge counters
+  const void** d_ptrs = nullptr;  // [9] batched-GEMM pointer arrays (A, B, C)
 };
 
 extern "C" {
@@ -456,10 +475,15 @@ dinfer_status dinfer_kv_create(const dinfer_kv_shape* s, void* stream, dinfer_kv
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t LH = static_cast<size_t>(s->L) * s->H;
-  c->part_rows = static_cast<size_t>(s->L) * 4 + 256;
+  // split partials: CUDA-core kernel <= 4 L rows; tcgen05 kernel one per 256-key tile
+  c->part_rows = std::max(static_cast<size_t>(s->L) * 4 + 256,
+                          static_cast<size_t>((s->L + kTK - 1) / kTK) * static_cast<size_t>(s->L));
   const size_t nml = c->part_rows * (s->H / kD);
   bool ok = cudaMalloc(&c->Q, LH * 2) == cudaSuccess && cudaMalloc(&c->opart, c->part_rows * s->H * 4) == cudaSuccess &&
             cudaMalloc(&c->mpart, nml * 4) == cudaSuccess && cudaMalloc(&c->lpart, nml * 4) == cudaSuccess;
+  const size_t ncnt = static_cast<size_t>(s->H / kD) * ((s->L + kTQ - 1) / kTQ);
+  if (ok) ok = cudaMalloc(&c->cnt, ncnt * 4) == cudaSuccess && cudaMemset(c->cnt, 0, ncnt * 4) == cudaSuccess &&
+               cudaMalloc(reinterpret_cast<void**>(&c->d_ptrs), 9 * sizeof(void*)) == cudaSuccess;
   if (ok) ok = cublasCreate(&c->blas) == CUBLAS_STATUS_SUCCESS;
   if (const char* e = std::getenv("DINFER_KV_TC")) c->tc = std::atoi(e) != 0;
   if (ok && c->tc) {
@@ -486,6 +510,8 @@ void dinfer_kv_destroy(dinfer_kv* c) {
   cudaFree(c->opart);
   cudaFree(c->mpart);
   cudaFree(c->lpart);
+  cudaFree(c->cnt);
+  cudaFree(const_cast<void**>(c->d_ptrs));
   delete c;
 }
 
@@ -510,16 +536,13 @@ dinfer_status dinfer_kv_step(dinfer_kv* c, const uint16_t* X, const uint16_t* Wq
   if (cublasSetStream(c->blas, c->stream) != CUBLAS_STATUS_SUCCESS) return DINFER_ERR_CUDA;
   const float one = 1.f, zero = 0.f;
   const long xoff = static_cast<long>(lo) * H;
-  struct Proj {
-    const uint16_t* W;
-    uint16_t* Y;
-  } proj[3] = {{Wk, Kc + xoff}, {Wv, Vc + xoff}, {Wq, c->Q}};
-  for (const Proj& pj : proj) {
-    if (cublasGemmEx(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, H, R, H, &one, pj.W, CUDA_R_16BF, H, X + xoff, CUDA_R_16BF,
-                     H, &zero, pj.Y, CUDA_R_16BF, H, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) !=
-        CUBLAS_STATUS_SUCCESS)
-      return DINFER_ERR_CUDA;
-  }
+  // one batched GEMM for the three projections (pointer arrays written on
+  // device, so consecutive forwards never race on a host staging buffer)
+  kv_set_ptrs<<<1, 32, 0, c->stream>>>(c->d_ptrs, Wk, Wv, Wq, X + xoff, Kc + xoff, Vc + xoff, c->Q);
+  if (cublasGemmBatchedEx(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, H, R, H, &one, c->d_ptrs, CUDA_R_16BF, H,
+                          c->d_ptrs + 3, CUDA_R_16BF, H, &zero, const_cast<void**>(c->d_ptrs + 6), CUDA_R_16BF, H,
+                          3, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
+    return DINFER_ERR_CUDA;
   // ---- attention over all L cached positions
   if (c->tc) {
     if (Kc != c->c_k) {
@@ -536,9 +559,13 @@ dinfer_status dinfer_kv_step(dinfer_kv* c, const uint16_t* X, const uint16_t* Wq
     t.L = L;
     t.H = H;
     t.R = R;
+    t.lo = lo;
+    t.nkt = nkt;
     t.opart = c->opart;
     t.mpart = c->mpart;
     t.lpart = c->lpart;
+    t.cnt = c->cnt;
+    t.out = out;
     kv_attention_tc<<<dim3(nh, nqt, nkt), 128, kTcSmem, c->stream>>>(c->map_q, c->map_k, c->map_v, t);
     AttnArgs m{};
     m.L = L;
@@ -550,8 +577,8 @@ dinfer_status dinfer_kv_step(dinfer_kv* c, const uint16_t* X, const uint16_t* Wq
     m.mpart = c->mpart;
     m.lpart = c->lpart;
     m.out = out;
-    const long n = static_cast<long>(R) * H;
-    kv_attention_merge<<<static_cast<unsigned>((n + 255) / 256), 256, 0, c->stream>>>(m);
+    const long n4 = static_cast<long>(R) * H / 4;
+    kv_attention_merge<<<static_cast<unsigned>((n4 + 127) / 128), 128, 0, c->stream>>>(m);
     if (cudaGetLastError() != cudaSuccess) return DINFER_ERR_CUDA;
     return DINFER_OK;
   }
@@ -577,8 +604,8 @@ dinfer_status dinfer_kv_step(dinfer_kv* c, const uint16_t* X, const uint16_t* Wq
   a.lpart = c->lpart;
   a.out = out;
   kv_attention<<<dim3(nheads, qtiles, nsplit), kAThreads, kAttnSmem, c->stream>>>(a);
-  const long n = static_cast<long>(R) * H;
-  kv_attention_merge<<<static_cast<unsigned>((n + 255) / 256), 256, 0, c->stream>>>(a);
+  const long n4 = static_cast<long>(R) * H / 4;
+  kv_attention_merge<<<static_cast<unsigned>((n4 + 127) / 128), 128, 0, c->stream>>>(a);
   if (cudaGetLastError() != cudaSuccess) return DINFER_ERR_CUDA;
   return DINFER_OK;
 }
