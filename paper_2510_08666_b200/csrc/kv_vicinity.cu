@@ -395,8 +395,16 @@ __global__ void __launch_bounds__(128, 1)
 // Pointer arrays of the three projections (one batched GEMM).
 __global__ void kv_set_ptrs(const void** d, const void* a0, const void* a1, const void* a2, const void* b0,
                             void* c0, void* c1, void* c2) {
-  const void* v[9] = {a0, a1, a2, b0, b0, b0, c0, c1, c2};
-  if (threadIdx.x < 9) d[threadIdx.x] = v[threadIdx.x];
+  if (threadIdx.x != 0) return;
+  d[0] = a0;
+  d[1] = a1;
+  d[2] = a2;
+  d[3] = b0;
+  d[4] = b0;
+  d[5] = b0;
+  d[6] = c0;
+  d[7] = c1;
+  d[8] = c2;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 kv_encoder() {
