@@ -175,7 +175,9 @@ dinfer_status dinfer_step_embed(dinfer_ctx* ctx, const uint16_t* hidden, const u
  * argument or of decoder / hier_runs_after_hi / use_credit / use_smooth /
  * stats_h nullness re-captures. Buffers the graph cannot capture (pageable
  * host memory) run the same sequence un-captured. hidden_h and smoothed_h
- * may be pageable; pinned buffers avoid a staging copy inside the driver. */
+ * may be pageable; pinned buffers avoid a staging copy inside the driver,
+ * and a pinned smoothed_h is written by the kernel directly (zero-copy; no
+ * D2H copy for the M*H*4-byte output). */
 dinfer_status dinfer_step_host(dinfer_ctx* ctx, const uint16_t* hidden_h,
                                const uint16_t* W_vocab, const uint16_t* E,
                                const uint16_t* e_mask, uint8_t* mask_h, int32_t* tokens_h,

@@ -1237,6 +1237,20 @@ dinfer_status dinfer_step_host(dinfer_ctx* c, const uint16_t* hidden_h, const ui
     std::memcpy(hs + o_cval, cval_h, 4 * M * K);
   }
   cudaStream_t sm = c->stream;
+  // smoothed (the largest output, M*H*4 B): if the caller's buffer is pinned,
+  // K34 writes it straight into host memory (zero-copy over PCIe, overlapped
+  // with the kernel) instead of a device buffer + a D2H copy
+  float* smoothed_dev = c->st_smoothed;
+  bool smoothed_zero_copy = false;
+  if (p->use_smooth && c->host_graph_ok) {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, smoothed_h) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer != nullptr && (reinterpret_cast<uintptr_t>(pa.devicePointer) % 16) == 0) {
+      smoothed_dev = static_cast<float*>(pa.devicePointer);
+      smoothed_zero_copy = true;
+    }
+    cudaGetLastError();
+  }
   // graph key: everything baked into the captured sequence (pointers + structural flags)
   const uint64_t key[12] = {reinterpret_cast<uint64_t>(hidden_h), reinterpret_cast<uint64_t>(W),
                             reinterpret_cast<uint64_t>(E),        reinterpret_cast<uint64_t>(e_mask),
@@ -1270,10 +1284,10 @@ dinfer_status dinfer_step_host(dinfer_ctx* c, const uint16_t* hidden_h, const ui
       st = dinfer_step(c, c->st_hidden, W, E, e_mask, d + o_mask, reinterpret_cast<int32_t*>(d + o_tok),
                        p->use_credit ? reinterpret_cast<int32_t*>(d + o_cid) : nullptr,
                        p->use_credit ? reinterpret_cast<float*>(d + o_cval) : nullptr, p, d + o_com,
-                       p->use_smooth ? c->st_smoothed : nullptr, reinterpret_cast<float*>(d + o_stats));
+                       p->use_smooth ? smoothed_dev : nullptr, reinterpret_cast<float*>(d + o_stats));
     c->pdev_active = nullptr;
     ok = ok && st == DINFER_OK && cudaMemcpyAsync(hs, d, total, cudaMemcpyDeviceToHost, sm) == cudaSuccess;
-    if (ok && p->use_smooth)
+    if (ok && p->use_smooth && !smoothed_zero_copy)
       ok = cudaMemcpyAsync(smoothed_h, c->st_smoothed, M * H * 4, cudaMemcpyDeviceToHost, sm) == cudaSuccess;
     const cudaError_t ee = cudaStreamEndCapture(sm, &g);
     c->stream = sm = user_stream;
@@ -1300,10 +1314,11 @@ dinfer_status dinfer_step_host(dinfer_ctx* c, const uint16_t* hidden_h, const ui
     s = dinfer_step(c, c->st_hidden, W, E, e_mask, d + o_mask, reinterpret_cast<int32_t*>(d + o_tok),
                     p->use_credit ? reinterpret_cast<int32_t*>(d + o_cid) : nullptr,
                     p->use_credit ? reinterpret_cast<float*>(d + o_cval) : nullptr, p, d + o_com,
-                    p->use_smooth ? c->st_smoothed : nullptr, reinterpret_cast<float*>(d + o_stats));
+                    p->use_smooth ? smoothed_dev : nullptr, reinterpret_cast<float*>(d + o_stats));
     if (s != DINFER_OK) return s;
     DI_CUDA(cudaMemcpyAsync(hs, d, total, cudaMemcpyDeviceToHost, sm));
-    if (p->use_smooth) DI_CUDA(cudaMemcpyAsync(smoothed_h, c->st_smoothed, M * H * 4, cudaMemcpyDeviceToHost, sm));
+    if (p->use_smooth && !smoothed_zero_copy)
+      DI_CUDA(cudaMemcpyAsync(smoothed_h, c->st_smoothed, M * H * 4, cudaMemcpyDeviceToHost, sm));
   }
   DI_CUDA(cudaStreamSynchronize(sm));
   std::memcpy(mask_h, hs + o_mask, M);
