@@ -117,6 +117,20 @@ def test_fused_and_two_kernel_smoothing_paths(torch_cuda, monkeypatch, fused):
     run_trajectory(torch_cuda, 2048, 1024, 2, 32, 32, 12, hier_credit_smooth, True, max_iters=3)
 
 
+def test_fused_four_hidden_slices(torch_cuda, monkeypatch):
+    """K12 with SPG = HS = 4 slabs per vocab group (the other-slab set B sums
+    three partner slabs): H = 4096 with N = 32 (1024-wide slices), and
+    H = 2048 with N = 64 (S = 64: 512-wide slices)."""
+    from paper_2510_08666_b200 import Context
+    monkeypatch.setenv("DINFER_FUSED", "2")
+    for (V, H, B, S) in ((8192, 4096, 1, 32), (4096, 2048, 1, 64)):
+        ctx = Context(B, S, H, 32, V, smooth_capable=True)
+        g = ctx.geometry()
+        ctx.close()
+        assert g["fused"] == 1 and g["k1_grid"] == 4 * g["k2_groups"], g
+        run_trajectory(torch_cuda, V, H, B, S, 32 if S == 32 else 64, 15, hier_credit_smooth, True, max_iters=3)
+
+
 @pytest.mark.parametrize("fused", ["0", "2"])
 def test_next_input_embedding(torch_cuda, monkeypatch, fused):
     """f2: dinfer_step_embed writes the next iteration's bf16 model input in
