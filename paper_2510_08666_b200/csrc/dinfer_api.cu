@@ -99,6 +99,8 @@ struct dinfer_ctx {
   uint64_t host_graph_key[12] = {};
   bool host_graph_failed = false;
   cudaStream_t cap_stream = nullptr;  // private capture stream
+  const float* zc_host = nullptr;     // smoothed_h whose device mapping zc_dev was looked up
+  float* zc_dev = nullptr;
   // dinfer_generate: block-local state, loop state and the cached loop graph
   uint8_t* g_mask = nullptr;
   int32_t* g_tok = nullptr;
@@ -1243,13 +1245,19 @@ dinfer_status dinfer_step_host(dinfer_ctx* c, const uint16_t* hidden_h, const ui
   float* smoothed_dev = c->st_smoothed;
   bool smoothed_zero_copy = false;
   if (p->use_smooth && c->host_graph_ok) {
-    cudaPointerAttributes pa{};
-    if (cudaPointerGetAttributes(&pa, smoothed_h) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
-        pa.devicePointer != nullptr && (reinterpret_cast<uintptr_t>(pa.devicePointer) % 16) == 0) {
-      smoothed_dev = static_cast<float*>(pa.devicePointer);
+    if (smoothed_h != c->zc_host) {  // pointer attributes cached per buffer
+      c->zc_host = smoothed_h;
+      c->zc_dev = nullptr;
+      cudaPointerAttributes pa{};
+      if (cudaPointerGetAttributes(&pa, smoothed_h) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+          pa.devicePointer != nullptr && (reinterpret_cast<uintptr_t>(pa.devicePointer) % 16) == 0)
+        c->zc_dev = static_cast<float*>(pa.devicePointer);
+      cudaGetLastError();
+    }
+    if (c->zc_dev != nullptr) {
+      smoothed_dev = c->zc_dev;
       smoothed_zero_copy = true;
     }
-    cudaGetLastError();
   }
   // graph key: everything baked into the captured sequence (pointers + structural flags)
   const uint64_t key[12] = {reinterpret_cast<uint64_t>(hidden_h), reinterpret_cast<uint64_t>(W),
@@ -1320,7 +1328,7 @@ dinfer_status dinfer_step_host(dinfer_ctx* c, const uint16_t* hidden_h, const ui
     if (p->use_smooth && !smoothed_zero_copy)
       DI_CUDA(cudaMemcpyAsync(smoothed_h, c->st_smoothed, M * H * 4, cudaMemcpyDeviceToHost, sm));
   }
-  DI_CUDA(cudaStreamSynchronize(sm));
+  DI_CUDA(cudaStreamSynchronize(sm));  // (polling cudaStreamQuery measured slower: e2e 289 -> 295-301 us)
   std::memcpy(mask_h, hs + o_mask, M);
   std::memcpy(tokens_h, hs + o_tok, 4 * M);
   std::memcpy(committed_h, hs + o_com, M);
