@@ -31,7 +31,7 @@
 // overlaps, so E loads start slot by slot as the W phase drains.  The logits /
 // P rings alias the credit-capture tables (used only in the W phase).
 //
-// Warp roles (7 warps):
+// Warp roles (8 warps):
 //   0-3  W phase: K1 epilogue (tcgen05.ld, warp-shuffle (m, idx, l) reduce-
 //        scatter, credited-logit capture, raw logits -> flog); E phase: P
 //        producers (P = exp(f - m_ref) as bf16 hi + lo, SWIZZLE_64B K-major
@@ -40,6 +40,7 @@
 //   5    MMA issuer: 128xNx16 bf16 UMMAs (W: swap-AB; E: A = E^T MN-major).
 //   6    logits producer: flog chunks [N x 32] by TMA (own chunks after the
 //        CTA's own W epilogue, others after the group counter), and m_oth.
+//   7    helper: with warps 4-6, the second half of the final epilogue.
 // TMEM: 512 columns.  W-phase accumulators double-buffered at [0, 2N); E
 // set A at [0, nsub N), set B at [256, 256 + nsub N) (E MMAs start only after
 // the W epilogue has drained its accumulators).
@@ -55,7 +56,7 @@ namespace {
 
 constexpr int kEpiWarps = 4;
 constexpr int kEpiThreads = kEpiWarps * kWarpThreads;
-constexpr int kThreads = (kEpiWarps + 3) * kWarpThreads;
+constexpr int kThreads = (kEpiWarps + 4) * kWarpThreads;  // + TMA, MMA, logits TMA, epilogue helper
 constexpr uint32_t kChunkBytes = kTileRows * 128;  // W [128 rows x 64 k] bf16 = 16 KB
 constexpr uint32_t kWBytes = 2 * kChunkBytes;      // two adjacent K chunks per stage (256 B per W row)
 constexpr int kMaxGroups = 2;                      // N <= 64 (32-column groups)
@@ -458,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       advance(ps, pph, b.pstages);
     }
     __syncwarp();
-  } else {
+  } else if (warp < kEpiWarps) {
     // ------------------------------------------------------------ W phase: K1 epilogue
     grid_dep_wait();  // mask / credit ids of the previous step's commit visible
     if (a.mask_snap != nullptr && blockIdx.x == 0)
@@ -644,33 +645,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       advance(ps, pph, b.pstages);
     }
 
-    // ------------------------------------------------------------ epilogue: partial rows
+    // reference rescales of the two accumulator sets (no MMA dependence)
     if (tid == 0) PROBE(4, n_all * 10000 + n_own * 10 + (has_oth ? 1 : 0));
-    if (n_all > 0) {
-      if (b.probe != nullptr) {
-        uint32_t spins = 0;
-        while (!mbar_try_wait(smem_u32(accfull), 0)) {
-          if (++spins > (1u << 24)) {
-            if (tid == 0) {
-              volatile int* o = b.probe + blockIdx.x * 64;
-              for (int w = 0; w < 8; ++w) o[w] = prog[w];
-              const int nb = 2 * a.stages + 4 + 4 * b.pstages + 3;
-              for (int w = 0; w < nb && w < 28; ++w) {
-                const uint64_t raw = *reinterpret_cast<volatile uint64_t*>(full + w);
-                o[8 + 2 * w] = static_cast<int>(raw & 0xffffffffu);
-                o[9 + 2 * w] = static_cast<int>(raw >> 32);
-              }
-              __threadfence_system();
-            }
-            __trap();
-          }
-        }
-      } else {
-        mbar_wait(accfull, 0);
-      }
-      tc_fence_after();
-    }
-    if (tid == 0) PROBE(5, 1);
     for (int s = tid; s < N; s += kEpiThreads) {
       const float mo = m_own[s], mt = m_oth[s];
       const float mg = fmaxf(mo, mt);
@@ -678,17 +654,52 @@ __global__ void __launch_bounds__(kThreads, 1)
       scB[s] = (has_oth && s < a.M) ? fexp(mt - mg) : 0.f;
       if (hs == 0 && s < a.M) b.mref[static_cast<long>(grp) * a.M + s] = mg;
     }
-    named_bar_epi();
-    // TMEM [128 h lanes x 32 s] -> smem tile [32 s][128 h] (the idle ring) ->
-    // coalesced float4 rows of the [M][H] partial (measured faster than 32
-    // scalar stores per lane straight from registers)
-    float* tile = reinterpret_cast<float*>(ring);
+  }
+
+  // ------------------------------------------------------------ epilogue: partial rows
+  // All 8 warps (the TMA / MMA / logits warps are idle by now): warps w and
+  // w + 4 read the same TMEM lane quarter, so the two warp groups take half of
+  // the hidden sub-tiles each.  TMEM [128 h lanes x 32 s] -> smem tile
+  // [32 s][128 h] (the idle ring, double-buffered per group) -> coalesced
+  // float4 rows of the [M][H] partial.
+  asm volatile("bar.sync 3, %0;" ::"n"(kThreads) : "memory");  // scA / scB visible
+  if (n_all > 0) {
+    if (b.probe != nullptr) {
+      uint32_t spins = 0;
+      while (!mbar_try_wait(smem_u32(accfull), 0)) {
+        if (++spins > (1u << 24)) {
+          if (threadIdx.x == 0) {
+            volatile int* o = b.probe + blockIdx.x * 64;
+            for (int w = 0; w < 8; ++w) o[w] = prog[w];
+            const int nb = 2 * a.stages + 4 + 4 * b.pstages + 3;
+            for (int w = 0; w < nb && w < 28; ++w) {
+              const uint64_t raw = *reinterpret_cast<volatile uint64_t*>(full + w);
+              o[8 + 2 * w] = static_cast<int>(raw & 0xffffffffu);
+              o[9 + 2 * w] = static_cast<int>(raw >> 32);
+            }
+            __threadfence_system();
+          }
+          __trap();
+        }
+      }
+    } else {
+      mbar_wait(accfull, 0);
+    }
+    tc_fence_after();
+  }
+  if (threadIdx.x == 0) PROBE(5, 1);
+  {
+    const int wg = warp / 4, wq = warp % 4, tg = threadIdx.x % kEpiThreads;
+    const int ng = N / 32;
+    const int half = (b.nsub + 1) / 2;
+    const int sub0 = (wg == 0) ? 0 : half, sub1 = (wg == 0) ? half : b.nsub;
+    float* tile = reinterpret_cast<float*>(ring) + wg * 2 * (32 * 128);
     const int hbase = hs * b.HW;
-    for (int sub = 0; sub < b.nsub; ++sub) {
+    const uint32_t lanebase = tmem_base + (static_cast<uint32_t>(wq * 32) << 16);
+    for (int sub = sub0; sub < sub1; ++sub) {
       for (int g = 0; g < ng; ++g) {
         float x[32];
         const uint32_t col = static_cast<uint32_t>(sub * N + g * 32);
-        const uint32_t lanebase = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
         if (n_own > 0) {
           tmem_ld32(lanebase + col, x);
 #pragma unroll
@@ -703,11 +714,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) x[jj] = fmaf(y[jj], scB[g * 32 + jj], x[jj]);
         }
-        float* t = tile + ((sub * ng + g) & 1) * (32 * 128);  // two tiles: one barrier per pass
+        float* t = tile + (((sub - sub0) * ng + g) & 1) * (32 * 128);  // two tiles: one barrier per pass
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) t[jj * 128 + warp * 32 + lane] = x[jj];
-        named_bar_epi();
-        for (int u = tid; u < 32 * 32; u += kEpiThreads) {
+        for (int jj = 0; jj < 32; ++jj) t[jj * 128 + wq * 32 + lane] = x[jj];
+        if (wg == 0) {
+          asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+        } else {
+          asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads) : "memory");
+        }
+        for (int u = tg; u < 32 * 32; u += kEpiThreads) {
           const int row = u >> 5, c4 = u & 31;
           const int s = g * 32 + row;
           if (s < a.M)
