@@ -447,6 +447,7 @@ def gpu_arm(args):
             "phases_ms": phases,
             "ms_per_step_with_kernel_events": ms_b,
             "ms_per_step_min": min(step_ms), "ms_per_step_max": max(step_ms),
+            "ms_per_step_p10_p50_p90": [float(np.percentile(step_ms, q)) for q in (10, 50, 90)],
             "geometry": geom,
             "clocks": sampler.report(),
             "wall_s_timed_loop": wall,
