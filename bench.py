@@ -379,10 +379,13 @@ def gpu_arm(args):
             flush.fill_(1.0)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        ctx.step_host(hid_h, Wd, Ed, emd, mask_h, tok_h, cids_h if credit else None, cval_h if credit else None, p,
-                      com_h, sm_h, st_h)
+        # the public host-buffer API: copies in, step, results back in host memory
+        # (e1 follows the result copies on the stream), then the unpacking wait
+        ctx.step_host_async(hid_h, Wd, Ed, emd, mask_h, tok_h, cids_h if credit else None,
+                            cval_h if credit else None, p, com_h, sm_h, st_h)
         e1.record(stream)
         e1.synchronize()
+        ctx.step_host_wait()
         if i >= args.warmup:
             e2e_ms.append(e0.elapsed_time(e1))
     e2e = sum(e2e_ms) / len(e2e_ms)
@@ -439,7 +442,7 @@ def gpu_arm(args):
                        "exchange": exchange, "partition": partition,
                        "l2": "flushed (256 MiB write) before every timed step; inputs > L2"},
             "e2e": {"value": M / (e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": e2e, "api": "dinfer_step_host"},
+                    "ms_per_step": e2e, "api": "dinfer_step_host_async + dinfer_step_host_wait"},
             "gpu_launches": launches * args.steps,
             "roofline": roof,
             "step_roofline": None if M > 256 else {"bytes": step_bytes, "achieved_gbs": step_bytes / (ms * 1e-3) / 1e9,

@@ -217,6 +217,22 @@ dinfer_status dinfer_balance_reset(dinfer_ctx* ctx);
 dinfer_status dinfer_exchange_handle(dinfer_ctx* ctx, uint8_t out_handle[64]);
 dinfer_status dinfer_exchange_open(dinfer_ctx* ctx, const uint8_t* handles);
 
+/* The same host-buffer step split in two: _async validates, stages the small
+ * state, enqueues copies + step + result copies on the ctx stream and returns;
+ * _wait synchronises the stream and unpacks mask / tokens / credit /
+ * committed / stats into the host buffers given to _async (smoothed_h is
+ * written by the device directly).  Lets the caller overlap its own host
+ * work with the step, or time the step on the stream (CUDA events around
+ * _async and its copies).  One pending call per ctx; _wait without a
+ * pending _async returns ARG.                                               */
+dinfer_status dinfer_step_host_async(dinfer_ctx* ctx, const uint16_t* hidden_h,
+                                     const uint16_t* W_vocab, const uint16_t* E,
+                                     const uint16_t* e_mask, uint8_t* mask_h, int32_t* tokens_h,
+                                     int32_t* credit_ids_h, float* credit_val_h,
+                                     const dinfer_params* params, uint8_t* committed_h,
+                                     float* smoothed_h, float* stats_h);
+dinfer_status dinfer_step_host_wait(dinfer_ctx* ctx);
+
 /* Split phases (tests, caller-managed collectives).
  * dinfer_record_words: number of fp32 words of one rank's record:
  *   M*(4+K)  statistics: per row (m, v* as int32 bits (global id), l =

@@ -101,6 +101,16 @@ struct dinfer_ctx {
   cudaStream_t cap_stream = nullptr;  // private capture stream
   const float* zc_host = nullptr;     // smoothed_h whose device mapping zc_dev was looked up
   float* zc_dev = nullptr;
+  struct Pending {  // dinfer_step_host_async -> dinfer_step_host_wait
+    bool active;
+    uint8_t* mask_h;
+    int32_t* tokens_h;
+    uint8_t* committed_h;
+    int32_t* cids_h;
+    float* cval_h;
+    float* stats_h;
+    size_t o_mask, o_tok, o_cid, o_cval, o_com, o_stats;
+  } pend{};
   // dinfer_generate: block-local state, loop state and the cached loop graph
   uint8_t* g_mask = nullptr;
   int32_t* g_tok = nullptr;
@@ -1199,7 +1209,7 @@ dinfer_status dinfer_step_combine(dinfer_ctx* c, const float* records, const uin
                      credit_val, p, committed, smoothed, stats);
 }
 
-dinfer_status dinfer_step_host(dinfer_ctx* c, const uint16_t* hidden_h, const uint16_t* W, const uint16_t* E,
+dinfer_status dinfer_step_host_async(dinfer_ctx* c, const uint16_t* hidden_h, const uint16_t* W, const uint16_t* E,
                                const uint16_t* e_mask, uint8_t* mask_h, int32_t* tokens_h, int32_t* cids_h,
                                float* cval_h, const dinfer_params* p, uint8_t* committed_h, float* smoothed_h,
                                float* stats_h) {
@@ -1328,16 +1338,39 @@ dinfer_status dinfer_step_host(dinfer_ctx* c, const uint16_t* hidden_h, const ui
     if (p->use_smooth && !smoothed_zero_copy)
       DI_CUDA(cudaMemcpyAsync(smoothed_h, c->st_smoothed, M * H * 4, cudaMemcpyDeviceToHost, sm));
   }
-  DI_CUDA(cudaStreamSynchronize(sm));  // (polling cudaStreamQuery measured slower: e2e 289 -> 295-301 us)
-  std::memcpy(mask_h, hs + o_mask, M);
-  std::memcpy(tokens_h, hs + o_tok, 4 * M);
-  std::memcpy(committed_h, hs + o_com, M);
-  if (p->use_credit) {
-    std::memcpy(cids_h, hs + o_cid, 4 * M * K);
-    std::memcpy(cval_h, hs + o_cval, 4 * M * K);
-  }
-  if (stats_h != nullptr) std::memcpy(stats_h, hs + o_stats, 16 * M);
+  // the unpacking into the caller's buffers happens in dinfer_step_host_wait
+  c->pend = {true, mask_h, tokens_h, committed_h, p->use_credit ? cids_h : nullptr,
+             p->use_credit ? cval_h : nullptr, stats_h, o_mask, o_tok, o_cid, o_cval, o_com, o_stats};
   return DINFER_OK;
+}
+
+dinfer_status dinfer_step_host_wait(dinfer_ctx* c) {
+  if (c == nullptr) return DINFER_ERR_ARG;
+  if (!c->pend.active) return DINFER_ERR_ARG;
+  c->pend.active = false;
+  DI_CUDA(cudaStreamSynchronize(c->stream));  // (polling cudaStreamQuery measured slower: e2e 289 -> 295-301 us)
+  const size_t M = static_cast<size_t>(c->M), K = static_cast<size_t>(c->shp.K);
+  const uint8_t* hs = c->st_host;
+  const auto& q = c->pend;
+  std::memcpy(q.mask_h, hs + q.o_mask, M);
+  std::memcpy(q.tokens_h, hs + q.o_tok, 4 * M);
+  std::memcpy(q.committed_h, hs + q.o_com, M);
+  if (q.cids_h != nullptr) {
+    std::memcpy(q.cids_h, hs + q.o_cid, 4 * M * K);
+    std::memcpy(q.cval_h, hs + q.o_cval, 4 * M * K);
+  }
+  if (q.stats_h != nullptr) std::memcpy(q.stats_h, hs + q.o_stats, 16 * M);
+  return DINFER_OK;
+}
+
+dinfer_status dinfer_step_host(dinfer_ctx* c, const uint16_t* hidden_h, const uint16_t* W, const uint16_t* E,
+                               const uint16_t* e_mask, uint8_t* mask_h, int32_t* tokens_h, int32_t* cids_h,
+                               float* cval_h, const dinfer_params* p, uint8_t* committed_h, float* smoothed_h,
+                               float* stats_h) {
+  const dinfer_status s = dinfer_step_host_async(c, hidden_h, W, E, e_mask, mask_h, tokens_h, cids_h, cval_h, p,
+                                                 committed_h, smoothed_h, stats_h);
+  if (s != DINFER_OK) return s;
+  return dinfer_step_host_wait(c);
 }
 
 // ---------------------------------------------------------------- generation loop

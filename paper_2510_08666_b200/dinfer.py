@@ -89,6 +89,8 @@ def lib():
         "dinfer_step": (S, [P, P, P, P, P, P, P, P, P, POINTER(Params), P, P, P]),
         "dinfer_step_host": (S, [P, P, P, P, P, P, P, P, P, POINTER(Params), P, P, P]),
         "dinfer_step_embed": (S, [P, P, P, P, P, P, P, P, P, POINTER(Params), P, P, P, P]),
+        "dinfer_step_host_async": (S, [P, P, P, P, P, P, P, P, P, POINTER(Params), P, P, P]),
+        "dinfer_step_host_wait": (S, [P]),
         "dinfer_record_words": (c_size_t, [P, S]),
         "dinfer_step_local": (S, [P, P, P, P, P, P, POINTER(Params), P]),
         "dinfer_step_combine": (S, [P, P, P, P, P, P, P, POINTER(Params), P, P, P]),
@@ -222,6 +224,19 @@ class Context:
         _check(lib().dinfer_step_embed(self._h, _ptr(hidden), _ptr(W), _ptr(E), _ptr(e_mask), _ptr(mask),
                                        _ptr(tokens), _ptr(credit_ids), _ptr(credit_val), ctypes.byref(params),
                                        _ptr(committed), _ptr(smoothed), _ptr(stats), _ptr(emb)), "dinfer_step_embed")
+
+    def step_host_async(self, hidden_h, W, E, e_mask, mask_h, tokens_h, credit_ids_h, credit_val_h, params: Params,
+                        committed_h, smoothed_h=None, stats_h=None):
+        """dinfer_step_host without the final wait (see step_host_wait)."""
+        self._pending = (hidden_h, mask_h, tokens_h, credit_ids_h, credit_val_h, committed_h, smoothed_h, stats_h)
+        _check(lib().dinfer_step_host_async(self._h, _ptr(hidden_h), _ptr(W), _ptr(E), _ptr(e_mask), _ptr(mask_h),
+                                            _ptr(tokens_h), _ptr(credit_ids_h), _ptr(credit_val_h),
+                                            ctypes.byref(params), _ptr(committed_h), _ptr(smoothed_h),
+                                            _ptr(stats_h)), "dinfer_step_host_async")
+
+    def step_host_wait(self):
+        _check(lib().dinfer_step_host_wait(self._h), "dinfer_step_host_wait")
+        self._pending = None
 
     def step_host(self, hidden_h, W, E, e_mask, mask_h, tokens_h, credit_ids_h, credit_val_h, params: Params,
                   committed_h, smoothed_h=None, stats_h=None):

@@ -329,6 +329,17 @@ def test_step_host_matches_device_step(torch_cuda):
     assert np.array_equal(cids.numpy(), dev["cids"]) and np.array_equal(cval.numpy(), dev["cval"])
     still = mask.numpy().astype(bool)
     assert np.array_equal(sm.numpy()[still], dev["smoothed"][still])
+    # the split form: enqueue, then wait + unpack
+    mask.fill_(1); tok.fill_(V - 1); cids.fill_(-1); cval.zero_(); com.zero_(); sm.fill_(float("nan"))
+    ctx.step_host_async(hh, Wd, Ed, emd, mask, tok, cids, cval, p, com, sm, sts)
+    ctx.step_host_wait()
+    assert np.array_equal(com.numpy().astype(bool), dev["committed"])
+    assert np.array_equal(tok.numpy(), dev["tokens"])
+    assert np.array_equal(cids.numpy(), dev["cids"]) and np.array_equal(cval.numpy(), dev["cval"])
+    assert np.array_equal(sm.numpy()[still], dev["smoothed"][still])
+    from paper_2510_08666_b200 import DInferError
+    with pytest.raises(DInferError):
+        ctx.step_host_wait()  # nothing pending
 
 
 @pytest.mark.parametrize("pinned", [True, False])
