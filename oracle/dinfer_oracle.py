@@ -18,8 +18,14 @@ order and notation.  A library primitive (matmul, argmax, exp, log) is used
 as a step; there is no blocking, fusion or reordering.
 
 Readings of silent / ambiguous passages are the SURVEY.md §8(c) readings
-c1..c20, restated in DESIGN.md "Readings"; each function names the ones it
-takes.
+c1..c20 plus c21..c27 for the §8(f) rows, restated in DESIGN.md "Readings";
+each function names the ones it takes.
+
+Beyond the step: the blockwise generation loop of Alg. 1
+(`generate`, f1), the next iteration's model input (`next_input_embedding`,
+f2), the vicinity KV-cache refresh on a synthetic attention layer
+(`refresh_region`, `vicinity_step`, `attention`, f3) and the credit-fused
+smoothing variant (`smooth_credit_fused`, f4).
 
 Parity pins: every function is pinned by tests under ``tests/`` (marked
 "not gpu") against worked examples, closed forms, brute force and
