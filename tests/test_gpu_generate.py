@@ -82,3 +82,15 @@ def test_generate_max_forwards_truncates(torch_cuda):
     cfg = O.GenConfig(prompt_len=2, S=S, mask_id=V - 1, eos_id=V - 2, tau_target=0.9, max_forwards=5)
     ref = _run(torch_cuda, 2, 3, 2, 6, base, cfg, eos_at=[])
     assert ref["truncated"] and ref["F"] == 5
+
+
+def test_generate_on_the_fused_kernel(torch_cuda, monkeypatch):
+    """The generation graph around K12 (forced: the tiny vocabulary would pick
+    K1 -> K2), hierarchical + credit + smoothing with early termination: the
+    loop must match the oracle token for token."""
+    monkeypatch.setenv("DINFER_FUSED", "2")
+    base = O.Params(decoder=O.DEC_HIERARCHICAL, theta_lo=0.62, use_credit=True, use_smooth=True)
+    cfg = O.GenConfig(prompt_len=3, S=S, mask_id=V - 1, eos_id=V - 2, tau_target=0.9, tau_decay_steps=3,
+                      alpha_init=0.1, alpha_growth=0.05, alpha_preset=0.3)
+    _run(torch_cuda, 2, 3, 3, 7, base, cfg, eos_at=[(1, 1, 5)], repeats=2)
+
