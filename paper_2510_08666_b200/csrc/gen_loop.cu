@@ -187,6 +187,10 @@ __global__ void __launch_bounds__(kGenThreads) gen_control_kernel(const GenArgs 
 // Model stand-in: hidden of global iteration n = st[2] (clamped to the
 // supplied trajectory) into the step's hidden buffer.
 __global__ void gen_hidden_kernel(const GenArgs a) {
+  // the step's first kernel (launched with PDL) may start now: it prefetches
+  // W (which does not depend on this copy) and waits for the copy before the
+  // hidden loads
+  grid_dep_launch_dependents();
   const long n = min(static_cast<long>(a.st[2]), a.hsrc_iters - 1);
   const uint4* src = reinterpret_cast<const uint4*>(a.hsrc + n * a.MH);
   uint4* dst = reinterpret_cast<uint4*>(a.hbuf);

@@ -149,6 +149,24 @@ DI void group_pass(const K2Args& b, int grp, int SPG) {
     if (prog != nullptr) prog[w] = (v); \
   } while (0)
 
+// The W boxes of W stage `idx` of a slab (tile idx / spt, K chunks 2 (idx % spt) ..+1).
+DI void issue_w_stage(const CUtensorMap* map_w, const CUtensorMap* map_w8, uint8_t* slot, uint64_t* bar, int r0,
+                      int r1, int idx, int spt, uint64_t pol) {
+  const int t = idx / spt, kc0 = (idx - t * spt) * 2;
+  const int row0 = r0 + t * kTileRows;
+  const int rows = min(kTileRows, r1 - row0);
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int kc = kc0 + j;
+    uint8_t* dst = slot + j * kChunkBytes;
+    if (rows == kTileRows) {
+      tma_load_2d(dst, map_w, bar, kc * kKChunk, row0, pol);
+    } else {  // slab tail: 8-row boxes land at the same swizzled offsets
+      for (int r = 0; r < rows; r += kRowGran) tma_load_2d(dst + r * 128, map_w8, bar, kc * kKChunk, row0 + r, pol);
+    }
+  }
+}
+
 DI void advance(int& stage, uint32_t& phase, int n) {
   if (++stage == n) {
     stage = 0;
@@ -270,6 +288,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(own_ready, 1);
     mbar_init(oth_ready, 1);
     fence_mbar_init();
+    // W does not depend on the preceding kernel: the first ring's worth of W
+    // stages is issued now (each stage's barrier expects W + hidden bytes; the
+    // hidden boxes follow after grid_dep_wait)
+    const int spt = a.num_kc / 2, npre = min(a.stages, ntiles * spt);
+    const uint64_t pol_first = policy_evict_first();
+    for (int i = 0; i < npre; ++i) {
+      const int t = i / spt;
+      const int rows = min(kTileRows, r1 - (r0 + t * kTileRows));
+      mbar_expect_tx(&full[i], 2u * (static_cast<uint32_t>(rows) * 128u + hchunk));
+      issue_w_stage(&map_w, &map_w8, ring + i * L.wslot, &full[i], r0, r1, i, spt, pol_first);
+    }
   }
   if (warp == 5) tmem_alloc(&misc[0], 512);
   if (warp < kEpiWarps) {
@@ -285,38 +314,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 4) {
     // ------------------------------------------------------------ TMA: W (+ hidden), then E
     if (lane == 0) {
-      grid_dep_wait();  // hidden may be produced by the preceding kernel
       const uint64_t pol_first = policy_evict_first();  // W and E are streamed exactly once
       const uint64_t pol_h = policy_evict_last();       // hidden is re-read by every CTA
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = 0; t < ntiles; ++t) {
-        const int row0 = r0 + t * kTileRows;
-        const int rows = min(kTileRows, r1 - row0);
-        for (int kc0 = 0; kc0 < a.num_kc; kc0 += 2) {
-          mbar_wait(&empty[stage], phase ^ 1u);
-          uint8_t* slot = ring + stage * L.wslot;
-          mbar_expect_tx(&full[stage], 2u * (static_cast<uint32_t>(rows) * 128u + hchunk));
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int kc = kc0 + j;
-            uint8_t* dst = slot + j * kChunkBytes;
-            if (rows == kTileRows) {
-              tma_load_2d(dst, &map_w, &full[stage], kc * kKChunk, row0, pol_first);
-            } else {  // slab tail: 8-row boxes land at the same swizzled offsets
-              for (int r = 0; r < rows; r += kRowGran)
-                tma_load_2d(dst + r * 128, &map_w8, &full[stage], kc * kKChunk, row0 + r, pol_first);
-            }
-            tma_load_2d(slot + kWBytes + j * hchunk, &map_h, &full[stage], kc * kKChunk, 0, pol_h);
-          }
-          advance(stage, phase, a.stages);
-        }
-        PROBE(0, 1000 + t);
+      const int spt = a.num_kc / 2, nW = ntiles * spt, npre = min(a.stages, nW);
+      grid_dep_wait();  // hidden may be produced by the preceding kernel
+      for (int i = 0; i < npre; ++i) {  // hidden boxes of the W stages issued before the wait
+        const int kc0 = (i % spt) * 2;
+        for (int j = 0; j < 2; ++j)
+          tma_load_2d(ring + i * L.wslot + kWBytes + j * hchunk, &map_h, &full[i], (kc0 + j) * kKChunk, 0, pol_h);
       }
+      int stage = npre % a.stages;
+      uint32_t phase = (npre == a.stages) ? 1u : 0u;
+      for (int idx = npre; idx < nW; ++idx) {
+        const int t = idx / spt, kc0 = (idx - t * spt) * 2;
+        const int rows = min(kTileRows, r1 - (r0 + t * kTileRows));
+        mbar_wait(&empty[stage], phase ^ 1u);
+        uint8_t* slot = ring + stage * L.wslot;
+        mbar_expect_tx(&full[stage], 2u * (static_cast<uint32_t>(rows) * 128u + hchunk));
+        issue_w_stage(&map_w, &map_w8, slot, &full[stage], r0, r1, idx, spt, pol_first);
+        for (int j = 0; j < 2; ++j)
+          tma_load_2d(slot + kWBytes + j * hchunk, &map_h, &full[stage], (kc0 + j) * kKChunk, 0, pol_h);
+        advance(stage, phase, a.stages);
+      }
+      PROBE(0, 1000 + ntiles);
       // E ring over the same bytes: slot j's first fill waits for the final
       // consumption of every W slot it overlaps (the f_i-th commit of W slot i
       // completes phase f_i - 1)
-      const int nW = ntiles * (a.num_kc / 2);
       int es = 0;
       uint32_t eph = 0;
       for (int j = 0; j < n_all; ++j) {
