@@ -255,6 +255,14 @@ dinfer_status dinfer_step_combine(dinfer_ctx* ctx, const float* records, const u
 /* Block start: empty every credit slot (ids = -1, values = 0). */
 dinfer_status dinfer_credit_reset(dinfer_ctx* ctx, int32_t* credit_ids, float* credit_val);
 
+/* Block start (Alg. 1 NextBlock, with the credit reset of P:327)
+ * as one kernel on the ctx stream: mask = 1 and tokens = mask_id for every
+ * position, credit slots empty (credit_ids / credit_val both NULL to skip).
+ * It lets the next dinfer_step start streaming W underneath it (programmatic
+ * dependent launch).  Errors: ARG.                                          */
+dinfer_status dinfer_block_reset(dinfer_ctx* ctx, uint8_t* mask, int32_t* tokens, int32_t* credit_ids,
+                                 float* credit_val, int32_t mask_id);
+
 /* Host schedule helpers.
  * alpha_t = min(init + growth*t, preset)
  * tau_t   = 1 - (1 - target)*min(t, decay_steps)/decay_steps,

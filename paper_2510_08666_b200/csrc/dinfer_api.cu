@@ -1544,6 +1544,15 @@ dinfer_status dinfer_credit_reset(dinfer_ctx* c, int32_t* credit_ids, float* cre
   return DINFER_OK;
 }
 
+dinfer_status dinfer_block_reset(dinfer_ctx* c, uint8_t* mask, int32_t* tokens, int32_t* credit_ids,
+                                 float* credit_val, int32_t mask_id) {
+  if (c == nullptr || mask == nullptr || tokens == nullptr) return DINFER_ERR_ARG;
+  if ((credit_ids == nullptr) != (credit_val == nullptr)) return DINFER_ERR_ARG;
+  if (mask_id < 0 || mask_id >= c->shp.V_total) return DINFER_ERR_ARG;
+  DI_CUDA(launch_block_reset(mask, tokens, credit_ids, credit_val, c->M, c->shp.K, mask_id, c->stream, c->pdl));
+  return DINFER_OK;
+}
+
 dinfer_status dinfer_sync(dinfer_ctx* c) {
   if (c == nullptr) return DINFER_ERR_ARG;
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) return DINFER_ERR_CUDA;

@@ -199,7 +199,31 @@ __global__ void gen_hidden_kernel(const GenArgs a) {
     dst[j] = src[j];
 }
 
+// Block start (Alg. 1 NextBlock; credit reset P:327): every
+// position of the block masked, credit slots empty.  Triggers its dependents
+// first, so the next step's kernel (PDL) can start streaming W underneath.
+__global__ void block_reset_kernel(uint8_t* mask, int32_t* tokens, int32_t* cids, float* cval, int M, int K,
+                                   int mask_id) {
+  grid_dep_launch_dependents();
+  grid_dep_wait();  // the previous step's commit is complete
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int i = tid; i < M; i += nt) {
+    mask[i] = 1;
+    tokens[i] = mask_id;
+  }
+  if (cids != nullptr)
+    for (int i = tid; i < M * K; i += nt) {
+      cids[i] = -1;
+      cval[i] = 0.f;
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_block_reset(uint8_t* mask, int32_t* tokens, int32_t* cids, float* cval, int M, int K, int mask_id,
+                               cudaStream_t st, bool pdl) {
+  return launch_ex(block_reset_kernel, dim3(1), dim3(1024), 0, st, pdl, mask, tokens, cids, cval, M, K, mask_id);
+}
 
 cudaError_t launch_gen_init(const GenArgs& a, cudaGraphConditionalHandle h, cudaStream_t st) {
   gen_init_kernel<<<1, kGenThreads, sizeof(int) * a.B, st>>>(a, h);

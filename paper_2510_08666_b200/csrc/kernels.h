@@ -217,6 +217,8 @@ struct GenArgs {
   uint16_t* hbuf;               // [M][H] the step's hidden input
 };
 cudaError_t launch_gen_init(const GenArgs& a, cudaGraphConditionalHandle h, cudaStream_t st);
+cudaError_t launch_block_reset(uint8_t* mask, int32_t* tokens, int32_t* cids, float* cval, int M, int K, int mask_id,
+                               cudaStream_t st, bool pdl);
 cudaError_t launch_gen_control(const GenArgs& a, cudaGraphConditionalHandle h, cudaStream_t st);
 cudaError_t launch_gen_hidden(const GenArgs& a, int grid, cudaStream_t st);
 

@@ -95,6 +95,7 @@ def lib():
         "dinfer_step_local": (S, [P, P, P, P, P, P, POINTER(Params), P]),
         "dinfer_step_combine": (S, [P, P, P, P, P, P, P, POINTER(Params), P, P, P]),
         "dinfer_credit_reset": (S, [P, P, P]),
+        "dinfer_block_reset": (S, [P, P, P, P, P, S]),
         "dinfer_alpha_schedule": (c_float, [c_float, c_float, c_float, S]),
         "dinfer_tau_schedule": (c_float, [c_float, S, S]),
         "dinfer_sync": (S, [P]),
@@ -224,6 +225,11 @@ class Context:
         _check(lib().dinfer_step_embed(self._h, _ptr(hidden), _ptr(W), _ptr(E), _ptr(e_mask), _ptr(mask),
                                        _ptr(tokens), _ptr(credit_ids), _ptr(credit_val), ctypes.byref(params),
                                        _ptr(committed), _ptr(smoothed), _ptr(stats), _ptr(emb)), "dinfer_step_embed")
+
+    def block_reset(self, mask, tokens, credit_ids, credit_val, mask_id: int):
+        """Block start on the device (mask = 1, tokens = mask_id, credit slots empty)."""
+        _check(lib().dinfer_block_reset(self._h, _ptr(mask), _ptr(tokens), _ptr(credit_ids), _ptr(credit_val),
+                                        int(mask_id)), "dinfer_block_reset")
 
     def step_host_async(self, hidden_h, W, E, e_mask, mask_h, tokens_h, credit_ids_h, credit_val_h, params: Params,
                         committed_h, smoothed_h=None, stats_h=None):

@@ -270,6 +270,42 @@ def test_determinism_repeat(torch_cuda):
         assert np.array_equal(np.nan_to_num(out["smoothed"]), np.nan_to_num(ref["smoothed"]))
 
 
+@pytest.mark.parametrize("fused", ["0", "2"])
+def test_block_reset_back_to_back(torch_cuda, monkeypatch, fused):
+    """dinfer_block_reset + dinfer_step chained back to back (PDL, no host sync,
+    the bench's headline loop): every step equals a step on fresh state."""
+    import torch
+    monkeypatch.setenv("DINFER_FUSED", fused)
+    from paper_2510_08666_b200 import Context
+    V, H, B, S, K = 4096, 512, 1, 32, 8
+    W, E = weights(V, H)
+    ctx = Context(B, S, H, K, V)
+    h = to_dev_bf16(synth.planted_hidden(W, B * S, seed=11))
+    Wd, Ed, emd = to_dev_bf16(W), to_dev_bf16(E), to_dev_bf16(E[V - 1])
+    p = gpu_params(O.Params(decoder=O.DEC_HIERARCHICAL, use_credit=True, use_smooth=True))
+    fresh = GpuState(B, S, H, K, synth.mask_id(V))
+    ctx.step(h, Wd, Ed, emd, fresh.mask, fresh.tokens, fresh.cids, fresh.cval, p, fresh.committed, fresh.smoothed,
+             fresh.stats)
+    torch.cuda.synchronize()
+    ref = fresh.snapshot()
+    assert ref["committed"].any()  # the step changes the state the reset has to undo
+    st = GpuState(B, S, H, K, synth.mask_id(V))
+    st.mask.zero_()
+    st.tokens.fill_(3)
+    st.cids.fill_(5)
+    st.cval.fill_(2.0)
+    torch.cuda.synchronize()
+    for _ in range(4):
+        ctx.block_reset(st.mask, st.tokens, st.cids, st.cval, synth.mask_id(V))
+        ctx.step(h, Wd, Ed, emd, st.mask, st.tokens, st.cids, st.cval, p, st.committed, st.smoothed, st.stats)
+    ctx.sync()
+    out = st.snapshot()
+    for k in ("committed", "tokens", "mask", "cids", "cval", "m", "lse", "ptilde"):
+        assert np.array_equal(out[k], ref[k]), k
+    assert np.array_equal(np.nan_to_num(out["smoothed"]), np.nan_to_num(ref["smoothed"]))
+    ctx.close()
+
+
 # ---------------------------------------------------------------- split phases / vocab sharding on one GPU
 @pytest.mark.parametrize("G", [2, 4, 8])
 def test_sharded_split_phase_matches_oracle(torch_cuda, G):
