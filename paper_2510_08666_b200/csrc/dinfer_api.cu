@@ -786,7 +786,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
   if (c->fused) {
     A(dev_alloc(&c->d_role, static_cast<size_t>(c->k1_grid)));
     A(dev_alloc(&c->d_split, static_cast<size_t>(c->k2_VG)));
-    A(dev_alloc(&c->d_wdur, static_cast<size_t>(c->k1_grid)));
+    A(dev_alloc(&c->d_wdur, 2 * static_cast<size_t>(c->k1_grid)));  // W phase | whole CTA, ns
   }
   if (s.world > 1) {
     A(dev_alloc(&c->rec_all, c->full_words * s.world));
@@ -948,11 +948,12 @@ dinfer_status dinfer_balance(dinfer_ctx* c, const uint16_t* hidden, const uint16
   };
   auto gbeg = [&](int g) { return static_cast<int>(static_cast<long>(g) * nch / VG); };
   std::vector<int> role(G), split(VG);
-  std::vector<double> dur(G, 0.0);
-  // measure W-phase durations per CTA under a given partition
+  std::vector<double> dur(G, 0.0), tot(G, 0.0);
+  // measure W-phase and whole-CTA durations per CTA under a given partition
   const L2Dirty dirty(c->dev);
   auto measure = [&](int n) -> dinfer_status {
     std::fill(dur.begin(), dur.end(), 0.0);
+    std::fill(tot.begin(), tot.end(), 0.0);
     c->record_wdur = true;
     for (int it = 0; it <= n; ++it) {
       dirty.apply(c->stream);
@@ -962,11 +963,14 @@ dinfer_status dinfer_balance(dinfer_ctx* c, const uint16_t* hidden, const uint16
       dinfer_status r = dinfer_step(c, hidden, W, E, e_mask, mask, tok, p->use_credit ? cid : nullptr,
                                     p->use_credit ? cval : nullptr, p, com, sm, st);
       if (r != DINFER_OK) return r;
-      std::vector<unsigned> w(G);
-      DI_CUDA(cudaMemcpyAsync(w.data(), c->d_wdur, 4 * G, cudaMemcpyDeviceToHost, c->stream));
+      std::vector<unsigned> w(2 * G);
+      DI_CUDA(cudaMemcpyAsync(w.data(), c->d_wdur, 8 * G, cudaMemcpyDeviceToHost, c->stream));
       DI_CUDA(cudaStreamSynchronize(c->stream));
       if (it > 0)
-        for (int b = 0; b < G; ++b) dur[b] += w[b];
+        for (int b = 0; b < G; ++b) {
+          dur[b] += w[b];
+          tot[b] += w[G + b];
+        }
     }
     c->record_wdur = false;
     return DINFER_OK;
@@ -982,14 +986,31 @@ dinfer_status dinfer_balance(dinfer_ctx* c, const uint16_t* hidden, const uint16
   if (s == DINFER_OK) s = upload();
   c->balanced = true;
   if (s == DINFER_OK) s = measure(iters);
+  // objective: equal whole-CTA times (DINFER_BALANCE_OBJ=total, default) or equal
+  // W-phase times (=w).  A CTA streams its W rows (H bf16 each) and then its
+  // hidden slice of every E row of its group (H/2 bf16 each), so with per-SM
+  // streaming rates r_x, r_y a group of n chunks gives CTA x
+  //   n0 = n ((a + e) r_x - e r_y) / (a (r_x + r_y))    (a = W, e = E bytes per chunk)
+  // for equal totals, n0 = n r_x / (r_x + r_y) for equal W phases.
+  bool obj_total = true;
+  if (const char* e = std::getenv("DINFER_BALANCE_OBJ")) obj_total = std::strcmp(e, "w") != 0;
+  const double wa = 2.0 * static_cast<double>(H), we = obj_total ? static_cast<double>(H) : 0.0;
+  auto own_chunks = [&](int b) {
+    const int g = role[b] / 2, q = role[b] % 2;
+    return q == 0 ? split[g] - gbeg(g) : gbeg(g) + gsz(g) - split[g];
+  };
+  auto cta_rate = [&](int b) {  // bytes per ns over the objective's span
+    const int g = role[b] / 2;
+    const double bytes = own_chunks(b) * wa + gsz(g) * we;
+    return bytes / std::max(1.0, (obj_total ? tot[b] : dur[b]) / iters);
+  };
+  auto target_n0 = [&](int n, double rx, double ry) {
+    return n * ((wa + we) * rx - we * ry) / (wa * (rx + ry));
+  };
   if (s == DINFER_OK) {
-    // rows per ns of each CTA's SM (the CTA -> SM mapping is fixed launch to launch)
+    // streaming rate of each CTA's SM (the CTA -> SM mapping is fixed launch to launch)
     std::vector<double> rate(G);
-    for (int b = 0; b < G; ++b) {
-      const int g = role[b] / 2, q = role[b] % 2;
-      const int rows = (q == 0 ? split[g] - gbeg(g) : gbeg(g) + gsz(g) - split[g]) * kChunkRows12;
-      rate[b] = rows / std::max(1.0, dur[b] / iters);
-    }
+    for (int b = 0; b < G; ++b) rate[b] = cta_rate(b);
     // 2) pair the slowest SM with the fastest (DINFER_BALANCE_PAIR=1) or keep
     //    the launch-order pairs, then move each group's split toward equal W
     //    times, damped (rates are not independent of the partition)
@@ -1010,7 +1031,7 @@ dinfer_status dinfer_balance(dinfer_ctx* c, const uint16_t* hidden, const uint16
       role[x] = 2 * k;
       role[y] = 2 * k + 1;
       const int n = gsz(k);
-      const double target = n * rate[x] / (rate[x] + rate[y]);
+      const double target = target_n0(n, rate[x], rate[y]);
       int n0 = static_cast<int>(std::lround(n / 2.0 + damp * (target - n / 2.0)));
       n0 = std::min(std::max(n0, std::max(1, n / 5)), std::min(n - 1, n - n / 5));
       split[k] = gbeg(k) + n0;
@@ -1026,8 +1047,7 @@ dinfer_status dinfer_balance(dinfer_ctx* c, const uint16_t* hidden, const uint16
       for (int k = 0; k < G / 2; ++k) {
         const int x = cta0[k], y = cta1[k];
         const int n = gsz(k), n0 = split[k] - gbeg(k);
-        const double rx = n0 / std::max(1.0, dur[x]), ry = (n - n0) / std::max(1.0, dur[y]);
-        const double target = n * rx / (rx + ry);
+        const double target = target_n0(n, cta_rate(x), cta_rate(y));
         int m0 = static_cast<int>(std::lround(n0 + damp * (target - n0)));
         m0 = std::min(std::max(m0, std::max(1, n / 5)), std::min(n - 1, n - n / 5));
         split[k] = gbeg(k) + m0;
@@ -1040,20 +1060,22 @@ dinfer_status dinfer_balance(dinfer_ctx* c, const uint16_t* hidden, const uint16
         dmin = std::min(dmin, dur[b] / iters);
         dmax = std::max(dmax, dur[b] / iters);
       }
-      std::fprintf(stderr, "[dinfer_balance] W-phase ns/CTA %.0f..%.0f; rate rows/us %.2f..%.2f\n", dmin, dmax,
-                   rate[order[0]] * 1e3, rate[order[G - 1]] * 1e3);
+      std::fprintf(stderr, "[dinfer_balance] objective %s; W-phase ns/CTA %.0f..%.0f; rate GB/s %.2f..%.2f\n",
+                   obj_total ? "total" : "w", dmin, dmax, rate[order[0]], rate[order[G - 1]]);
       for (int k = 0; k < std::min(G / 2, 6); ++k)
         std::fprintf(stderr, "  group %d: slow cta %d (%.0f ns) + fast cta %d (%.0f ns): %d / %d chunks\n", k,
                      cta0[k], dur[cta0[k]] / iters, cta1[k], dur[cta1[k]] / iters,
                      split[k] - gbeg(k), gsz(k) - (split[k] - gbeg(k)));
       if (measure(iters) == DINFER_OK) {
-        double amin = 1e30, amax = 0;
+        double amin = 1e30, amax = 0, tmin = 1e30, tmax = 0;
         for (int b = 0; b < G; ++b) {
           amin = std::min(amin, dur[b] / iters);
           amax = std::max(amax, dur[b] / iters);
+          tmin = std::min(tmin, tot[b] / iters);
+          tmax = std::max(tmax, tot[b] / iters);
         }
-        std::fprintf(stderr, "  after: W-phase ns/CTA %.0f..%.0f; pair 0: %.0f / %.0f ns\n", amin, amax,
-                     dur[cta0[0]] / iters, dur[cta1[0]] / iters);
+        std::fprintf(stderr, "  after: W-phase ns/CTA %.0f..%.0f, whole CTA %.0f..%.0f; pair 0: %.0f / %.0f ns\n",
+                     amin, amax, tmin, tmax, tot[cta0[0]] / iters, tot[cta1[0]] / iters);
       }
     }
   }

@@ -760,6 +760,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 5) tmem_dealloc(tmem_base, 512);
+  if (a.wdur != nullptr && threadIdx.x == 0)  // whole-CTA duration (calibration objective)
+    a.wdur[gridDim.x + blockIdx.x] = static_cast<unsigned>(globaltimer_ns() - t_start);
   if (tr != nullptr && threadIdx.x == 0) {
     tr[3] = globaltimer_ns();
     if (tr2 != nullptr) {
