@@ -42,3 +42,29 @@ def test_gpu_arm_line_tiny():
     assert d["gpu_launches"] >= 3 * 5  # block reset + K1 + K34 per step
     assert d["roofline"]["bound"] in ("hbm", "tensor") and d["roofline"]["frac"] > 0
     assert "no flush" in d["config"]["l2"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config,exchange", [("tiny", "p2p"), ("moe", "p2p")])
+def test_gpu_arm_two_ranks_one_device(config, exchange):
+    """The N = 2 code path of bench.py end to end on one GPU (both ranks on
+    cuda:0, gloo process group; BENCH_SAME_DEVICE=1): vocab-sharded contexts,
+    the peer-memory record exchange (CUDA IPC; NCCL refuses two ranks on one
+    device, so its allgather is covered by the split-phase tests), the
+    back-to-back timed loop.  Time-sliced on one device, so only the contract
+    is checked, not the timing."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ, BENCH_SAME_DEVICE="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", config,
+           "--steps", "3", "--warmup", "3", "--exchange", exchange, "--no-balance"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["vocab_shards"] == 2 and d["config"]["exchange"] == exchange
+    assert d["value"] > 0 and d["e2e"]["value"] > 0
