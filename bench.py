@@ -307,8 +307,8 @@ def gpu_arm(args):
     if not args.no_balance and smooth:
         from paper_2510_08666_b200 import DInferError
         try:
-            ctx.balance(hid, Wd, Ed, emd, p, iters=4)
-            partition = "calibrated (dinfer_balance, 4 steps)"
+            ctx.balance(hid, Wd, Ed, emd, p, iters=4, mode="back_to_back")
+            partition = "calibrated for back-to-back steps (dinfer_balance, 4 steps)"
         except DInferError:
             pass
     # warm-up
@@ -324,9 +324,9 @@ def gpu_arm(args):
     # it.  No L2 flush: each step streams 1.29 GB of W + E (> 126 MB L2).
     # Loop A2: the same K steps one at a time with L2 flushed before each
     # (outside the events): no overlap with the previous step.
-    # Loop B: as A2 with the library's per-kernel events on (these serialise the
+    # Loop B: as A with the library's per-kernel events on (these serialise the
     # PDL overlap between kernels, so B's per-kernel times are upper bounds)
-    # -> roofline per kernel.
+    # and a stream sync per step to read them -> roofline per kernel.
     ea = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     evb = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -352,7 +352,7 @@ def gpu_arm(args):
         torch.cuda.synchronize()
         ctx.set_timing(True)
         for i in range(args.steps):
-            reset_and_flush()
+            block_reset()
             evb[i][0].record(stream)
             one_step()
             evb[i][1].record(stream)

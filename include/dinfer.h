@@ -191,16 +191,23 @@ dinfer_status dinfer_step_host(dinfer_ctx* ctx, const uint16_t* hidden_h,
  * CTA -> SM placement of a full-machine launch is the same every launch),
  * so the finishing spread of equal slabs is exposed at the end of the step.
  * dinfer_balance runs `iters` (+1 warm-up) steps with the given weights on
- * scratch state, measures each CTA's W-phase time, pairs the slowest SM with
- * the fastest in each vocab group and splits the group's rows so both finish
- * their W slabs together (20..80 % bounds); later steps use that partition
- * (results are the same up to fp32 summation order).  Synchronous; allocates
- * scratch temporarily.  UNSUPPORTED unless the ctx runs K12 with two hidden
- * slices and params.use_smooth.  dinfer_balance_reset restores the even
- * partition.                                                                */
+ * scratch state, measures each CTA's time, pairs the slowest SM with the
+ * fastest in each vocab group and splits the group's rows so both finish
+ * together (W rows plus the group's E slice per CTA; 20..80 % bounds); later
+ * steps use that partition (results are the same up to fp32 summation
+ * order).  `mode` is the state the steps will run in, which shifts the per-SM
+ * rates: DINFER_BALANCE_AFTER_FORWARD (0) -- each step follows an L2-dirtying
+ * model forward (the calibration steps run after a 2x-L2 write);
+ * DINFER_BALANCE_BACK_TO_BACK (1) -- steps follow each other directly (block
+ * reset + step, PDL chain intact).  Synchronous; allocates scratch
+ * temporarily.  UNSUPPORTED unless the ctx runs K12 with two hidden slices
+ * and params.use_smooth; ARG for another mode.  dinfer_balance_reset restores
+ * the even partition.                                                       */
+#define DINFER_BALANCE_AFTER_FORWARD 0
+#define DINFER_BALANCE_BACK_TO_BACK 1
 dinfer_status dinfer_balance(dinfer_ctx* ctx, const uint16_t* hidden, const uint16_t* W_vocab,
                              const uint16_t* E, const uint16_t* e_mask, const dinfer_params* params,
-                             int32_t iters);
+                             int32_t iters, int32_t mode);
 dinfer_status dinfer_balance_reset(dinfer_ctx* ctx);
 
 /* Peer-memory exchange of the per-rank records (world > 1),

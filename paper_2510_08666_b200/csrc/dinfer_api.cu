@@ -923,8 +923,9 @@ struct L2Dirty {
 extern "C" {
 
 dinfer_status dinfer_balance(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W, const uint16_t* E,
-                             const uint16_t* e_mask, const dinfer_params* p, int32_t iters) {
+                             const uint16_t* e_mask, const dinfer_params* p, int32_t iters, int32_t mode) {
   if (c == nullptr || p == nullptr || hidden == nullptr || W == nullptr || iters < 1) return DINFER_ERR_ARG;
+  if (mode != DINFER_BALANCE_AFTER_FORWARD && mode != DINFER_BALANCE_BACK_TO_BACK) return DINFER_ERR_ARG;
   if (!c->fused || c->k2_HS != 2 || !p->use_smooth) return DINFER_ERR_UNSUPPORTED;
   dinfer_status s = check_params(c, p);
   if (s != DINFER_OK) return s;
@@ -950,19 +951,33 @@ dinfer_status dinfer_balance(dinfer_ctx* c, const uint16_t* hidden, const uint16
   std::vector<int> role(G), split(VG);
   std::vector<double> dur(G, 0.0), tot(G, 0.0);
   // measure W-phase and whole-CTA durations per CTA under a given partition
+  // AFTER_FORWARD: each measured step follows an L2-dirtying write (a model
+  // forward between steps); BACK_TO_BACK: the measured step runs right behind
+  // another step (block reset + step, PDL chain intact)
+  const bool chain = mode == DINFER_BALANCE_BACK_TO_BACK;
   const L2Dirty dirty(c->dev);
   auto measure = [&](int n) -> dinfer_status {
     std::fill(dur.begin(), dur.end(), 0.0);
     std::fill(tot.begin(), tot.end(), 0.0);
-    c->record_wdur = true;
     for (int it = 0; it <= n; ++it) {
-      dirty.apply(c->stream);
-      DI_CUDA(cudaMemsetAsync(mask, 1, M, c->stream));
-      DI_CUDA(cudaMemsetAsync(cid, 0xff, 4 * M * K, c->stream));
-      DI_CUDA(cudaMemsetAsync(cval, 0, 4 * M * K, c->stream));
-      dinfer_status r = dinfer_step(c, hidden, W, E, e_mask, mask, tok, p->use_credit ? cid : nullptr,
-                                    p->use_credit ? cval : nullptr, p, com, sm, st);
-      if (r != DINFER_OK) return r;
+      const int reps = chain ? 2 : 1;
+      for (int r = 0; r < reps; ++r) {
+        c->record_wdur = r == reps - 1;
+        if (chain) {
+          DI_CUDA(launch_block_reset(mask, tok, cid, cval, c->M, c->shp.K, 0, c->stream, c->pdl));
+        } else {
+          dirty.apply(c->stream);
+          DI_CUDA(cudaMemsetAsync(mask, 1, M, c->stream));
+          DI_CUDA(cudaMemsetAsync(cid, 0xff, 4 * M * K, c->stream));
+          DI_CUDA(cudaMemsetAsync(cval, 0, 4 * M * K, c->stream));
+        }
+        dinfer_status rs = dinfer_step(c, hidden, W, E, e_mask, mask, tok, p->use_credit ? cid : nullptr,
+                                       p->use_credit ? cval : nullptr, p, com, sm, st);
+        if (rs != DINFER_OK) {
+          c->record_wdur = false;
+          return rs;
+        }
+      }
       std::vector<unsigned> w(2 * G);
       DI_CUDA(cudaMemcpyAsync(w.data(), c->d_wdur, 8 * G, cudaMemcpyDeviceToHost, c->stream));
       DI_CUDA(cudaStreamSynchronize(c->stream));

@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     sc0 = (q == 0) ? gc0 : sp;
     sc1 = (q == 0) ? sp : gc1;
   }
-  const unsigned long long t_start = (a.wdur != nullptr) ? globaltimer_ns() : 0ull;
+  unsigned long long t_start = 0ull;  // calibration stamps: from the dependency wait (thread 0)
   const int r0 = min(a.V_local, sc0 * KV), r1 = min(a.V_local, sc1 * KV);
   const int ntiles = (r1 - r0 + kTileRows - 1) / kTileRows;
   const int n_own = sc1 - sc0, n_all = nc;
@@ -485,6 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp < kEpiWarps) {
     // ------------------------------------------------------------ W phase: K1 epilogue
     grid_dep_wait();  // mask / credit ids of the previous step's commit visible
+    if (a.wdur != nullptr && threadIdx.x == 0) t_start = globaltimer_ns();
     if (a.mask_snap != nullptr && blockIdx.x == 0)
       for (int s = threadIdx.x; s < a.M; s += kEpiThreads) a.mask_snap[s] = a.mask[s];
     if (a.cids_snap != nullptr && blockIdx.x == 0)

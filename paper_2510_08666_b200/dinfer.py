@@ -107,7 +107,7 @@ def lib():
         "dinfer_get_geometry": (S, [P, POINTER(Geometry)]),
         "dinfer_get_trace": (S, [P, P, S]),
         "dinfer_generate": (S, [P, POINTER(GenConfig), POINTER(Params), P, P, P, P, c_int64, P, P]),
-        "dinfer_balance": (S, [P, P, P, P, P, POINTER(Params), S]),
+        "dinfer_balance": (S, [P, P, P, P, P, POINTER(Params), S, S]),
         "dinfer_balance_reset": (S, [P]),
         "dinfer_exchange_handle": (S, [P, P]),
         "dinfer_exchange_open": (S, [P, P]),
@@ -199,10 +199,14 @@ class Context:
                                  _ptr(credit_ids), _ptr(credit_val), ctypes.byref(params), _ptr(committed),
                                  _ptr(smoothed), _ptr(stats)), "dinfer_step")
 
-    def balance(self, hidden, W, E, e_mask, params: Params, iters: int = 4):
-        """Calibrate the K12 vocab partition to this GPU's per-SM rates (dinfer_balance)."""
+    BALANCE_MODES = {"after_forward": 0, "back_to_back": 1}
+
+    def balance(self, hidden, W, E, e_mask, params: Params, iters: int = 4, mode: str = "after_forward"):
+        """Calibrate the K12 vocab partition to this GPU's per-SM rates
+        (dinfer_balance) for steps that follow a model forward
+        ("after_forward") or each other directly ("back_to_back")."""
         _check(lib().dinfer_balance(self._h, _ptr(hidden), _ptr(W), _ptr(E), _ptr(e_mask), ctypes.byref(params),
-                                    int(iters)), "dinfer_balance")
+                                    int(iters), self.BALANCE_MODES[mode]), "dinfer_balance")
 
     def balance_reset(self):
         _check(lib().dinfer_balance_reset(self._h), "dinfer_balance_reset")

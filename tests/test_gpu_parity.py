@@ -195,10 +195,12 @@ def test_next_input_embedding_rejects_unsupported(torch_cuda):
     ctx.close()
 
 
-def test_balanced_partition_matches_oracle(torch_cuda):
+@pytest.mark.parametrize("mode", ["after_forward", "back_to_back"])
+def test_balanced_partition_matches_oracle(torch_cuda, mode):
     """dinfer_balance re-pairs CTAs and moves each group's split point to the
-    measured per-SM rates; the step's results must not change beyond fp32
-    summation order (decisions bit-exact), including with a skewed split."""
+    measured per-SM rates (either calibration mode); the step's results must
+    not change beyond fp32 summation order (decisions bit-exact), including
+    with a skewed split.  An unknown mode is rejected."""
     from paper_2510_08666_b200 import Context
     V, H, B, S, K = 32768, 2048, 1, 32, 32
     W, E = weights(V, H)
@@ -206,7 +208,13 @@ def test_balanced_partition_matches_oracle(torch_cuda):
     ctx = Context(B, S, H, K, V, smooth_capable=True)
     assert ctx.geometry()["fused"] == 1
     Wd, Ed, emd = to_dev_bf16(W), to_dev_bf16(E), to_dev_bf16(E[synth.mask_id(V)])
-    ctx.balance(to_dev_bf16(steps[0]["h"].reshape(B * S, H)), Wd, Ed, emd, gpu_params(steps[0]["params"]), iters=3)
+    h0, p0 = to_dev_bf16(steps[0]["h"].reshape(B * S, H)), gpu_params(steps[0]["params"])
+    import ctypes
+    from paper_2510_08666_b200.dinfer import lib
+    rc = lib().dinfer_balance(ctx._h, h0.data_ptr(), Wd.data_ptr(), Ed.data_ptr(), emd.data_ptr(), ctypes.byref(p0),
+                              3, 7)
+    assert rc != 0  # DINFER_ERR_ARG: no such mode
+    ctx.balance(h0, Wd, Ed, emd, p0, iters=3, mode=mode)
     replay(ctx, Wd, Ed, emd, steps, B, S, H, K, V)
     ctx.balance_reset()
     replay(ctx, Wd, Ed, emd, steps, B, S, H, K, V)

@@ -26,7 +26,7 @@ ctxs = [Context(B, S, H, K, V, stream=stream.cuda_stream) for _ in range(2)]
 p = make_params(decoder="hierarchical", use_credit=True, use_smooth=True, alpha_t=0.1)
 if "balance" in sys.argv:
     for c in ctxs:
-        c.balance(h, Wd, Ed, em, p, iters=4)
+        c.balance(h, Wd, Ed, em, p, iters=4, mode="back_to_back")
 mk = lambda: dict(mask=torch.ones((B, S), dtype=torch.uint8, device="cuda"),
                   tok=torch.full((B, S), V - 1, dtype=torch.int32, device="cuda"),
                   cids=torch.full((B, S, K), -1, dtype=torch.int32, device="cuda"),
@@ -36,7 +36,8 @@ mk = lambda: dict(mask=torch.ones((B, S), dtype=torch.uint8, device="cuda"),
                   st=torch.zeros((B, S, 4), dtype=torch.float32, device="cuda"))
 bufs = [mk(), mk()]
 torch.cuda.synchronize()
-for rep in range(3):
+hist = []
+for rep in range(int(os.environ.get('REPS', '3'))):
     for it in range(8):
         c, b = ctxs[it & 1], bufs[it & 1]
         c.block_reset(b["mask"], b["tok"], b["cids"], b["cval"], V - 1)
@@ -64,5 +65,23 @@ for rep in range(3):
     print(f"  step period (K12 start to K12 start): {period:.1f} us; "
           f"B K12 start after A K12 last exit: {(int(b1[:, 0].min()) - int(a2[:, 3].max())) / 1e3:.1f} us; "
           f"A K34 span {(int(a34[:, 3].max()) - int(a34[:, 0].min())) / 1e3:.1f} us")
+    hist.append(((a1[:, 2].astype(np.int64) - int(a1[:, 1].min())) / 1e3,
+                 (a1[:, 3].astype(np.int64) - int(a1[:, 1].min())) / 1e3))
+# systematic or noise?  per-CTA W-done / exit (from the first W MMA) across reps,
+# and (even partition: CTAs 2g, 2g+1 form vocab group g) within-pair differences
+wd = np.array([h[0] for h in hist])
+ex = np.array([h[1] for h in hist])
+if len(hist) > 1:
+    cw = np.corrcoef(wd[0], wd[-1])[0, 1]
+    ce = np.corrcoef(ex[0], ex[-1])[0, 1]
+    print(f"per-CTA correlation first vs last rep: W done {cw:.2f}, exit {ce:.2f}")
+mw, me = wd.mean(axis=0), ex.mean(axis=0)
+print(f"mean over reps: W done {mw.min():.1f}..{mw.max():.1f} (sd {mw.std():.1f}); exit {me.min():.1f}..{me.max():.1f} "
+      f"(sd {me.std():.1f}); single-rep exit sd {ex.std(axis=1).mean():.1f}")
+if "balance" not in sys.argv:
+    dpair = np.abs(wd[:, 0::2] - wd[:, 1::2])
+    epair = np.maximum(ex[:, 0::2], ex[:, 1::2])
+    print(f"within-pair |W done diff|: median {np.median(dpair):.1f} p90 {np.percentile(dpair, 90):.1f} us; "
+          f"pair exit (max of two) sd {epair.std(axis=1).mean():.1f}")
 for c in ctxs:
     c.close()
