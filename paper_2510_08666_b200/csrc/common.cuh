@@ -7,6 +7,8 @@
 #include <stdint.h>
 #include <cstdio>
 
+#include <cuda_fp16.h>
+
 #define DI __device__ __forceinline__
 
 namespace dinfer {
@@ -242,6 +244,22 @@ DI void stat_combine(float& m, int& idx, float& l, float m2, int idx2, float l2)
   l = first_ge ? fmaf(l2, e, l) : fmaf(l, e, l2);
   idx = (m > m2) ? idx : ((m2 > m) ? idx2 : min(idx, idx2));
   m = fmaxf(m, m2);
+}
+
+// The smoothing partials ([VG][M][H], written by K2 / K12, read by K34 and
+// the record finalize) are stored as fp16: each is relative to its vocab
+// group's max (softmax weights <= 1), so |value| <= group rows x max|E|, far
+// inside fp16's range for embedding tables; 11-bit significands put the
+// rounding (<= 2^-11 relative per element) well under the 2e-3 tolerance of
+// the smoothed output, and halve the partial traffic.
+DI uint2 pack_half4(float4 v) {
+  const __half2 a = __floats2half2_rn(v.x, v.y), b = __floats2half2_rn(v.z, v.w);
+  return make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+}
+DI float4 unpack_half4(uint2 u) {
+  const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+  const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+  return make_float4(a.x, a.y, b.x, b.y);
 }
 
 }  // namespace dinfer

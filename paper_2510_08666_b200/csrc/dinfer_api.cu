@@ -75,7 +75,7 @@ struct dinfer_ctx {
   float* rec_local = nullptr;
   float* rec_all = nullptr;
   float* flog = nullptr;
-  float* part2 = nullptr;
+  uint16_t* part2 = nullptr;  // fp16 smoothing partials [VG][M][H]
   float* ml = nullptr;
   float4* sel = nullptr;    // K34 phase-1 -> phase-2 exchange [M]
   int* row_cnt = nullptr;   // [B] K34 arrival counters
@@ -458,7 +458,7 @@ dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, in
     f.M = c->M;
     f.H = c->shp.H;
     if (acc_from_part2) {
-      f.acc = c->part2;
+      f.acc_h = c->part2;
       f.acc_stride = static_cast<long>(c->M) * c->shp.H;
       f.nparts = c->k2_VG;
       f.m_part = c->mref;  // partial g is relative to its vocab group's max m_g

@@ -750,9 +750,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int row = u >> 5, c4 = u & 31;
           const int s = g * 32 + row;
           if (s < a.M)
-            __stcg(reinterpret_cast<float4*>(b.part + (static_cast<long>(grp) * a.M + s) * a.H + hbase + sub * 128 +
-                                             c4 * 4),
-                   *reinterpret_cast<const float4*>(t + row * 128 + c4 * 4));
+            __stcg(reinterpret_cast<uint2*>(b.part + (static_cast<long>(grp) * a.M + s) * a.H + hbase + sub * 128 +
+                                            c4 * 4),
+                   pack_half4(*reinterpret_cast<const float4*>(t + row * 128 + c4 * 4)));
         }
       }
     }

@@ -299,8 +299,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int row = q >> 5, c4 = q & 31;
           const int s = g * 32 + row;
           if (s < a.M)
-            *reinterpret_cast<float4*>(a.part + (static_cast<long>(vg) * a.M + s) * a.H + hbase + sub * 128 + c4 * 4) =
-                *reinterpret_cast<const float4*>(tile + row * 128 + c4 * 4);
+            *reinterpret_cast<uint2*>(a.part + (static_cast<long>(vg) * a.M + s) * a.H + hbase + sub * 128 + c4 * 4) =
+                pack_half4(*reinterpret_cast<const float4*>(tile + row * 128 + c4 * 4));
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * kWarpThreads) : "memory");
       }
@@ -378,7 +378,8 @@ __global__ void rec_finalize_kernel(const RecArgs a) {
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int g = 0; g < a.VG; ++g) {
         const float sc = expf(a.mref[static_cast<long>(g) * a.M + s] - mr);
-        const float4 v = __ldcg(reinterpret_cast<const float4*>(a.part2 + (static_cast<long>(g) * a.M + s) * a.H + h));
+        const float4 v =
+            unpack_half4(__ldcg(reinterpret_cast<const uint2*>(a.part2 + (static_cast<long>(g) * a.M + s) * a.H + h)));
         acc.x = fmaf(v.x, sc, acc.x);
         acc.y = fmaf(v.y, sc, acc.y);
         acc.z = fmaf(v.z, sc, acc.z);

@@ -24,6 +24,7 @@
 //     for rows still undecided (App. A.1).
 #include <algorithm>
 #include <climits>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -174,6 +175,10 @@ constexpr int kSelPos = 8;
 // smoothing blocks: 128 float4 columns x 4 partial groups (512 consecutive elements; one
 // wave of <= 144 blocks at the MoE shape)
 constexpr int kSmCols = 128, kSmGroups = 4, kSmBatch = 8;
+#ifndef DINFER_SM_HB
+#define DINFER_SM_HB 8
+#endif
+constexpr int kSmBatchH = DINFER_SM_HB;  // fp16 partial loads in flight per thread
 DI int sel_ctas_per_row(int S) { return (S + kSelPos - 1) / kSelPos; }
 
 DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
@@ -457,13 +462,61 @@ DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
 }
 
 // Smoothing block: 512 threads = 128 float4 columns x 4 partial groups, i.e.
-// 512 consecutive elements of the [M, H] output.  Each thread loads a strided
-// subset of the nparts partials (issued before the statistics merge so both
-// latencies overlap), the 8 groups are combined in a fixed order through
+// 512 consecutive elements of the [M, H] output.  Each thread accumulates a
+// strided subset of the nparts partials (online rescale, overlapping the
+// statistics merge), the 4 groups are combined in a fixed order through
 // shared memory (deterministic).  The block merges the statistics (m, l) of
 // the rows it covers itself (one warp per row), so it does not wait for the
 // selection; rows undecided at step START are written (e_{t+1} matters for
 // those still undecided after the commit).
+// Partials p = grp, grp + kSmGroups, ... of element (s, h..h+3), kB loads in
+// flight per round, accumulated in that fixed order with an online rescale to
+// the running max: pacc = sum_p e^{m_p - mrun} acc_p.
+template <int kB, bool kHalf>
+DI void accumulate_parts(const K4Args& a, int s, int h, int grp, float4& pacc, float& mrun) {
+  const long base = static_cast<long>(s) * a.H + h;
+  // all kB loads are issued before any use (raw fp16 words are converted in
+  // the combine loop, so no conversion waits on a load between two issues)
+  using Raw = typename std::conditional<kHalf, uint2, float4>::type;
+  Raw raw[kB];
+  float mp[kB];
+  for (int p0 = grp; p0 < a.nparts; p0 += kB * kSmGroups) {
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const int p = p0 + j * kSmGroups;
+      const bool ok = p < a.nparts;
+      if constexpr (kHalf)
+        raw[j] = ok ? __ldcg(reinterpret_cast<const uint2*>(a.acc_h + base + p * a.acc_stride)) : make_uint2(0u, 0u);
+      else
+        raw[j] = ok ? __ldcg(reinterpret_cast<const float4*>(a.acc + base + p * a.acc_stride))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      mp[j] = ok ? a.m_part[p * a.m_stride + static_cast<long>(s) * a.m_rowstride] : neg_inf();
+    }
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {  // fixed summation order
+      if (mp[j] == neg_inf()) continue;  // past the last partial (or an empty one)
+      float4 vj;
+      if constexpr (kHalf)
+        vj = unpack_half4(raw[j]);
+      else
+        vj = raw[j];
+      if (mp[j] > mrun) {
+        const float r = __expf(mrun - mp[j]);
+        pacc.x *= r;
+        pacc.y *= r;
+        pacc.z *= r;
+        pacc.w *= r;
+        mrun = mp[j];
+      }
+      const float sc = __expf(mp[j] - mrun);
+      pacc.x = fmaf(vj.x, sc, pacc.x);
+      pacc.y = fmaf(vj.y, sc, pacc.y);
+      pacc.z = fmaf(vj.z, sc, pacc.z);
+      pacc.w = fmaf(vj.w, sc, pacc.w);
+    }
+  }
+}
+
 DI void smooth_block(const K3Args& a3, const K4Args& a, int blk, unsigned long long* tr) {
   __shared__ float s_m[8], s_w[8];
   __shared__ float s_cw[8][32];  // credit-fused smoothing: per-slot weights w_k and ids
@@ -480,17 +533,11 @@ DI void smooth_block(const K3Args& a3, const K4Args& a, int blk, unsigned long l
   const int s = in ? static_cast<int>(e / a.H) : s0;
   const int h = in ? static_cast<int>(e - static_cast<long>(s) * a.H) : 0;
   const bool active = in && a.mask_start[s] != 0;
-  const float* src = a.acc + static_cast<long>(s) * a.H + h;
-  // first batch of partials in flight before the statistics merge
-  float4 v[kSmBatch];
-  float mp[kSmBatch];
-#pragma unroll
-  for (int j = 0; j < kSmBatch; ++j) {
-    const int p = grp + j * kSmGroups;
-    const bool ok = active && p < a.nparts;
-    v[j] = ok ? __ldcg(reinterpret_cast<const float4*>(src + p * a.acc_stride)) : make_float4(0.f, 0.f, 0.f, 0.f);
-    mp[j] = ok ? a.m_part[p * a.m_stride + static_cast<long>(s) * a.m_rowstride] : 0.f;
-  }
+  // The row warps merge their row's statistics first (their loads go out ahead
+  // of the partial stream); every warp then streams its strided subset of the
+  // partials, 8 loads in flight, with an online rescale to the running max
+  // (pacc = sum_p e^{m_p - mrun} acc_p, fixed order), so the statistics are
+  // needed only for the final scale and both latencies overlap.
   if (warp <= s1 - s0) {
     float m, l;
     int vs;
@@ -521,30 +568,20 @@ DI void smooth_block(const K3Args& a3, const K4Args& a, int blk, unsigned long l
       s_w[warp] = a.alpha_t / (l + extra);
     }
   }
+  float4 pacc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float mrun = neg_inf();
+  if (active) {
+    if (a.acc_h != nullptr)  // fp16 partials
+      accumulate_parts<kSmBatchH, true>(a, s, h, grp, pacc, mrun);
+    else
+      accumulate_parts<kSmBatch, false>(a, s, h, grp, pacc, mrun);
+  }
   __syncthreads();
   if (tr != nullptr) tr[2] = globaltimer_ns();
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (active) {
-    const float m = s_m[s - s0];
-    for (int p0 = 0;; p0 += kSmBatch * kSmGroups) {
-#pragma unroll
-      for (int j = 0; j < kSmBatch; ++j) {  // fixed summation order
-        const int p = grp + p0 + j * kSmGroups;
-        const float sc = (p < a.nparts) ? __expf(mp[j] - m) : 0.f;
-        acc.x = fmaf(v[j].x, sc, acc.x);
-        acc.y = fmaf(v[j].y, sc, acc.y);
-        acc.z = fmaf(v[j].z, sc, acc.z);
-        acc.w = fmaf(v[j].w, sc, acc.w);
-      }
-      if (grp + p0 + kSmBatch * kSmGroups >= a.nparts) break;
-#pragma unroll
-      for (int j = 0; j < kSmBatch; ++j) {
-        const int p = grp + p0 + kSmBatch * kSmGroups + j * kSmGroups;
-        const bool ok = p < a.nparts;
-        v[j] = ok ? __ldcg(reinterpret_cast<const float4*>(src + p * a.acc_stride)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        mp[j] = ok ? a.m_part[p * a.m_stride + static_cast<long>(s) * a.m_rowstride] : 0.f;
-      }
-    }
+  if (active && mrun != neg_inf()) {
+    const float sc = __expf(mrun - s_m[s - s0]);
+    acc = make_float4(pacc.x * sc, pacc.y * sc, pacc.z * sc, pacc.w * sc);
   }
   red[grp][cl] = acc;
   __syncthreads();

@@ -94,7 +94,7 @@ struct K2Args {
   unsigned* grp_cnt;       // [VG] K1 slabs done per group
   unsigned* grp_pass;      // [VG] K2 CTAs past the wait (the last resets both)
   float* mref;             // [VG][M] out: per-group reference max m_g (acc is relative to it)
-  float* part;             // [VG][M][H]
+  uint16_t* part;          // [VG][M][H] fp16 (common.cuh: pack_half4)
   unsigned long long* trace;  // optional [grid][5]: globaltimer ns start, first E stage, MMAs done, exit; smid
   volatile int* probe;     // K12 diagnostics (env DINFER_K12_PROBE): [grid][8] progress words in mapped host memory
 };
@@ -117,7 +117,7 @@ cudaError_t launch_k12(const CUtensorMap& map_w, const CUtensorMap& map_w8, cons
 struct RecArgs {
   int M, H, grid1, VG, rec_stride;
   const float4* part1;
-  const float* part2;      // [VG][M][H] or nullptr
+  const uint16_t* part2;   // [VG][M][H] fp16 or nullptr
   const float* mref;       // [VG][M]
   float* rec;              // stats rows
   float* rec_acc;          // [M][H]
@@ -174,7 +174,8 @@ struct K3Args {
 // ---------------------------------------------------------------- K4
 struct K4Args {
   int M, H;
-  const float* acc;        // partial p at acc + p*acc_stride, [M][H] each
+  const float* acc;        // partial p at acc + p*acc_stride, [M][H] each (fp32 rank records)
+  const uint16_t* acc_h;   // or, when non-null, fp16 partials (single rank: K2 / K12 output) at acc_h + p*acc_stride
   long acc_stride;
   int nparts;
   const float* m_part;     // m of partial p, row s at m_part[p*m_stride + s*m_rowstride]; nullptr = scale 1
