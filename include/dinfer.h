@@ -130,7 +130,10 @@ dinfer_status dinfer_set_stream(dinfer_ctx* ctx, void* stream);
  *   tokens      [B,S] int32 in/out; written only at newly committed positions.
  *   credit_ids  [B,S,K] int32 in/out, -1 = empty slot; credit_val [B,S,K]
  *               float in/out.  Only rows undecided at step start change.
- *               May be NULL iff !use_credit.
+ *               May be NULL iff !use_credit.  Device-checked precondition
+ *               (sticky, DINFER_ERR_DEVICE from dinfer_sync): every used
+ *               slot of an undecided row has an id in [0, V_total) and a
+ *               value >= 0, and a new id finds a free slot.
  *   committed   [B,S] uint8 out, 1 = committed by this step.
  *   smoothed    [B,S,H] float out: e_{t+1} for every row undecided at
  *               step start; it is meaningful for the rows still undecided

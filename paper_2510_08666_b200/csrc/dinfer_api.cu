@@ -420,6 +420,7 @@ dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, in
   k.rowdone = c->rowdone;
   k.trace = c->trace == nullptr ? nullptr : c->trace + 5 * (c->k1_grid + c->k2_HS * c->k2_VG);
   k.B = c->shp.B;
+  k.V_total = static_cast<long>(c->shp.V_total);
   k.S = c->shp.S;
   k.K = c->shp.K;
   k.world = world;

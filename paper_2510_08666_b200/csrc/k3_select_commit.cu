@@ -208,6 +208,9 @@ DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
     const bool slot = fast && lane < a.K;
     int cid = slot ? a.credit_ids[cbase + lane] : -1;
     float cv = slot ? a.credit_val[cbase + lane] : 0.f;
+    // device-checked precondition (SPEC: a credit entry is never negative; ids
+    // index the vocabulary): sticky flag, surfaced by dinfer_sync
+    if (und && slot && cid >= 0 && (cid >= a.V_total || !(cv >= 0.f))) atomicOr(a.err, kErrCreditInvalid);
     float fc = 0.f;  // raw logit of the credited token (max over ranks: -inf where not owned)
     if (slot) {
       fc = a.recs[roff + kStatWords + lane];
@@ -250,7 +253,11 @@ DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
       for (int k0 = 0; k0 < a.K; k0 += 32) {
         const int k = k0 + lane;
         const int id = (k < a.K) ? a.credit_ids[cbase + k] : INT_MAX;
-        if (k < a.K && id >= 0) a.credit_val[cbase + k] = a.c_beta * a.credit_val[cbase + k];
+        if (k < a.K && id >= 0) {
+          const float cv0 = a.credit_val[cbase + k];
+          if (id >= a.V_total || !(cv0 >= 0.f)) atomicOr(a.err, kErrCreditInvalid);
+          a.credit_val[cbase + k] = a.c_beta * cv0;
+        }
         const unsigned hb = __ballot_sync(0xffffffffu, k < a.K && id == vstar);
         const unsigned eb = __ballot_sync(0xffffffffu, k < a.K && id < 0);
         if (hit < 0 && hb) hit = k0 + __ffs(hb) - 1;
@@ -597,7 +604,7 @@ DI void smooth_block(const K3Args& a3, const K4Args& a, int blk, unsigned long l
       const int rr = s - s0;
       for (int k = 0; k < a3.K; ++k) {
         const int id = s_cid[rr][k];
-        if (id < 0) continue;
+        if (id < 0 || id >= a3.V_total) continue;  // invalid ids are flagged by the selection
         const float wk = s_cw[rr][k];
         const uint2 ev = *reinterpret_cast<const uint2*>(a.E + static_cast<long>(id) * a.H + h);
         const __nv_bfloat162 e01 = *reinterpret_cast<const __nv_bfloat162*>(&ev.x);

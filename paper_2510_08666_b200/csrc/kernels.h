@@ -34,7 +34,7 @@ cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sm
 }
 
 // Device-side sticky error bits (dinfer_sync reads and clears them).
-enum : int { kErrCreditEntOverflow = 1, kErrCreditSlotsFull = 2 };
+enum : int { kErrCreditEntOverflow = 1, kErrCreditSlotsFull = 2, kErrCreditInvalid = 4 };
 
 // ---------------------------------------------------------------- K1
 struct K1Args {
@@ -136,6 +136,7 @@ cudaError_t launch_rec_finalize(const RecArgs& a, cudaStream_t st, bool pdl);
 // ---------------------------------------------------------------- K3
 struct K3Args {
   int B, S, K, world;
+  long V_total;            // credit ids outside [0, V_total) or negative credit values set kErrCreditInvalid
   const float4* part1;     // G = 1: K1 per-slab partials [M][grid1] (stats merged here), else nullptr
   int grid1;
   const float* recs;       // world records, `rec_words` apart (stats used when part1 == nullptr; fcred always)

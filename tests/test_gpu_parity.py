@@ -446,6 +446,37 @@ def test_credit_slot_overflow_is_reported(torch_cuda):
     ctx.sync()  # sticky flag cleared
 
 
+@pytest.mark.parametrize("K", [8, 40])
+@pytest.mark.parametrize("bad", ["negative", "out_of_range"])
+def test_invalid_credit_slot_is_reported(torch_cuda, K, bad):
+    """A negative credit value or an id outside the vocabulary in an
+    undecided row's slots is a device-checked precondition: DINFER_ERR_DEVICE
+    through dinfer_sync (K <= 32 register path and the strided K > 32 path)."""
+    from paper_2510_08666_b200 import Context, DInferError
+    V, H, B, S = 1024, 256, 1, 32
+    W, E = weights(V, H)
+    ctx = Context(B, S, H, K, V)
+    st = GpuState(B, S, H, K, V - 1)
+    p = gpu_params(O.Params(decoder=O.DEC_THRESHOLD, tau=0.9, use_credit=True))
+    h = to_dev_bf16(synth.planted_hidden(W, B * S, seed=13))
+    Wd = to_dev_bf16(W)
+    ctx.step(h, Wd, None, None, st.mask, st.tokens, st.cids, st.cval, p, st.committed, None, st.stats)
+    ctx.sync()  # valid state: no flag
+    st = GpuState(B, S, H, K, V - 1)
+    if bad == "negative":
+        st.cids[0, 3, 0] = 7
+        st.cval[0, 3, 0] = -0.25
+    else:
+        st.cids[0, 3, 0] = V + 5
+        st.cval[0, 3, 0] = 0.25
+    ctx.step(h, Wd, None, None, st.mask, st.tokens, st.cids, st.cval, p, st.committed, None, st.stats)
+    with pytest.raises(DInferError) as ei:
+        ctx.sync()
+    assert ei.value.status == 7
+    ctx.sync()
+    ctx.close()
+
+
 # ---------------------------------------------------------------- full paper shapes
 @pytest.mark.slow
 def test_moe_shape_hier_credit_smooth(torch_cuda):

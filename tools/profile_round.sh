@@ -3,15 +3,8 @@
 #   tools/profile_round.sh TAG
 TAG=${1:-r1}
 mkdir -p gpurun_out
-# 1) bench lines (default = headline, with cpu_baseline)
-timeout 900 python bench.py > gpurun_out/${TAG}_bench_moe.json 2> gpurun_out/${TAG}_bench_moe.err; echo "bench moe rc=$?"
-for c in 8b 8b-bs64 tiny; do
-  timeout 600 python bench.py --config $c --no-cpu-baseline > gpurun_out/${TAG}_bench_$c.json 2> gpurun_out/${TAG}_bench_$c.err
-  echo "bench $c rc=$?"
-done
-# 2) ncu launch list of the bench command itself (per-launch durations, cold, serialised)
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches_bench.csv \
-  python bench.py --steps 5 --warmup 3 > gpurun_out/${TAG}_launches_bench.out 2>&1; echo "ncu launches rc=$?"
+# 1-2) bench lines for every config (+ even / two-kernel variants) and the ncu launch list
+bash tools/profile_bench.sh ${TAG}
 # 3) one --set full capture per kernel (steady-state launches of the step loop)
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k12_proj|k34_select" \
   --launch-skip 4 -c 2 -f -o gpurun_out/${TAG}_full_moe python tools/step_loop.py --steps 4 > gpurun_out/${TAG}_full_moe.out 2>&1
