@@ -180,7 +180,11 @@ dinfer_status dinfer_step_embed(dinfer_ctx* ctx, const uint16_t* hidden, const u
  * host memory) run the same sequence un-captured. hidden_h and smoothed_h
  * may be pageable; pinned buffers avoid a staging copy inside the driver,
  * and a pinned smoothed_h is written by the kernel directly (zero-copy; no
- * D2H copy for the M*H*4-byte output). */
+ * D2H copy for the M*H*4-byte output).  With a pinned hidden_h the two
+ * host->device transfers become one staging kernel reading the mapped host
+ * memory, chained ahead of the step by programmatic dependent launch (the
+ * W stream starts under the PCIe reads), and the state goes back through a
+ * second staging kernel writing the mapped pinned block. */
 dinfer_status dinfer_step_host(dinfer_ctx* ctx, const uint16_t* hidden_h,
                                const uint16_t* W_vocab, const uint16_t* E,
                                const uint16_t* e_mask, uint8_t* mask_h, int32_t* tokens_h,

@@ -65,6 +65,7 @@ struct dinfer_ctx {
   int* d_split = nullptr;
   unsigned* d_wdur = nullptr;
   bool balanced = false;
+  bool stage_kernels = true;  // dinfer_step_host: zero-copy staging kernels (env DINFER_STAGE_KERNELS=0: copies)
   bool record_wdur = false;
   int f_stages = 0, f_pstages = 0;
   size_t f_smem = 0;
@@ -101,6 +102,9 @@ struct dinfer_ctx {
   cudaStream_t cap_stream = nullptr;  // private capture stream
   const float* zc_host = nullptr;     // smoothed_h whose device mapping zc_dev was looked up
   float* zc_dev = nullptr;
+  const uint16_t* zh_host = nullptr;  // hidden_h whose device mapping zh_dev was looked up
+  const uint16_t* zh_dev = nullptr;
+  uint8_t* st_host_dev = nullptr;     // device mapping of st_host (mapped pinned allocation)
   struct Pending {  // dinfer_step_host_async -> dinfer_step_host_wait
     bool active;
     uint8_t* mask_h;
@@ -765,6 +769,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
     if (const char* e = std::getenv("DINFER_PDL")) c->pdl = std::atoi(e) != 0;
   }
   if (const char* e = std::getenv("DINFER_HOST_GRAPH")) c->host_graph_ok = std::atoi(e) != 0;
+  if (const char* e = std::getenv("DINFER_STAGE_KERNELS")) c->stage_kernels = std::atoi(e) != 0;
 
   // ---- workspace
   c->stats_words = static_cast<size_t>(M) * (kStatWords + s.K);
@@ -1269,9 +1274,12 @@ dinfer_status dinfer_step_host_async(dinfer_ctx* c, const uint16_t* hidden_h, co
     A(dev_alloc(&c->st_hidden, M * H));
     A(dev_alloc(&c->st_block, total));
     if (c->shp.smooth_capable) A(dev_alloc(&c->st_smoothed, M * H));
-    if (st == DINFER_OK && cudaMallocHost(reinterpret_cast<void**>(&c->st_host), total) != cudaSuccess)
+    if (st == DINFER_OK && cudaHostAlloc(reinterpret_cast<void**>(&c->st_host), total, cudaHostAllocMapped) != cudaSuccess)
       st = DINFER_ERR_NOMEM;
     if (st != DINFER_OK) return st;
+    void* dp = nullptr;
+    if (cudaHostGetDevicePointer(&dp, c->st_host, 0) == cudaSuccess) c->st_host_dev = static_cast<uint8_t*>(dp);
+    cudaGetLastError();
   }
   dinfer_status s = check_params(c, p);
   if (s != DINFER_OK) return s;
@@ -1307,6 +1315,31 @@ dinfer_status dinfer_step_host_async(dinfer_ctx* c, const uint16_t* hidden_h, co
       smoothed_zero_copy = true;
     }
   }
+  // hidden_h pinned (and mapped): the inputs are staged by a kernel in the PDL
+  // chain (the W stream of K12 / K1 starts under the PCIe reads), and the small
+  // state goes back the same way (stage.cu); otherwise copy-engine transfers
+  if (hidden_h != c->zh_host) {
+    c->zh_host = hidden_h;
+    c->zh_dev = nullptr;
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, hidden_h) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer != nullptr && (reinterpret_cast<uintptr_t>(pa.devicePointer) % 16) == 0)
+      c->zh_dev = static_cast<const uint16_t*>(pa.devicePointer);
+    cudaGetLastError();
+  }
+  const bool kstage = c->zh_dev != nullptr && c->st_host_dev != nullptr && c->stage_kernels;
+  const size_t in_bytes = al(p->use_credit ? o_com : o_cid);
+  auto stage_in = [&](cudaStream_t q) -> cudaError_t {
+    if (kstage)
+      return launch_stage_copy(c->zh_dev, c->st_hidden, M * H * 2, c->st_host_dev, d, in_bytes, true, q, c->pdl);
+    cudaError_t e = cudaMemcpyAsync(c->st_hidden, hidden_h, M * H * 2, cudaMemcpyHostToDevice, q);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d, hs, in_bytes, cudaMemcpyHostToDevice, q);
+    return e;
+  };
+  auto stage_out = [&](cudaStream_t q) -> cudaError_t {
+    if (kstage) return launch_stage_copy(d, c->st_host_dev, al(total), nullptr, nullptr, 0, false, q, c->pdl);
+    return cudaMemcpyAsync(hs, d, total, cudaMemcpyDeviceToHost, q);
+  };
   // graph key: everything baked into the captured sequence (pointers + structural flags)
   const uint64_t key[12] = {reinterpret_cast<uint64_t>(hidden_h), reinterpret_cast<uint64_t>(W),
                             reinterpret_cast<uint64_t>(E),        reinterpret_cast<uint64_t>(e_mask),
@@ -1314,7 +1347,7 @@ dinfer_status dinfer_step_host_async(dinfer_ctx* c, const uint16_t* hidden_h, co
                             static_cast<uint64_t>(p->hier_runs_after_hi), static_cast<uint64_t>(p->use_credit),
                             static_cast<uint64_t>(p->use_smooth), static_cast<uint64_t>(c->timing),
                             static_cast<uint64_t>(stats_h != nullptr),
-                            static_cast<uint64_t>(p->smooth_credit_fused) + 1};
+                            static_cast<uint64_t>(p->smooth_credit_fused) + 1 + 2 * static_cast<uint64_t>(kstage)};
   // timing events / NCCL: plain enqueue; a key whose capture failed (e.g. pageable
   // host buffers) also stays on the plain path
   const bool same_key = std::memcmp(key, c->host_graph_key, sizeof(key)) == 0;
@@ -1333,8 +1366,7 @@ dinfer_status dinfer_step_host_async(dinfer_ctx* c, const uint16_t* hidden_h, co
     DI_CUDA(cudaStreamBeginCapture(sm, cudaStreamCaptureModeRelaxed));
     c->stream = sm;
     c->pdev_active = reinterpret_cast<const float*>(d + o_par);
-    bool ok = cudaMemcpyAsync(c->st_hidden, hidden_h, M * H * 2, cudaMemcpyHostToDevice, sm) == cudaSuccess &&
-              cudaMemcpyAsync(d, hs, o_com, cudaMemcpyHostToDevice, sm) == cudaSuccess;
+    bool ok = stage_in(sm) == cudaSuccess;
     dinfer_status st = DINFER_OK;
     if (ok)
       st = dinfer_step(c, c->st_hidden, W, E, e_mask, d + o_mask, reinterpret_cast<int32_t*>(d + o_tok),
@@ -1342,7 +1374,7 @@ dinfer_status dinfer_step_host_async(dinfer_ctx* c, const uint16_t* hidden_h, co
                        p->use_credit ? reinterpret_cast<float*>(d + o_cval) : nullptr, p, d + o_com,
                        p->use_smooth ? smoothed_dev : nullptr, reinterpret_cast<float*>(d + o_stats));
     c->pdev_active = nullptr;
-    ok = ok && st == DINFER_OK && cudaMemcpyAsync(hs, d, total, cudaMemcpyDeviceToHost, sm) == cudaSuccess;
+    ok = ok && st == DINFER_OK && stage_out(sm) == cudaSuccess;
     if (ok && p->use_smooth && !smoothed_zero_copy)
       ok = cudaMemcpyAsync(smoothed_h, c->st_smoothed, M * H * 4, cudaMemcpyDeviceToHost, sm) == cudaSuccess;
     const cudaError_t ee = cudaStreamEndCapture(sm, &g);
@@ -1365,14 +1397,13 @@ dinfer_status dinfer_step_host_async(dinfer_ctx* c, const uint16_t* hidden_h, co
   if (use_graph) {
     DI_CUDA(cudaGraphLaunch(c->host_graph, sm));
   } else {
-    DI_CUDA(cudaMemcpyAsync(c->st_hidden, hidden_h, M * H * 2, cudaMemcpyHostToDevice, sm));
-    DI_CUDA(cudaMemcpyAsync(d, hs, p->use_credit ? o_com : o_cid, cudaMemcpyHostToDevice, sm));
+    DI_CUDA(stage_in(sm));
     s = dinfer_step(c, c->st_hidden, W, E, e_mask, d + o_mask, reinterpret_cast<int32_t*>(d + o_tok),
                     p->use_credit ? reinterpret_cast<int32_t*>(d + o_cid) : nullptr,
                     p->use_credit ? reinterpret_cast<float*>(d + o_cval) : nullptr, p, d + o_com,
                     p->use_smooth ? smoothed_dev : nullptr, reinterpret_cast<float*>(d + o_stats));
     if (s != DINFER_OK) return s;
-    DI_CUDA(cudaMemcpyAsync(hs, d, total, cudaMemcpyDeviceToHost, sm));
+    DI_CUDA(stage_out(sm));
     if (p->use_smooth && !smoothed_zero_copy)
       DI_CUDA(cudaMemcpyAsync(smoothed_h, c->st_smoothed, M * H * 4, cudaMemcpyDeviceToHost, sm));
   }

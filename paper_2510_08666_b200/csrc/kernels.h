@@ -219,6 +219,10 @@ struct GenArgs {
   uint16_t* hbuf;               // [M][H] the step's hidden input
 };
 cudaError_t launch_gen_init(const GenArgs& a, cudaGraphConditionalHandle h, cudaStream_t st);
+// host-buffer staging (stage.cu): zero-copy kernel copies of two 16-B aligned
+// segments; `in`: trigger dependents at entry (host -> device inputs)
+cudaError_t launch_stage_copy(const void* src0, void* dst0, size_t bytes0, const void* src1, void* dst1,
+                              size_t bytes1, bool in, cudaStream_t st, bool pdl);
 cudaError_t launch_block_reset(uint8_t* mask, int32_t* tokens, int32_t* cids, float* cval, int M, int K, int mask_id,
                                cudaStream_t st, bool pdl);
 cudaError_t launch_gen_control(const GenArgs& a, cudaGraphConditionalHandle h, cudaStream_t st);
