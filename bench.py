@@ -304,7 +304,7 @@ def gpu_arm(args):
 
     # calibrated vocab partition (K12): measured per-SM streaming rates -> slab split
     partition = "even"
-    if not args.no_balance and smooth:
+    if not args.no_balance:  # K12 pairs + splits (smoothing) or K1 slab sizes (stats only); dense: none
         from paper_2510_08666_b200 import DInferError
         try:
             ctx.balance(hid, Wd, Ed, emd, p, iters=4, mode="back_to_back")

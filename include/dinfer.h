@@ -207,9 +207,12 @@ dinfer_status dinfer_step_host(dinfer_ctx* ctx, const uint16_t* hidden_h,
  * model forward (the calibration steps run after a 2x-L2 write);
  * DINFER_BALANCE_BACK_TO_BACK (1) -- steps follow each other directly (block
  * reset + step, PDL chain intact).  Synchronous; allocates scratch
- * temporarily.  UNSUPPORTED unless the ctx runs K12 with two hidden slices
- * and params.use_smooth; ARG for another mode.  dinfer_balance_reset restores
- * the even partition.                                                       */
+ * temporarily.  On a stats-only context (smooth_capable = 0, params
+ * without smoothing) it calibrates K1's slab sizes instead: rows per CTA
+ * proportional to the measured per-SM rates (damped, 8-row units, at most
+ * 1.3x the even slab).  UNSUPPORTED otherwise (two-kernel smoothing path,
+ * M > 256); ARG for another mode.  dinfer_balance_reset restores the even
+ * partition.                                                                */
 #define DINFER_BALANCE_AFTER_FORWARD 0
 #define DINFER_BALANCE_BACK_TO_BACK 1
 dinfer_status dinfer_balance(dinfer_ctx* ctx, const uint16_t* hidden, const uint16_t* W_vocab,

@@ -65,6 +65,8 @@ struct dinfer_ctx {
   int* d_split = nullptr;
   unsigned* d_wdur = nullptr;
   bool balanced = false;
+  int* d_slab = nullptr;      // K1 calibrated slab boundaries [k1_grid + 1] (stats-only contexts)
+  bool k1_balanced = false;
   bool stage_kernels = true;  // dinfer_step_host: zero-copy staging kernels (env DINFER_STAGE_KERNELS=0: copies)
   bool record_wdur = false;
   int f_stages = 0, f_pstages = 0;
@@ -302,6 +304,8 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
   }
   a.err = c->err;
   a.trace = c->trace;
+  if (c->record_wdur) a.wdur = c->d_wdur;
+  if (c->k1_balanced && !(smooth && c->fused)) a.slab_start = c->d_slab;
   if (smooth && c->fused) {
     // K12: the vocab slab partition at 16-row chunk granularity (nchunks /
     // chunk_rows), the E phase over the slab's vocab group
@@ -312,7 +316,6 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
       a.role_of = c->d_role;
       a.split = c->d_split;
     }
-    if (c->record_wdur) a.wdur = c->d_wdur;
     K2Args b{};
     b.M = c->M;
     b.N = c->N;
@@ -567,7 +570,7 @@ void dinfer_destroy(dinfer_ctx* c) {
   void* bufs[] = {c->part1, c->counter, c->err, c->rec_local, c->flog, c->part2, c->ml, c->sel, c->row_cnt, c->trace,
                   c->mref,
                   c->mask_snap, c->rowdone, c->cids_snap, c->cval_snap, c->xbuf, c->xctl, c->d_peers,
-                  c->d_role, c->d_split, c->d_wdur,
+                  c->d_role, c->d_split, c->d_wdur, c->d_slab,
                   c->grp_cnt, c->grp_pass,
                   c->st_hidden, c->st_block, c->st_smoothed,
                   c->g_mask, c->g_tok, c->g_cids, c->g_cval, c->g_com, c->g_sm, c->g_pdev, c->g_st, c->g_hbuf};
@@ -740,6 +743,9 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
         c->slab_rows_max = std::max<int>(c->slab_rows_max, static_cast<int>(rows));
       }
     }
+    // stats-only contexts: room for calibrated slabs up to 1.3x the even size
+    if (!c->fused && c->k1_VG == 1)
+      c->slab_rows_max = kRowGran * ((c->slab_rows_max * 13 / 10 + kRowGran - 1) / kRowGran);
     // Hidden block resident in smem (loaded once) or streamed from L2 with every
     // W stage.  Residency only pays if it still leaves >= 4 W stages: at MoE
     // shape it leaves 2 (measured 144 us) against 5 streamed stages (134 us).
@@ -788,6 +794,10 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
   if (s.smooth_capable) {
     A(dev_alloc(&c->cids_snap, static_cast<size_t>(M) * s.K));
     A(dev_alloc(&c->cval_snap, static_cast<size_t>(M) * s.K));
+  }
+  if (!c->fused && !c->dense && c->k1_VG == 1) {
+    A(dev_alloc(&c->d_slab, static_cast<size_t>(c->k1_grid) + 1));
+    A(dev_alloc(&c->d_wdur, 2 * static_cast<size_t>(c->k1_grid)));
   }
   if (c->fused) {
     A(dev_alloc(&c->d_role, static_cast<size_t>(c->k1_grid)));
@@ -924,6 +934,129 @@ struct L2Dirty {
   ~L2Dirty() { cudaFree(buf); }
 };
 
+// K1 slab calibration (stats-only contexts, one vocab group of k1_grid slabs):
+// per-CTA rates rows / (dependency wait -> last epilogue) under the current
+// slabs, then slab sizes moved a damped step toward rate-proportional ones
+// (8-row units, sum preserved by largest remainders, within [8, slab_rows_max]).
+dinfer_status balance_k1(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W, const dinfer_params* p,
+                         int32_t iters, int32_t mode) {
+  const int G = c->k1_grid;
+  const size_t M = static_cast<size_t>(c->M), K = static_cast<size_t>(c->shp.K);
+  const long n8 = static_cast<long>(c->shp.V_local) / kRowGran;
+  const long cap8 = std::max<long>(1, c->slab_rows_max / kRowGran);
+  uint8_t *mask = nullptr, *com = nullptr;
+  int32_t *tok = nullptr, *cid = nullptr;
+  float *cval = nullptr, *st = nullptr;
+  dinfer_status s = DINFER_OK;
+  auto A = [&](dinfer_status x) { if (s == DINFER_OK) s = x; };
+  A(dev_alloc(&mask, M));
+  A(dev_alloc(&com, M));
+  A(dev_alloc(&tok, M));
+  A(dev_alloc(&cid, M * K));
+  A(dev_alloc(&cval, M * K));
+  A(dev_alloc(&st, M * 4));
+  std::vector<long> units(G);  // slab sizes in 8-row units
+  for (int b = 0; b < G; ++b) units[b] = (b + 1) * n8 / G - b * n8 / G;
+  std::vector<double> dur(G, 0.0);
+  const bool chain = mode == DINFER_BALANCE_BACK_TO_BACK;
+  const L2Dirty dirty(c->dev);
+  auto upload = [&]() -> dinfer_status {
+    std::vector<int> start(G + 1, 0);
+    for (int b = 0; b < G; ++b) start[b + 1] = start[b] + static_cast<int>(units[b] * kRowGran);
+    DI_CUDA(cudaMemcpy(c->d_slab, start.data(), 4 * (G + 1), cudaMemcpyHostToDevice));
+    return DINFER_OK;
+  };
+  auto measure = [&](int n) -> dinfer_status {
+    std::fill(dur.begin(), dur.end(), 0.0);
+    for (int it = 0; it <= n; ++it) {
+      const int reps = chain ? 2 : 1;
+      for (int r = 0; r < reps; ++r) {
+        c->record_wdur = r == reps - 1;
+        if (chain) {
+          DI_CUDA(launch_block_reset(mask, tok, cid, cval, c->M, c->shp.K, 0, c->stream, c->pdl));
+        } else {
+          dirty.apply(c->stream);
+          DI_CUDA(cudaMemsetAsync(mask, 1, M, c->stream));
+          DI_CUDA(cudaMemsetAsync(cid, 0xff, 4 * M * K, c->stream));
+          DI_CUDA(cudaMemsetAsync(cval, 0, 4 * M * K, c->stream));
+        }
+        const dinfer_status rs = dinfer_step(c, hidden, W, nullptr, nullptr, mask, tok, p->use_credit ? cid : nullptr,
+                                             p->use_credit ? cval : nullptr, p, com, nullptr, st);
+        if (rs != DINFER_OK) {
+          c->record_wdur = false;
+          return rs;
+        }
+      }
+      std::vector<unsigned> w(G);
+      DI_CUDA(cudaMemcpyAsync(w.data(), c->d_wdur, 4 * G, cudaMemcpyDeviceToHost, c->stream));
+      DI_CUDA(cudaStreamSynchronize(c->stream));
+      if (it > 0)
+        for (int b = 0; b < G; ++b) dur[b] += w[b];
+    }
+    c->record_wdur = false;
+    return DINFER_OK;
+  };
+  double damp = 0.5;
+  if (const char* e = std::getenv("DINFER_BALANCE_DAMP")) damp = std::atof(e);
+  int rounds = 1;
+  if (const char* e = std::getenv("DINFER_BALANCE_ROUNDS")) rounds = std::max(1, std::atoi(e));
+  if (s == DINFER_OK) s = upload();
+  c->k1_balanced = true;
+  for (int r = 0; r < rounds && s == DINFER_OK; ++r) {
+    s = measure(iters);
+    if (s != DINFER_OK) break;
+    std::vector<double> rate(G);
+    double rsum = 0.0;
+    for (int b = 0; b < G; ++b) {
+      rate[b] = units[b] / std::max(1.0, dur[b] / iters);
+      rsum += rate[b];
+    }
+    std::vector<double> want(G);
+    for (int b = 0; b < G; ++b) {
+      const double target = n8 * rate[b] / rsum;
+      want[b] = std::min<double>(cap8, std::max<double>(1.0, units[b] + damp * (target - units[b])));
+    }
+    // integer sizes with the same total (largest remainders)
+    long tot = 0;
+    std::vector<std::pair<double, int>> rem(G);
+    for (int b = 0; b < G; ++b) {
+      units[b] = static_cast<long>(std::floor(want[b]));
+      tot += units[b];
+      rem[b] = {want[b] - units[b], b};
+    }
+    std::sort(rem.begin(), rem.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    for (int k = 0; tot < n8; k = (k + 1) % G)
+      if (units[rem[k].second] < cap8) {
+        ++units[rem[k].second];
+        ++tot;
+      }
+    for (int k = G - 1; tot > n8; k = (k + G - 1) % G)
+      if (units[rem[k].second] > 1) {
+        --units[rem[k].second];
+        --tot;
+      }
+    s = upload();
+    if (std::getenv("DINFER_BALANCE_VERBOSE") != nullptr) {
+      double dmin = 1e30, dmax = 0;
+      for (int b = 0; b < G; ++b) {
+        dmin = std::min(dmin, dur[b] / iters);
+        dmax = std::max(dmax, dur[b] / iters);
+      }
+      long umin = n8, umax = 0;
+      for (int b = 0; b < G; ++b) {
+        umin = std::min(umin, units[b]);
+        umax = std::max(umax, units[b]);
+      }
+      std::fprintf(stderr, "[dinfer_balance K1] round %d: ns/CTA %.0f..%.0f -> slabs %ld..%ld rows\n", r, dmin, dmax,
+                   umin * kRowGran, umax * kRowGran);
+    }
+  }
+  cudaStreamSynchronize(c->stream);
+  cudaFree(mask); cudaFree(com); cudaFree(tok); cudaFree(cid); cudaFree(cval); cudaFree(st);
+  if (s != DINFER_OK) c->k1_balanced = false;
+  return s;
+}
+
 }  // namespace
 
 extern "C" {
@@ -932,6 +1065,7 @@ dinfer_status dinfer_balance(dinfer_ctx* c, const uint16_t* hidden, const uint16
                              const uint16_t* e_mask, const dinfer_params* p, int32_t iters, int32_t mode) {
   if (c == nullptr || p == nullptr || hidden == nullptr || W == nullptr || iters < 1) return DINFER_ERR_ARG;
   if (mode != DINFER_BALANCE_AFTER_FORWARD && mode != DINFER_BALANCE_BACK_TO_BACK) return DINFER_ERR_ARG;
+  if (!c->fused && c->d_slab != nullptr && !p->use_smooth) return balance_k1(c, hidden, W, p, iters, mode);
   if (!c->fused || c->k2_HS != 2 || !p->use_smooth) return DINFER_ERR_UNSUPPORTED;
   dinfer_status s = check_params(c, p);
   if (s != DINFER_OK) return s;
@@ -1126,6 +1260,7 @@ dinfer_status dinfer_debug_role_shift(dinfer_ctx* c, int32_t shift) {
 dinfer_status dinfer_balance_reset(dinfer_ctx* c) {
   if (c == nullptr) return DINFER_ERR_ARG;
   c->balanced = false;
+  c->k1_balanced = false;
   return DINFER_OK;
 }
 

@@ -128,8 +128,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int rg0 = a.chunk_rows * static_cast<int>(static_cast<long>(grp) * a.nchunks / a.VG);
   const int rg1 = min(a.V_local, a.chunk_rows * static_cast<int>(static_cast<long>(grp + 1) * a.nchunks / a.VG));
   const int n8 = (rg1 - rg0) / kRowGran;
-  const int r0 = rg0 + kRowGran * static_cast<int>(static_cast<long>(q) * n8 / a.SPG);
-  const int r1 = rg0 + kRowGran * static_cast<int>(static_cast<long>(q + 1) * n8 / a.SPG);
+  int r0 = rg0 + kRowGran * static_cast<int>(static_cast<long>(q) * n8 / a.SPG);
+  int r1 = rg0 + kRowGran * static_cast<int>(static_cast<long>(q + 1) * n8 / a.SPG);
+  if (a.slab_start != nullptr) {  // calibrated slabs (dinfer_balance, stats-only contexts)
+    r0 = a.slab_start[blockIdx.x];
+    r1 = min(a.V_local, a.slab_start[blockIdx.x + 1]);
+  }
+  unsigned long long t_start = 0ull;  // calibration stamp: from the dependency wait (thread 0)
   const int ntiles = (r1 - r0 + kTileRows - 1) / kTileRows;
   const uint32_t tmem_cols = tmem_cols_pow2(2u * N);
 
@@ -244,6 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // raw logits are captured for the credit fuse.  Rows decided at step start
     // are frozen (reading c7) and skipped.  Runs while the first W chunks fly.
     grid_dep_wait();  // mask / credit ids of the previous step's commit visible
+    if (a.wdur != nullptr && threadIdx.x == 0) t_start = globaltimer_ns();
     if (a.mask_snap != nullptr && blockIdx.x == 0)
       for (int s = threadIdx.x; s < a.M; s += kEpiWarps * kWarpThreads) a.mask_snap[s] = a.mask[s];
     if (a.cids_snap != nullptr && blockIdx.x == 0)
@@ -336,6 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&tempty[buf]);
     }
     if (a.trace != nullptr && threadIdx.x == 0) a.trace[blockIdx.x * 5 + 2] = globaltimer_ns();
+    if (a.wdur != nullptr && threadIdx.x == 0) a.wdur[blockIdx.x] = static_cast<unsigned>(globaltimer_ns() - t_start);
     // cross-warp merge (fixed warp order)
 #pragma unroll
     for (int g = 0; g < kMaxGroups; ++g) {

@@ -221,6 +221,25 @@ def test_balanced_partition_matches_oracle(torch_cuda, mode):
     ctx.close()
 
 
+@pytest.mark.parametrize("mode", ["after_forward", "back_to_back"])
+def test_calibrated_k1_slabs_match_oracle(torch_cuda, mode):
+    """Stats-only contexts: dinfer_balance resizes K1's slabs to the measured
+    per-SM rates; decisions stay bit-exact, statistics within tolerance
+    (summation order only), and balance_reset restores the even slabs."""
+    from paper_2510_08666_b200 import Context
+    V, H, B, S, K = 32768, 2048, 1, 32, 32
+    W, E = weights(V, H)
+    _, _, _, steps = vetted_trajectory(W, E, B, S, 21, thr_params(0.9), max_iters=4)
+    ctx = Context(B, S, H, K, V, smooth_capable=False)
+    Wd = to_dev_bf16(W)
+    ctx.balance(to_dev_bf16(steps[0]["h"].reshape(B * S, H)), Wd, None, None, gpu_params(steps[0]["params"]),
+                iters=3, mode=mode)
+    replay(ctx, Wd, None, None, steps, B, S, H, K, V)
+    ctx.balance_reset()
+    replay(ctx, Wd, None, None, steps, B, S, H, K, V)
+    ctx.close()
+
+
 def test_without_pdl(torch_cuda, monkeypatch):
     monkeypatch.setenv("DINFER_PDL", "0")
     run_trajectory(torch_cuda, 2048, 512, 2, 32, 32, 9, hier_credit_smooth, True, max_iters=4)
