@@ -66,6 +66,9 @@ struct dinfer_ctx {
   unsigned* d_wdur = nullptr;
   bool balanced = false;
   int* d_slab = nullptr;      // K1 calibrated slab boundaries [k1_grid + 1] (stats-only contexts)
+  int* d_gstart = nullptr;    // K12 calibrated vocab-group boundaries [VG + 1] (chunks)
+  bool groups_balanced = false;
+  int grp_cap_chunks = 0;     // largest group the K12 head table admits
   bool k1_balanced = false;
   bool stage_kernels = true;  // dinfer_step_host: zero-copy staging kernels (env DINFER_STAGE_KERNELS=0: copies)
   bool record_wdur = false;
@@ -315,6 +318,7 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
     if (c->balanced) {
       a.role_of = c->d_role;
       a.split = c->d_split;
+      if (c->groups_balanced) a.grp_start = c->d_gstart;
     }
     K2Args b{};
     b.M = c->M;
@@ -570,7 +574,7 @@ void dinfer_destroy(dinfer_ctx* c) {
   void* bufs[] = {c->part1, c->counter, c->err, c->rec_local, c->flog, c->part2, c->ml, c->sel, c->row_cnt, c->trace,
                   c->mref,
                   c->mask_snap, c->rowdone, c->cids_snap, c->cval_snap, c->xbuf, c->xctl, c->d_peers,
-                  c->d_role, c->d_split, c->d_wdur, c->d_slab,
+                  c->d_role, c->d_split, c->d_wdur, c->d_slab, c->d_gstart,
                   c->grp_cnt, c->grp_pass,
                   c->st_hidden, c->st_block, c->st_smoothed,
                   c->g_mask, c->g_tok, c->g_cids, c->g_cval, c->g_com, c->g_sm, c->g_pdev, c->g_st, c->g_hbuf};
@@ -673,13 +677,24 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
         int st_max = 6, pst_max = 4;  // tuning overrides (measurement only)
         if (const char* e = std::getenv("DINFER_K12_STAGES")) st_max = std::max(3, std::atoi(e));
         if (const char* e = std::getenv("DINFER_K12_PSTAGES")) pst_max = std::max(2, std::atoi(e));
-        for (int st = st_max; st >= 3 && c->f_stages == 0; --st)
-          for (int pst = pst_max; pst >= 2; --pst)
-            if (k12_smem_bytes(c->N, hw, st, pst, srm) <= c->smem_optin) {
-              c->f_stages = st;
-              c->f_pstages = pst;
-              break;
-            }
+        auto fit = [&](int rows, int* fst, int* fpst) {
+          *fst = *fpst = 0;
+          for (int st = st_max; st >= 3 && *fst == 0; --st)
+            for (int pst = pst_max; pst >= 2; --pst)
+              if (k12_smem_bytes(c->N, hw, st, pst, rows) <= c->smem_optin) {
+                *fst = st;
+                *fpst = pst;
+                break;
+              }
+        };
+        fit(srm, &c->f_stages, &c->f_pstages);
+        if (HS == 2) {  // room for calibrated groups up to 1.15x the largest even group, if it costs no stage
+          const int big = kChunkRows12 * ((srm / kChunkRows12) * 115 / 100);
+          int bst = 0, bpst = 0;
+          fit(big, &bst, &bpst);
+          if (bst == c->f_stages && bpst == c->f_pstages && bst > 0) srm = big;
+          c->grp_cap_chunks = srm / kChunkRows12;
+        }
         if (c->f_stages > 0) {
           c->fused = true;
           c->k2_HW = hw;
@@ -803,6 +818,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
     A(dev_alloc(&c->d_role, static_cast<size_t>(c->k1_grid)));
     A(dev_alloc(&c->d_split, static_cast<size_t>(c->k2_VG)));
     A(dev_alloc(&c->d_wdur, 2 * static_cast<size_t>(c->k1_grid)));  // W phase | whole CTA, ns
+    A(dev_alloc(&c->d_gstart, static_cast<size_t>(c->k2_VG) + 1));
   }
   if (s.world > 1) {
     A(dev_alloc(&c->rec_all, c->full_words * s.world));
@@ -1084,10 +1100,11 @@ dinfer_status dinfer_balance(dinfer_ctx* c, const uint16_t* hidden, const uint16
   A(dev_alloc(&cval, M * K));
   A(dev_alloc(&sm, M * H));
   A(dev_alloc(&st, M * 4));
-  auto gsz = [&](int g) {
-    return static_cast<int>(static_cast<long>(g + 1) * nch / VG) - static_cast<int>(static_cast<long>(g) * nch / VG);
-  };
-  auto gbeg = [&](int g) { return static_cast<int>(static_cast<long>(g) * nch / VG); };
+  std::vector<int> gstart(VG + 1);  // group boundaries (chunks): even until step 4
+  for (int g = 0; g <= VG; ++g) gstart[g] = static_cast<int>(static_cast<long>(g) * nch / VG);
+  auto gsz = [&](int g) { return gstart[g + 1] - gstart[g]; };
+  auto gbeg = [&](int g) { return gstart[g]; };
+  c->groups_balanced = false;
   std::vector<int> role(G), split(VG);
   std::vector<double> dur(G, 0.0), tot(G, 0.0);
   // measure W-phase and whole-CTA durations per CTA under a given partition
@@ -1133,6 +1150,7 @@ dinfer_status dinfer_balance(dinfer_ctx* c, const uint16_t* hidden, const uint16
   auto upload = [&]() -> dinfer_status {
     DI_CUDA(cudaMemcpy(c->d_role, role.data(), 4 * G, cudaMemcpyHostToDevice));
     DI_CUDA(cudaMemcpy(c->d_split, split.data(), 4 * VG, cudaMemcpyHostToDevice));
+    DI_CUDA(cudaMemcpy(c->d_gstart, gstart.data(), 4 * (VG + 1), cudaMemcpyHostToDevice));
     return DINFER_OK;
   };
   // 1) the even partition
@@ -1209,6 +1227,55 @@ dinfer_status dinfer_balance(dinfer_ctx* c, const uint16_t* hidden, const uint16
       }
       s = upload();
     }
+    // 4) group sizes (DINFER_BALANCE_GROUPS=1): each pair's chunks toward its
+    //    measured rate (chunks / pair finish time), damped, within the head
+    //    table's cap; each pair keeps its split fraction
+    bool groups = false;
+    if (const char* e = std::getenv("DINFER_BALANCE_GROUPS")) groups = std::atoi(e) != 0;
+    double gdamp = 0.5;
+    if (const char* e = std::getenv("DINFER_BALANCE_GDAMP")) gdamp = std::atof(e);
+    if (groups && s == DINFER_OK && c->grp_cap_chunks > 0 && (s = measure(iters)) == DINFER_OK) {
+      const int P = G / 2, cap = c->grp_cap_chunks;
+      std::vector<double> prate(P), want(P);
+      double rsum = 0.0;
+      for (int k = 0; k < P; ++k) {
+        const double t = std::max(tot[cta0[k]], tot[cta1[k]]) / iters;
+        prate[k] = gsz(k) / std::max(1.0, t);
+        rsum += prate[k];
+      }
+      for (int k = 0; k < P; ++k)
+        want[k] = std::min<double>(cap, std::max<double>(4.0, gsz(k) + gdamp * (nch * prate[k] / rsum - gsz(k))));
+      std::vector<int> sz(P);
+      long tsum = 0;
+      std::vector<std::pair<double, int>> rem(P);
+      for (int k = 0; k < P; ++k) {
+        sz[k] = static_cast<int>(std::floor(want[k]));
+        tsum += sz[k];
+        rem[k] = {want[k] - sz[k], k};
+      }
+      std::sort(rem.begin(), rem.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+      for (int i = 0; tsum < nch; i = (i + 1) % P)
+        if (sz[rem[i].second] < cap) {
+          ++sz[rem[i].second];
+          ++tsum;
+        }
+      for (int i = P - 1; tsum > nch; i = (i + P - 1) % P)
+        if (sz[rem[i].second] > 4) {
+          --sz[rem[i].second];
+          --tsum;
+        }
+      std::vector<double> frac(P);
+      for (int k = 0; k < P; ++k) frac[k] = static_cast<double>(split[k] - gbeg(k)) / gsz(k);
+      for (int k = 0; k < P; ++k) gstart[k + 1] = gstart[k] + sz[k];
+      for (int k = 0; k < P; ++k) {
+        const int n = gsz(k);
+        int n0 = static_cast<int>(std::lround(frac[k] * n));
+        n0 = std::min(std::max(n0, std::max(1, n / 5)), std::min(n - 1, n - n / 5));
+        split[k] = gbeg(k) + n0;
+      }
+      s = upload();
+      c->groups_balanced = s == DINFER_OK;
+    }
     if (std::getenv("DINFER_BALANCE_VERBOSE") != nullptr) {
       double dmin = 1e30, dmax = 0;
       for (int b = 0; b < G; ++b) {
@@ -1236,7 +1303,10 @@ dinfer_status dinfer_balance(dinfer_ctx* c, const uint16_t* hidden, const uint16
   }
   cudaStreamSynchronize(c->stream);
   cudaFree(mask); cudaFree(com); cudaFree(tok); cudaFree(cid); cudaFree(cval); cudaFree(sm); cudaFree(st);
-  if (s != DINFER_OK) c->balanced = false;
+  if (s != DINFER_OK) {
+    c->balanced = false;
+    c->groups_balanced = false;
+  }
   return s;
 }
 
@@ -1254,12 +1324,14 @@ dinfer_status dinfer_debug_role_shift(dinfer_ctx* c, int32_t shift) {
   DI_CUDA(cudaMemcpy(c->d_role, role.data(), 4 * G, cudaMemcpyHostToDevice));
   DI_CUDA(cudaMemcpy(c->d_split, split.data(), 4 * VG, cudaMemcpyHostToDevice));
   c->balanced = true;
+  c->groups_balanced = false;
   return DINFER_OK;
 }
 
 dinfer_status dinfer_balance_reset(dinfer_ctx* c) {
   if (c == nullptr) return DINFER_ERR_ARG;
   c->balanced = false;
+  c->groups_balanced = false;
   c->k1_balanced = false;
   return DINFER_OK;
 }

@@ -226,8 +226,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int SPG = a.SPG;
   const int role = (a.role_of != nullptr) ? a.role_of[blockIdx.x] : static_cast<int>(blockIdx.x);
   const int grp = role / SPG, q = role - grp * SPG;
-  const int gc0 = static_cast<int>(static_cast<long>(grp) * a.nchunks / a.VG);
-  const int gc1 = static_cast<int>(static_cast<long>(grp + 1) * a.nchunks / a.VG);
+  const int gc0 = (a.grp_start != nullptr) ? a.grp_start[grp] : static_cast<int>(static_cast<long>(grp) * a.nchunks / a.VG);
+  const int gc1 =
+      (a.grp_start != nullptr) ? a.grp_start[grp + 1] : static_cast<int>(static_cast<long>(grp + 1) * a.nchunks / a.VG);
   const int nc = gc1 - gc0;
   int sc0 = gc0 + static_cast<int>(static_cast<long>(q) * nc / SPG);
   int sc1 = gc0 + static_cast<int>(static_cast<long>(q + 1) * nc / SPG);

@@ -67,6 +67,8 @@ struct K1Args {
   // K1 calibrated slabs (stats-only contexts, VG == 1; nullptr = even):
   // CTA b covers rows [slab_start[b], slab_start[b+1]) (8-row multiples)
   const int* slab_start;
+  // K12 calibrated vocab groups (nullptr = even): group g = chunks [grp_start[g], grp_start[g+1])
+  const int* grp_start;
 };
 size_t k1_smem_bytes(int N, int H, int stages, int h_resident, int slab_rows_max);
 cudaError_t launch_k1(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,

@@ -195,12 +195,14 @@ def test_next_input_embedding_rejects_unsupported(torch_cuda):
     ctx.close()
 
 
-@pytest.mark.parametrize("mode", ["after_forward", "back_to_back"])
-def test_balanced_partition_matches_oracle(torch_cuda, mode):
+@pytest.mark.parametrize("mode,groups", [("after_forward", "0"), ("back_to_back", "0"), ("back_to_back", "1")])
+def test_balanced_partition_matches_oracle(torch_cuda, monkeypatch, mode, groups):
     """dinfer_balance re-pairs CTAs and moves each group's split point to the
     measured per-SM rates (either calibration mode); the step's results must
     not change beyond fp32 summation order (decisions bit-exact), including
-    with a skewed split.  An unknown mode is rejected."""
+    with a skewed split, and with resized vocab groups (DINFER_BALANCE_GROUPS=1).
+    An unknown mode is rejected."""
+    monkeypatch.setenv("DINFER_BALANCE_GROUPS", groups)
     from paper_2510_08666_b200 import Context
     V, H, B, S, K = 32768, 2048, 1, 32, 32
     W, E = weights(V, H)
