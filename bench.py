@@ -304,14 +304,21 @@ def gpu_arm(args):
 
     # calibrated vocab partition (K12): measured per-SM streaming rates -> slab split
     partition = "even"
-    if not args.no_balance:  # K12 pairs + splits (smoothing) or K1 slab sizes (stats only); dense: none
+    # K12 pairs + splits (smoothing steps).  K1 slab calibration (stats-only
+    # contexts) measured no gain here, so stats-only configs run even slabs.
+    if not args.no_balance and smooth:
         from paper_2510_08666_b200 import DInferError
         try:
             ctx.balance(hid, Wd, Ed, emd, p, iters=4, mode="back_to_back")
             partition = "calibrated for back-to-back steps (dinfer_balance, 4 steps)"
         except DInferError:
             pass
-    # warm-up
+    # warm-up: every kernel of every timed loop runs here first (CUDA loads
+    # modules lazily on first launch: a first launch inside a timed loop would
+    # be charged to it), the back-to-back sequence W times, then W flushed steps
+    for _ in range(args.warmup):
+        block_reset()
+        one_step()
     for _ in range(args.warmup):
         reset_and_flush()
         one_step()
