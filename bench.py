@@ -12,7 +12,7 @@ stats, K2 smoothing mix, [acc reduce + allgather], K3 select/commit, K4
 smoothing finalize) on the first iteration of a block (all 32 positions
 undecided, fresh credit).  Synthetic seeded weights and planted hidden states
 (paper_2510_08666_b200.synth).  The headline times K back-to-back steps
-(each preceded by the library's block-start kernel, dinfer_block_reset) under
+(each a block's first iteration, params.block_start) under
 one event pair with no L2 flush: every step streams the weights (1.29 GB of
 W + E at N=1), far more than the 126 MB L2.  The same steps timed one at a
 time with L2 flushed before each are reported under "l2_flushed".
@@ -295,12 +295,16 @@ def gpu_arm(args):
             cids.fill_(-1)
             cval.zero_()
 
-    def block_reset():  # the library's block-start kernel (keeps the PDL chain between steps)
-        ctx.block_reset(mask, tokens, cids if credit else None, cval if credit else None, V - 1)
+    p_bs = make_params(decoder=CFG["decoder"], tau=0.9, theta_hi=0.92, theta_lo=0.62, use_credit=credit,
+                       use_smooth=smooth, alpha_t=0.1, block_start=True, mask_id=V - 1)
 
     def one_step():
         ctx.step(hid, Wd, Ed, emd, mask, tokens, cids if credit else None, cval if credit else None, p, committed,
                  smoothed, stats)
+
+    def block_start_step():  # a block's first iteration: the state inputs are not read (params.block_start)
+        ctx.step(hid, Wd, Ed, emd, mask, tokens, cids if credit else None, cval if credit else None, p_bs,
+                 committed, smoothed, stats)
 
     # calibrated vocab partition (K12): measured per-SM streaming rates -> slab split
     partition = "even"
@@ -317,8 +321,7 @@ def gpu_arm(args):
     # modules lazily on first launch: a first launch inside a timed loop would
     # be charged to it), the back-to-back sequence W times, then W flushed steps
     for _ in range(args.warmup):
-        block_reset()
-        one_step()
+        block_start_step()
     for _ in range(args.warmup):
         reset_and_flush()
         one_step()
@@ -326,9 +329,9 @@ def gpu_arm(args):
     torch.cuda.synchronize()
 
     # ---- timed region.
-    # Loop A (headline): K back-to-back steps, each a block start (dinfer_block_reset)
-    # + dinfer_step, bracketed by one event pair: the decode loop as a user runs
-    # it.  No L2 flush: each step streams 1.29 GB of W + E (> 126 MB L2).
+    # Loop A (headline): K back-to-back steps, each a block's first iteration
+    # (params.block_start: all positions undecided, credit slots empty), bracketed
+    # by one event pair.  No L2 flush: each step streams 1.29 GB of W + E (> 126 MB L2).
     # Loop A2: the same K steps one at a time with L2 flushed before each
     # (outside the events): no overlap with the previous step.
     # Loop B: as A with the library's per-kernel events on (these serialise the
@@ -346,8 +349,7 @@ def gpu_arm(args):
     with sampler:
         ea[0].record(stream)
         for i in range(args.steps):
-            block_reset()
-            one_step()
+            block_start_step()
         ea[1].record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - wall0
@@ -359,9 +361,8 @@ def gpu_arm(args):
         torch.cuda.synchronize()
         ctx.set_timing(True)
         for i in range(args.steps):
-            block_reset()
             evb[i][0].record(stream)
-            one_step()
+            block_start_step()
             evb[i][1].record(stream)
             ph = ctx.get_timing()  # syncs the stream (outside the event pair)
             for k_, v_ in ph.items():
@@ -467,12 +468,12 @@ def gpu_arm(args):
                                           else "NCCL allgather") + ")") if world > 1 else "single GPU",
                        "exchange": exchange, "partition": partition,
                        "l2": f"no flush: inputs > L2 ({step_bytes / 1e9:.2f} GB of W/E streamed per step vs 126 MB L2); "
-                             "K back-to-back steps (block reset + step) under one event pair"},
+                             "K back-to-back block-start steps under one event pair"},
             "e2e": {"value": M / (e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e, "api": "dinfer_step_host_async + dinfer_step_host_wait",
                     "timing": "per call: CUDA events around the call's copies + kernels on the ctx stream, "
                               "host wait between calls, no L2 flush"},
-            "gpu_launches": (launches + 1) * args.steps,  # + the block-reset kernel per step
+            "gpu_launches": launches * args.steps,
             "roofline": roof,
             "step_roofline": None if M > 256 else {"bytes": step_bytes, "achieved_gbs": step_bytes / (ms * 1e-3) / 1e9,
                               "frac": step_bytes / (ms * 1e-3) / 1e9 / hbm},

@@ -93,7 +93,16 @@ typedef struct {
  *                c13); 1: with the distribution the decoder decided on,
  *                softmax(f + c_alpha ln(1 + C)) -- exact, via the
  *                credited tokens' correction.  Requires use_credit,
- *                use_smooth, K <= 32 and world == 1 (else UNSUPPORTED).      */
+ *                use_smooth, K <= 32 and world == 1 (else UNSUPPORTED).
+ *   block_start  1: the step is the first iteration of a block (Alg. 1
+ *                NextBlock; credit reset P:327): the mask / tokens /
+ *                credit inputs are NOT read -- every position is undecided
+ *                and every credit slot empty -- and all of them are written:
+ *                mask = !committed, tokens = v~ where committed else mask_id,
+ *                credit slots = this step's update from empty.  Same result
+ *                as dinfer_block_reset + a step, one kernel boundary fewer.
+ *   mask_id      token id of an undecided position (block_start only;
+ *                in [0, V_total)).                                          */
 typedef struct {
   int32_t decoder;
   float tau;
@@ -104,6 +113,8 @@ typedef struct {
   int32_t use_smooth;
   float alpha_t;
   int32_t smooth_credit_fused;
+  int32_t block_start;
+  int32_t mask_id;
 } dinfer_params;
 
 /* 128-byte NCCL unique id for world > 1 (rank 0 calls it and broadcasts). */

@@ -245,6 +245,7 @@ dinfer_status check_params(const dinfer_ctx* c, const dinfer_params* p) {
   }
   if (p->smooth_credit_fused && (!p->use_credit || !p->use_smooth || c->shp.K > 32 || c->shp.world != 1))
     return DINFER_ERR_UNSUPPORTED;
+  if (p->block_start && (p->mask_id < 0 || p->mask_id >= c->shp.V_total)) return DINFER_ERR_ARG;
   return DINFER_OK;
 }
 
@@ -307,6 +308,7 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
   }
   a.err = c->err;
   a.trace = c->trace;
+  a.block_start = p->block_start ? 1 : 0;
   if (c->record_wdur) a.wdur = c->d_wdur;
   if (c->k1_balanced && !(smooth && c->fused)) a.slab_start = c->d_slab;
   if (smooth && c->fused) {
@@ -432,6 +434,8 @@ dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, in
   k.trace = c->trace == nullptr ? nullptr : c->trace + 5 * (c->k1_grid + c->k2_HS * c->k2_VG);
   k.B = c->shp.B;
   k.V_total = static_cast<long>(c->shp.V_total);
+  k.block_start = p->block_start ? 1 : 0;
+  k.mask_id = p->mask_id;
   k.S = c->shp.S;
   k.K = c->shp.K;
   k.world = world;
@@ -1554,7 +1558,9 @@ dinfer_status dinfer_step_host_async(dinfer_ctx* c, const uint16_t* hidden_h, co
                             static_cast<uint64_t>(p->hier_runs_after_hi), static_cast<uint64_t>(p->use_credit),
                             static_cast<uint64_t>(p->use_smooth), static_cast<uint64_t>(c->timing),
                             static_cast<uint64_t>(stats_h != nullptr),
-                            static_cast<uint64_t>(p->smooth_credit_fused) + 1 + 2 * static_cast<uint64_t>(kstage)};
+                            static_cast<uint64_t>(p->smooth_credit_fused) + 1 + 2 * static_cast<uint64_t>(kstage) +
+                                4 * static_cast<uint64_t>(p->block_start != 0) +
+                                8 * static_cast<uint64_t>(static_cast<uint32_t>(p->block_start ? p->mask_id : 0))};
   // timing events / NCCL: plain enqueue; a key whose capture failed (e.g. pageable
   // host buffers) also stays on the plain path
   const bool same_key = std::memcmp(key, c->host_graph_key, sizeof(key)) == 0;
@@ -1729,6 +1735,7 @@ dinfer_status dinfer_generate(dinfer_ctx* c, const dinfer_gen_config* cfg, const
       out == nullptr || hidden_iters < 1)
     return DINFER_ERR_ARG;
   if (c->shp.world != 1) return DINFER_ERR_UNSUPPORTED;
+  if (base->block_start) return DINFER_ERR_ARG;  // the loop manages block starts itself
   dinfer_status s = check_params(c, base);
   if (s != DINFER_OK) return s;
   const int B = c->shp.B, S = c->shp.S, K = c->shp.K, M = c->M;

@@ -251,13 +251,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     grid_dep_wait();  // mask / credit ids of the previous step's commit visible
     if (a.wdur != nullptr && threadIdx.x == 0) t_start = globaltimer_ns();
     if (a.mask_snap != nullptr && blockIdx.x == 0)
-      for (int s = threadIdx.x; s < a.M; s += kEpiWarps * kWarpThreads) a.mask_snap[s] = a.mask[s];
+      for (int s = threadIdx.x; s < a.M; s += kEpiWarps * kWarpThreads) a.mask_snap[s] = a.block_start ? 1 : a.mask[s];
     if (a.cids_snap != nullptr && blockIdx.x == 0)
       for (int e = threadIdx.x; e < a.M * a.K; e += kEpiWarps * kWarpThreads) {
-        a.cids_snap[e] = a.credit_ids[e];
-        a.cval_snap[e] = a.credit_val[e];
+        a.cids_snap[e] = a.block_start ? -1 : a.credit_ids[e];
+        a.cval_snap[e] = a.block_start ? 0.f : a.credit_val[e];
       }
-    if (a.credit_ids != nullptr) {
+    if (a.credit_ids != nullptr && !a.block_start) {  // block start: no credited token yet
       const int stride = kStatWords + a.K;
       for (int e = threadIdx.x; e < a.M * a.K; e += kEpiWarps * kWarpThreads) {
         const int s = e / a.K, k = e - s * a.K;

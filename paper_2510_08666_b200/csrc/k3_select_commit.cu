@@ -203,11 +203,11 @@ DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
     const long roff = static_cast<long>(i) * a.rec_stride;
     const long cbase = static_cast<long>(i) * a.K;
     // state loads issued before the statistics merge (independent round trips)
-    const bool und = a.mask[i] != 0;
+    const bool und = a.block_start || a.mask[i] != 0;  // block start: every position undecided
     const bool fast = a.use_credit && a.K <= 32;  // slot k in lane k, kept in registers
     const bool slot = fast && lane < a.K;
-    int cid = slot ? a.credit_ids[cbase + lane] : -1;
-    float cv = slot ? a.credit_val[cbase + lane] : 0.f;
+    int cid = (slot && !a.block_start) ? a.credit_ids[cbase + lane] : -1;  // block start: slots empty
+    float cv = (slot && !a.block_start) ? a.credit_val[cbase + lane] : 0.f;
     // device-checked precondition (SPEC: a credit entry is never negative; ids
     // index the vocabulary): sticky flag, surfaced by dinfer_sync
     if (und && slot && cid >= 0 && (cid >= a.V_total || !(cv >= 0.f))) atomicOr(a.err, kErrCreditInvalid);
@@ -247,6 +247,13 @@ DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
       vt = best_id;
       pt = __expf(best - lse_t);
     } else if (a.use_credit && und) {  // K > 32: slots strided over the lanes
+      if (a.block_start) {  // slots empty before this step's update
+        for (int k = lane; k < a.K; k += 32) {
+          a.credit_ids[cbase + k] = -1;
+          a.credit_val[cbase + k] = 0.f;
+        }
+        __syncwarp();
+      }
       const float gain = ex2(a.c_gamma * __log2f(pstar));  // p*^gamma
       // pass 1: decay, locate the slot of v* (or the first empty one)
       int hit = -1, empty = -1;
@@ -433,6 +440,9 @@ DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
       if (A[q]) {
         a.tokens[i] = s_vt[s];
         a.mask[i] = 0;
+      } else if (a.block_start) {  // the block's state is written whole
+        a.tokens[i] = a.mask_id;
+        a.mask[i] = 1;
       }
     }
   }

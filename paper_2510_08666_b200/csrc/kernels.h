@@ -69,6 +69,7 @@ struct K1Args {
   const int* slab_start;
   // K12 calibrated vocab groups (nullptr = even): group g = chunks [grp_start[g], grp_start[g+1])
   const int* grp_start;
+  int block_start;         // params.block_start: mask / credit inputs not read (all undecided, slots empty)
 };
 size_t k1_smem_bytes(int N, int H, int stages, int h_resident, int slab_rows_max);
 cudaError_t launch_k1(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
@@ -142,6 +143,7 @@ cudaError_t launch_rec_finalize(const RecArgs& a, cudaStream_t st, bool pdl);
 struct K3Args {
   int B, S, K, world;
   long V_total;            // credit ids outside [0, V_total) or negative credit values set kErrCreditInvalid
+  int block_start, mask_id;  // params.block_start: state inputs not read; mask / tokens / slots all written
   const float4* part1;     // G = 1: K1 per-slab partials [M][grid1] (stats merged here), else nullptr
   int grid1;
   const float* recs;       // world records, `rec_words` apart (stats used when part1 == nullptr; fcred always)

@@ -40,7 +40,7 @@ class Params(ctypes.Structure):
     _fields_ = [("decoder", c_int32), ("tau", c_float), ("theta_hi", c_float), ("theta_lo", c_float),
                 ("hier_runs_after_hi", c_int32), ("use_credit", c_int32), ("c_alpha", c_float),
                 ("c_beta", c_float), ("c_gamma", c_float), ("use_smooth", c_int32), ("alpha_t", c_float),
-                ("smooth_credit_fused", c_int32)]
+                ("smooth_credit_fused", c_int32), ("block_start", c_int32), ("mask_id", c_int32)]
 
 
 class GenConfig(ctypes.Structure):
@@ -136,12 +136,12 @@ def _check(status: int, what: str):
 
 def make_params(decoder=DEC_THRESHOLD, tau=0.9, theta_hi=0.92, theta_lo=0.62, hier_runs_after_hi=False,
                 use_credit=False, c_alpha=1.0, c_beta=0.9, c_gamma=0.5, use_smooth=False, alpha_t=0.1,
-                smooth_credit_fused=False) -> Params:
+                smooth_credit_fused=False, block_start=False, mask_id=0) -> Params:
     if isinstance(decoder, str):
         decoder = {"threshold": DEC_THRESHOLD, "hierarchical": DEC_HIERARCHICAL}[decoder]
     return Params(int(decoder), float(tau), float(theta_hi), float(theta_lo), int(bool(hier_runs_after_hi)),
                   int(bool(use_credit)), float(c_alpha), float(c_beta), float(c_gamma), int(bool(use_smooth)),
-                  float(alpha_t), int(bool(smooth_credit_fused)))
+                  float(alpha_t), int(bool(smooth_credit_fused)), int(bool(block_start)), int(mask_id))
 
 
 def alpha_schedule(init: float, growth: float, preset: float, t: int) -> float:

@@ -335,6 +335,48 @@ def test_block_reset_back_to_back(torch_cuda, monkeypatch, fused):
     ctx.close()
 
 
+@pytest.mark.parametrize("fused,K", [("0", 8), ("2", 8), ("2", 40)])
+def test_block_start_step_equals_reset_plus_step(torch_cuda, monkeypatch, fused, K):
+    """params.block_start: a step on garbage state (not read) writes the same
+    mask / tokens / credit slots / outputs as block reset + step (K <= 32
+    register slots and the strided K > 32 path; fused and two-kernel)."""
+    import torch
+    monkeypatch.setenv("DINFER_FUSED", fused)
+    from paper_2510_08666_b200 import Context
+    V, H, B, S = 4096, 512, 2, 32
+    W, E = weights(V, H)
+    mid = synth.mask_id(V)
+    ctx = Context(B, S, H, K, V)
+    h = to_dev_bf16(synth.planted_hidden(W, B * S, seed=17))
+    Wd, Ed, emd = to_dev_bf16(W), to_dev_bf16(E), to_dev_bf16(E[mid])
+    op = O.Params(decoder=O.DEC_HIERARCHICAL, use_credit=True, use_smooth=True)
+    ref = GpuState(B, S, H, K, mid)
+    ctx.block_reset(ref.mask, ref.tokens, ref.cids, ref.cval, mid)
+    ctx.step(h, Wd, Ed, emd, ref.mask, ref.tokens, ref.cids, ref.cval, gpu_params(op), ref.committed, ref.smoothed,
+             ref.stats)
+    ctx.sync()
+    want = ref.snapshot()
+    st = GpuState(B, S, H, K, mid)
+    st.mask.zero_()
+    st.tokens.fill_(5)
+    st.cids.fill_(3)
+    st.cval.fill_(-1.0)  # would be flagged if read
+    p = gpu_params(op)
+    p.block_start, p.mask_id = 1, mid
+    torch.cuda.synchronize()
+    for _ in range(2):  # back to back: the second step reads nothing the first wrote
+        ctx.step(h, Wd, Ed, emd, st.mask, st.tokens, st.cids, st.cval, p, st.committed, st.smoothed, st.stats)
+    ctx.sync()  # no device flag: the garbage state was not read
+    got = st.snapshot()
+    for k in ("committed", "tokens", "mask", "cids", "cval", "m", "lse", "ptilde"):
+        assert np.array_equal(got[k], want[k]), k
+    assert np.array_equal(np.nan_to_num(got["smoothed"]), np.nan_to_num(want["smoothed"]))
+    p.mask_id = V  # out of range
+    with pytest.raises(Exception):
+        ctx.step(h, Wd, Ed, emd, st.mask, st.tokens, st.cids, st.cval, p, st.committed, st.smoothed, st.stats)
+    ctx.close()
+
+
 # ---------------------------------------------------------------- split phases / vocab sharding on one GPU
 @pytest.mark.parametrize("G", [2, 4, 8])
 def test_sharded_split_phase_matches_oracle(torch_cuda, G):
