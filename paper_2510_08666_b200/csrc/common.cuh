@@ -98,6 +98,18 @@ DI uint64_t policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// 8-byte global store / load with an L2 cache policy (the smoothing partials:
+// stored evict_last so they survive the weight stream in L2 until K34 reads
+// them, read back evict_first)
+DI void st_global_hint_v2(void* ptr, uint2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(ptr), "r"(v.x), "r"(v.y), "l"(pol)
+               : "memory");
+}
+DI uint2 ld_global_hint_v2(const void* ptr, uint64_t pol) {
+  uint2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(ptr), "l"(pol));
+  return v;
+}
 // 2-D tile load global -> shared (c0 = innermost coordinate), completes on `bar`.
 DI void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, uint64_t policy) {
   asm volatile(

@@ -720,6 +720,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int sub0 = (wg == 0) ? 0 : half, sub1 = (wg == 0) ? half : b.nsub;
     float* tile = reinterpret_cast<float*>(ring) + wg * 2 * (32 * 128);
     const int hbase = hs * b.HW;
+    const uint64_t pol_part = policy_evict_last();  // kept in L2 for K34 (the weight streams are evict_first)
     const uint32_t lanebase = tmem_base + (static_cast<uint32_t>(wq * 32) << 16);
     for (int sub = sub0; sub < sub1; ++sub) {
       for (int g = 0; g < ng; ++g) {
@@ -751,9 +752,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int row = u >> 5, c4 = u & 31;
           const int s = g * 32 + row;
           if (s < a.M)
-            __stcg(reinterpret_cast<uint2*>(b.part + (static_cast<long>(grp) * a.M + s) * a.H + hbase + sub * 128 +
-                                            c4 * 4),
-                   pack_half4(*reinterpret_cast<const float4*>(t + row * 128 + c4 * 4)));
+            st_global_hint_v2(b.part + (static_cast<long>(grp) * a.M + s) * a.H + hbase + sub * 128 + c4 * 4,
+                              pack_half4(*reinterpret_cast<const float4*>(t + row * 128 + c4 * 4)), pol_part);
         }
       }
     }

@@ -299,8 +299,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int row = q >> 5, c4 = q & 31;
           const int s = g * 32 + row;
           if (s < a.M)
-            *reinterpret_cast<uint2*>(a.part + (static_cast<long>(vg) * a.M + s) * a.H + hbase + sub * 128 + c4 * 4) =
-                pack_half4(*reinterpret_cast<const float4*>(tile + row * 128 + c4 * 4));
+            st_global_hint_v2(a.part + (static_cast<long>(vg) * a.M + s) * a.H + hbase + sub * 128 + c4 * 4,
+                              pack_half4(*reinterpret_cast<const float4*>(tile + row * 128 + c4 * 4)),
+                              policy_evict_last());
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * kWarpThreads) : "memory");
       }

@@ -497,13 +497,14 @@ DI void accumulate_parts(const K4Args& a, int s, int h, int grp, float4& pacc, f
   using Raw = typename std::conditional<kHalf, uint2, float4>::type;
   Raw raw[kB];
   float mp[kB];
+  const uint64_t pol = policy_evict_first();  // read once
   for (int p0 = grp; p0 < a.nparts; p0 += kB * kSmGroups) {
 #pragma unroll
     for (int j = 0; j < kB; ++j) {
       const int p = p0 + j * kSmGroups;
       const bool ok = p < a.nparts;
       if constexpr (kHalf)
-        raw[j] = ok ? __ldcg(reinterpret_cast<const uint2*>(a.acc_h + base + p * a.acc_stride)) : make_uint2(0u, 0u);
+        raw[j] = ok ? ld_global_hint_v2(a.acc_h + base + p * a.acc_stride, pol) : make_uint2(0u, 0u);
       else
         raw[j] = ok ? __ldcg(reinterpret_cast<const float4*>(a.acc + base + p * a.acc_stride))
                     : make_float4(0.f, 0.f, 0.f, 0.f);
