@@ -71,6 +71,7 @@ struct dinfer_ctx {
   int grp_cap_chunks = 0;     // largest group the K12 head table admits
   bool k1_balanced = false;
   bool stage_kernels = true;  // dinfer_step_host: zero-copy staging kernels (env DINFER_STAGE_KERNELS=0: copies)
+  bool k12_probe = false;     // env DINFER_K12_PROBE (read once at create): K12 progress words on a timeout
   bool record_wdur = false;
   int f_stages = 0, f_pstages = 0;
   size_t f_smem = 0;
@@ -344,7 +345,7 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
     b.mref = c->mref;
     b.part = c->part2;
     b.trace = c->trace == nullptr ? nullptr : c->trace + 5 * c->k1_grid;
-    if (std::getenv("DINFER_K12_PROBE") != nullptr) {
+    if (c->k12_probe) {
       if (c->probe_h == nullptr) {
         void* hp = nullptr;
         if (cudaHostAlloc(&hp, 64 * 4 * 1024, cudaHostAllocMapped) == cudaSuccess) {
@@ -795,6 +796,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
   }
   if (const char* e = std::getenv("DINFER_HOST_GRAPH")) c->host_graph_ok = std::atoi(e) != 0;
   if (const char* e = std::getenv("DINFER_STAGE_KERNELS")) c->stage_kernels = std::atoi(e) != 0;
+  c->k12_probe = std::getenv("DINFER_K12_PROBE") != nullptr;
 
   // ---- workspace
   c->stats_words = static_cast<size_t>(M) * (kStatWords + s.K);
