@@ -72,6 +72,7 @@ struct dinfer_ctx {
   bool k1_balanced = false;
   bool stage_kernels = true;  // dinfer_step_host: zero-copy staging kernels (env DINFER_STAGE_KERNELS=0: copies)
   bool k12_probe = false;     // env DINFER_K12_PROBE (read once at create): K12 progress words on a timeout
+  int k12_npre = 0;           // env DINFER_K12_NPRE: W stages issued before the dependency wait (0 = ring)
   bool record_wdur = false;
   int f_stages = 0, f_pstages = 0;
   size_t f_smem = 0;
@@ -316,6 +317,7 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
     // K12: the vocab slab partition at 16-row chunk granularity (nchunks /
     // chunk_rows), the E phase over the slab's vocab group
     a.stages = c->f_stages;
+    a.npre = std::min(c->k12_npre, c->f_stages);
     a.nchunks = c->k2_nchunks;
     a.chunk_rows = kChunkRows12;
     if (c->balanced) {
@@ -800,6 +802,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
   if (const char* e = std::getenv("DINFER_HOST_GRAPH")) c->host_graph_ok = std::atoi(e) != 0;
   if (const char* e = std::getenv("DINFER_STAGE_KERNELS")) c->stage_kernels = std::atoi(e) != 0;
   c->k12_probe = std::getenv("DINFER_K12_PROBE") != nullptr;
+  if (const char* e = std::getenv("DINFER_K12_NPRE")) c->k12_npre = std::max(0, std::atoi(e));
 
   // ---- workspace
   c->stats_words = static_cast<size_t>(M) * (kStatWords + s.K);

@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // W does not depend on the preceding kernel: the first ring's worth of W
     // stages is issued now (each stage's barrier expects W + hidden bytes; the
     // hidden boxes follow after grid_dep_wait)
-    const int spt = a.num_kc / 2, npre = min(a.stages, ntiles * spt);
+    const int spt = a.num_kc / 2, npre = min(a.npre > 0 ? a.npre : a.stages, ntiles * spt);
     const uint64_t pol_first = policy_evict_first();
     for (int i = 0; i < npre; ++i) {
       const int t = i / spt;
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const uint64_t pol_first = policy_evict_first();  // W and E are streamed exactly once
       const uint64_t pol_h = policy_evict_last();       // hidden is re-read by every CTA
-      const int spt = a.num_kc / 2, nW = ntiles * spt, npre = min(a.stages, nW);
+      const int spt = a.num_kc / 2, nW = ntiles * spt, npre = min(a.npre > 0 ? a.npre : a.stages, nW);
       grid_dep_wait();  // hidden may be produced by the preceding kernel
       for (int i = 0; i < npre; ++i) {  // hidden boxes of the W stages issued before the wait
         const int kc0 = (i % spt) * 2;

@@ -70,6 +70,7 @@ struct K1Args {
   // K12 calibrated vocab groups (nullptr = even): group g = chunks [grp_start[g], grp_start[g+1])
   const int* grp_start;
   int block_start;         // params.block_start: mask / credit inputs not read (all undecided, slots empty)
+  int npre;                // K12: W stages issued before the dependency wait (0 = the whole ring; tuning)
 };
 size_t k1_smem_bytes(int N, int H, int stages, int h_resident, int slab_rows_max);
 cudaError_t launch_k1(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
