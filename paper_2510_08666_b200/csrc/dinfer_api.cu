@@ -774,11 +774,15 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
     // Hidden block resident in smem (loaded once) or streamed from L2 with every
     // W stage.  Residency only pays if it still leaves >= 4 W stages: at MoE
     // shape it leaves 2 (measured 144 us) against 5 streamed stages (134 us).
-    int st_res = 0, st_str = 0;
+    // ring depth cap 4 (DINFER_K1_STAGES overrides): at 8B bs1 4 and 5 stages give the
+    // same back-to-back step (191.0 vs 190.6-190.9 us) and 4 is faster after an L2
+    // flush (207.1-207.5 vs 211.0-211.2 us); 3 is slower (195.5 us)
+    int st_res = 0, st_str = 0, k1_st_max = 4;
+    if (const char* e = std::getenv("DINFER_K1_STAGES")) k1_st_max = std::max(2, std::atoi(e));
     if (static_cast<long>(c->N) * s.H * 2 <= 160 * 1024)
-      for (int st = 8; st >= 2 && st_res == 0; --st)
+      for (int st = k1_st_max; st >= 2 && st_res == 0; --st)
         if (k1_smem_bytes(c->N, s.H, st, 1, c->slab_rows_max) <= c->smem_optin) st_res = st;
-    for (int st = 8; st >= 2 && st_str == 0; --st)
+    for (int st = k1_st_max; st >= 2 && st_str == 0; --st)
       if (k1_smem_bytes(c->N, s.H, st, 0, c->slab_rows_max) <= c->smem_optin) st_str = st;
     bool use_res = st_res >= 4 || (st_res > 0 && st_str == 0);
     if (const char* e = std::getenv("DINFER_K1_HRES")) use_res = (std::atoi(e) != 0 && st_res > 0) || st_str == 0;
