@@ -11,9 +11,11 @@
  *   (App. A.1) for positions still masked.
  *
  * The vocabulary may be sharded over `world` GPUs (contiguous rows of W_vocab
- * and W_emb); per-rank partial statistics are exchanged with one NCCL
- * allgather and every rank runs the identical combine, so decode state stays
- * replicated and bit-identical across ranks.
+ * and W_emb); each rank's partial record (statistics + smoothing partial) is
+ * exchanged in-kernel over peer memory (dinfer_exchange_open; the producing
+ * kernel stores it into every peer's gather buffer over NVLink) or, without
+ * opened peer buffers, by one NCCL allgather; every rank then runs the
+ * identical combine, so decode state stays replicated and bit-identical.
  *
  * Conventions (all entry points):
  *  - Every pointer is CALLER-OWNED; the library never frees or retains it
@@ -102,7 +104,12 @@ typedef struct {
  *                credit slots = this step's update from empty.  Same result
  *                as dinfer_block_reset + a step, one kernel boundary fewer.
  *   mask_id      token id of an undecided position (block_start only;
- *                in [0, V_total)).                                          */
+ *                in [0, V_total)).
+ *   inclusive    0: threshold tests are strict, p~ > tau / theta (P:118
+ *                "exceeds", reading c1; tau = 1 then commits exactly one
+ *                position per step); 1: inclusive p~ >= tau / theta, the
+ *                SPEC's reading (variant c1').  Both sides of every
+ *                comparison are fp32 on the device.                         */
 typedef struct {
   int32_t decoder;
   float tau;
@@ -115,6 +122,7 @@ typedef struct {
   int32_t smooth_credit_fused;
   int32_t block_start;
   int32_t mask_id;
+  int32_t inclusive;
 } dinfer_params;
 
 /* 128-byte NCCL unique id for world > 1 (rank 0 calls it and broadcasts). */

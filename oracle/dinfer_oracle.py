@@ -124,11 +124,17 @@ def confidence(ftilde: np.ndarray):
 # Reading c2: if nothing clears, commit the undecided position with the
 # highest confidence (lowest index on ties).
 # ---------------------------------------------------------------------------
-def threshold_decode(ptilde, undecided, tau: float) -> np.ndarray:
+def _clears(p, thr, inclusive: bool) -> bool:
+    """Reading c1: "exceeds" is strict '>'; the SPEC's inclusive
+    '>=' is the `inclusive` variant (DESIGN.md c1')."""
+    return p >= thr if inclusive else p > thr
+
+
+def threshold_decode(ptilde, undecided, tau: float, inclusive: bool = False) -> np.ndarray:
     S = len(undecided)
     A = np.zeros(S, dtype=bool)
     for s in range(S):
-        if undecided[s] and ptilde[s] > tau:
+        if undecided[s] and _clears(ptilde[s], tau, inclusive):
             A[s] = True
     if not A.any():
         best = _fallback_argmax(ptilde, undecided)
@@ -174,11 +180,11 @@ def undecided_runs(undecided):
 # The recursion happens across iterations: every commit splits its run.
 # ---------------------------------------------------------------------------
 def hierarchical_decode(ptilde, undecided, theta_hi: float, theta_lo: float,
-                        runs_after_hi: bool = False) -> np.ndarray:
+                        runs_after_hi: bool = False, inclusive: bool = False) -> np.ndarray:
     S = len(undecided)
     A = np.zeros(S, dtype=bool)
     for s in range(S):                                            # (a)
-        if undecided[s] and ptilde[s] > theta_hi:
+        if undecided[s] and _clears(ptilde[s], theta_hi, inclusive):
             A[s] = True
     region_mask = [bool(undecided[s]) and not (runs_after_hi and A[s]) for s in range(S)]
     for first, last in undecided_runs(region_mask):               # (b)
@@ -188,7 +194,7 @@ def hierarchical_decode(ptilde, undecided, theta_hi: float, theta_lo: float,
         for s in range(first, last + 1):
             if best is None or _hier_better(s, best, ptilde, first, last):
                 best = s
-        if ptilde[best] > theta_lo:
+        if _clears(ptilde[best], theta_lo, inclusive):
             A[best] = True
     if not A.any():                                               # (c)
         best = _fallback_argmax(ptilde, undecided)
@@ -289,6 +295,7 @@ class Params:
     alpha_t: float = 0.1
     hier_runs_after_hi: bool = False
     smooth_credit_fused: bool = False   # f4: smooth with softmax(f~) instead of softmax(f)
+    inclusive: bool = False             # c1': thresholds compare '>=' instead of '>'
 
 
 def step(h, W, E, e_mask, mask, tokens, C, params: Params, f=None):
@@ -324,10 +331,10 @@ def step(h, W, E, e_mask, mask, tokens, C, params: Params, f=None):
         if not und.any():
             A = np.zeros(S, dtype=bool)           # empty row: defined no-op (§8b)
         elif params.decoder == DEC_THRESHOLD:
-            A = threshold_decode(pt, und, params.tau)
+            A = threshold_decode(pt, und, params.tau, params.inclusive)
         else:
             A = hierarchical_decode(pt, und, params.theta_hi, params.theta_lo,
-                                    params.hier_runs_after_hi)
+                                    params.hier_runs_after_hi, params.inclusive)
         for s in range(S):                         # commit
             if A[s]:
                 tokens[b, s] = vt[s]

@@ -11,7 +11,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
+#include <utility>
 #include <vector>
 
 #include "dinfer.h"
@@ -22,6 +25,30 @@
 #endif
 
 using namespace dinfer;
+
+namespace dinfer {
+cudaError_t ensure_func_smem(const void* fn, size_t smem, int carveout_pct) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, std::pair<size_t, int>> done;  // (kernel, device) -> (smem, carveout)
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find({fn, dev});
+  const size_t have = (it == done.end()) ? 0 : it->second.first;
+  const int have_c = (it == done.end()) ? -1 : it->second.second;
+  if (smem > have) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  if (carveout_pct >= 0 && carveout_pct != have_c) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carveout_pct);
+    if (e != cudaSuccess) return e;
+  }
+  done[{fn, dev}] = {smem > have ? smem : have, carveout_pct >= 0 ? carveout_pct : have_c};
+  return cudaSuccess;
+}
+}  // namespace dinfer
 
 namespace {
 
@@ -73,6 +100,7 @@ struct dinfer_ctx {
   bool stage_kernels = true;  // dinfer_step_host: zero-copy staging kernels (env DINFER_STAGE_KERNELS=0: copies)
   bool k12_probe = false;     // env DINFER_K12_PROBE (read once at create): K12 progress words on a timeout
   int k12_npre = 0;           // env DINFER_K12_NPRE: W stages issued before the dependency wait (0 = ring)
+  int k12_x = 0;              // env DINFER_K12_X: measurement-only K12 experiments (kernels.h K1Args::xbits)
   bool record_wdur = false;
   int f_stages = 0, f_pstages = 0;
   size_t f_smem = 0;
@@ -318,6 +346,7 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
     // chunk_rows), the E phase over the slab's vocab group
     a.stages = c->f_stages;
     a.npre = std::min(c->k12_npre, c->f_stages);
+    a.xbits = c->k12_x;
     a.nchunks = c->k2_nchunks;
     a.chunk_rows = kChunkRows12;
     if (c->balanced) {
@@ -458,6 +487,7 @@ dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, in
   k.row_cnt = c->row_cnt;
   k.decoder = p->decoder;
   k.runs_after_hi = p->hier_runs_after_hi;
+  k.inclusive = p->inclusive;
   k.use_credit = p->use_credit;
   k.tau = p->tau;
   k.theta_hi = p->theta_hi;
@@ -705,6 +735,15 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
           if (bst == c->f_stages && bpst == c->f_pstages && bst > 0) srm = big;
           c->grp_cap_chunks = srm / kChunkRows12;
         }
+        // K12's CTAs of a vocab group wait for each other (group counters): the
+        // grid (VG x HS CTAs, one per SM) must be co-resident.  If the SMs
+        // cannot hold it (e.g. an MPS SM limit, or a larger smem than one CTA
+        // per SM admits), use K1 -> K2 instead, whose cross-CTA waits only go
+        // from the later kernel to the earlier.
+        if (c->f_stages > 0 &&
+            static_cast<long>(k12_blocks_per_sm(k12_smem_bytes(c->N, hw, c->f_stages, c->f_pstages, srm))) *
+                    c->num_sms < static_cast<long>(VG) * HS)
+          c->f_stages = 0;
         if (c->f_stages > 0) {
           c->fused = true;
           c->k2_HW = hw;
@@ -807,6 +846,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
   if (const char* e = std::getenv("DINFER_STAGE_KERNELS")) c->stage_kernels = std::atoi(e) != 0;
   c->k12_probe = std::getenv("DINFER_K12_PROBE") != nullptr;
   if (const char* e = std::getenv("DINFER_K12_NPRE")) c->k12_npre = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("DINFER_K12_X")) c->k12_x = std::atoi(e);
 
   // ---- workspace
   c->stats_words = static_cast<size_t>(M) * (kStatWords + s.K);
@@ -1470,7 +1510,12 @@ dinfer_status dinfer_step_combine(dinfer_ctx* c, const float* records, const uin
                         !aligned(e_mask, 8) || !aligned(smoothed, 16)))
     return DINFER_ERR_ARG;
   const size_t words = p->use_smooth ? c->full_words : c->stats_words;
-  if (p->use_smooth) DI_CUDA(cudaMemcpyAsync(c->mask_snap, mask, c->M, cudaMemcpyDeviceToDevice, c->stream));
+  // the smoothing blocks write the rows undecided at step start: every row on a
+  // block's first iteration (the mask input is not read then)
+  if (p->use_smooth) {
+    if (p->block_start) DI_CUDA(cudaMemsetAsync(c->mask_snap, 1, c->M, c->stream));
+    else DI_CUDA(cudaMemcpyAsync(c->mask_snap, mask, c->M, cudaMemcpyDeviceToDevice, c->stream));
+  }
   return run_combine(c, records, words, c->shp.world, /*acc_from_part2=*/false, e_mask, mask, tokens, credit_ids,
                      credit_val, p, committed, smoothed, stats);
 }
@@ -1484,6 +1529,9 @@ dinfer_status dinfer_step_host_async(dinfer_ctx* c, const uint16_t* hidden_h, co
     return DINFER_ERR_ARG;
   if (p->use_credit && (cids_h == nullptr || cval_h == nullptr)) return DINFER_ERR_ARG;
   if (p->use_smooth && smoothed_h == nullptr) return DINFER_ERR_ARG;
+  // one pending call per ctx: a second _async would rewrite the mapped pinned
+  // staging block while the pending step's staging kernels may still read it
+  if (c->pend.active) return DINFER_ERR_ARG;
   const size_t M = static_cast<size_t>(c->M), H = static_cast<size_t>(c->shp.H), K = static_cast<size_t>(c->shp.K);
   // One device block + one pinned host mirror for the small per-step state, so
   // the step moves it with one H2D and one D2H copy (hidden and smoothed go
@@ -1568,7 +1616,8 @@ dinfer_status dinfer_step_host_async(dinfer_ctx* c, const uint16_t* hidden_h, co
                             reinterpret_cast<uint64_t>(E),        reinterpret_cast<uint64_t>(e_mask),
                             reinterpret_cast<uint64_t>(smoothed_h), static_cast<uint64_t>(p->decoder),
                             static_cast<uint64_t>(p->hier_runs_after_hi), static_cast<uint64_t>(p->use_credit),
-                            static_cast<uint64_t>(p->use_smooth), static_cast<uint64_t>(c->timing),
+                            static_cast<uint64_t>(p->use_smooth) | (static_cast<uint64_t>(p->inclusive != 0) << 1),
+                            static_cast<uint64_t>(c->timing),
                             static_cast<uint64_t>(stats_h != nullptr),
                             static_cast<uint64_t>(p->smooth_credit_fused) + 1 + 2 * static_cast<uint64_t>(kstage) +
                                 4 * static_cast<uint64_t>(p->block_start != 0) +

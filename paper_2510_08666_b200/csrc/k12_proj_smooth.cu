@@ -293,11 +293,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     // stages is issued now (each stage's barrier expects W + hidden bytes; the
     // hidden boxes follow after grid_dep_wait)
     const int spt = a.num_kc / 2, npre = min(a.npre > 0 ? a.npre : a.stages, ntiles * spt);
-    const uint64_t pol_first = policy_evict_first();
+    const uint64_t pol_first = (a.xbits & 4) ? policy_evict_normal() : policy_evict_first();
+    const uint32_t hbytes = (a.xbits & 1) ? 0u : hchunk;
     for (int i = 0; i < npre; ++i) {
       const int t = i / spt;
       const int rows = min(kTileRows, r1 - (r0 + t * kTileRows));
-      mbar_expect_tx(&full[i], 2u * (static_cast<uint32_t>(rows) * 128u + hchunk));
+      mbar_expect_tx(&full[i], 2u * (static_cast<uint32_t>(rows) * 128u + hbytes));
       issue_w_stage(&map_w, &map_w8, ring + i * L.wslot, &full[i], r0, r1, i, spt, pol_first);
     }
   }
@@ -315,11 +316,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 4) {
     // ------------------------------------------------------------ TMA: W (+ hidden), then E
     if (lane == 0) {
-      const uint64_t pol_first = policy_evict_first();  // W and E are streamed exactly once
+      // W and E are streamed exactly once (xbits 4 / 8: measurement variants)
+      const uint64_t pol_first = (a.xbits & 4) ? policy_evict_normal() : policy_evict_first();
+      const uint64_t pol_e = (a.xbits & 8) ? policy_evict_normal() : policy_evict_first();
       const uint64_t pol_h = policy_evict_last();       // hidden is re-read by every CTA
+      const bool ld_h = (a.xbits & 1) == 0;
+      const uint32_t hbytes = ld_h ? hchunk : 0u;
       const int spt = a.num_kc / 2, nW = ntiles * spt, npre = min(a.npre > 0 ? a.npre : a.stages, nW);
       grid_dep_wait();  // hidden may be produced by the preceding kernel
-      for (int i = 0; i < npre; ++i) {  // hidden boxes of the W stages issued before the wait
+      for (int i = 0; i < npre && ld_h; ++i) {  // hidden boxes of the W stages issued before the wait
         const int kc0 = (i % spt) * 2;
         for (int j = 0; j < 2; ++j)
           tma_load_2d(ring + i * L.wslot + kWBytes + j * hchunk, &map_h, &full[i], (kc0 + j) * kKChunk, 0, pol_h);
@@ -331,9 +336,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int rows = min(kTileRows, r1 - (r0 + t * kTileRows));
         mbar_wait(&empty[stage], phase ^ 1u);
         uint8_t* slot = ring + stage * L.wslot;
-        mbar_expect_tx(&full[stage], 2u * (static_cast<uint32_t>(rows) * 128u + hchunk));
+        mbar_expect_tx(&full[stage], 2u * (static_cast<uint32_t>(rows) * 128u + hbytes));
         issue_w_stage(&map_w, &map_w8, slot, &full[stage], r0, r1, idx, spt, pol_first);
-        for (int j = 0; j < 2; ++j)
+        for (int j = 0; j < 2 && ld_h; ++j)
           tma_load_2d(slot + kWBytes + j * hchunk, &map_h, &full[stage], (kc0 + j) * kKChunk, 0, pol_h);
         advance(stage, phase, a.stages);
       }
@@ -357,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* slot = ring + es * L.eslot;
         mbar_expect_tx(&efull[es], e_bytes);
         for (int bx = 0; bx < b.HW / 64; ++bx)
-          tma_load_2d(slot + bx * ebox, &map_e, &efull[es], hs * b.HW + bx * 64, c * KV, pol_first);
+          tma_load_2d(slot + bx * ebox, &map_e, &efull[es], hs * b.HW + bx * 64, c * KV, pol_e);
         advance(es, eph, static_cast<int>(L.estages));
         PROBE(0, 100000 + j);
       }
@@ -548,7 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           float x[32];
           tmem_ld32(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(buf * N + g * 32),
                     x);
-          if (valid) {
+          if (valid && (a.xbits & 2) == 0) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const int col = g * 32 + j;
@@ -781,15 +786,25 @@ size_t k12_smem_bytes(int N, int HW, int stages, int pstages, int slab_rows_max)
   return L.total + 1024;
 }
 
+int k12_blocks_per_sm(size_t smem) {
+  if (ensure_func_smem(reinterpret_cast<const void*>(k12_proj_smooth), smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k12_proj_smooth, kThreads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 cudaError_t launch_k12(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
                        const CUtensorMap& map_e, const CUtensorMap& map_f, const K1Args& a, const K2Args& b, int grid,
                        size_t smem, cudaStream_t st, bool pdl) {
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k12_proj_smooth, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+  {
+    const cudaError_t e = ensure_func_smem(reinterpret_cast<const void*>(k12_proj_smooth), smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   return launch_ex(k12_proj_smooth, dim3(grid), dim3(kThreads), smem, st, pdl, map_w, map_w8, map_h, map_e, map_f, a,
                    b);

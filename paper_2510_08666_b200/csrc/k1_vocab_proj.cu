@@ -392,12 +392,9 @@ size_t k1_smem_bytes(int N, int H, int stages, int h_resident, int slab_rows_max
 
 cudaError_t launch_k1(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
                       const K1Args& a, int grid, size_t smem, cudaStream_t st, bool pdl) {
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k1_vocab_proj, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+  {
+    const cudaError_t e = ensure_func_smem(reinterpret_cast<const void*>(k1_vocab_proj), smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   return launch_ex(k1_vocab_proj, dim3(grid), dim3(kThreads), smem, st, pdl, map_w, map_w8, map_h, a);
 }

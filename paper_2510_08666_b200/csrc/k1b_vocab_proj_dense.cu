@@ -238,12 +238,9 @@ size_t k1b_smem_bytes(int stages) { return make_layout(stages).total + 1024; }
 
 cudaError_t launch_k1b(const CUtensorMap& map_h, const CUtensorMap& map_w, const K1bArgs& a, int grid, size_t smem,
                        cudaStream_t st, bool pdl) {
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k1b_vocab_proj_dense, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+  {
+    const cudaError_t e = ensure_func_smem(reinterpret_cast<const void*>(k1b_vocab_proj_dense), smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   return launch_ex(k1b_vocab_proj_dense, dim3(grid), dim3(kThreads), smem, st, pdl, map_h, map_w, a);
 }

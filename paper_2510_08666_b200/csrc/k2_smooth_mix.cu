@@ -423,12 +423,9 @@ size_t k2_smem_bytes(int N, int HW, int KV, int stages, int pstages) {
 
 cudaError_t launch_k2(const CUtensorMap& map_e, const CUtensorMap& map_f, const K2Args& a, size_t smem,
                       cudaStream_t st, bool pdl) {
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k2_smooth_mix, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+  {
+    const cudaError_t e = ensure_func_smem(reinterpret_cast<const void*>(k2_smooth_mix), smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   return launch_ex(k2_smooth_mix, dim3(a.HS * a.VG), dim3(kThreads), smem, st, pdl, map_e, map_f, a);
 }

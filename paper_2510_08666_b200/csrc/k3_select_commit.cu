@@ -15,7 +15,8 @@
 //             v~ = argmax_{cred u {v*}} f~ (lowest id on ties), p~ = e^{f~_{v~} - lse~}
 //             (warp-shuffle reductions in a fixed order).
 // Phase 2 is thread-per-position:
-//   select    threshold (strict '>', fallback max) or hierarchical
+//   select    threshold (strict '>' or '>=' with params.inclusive,
+//             fallback max) or hierarchical
 //             (maximal runs of undecided positions; per run the
 //             best position, ties nearest the run centre then lower index,
 //             if p~ > theta_lo), via ballots and shared-memory atomics.
@@ -362,6 +363,9 @@ DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
   // position s = threadIdx.x + q * kK3Threads (q < kPer); its ballot word is warp + q * nwarps
   const int nwords = (a.S + 31) / 32;
   const float thr_primary = (a.decoder == 0) ? a.tau : a.theta_hi;
+  // reading c1: "exceeds" is strict; variant c1' (params.inclusive) is SPEC's '>='
+  const bool incl = a.inclusive != 0;
+  auto clears = [incl](float p, float thr) { return incl ? p >= thr : p > thr; };
   bool A[kPer], und[kPer], region[kPer];
   float pt[kPer];
   int first[kPer];
@@ -372,7 +376,7 @@ DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
     const bool valid = s < a.S;
     und[q] = valid && s_und[s];
     pt[q] = valid ? s_pt[s] : 0.f;
-    A[q] = und[q] && pt[q] > thr_primary;
+    A[q] = und[q] && clears(pt[q], thr_primary);
     region[q] = false;
     first[q] = 0;
     key[q] = 0ull;
@@ -405,7 +409,7 @@ DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < kPer; ++q)
-      if (region[q] && !s_runA[first[q]] && s_runkey[first[q]] == key[q] && pt[q] > a.theta_lo) A[q] = true;
+      if (region[q] && !s_runA[first[q]] && s_runkey[first[q]] == key[q] && clears(pt[q], a.theta_lo)) A[q] = true;
   }
   if (threadIdx.x == 0) s_best = 0ull;
   bool mine = false;
@@ -726,11 +730,9 @@ __global__ void __launch_bounds__(kK3Threads) k34_select_smooth(const K3Args a3i
 }  // namespace
 
 cudaError_t launch_k34(const K3Args& a3, const K4Args* a4, cudaStream_t st, bool pdl) {
-  static bool configured = false;
-  if (!configured) {  // same smem carveout as K1/K2 (no L1/smem reconfiguration between kernels)
-    cudaError_t e = cudaFuncSetAttribute(k34_select_smooth, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  {  // same smem carveout as K1/K2 (no L1/smem reconfiguration between kernels)
+    const cudaError_t e = ensure_func_smem(reinterpret_cast<const void*>(k34_select_smooth), 0, 100);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   int nsm = 0;
   K4Args f{};

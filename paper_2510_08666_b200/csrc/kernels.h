@@ -33,6 +33,12 @@ cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sm
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
+// cudaFuncSetAttribute applies to the CURRENT device only: the dynamic
+// shared-memory limit (and optionally the carveout) of each kernel is raised
+// per (kernel, device) pair, under a mutex (host threads may create contexts
+// concurrently, on different devices).  Implemented in dinfer_api.cu.
+cudaError_t ensure_func_smem(const void* fn, size_t smem, int carveout_pct = -1);
+
 // Device-side sticky error bits (dinfer_sync reads and clears them).
 enum : int { kErrCreditEntOverflow = 1, kErrCreditSlotsFull = 2, kErrCreditInvalid = 4 };
 
@@ -71,6 +77,8 @@ struct K1Args {
   const int* grp_start;
   int block_start;         // params.block_start: mask / credit inputs not read (all undecided, slots empty)
   int npre;                // K12: W stages issued before the dependency wait (0 = the whole ring; tuning)
+  int xbits;               // K12 measurement-only experiments (env DINFER_K12_X; 0 in the product):
+                           //   1 no hidden loads, 2 no flog stores, 4 W evict_normal, 8 E evict_normal
 };
 size_t k1_smem_bytes(int N, int H, int stages, int h_resident, int slab_rows_max);
 cudaError_t launch_k1(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
@@ -114,6 +122,9 @@ cudaError_t launch_k2(const CUtensorMap& map_e, const CUtensorMap& map_f, const 
 // nchunks / chunk_rows in 16-row chunks) and K2Args (E phase; HS == SPG
 // hidden slices of HW columns, pstages logits / P ring depth; stages unused).
 size_t k12_smem_bytes(int N, int HW, int stages, int pstages, int slab_rows_max);
+// Co-resident K12 CTAs per SM at this shared-memory size (K12 CTAs of a vocab
+// group wait for each other's W phase, so the whole grid must be resident).
+int k12_blocks_per_sm(size_t smem);
 cudaError_t launch_k12(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
                        const CUtensorMap& map_e, const CUtensorMap& map_f, const K1Args& a, const K2Args& b, int grid,
                        size_t smem, cudaStream_t st, bool pdl);
@@ -160,6 +171,7 @@ struct K3Args {
   float4* sel;             // [M] per-position (p~, v~ bits, undecided, 0) from the phase-1 CTAs
   int* row_cnt;            // [B] phase-1 CTAs arrived per batch row (zero between steps)
   int decoder, runs_after_hi, use_credit;
+  int inclusive;           // thresholds compare '>=' instead of '>' (reading c1)
   float tau, theta_hi, theta_lo, c_alpha, c_beta, c_gamma;
   unsigned long long* trace;  // DINFER_TRACE: blocks < kTraceK34 stamp [entry, deps, phase1, end, smid]
   int H;

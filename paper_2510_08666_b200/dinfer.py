@@ -40,7 +40,8 @@ class Params(ctypes.Structure):
     _fields_ = [("decoder", c_int32), ("tau", c_float), ("theta_hi", c_float), ("theta_lo", c_float),
                 ("hier_runs_after_hi", c_int32), ("use_credit", c_int32), ("c_alpha", c_float),
                 ("c_beta", c_float), ("c_gamma", c_float), ("use_smooth", c_int32), ("alpha_t", c_float),
-                ("smooth_credit_fused", c_int32), ("block_start", c_int32), ("mask_id", c_int32)]
+                ("smooth_credit_fused", c_int32), ("block_start", c_int32), ("mask_id", c_int32),
+                ("inclusive", c_int32)]
 
 
 class GenConfig(ctypes.Structure):
@@ -129,6 +130,34 @@ def _ptr(t):
     return c_void_p(t.data_ptr())
 
 
+def _expect(t, name: str, dtypes, numel: int, device: str, at_least: bool = False):
+    """Argument marshalling guard: the C ABI takes bare pointers and cannot
+    check sizes, so a wrong dtype, a strided view, the wrong device or a short
+    buffer would be silent garbage or an out-of-bounds device access.  None is
+    passed through (the library checks which pointers may be NULL)."""
+    if t is None:
+        return
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name}: expected a torch.Tensor, got {type(t).__name__}")
+    if t.dtype not in dtypes:
+        raise TypeError(f"{name}: dtype {t.dtype}, expected one of {[str(d) for d in dtypes]}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous")
+    if t.numel() < numel or (t.numel() != numel and not at_least):
+        raise ValueError(f"{name}: {t.numel()} elements, expected {'at least ' if at_least else ''}{numel}")
+    if device == "cuda" and not t.is_cuda:
+        raise ValueError(f"{name}: must be a CUDA tensor")
+    if device == "cpu" and t.is_cuda:
+        raise ValueError(f"{name}: must be a host (CPU) tensor")
+
+
+def _dt():
+    import torch
+    return dict(bf16=(torch.bfloat16, torch.int16), u8=(torch.uint8, torch.bool), i32=(torch.int32,),
+                f32=(torch.float32,))
+
+
 def _check(status: int, what: str):
     if status != 0:
         raise DInferError(status, what)
@@ -136,12 +165,13 @@ def _check(status: int, what: str):
 
 def make_params(decoder=DEC_THRESHOLD, tau=0.9, theta_hi=0.92, theta_lo=0.62, hier_runs_after_hi=False,
                 use_credit=False, c_alpha=1.0, c_beta=0.9, c_gamma=0.5, use_smooth=False, alpha_t=0.1,
-                smooth_credit_fused=False, block_start=False, mask_id=0) -> Params:
+                smooth_credit_fused=False, block_start=False, mask_id=0, inclusive=False) -> Params:
     if isinstance(decoder, str):
         decoder = {"threshold": DEC_THRESHOLD, "hierarchical": DEC_HIERARCHICAL}[decoder]
     return Params(int(decoder), float(tau), float(theta_hi), float(theta_lo), int(bool(hier_runs_after_hi)),
                   int(bool(use_credit)), float(c_alpha), float(c_beta), float(c_gamma), int(bool(use_smooth)),
-                  float(alpha_t), int(bool(smooth_credit_fused)), int(bool(block_start)), int(mask_id))
+                  float(alpha_t), int(bool(smooth_credit_fused)), int(bool(block_start)), int(mask_id),
+                  int(bool(inclusive)))
 
 
 def alpha_schedule(init: float, growth: float, preset: float, t: int) -> float:
@@ -188,6 +218,24 @@ class Context:
         except Exception:
             pass
 
+    def _check_step(self, dev, hidden, W, E, e_mask, mask, tokens, credit_ids, credit_val, committed, smoothed,
+                    stats, emb=None):
+        d = _dt()
+        sh = self.shape
+        M = sh.B * sh.S
+        _expect(hidden, "hidden", d["bf16"], M * sh.H, dev)
+        _expect(W, "W_vocab", d["bf16"], sh.V_local * sh.H, "cuda")
+        _expect(E, "E", d["bf16"], sh.V_local * sh.H, "cuda")
+        _expect(e_mask, "e_mask", d["bf16"], sh.H, "cuda")
+        _expect(mask, "mask", d["u8"], M, dev)
+        _expect(tokens, "tokens", d["i32"], M, dev)
+        _expect(credit_ids, "credit_ids", d["i32"], M * sh.K, dev)
+        _expect(credit_val, "credit_val", d["f32"], M * sh.K, dev)
+        _expect(committed, "committed", d["u8"], M, dev)
+        _expect(smoothed, "smoothed", d["f32"], M * sh.H, dev)
+        _expect(stats, "stats", d["f32"], M * 4, dev)
+        _expect(emb, "emb", d["bf16"], M * sh.H, "cuda")
+
     def set_stream(self, stream):
         self._stream = stream
         _check(lib().dinfer_set_stream(self._h, c_void_p(stream)), "dinfer_set_stream")
@@ -195,6 +243,8 @@ class Context:
     # -- the step
     def step(self, hidden, W, E, e_mask, mask, tokens, credit_ids, credit_val, params: Params, committed,
              smoothed=None, stats=None):
+        self._check_step("cuda", hidden, W, E, e_mask, mask, tokens, credit_ids, credit_val, committed, smoothed,
+                         stats)
         _check(lib().dinfer_step(self._h, _ptr(hidden), _ptr(W), _ptr(E), _ptr(e_mask), _ptr(mask), _ptr(tokens),
                                  _ptr(credit_ids), _ptr(credit_val), ctypes.byref(params), _ptr(committed),
                                  _ptr(smoothed), _ptr(stats)), "dinfer_step")
@@ -205,6 +255,7 @@ class Context:
         """Calibrate the K12 vocab partition to this GPU's per-SM rates
         (dinfer_balance) for steps that follow a model forward
         ("after_forward") or each other directly ("back_to_back")."""
+        self._check_step("cuda", hidden, W, E, e_mask, None, None, None, None, None, None, None)
         _check(lib().dinfer_balance(self._h, _ptr(hidden), _ptr(W), _ptr(E), _ptr(e_mask), ctypes.byref(params),
                                     int(iters), self.BALANCE_MODES[mode]), "dinfer_balance")
 
@@ -226,6 +277,8 @@ class Context:
     def step_embed(self, hidden, W, E, e_mask, mask, tokens, credit_ids, credit_val, params: Params, committed,
                    smoothed, stats, emb):
         """dinfer_step + the next iteration's bf16 input embedding `emb` [B,S,H]."""
+        self._check_step("cuda", hidden, W, E, e_mask, mask, tokens, credit_ids, credit_val, committed, smoothed,
+                         stats, emb)
         _check(lib().dinfer_step_embed(self._h, _ptr(hidden), _ptr(W), _ptr(E), _ptr(e_mask), _ptr(mask),
                                        _ptr(tokens), _ptr(credit_ids), _ptr(credit_val), ctypes.byref(params),
                                        _ptr(committed), _ptr(smoothed), _ptr(stats), _ptr(emb)), "dinfer_step_embed")
@@ -238,6 +291,8 @@ class Context:
     def step_host_async(self, hidden_h, W, E, e_mask, mask_h, tokens_h, credit_ids_h, credit_val_h, params: Params,
                         committed_h, smoothed_h=None, stats_h=None):
         """dinfer_step_host without the final wait (see step_host_wait)."""
+        self._check_step("cpu", hidden_h, W, E, e_mask, mask_h, tokens_h, credit_ids_h, credit_val_h, committed_h,
+                         smoothed_h, stats_h)
         self._pending = (hidden_h, mask_h, tokens_h, credit_ids_h, credit_val_h, committed_h, smoothed_h, stats_h)
         _check(lib().dinfer_step_host_async(self._h, _ptr(hidden_h), _ptr(W), _ptr(E), _ptr(e_mask), _ptr(mask_h),
                                             _ptr(tokens_h), _ptr(credit_ids_h), _ptr(credit_val_h),
@@ -250,6 +305,8 @@ class Context:
 
     def step_host(self, hidden_h, W, E, e_mask, mask_h, tokens_h, credit_ids_h, credit_val_h, params: Params,
                   committed_h, smoothed_h=None, stats_h=None):
+        self._check_step("cpu", hidden_h, W, E, e_mask, mask_h, tokens_h, credit_ids_h, credit_val_h, committed_h,
+                         smoothed_h, stats_h)
         _check(lib().dinfer_step_host(self._h, _ptr(hidden_h), _ptr(W), _ptr(E), _ptr(e_mask), _ptr(mask_h),
                                       _ptr(tokens_h), _ptr(credit_ids_h), _ptr(credit_val_h), ctypes.byref(params),
                                       _ptr(committed_h), _ptr(smoothed_h), _ptr(stats_h)), "dinfer_step_host")
@@ -259,6 +316,13 @@ class Context:
         [iters, B*S, H] bf16 is the model stand-in; out int32 [B + 2] receives
         T_b, F, truncated.  Asynchronous on the ctx stream."""
         iters = int(hidden_src.shape[0])
+        d, sh = _dt(), self.shape
+        _expect(hidden_src, "hidden_src", d["bf16"], iters * sh.B * sh.S * sh.H, "cuda")
+        _expect(X, "X", d["i32"], sh.B * int(cfg.L), "cuda")
+        _expect(out, "out", d["i32"], sh.B + 2, "cuda")
+        _expect(W, "W_vocab", d["bf16"], sh.V_local * sh.H, "cuda")
+        _expect(E, "E", d["bf16"], sh.V_local * sh.H, "cuda")
+        _expect(e_mask, "e_mask", d["bf16"], sh.H, "cuda")
         _check(lib().dinfer_generate(self._h, ctypes.byref(cfg), ctypes.byref(base), _ptr(W), _ptr(E), _ptr(e_mask),
                                      _ptr(hidden_src), iters, _ptr(X), _ptr(out)), "dinfer_generate")
 
@@ -266,11 +330,17 @@ class Context:
         return int(lib().dinfer_record_words(self._h, int(bool(use_smooth))))
 
     def step_local(self, hidden, W, E, mask, credit_ids, params: Params, record):
+        self._check_step("cuda", hidden, W, E, None, mask, None, credit_ids, None, None, None, None)
+        _expect(record, "record", _dt()["f32"], self.record_words(bool(params.use_smooth)), "cuda", at_least=True)
         _check(lib().dinfer_step_local(self._h, _ptr(hidden), _ptr(W), _ptr(E), _ptr(mask), _ptr(credit_ids),
                                        ctypes.byref(params), _ptr(record)), "dinfer_step_local")
 
     def step_combine(self, records, e_mask, mask, tokens, credit_ids, credit_val, params: Params, committed,
                      smoothed=None, stats=None):
+        self._check_step("cuda", None, None, None, e_mask, mask, tokens, credit_ids, credit_val, committed, smoothed,
+                         stats)
+        _expect(records, "records", _dt()["f32"], self.shape.world * self.record_words(bool(params.use_smooth)),
+                "cuda", at_least=True)
         _check(lib().dinfer_step_combine(self._h, _ptr(records), _ptr(e_mask), _ptr(mask), _ptr(tokens),
                                          _ptr(credit_ids), _ptr(credit_val), ctypes.byref(params),
                                          _ptr(committed), _ptr(smoothed), _ptr(stats)), "dinfer_step_combine")

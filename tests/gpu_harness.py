@@ -48,13 +48,19 @@ def gpu_params(p: O.Params):
     return make_params(decoder=p.decoder, tau=p.tau, theta_hi=p.theta_hi, theta_lo=p.theta_lo,
                        hier_runs_after_hi=p.hier_runs_after_hi, use_credit=p.use_credit, c_alpha=p.c_alpha,
                        c_beta=p.c_beta, c_gamma=p.c_gamma, use_smooth=p.use_smooth, alpha_t=p.alpha_t,
-                       smooth_credit_fused=p.smooth_credit_fused)
+                       smooth_credit_fused=p.smooth_credit_fused, inclusive=p.inclusive)
 
 
-def compare(out, gold, mask_before, params: O.Params, where=""):
+def compare(out, gold, mask_before, params: O.Params, where="", exclude=()):
     """Element-by-element parity of one step.  Integer / decision state is
-    bit-exact; floating outputs within the stated tolerances."""
+    bit-exact; floating outputs within the stated tolerances.  `exclude`:
+    positions (b, s) whose own top-2 margin is within 1e-3 (reading c19) --
+    their v~ / p~ / credit slots are not compared (every decision still is)."""
     B, S = mask_before.shape
+    und_all = np.array(mask_before, bool)
+    mask_before = und_all.copy()
+    for b, s in exclude:
+        mask_before[b, s] = False
     np.testing.assert_array_equal(out["committed"], gold["committed"], err_msg=f"committed {where}")
     np.testing.assert_array_equal(out["mask"], gold["mask"], err_msg=f"mask {where}")
     np.testing.assert_array_equal(out["tokens"], gold["tokens"], err_msg=f"tokens {where}")
@@ -80,7 +86,7 @@ def compare(out, gold, mask_before, params: O.Params, where=""):
                     assert abs(got[v] - want[v]) <= TOL_CREDIT_REL * max(1.0, abs(want[v])), \
                         f"credit val b{b} s{s} v{v} {got[v]} vs {want[v]} {where}"
     if params.use_smooth:
-        still = gold["mask"]
+        still = gold["mask"] & und_all
         for b in range(B):
             for s in np.nonzero(still[b])[0]:
                 ref = gold["smoothed"][b, s]

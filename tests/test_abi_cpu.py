@@ -109,3 +109,33 @@ def test_kv_region_helper_matches_oracle(L):
         n = L.dinfer_kv_region(ctypes.byref(s), start, end, t, int(full), ctypes.byref(lo), ctypes.byref(hi))
         want = O.refresh_region(Ls, start, end, t, pre, aft, warm % 6, full)
         assert (lo.value, hi.value) == want and n == want[1] - want[0]
+
+
+def test_binding_rejects_bad_tensors_before_the_abi():
+    """The ctypes binding checks dtype, contiguity, device and element count
+    against the ctx shape before handing bare pointers to the C ABI (ADVICE
+    r1): a wrong buffer must raise, not become silent garbage."""
+    import torch
+    from paper_2510_08666_b200.dinfer import _dt, _expect
+    d = _dt()
+    _expect(torch.zeros(64, dtype=torch.int32), "tokens", d["i32"], 64, "cpu")
+    with pytest.raises(TypeError):
+        _expect(torch.zeros(64, dtype=torch.int64), "tokens", d["i32"], 64, "cpu")
+    with pytest.raises(ValueError):
+        _expect(torch.zeros(63, dtype=torch.int32), "tokens", d["i32"], 64, "cpu")
+    with pytest.raises(ValueError):
+        _expect(torch.zeros(8, 16, dtype=torch.int32).t(), "tokens", d["i32"], 128, "cpu")
+    with pytest.raises(ValueError):
+        _expect(torch.zeros(64, dtype=torch.int32), "tokens", d["i32"], 64, "cuda")
+    _expect(torch.zeros(70, dtype=torch.float32), "records", d["f32"], 64, "cpu", at_least=True)
+    with pytest.raises(TypeError):
+        _expect(np.zeros(64, np.int32), "tokens", d["i32"], 64, "cpu")
+    _expect(None, "E", d["bf16"], 10, "cuda")
+
+
+def test_params_struct_matches_header():
+    """dinfer_params field order / count in the binding equals include/dinfer.h."""
+    src = open(os.path.join(ROOT, "include", "dinfer.h")).read()
+    body = re.search(r"typedef struct \{([^}]*)\} dinfer_params;", src).group(1)
+    names = re.findall(r"(\w+)\s*[,;]", re.sub(r"/\*.*?\*/", "", body, flags=re.S))
+    assert names == [n for n, _ in dinfer.Params._fields_]

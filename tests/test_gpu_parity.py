@@ -621,3 +621,107 @@ def test_8b_bs64_block64_sampled_rows(torch_cuda):
             one = {k: (v[b:b + 1] if isinstance(v, np.ndarray) and v.ndim >= 1 and v.shape[0] == B else v)
                    for k, v in out.items()}
             compare(one, gold, trajs[b][t]["mask"], p, where=f"row {b} iter {t}")
+
+
+# ---------------------------------------------------------------- round-2 API fixes
+def test_inclusive_thresholds(torch_cuda):
+    """params.inclusive (variant c1'): a position whose fp32 p~
+    sits exactly on tau commits with '>=' and not with '>' (both sides of
+    the comparison are the device's fp32 values: tau is set to the p~ the
+    device reported)."""
+    import torch
+    from paper_2510_08666_b200 import Context, make_params
+    V, H, B, S, K = 1024, 256, 1, 32, 8
+    W, E = weights(V, H)
+    h = to_dev_bf16(synth.planted_hidden(W, B * S, seed=5))
+    Wd = to_dev_bf16(W)
+    ctx = Context(B, S, H, K, V, smooth_capable=False)
+    st = GpuState(B, S, H, K, V - 1)
+    ctx.step(h, Wd, None, None, st.mask, st.tokens, None, None, make_params(tau=1.0), st.committed, None, st.stats)
+    torch.cuda.synchronize()
+    pt = st.stats[0, :, 2].cpu().numpy()
+    order = np.argsort(-pt)
+    s_hi = int(order[1])  # the second best: not the fallback
+    tau = float(pt[s_hi])
+    assert pt[order[0]] > tau and np.sum(pt == tau) == 1
+    for incl, want in ((False, {int(order[0])} | {int(s) for s in np.nonzero(pt > tau)[0]}),
+                       (True, {int(s) for s in np.nonzero(pt >= tau)[0]})):
+        st = GpuState(B, S, H, K, V - 1)
+        ctx.step(h, Wd, None, None, st.mask, st.tokens, None, None, make_params(tau=tau, inclusive=incl),
+                 st.committed, None, st.stats)
+        torch.cuda.synchronize()
+        got = set(np.nonzero(st.committed.cpu().numpy()[0])[0].tolist())
+        assert got == want, (incl, got, want)
+        assert (s_hi in got) == incl
+    ctx.close()
+
+
+def test_combine_block_start_writes_smoothed_rows(torch_cuda):
+    """dinfer_step_combine with params.block_start on an all-decided (garbage)
+    mask: every row counts as undecided at step start, so the smoothing output
+    is written for every row still masked (the mask snapshot must
+    not be copied from the unread mask input)."""
+    import torch
+    from paper_2510_08666_b200 import Context
+    V, H, B, S, K = 2048, 256, 1, 32, 8
+    W, E = weights(V, H)
+    mid = synth.mask_id(V)
+    G = 2
+    Vl = V // G
+    ctxs = [Context(B, S, H, K, V, V_local=Vl, v_offset=r * Vl, world=G, rank=r) for r in range(G)]
+    h = to_dev_bf16(synth.planted_hidden(W, B * S, seed=19))
+    emd = to_dev_bf16(E[mid])
+    op = O.Params(decoder=O.DEC_HIERARCHICAL, use_credit=True, use_smooth=True, alpha_t=0.2)
+    words = ctxs[0].record_words(True)
+    recs = torch.zeros((G, words), dtype=torch.float32, device="cuda")
+    ref = GpuState(B, S, H, K, mid)
+    for r in range(G):
+        ctxs[r].step_local(h, to_dev_bf16(W[r * Vl:(r + 1) * Vl]), to_dev_bf16(E[r * Vl:(r + 1) * Vl]), ref.mask,
+                           ref.cids, gpu_params(op), recs[r])
+    ctxs[0].step_combine(recs, emd, ref.mask, ref.tokens, ref.cids, ref.cval, gpu_params(op), ref.committed,
+                         ref.smoothed, ref.stats)
+    torch.cuda.synchronize()
+    want = ref.snapshot()
+    p = gpu_params(op)
+    p.block_start, p.mask_id = 1, mid
+    st = GpuState(B, S, H, K, mid)
+    st.mask.zero_()  # garbage: all decided
+    st.cids.fill_(3)
+    recs2 = torch.zeros_like(recs)
+    for r in range(G):
+        ctxs[r].step_local(h, to_dev_bf16(W[r * Vl:(r + 1) * Vl]), to_dev_bf16(E[r * Vl:(r + 1) * Vl]), st.mask,
+                           st.cids, p, recs2[r])
+    ctxs[0].step_combine(recs2, emd, st.mask, st.tokens, st.cids, st.cval, p, st.committed, st.smoothed, st.stats)
+    torch.cuda.synchronize()
+    ctxs[0].sync()
+    got = st.snapshot()
+    for k in ("committed", "tokens", "mask", "cids", "cval", "m", "lse", "ptilde"):
+        assert np.array_equal(got[k], want[k]), k
+    still = want["mask"]
+    assert still.any()
+    assert np.array_equal(got["smoothed"][still], want["smoothed"][still])
+
+
+def test_second_host_async_is_rejected(torch_cuda):
+    """One pending dinfer_step_host_async per ctx (include/dinfer.h): a second
+    call before _wait returns ERR_ARG and enqueues nothing."""
+    import torch
+    from paper_2510_08666_b200 import Context, DInferError
+    V, H, B, S, K = 1024, 256, 1, 32, 8
+    W, E = weights(V, H)
+    Wd = to_dev_bf16(W)
+    ctx = Context(B, S, H, K, V, smooth_capable=False)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    hh = pin(synth.planted_hidden(W, B * S, seed=3).view(np.int16))
+    mask, tok = pin(np.ones((B, S), np.uint8)), pin(np.full((B, S), V - 1, np.int32))
+    com = pin(np.zeros((B, S), np.uint8))
+    p = gpu_params(O.Params(decoder=O.DEC_THRESHOLD, tau=0.9))
+    ctx.step_host_async(hh, Wd, None, None, mask, tok, None, None, p, com)
+    with pytest.raises(DInferError) as ei:
+        ctx.step_host_async(hh, Wd, None, None, mask, tok, None, None, p, com)
+    assert ei.value.status == 1
+    ctx.step_host_wait()
+    assert com.numpy().sum() >= 1
+    ctx.step_host_async(hh, Wd, None, None, mask, tok, None, None, p, com)  # accepted again
+    ctx.step_host_wait()
+    ctx.close()

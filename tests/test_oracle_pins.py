@@ -286,6 +286,30 @@ def test_hierarchical_hand_examples():
         assert np.nonzero(A)[0].tolist() == c["expected_A"], c["name"]
         A2 = O.hierarchical_decode(p, m, c["theta_hi"], c["theta_lo"], runs_after_hi=True)
         assert np.nonzero(A2)[0].tolist() == c["expected_A_prime"], c["name"]
+        if "expected_A_inclusive" in c:
+            A3 = O.hierarchical_decode(p, m, c["theta_hi"], c["theta_lo"], inclusive=True)
+            assert np.nonzero(A3)[0].tolist() == c["expected_A_inclusive"], c["name"]
+
+
+def test_inclusive_variant_pins():
+    """Variant c1' (comparisons '>='), hand-evaluated fixtures:
+    T1 commits the position sitting exactly on tau; tau = 1.0 commits every
+    saturated position (p~ = 1.0) instead of only the fallback; away from the
+    thresholds both readings agree."""
+    cases = _gold("hierarchical_examples.json")["cases"]
+    t1 = [c for c in cases if c["name"] == "T1_threshold_strict"][0]
+    A = O.threshold_decode(np.array(t1["ptilde"]), np.array(t1["mask"], bool), t1["tau"], inclusive=True)
+    assert np.nonzero(A)[0].tolist() == t1["expected_A_inclusive"]
+    A = O.threshold_decode(np.array([1.0, 1.0, 0.3]), np.ones(3, bool), 1.0, inclusive=True)
+    assert A.tolist() == [True, True, False]
+    rng = np.random.default_rng(12)
+    for _ in range(200):
+        S = int(rng.integers(1, 40))
+        p = np.round(rng.uniform(0, 1, S), 3) + 2e-4  # never on a 3-decimal threshold
+        m = rng.uniform(size=S) < 0.7
+        for tau in (0.5, 0.8, 0.9):
+            assert (O.threshold_decode(p, m, tau) == O.threshold_decode(p, m, tau, True)).all()
+        assert (O.hierarchical_decode(p, m, 0.92, 0.62) == O.hierarchical_decode(p, m, 0.92, 0.62, inclusive=True)).all()
 
 
 def test_hierarchical_saturated_and_floor():
