@@ -2,20 +2,30 @@
 """Benchmark of the fused denoise-and-commit step (dInfer, arXiv 2510.08666).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+                  [--config moe|8b|8b-bs64|tiny] [--shard-sim G]
 
 Workload (BASELINE.json metric: "denoise-step positions/sec and HBM GB/s
 fraction, LLaDA-MoE shape bs1, 1/2/4/8 B200"): configs[2], LLaDA-MoE shape
 H=2048, V=157184, block S=32, batch 1, hierarchical + credit decoding +
-iteration smoothing; the vocabulary is sharded over N GPUs (configs[3]) with
-one NCCL allgather per step.  A step = one dinfer_step (K1 vocab projection +
-stats, K2 smoothing mix, [acc reduce + allgather], K3 select/commit, K4
-smoothing finalize) on the first iteration of a block (all 32 positions
-undecided, fresh credit).  Synthetic seeded weights and planted hidden states
-(paper_2510_08666_b200.synth).  The headline times K back-to-back steps
-(each a block's first iteration, params.block_start) under
-one event pair with no L2 flush: every step streams the weights (1.29 GB of
-W + E at N=1), far more than the 126 MB L2.  The same steps timed one at a
-time with L2 flushed before each are reported under "l2_flushed".
+iteration smoothing; for N > 1 the vocabulary is sharded over the N GPUs
+(configs[3]) and each rank's record is pushed into every peer's gather buffer
+by the producing kernel (peer-memory exchange; NCCL allgather fallback).  A
+step = one dinfer_step on the first iteration of a block (all 32 positions
+undecided, fresh credit): K12 (vocab projection + softmax statistics +
+smoothing contraction, with the rank-record finalize folded into its tail when
+sharded) then K34 (combine, credit, selection, commit, smoothing output).
+Synthetic seeded weights and planted hidden states (paper_2510_08666_b200.synth).
+The headline times K back-to-back steps (each a block's first iteration,
+params.block_start) under one event pair; every step reads weights the L2 does
+not hold (1.29 GB per step at N=1; for shards smaller than 3x the L2 the loop
+rotates over enough weight copies).  The same steps timed one at a time with
+the L2 flushed before each are reported under "l2_flushed", and the steps
+replayed from one CUDA graph under "graph_replay".
+
+--shard-sim G (N=1 only, measurement): one rank of a G-way vocab shard on one
+GPU (V_local = V/G, the record stored into all G slots of its own gather
+buffer -- dinfer_exchange_loopback), i.e. the per-rank step of configs[3]
+minus the NVLink latency; its decisions are not meaningful.
 
 Prints ONE JSON line on rank 0.  --impl reference times the CPU oracle (the
 reference arm of this tier) on the host cores instead.
@@ -139,11 +149,13 @@ def dist_env():
 
 
 # ------------------------------------------------------------------ oracle (CPU) arm
-def oracle_run(n_steps: int, n_warm: int, rows: int, budget_s: float | None = None):
+def oracle_run(n_steps: int, n_warm: int, rows: int, budget_s: float | None = None, threads: int | None = None):
     """Time the CPU oracle (as it stands) on `rows` positions of the workload
-    per step.  Returns (seconds per step list, cores)."""
+    per step, with the BLAS pools limited to `threads` (None: all host cores).
+    Returns (seconds per step list, threads used)."""
     import oracle as O
     from paper_2510_08666_b200 import synth
+    from threadpoolctl import threadpool_info, threadpool_limits
     W_u16 = synth.make_W(V, H, 1)
     W = O.bf16_bits_to_f64(W_u16)
     E = O.bf16_bits_to_f64(synth.make_E(V, H, 2)) if CFG["smooth"] else W[:1]
@@ -154,23 +166,50 @@ def oracle_run(n_steps: int, n_warm: int, rows: int, budget_s: float | None = No
                  tau=0.9, theta_hi=0.92, theta_lo=0.62, use_credit=CFG["credit"], use_smooth=CFG["smooth"],
                  alpha_t=0.1)
     times = []
-    for i in range(n_warm + n_steps):
-        mask = np.ones((1, rows), bool)
-        tok = np.full((1, rows), V - 1)
-        C = np.zeros((1, rows, V)) if CFG["credit"] else None
-        t0 = time.perf_counter()
-        O.step(h, W, E, em, mask, tok, C, p)
-        dt = time.perf_counter() - t0
-        if i >= n_warm:
-            times.append(dt)
-        if budget_s is not None and i >= n_warm and sum(times) > budget_s:
-            break
-    try:
-        from threadpoolctl import threadpool_info
+    with threadpool_limits(limits=threads):
         cores = max((d.get("num_threads", 1) for d in threadpool_info()), default=1)
-    except Exception:
-        cores = os.cpu_count()
+        for i in range(n_warm + n_steps):
+            mask = np.ones((1, rows), bool)
+            tok = np.full((1, rows), V - 1)
+            C = np.zeros((1, rows, V)) if CFG["credit"] else None
+            t0 = time.perf_counter()
+            O.step(h, W, E, em, mask, tok, C, p)
+            dt = time.perf_counter() - t0
+            if i >= n_warm:
+                times.append(dt)
+            if budget_s is not None and i >= n_warm and sum(times) > budget_s:
+                break
     return times, cores
+
+
+def bench_config(world: int, Vl: int, exchange: str, partition: str, weight_copies: int, shard_sim: int = 0):
+    """The `config` object of both arms (same keys, so the driver can match them)."""
+    G = shard_sim or world
+    step_bytes = Vl * H * 2 * (2 if CFG["smooth"] else 1)
+    if shard_sim:
+        par = f"one rank of a {shard_sim}-way vocab shard on one GPU (loopback record exchange; measurement)"
+    elif world > 1:
+        par = f"vocab-sharded x{world} (" + ("in-kernel peer-memory record exchange" if exchange == "p2p"
+                                              else "NCCL allgather") + ")"
+    else:
+        par = "single GPU"
+    return {"workload": WORKLOAD, "name": CFG["name"], "B": B, "S": S, "H": H, "V": V, "K": K,
+            "decoder": CFG["decoder"], "credit": CFG["credit"], "smooth": CFG["smooth"], "vocab_shards": G,
+            "V_local": Vl, "parallelism": par, "exchange": exchange, "partition": partition,
+            "l2": (f"no flush: every step reads weights the L2 does not hold ({step_bytes / 1e9:.2f} GB of W/E per "
+                   f"step per GPU, {weight_copies} weight cop{'y' if weight_copies == 1 else 'ies'} rotated, "
+                   f"vs 126 MB L2); K back-to-back block-start steps under one event pair")}
+
+
+def default_partition(no_balance: bool) -> str:
+    return ("calibrated for back-to-back steps (dinfer_balance, 4 steps)" if CFG["smooth"] and not no_balance
+            else "even")
+
+
+def weight_copies_for(shard_bytes: int, l2_bytes: int = 126 * 1024 * 1024) -> int:
+    """Copies of the weight shard rotated by the headline loop so that each
+    step reads bytes the L2 cannot hold: >= 3x the L2 in total."""
+    return max(1, min(4, math.ceil(3 * l2_bytes / max(1, shard_bytes))))
 
 
 def reference_arm(args):
@@ -181,13 +220,15 @@ def reference_arm(args):
     times, cores = oracle_run(args.steps, args.warmup, rows)
     sec = sum(times) / len(times)
     value = rows / sec
+    G = args.gpus
+    Vl = V // G
+    cfg = bench_config(G, Vl, "p2p" if G > 1 else "none", default_partition(args.no_balance),
+                       weight_copies_for(Vl * H * 2 * (2 if CFG["smooth"] else 1)))
+    cfg["oracle"] = "host cores (numpy fp64 oracle, whole vocabulary)"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "name": args.config, "B": B, "S": S, "H": H, "V": V, "K": K,
-                   "decoder": CFG["decoder"], "credit": CFG["credit"], "smooth": CFG["smooth"],
-                   "parallelism": "host cores (numpy fp64 oracle)"},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                          "sample": f"{rows} of {B * S} positions per step, full vocab {V}, fp64 numpy oracle step "
                                    f"({CFG['decoder']}, credit={CFG['credit']}, smoothing={CFG['smooth']})"},
@@ -202,11 +243,13 @@ def gpu_arm(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2510_08666_b200 import Context, build, get_unique_id, make_params, synth
+    from paper_2510_08666_b200 import Context, build, make_params, synth
 
     rank, world, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.shard_sim and world != 1:
+        raise SystemExit("--shard-sim is a single-GPU measurement")
     # BENCH_SAME_DEVICE=1 (test hook): every rank on cuda:0 with a gloo process
     # group, so the N > 1 code path can run on a one-GPU box (--exchange p2p)
     same_dev = os.environ.get("BENCH_SAME_DEVICE") == "1"
@@ -226,19 +269,26 @@ def gpu_arm(args):
     _d.lib()
 
     # ---- synthetic inputs: this rank's vocab shard of W and E
-    v0, v1 = synth.shard_range(V, rank, world)
+    G = args.shard_sim or world  # vocab shards
+    v0, v1 = synth.shard_range(V, rank, G)
     Vl = v1 - v0
     smooth, credit = CFG["smooth"], CFG["credit"]
     W_u16 = synth.make_W(V, H, 1, rows=(v0, v1))
-    Wfull_rows = synth.make_W(V, H, 1) if world > 1 else W_u16  # planted hidden needs W[target] rows
+    Wfull_rows = synth.make_W(V, H, 1) if G > 1 else W_u16  # planted hidden needs W[target] rows
     hid_u16 = synth.planted_hidden(Wfull_rows, B * S, seed=0)
     del Wfull_rows
 
     def dev_bf16(u):
         return torch.from_numpy(np.ascontiguousarray(u).view(np.int16)).view(torch.bfloat16).cuda()
 
-    Wd, hid = dev_bf16(W_u16), dev_bf16(hid_u16)
-    Ed = dev_bf16(synth.make_E(V, H, 2, rows=(v0, v1))) if smooth else None
+    hid = dev_bf16(hid_u16)
+    shard_bytes = Vl * H * 2 * (2 if smooth else 1)
+    R = weight_copies_for(shard_bytes, torch.cuda.get_device_properties(local).L2_cache_size)
+    Wd = [dev_bf16(W_u16)]
+    Ed = [dev_bf16(synth.make_E(V, H, 2, rows=(v0, v1)))] if smooth else [None]
+    for _ in range(R - 1):  # identical copies at other addresses (L2-cold rotation)
+        Wd.append(Wd[0].clone())
+        Ed.append(Ed[0].clone() if smooth else None)
     emd = dev_bf16(synth.make_E(V, H, 2, rows=(V - 1, V))[0]) if smooth else None
     del W_u16
 
@@ -247,12 +297,15 @@ def gpu_arm(args):
     if world > 1 and args.exchange != "p2p":  # the NCCL communicator (allgather / fallback)
         from paper_2510_08666_b200.dist import broadcast_unique_id
         nid = broadcast_unique_id("cpu" if same_dev else "cuda")
-    ctx = Context(B, S, H, K, V, V_local=Vl, v_offset=v0, world=world, rank=rank, stream=stream.cuda_stream,
+    ctx = Context(B, S, H, K, V, V_local=Vl, v_offset=v0, world=G, rank=rank, stream=stream.cuda_stream,
                   nccl_id=nid, smooth_capable=smooth)
     exchange = "none"
-    if world > 1:
+    if args.shard_sim:
+        ctx.exchange_loopback()
+        exchange = "loopback"
+    elif world > 1:
         # the product's exchange: records pushed into every rank's gather buffer by
-        # the record-finalize kernel over NVLink P2P (CUDA IPC handles shared via
+        # the producing kernel over NVLink P2P (CUDA IPC handles shared via
         # torch.distributed); the NCCL allgather stays as the fallback / --exchange nccl
         exchange = "nccl"
         if args.exchange in ("auto", "p2p"):
@@ -298,46 +351,59 @@ def gpu_arm(args):
     p_bs = make_params(decoder=CFG["decoder"], tau=0.9, theta_hi=0.92, theta_lo=0.62, use_credit=credit,
                        use_smooth=smooth, alpha_t=0.1, block_start=True, mask_id=V - 1)
 
-    def one_step():
-        ctx.step(hid, Wd, Ed, emd, mask, tokens, cids if credit else None, cval if credit else None, p, committed,
-                 smoothed, stats)
+    def one_step(c=0):
+        ctx.step(hid, Wd[c], Ed[c], emd, mask, tokens, cids if credit else None, cval if credit else None, p,
+                 committed, smoothed, stats)
 
-    def block_start_step():  # a block's first iteration: the state inputs are not read (params.block_start)
-        ctx.step(hid, Wd, Ed, emd, mask, tokens, cids if credit else None, cval if credit else None, p_bs,
+    def block_start_step(c=0):  # a block's first iteration: the state inputs are not read (params.block_start)
+        ctx.step(hid, Wd[c], Ed[c], emd, mask, tokens, cids if credit else None, cval if credit else None, p_bs,
                  committed, smoothed, stats)
 
     # calibrated vocab partition (K12): measured per-SM streaming rates -> slab split
     partition = "even"
-    # K12 pairs + splits (smoothing steps).  K1 slab calibration (stats-only
-    # contexts) measured no gain here, so stats-only configs run even slabs.
     if not args.no_balance and smooth:
         from paper_2510_08666_b200 import DInferError
         try:
-            ctx.balance(hid, Wd, Ed, emd, p, iters=4, mode="back_to_back")
-            partition = "calibrated for back-to-back steps (dinfer_balance, 4 steps)"
+            ctx.balance(hid, Wd[0], Ed[0], emd, p, iters=4, mode="back_to_back")
+            partition = default_partition(False)
         except DInferError:
             pass
     # warm-up: every kernel of every timed loop runs here first (CUDA loads
     # modules lazily on first launch: a first launch inside a timed loop would
     # be charged to it), the back-to-back sequence W times, then W flushed steps
-    for _ in range(args.warmup):
-        block_start_step()
+    for i in range(max(args.warmup, R)):
+        block_start_step(i % R)
     for _ in range(args.warmup):
         reset_and_flush()
         one_step()
     ctx.sync()
     torch.cuda.synchronize()
+    # the same back-to-back steps as one CUDA graph (R steps per replay)
+    graph = None
+    try:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            for c in range(R):
+                block_start_step(c)
+        for _ in range(2):
+            graph.replay()
+        torch.cuda.synchronize()
+    except Exception as e:  # noqa: BLE001 -- reported, not fatal
+        print(f"[bench] graph capture failed: {e}", file=sys.stderr)
+        graph = None
 
     # ---- timed region.
     # Loop A (headline): K back-to-back steps, each a block's first iteration
     # (params.block_start: all positions undecided, credit slots empty), bracketed
-    # by one event pair.  No L2 flush: each step streams 1.29 GB of W + E (> 126 MB L2).
+    # by one event pair, rotating over R weight copies (R x shard >= 3x L2).
     # Loop A2: the same K steps one at a time with L2 flushed before each
     # (outside the events): no overlap with the previous step.
+    # Loop A3: the steps replayed from one CUDA graph.
     # Loop B: as A with the library's per-kernel events on (these serialise the
     # PDL overlap between kernels, so B's per-kernel times are upper bounds)
     # and a stream sync per step to read them -> roofline per kernel.
     ea = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    eg = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     evb = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     phase_acc = {}
@@ -346,10 +412,11 @@ def gpu_arm(args):
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
     wall0 = time.perf_counter()
+    n_graph = 0
     with sampler:
         ea[0].record(stream)
         for i in range(args.steps):
-            block_start_step()
+            block_start_step(i % R)
         ea[1].record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - wall0
@@ -359,10 +426,19 @@ def gpu_arm(args):
             one_step()
             evs[i][1].record(stream)
         torch.cuda.synchronize()
+        if graph is not None:
+            reps = max(1, args.steps // R)
+            eg[0].record(stream)
+            with torch.cuda.stream(stream):
+                for _ in range(reps):
+                    graph.replay()
+            eg[1].record(stream)
+            n_graph = reps * R
+            torch.cuda.synchronize()
         ctx.set_timing(True)
         for i in range(args.steps):
             evb[i][0].record(stream)
-            block_start_step()
+            block_start_step(i % R)
             evb[i][1].record(stream)
             ph = ctx.get_timing()  # syncs the stream (outside the event pair)
             for k_, v_ in ph.items():
@@ -373,17 +449,18 @@ def gpu_arm(args):
         dist.barrier()
     ctx.sync()
     ms = ea[0].elapsed_time(ea[1]) / args.steps
+    ms_graph = eg[0].elapsed_time(eg[1]) / n_graph if n_graph else float("nan")
     step_ms = [a.elapsed_time(b) for a, b in evs]
     ms_fl = sum(step_ms) / len(step_ms)
     ms_b = sum(a.elapsed_time(b) for a, b in evb) / len(evb)
     phases = {k_: v_ / args.steps for k_, v_ in phase_acc.items()}
     if world > 1:
-        t = torch.tensor([ms, ms_fl, ms_b] + [phases[k_] for k_ in sorted(phases)], dtype=torch.float64,
+        t = torch.tensor([ms, ms_fl, ms_b, ms_graph] + [phases[k_] for k_ in sorted(phases)], dtype=torch.float64,
                          device="cpu" if same_dev else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, ms_fl, ms_b = float(t[0]), float(t[1]), float(t[2])
+        ms, ms_fl, ms_b, ms_graph = float(t[0]), float(t[1]), float(t[2]), float(t[3])
         for j, k_ in enumerate(sorted(phases)):
-            phases[k_] = float(t[3 + j])
+            phases[k_] = float(t[4 + j])
 
     # ---- e2e: the public host-buffer call (H2D of hidden + state, D2H of state + outputs)
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
@@ -401,14 +478,13 @@ def gpu_arm(args):
     e2e_steps = max(3, min(args.steps, 50))
     e2e_ms = []
     for i in range(args.warmup + e2e_steps):
-        # a new block each call (host state reset); no L2 flush: every step streams
-        # 1.29 GB of weights, ten times the L2
+        # a new block each call (host state reset)
         mask_h.fill_(1); tok_h.fill_(V - 1); cids_h.fill_(-1); cval_h.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         # the public host-buffer API: copies in, step, results back in host memory
         # (e1 follows the result copies on the stream), then the unpacking wait
-        ctx.step_host_async(hid_h, Wd, Ed, emd, mask_h, tok_h, cids_h if credit else None,
+        ctx.step_host_async(hid_h, Wd[i % R], Ed[i % R], emd, mask_h, tok_h, cids_h if credit else None,
                             cval_h if credit else None, p, com_h, sm_h, st_h)
         e1.record(stream)
         e1.synchronize()
@@ -449,30 +525,28 @@ def gpu_arm(args):
                     "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
                     "algorithmic_bytes_per_launch": dom_bytes, "ms_per_launch": dom_ms}
         cpu = None
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline and not args.shard_sim:
             rows = 8
             times, cores = oracle_run(100, 1, rows, budget_s=args.cpu_budget)
             sec = sum(times) / len(times)
+            times1, _ = oracle_run(100, 0, rows, budget_s=args.cpu_budget / 2, threads=1)
+            sec1 = sum(times1) / len(times1)
             cpu = {"value": rows / sec, "unit": UNIT, "cores": cores, "kind": "oracle",
                    "sample": f"{len(times)} oracle steps of {rows} of {B * S} positions (full vocab {V}, fp64 numpy; "
-                             f"{sum(times):.1f} s of CPU work)"}
+                             f"{sum(times):.1f} s of CPU work)",
+                   "one_thread": {"value": rows / sec1, "unit": UNIT, "cores": 1,
+                                  "sample": f"{len(times1)} oracle steps of {rows} positions, BLAS limited to 1 "
+                                            f"thread ({sum(times1):.1f} s)"}}
+        value = M / (ms * 1e-3)
         line = {
-            "metric": METRIC, "value": M / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "name": args.config, "B": B, "S": S, "H": H, "V": V, "K": K,
-                       "decoder": CFG["decoder"], "credit": credit, "smooth": smooth, "vocab_shards": world,
-                       "V_local": Vl,
-                       "parallelism": (f"vocab-sharded x{world} ("
-                                       + ("in-kernel peer-memory record exchange" if exchange == "p2p"
-                                          else "NCCL allgather") + ")") if world > 1 else "single GPU",
-                       "exchange": exchange, "partition": partition,
-                       "l2": f"no flush: inputs > L2 ({step_bytes / 1e9:.2f} GB of W/E streamed per step vs 126 MB L2); "
-                             "K back-to-back block-start steps under one event pair"},
+            "config": bench_config(world, Vl, exchange, partition, R, args.shard_sim),
             "e2e": {"value": M / (e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e, "api": "dinfer_step_host_async + dinfer_step_host_wait",
                     "timing": "per call: CUDA events around the call's copies + kernels on the ctx stream, "
-                              "host wait between calls, no L2 flush"},
+                              "host wait between calls"},
             "gpu_launches": launches * args.steps,
             "roofline": roof,
             "step_roofline": None if M > 256 else {"bytes": step_bytes, "achieved_gbs": step_bytes / (ms * 1e-3) / 1e9,
@@ -483,6 +557,10 @@ def gpu_arm(args):
                                    "per-step event pairs (no overlap with the previous step)",
                            "ms_per_step_min": min(step_ms), "ms_per_step_max": max(step_ms),
                            "ms_per_step_p10_p50_p90": [float(np.percentile(step_ms, q)) for q in (10, 50, 90)]},
+            "graph_replay": None if not n_graph else {
+                "ms_per_step": ms_graph, "value": M / (ms_graph * 1e-3),
+                "note": f"the back-to-back block-start steps captured once into a CUDA graph ({R} per graph), "
+                        f"{n_graph} steps replayed under one event pair"},
             "ms_per_step_with_kernel_events": ms_b,
             "geometry": geom,
             "clocks": sampler.report(),
@@ -509,6 +587,8 @@ def main():
     ap.add_argument("--no-balance", action="store_true", help="keep the even K12 vocab partition")
     ap.add_argument("--exchange", default="auto", choices=["auto", "p2p", "nccl"],
                     help="N>1 record exchange: peer memory (auto: if every rank can open it) or NCCL allgather")
+    ap.add_argument("--shard-sim", type=int, default=0, choices=[0, 2, 4, 8],
+                    help="measurement: one rank of a G-way vocab shard on one GPU (loopback exchange)")
     args = ap.parse_args()
     set_config(args.config)
     if args.warmup < 3:

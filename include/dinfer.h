@@ -252,6 +252,13 @@ dinfer_status dinfer_balance_reset(dinfer_ctx* ctx);
  * (no communicator needed).  Errors: ARG, UNSUPPORTED (world == 1), CUDA.  */
 dinfer_status dinfer_exchange_handle(dinfer_ctx* ctx, uint8_t out_handle[64]);
 dinfer_status dinfer_exchange_open(dinfer_ctx* ctx, const uint8_t* handles);
+/* Measurement only: one rank of a `world`-way vocab shard on ONE GPU.  Every
+ * "peer" is this ctx's own gather buffer and each step stores its record into
+ * all `world` slots and raises all `world` flags, so the step moves the bytes
+ * and runs the kernels of a real rank (minus the NVLink latency); the combined
+ * results are NOT meaningful (the G records are copies of one shard's).
+ * Errors: ARG (already open), UNSUPPORTED (world == 1), CUDA.               */
+dinfer_status dinfer_exchange_loopback(dinfer_ctx* ctx);
 
 /* The same host-buffer step split in two: _async validates, stages the small
  * state, enqueues copies + step + result copies on the ctx stream and returns;
@@ -273,7 +280,8 @@ dinfer_status dinfer_step_host_wait(dinfer_ctx* ctx);
  * dinfer_record_words: number of fp32 words of one rank's record:
  *   M*(4+K)  statistics: per row (m, v* as int32 bits (global id), l =
  *            sum_{v in shard} exp(f_v - m), 0, fcred[K] = raw logit of each
- *            credited token if this rank owns it else -inf)
+ *            credited token if this rank owns it else -inf), padded to a
+ *            multiple of 4 words (the acc part stays 16-byte aligned)
  *   + M*H    (use_smooth only) acc[s,:] = sum_{v in shard} exp(f_v - m) E[v,:].
  * dinfer_step_local writes this rank's record to `record` (device, that many
  * words).  dinfer_step_combine reads `records` = `world` records back to back

@@ -42,12 +42,14 @@
 //        CTA's own W epilogue, others after the group counter), and m_oth.
 //   7    helper: with warps 4-6, the second half of the final epilogue.
 // TMEM: 512 columns.  W-phase accumulators double-buffered at [0, 2N); E
-// set A at [0, nsub N), set B at [256, 256 + nsub N) (E MMAs start only after
-// the W epilogue has drained its accumulators).
+// set A at [0, nsub NE), set B at [256, 256 + nsub NE), NE = 2N when the hi /
+// lo P tiles are stacked into one MMA (b.stack), else N (E MMAs start only
+// after the W epilogue has drained its accumulators).
 #include <climits>
 
 #include "common.cuh"
 #include "kernels.h"
+#include "rank_fin.cuh"
 
 #include <cuda_bf16.h>
 
@@ -372,7 +374,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t idesc_w = idesc_bf16(kTileRows, N, false, false);
-      const uint32_t idesc_e = idesc_bf16(128, N, /*a MN-major*/ true, /*b K-major*/ false);
+      // E phase: with b.stack the hi and lo P tiles (rows [0, N) and [N, 2N) of
+      // one SW64 tile) are ONE B operand of 2N rows -- one MMA per k-step
+      // writes E.hi into columns [0, N) and E.lo into [N, 2N) of the sub-tile,
+      // so the E tile (A) is read from shared memory once instead of twice
+      const int NE = b.stack ? 2 * N : N;
+      const uint32_t idesc_e = idesc_bf16(128, NE, /*a MN-major*/ true, /*b K-major*/ false);
       int stage = 0;
       uint32_t phase = 0;
       for (int t = 0; t < ntiles; ++t) {
@@ -386,6 +393,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           if (tr != nullptr && t == 0 && kc0 == 0) tr[1] = globaltimer_ns();
           const uint32_t slot = smem_u32(ring + stage * L.wslot);
+          if (a.xbits & 16) {  // measurement only: release the stage without its MMAs
+            mbar_arrive(&empty[stage]);
+            advance(stage, phase, a.stages);
+            continue;
+          }
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             const uint32_t a_addr = slot + j * kChunkBytes;
@@ -416,6 +428,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (tr2 != nullptr && j == 0) tr2[1] = globaltimer_ns();
         const uint32_t e_addr = smem_u32(ring + es * L.eslot);
         const uint32_t phi = smem_u32(p_sm + ps * L.p_stage);
+        if (a.xbits & 32) {  // measurement only: release the stages without their MMAs
+          mbar_arrive(&eempty[es]);
+          mbar_arrive(&pempty[ps]);
+          advance(es, eph, static_cast<int>(L.estages));
+          advance(ps, pph, b.pstages);
+          continue;
+        }
 #pragma unroll
         for (int k = 0; k < KV / 16; ++k) {
           // B: P tile [N x 16 v] K-major SWIZZLE_64B (64-B rows, 8-row atoms of 512 B)
@@ -424,9 +443,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int sub = 0; sub < b.nsub; ++sub) {
             // A: [128 h x 16 v] = two 64-h boxes (LBO = box bytes), 8-v groups 1 KB apart (SBO)
             const uint64_t ad = sdesc_sw128(e_addr + sub * 2 * ebox + k * 16 * 128, ebox, 1024);
-            const uint32_t d = tmem_base + set + static_cast<uint32_t>(sub * N);
+            const uint32_t d = tmem_base + set + static_cast<uint32_t>(sub * NE);
             mma_bf16(d, ad, bhi, idesc_e, (first && k == 0) ? 0u : 1u);
-            mma_bf16(d, ad, blo, idesc_e, 1u);
+            if (!b.stack) mma_bf16(d, ad, blo, idesc_e, 1u);
           }
         }
         mma_commit(&eempty[es]);
@@ -727,21 +746,36 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int hbase = hs * b.HW;
     const uint64_t pol_part = policy_evict_last();  // kept in L2 for K34 (the weight streams are evict_first)
     const uint32_t lanebase = tmem_base + (static_cast<uint32_t>(wq * 32) << 16);
+    const int NE = b.stack ? 2 * N : N;
     for (int sub = sub0; sub < sub1; ++sub) {
       for (int g = 0; g < ng; ++g) {
         float x[32];
-        const uint32_t col = static_cast<uint32_t>(sub * N + g * 32);
+        const uint32_t col = static_cast<uint32_t>(sub * NE + g * 32);
         if (n_own > 0) {
-          tmem_ld32(lanebase + col, x);
+          if (b.stack) {  // E.hi + E.lo (columns col and col + N)
+            float y[32];
+            tmem_ld32x2(lanebase + col, lanebase + col + N, x, y);
 #pragma unroll
-          for (int jj = 0; jj < 32; ++jj) x[jj] *= scA[g * 32 + jj];
+            for (int jj = 0; jj < 32; ++jj) x[jj] = (x[jj] + y[jj]) * scA[g * 32 + jj];
+          } else {
+            tmem_ld32(lanebase + col, x);
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) x[jj] *= scA[g * 32 + jj];
+          }
         } else {
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) x[jj] = 0.f;
         }
         if (has_oth) {
           float y[32];
-          tmem_ld32(lanebase + kSetB + col, y);
+          if (b.stack) {
+            float z[32];
+            tmem_ld32x2(lanebase + kSetB + col, lanebase + kSetB + col + N, y, z);
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) y[jj] += z[jj];
+          } else {
+            tmem_ld32(lanebase + kSetB + col, y);
+          }
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) x[jj] = fmaf(y[jj], scB[g * 32 + jj], x[jj]);
         }
@@ -769,6 +803,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 5) tmem_dealloc(tmem_base, 512);
   if (a.wdur != nullptr && threadIdx.x == 0)  // whole-CTA duration (calibration objective)
     a.wdur[gridDim.x + blockIdx.x] = static_cast<unsigned>(globaltimer_ns() - t_start);
+  // the rank record (statistics + smoothing accumulator) merged across the
+  // grid and, with peers, pushed into every rank's gather buffer (rank_fin.cuh)
+  if (b.rank_fin) rank_finalize(b.rf, b.gbar, reinterpret_cast<float*>(ring));
   if (tr != nullptr && threadIdx.x == 0) {
     tr[3] = globaltimer_ns();
     if (tr2 != nullptr) {

@@ -321,15 +321,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 // group maxima (identical to the merged m: the groups tile the shard).
 // Store one record word (or float4) locally and, with the peer exchange, into
 // every rank's gather buffer (NVLink P2P stores).
+DI long rec_slot(const RecArgs& a, int j, unsigned par) {  // loopback: see rank_fin.cuh
+  return (static_cast<long>(par) * a.world + (a.loopback ? j : a.rank)) * a.rec_words;
+}
 DI void rec_put(const RecArgs& a, long word, float v, unsigned par) {
   if (a.peers == nullptr) return;
-  const long off = (static_cast<long>(par) * a.world + a.rank) * a.rec_words + word;
-  for (int j = 0; j < a.world; ++j) a.peers[j][off] = v;
+  for (int j = 0; j < a.world; ++j) a.peers[j][rec_slot(a, j, par) + word] = v;
 }
 DI void rec_put4(const RecArgs& a, long word, float4 v, unsigned par) {
   if (a.peers == nullptr) return;
-  const long off = (static_cast<long>(par) * a.world + a.rank) * a.rec_words + word;
-  for (int j = 0; j < a.world; ++j) *reinterpret_cast<float4*>(a.peers[j] + off) = v;
+  for (int j = 0; j < a.world; ++j) *reinterpret_cast<float4*>(a.peers[j] + rec_slot(a, j, par) + word) = v;
 }
 
 __global__ void rec_finalize_kernel(const RecArgs a) {
@@ -408,7 +409,7 @@ __global__ void rec_finalize_kernel(const RecArgs a) {
       a.ctl[1] = 0u;
       __threadfence_system();
       for (int j = 0; j < a.world; ++j) {
-        unsigned* f = reinterpret_cast<unsigned*>(a.peers[j] + a.flags_off) + par * a.world + a.rank;
+        unsigned* f = reinterpret_cast<unsigned*>(a.peers[j] + a.flags_off) + par * a.world + (a.loopback ? j : a.rank);
         asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch + 1u) : "memory");
       }
     }

@@ -78,7 +78,8 @@ struct K1Args {
   int block_start;         // params.block_start: mask / credit inputs not read (all undecided, slots empty)
   int npre;                // K12: W stages issued before the dependency wait (0 = the whole ring; tuning)
   int xbits;               // K12 measurement-only experiments (env DINFER_K12_X; 0 in the product):
-                           //   1 no hidden loads, 2 no flog stores, 4 W evict_normal, 8 E evict_normal
+                           //   1 no hidden loads, 2 no flog stores, 4 W evict_normal, 8 E evict_normal,
+                           //   16 W stages released without MMAs, 32 E stages released without MMAs
 };
 size_t k1_smem_bytes(int N, int H, int stages, int h_resident, int slab_rows_max);
 cudaError_t launch_k1(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
@@ -94,40 +95,6 @@ struct K1bArgs {
 size_t k1b_smem_bytes(int stages);
 cudaError_t launch_k1b(const CUtensorMap& map_h, const CUtensorMap& map_w, const K1bArgs& a, int grid, size_t smem,
                        cudaStream_t st, bool pdl);
-
-// ---------------------------------------------------------------- K2
-struct K2Args {
-  int M, N, H, V_local;
-  int HW, nsub;            // hidden columns per CTA (128 .. 1024), HW/128
-  int KV;                  // vocab rows per chunk: 64 (P tile SW128) or 32 (SW64, for HW = 1024)
-  int HS, VG;              // H/HW slices, vocab groups
-  int nchunks;             // ceil(V_local / KV)
-  int stages, pstages;
-  const float* flog;       // [M][V_local]
-  const float4* part1;     // K1 partials [M][grid1]
-  int grid1, SPG;          // K1 slabs, slabs per vocab group
-  unsigned* grp_cnt;       // [VG] K1 slabs done per group
-  unsigned* grp_pass;      // [VG] K2 CTAs past the wait (the last resets both)
-  float* mref;             // [VG][M] out: per-group reference max m_g (acc is relative to it)
-  uint16_t* part;          // [VG][M][H] fp16 (common.cuh: pack_half4)
-  unsigned long long* trace;  // optional [grid][5]: globaltimer ns start, first E stage, MMAs done, exit; smid
-  volatile int* probe;     // K12 diagnostics (env DINFER_K12_PROBE): [grid][8] progress words in mapped host memory
-};
-size_t k2_smem_bytes(int N, int HW, int KV, int stages, int pstages);
-cudaError_t launch_k2(const CUtensorMap& map_e, const CUtensorMap& map_f, const K2Args& a, size_t smem,
-                      cudaStream_t st, bool pdl);
-
-// ---------------------------------------------------------------- K12 (K1 + K2 fused, N <= 64)
-// Uses K1Args (W phase; VG x SPG slabs at 16-row chunk granularity,
-// nchunks / chunk_rows in 16-row chunks) and K2Args (E phase; HS == SPG
-// hidden slices of HW columns, pstages logits / P ring depth; stages unused).
-size_t k12_smem_bytes(int N, int HW, int stages, int pstages, int slab_rows_max);
-// Co-resident K12 CTAs per SM at this shared-memory size (K12 CTAs of a vocab
-// group wait for each other's W phase, so the whole grid must be resident).
-int k12_blocks_per_sm(size_t smem);
-cudaError_t launch_k12(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
-                       const CUtensorMap& map_e, const CUtensorMap& map_f, const K1Args& a, const K2Args& b, int grid,
-                       size_t smem, cudaStream_t st, bool pdl);
 
 // Rank record finalize (sharded / split-phase path):
 //   stats: rec[s] = merge of K1's per-slab partials (fixed order);
@@ -148,7 +115,50 @@ struct RecArgs {
   long flags_off;          // word offset of the flags [2][world] in a gather buffer
   unsigned* ctl;           // local control words: [0] epoch, [1] finished blocks of this kernel
   int K;                   // credit slots (fcred words per stats row, copied from `rec`)
+  int loopback;            // measurement: peers are this GPU's own buffer, all `world` slots written
 };
+
+// ---------------------------------------------------------------- K2
+struct K2Args {
+  int M, N, H, V_local;
+  int HW, nsub;            // hidden columns per CTA (128 .. 1024), HW/128
+  int KV;                  // vocab rows per chunk: 64 (P tile SW128) or 32 (SW64, for HW = 1024)
+  int HS, VG;              // H/HW slices, vocab groups
+  int nchunks;             // ceil(V_local / KV)
+  int stages, pstages;
+  const float* flog;       // [M][V_local]
+  const float4* part1;     // K1 partials [M][grid1]
+  int grid1, SPG;          // K1 slabs, slabs per vocab group
+  unsigned* grp_cnt;       // [VG] K1 slabs done per group
+  unsigned* grp_pass;      // [VG] K2 CTAs past the wait (the last resets both)
+  float* mref;             // [VG][M] out: per-group reference max m_g (acc is relative to it)
+  uint16_t* part;          // [VG][M][H] fp16 (common.cuh: pack_half4)
+  unsigned long long* trace;  // optional [grid][5]: globaltimer ns start, first E stage, MMAs done, exit; smid
+  volatile int* probe;     // K12 diagnostics (env DINFER_K12_PROBE): [grid][8] progress words in mapped host memory
+  // K12 only: the rank-record finalize folded into the kernel's tail
+  // (rank_fin.cuh; grid barrier on gbar[0..1], then every CTA merges a slice
+  // of the record and, with peers, pushes it into every rank's gather buffer)
+  int stack;               // K12: hi / lo P tiles stacked into one 2N-column MMA (TMEM nsub x 2N per set)
+  int rank_fin;
+  unsigned* gbar;
+  RecArgs rf;
+};
+size_t k2_smem_bytes(int N, int HW, int KV, int stages, int pstages);
+cudaError_t launch_k2(const CUtensorMap& map_e, const CUtensorMap& map_f, const K2Args& a, size_t smem,
+                      cudaStream_t st, bool pdl);
+
+// ---------------------------------------------------------------- K12 (K1 + K2 fused, N <= 64)
+// Uses K1Args (W phase; VG x SPG slabs at 16-row chunk granularity,
+// nchunks / chunk_rows in 16-row chunks) and K2Args (E phase; HS == SPG
+// hidden slices of HW columns, pstages logits / P ring depth; stages unused).
+size_t k12_smem_bytes(int N, int HW, int stages, int pstages, int slab_rows_max);
+// Co-resident K12 CTAs per SM at this shared-memory size (K12 CTAs of a vocab
+// group wait for each other's W phase, so the whole grid must be resident).
+int k12_blocks_per_sm(size_t smem);
+cudaError_t launch_k12(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
+                       const CUtensorMap& map_e, const CUtensorMap& map_f, const K1Args& a, const K2Args& b, int grid,
+                       size_t smem, cudaStream_t st, bool pdl);
+
 cudaError_t launch_rec_finalize(const RecArgs& a, cudaStream_t st, bool pdl);
 
 // ---------------------------------------------------------------- K3

@@ -112,6 +112,7 @@ def lib():
         "dinfer_balance_reset": (S, [P]),
         "dinfer_exchange_handle": (S, [P, P]),
         "dinfer_exchange_open": (S, [P, P]),
+        "dinfer_exchange_loopback": (S, [P]),
         "dinfer_kv_create": (S, [POINTER(KvShape), P, POINTER(c_void_p)]),
         "dinfer_kv_destroy": (None, [P]),
         "dinfer_kv_region": (S, [POINTER(KvShape), S, S, S, S, POINTER(c_int32), POINTER(c_int32)]),
@@ -273,6 +274,11 @@ class Context:
         then exchanges the records over peer memory instead of NCCL."""
         buf = (ctypes.c_uint8 * len(handles)).from_buffer_copy(handles)
         _check(lib().dinfer_exchange_open(self._h, buf), "dinfer_exchange_open")
+
+    def exchange_loopback(self):
+        """Measurement only: run as one rank of a `world`-way shard on one GPU
+        (records stored into all of this GPU's own slots; results not meaningful)."""
+        _check(lib().dinfer_exchange_loopback(self._h), "dinfer_exchange_loopback")
 
     def step_embed(self, hidden, W, E, e_mask, mask, tokens, credit_ids, credit_val, params: Params, committed,
                    smoothed, stats, emb):

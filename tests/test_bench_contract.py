@@ -68,3 +68,30 @@ def test_gpu_arm_two_ranks_one_device(config, exchange):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["vocab_shards"] == 2 and d["config"]["exchange"] == exchange
     assert d["value"] > 0 and d["e2e"]["value"] > 0
+
+
+@pytest.mark.gpu
+def test_gpu_arm_shard_sim():
+    """--shard-sim 8: one rank of the 8-way LLaDA-MoE vocab shard on one GPU
+    (loopback record exchange), rotating weight copies so each step reads
+    bytes the L2 does not hold."""
+    d = run_bench("--config", "moe", "--shard-sim", "8", "--steps", "5", "--warmup", "3", "--no-cpu-baseline")
+    c = d["config"]
+    assert c["vocab_shards"] == 8 and c["V_local"] == 157184 // 8 and c["exchange"] == "loopback"
+    assert "3 weight copies" in c["l2"]
+    assert d["value"] > 0 and d["roofline"]["frac"] > 0
+    assert d["graph_replay"]["ms_per_step"] > 0
+
+
+def test_reference_config_keys_match_gpu_arm():
+    """Both arms build `config` with the same function (bench.bench_config), so
+    the driver sees the same keys; the reference arm adds only `oracle`."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    b.set_config("moe")
+    g = b.bench_config(1, 157184, "none", b.default_partition(False), 1)
+    d = run_bench("--impl", "reference", "--steps", "1", "--warmup", "3")
+    assert set(d["config"]) - {"oracle"} == set(g)
+    assert {k: d["config"][k] for k in g} == g

@@ -203,6 +203,7 @@ def test_balanced_partition_matches_oracle(torch_cuda, monkeypatch, mode, groups
     with a skewed split, and with resized vocab groups (DINFER_BALANCE_GROUPS=1).
     An unknown mode is rejected."""
     monkeypatch.setenv("DINFER_BALANCE_GROUPS", groups)
+    monkeypatch.setenv("DINFER_K12_STACK", "0")  # the two-slab geometry dinfer_balance calibrates
     from paper_2510_08666_b200 import Context
     V, H, B, S, K = 32768, 2048, 1, 32, 32
     W, E = weights(V, H)

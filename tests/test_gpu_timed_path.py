@@ -92,7 +92,11 @@ def test_headline_loop_block_start_calibrated(moe):
     ctx = Context(B, S, H, K, V)
     assert ctx.geometry()["fused"] == 1  # K12, the kernel the bench's roofline names
     gp = gpu_params(moe["p"])
-    ctx.balance(d["h"], d["W"], d["E"], d["em"], gp, iters=4, mode="back_to_back")
+    from paper_2510_08666_b200 import DInferError
+    try:  # bench.py calibrates when the geometry supports it (two slabs per vocab group)
+        ctx.balance(d["h"], d["W"], d["E"], d["em"], gp, iters=4, mode="back_to_back")
+    except DInferError as e:
+        assert e.status == 6 and ctx.geometry()["k2_hw"] * 2 != H  # UNSUPPORTED only for HS != 2
     pbs = gpu_params(moe["p"])
     pbs.block_start, pbs.mask_id = 1, synth.mask_id(V)
     st = GpuState(B, S, H, K, synth.mask_id(V))
