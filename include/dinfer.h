@@ -387,8 +387,8 @@ dinfer_status dinfer_generate(dinfer_ctx* ctx, const dinfer_gen_config* cfg, con
  *            region's queries (q = bf16(x Wq^T)) over all L cached positions,
  *            per head softmax(q k^T / sqrt(d_head)) v; other rows untouched
  *   lo_hi    optional HOST int32[2] receiving the region.
- * The projections run on cuBLAS (plain GEMMs); the attention on this
- * library's kernels.  Errors: ARG (null / bad block), SHAPE (alignment).    */
+ * The projections and the attention both run on this library's tcgen05
+ * kernels.  Errors: ARG (null / bad block), SHAPE (alignment).             */
 typedef struct dinfer_kv dinfer_kv;
 typedef struct {
   int32_t L, H, d_head;

@@ -17,17 +17,6 @@ LIB = os.path.join(PKG, "libdinfer.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
-def cublas_paths():
-    """The cuBLAS torch loads (nvidia-cublas wheel), so the process has one copy."""
-    import importlib.util
-    spec = importlib.util.find_spec("nvidia")
-    for base in (spec.submodule_search_locations or []) if spec else []:
-        inc, lib = os.path.join(base, "cublas", "include"), os.path.join(base, "cublas", "lib")
-        if os.path.exists(os.path.join(inc, "cublas_v2.h")) and os.path.exists(os.path.join(lib, "libcublas.so.12")):
-            return inc, lib
-    return "/usr/local/cuda/include", "/usr/local/cuda/lib64"
-
-
 def nccl_paths():
     import importlib.util
     spec = importlib.util.find_spec("nvidia")
@@ -57,7 +46,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     inc, lib = nccl_paths()
     cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
-           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(PKG, "csrc"), "-I", cublas_paths()[0]]
+           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(PKG, "csrc")]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     if inc:
@@ -68,8 +57,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd += ["-o", tmp]
     if lib:
         cmd += ["-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib]
-    binc, blib = cublas_paths()
-    cmd += ["-L", blib, "-l:libcublas.so.12", "-Xlinker", "-rpath=" + blib]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

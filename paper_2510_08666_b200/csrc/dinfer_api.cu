@@ -104,6 +104,7 @@ struct dinfer_ctx {
   int k12_npre = 0;           // env DINFER_K12_NPRE: W stages issued before the dependency wait (0 = ring)
   int k12_x = 0;              // env DINFER_K12_X: measurement-only K12 experiments (kernels.h K1Args::xbits)
   int k12_stack = 0;          // K12 E phase: hi / lo P stacked into one MMA (K2Args::stack)
+  int k12_emin = 2;           // K12 E-ring depth the smem layout is sized for (K2Args::emin)
   bool rankfin_ok = false;    // K12 can fold the record finalize (rank_fin.cuh: <= 8 rows per CTA slice)
   bool rankfin_g1 = false;    // world 1 also takes the record path (env DINFER_RANKFIN_G1; measurement)
   unsigned* gbar = nullptr;   // K12 grid barrier words [count, generation]
@@ -436,6 +437,7 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
     b.part = c->part2;
     b.trace = c->trace == nullptr ? nullptr : c->trace + 5 * c->k1_grid;
     b.stack = c->k12_stack;
+    b.emin = c->k12_emin;
     if (fold) {
       b.rank_fin = 1;
       b.gbar = c->gbar;
@@ -740,7 +742,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
       // the TMEM), HS = H/HW slabs per vocab group, VG groups of 16-row chunks.
       // Stacked hi / lo P (one 2N-column MMA per k-step, DINFER_K12_STACK=0 to
       // disable) needs HW/128 x 2N columns per accumulator set.
-      int stack = 1;
+      int stack = 0;  // measured no faster (HW 512 geometry slower); kept as a measurement knob
       if (const char* e = std::getenv("DINFER_K12_STACK")) stack = std::atoi(e) != 0;
       int hw = 0;
       for (int w = 1024; w >= 128 && hw == 0; w /= 2)
@@ -767,22 +769,26 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
         int st_max = 4, pst_max = 4;  // tuning overrides (measurement only)
         if (const char* e = std::getenv("DINFER_K12_STAGES")) st_max = std::max(3, std::atoi(e));
         if (const char* e = std::getenv("DINFER_K12_PSTAGES")) pst_max = std::max(2, std::atoi(e));
-        auto fit = [&](int rows, int* fst, int* fpst) {
-          *fst = *fpst = 0;
-          for (int st = st_max; st >= 3 && *fst == 0; --st)
-            for (int pst = pst_max; pst >= 2; --pst)
-              if (k12_smem_bytes(c->N, hw, st, pst, rows) <= c->smem_optin) {
-                *fst = st;
-                *fpst = pst;
-                break;
-              }
+        int emin = 3;  // E-ring depth target (DINFER_K12_ESTAGES); 2 if it does not fit
+        if (const char* e = std::getenv("DINFER_K12_ESTAGES")) emin = std::max(2, std::atoi(e));
+        auto fit = [&](int rows, int* fst, int* fpst, int* fem) {
+          *fst = *fpst = *fem = 0;
+          for (int em = emin; em >= 2 && *fst == 0; --em)
+            for (int st = st_max; st >= 3 && *fst == 0; --st)
+              for (int pst = pst_max; pst >= 2; --pst)
+                if (k12_smem_bytes(c->N, hw, st, pst, rows, em) <= c->smem_optin) {
+                  *fem = em;
+                  *fst = st;
+                  *fpst = pst;
+                  break;
+                }
         };
-        fit(srm, &c->f_stages, &c->f_pstages);
+        fit(srm, &c->f_stages, &c->f_pstages, &c->k12_emin);
         if (HS == 2) {  // room for calibrated groups up to 1.15x the largest even group, if it costs no stage
           const int big = kChunkRows12 * ((srm / kChunkRows12) * 115 / 100);
-          int bst = 0, bpst = 0;
-          fit(big, &bst, &bpst);
-          if (bst == c->f_stages && bpst == c->f_pstages && bst > 0) srm = big;
+          int bst = 0, bpst = 0, bem = 0;
+          fit(big, &bst, &bpst, &bem);
+          if (bst == c->f_stages && bpst == c->f_pstages && bem == c->k12_emin && bst > 0) srm = big;
           c->grp_cap_chunks = srm / kChunkRows12;
         }
         // K12's CTAs of a vocab group wait for each other (group counters): the
@@ -791,7 +797,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
         // per SM admits), use K1 -> K2 instead, whose cross-CTA waits only go
         // from the later kernel to the earlier.
         if (c->f_stages > 0 &&
-            static_cast<long>(k12_blocks_per_sm(k12_smem_bytes(c->N, hw, c->f_stages, c->f_pstages, srm))) *
+            static_cast<long>(k12_blocks_per_sm(k12_smem_bytes(c->N, hw, c->f_stages, c->f_pstages, srm, c->k12_emin))) *
                     c->num_sms < static_cast<long>(VG) * HS)
           c->f_stages = 0;
         if (c->f_stages > 0) {
@@ -803,7 +809,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
           c->k2_nchunks = nch;
           c->k2_stages = c->f_stages;
           c->k2_pstages = c->f_pstages;
-          c->f_smem = k12_smem_bytes(c->N, hw, c->f_stages, c->f_pstages, srm);
+          c->f_smem = k12_smem_bytes(c->N, hw, c->f_stages, c->f_pstages, srm, c->k12_emin);
           c->slab_rows_max = srm;
         }
       }
@@ -880,14 +886,14 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
     if (c->k1_stages == 0) { delete c; return DINFER_ERR_UNSUPPORTED; }
     c->k1_smem = k1_smem_bytes(c->N, s.H, c->k1_stages, c->k1_hres, c->slab_rows_max);
     if (c->fused) {  // the head table covers the larger of the K1 / K12 slabs
-      while (k12_smem_bytes(c->N, c->k2_HW, c->f_stages, c->f_pstages, c->slab_rows_max) > c->smem_optin) {
+      while (k12_smem_bytes(c->N, c->k2_HW, c->f_stages, c->f_pstages, c->slab_rows_max, c->k12_emin) > c->smem_optin) {
         if (c->f_pstages > 2) --c->f_pstages;
         else if (c->f_stages > 3) --c->f_stages;
         else { delete c; return DINFER_ERR_UNSUPPORTED; }
       }
       c->k2_stages = c->f_stages;
       c->k2_pstages = c->f_pstages;
-      c->f_smem = k12_smem_bytes(c->N, c->k2_HW, c->f_stages, c->f_pstages, c->slab_rows_max);
+      c->f_smem = k12_smem_bytes(c->N, c->k2_HW, c->f_stages, c->f_pstages, c->slab_rows_max, c->k12_emin);
     }
 
     if (const char* e = std::getenv("DINFER_PDL")) c->pdl = std::atoi(e) != 0;

@@ -69,11 +69,14 @@ struct Layout {
       m_off, red_off, total;
 };
 
-__host__ __device__ inline Layout make_layout(int N, int HW, int stages, int pstages, int slab_rows_max) {
+__host__ __device__ inline Layout make_layout(int N, int HW, int stages, int pstages, int slab_rows_max, int emin) {
   Layout L;
   L.wslot = (kWBytes + 2u * static_cast<uint32_t>(N) * 128u + 1023u) & ~1023u;  // W + two hidden chunks
   L.eslot = static_cast<uint32_t>(HW) * kChunkRows12 * 2u;                        // [HW h x 32 v] bf16
-  const uint32_t ring = static_cast<uint32_t>(stages) * L.wslot;
+  // the ring holds `stages` W slots and at least `emin` E slots (E slots past
+  // the W slots' bytes start without waiting for the W phase)
+  uint32_t ring = static_cast<uint32_t>(stages) * L.wslot;
+  if (ring < static_cast<uint32_t>(emin) * L.eslot) ring = static_cast<uint32_t>(emin) * L.eslot;
   L.estages = ring / L.eslot;
   if (L.estages > 6u) L.estages = 6u;
   L.ring_off = 0;
@@ -182,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const __grid_constant__ CUtensorMap map_f, const K1Args a, const K2Args b) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const Layout L = make_layout(a.N, b.HW, a.stages, b.pstages, a.slab_rows_max);
+  const Layout L = make_layout(a.N, b.HW, a.stages, b.pstages, a.slab_rows_max, b.emin);
   if (L.estages < 2u) __trap();  // host geometry guarantees >= 2 E stages
   const int warp = threadIdx.x / kWarpThreads;
   const int lane = threadIdx.x % kWarpThreads;
@@ -805,20 +808,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     a.wdur[gridDim.x + blockIdx.x] = static_cast<unsigned>(globaltimer_ns() - t_start);
   // the rank record (statistics + smoothing accumulator) merged across the
   // grid and, with peers, pushed into every rank's gather buffer (rank_fin.cuh)
-  if (b.rank_fin) rank_finalize(b.rf, b.gbar, reinterpret_cast<float*>(ring));
-  if (tr != nullptr && threadIdx.x == 0) {
-    tr[3] = globaltimer_ns();
-    if (tr2 != nullptr) {
-      tr2[0] = tr[2];
-      tr2[3] = tr[3];
-    }
+  // trace: K2-slot exit = end of the partial write-out, K1-slot exit = kernel exit
+  if (tr2 != nullptr && threadIdx.x == 0) {
+    tr2[0] = tr[2];
+    tr2[3] = globaltimer_ns();
   }
+  if (b.rank_fin) rank_finalize(b.rf, b.gbar, reinterpret_cast<float*>(ring));
+  if (tr != nullptr && threadIdx.x == 0) tr[3] = globaltimer_ns();
 }
 
 }  // namespace
 
-size_t k12_smem_bytes(int N, int HW, int stages, int pstages, int slab_rows_max) {
-  const Layout L = make_layout(N, HW, stages, pstages, slab_rows_max);
+size_t k12_smem_bytes(int N, int HW, int stages, int pstages, int slab_rows_max, int emin) {
+  const Layout L = make_layout(N, HW, stages, pstages, slab_rows_max, emin);
   if (L.estages < 2u) return ~size_t(0) >> 1;  // the E ring needs >= 2 slots: never fits
   return L.total + 1024;
 }

@@ -139,6 +139,7 @@ struct K2Args {
   // (rank_fin.cuh; grid barrier on gbar[0..1], then every CTA merges a slice
   // of the record and, with peers, pushes it into every rank's gather buffer)
   int stack;               // K12: hi / lo P tiles stacked into one 2N-column MMA (TMEM nsub x 2N per set)
+  int emin;                // K12: minimum E-ring depth (the ring is sized for it)
   int rank_fin;
   unsigned* gbar;
   RecArgs rf;
@@ -151,7 +152,7 @@ cudaError_t launch_k2(const CUtensorMap& map_e, const CUtensorMap& map_f, const 
 // Uses K1Args (W phase; VG x SPG slabs at 16-row chunk granularity,
 // nchunks / chunk_rows in 16-row chunks) and K2Args (E phase; HS == SPG
 // hidden slices of HW columns, pstages logits / P ring depth; stages unused).
-size_t k12_smem_bytes(int N, int HW, int stages, int pstages, int slab_rows_max);
+size_t k12_smem_bytes(int N, int HW, int stages, int pstages, int slab_rows_max, int emin = 0);
 // Co-resident K12 CTAs per SM at this shared-memory size (K12 CTAs of a vocab
 // group wait for each other's W phase, so the whole grid must be resident).
 int k12_blocks_per_sm(size_t smem);

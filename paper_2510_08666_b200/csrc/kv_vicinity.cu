@@ -12,15 +12,16 @@
 //   queries Q = bf16(X[lo:hi] Wq^T) (the region is the forward's query region);
 //   attention  out[lo:hi] = per head softmax(Q K^T / sqrt(d)) V over all L
 //           cached positions (bidirectional, no mask).
-// The three projections are plain GEMMs (cuBLAS, bf16 in, fp32 accumulate,
-// bf16 out straight into the cache rows).  The attention is a hand-written
-// split-key flash kernel: CTA = (head, 16-query tile, key split), 64-key
-// tiles staged in shared memory as fp32, online softmax in base 2, per-split
-// (m, l, O) partials merged by a second kernel in a fixed order.  At the
-// steady-state region (block 32 + 2 x 16 looks = 64 queries) the layer is
-// bound by the weight (3 H^2 bf16) and cache (2 L H bf16) reads; the
-// attention's 64 x L x H x 4 flop run on CUDA cores.
-#include <cublas_v2.h>
+// All of it runs on this file's kernels:
+//   kv_proj_tc        the three projections on tcgen05 (swap-AB tiles, K split
+//                     over a thread-block cluster, DSMEM reduction, bf16 rows
+//                     straight into the cache / Q buffer);
+//   kv_attention_tc   S = Q K^T and O = P V as tcgen05 UMMA chains per (head,
+//                     128-query tile, 256-key tile), softmax from TMEM;
+//   kv_attention_merge  the per-key-tile (m, l, O) partials in index order.
+// The CUDA-core split-key attention (kv_attention) stays behind DINFER_KV_TC=0.
+// At the steady-state region (block 32 + 2 x 16 looks = 64 queries) the layer
+// is bound by the weight (3 H^2 bf16) and cache (2 L H bf16) reads.
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
@@ -392,19 +393,178 @@ __global__ void __launch_bounds__(128, 1)
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
-// Pointer arrays of the three projections (one batched GEMM).
-__global__ void kv_set_ptrs(const void** d, const void* a0, const void* a1, const void* a2, const void* b0,
-                            void* c0, void* c1, void* c2) {
-  if (threadIdx.x != 0) return;
-  d[0] = a0;
-  d[1] = a1;
-  d[2] = a2;
-  d[3] = b0;
-  d[4] = b0;
-  d[5] = b0;
-  d[6] = c0;
-  d[7] = c1;
-  d[8] = c2;
+// ---------------------------------------------------------------------------
+// K.Update + queries on tcgen05 (`kv_proj_tc`): Y_m[p, :] = bf16(X[p, :] W_m^T)
+// for the three projections m = K, V, Q over the refresh region's positions.
+// Swap-AB tiles: D[128 output features x NT positions] = W_m[f-tile, :] X[p-tile, :]^T,
+// both operands K-major SW128 straight from the row-major weights / layer
+// input (TMA boxes [128 | NT rows x 64 k]), fp32 accumulator in TMEM.  At the
+// steady-state region (64 positions) the 3 H^2 weights are the only real
+// traffic (HBM-bound, AI = 64 flop/B), so the H-deep contraction is split
+// over a thread-block cluster of `ks` CTAs along K (grid = 3 H/128 tiles x ks
+// ~ one CTA per SM); the partial accumulators are reduced in the leader CTA
+// through distributed shared memory in rank order (deterministic), and the
+// leader writes bf16 rows of 16-B chunks into the cache / Q buffer.
+// ---------------------------------------------------------------------------
+constexpr int kPjStages = 4;
+constexpr uint32_t kPjWBox = 128u * 128u;  // [128 rows x 64 k] bf16
+
+struct ProjArgs {
+  int H, R, lo, NT, nkc, ks;
+  uint16_t* dst[3];   // row p of projection m at dst[m] + (p - dst_row0[m]) * H
+  int dst_row0[3];
+};
+
+__host__ __device__ inline size_t kv_proj_smem(int NT) {
+  return static_cast<size_t>(kPjStages) * (kPjWBox + static_cast<uint32_t>(NT) * 128u) + 2 * kPjStages * 8 + 64 +
+         1024;
+}
+
+DI uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+DI void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 16 B of CTA `rank`'s shared memory at this CTA's address `local_addr`
+// (distributed shared memory); no completion wait, so several can be in flight.
+DI float4 ld_dsmem_v4(const void* local_addr, uint32_t rank) {
+  uint32_t a = smem_u32(local_addr), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(r));
+  return v;
+}
+
+__global__ void __launch_bounds__(128, 1)
+    kv_proj_tc(const __grid_constant__ CUtensorMap map_w0, const __grid_constant__ CUtensorMap map_w1,
+               const __grid_constant__ CUtensorMap map_w2, const __grid_constant__ CUtensorMap map_x, const ProjArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t xbox = static_cast<uint32_t>(a.NT) * 128u;
+  const uint32_t slot = kPjWBox + xbox;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPjStages * slot);
+  uint64_t* empty = full + kPjStages;
+  uint64_t* done = empty + kPjStages;
+  uint32_t* misc = reinterpret_cast<uint32_t*>(done + 1);
+  const int ftiles = a.H / 128;
+  const int m = blockIdx.x / ftiles, ft = blockIdx.x - m * ftiles;
+  const int p0 = a.lo + blockIdx.y * a.NT;
+  const int z = static_cast<int>(blockIdx.z);
+  const int kc0 = z * a.nkc / a.ks, kc1 = (z + 1) * a.nkc / a.ks;
+  const CUtensorMap* mw = (m == 0) ? &map_w0 : (m == 1) ? &map_w1 : &map_w2;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    prefetch_tmap(mw);
+    prefetch_tmap(&map_x);
+    for (int i = 0; i < kPjStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(&misc[0], 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = misc[0];
+  if (threadIdx.x == 0) {  // TMA producer
+    const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
+    for (int kc = kc0, i = 0; kc < kc1; ++kc, ++i) {
+      const int st = i % kPjStages;
+      if (i >= kPjStages) mbar_wait(&empty[st], static_cast<uint32_t>((i / kPjStages - 1) & 1));
+      uint8_t* sl = smem + st * slot;
+      mbar_expect_tx(&full[st], slot);
+      tma_load_2d(sl, mw, &full[st], kc * 64, ft * 128, pol_w);
+      tma_load_2d(sl + kPjWBox, &map_x, &full[st], kc * 64, p0, pol_x);  // rows past L: zero fill
+    }
+  } else if (threadIdx.x == 32) {  // MMA issuer
+    const uint32_t idesc = idesc_bf16(128, a.NT, false, false);
+    for (int kc = kc0, i = 0; kc < kc1; ++kc, ++i) {
+      const int st = i % kPjStages;
+      mbar_wait(&full[st], static_cast<uint32_t>((i / kPjStages) & 1));
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + st * slot), sb = sa + kPjWBox;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        mma_bf16(tmem, sdesc_sw128(sa + k * 32, 16, 1024), sdesc_sw128(sb + k * 32, 16, 1024), idesc,
+                 (i | k) != 0 ? 1u : 0u);
+      mma_commit(&empty[st]);
+    }
+    mma_commit(done);
+  }
+  __syncwarp();
+  mbar_wait(done, 0);
+  tc_fence_after();
+  // ---- epilogue: thread = output feature (TMEM lane); columns = positions
+  float* red = reinterpret_cast<float*>(smem);  // [NT][128] fp32 (the idle ring)
+  const uint32_t lrow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  const int feat = threadIdx.x;
+  const bool split = a.ks > 1;
+  const bool leader = !split || cluster_ctarank() == 0;
+  for (int c0 = 0; c0 < a.NT; c0 += 32) {
+    float x[32];
+    tmem_ld32(lrow + c0, x);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) red[(c0 + j) * 128 + feat] = x[j];
+  }
+  tc_fence_before();
+  if (split) cluster_sync_all();  // every CTA's partial in its shared memory
+  else __syncthreads();
+  if (leader) {
+    if (split) {  // + the other ranks' partials, in rank order; 4 x (ks - 1) loads in flight
+      float4* red4 = reinterpret_cast<float4*>(red);
+      const int nq = a.NT * 32;
+      for (int q0 = threadIdx.x; q0 < nq; q0 += 4 * 128) {
+        float4 acc[4], v[4][3];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] = (q0 + u * 128 < nq) ? red4[q0 + u * 128] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int r = 1; r < 4; ++r)
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (r < a.ks && q0 + u * 128 < nq) v[u][r - 1] = ld_dsmem_v4(red4 + q0 + u * 128, r);
+#pragma unroll
+        for (int r = 1; r < 4; ++r)
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (r < a.ks && q0 + u * 128 < nq) {
+              acc[u].x += v[u][r - 1].x;
+              acc[u].y += v[u][r - 1].y;
+              acc[u].z += v[u][r - 1].z;
+              acc[u].w += v[u][r - 1].w;
+            }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (q0 + u * 128 < nq) red4[q0 + u * 128] = acc[u];
+      }
+      __syncthreads();
+    }
+    // bf16 rows [NT positions][128 features] (256 B each) staged after the fp32 tile
+    uint16_t* ob = reinterpret_cast<uint16_t*>(red + a.NT * 128);
+    for (int c = 0; c < a.NT; ++c) {
+      const __nv_bfloat16 v = __float2bfloat16_rn(red[c * 128 + feat]);
+      ob[c * 128 + feat] = *reinterpret_cast<const uint16_t*>(&v);
+    }
+    __syncthreads();
+    uint16_t* dst = (m == 0) ? a.dst[0] : (m == 1) ? a.dst[1] : a.dst[2];  // no dynamic param indexing
+    const int row0 = (m == 0) ? a.dst_row0[0] : (m == 1) ? a.dst_row0[1] : a.dst_row0[2];
+    for (int u = threadIdx.x; u < a.NT * 16; u += 128) {
+      const int c = u / 16, q = u % 16;
+      const int pos = p0 + c;
+      if (pos < a.lo + a.R)
+        *reinterpret_cast<uint4*>(dst + static_cast<long>(pos - row0) * a.H + ft * 128 + q * 8) =
+            *reinterpret_cast<const uint4*>(ob + c * 128 + q * 8);
+    }
+  }
+  if (split) cluster_sync_all();  // the peers' shared memory stays valid until the leader has read it
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 256);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 kv_encoder() {
@@ -440,7 +600,6 @@ using namespace dinfer;
 struct dinfer_kv {
   dinfer_kv_shape shp{};
   cudaStream_t stream = nullptr;
-  cublasHandle_t blas = nullptr;
   int num_sms = 0;
   uint16_t* Q = nullptr;  // [L][H]
   float* opart = nullptr;
@@ -452,7 +611,13 @@ struct dinfer_kv {
   const void* c_k = nullptr;
   const void* c_v = nullptr;
   int* cnt = nullptr;          // [nheads][query tiles] merge counters
-  const void** d_ptrs = nullptr;  // [9] batched-GEMM pointer arrays (A, B, C)
+  // projection maps (kv_proj_tc), cached per pointer / per position-tile width
+  CUtensorMap map_wq{}, map_wk{}, map_wv{}, map_x{};
+  const void* c_wq = nullptr;
+  const void* c_wk = nullptr;
+  const void* c_wv = nullptr;
+  const void* c_x = nullptr;
+  int c_xnt = 0;
 };
 
 extern "C" {
@@ -490,9 +655,8 @@ dinfer_status dinfer_kv_create(const dinfer_kv_shape* s, void* stream, dinfer_kv
   bool ok = cudaMalloc(&c->Q, LH * 2) == cudaSuccess && cudaMalloc(&c->opart, c->part_rows * s->H * 4) == cudaSuccess &&
             cudaMalloc(&c->mpart, nml * 4) == cudaSuccess && cudaMalloc(&c->lpart, nml * 4) == cudaSuccess;
   const size_t ncnt = static_cast<size_t>(s->H / kD) * ((s->L + kTQ - 1) / kTQ);
-  if (ok) ok = cudaMalloc(&c->cnt, ncnt * 4) == cudaSuccess && cudaMemset(c->cnt, 0, ncnt * 4) == cudaSuccess &&
-               cudaMalloc(reinterpret_cast<void**>(&c->d_ptrs), 9 * sizeof(void*)) == cudaSuccess;
-  if (ok) ok = cublasCreate(&c->blas) == CUBLAS_STATUS_SUCCESS;
+  if (ok) ok = cudaMalloc(&c->cnt, ncnt * 4) == cudaSuccess && cudaMemset(c->cnt, 0, ncnt * 4) == cudaSuccess;
+  if (ok) ok = ensure_func_smem(reinterpret_cast<const void*>(kv_proj_tc), kv_proj_smem(256)) == cudaSuccess;
   if (const char* e = std::getenv("DINFER_KV_TC")) c->tc = std::atoi(e) != 0;
   if (ok && c->tc) {
     ok = kv_map(&c->map_q, c->Q, static_cast<uint64_t>(s->H), static_cast<uint64_t>(s->L), kTQ) &&
@@ -513,13 +677,11 @@ dinfer_status dinfer_kv_create(const dinfer_kv_shape* s, void* stream, dinfer_kv
 void dinfer_kv_destroy(dinfer_kv* c) {
   if (c == nullptr) return;
   if (c->stream != nullptr) cudaStreamSynchronize(c->stream);
-  if (c->blas != nullptr) cublasDestroy(c->blas);
   cudaFree(c->Q);
   cudaFree(c->opart);
   cudaFree(c->mpart);
   cudaFree(c->lpart);
   cudaFree(c->cnt);
-  cudaFree(const_cast<void**>(c->d_ptrs));
   delete c;
 }
 
@@ -539,18 +701,57 @@ dinfer_status dinfer_kv_step(dinfer_kv* c, const uint16_t* X, const uint16_t* Wq
     lo_hi[0] = lo;
     lo_hi[1] = hi;
   }
-  // ---- K.Update + queries: Y[R, H] = X[lo:hi] W^T (bf16 out, fp32 accumulate), cuBLAS
-  // column-major view: Y^T [H x R] = W^T^T ... = op_T(W as [H_in x H_out]) * X^T [H_in x R]
-  if (cublasSetStream(c->blas, c->stream) != CUBLAS_STATUS_SUCCESS) return DINFER_ERR_CUDA;
-  const float one = 1.f, zero = 0.f;
-  const long xoff = static_cast<long>(lo) * H;
-  // one batched GEMM for the three projections (pointer arrays written on
-  // device, so consecutive forwards never race on a host staging buffer)
-  kv_set_ptrs<<<1, 32, 0, c->stream>>>(c->d_ptrs, Wk, Wv, Wq, X + xoff, Kc + xoff, Vc + xoff, c->Q);
-  if (cublasGemmBatchedEx(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, H, R, H, &one, c->d_ptrs, CUDA_R_16BF, H,
-                          c->d_ptrs + 3, CUDA_R_16BF, H, &zero, const_cast<void**>(c->d_ptrs + 6), CUDA_R_16BF, H,
-                          3, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
-    return DINFER_ERR_CUDA;
+  // ---- K.Update + queries: Y_m[R, H] = bf16(X[lo:hi] W_m^T), m = K, V, Q, on
+  // tcgen05 (kv_proj_tc): K / V straight into the cache rows, Q into c->Q
+  {
+    auto wmap = [&](CUtensorMap* mp, const void** cache, const uint16_t* Wp) {
+      if (*cache == Wp) return true;
+      if (!kv_map(mp, Wp, static_cast<uint64_t>(H), static_cast<uint64_t>(H), 128)) return false;
+      *cache = Wp;
+      return true;
+    };
+    if (!wmap(&c->map_wk, &c->c_wk, Wk) || !wmap(&c->map_wv, &c->c_wv, Wv) || !wmap(&c->map_wq, &c->c_wq, Wq))
+      return DINFER_ERR_CUDA;
+    // position tiles of NT <= 256 (multiple of 16), then split K over a
+    // cluster of up to 4 CTAs while the grid is under one CTA per SM
+    const int ntp = (R + 255) / 256;
+    const int NT = ((R + ntp - 1) / ntp + 15) / 16 * 16;
+    if (X != c->c_x || NT != c->c_xnt) {
+      if (!kv_map(&c->map_x, X, static_cast<uint64_t>(H), static_cast<uint64_t>(L), static_cast<uint32_t>(NT)))
+        return DINFER_ERR_CUDA;
+      c->c_x = X;
+      c->c_xnt = NT;
+    }
+    const int tiles = 3 * (H / 128) * ntp, nkc = H / 64;
+    const int ks = std::max(1, std::min({4, c->num_sms / tiles, nkc}));
+    ProjArgs pa{};
+    pa.H = H;
+    pa.R = R;
+    pa.lo = lo;
+    pa.NT = NT;
+    pa.nkc = nkc;
+    pa.ks = ks;
+    pa.dst[0] = Kc;
+    pa.dst[1] = Vc;
+    pa.dst[2] = c->Q;
+    pa.dst_row0[0] = 0;
+    pa.dst_row0[1] = 0;
+    pa.dst_row0[2] = lo;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(3 * (H / 128), ntp, ks);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = kv_proj_smem(NT);
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 1;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = static_cast<unsigned>(ks);
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kv_proj_tc, c->map_wk, c->map_wv, c->map_wq, c->map_x, pa) != cudaSuccess)
+      return DINFER_ERR_CUDA;
+  }
   // ---- attention over all L cached positions
   if (c->tc) {
     if (Kc != c->c_k) {

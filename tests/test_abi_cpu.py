@@ -139,3 +139,17 @@ def test_params_struct_matches_header():
     body = re.search(r"typedef struct \{([^}]*)\} dinfer_params;", src).group(1)
     names = re.findall(r"(\w+)\s*[,;]", re.sub(r"/\*.*?\*/", "", body, flags=re.S))
     assert names == [n for n, _ in dinfer.Params._fields_]
+
+
+def test_library_links_no_cublas():
+    """Every contraction of the path (vocab projection, smoothing mix, the
+    vicinity layer's projections and attention) is a hand-written tcgen05
+    kernel: libdinfer.so has no cuBLAS dependency."""
+    import subprocess
+    build.build()
+    out = subprocess.run(["readelf", "-d", dinfer.LIB_PATH], capture_output=True, text=True).stdout
+    assert "NEEDED" in out and "cublas" not in out.lower(), out
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", dinfer.LIB_PATH], capture_output=True,
+                          text=True).stdout
+    fn = [blk for blk in sass.split("Function : ") if blk.split("\n")[0].find("kv_proj_tc") >= 0]
+    assert len(fn) == 1 and "UTCHMMA" in fn[0] and "UTMALDG" in fn[0]
