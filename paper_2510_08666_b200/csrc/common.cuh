@@ -152,6 +152,34 @@ DI void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Warp-collective issue: every lane of the warp executes it with the same
+// (warp-uniform) operands and elect.sync picks the issuing lane inside the
+// asm, so the compiler keeps the descriptors in uniform registers and emits
+// no per-MMA ELECT / R2UR waterfall.  Measured (tools/mma_rate2.cu, M = 128,
+// N = 32): 40 cycles per UTCHMMA warp-issued vs 54 from one divergent thread
+// with hoisted descriptors and ~120-150 with descriptors rebuilt per MMA in a
+// runtime-length loop (the floor at N >= 128 is N/2 cycles either way).
+DI void mma_bf16_warp(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Warp-collective commit (one elected lane arrives on `bar`).
+DI void mma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+// A shared-memory descriptor advanced by `bytes` (start address field, bits
+// [0,14) in 16-B units; shared-memory addresses stay below 256 KB, so the
+// field never carries into the next one).
+DI uint64_t sdesc_add(uint64_t desc, uint32_t bytes) { return desc + static_cast<uint64_t>(bytes >> 4); }
+
 // Arrive on `bar` once all previously issued tcgen05.mma of this thread complete.
 DI void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -177,6 +205,21 @@ DI void tmem_ld32(uint32_t taddr, float (&v)[32]) {
       : "memory");
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+// Store 32 consecutive fp32 columns of this thread's TMEM lane (32x32b.x32)
+// and wait for completion.
+DI void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n\t"
+      "tcgen05.wait::st.sync.aligned;" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+      "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+      "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
 }
 
 // Two 32-column loads (e.g. two accumulator sets) in flight together, one wait.

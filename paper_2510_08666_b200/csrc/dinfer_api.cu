@@ -742,11 +742,14 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
       // the TMEM), HS = H/HW slabs per vocab group, VG groups of 16-row chunks.
       // Stacked hi / lo P (one 2N-column MMA per k-step, DINFER_K12_STACK=0 to
       // disable) needs HW/128 x 2N columns per accumulator set.
-      int stack = 0;  // measured no faster (HW 512 geometry slower); kept as a measurement knob
+      // Stacked hi / lo P (one 2N-column MMA per k-step, one accumulator for
+      // all rows of the group: HW/128 x 2N <= 512 columns) unless
+      // DINFER_K12_STACK=0 (two accumulator sets of HW/128 x N <= 256 columns)
+      int stack = 1;
       if (const char* e = std::getenv("DINFER_K12_STACK")) stack = std::atoi(e) != 0;
       int hw = 0;
       for (int w = 1024; w >= 128 && hw == 0; w /= 2)
-        if (w <= hw_pref && s.H % w == 0 && (w / 128) * c->N * (stack ? 2 : 1) <= 256) hw = w;
+        if (w <= hw_pref && s.H % w == 0 && (w / 128) * c->N * 2 <= 512) hw = w;  // same budget both ways
       c->k12_stack = stack;
       const int nch = static_cast<int>((s.V_local + kChunkRows12 - 1) / kChunkRows12);
       const int HS = hw > 0 ? s.H / hw : 0;

@@ -90,8 +90,9 @@ __host__ __device__ inline Layout make_layout(int N, int HW, int stages, int pst
   L.ent_off = L.head_off + ((static_cast<uint32_t>(slab_rows_max) * 4u + 15u) & ~15u);
   const uint32_t tables = L.ent_off - L.un_off + 3u * kMaxCreditEnt * 2u;
   L.bar_off = (L.un_off + (rings > tables ? rings : tables) + 15u) & ~15u;
-  // full/empty[stages], efull/eempty[estages], tfull/tempty[2], ffull/fempty/pfull/pempty[pstages], accfull, own, oth
-  L.misc_off = L.bar_off + (2u * stages + 2u * L.estages + 4u + 4u * pstages + 3u) * 8u;
+  // full/empty[stages], efull/eempty[estages], tfull/tempty[2], ffull/fempty/pfull/pempty[pstages], accfull, own,
+  // oth, owndone
+  L.misc_off = L.bar_off + (2u * stages + 2u * L.estages + 4u + 4u * pstages + 4u) * 8u;
   L.m_off = L.misc_off + 64u;  // tmem base, entry count, diagnostics words [4, 12)
   L.red_off = L.m_off + static_cast<uint32_t>(4 * N) * 4u;  // m_own, m_oth, scale A, scale B
   L.total = L.red_off + static_cast<uint32_t>(kEpiWarps * N * 3) * 4u;
@@ -213,6 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* accfull = pempty + b.pstages;
   uint64_t* own_ready = accfull + 1;    // own slab's flog / m_own complete
   uint64_t* oth_ready = own_ready + 1;  // m_oth in smem, other slabs' flog visible
+  uint64_t* owndone = oth_ready + 1;    // stack mode: every own-slab E MMA complete
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L.misc_off);  // tmem base, entry count
   volatile int* prog = b.probe != nullptr ? reinterpret_cast<volatile int*>(misc + 4) : nullptr;
   float* m_own = reinterpret_cast<float*>(smem + L.m_off);
@@ -293,6 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(accfull, 1);
     mbar_init(own_ready, 1);
     mbar_init(oth_ready, 1);
+    mbar_init(owndone, 1);
     fence_mbar_init();
     // W does not depend on the preceding kernel: the first ring's worth of W
     // stages is issued now (each stage's barrier expects W + hidden bytes; the
@@ -375,93 +378,89 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp == 5) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc_w = idesc_bf16(kTileRows, N, false, false);
-      // E phase: with b.stack the hi and lo P tiles (rows [0, N) and [N, 2N) of
-      // one SW64 tile) are ONE B operand of 2N rows -- one MMA per k-step
-      // writes E.hi into columns [0, N) and E.lo into [N, 2N) of the sub-tile,
-      // so the E tile (A) is read from shared memory once instead of twice
-      const int NE = b.stack ? 2 * N : N;
-      const uint32_t idesc_e = idesc_bf16(128, NE, /*a MN-major*/ true, /*b K-major*/ false);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = 0; t < ntiles; ++t) {
-        const int buf = t & 1;
-        const uint32_t use = static_cast<uint32_t>(t >> 1);
-        mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
+    // The whole warp runs the loops; each MMA / commit is issued by one
+    // elected lane inside the asm (mma_bf16_warp: no per-MMA waterfall), and
+    // the shared-memory descriptors are built once per stage and advanced by
+    // constant offsets (sdesc_add).  Single-thread issue with per-MMA
+    // descriptors cost ~120-150 cycles per UTCHMMA (tools/mma_rate*.cu) --
+    // at N = 32 slower than the E stream delivers its 64-KB stages.
+    const uint32_t idesc_w = idesc_bf16(kTileRows, N, false, false);
+    // E phase: with b.stack the hi and lo P tiles (rows [0, N) and [N, 2N) of
+    // one SW64 tile) are ONE B operand of 2N rows -- one MMA per k-step
+    // writes E.hi into columns [0, N) and E.lo into [N, 2N) of the sub-tile,
+    // so the E tile (A) is read from shared memory once instead of twice
+    const int NE = b.stack ? 2 * N : N;
+    const uint32_t idesc_e = idesc_bf16(128, NE, /*a MN-major*/ true, /*b K-major*/ false);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = 0; t < ntiles; ++t) {
+      const int buf = t & 1;
+      const uint32_t use = static_cast<uint32_t>(t >> 1);
+      mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
+      tc_fence_after();
+      const uint32_t d = tmem_base + static_cast<uint32_t>(buf * N);
+      for (int kc0 = 0; kc0 < a.num_kc; kc0 += 2) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t d = tmem_base + static_cast<uint32_t>(buf * N);
-        for (int kc0 = 0; kc0 < a.num_kc; kc0 += 2) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          if (tr != nullptr && t == 0 && kc0 == 0) tr[1] = globaltimer_ns();
-          const uint32_t slot = smem_u32(ring + stage * L.wslot);
-          if (a.xbits & 16) {  // measurement only: release the stage without its MMAs
-            mbar_arrive(&empty[stage]);
-            advance(stage, phase, a.stages);
-            continue;
-          }
+        if (tr != nullptr && t == 0 && kc0 == 0) tr[1] = globaltimer_ns();
+        const uint32_t slot = smem_u32(ring + stage * L.wslot);
+        const uint64_t a0 = sdesc_sw128(slot, 16, 1024), b0 = sdesc_sw128(slot + kWBytes, 16, 1024);
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const uint32_t a_addr = slot + j * kChunkBytes;
-            const uint32_t b_addr = slot + kWBytes + j * hchunk;
+        for (int j = 0; j < 2; ++j)
 #pragma unroll
-            for (int k = 0; k < kKChunk / 16; ++k)
-              mma_bf16(d, sdesc_sw128(a_addr + k * 32, 16, 1024), sdesc_sw128(b_addr + k * 32, 16, 1024), idesc_w,
-                       (kc0 + j) != 0 || k != 0);
-          }
-          mma_commit(&empty[stage]);
-          advance(stage, phase, a.stages);
-        }
-        mma_commit(&tfull[buf]);
-        PROBE(1, 1000 + t);
+          for (int k = 0; k < kKChunk / 16; ++k)
+            mma_bf16_warp(d, sdesc_add(a0, j * kChunkBytes + k * 32), sdesc_add(b0, j * hchunk + k * 32), idesc_w,
+                          (kc0 + j) != 0 || k != 0);
+        mma_commit_warp(&empty[stage]);
+        advance(stage, phase, a.stages);
       }
-      int ps = 0, es = 0;
-      uint32_t pph = 0, eph = 0;
-      for (int j = 0; j < n_all; ++j) {
-        const bool own = j < n_own;
-        const uint32_t set = own ? 0u : kSetB;
-        const bool first = (j == 0) || (j == n_own);
-        PROBE(1, 100000 + j);
-        mbar_wait(&pfull[ps], pph);
-        PROBE(1, 200000 + j);
-        mbar_wait(&efull[es], eph);
-        PROBE(1, 300000 + j);
-        tc_fence_after();
-        if (tr2 != nullptr && j == 0) tr2[1] = globaltimer_ns();
-        const uint32_t e_addr = smem_u32(ring + es * L.eslot);
-        const uint32_t phi = smem_u32(p_sm + ps * L.p_stage);
-        if (a.xbits & 32) {  // measurement only: release the stages without their MMAs
-          mbar_arrive(&eempty[es]);
-          mbar_arrive(&pempty[ps]);
-          advance(es, eph, static_cast<int>(L.estages));
-          advance(ps, pph, b.pstages);
-          continue;
-        }
+      mma_commit_warp(&tfull[buf]);
+      if (lane == 0) PROBE(1, 1000 + t);
+    }
+    int ps = 0, es = 0;
+    uint32_t pph = 0, eph = 0;
+    const int nsub = b.nsub;  // <= 8 (HW <= 1024)
+    for (int j = 0; j < n_all; ++j) {
+      const bool own = j < n_own;
+      // stack mode: ONE accumulator (relative to the per-row reference the P
+      // producers choose); else own rows in set A, the other slabs' in set B
+      const uint32_t set = (own || b.stack) ? 0u : kSetB;
+      const bool first = (j == 0) || (j == n_own && !b.stack);
+      if (lane == 0) PROBE(1, 100000 + j);
+      mbar_wait(&pfull[ps], pph);
+      if (lane == 0) PROBE(1, 200000 + j);
+      mbar_wait(&efull[es], eph);
+      if (lane == 0) PROBE(1, 300000 + j);
+      tc_fence_after();
+      if (tr2 != nullptr && j == 0) tr2[1] = globaltimer_ns();
+      // A: [128 h x 16 v] = two 64-h boxes (LBO = box bytes), 8-v groups 1 KB apart (SBO);
+      // B: P tile [N x 16 v] K-major SWIZZLE_64B (64-B rows, 8-row atoms of 512 B)
+      const uint64_t a0 = sdesc_sw128(smem_u32(ring + es * L.eslot), ebox, 1024);
+      const uint64_t bh0 = sdesc_swz(smem_u32(p_sm + ps * L.p_stage), 16, 512, 4);
 #pragma unroll
-        for (int k = 0; k < KV / 16; ++k) {
-          // B: P tile [N x 16 v] K-major SWIZZLE_64B (64-B rows, 8-row atoms of 512 B)
-          const uint64_t bhi = sdesc_swz(phi + k * 32, 16, 512, 4);
-          const uint64_t blo = sdesc_swz(phi + p_half + k * 32, 16, 512, 4);
-          for (int sub = 0; sub < b.nsub; ++sub) {
-            // A: [128 h x 16 v] = two 64-h boxes (LBO = box bytes), 8-v groups 1 KB apart (SBO)
-            const uint64_t ad = sdesc_sw128(e_addr + sub * 2 * ebox + k * 16 * 128, ebox, 1024);
+      for (int k = 0; k < KV / 16; ++k) {
+        const uint64_t bhi = sdesc_add(bh0, k * 32), blo = sdesc_add(bh0, p_half + k * 32);
+#pragma unroll
+        for (int sub = 0; sub < 8; ++sub) {
+          if (sub < nsub) {
+            const uint64_t ad = sdesc_add(a0, sub * 2 * ebox + k * 16 * 128);
             const uint32_t d = tmem_base + set + static_cast<uint32_t>(sub * NE);
-            mma_bf16(d, ad, bhi, idesc_e, (first && k == 0) ? 0u : 1u);
-            if (!b.stack) mma_bf16(d, ad, blo, idesc_e, 1u);
+            mma_bf16_warp(d, ad, bhi, idesc_e, (first && k == 0) ? 0u : 1u);
+            if (!b.stack) mma_bf16_warp(d, ad, blo, idesc_e, 1u);
           }
         }
-        mma_commit(&eempty[es]);
-        mma_commit(&pempty[ps]);
-        advance(es, eph, static_cast<int>(L.estages));
-        advance(ps, pph, b.pstages);
       }
-      mma_commit(accfull);
-      PROBE(1, 999999);
-      if (tr2 != nullptr) {
-        mbar_wait(accfull, 0);
-        tr2[2] = globaltimer_ns();
-      }
+      mma_commit_warp(&eempty[es]);
+      mma_commit_warp(&pempty[ps]);
+      if (b.stack && j == n_own - 1 && has_oth) mma_commit_warp(owndone);  // (rare) reference switch waits on it
+      advance(es, eph, static_cast<int>(L.estages));
+      advance(ps, pph, b.pstages);
+    }
+    mma_commit_warp(accfull);
+    if (lane == 0) PROBE(1, 999999);
+    if (tr2 != nullptr) {
+      mbar_wait(accfull, 0);
+      tr2[2] = globaltimer_ns();
     }
     __syncwarp();
   } else if (warp == 6) {
@@ -655,9 +654,52 @@ __global__ void __launch_bounds__(kThreads, 1)
     int ps = 0;
     uint32_t pph = 0;
     const int cpr = KV / 8;  // 16-B chunks per P row (4)
+    // Stack mode: one accumulator, reference ref[s] per row = the own slab max;
+    // the other slabs' rows use it too (their weights e^{f - m_own} may exceed
+    // 1: exact in bf16 hi + lo and fp32) unless the other slabs' max exceeds
+    // it by more than kRefGap nats -- then (practically never) the finished
+    // own-row accumulation is rescaled in TMEM to the other slabs' max.
+    constexpr float kRefGap = 32.f;
+    float* ref = scB;  // (stack mode does not use set B's scale)
+    if (b.stack)
+      for (int s = tid; s < N; s += kEpiThreads) ref[s] = m_own[s];
     for (int j = 0; j < n_all; ++j) {
-      if (j == n_own) mbar_wait(oth_ready, 0);
-      const float* mref = (j < n_own) ? m_own : m_oth;
+      if (j == n_own) {
+        mbar_wait(oth_ready, 0);
+        if (b.stack) {
+          if (tid == 0) misc[3] = 0u;
+          named_bar_epi();
+          for (int s = tid; s < N; s += kEpiThreads) {
+            float r = (n_own > 0) ? m_own[s] : m_oth[s];
+            if (n_own > 0 && s < a.M && m_oth[s] > m_own[s] + kRefGap) {
+              r = m_oth[s];
+              atomicOr(&misc[3], 1u);
+            }
+            ref[s] = r;
+          }
+          named_bar_epi();
+          if (misc[3] != 0u) {  // rescale columns s of every sub-tile by e^{m_own - m_oth}
+            mbar_wait(owndone, 0);
+            tc_fence_after();
+            const int NE = 2 * N;
+            const uint32_t lb = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
+            for (int sub = 0; sub < b.nsub; ++sub)
+              for (int c0 = 0; c0 < NE; c0 += 32) {
+                float x[32];
+                tmem_ld32(lb + static_cast<uint32_t>(sub * NE + c0), x);
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) {
+                  const int s = (c0 + jj) % N;
+                  if (s < a.M && ref[s] != m_own[s]) x[jj] *= fexp(m_own[s] - ref[s]);
+                }
+                tmem_st32(lb + static_cast<uint32_t>(sub * NE + c0), x);
+              }
+            tc_fence_before();
+            named_bar_epi();
+          }
+        }
+      }
+      const float* mref = b.stack ? ref : ((j < n_own) ? m_own : m_oth);
       const int c = chunk_at(j);
       mbar_wait(&ffull[ps], pph);
       mbar_wait(&pempty[ps], pph ^ 1u);
@@ -702,8 +744,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = tid; s < N; s += kEpiThreads) {
       const float mo = m_own[s], mt = m_oth[s];
       const float mg = fmaxf(mo, mt);
-      scA[s] = (n_own > 0 && s < a.M) ? fexp(mo - mg) : 0.f;
-      scB[s] = (has_oth && s < a.M) ? fexp(mt - mg) : 0.f;
+      if (b.stack) {  // the single accumulator is relative to ref[s]
+        scA[s] = (n_all > 0 && s < a.M) ? fexp(ref[s] - mg) : 0.f;
+      } else {
+        scA[s] = (n_own > 0 && s < a.M) ? fexp(mo - mg) : 0.f;
+        scB[s] = (has_oth && s < a.M) ? fexp(mt - mg) : 0.f;
+      }
       if (hs == 0 && s < a.M) b.mref[static_cast<long>(grp) * a.M + s] = mg;
     }
   }
@@ -754,8 +800,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int g = 0; g < ng; ++g) {
         float x[32];
         const uint32_t col = static_cast<uint32_t>(sub * NE + g * 32);
-        if (n_own > 0) {
-          if (b.stack) {  // E.hi + E.lo (columns col and col + N)
+        if (n_own > 0 || (b.stack && n_all > 0)) {
+          if (b.stack) {  // E.hi + E.lo (columns col and col + N), the single accumulator
             float y[32];
             tmem_ld32x2(lanebase + col, lanebase + col + N, x, y);
 #pragma unroll
@@ -769,7 +815,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) x[jj] = 0.f;
         }
-        if (has_oth) {
+        if (has_oth && !b.stack) {
           float y[32];
           if (b.stack) {
             float z[32];

@@ -208,39 +208,37 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp == 5) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc = idesc_bf16(kTileRows, N, false, false);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = 0; t < ntiles; ++t) {
-        const int buf = t & 1;
-        const uint32_t use = static_cast<uint32_t>(t >> 1);
-        mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
+    // warp-collective issue with per-stage descriptors advanced by constant
+    // offsets (common.cuh mma_bf16_warp: no per-MMA ELECT waterfall)
+    const uint32_t idesc = idesc_bf16(kTileRows, N, false, false);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = 0; t < ntiles; ++t) {
+      const int buf = t & 1;
+      const uint32_t use = static_cast<uint32_t>(t >> 1);
+      mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
+      tc_fence_after();
+      const uint32_t d = tmem_base + static_cast<uint32_t>(buf * N);
+      for (int kc0 = 0; kc0 < a.num_kc; kc0 += kChunksPerStage) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t d = tmem_base + static_cast<uint32_t>(buf * N);
-        for (int kc0 = 0; kc0 < a.num_kc; kc0 += kChunksPerStage) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          if (a.trace != nullptr && t == 0 && kc0 == 0) a.trace[blockIdx.x * 5 + 1] = globaltimer_ns();
+        if (lane == 0 && a.trace != nullptr && t == 0 && kc0 == 0) a.trace[blockIdx.x * 5 + 1] = globaltimer_ns();
+        const uint64_t a0 = sdesc_sw128(smem_u32(w_sm + stage * kWStageBytes), 16, 1024);
+        const uint64_t b0 = sdesc_sw128(smem_u32(h_sm + (a.h_resident ? kc0 : stage * kChunksPerStage) * hchunk), 16,
+                                        1024);
 #pragma unroll
-          for (int j = 0; j < kChunksPerStage; ++j) {
-            const int kc = kc0 + j;
-            const uint32_t a_addr = smem_u32(w_sm + stage * kWStageBytes + j * kChunkBytes);
-            const uint32_t b_addr = smem_u32(h_sm + (a.h_resident ? kc : stage * kChunksPerStage + j) * hchunk);
+        for (int j = 0; j < kChunksPerStage; ++j)
 #pragma unroll
-            for (int k = 0; k < kKChunk / 16; ++k) {
-              mma_bf16(d, sdesc_sw128(a_addr + k * 32, 16, 1024), sdesc_sw128(b_addr + k * 32, 16, 1024), idesc,
-                       (kc | k) != 0);
-            }
-          }
-          mma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
-          if (++stage == a.stages) {
-            stage = 0;
-            phase ^= 1u;
-          }
+          for (int k = 0; k < kKChunk / 16; ++k)
+            mma_bf16_warp(d, sdesc_add(a0, j * kChunkBytes + k * 32), sdesc_add(b0, j * hchunk + k * 32), idesc,
+                          ((kc0 + j) | k) != 0);
+        mma_commit_warp(&empty[stage]);  // frees the smem slot when these MMAs finish
+        if (++stage == a.stages) {
+          stage = 0;
+          phase ^= 1u;
         }
-        mma_commit(&tfull[buf]);  // accumulator ready for the epilogue
       }
+      mma_commit_warp(&tfull[buf]);  // accumulator ready for the epilogue
     }
     __syncwarp();
   } else {

@@ -153,38 +153,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp == 5) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc = idesc_bf16(128, kBN, false, false);
-      int stage = 0;
-      uint32_t phase = 0, tuse = 0;
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-        int mb, g, b0, b1;
-        unit_coords(u, mb, g);
-        block_range(g, b0, b1);
-        for (int nb = b0; nb < b1; ++nb) {
-          mbar_wait(tempty, (tuse & 1u) ^ 1u);  // epilogue drained both accumulators
+    // warp-collective issue, per-stage descriptors advanced by constant offsets
+    const uint32_t idesc = idesc_bf16(128, kBN, false, false);
+    int stage = 0;
+    uint32_t phase = 0, tuse = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      int mb, g, b0, b1;
+      unit_coords(u, mb, g);
+      block_range(g, b0, b1);
+      for (int nb = b0; nb < b1; ++nb) {
+        mbar_wait(tempty, (tuse & 1u) ^ 1u);  // epilogue drained both accumulators
+        tc_fence_after();
+        for (int kc = 0; kc < nkc; ++kc) {
+          mbar_wait(&full[stage], phase);
           tc_fence_after();
-          for (int kc = 0; kc < nkc; ++kc) {
-            mbar_wait(&full[stage], phase);
-            tc_fence_after();
-            const uint32_t base = smem_u32(st_sm + stage * kStageBytes);
+          // B = W rows [256 x 16]: two 128-row boxes 16 KB apart = rows 8..255 at SBO 1 KB,
+          // so one descriptor spans both boxes (box 1 follows box 0 contiguously)
+          const uint64_t d0 = sdesc_sw128(smem_u32(st_sm + stage * kStageBytes), 16, 1024);
 #pragma unroll
-            for (int k = 0; k < kKChunk / 16; ++k) {
-              // B = W rows [256 x 16]: two 128-row boxes 16 KB apart = rows 8..255 at SBO 1 KB,
-              // so one descriptor spans both boxes (box 1 follows box 0 contiguously)
-              const uint64_t bd = sdesc_sw128(base + 2 * kBox + k * 32, 16, 1024);
-              const uint64_t a0 = sdesc_sw128(base + k * 32, 16, 1024);
-              const uint64_t a1 = sdesc_sw128(base + kBox + k * 32, 16, 1024);
-              const uint32_t acc = (kc | k) != 0;
-              mma_bf16(tmem_base, a0, bd, idesc, acc);
-              mma_bf16(tmem_base + kBN, a1, bd, idesc, acc);
-            }
-            mma_commit(&empty[stage]);
-            advance(stage, phase, a.stages);
+          for (int k = 0; k < kKChunk / 16; ++k) {
+            const uint32_t acc = (kc | k) != 0;
+            const uint64_t bd = sdesc_add(d0, 2 * kBox + k * 32);
+            mma_bf16_warp(tmem_base, sdesc_add(d0, k * 32), bd, idesc, acc);
+            mma_bf16_warp(tmem_base + kBN, sdesc_add(d0, kBox + k * 32), bd, idesc, acc);
           }
-          mma_commit(tfull);
-          ++tuse;
+          mma_commit_warp(&empty[stage]);
+          advance(stage, phase, a.stages);
         }
+        mma_commit_warp(tfull);
+        ++tuse;
       }
     }
     __syncwarp();

@@ -178,37 +178,40 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp == 5) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0 && c1 > c0) {
+    // warp-collective issue, per-stage descriptors advanced by constant offsets
+    if (c1 > c0) {
       const uint32_t idesc = idesc_bf16(128, N, /*a MN-major*/ true, /*b K-major*/ false);
       int es = 0, ps = 0;
       uint32_t eph = 0, pph = 0;
+      const int nsub = a.nsub;  // <= 8
+      const uint32_t play = (KV == 64) ? 2u : 4u, psbo = 8u * p_row;  // SW128 / SW64 K-major
       for (int c = c0; c < c1; ++c) {
         mbar_wait(&pfull[ps], pph);
         mbar_wait(&efull[es], eph);
         tc_fence_after();
-        if (a.trace != nullptr && c == c0) a.trace[blockIdx.x * 5 + 1] = globaltimer_ns();
-        const uint32_t e_addr = smem_u32(e_sm + es * e_stage);
-        const uint32_t phi = smem_u32(p_sm + ps * 2 * p_half);
-        const uint32_t plo = phi + p_half;
-        const uint32_t play = (KV == 64) ? 2u : 4u, psbo = 8u * p_row;  // SW128 / SW64 K-major
+        if (lane == 0 && a.trace != nullptr && c == c0) a.trace[blockIdx.x * 5 + 1] = globaltimer_ns();
+        // A: [128 h x 16 v] = two 64-h blocks (LBO = box bytes), 8-v groups 1 KB apart (SBO)
+        const uint64_t a0 = sdesc_sw128(smem_u32(e_sm + es * e_stage), ebox, 1024);
+        const uint64_t bh0 = sdesc_swz(smem_u32(p_sm + ps * 2 * p_half), 16, psbo, play);
         for (int k = 0; k < KV / 16; ++k) {
-          const uint64_t bhi = sdesc_swz(phi + k * 32, 16, psbo, play);
-          const uint64_t blo = sdesc_swz(plo + k * 32, 16, psbo, play);
-          for (int sub = 0; sub < a.nsub; ++sub) {
-            // A: [128 h x 16 v] = two 64-h blocks 8 KB apart (LBO), 8-v groups 1 KB apart (SBO)
-            const uint64_t ad = sdesc_sw128(e_addr + sub * 2 * ebox + k * 16 * 128, ebox, 1024);
-            const uint32_t d = tmem_base + static_cast<uint32_t>(sub * N);
-            mma_bf16(d, ad, bhi, idesc, (c > c0 || k > 0) ? 1u : 0u);
-            mma_bf16(d, ad, blo, idesc, 1u);
+          const uint64_t bhi = sdesc_add(bh0, k * 32), blo = sdesc_add(bh0, p_half + k * 32);
+#pragma unroll
+          for (int sub = 0; sub < 8; ++sub) {
+            if (sub < nsub) {
+              const uint64_t ad = sdesc_add(a0, sub * 2 * ebox + k * 16 * 128);
+              const uint32_t d = tmem_base + static_cast<uint32_t>(sub * N);
+              mma_bf16_warp(d, ad, bhi, idesc, (c > c0 || k > 0) ? 1u : 0u);
+              mma_bf16_warp(d, ad, blo, idesc, 1u);
+            }
           }
         }
-        mma_commit(&eempty[es]);
-        mma_commit(&pempty[ps]);
+        mma_commit_warp(&eempty[es]);
+        mma_commit_warp(&pempty[ps]);
         advance(es, eph, a.stages);
         advance(ps, pph, a.pstages);
       }
-      mma_commit(accfull);
-      if (a.trace != nullptr) {
+      mma_commit_warp(accfull);
+      if (lane == 0 && a.trace != nullptr) {
         mbar_wait(accfull, 0);
         a.trace[blockIdx.x * 5 + 2] = globaltimer_ns();
       }

@@ -78,8 +78,7 @@ struct K1Args {
   int block_start;         // params.block_start: mask / credit inputs not read (all undecided, slots empty)
   int npre;                // K12: W stages issued before the dependency wait (0 = the whole ring; tuning)
   int xbits;               // K12 measurement-only experiments (env DINFER_K12_X; 0 in the product):
-                           //   1 no hidden loads, 2 no flog stores, 4 W evict_normal, 8 E evict_normal,
-                           //   16 W stages released without MMAs, 32 E stages released without MMAs
+                           //   1 no hidden loads, 2 no flog stores, 4 W evict_normal, 8 E evict_normal
 };
 size_t k1_smem_bytes(int N, int H, int stages, int h_resident, int slab_rows_max);
 cudaError_t launch_k1(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,

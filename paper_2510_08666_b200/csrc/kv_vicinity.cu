@@ -481,20 +481,20 @@ __global__ void __launch_bounds__(128, 1)
       tma_load_2d(sl, mw, &full[st], kc * 64, ft * 128, pol_w);
       tma_load_2d(sl + kPjWBox, &map_x, &full[st], kc * 64, p0, pol_x);  // rows past L: zero fill
     }
-  } else if (threadIdx.x == 32) {  // MMA issuer
+  } else if (warp == 1) {  // MMA issuer (warp-collective issue, common.cuh mma_bf16_warp)
     const uint32_t idesc = idesc_bf16(128, a.NT, false, false);
     for (int kc = kc0, i = 0; kc < kc1; ++kc, ++i) {
       const int st = i % kPjStages;
       mbar_wait(&full[st], static_cast<uint32_t>((i / kPjStages) & 1));
       tc_fence_after();
-      const uint32_t sa = smem_u32(smem + st * slot), sb = sa + kPjWBox;
+      const uint64_t da = sdesc_sw128(smem_u32(smem + st * slot), 16, 1024);
+      const uint64_t db = sdesc_add(da, kPjWBox);
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        mma_bf16(tmem, sdesc_sw128(sa + k * 32, 16, 1024), sdesc_sw128(sb + k * 32, 16, 1024), idesc,
-                 (i | k) != 0 ? 1u : 0u);
-      mma_commit(&empty[st]);
+        mma_bf16_warp(tmem, sdesc_add(da, k * 32), sdesc_add(db, k * 32), idesc, (i | k) != 0 ? 1u : 0u);
+      mma_commit_warp(&empty[st]);
     }
-    mma_commit(done);
+    mma_commit_warp(done);
   }
   __syncwarp();
   mbar_wait(done, 0);

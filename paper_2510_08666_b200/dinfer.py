@@ -13,6 +13,8 @@ from ctypes import POINTER, c_float, c_int32, c_int64, c_size_t, c_uint8, c_uint
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdinfer.so")
+if os.environ.get("DINFER_LIB"):  # measurement only: A/B against another in-tree build (tools/ab_lib.sh)
+    LIB_PATH = os.path.abspath(os.environ["DINFER_LIB"])
 
 DEC_THRESHOLD = 0
 DEC_HIERARCHICAL = 1

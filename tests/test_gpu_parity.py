@@ -97,8 +97,8 @@ def test_k1_hidden_resident_or_streamed(torch_cuda, monkeypatch, hres):
     run_trajectory(torch_cuda, 3000, 512, 2, 32, 32, 10, hier_credit_smooth, True, max_iters=4)
 
 
-@pytest.mark.parametrize("fused", ["0", "2"])
-def test_fused_and_two_kernel_smoothing_paths(torch_cuda, monkeypatch, fused):
+@pytest.mark.parametrize("fused,stack", [("0", "1"), ("2", "1"), ("2", "0")])
+def test_fused_and_two_kernel_smoothing_paths(torch_cuda, monkeypatch, fused, stack):
     """Smoothing steps run K12 (K1 + K2 in one kernel, N <= 64; DINFER_FUSED=2
     forces it even for vocabularies too small to fill the machine) or the
     two-kernel K1 -> K2 path (DINFER_FUSED=0); both must match the oracle: ragged vocab /
@@ -106,6 +106,7 @@ def test_fused_and_two_kernel_smoothing_paths(torch_cuda, monkeypatch, fused):
     other-slab accumulator set in use), N = 64 (B = 2, S = 32)."""
     from paper_2510_08666_b200 import Context
     monkeypatch.setenv("DINFER_FUSED", fused)
+    monkeypatch.setenv("DINFER_K12_STACK", stack)  # 1: one accumulator + stacked hi/lo MMA; 0: two sets
     ctx = Context(1, 32, 2048, 32, 4096, smooth_capable=True)
     g = ctx.geometry()
     ctx.close()
@@ -117,12 +118,14 @@ def test_fused_and_two_kernel_smoothing_paths(torch_cuda, monkeypatch, fused):
     run_trajectory(torch_cuda, 2048, 1024, 2, 32, 32, 12, hier_credit_smooth, True, max_iters=3)
 
 
-def test_fused_four_hidden_slices(torch_cuda, monkeypatch):
-    """K12 with SPG = HS = 4 slabs per vocab group (the other-slab set B sums
+@pytest.mark.parametrize("stack", ["1", "0"])
+def test_fused_four_hidden_slices(torch_cuda, monkeypatch, stack):
+    """K12 with SPG = HS = 4 slabs per vocab group (the other slabs' rows sum
     three partner slabs): H = 4096 with N = 32 (1024-wide slices), and
-    H = 2048 with N = 64 (S = 64: 512-wide slices)."""
+    H = 2048 with N = 64 (S = 64: 512-wide slices); both accumulator layouts."""
     from paper_2510_08666_b200 import Context
     monkeypatch.setenv("DINFER_FUSED", "2")
+    monkeypatch.setenv("DINFER_K12_STACK", stack)
     for (V, H, B, S) in ((8192, 4096, 1, 32), (4096, 2048, 1, 64)):
         ctx = Context(B, S, H, 32, V, smooth_capable=True)
         g = ctx.geometry()
@@ -725,4 +728,50 @@ def test_second_host_async_is_rejected(torch_cuda):
     assert com.numpy().sum() >= 1
     ctx.step_host_async(hh, Wd, None, None, mask, tok, None, None, p, com)  # accepted again
     ctx.step_host_wait()
+    ctx.close()
+
+
+def test_k12_reference_switch_for_far_larger_partner_max(torch_cuda, monkeypatch):
+    """K12's single accumulator (stack mode) weighs the partner slabs' rows
+    relative to the own slab's max; when a partner slab's max exceeds it by
+    more than 32 nats the finished own-row sums are rescaled in TMEM to the
+    partner's max (the rare path).  Planted: position 1 has one logit of ~40
+    in a vocab row of the second slab of a group whose first slab stays near
+    0 (and position 0 one of ~60, so the tau = 1 fallback commits position 0
+    and position 1's smoothed row -- the rescaled one -- is compared with the
+    oracle's fp64 softmax(z) W_emb, App. A.1)."""
+    import torch
+    from paper_2510_08666_b200 import Context
+    monkeypatch.setenv("DINFER_FUSED", "2")
+    monkeypatch.setenv("DINFER_K12_STACK", "1")
+    V, H, B, S, K = 8192, 2048, 1, 32, 8  # groups of 3-4 chunks: both slabs non-empty
+    W, E = weights(V, H)
+    W = W.copy()
+    h = synth.planted_hidden(W, B * S, seed=21).reshape(B * S, H)
+    ctx = Context(B, S, H, K, V, smooth_capable=True)
+    g = ctx.geometry()
+    assert g["fused"] == 1 and g["k1_grid"] == 2 * g["k2_groups"]
+    # group 3's rows are chunks [3 * nch / VG, 4 * nch / VG) of 32 rows; its second slab starts halfway
+    nch, VG = (V + 31) // 32, g["k2_groups"]
+    g0, g1 = 3 * nch // VG, 4 * nch // VG
+    v_far = (g0 + (g1 - g0) // 2) * 32 + (g1 - g0) * 8  # a row of the group's second slab
+    v_top = 7 * nch // VG * 32 + 5
+    hf = O.bf16_bits_to_f64(h)
+    for s_, v_, f_ in ((1, v_far, 40.0), (0, v_top, 60.0)):
+        hv = hf[s_]
+        W[v_] = synth.bf16_round(f_ * hv / np.dot(hv, hv))
+    W64, E64 = O.bf16_bits_to_f64(W), O.bf16_bits_to_f64(E)
+    p = O.Params(decoder=O.DEC_THRESHOLD, tau=1.0, use_credit=False, use_smooth=True, alpha_t=0.3)
+    mask = np.ones((B, S), bool)
+    res = O.step(hf.reshape(B, S, H), W64, E64, E64[synth.mask_id(V)], mask, np.full((B, S), synth.mask_id(V)),
+                 None, p)
+    assert res["committed"][0].nonzero()[0].tolist() == [0]
+    f1 = O.logits(hf[1:2], W64)[0]
+    assert f1[v_far] > 35 and f1[g0 * 32:(g0 + (g1 - g0) // 2) * 32].max() < 5  # the planted gap
+    st = GpuState(B, S, H, K, synth.mask_id(V))
+    ctx.step(to_dev_bf16(h), to_dev_bf16(W), to_dev_bf16(E), to_dev_bf16(E[synth.mask_id(V)]), st.mask, st.tokens,
+             None, None, gpu_params(p), st.committed, st.smoothed, st.stats)
+    torch.cuda.synchronize()
+    ctx.sync()
+    compare(st.snapshot(), res, mask, p, where="reference switch")
     ctx.close()
