@@ -179,9 +179,9 @@ struct dinfer_ctx {
   const void* c_e = nullptr;
   const void* mc_w[kMapCache] = {};
   const void* mc_e[kMapCache] = {};
-  CUtensorMap mc_map_w[kMapCache]{}, mc_map_w8[kMapCache]{}, mc_map_e[kMapCache]{};
+  CUtensorMap mc_map_w[kMapCache]{}, mc_map_w8[kMapCache]{}, mc_map_w32[kMapCache]{}, mc_map_e[kMapCache]{};
   int mc_next_w = 0, mc_next_e = 0;
-  CUtensorMap map_w{}, map_w8{}, map_h{}, map_e{}, map_f{};
+  CUtensorMap map_w{}, map_w8{}, map_w32{}, map_h{}, map_e{}, map_f{};  // W boxes of 128 / 8 / 32 rows
   // timing
   int timing = 0;
   bool pdl = true;  // programmatic dependent launch between the step's kernels
@@ -301,14 +301,17 @@ dinfer_status ensure_maps(dinfer_ctx* c, const uint16_t* hidden, const uint16_t*
     if (hit >= 0) {
       c->map_w = c->mc_map_w[hit];
       c->map_w8 = c->mc_map_w8[hit];
+      c->map_w32 = c->mc_map_w32[hit];
     } else {
       if (!encode_2d(&c->map_w, W, H, static_cast<uint64_t>(c->shp.V_local), kKChunk, kTileRows) ||
-          !encode_2d(&c->map_w8, W, H, static_cast<uint64_t>(c->shp.V_local), kKChunk, kRowGran))
+          !encode_2d(&c->map_w8, W, H, static_cast<uint64_t>(c->shp.V_local), kKChunk, kRowGran) ||
+          !encode_2d(&c->map_w32, W, H, static_cast<uint64_t>(c->shp.V_local), kKChunk, kChunkRows12))
         return DINFER_ERR_CUDA;
       const int slot = c->mc_next_w++ % kMapCache;
       c->mc_w[slot] = W;
       c->mc_map_w[slot] = c->map_w;
       c->mc_map_w8[slot] = c->map_w8;
+      c->mc_map_w32[slot] = c->map_w32;
     }
     c->c_w = W;
   }
@@ -356,6 +359,7 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
     r.rec = rec;
     r.rec_acc = rec + c->stats_words;
     r.K = c->shp.K;
+    if (c->trace != nullptr) r.trace = c->trace + 5 * (c->k1_grid + c->k2_HS * c->k2_VG + kTraceK34);
     if (c->p2p && rec == c->rec_local) {  // dinfer_step: push the record into every rank's gather buffer
       r.peers = c->d_peers;
       r.world = c->shp.world;
@@ -456,7 +460,7 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
         b.probe = static_cast<volatile int*>(dp);
     }
     ev_begin(c, kPK1);
-    DI_CUDA(launch_k12(c->map_w, c->map_w8, c->map_h, c->map_e, c->map_f, a, b, c->k1_grid, c->f_smem, c->stream,
+    DI_CUDA(launch_k12(c->map_w, c->map_w32, c->map_h, c->map_e, c->map_f, a, b, c->k1_grid, c->f_smem, c->stream,
                        c->pdl));
     ev_finish(c, kPK1);
   } else {
@@ -962,7 +966,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
     A(dev_alloc(&c->grp_pass, static_cast<size_t>(c->k2_VG)));
   }
   if (std::getenv("DINFER_TRACE") != nullptr && std::atoi(std::getenv("DINFER_TRACE")) != 0)
-    A(dev_alloc(&c->trace, static_cast<size_t>(5) * (c->k1_grid + c->k2_HS * c->k2_VG + kTraceK34)));
+    A(dev_alloc(&c->trace, static_cast<size_t>(5) * (2 * c->k1_grid + c->k2_HS * c->k2_VG + kTraceK34)));
   if (st == DINFER_OK) {
     if (c->grp_cnt != nullptr && (cudaMemset(c->grp_cnt, 0, 4 * c->k2_VG) != cudaSuccess ||
                                   cudaMemset(c->grp_pass, 0, 4 * c->k2_VG) != cudaSuccess))
@@ -2022,7 +2026,7 @@ dinfer_status dinfer_get_timing(dinfer_ctx* c, float* ms, int32_t n) {
 
 int32_t dinfer_get_trace(dinfer_ctx* c, uint64_t* out, int32_t n) {
   if (c == nullptr || c->trace == nullptr) return 0;
-  const int total = 5 * (c->k1_grid + c->k2_HS * c->k2_VG + kTraceK34);
+  const int total = 5 * (2 * c->k1_grid + c->k2_HS * c->k2_VG + kTraceK34);
   if (out == nullptr) return total;
   cudaStreamSynchronize(c->stream);
   const int k = n < total ? n : total;

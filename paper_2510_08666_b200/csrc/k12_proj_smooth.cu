@@ -41,7 +41,8 @@
 //   6    logits producer: flog chunks [N x 32] by TMA (own chunks after the
 //        CTA's own W epilogue, others after the group counter), and m_oth.
 //   7    helper: with warps 4-6, the second half of the final epilogue.
-// TMEM: 512 columns.  W-phase accumulators double-buffered at [0, 2N); E
+// TMEM: 512 columns.  W-phase accumulators (two UMMA outputs per tile)
+// double-buffered at [0, 4N); E
 // set A at [0, nsub NE), set B at [256, 256 + nsub NE), NE = 2N when the hi /
 // lo P tiles are stacked into one MMA (b.stack), else N (E MMAs start only
 // after the W epilogue has drained its accumulators).
@@ -59,8 +60,16 @@ namespace {
 constexpr int kEpiWarps = 4;
 constexpr int kEpiThreads = kEpiWarps * kWarpThreads;
 constexpr int kThreads = (kEpiWarps + 4) * kWarpThreads;  // + TMA, MMA, logits TMA, epilogue helper
-constexpr uint32_t kChunkBytes = kTileRows * 128;  // W [128 rows x 64 k] bf16 = 16 KB
-constexpr uint32_t kWBytes = 2 * kChunkBytes;      // two adjacent K chunks per stage (256 B per W row)
+// W tiles of 1-5 units of 32 rows (the slab's 32-row chunks): rows [0, 128)
+// are one UMMA (M = 128), rows [128, 160) a second one over the next 128 rows
+// of the same chunk (the rows past the tile are stale and ignored).  A slab of
+// n chunks is cut into ceil(n / 5) near-equal tiles, so no tile is a short
+// tail: a 32-row tail tile streamed 16 stages of 8 KB through the same 4-deep
+// ring, as 8-row boxes -- ~12 us for 128 KB vs ~3.3 us per 128 KB in a full
+// tile (K12 trace at V/8).  Every box is 128 or 32 rows (map_w / map_w32).
+constexpr int kTileMax = 160;
+constexpr uint32_t kChunkSpace = kTileMax * 128;   // one K chunk of a W stage: [160 rows x 64 k] bf16 = 20 KB
+constexpr uint32_t kWBytes = 2 * kChunkSpace;      // two adjacent K chunks per stage (256 B per W row)
 constexpr int kMaxGroups = 2;                      // N <= 64 (32-column groups)
 constexpr uint32_t kSetB = 256;                    // TMEM column of accumulator set B
 
@@ -71,7 +80,7 @@ struct Layout {
 
 __host__ __device__ inline Layout make_layout(int N, int HW, int stages, int pstages, int slab_rows_max, int emin) {
   Layout L;
-  L.wslot = (kWBytes + 2u * static_cast<uint32_t>(N) * 128u + 1023u) & ~1023u;  // W + two hidden chunks
+  L.wslot = (kWBytes + 2u * static_cast<uint32_t>(N) * 128u + 1023u) & ~1023u;  // W (<= 160 rows) + two hidden chunks
   L.eslot = static_cast<uint32_t>(HW) * kChunkRows12 * 2u;                        // [HW h x 32 v] bf16
   // the ring holds `stages` W slots and at least `emin` E slots (E slots past
   // the W slots' bytes start without waiting for the W phase)
@@ -155,21 +164,26 @@ DI void group_pass(const K2Args& b, int grp, int SPG) {
     if (prog != nullptr) prog[w] = (v); \
   } while (0)
 
-// The W boxes of W stage `idx` of a slab (tile idx / spt, K chunks 2 (idx % spt) ..+1).
-DI void issue_w_stage(const CUtensorMap* map_w, const CUtensorMap* map_w8, uint8_t* slot, uint64_t* bar, int r0,
-                      int r1, int idx, int spt, uint64_t pol) {
-  const int t = idx / spt, kc0 = (idx - t * spt) * 2;
-  const int row0 = r0 + t * kTileRows;
-  const int rows = min(kTileRows, r1 - row0);
+// First 32-row unit (chunk) of tile i of a slab of chunks [c0, c0 + n) cut into nt near-equal tiles.
+DI int tile_unit(int c0, int n, int nt, int i) { return c0 + static_cast<int>(static_cast<long>(i) * n / nt); }
+
+// The W boxes of the stage covering K chunks kc0, kc0 + 1 of the tile of
+// `units` 32-row units from row0: row r of K chunk j lands at slot + j *
+// kChunkSpace + r * 128 (SW128 atoms of 8 rows), so rows >= 128 start exactly
+// at the second UMMA's A operand (+16 KB).  Rows past V_local are zero-filled
+// by the TMA (and counted in the transaction bytes).
+DI void issue_w_stage(const CUtensorMap* map_w, const CUtensorMap* map_w32, uint8_t* slot, uint64_t* bar, int row0,
+                      int units, int kc0, uint64_t pol) {
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
     const int kc = kc0 + j;
-    uint8_t* dst = slot + j * kChunkBytes;
-    if (rows == kTileRows) {
+    uint8_t* dst = slot + j * kChunkSpace;
+    int u = 0;
+    if (units >= 4) {
       tma_load_2d(dst, map_w, bar, kc * kKChunk, row0, pol);
-    } else {  // slab tail: 8-row boxes land at the same swizzled offsets
-      for (int r = 0; r < rows; r += kRowGran) tma_load_2d(dst + r * 128, map_w8, bar, kc * kKChunk, row0 + r, pol);
+      u = 4;
     }
+    for (; u < units; ++u) tma_load_2d(dst + u * kChunkRows12 * 128, map_w32, bar, kc * kKChunk, row0 + u * kChunkRows12, pol);
   }
 }
 
@@ -181,7 +195,7 @@ DI void advance(int& stage, uint32_t& phase, int n) {
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    k12_proj_smooth(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_w8,
+    k12_proj_smooth(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_w32,
                     const __grid_constant__ CUtensorMap map_h, const __grid_constant__ CUtensorMap map_e,
                     const __grid_constant__ CUtensorMap map_f, const K1Args a, const K2Args b) {
   extern __shared__ uint8_t smem_raw[];
@@ -246,7 +260,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   unsigned long long t_start = 0ull;  // calibration stamps: from the dependency wait (thread 0)
   const int r0 = min(a.V_local, sc0 * KV), r1 = min(a.V_local, sc1 * KV);
-  const int ntiles = (r1 - r0 + kTileRows - 1) / kTileRows;
+  const int nunits = sc1 - sc0;                      // 32-row chunks of the slab
+  const int ntiles = (nunits + 4) / 5;               // W tiles of <= 5 chunks (kTileMax rows)
   const int n_own = sc1 - sc0, n_all = nc;
   const bool has_oth = n_all > n_own;
   const int hs = q;  // hidden slice of this CTA in the E phase (SPG == HS)
@@ -270,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 4 && lane == 0) {
     prefetch_tmap(&map_w);
-    prefetch_tmap(&map_w8);
+    prefetch_tmap(&map_w32);
     prefetch_tmap(&map_h);
     prefetch_tmap(&map_e);
     prefetch_tmap(&map_f);
@@ -305,9 +320,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t hbytes = (a.xbits & 1) ? 0u : hchunk;
     for (int i = 0; i < npre; ++i) {
       const int t = i / spt;
-      const int rows = min(kTileRows, r1 - (r0 + t * kTileRows));
-      mbar_expect_tx(&full[i], 2u * (static_cast<uint32_t>(rows) * 128u + hbytes));
-      issue_w_stage(&map_w, &map_w8, ring + i * L.wslot, &full[i], r0, r1, i, spt, pol_first);
+      const int u0 = tile_unit(sc0, nunits, ntiles, t), nu = tile_unit(sc0, nunits, ntiles, t + 1) - u0;
+      mbar_expect_tx(&full[i], 2u * (static_cast<uint32_t>(nu * KV) * 128u + hbytes));
+      issue_w_stage(&map_w, &map_w32, ring + i * L.wslot, &full[i], u0 * KV, nu, (i - t * spt) * 2, pol_first);
     }
   }
   if (warp == 5) tmem_alloc(&misc[0], 512);
@@ -341,11 +356,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = (npre == a.stages) ? 1u : 0u;
       for (int idx = npre; idx < nW; ++idx) {
         const int t = idx / spt, kc0 = (idx - t * spt) * 2;
-        const int rows = min(kTileRows, r1 - (r0 + t * kTileRows));
+        const int u0 = tile_unit(sc0, nunits, ntiles, t), nu = tile_unit(sc0, nunits, ntiles, t + 1) - u0;
         mbar_wait(&empty[stage], phase ^ 1u);
         uint8_t* slot = ring + stage * L.wslot;
-        mbar_expect_tx(&full[stage], 2u * (static_cast<uint32_t>(rows) * 128u + hbytes));
-        issue_w_stage(&map_w, &map_w8, slot, &full[stage], r0, r1, idx, spt, pol_first);
+        mbar_expect_tx(&full[stage], 2u * (static_cast<uint32_t>(nu * KV) * 128u + hbytes));
+        issue_w_stage(&map_w, &map_w32, slot, &full[stage], u0 * KV, nu, kc0, pol_first);
         for (int j = 0; j < 2 && ld_h; ++j)
           tma_load_2d(slot + kWBytes + j * hchunk, &map_h, &full[stage], (kc0 + j) * kKChunk, 0, pol_h);
         advance(stage, phase, a.stages);
@@ -396,9 +411,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = 0; t < ntiles; ++t) {
       const int buf = t & 1;
       const uint32_t use = static_cast<uint32_t>(t >> 1);
+      // a tile of more than 128 rows: a second UMMA over rows [128, 256) of each chunk
+      const bool two = tile_unit(sc0, nunits, ntiles, t + 1) - tile_unit(sc0, nunits, ntiles, t) > 4;
       mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
       tc_fence_after();
-      const uint32_t d = tmem_base + static_cast<uint32_t>(buf * N);
+      const uint32_t d = tmem_base + static_cast<uint32_t>(buf * 2 * N);
       for (int kc0 = 0; kc0 < a.num_kc; kc0 += 2) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
@@ -408,9 +425,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
-          for (int k = 0; k < kKChunk / 16; ++k)
-            mma_bf16_warp(d, sdesc_add(a0, j * kChunkBytes + k * 32), sdesc_add(b0, j * hchunk + k * 32), idesc_w,
-                          (kc0 + j) != 0 || k != 0);
+          for (int k = 0; k < kKChunk / 16; ++k) {
+            const uint64_t bd = sdesc_add(b0, j * hchunk + k * 32);
+            const uint32_t acc = ((kc0 + j) != 0 || k != 0) ? 1u : 0u;
+            mma_bf16_warp(d, sdesc_add(a0, j * kChunkSpace + k * 32), bd, idesc_w, acc);
+            if (two) mma_bf16_warp(d + N, sdesc_add(a0, j * kChunkSpace + kTileRows * 128 + k * 32), bd, idesc_w, acc);
+          }
         mma_commit_warp(&empty[stage]);
         advance(stage, phase, a.stages);
       }
@@ -561,8 +581,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t use = static_cast<uint32_t>(t >> 1);
       mbar_wait(&tfull[buf], use & 1u);
       tc_fence_after();
-      const int row0 = r0 + t * kTileRows;
-      const int rows = min(kTileRows, r1 - row0);
+      const int trow0 = min(a.V_local, KV * tile_unit(sc0, nunits, ntiles, t));
+      const int trows = min(a.V_local, KV * tile_unit(sc0, nunits, ntiles, t + 1)) - trow0;  // valid rows
+      for (int u = 0; u * kTileRows < trows; ++u) {  // the tile's UMMA outputs: rows [128 u, 128 u + 128)
+      const int row0 = trow0 + u * kTileRows;
+      const int rows = min(kTileRows, trows - u * kTileRows);
       const int rit = warp * 32 + lane;
       const bool valid = rit < rows;
       const int lv = row0 + rit;
@@ -572,7 +595,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int g = 0; g < kMaxGroups; ++g) {
         if (g < ng) {
           float x[32];
-          tmem_ld32(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(buf * N + g * 32),
+          tmem_ld32(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) +
+                        static_cast<uint32_t>((buf * 2 + u) * N + g * 32),
                     x);
           if (valid && (a.xbits & 2) == 0) {
 #pragma unroll
@@ -601,6 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           stat_combine(Rm[g], Ri[g], Rl[g], m[0], ix[0], l[0]);  // lane = column g*32+lane
         }
       }
+      }  // u
       tc_fence_before();
       mbar_arrive(&tempty[buf]);
     }
@@ -630,6 +655,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
         m_own[col] = 0.f;
       }
+      if (b.stack) scB[col] = m_own[col];  // the E phase's reference (ref below), ordered by the barrier
       if (!has_oth) m_oth[col] = neg_inf();
     }
     // Publish: flog rows, captured credited logits and the partial of this
@@ -660,9 +686,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // it by more than kRefGap nats -- then (practically never) the finished
     // own-row accumulation is rescaled in TMEM to the other slabs' max.
     constexpr float kRefGap = 32.f;
-    float* ref = scB;  // (stack mode does not use set B's scale)
-    if (b.stack)
-      for (int s = tid; s < N; s += kEpiThreads) ref[s] = m_own[s];
+    float* ref = scB;  // (stack mode does not use set B's scale); = m_own, written before the barrier above
     for (int j = 0; j < n_all; ++j) {
       if (j == n_own) {
         mbar_wait(oth_ready, 0);
@@ -859,7 +883,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     tr2[0] = tr[2];
     tr2[3] = globaltimer_ns();
   }
-  if (b.rank_fin) rank_finalize(b.rf, b.gbar, reinterpret_cast<float*>(ring));
+  if (b.rank_fin) {
+    unsigned long long* trf = (b.rf.trace != nullptr && threadIdx.x == 0) ? b.rf.trace + blockIdx.x * 5 : nullptr;
+    if (trf != nullptr && tr != nullptr) trf[4] = tr[4];
+    rank_finalize(b.rf, b.gbar, reinterpret_cast<float*>(ring), trf);
+  }
   if (tr != nullptr && threadIdx.x == 0) tr[3] = globaltimer_ns();
 }
 
@@ -884,14 +912,14 @@ int k12_blocks_per_sm(size_t smem) {
   return n;
 }
 
-cudaError_t launch_k12(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
+cudaError_t launch_k12(const CUtensorMap& map_w, const CUtensorMap& map_w32, const CUtensorMap& map_h,
                        const CUtensorMap& map_e, const CUtensorMap& map_f, const K1Args& a, const K2Args& b, int grid,
                        size_t smem, cudaStream_t st, bool pdl) {
   {
     const cudaError_t e = ensure_func_smem(reinterpret_cast<const void*>(k12_proj_smooth), smem);
     if (e != cudaSuccess) return e;
   }
-  return launch_ex(k12_proj_smooth, dim3(grid), dim3(kThreads), smem, st, pdl, map_w, map_w8, map_h, map_e, map_f, a,
+  return launch_ex(k12_proj_smooth, dim3(grid), dim3(kThreads), smem, st, pdl, map_w, map_w32, map_h, map_e, map_f, a,
                    b);
 }
 

@@ -115,6 +115,7 @@ struct RecArgs {
   unsigned* ctl;           // local control words: [0] epoch, [1] finished blocks of this kernel
   int K;                   // credit slots (fcred words per stats row, copied from `rec`)
   int loopback;            // measurement: peers are this GPU's own buffer, all `world` slots written
+  unsigned long long* trace;  // DINFER_TRACE (K12 fold): [grid][5] barrier passed, merged, stored, flag; smid
 };
 
 // ---------------------------------------------------------------- K2
@@ -155,7 +156,7 @@ size_t k12_smem_bytes(int N, int HW, int stages, int pstages, int slab_rows_max,
 // Co-resident K12 CTAs per SM at this shared-memory size (K12 CTAs of a vocab
 // group wait for each other's W phase, so the whole grid must be resident).
 int k12_blocks_per_sm(size_t smem);
-cudaError_t launch_k12(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
+cudaError_t launch_k12(const CUtensorMap& map_w, const CUtensorMap& map_w32, const CUtensorMap& map_h,
                        const CUtensorMap& map_e, const CUtensorMap& map_f, const K1Args& a, const K2Args& b, int grid,
                        size_t smem, cudaStream_t st, bool pdl);
 

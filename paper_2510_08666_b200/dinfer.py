@@ -382,9 +382,12 @@ class Context:
         buf = np.zeros(n, dtype=np.uint64)
         lib().dinfer_get_trace(self._h, c_void_p(buf.ctypes.data), n)
         g = self.geometry()
-        k1 = buf[:5 * g["k1_grid"]].reshape(-1, 5)
-        rest = buf[5 * g["k1_grid"]:].reshape(-1, 5)
-        return k1, rest[:-64], rest[-64:]  # K1, K2, K34 (first 64 blocks)
+        n1, n2 = 5 * g["k1_grid"], 5 * g["k2_grid"]
+        k1 = buf[:n1].reshape(-1, 5)
+        k2 = buf[n1:n1 + n2].reshape(-1, 5)
+        k34 = buf[n1 + n2:n1 + n2 + 5 * 64].reshape(-1, 5)
+        self.trace_rankfin = buf[n1 + n2 + 5 * 64:].reshape(-1, 5)  # K12 record finalize stamps
+        return k1, k2, k34  # K1, K2, K34 (first 64 blocks)
 
     def geometry(self) -> dict:
         g = Geometry()

@@ -152,3 +152,42 @@ def test_credit_table_resets_at_every_block():
     for i in firsts:
         assert not trace[i]["C"].any()
     assert any(r["C"].any() for r in trace if r["t"] > 0)
+
+
+def _stable_suite_tpf(base, seeds, nb=2, P=3):
+    """Mean TPF (T_i / F_i averaged over the suite) of the oracle's
+    generate() on a scripted stable suite: every position keeps ONE target for
+    the whole block (no flips) and its planted top logit rises monotonically,
+    ramp 1.0 per iteration plus a U(0,1) jitter, from below the threshold
+    (a0 ~ U[ln V - 3, ln V + 1], onset 0)."""
+    W64, W = _weights()
+    tpf = []
+    for seed in seeds:
+        sch = {}
+
+        def hidden_of(n, st):
+            k, t = st["block"], st["t"]
+            if k not in sch:
+                sch[k] = synth.PlantedSchedule(S, V, H, seed * 100 + k, ramp=1.0, flip_prob=0.0, onset_max=0)
+            tgt, a = sch[k].targets_and_amplitudes(t)
+            return O.bf16_bits_to_f64(sch[k].hidden(W[tgt], a)).reshape(1, S, H)
+
+        cfg = O.GenConfig(prompt_len=P, S=S, mask_id=MASK, eos_id=EOS, tau_target=0.9, early_termination=False)
+        out = O.generate(hidden_of, W64, None, None, _X0(1, P, nb, seed), cfg, base)
+        T, F = int(out["T"][0]), out["F"]
+        assert 1.0 <= T / F <= S                     # SPEC invariant: TPF in [1, S]
+        tpf.append(T / F)
+    return float(np.mean(tpf)), tpf
+
+
+def test_credit_mean_tpf_exceeds_threshold_on_stable_suite():
+    """SPEC S:542 (directional): on a suite whose under-threshold tokens are
+    stable and whose confidences rise monotonically, credit decoding (P:306-327,
+    the credit accumulated on the stable argmax raises its fused confidence)
+    commits earlier than plain threshold decoding at the same tau, so its mean
+    TPF is strictly higher; both decode the same targets."""
+    seeds = range(6)
+    thr, thr_each = _stable_suite_tpf(O.Params(decoder=O.DEC_THRESHOLD, tau=0.9), seeds)
+    cred, cred_each = _stable_suite_tpf(O.Params(decoder=O.DEC_THRESHOLD, tau=0.9, use_credit=True), seeds)
+    assert cred > thr, (cred_each, thr_each)
+    assert all(c >= t for c, t in zip(cred_each, thr_each)), (cred_each, thr_each)

@@ -31,10 +31,10 @@ def _gen_cfg(ocfg: O.GenConfig, L):
                            min(ocfg.max_forwards, 1 << 30))
 
 
-def _run(torch, B, nblocks, P, seed, base, ocfg, eos_at, K=16, repeats=1):
+def _run(torch, B, nblocks, P, seed, base, ocfg, eos_at, K=16, repeats=1, **sched):
     from paper_2510_08666_b200 import Context
     W, E = synth.make_W(V, H, 1), synth.make_E(V, H, 2)
-    hid, X0, ref = vetted_generation(W, E, B, S, nblocks, P, seed, base, ocfg, eos_at=eos_at)
+    hid, X0, ref = vetted_generation(W, E, B, S, nblocks, P, seed, base, ocfg, eos_at=eos_at, **sched)
     ctx = Context(B, S, H, K, V)
     Wd, Ed, emd = to_dev_bf16(W), to_dev_bf16(E), to_dev_bf16(E[ocfg.mask_id])
     hsrc = to_dev_bf16(hid)
@@ -94,3 +94,22 @@ def test_generate_on_the_fused_kernel(torch_cuda, monkeypatch):
                       alpha_init=0.1, alpha_growth=0.05, alpha_preset=0.3)
     _run(torch_cuda, 2, 3, 3, 7, base, cfg, eos_at=[(1, 1, 5)], repeats=2)
 
+
+
+def test_generate_credit_tpf_exceeds_threshold(torch_cuda):
+    """SPEC S:542 directional check, on the GPU loop: a stable suite (fixed
+    targets, confidence rising monotonically: ramp 1.0, onset 0, no flips),
+    every forward margin-vetted against the oracle.  X, T_b and F match the
+    oracle exactly for both decoders, and credit decoding's mean TPF
+    (T_i / F_i over the suite) strictly exceeds threshold
+    decoding's at the same tau."""
+    cfg = O.GenConfig(prompt_len=3, S=S, mask_id=V - 1, eos_id=V - 2, tau_target=0.9, early_termination=False)
+    tpf = {}
+    for name, base in (("threshold", O.Params(decoder=O.DEC_THRESHOLD)),
+                       ("credit", O.Params(decoder=O.DEC_THRESHOLD, use_credit=True))):
+        per = []
+        for seed in range(3):
+            ref = _run(torch_cuda, 1, 2, 3, 20 + seed, base, cfg, eos_at=[], ramp=1.0, flip_prob=0.0, onset_max=0)
+            per.append(ref["T"][0] / ref["F"])
+        tpf[name] = float(np.mean(per))
+    assert tpf["credit"] > tpf["threshold"], tpf

@@ -102,7 +102,7 @@ def vetted_trajectory(W_u16, E_u16, B, S, seed, params_fn, max_iters=None,
 
 
 def vetted_generation(W_u16, E_u16, B, S, nblocks, prompt_len, seed, base: O.Params, cfg: O.GenConfig,
-                      eos_at=(), ramp=2.5, flip_prob=0.1, max_rounds=400):
+                      eos_at=(), ramp=2.5, flip_prob=0.1, max_rounds=400, onset_max=5):
     """A whole blockwise generation (Alg. 1) driven by planted hidden states,
     every iteration vetted against the decision margins (c19) on the oracle's
     carried state.  Block k draws from PlantedSchedule(seed*100 + k); eos_at =
@@ -123,7 +123,8 @@ def vetted_generation(W_u16, E_u16, B, S, nblocks, prompt_len, seed, base: O.Par
     def hidden_of(n, st):
         k, t = st["block"], st["t"]
         if k not in schedules:
-            sch = synth.PlantedSchedule(M, V, H, seed * 100 + k, ramp=ramp, flip_prob=flip_prob)
+            sch = synth.PlantedSchedule(M, V, H, seed * 100 + k, ramp=ramp, flip_prob=flip_prob,
+                                        onset_max=onset_max)
             for (r, blk, off) in eos_at:
                 if blk == k:
                     sch.tgt[r * S + off] = cfg.eos_id

@@ -59,13 +59,16 @@ __global__ void ldg_kernel(const uint4* src, size_t words, unsigned long long* s
 }
 
 // TMA ring: one producer thread, stages of `bps` [128 x 64] bf16 boxes (16 KB each).
+// br = box rows (128: K12's W boxes; 32: its E boxes); a stage's boxes are
+// adjacent 64-column chunks of one br-row tile, so a stage covers br rows x
+// bps * 128 contiguous bytes per row.
 __global__ void __launch_bounds__(32) tma_kernel(const __grid_constant__ CUtensorMap map, int rows, int cols, int stages,
-                                                 int bps, unsigned long long* sink) {
+                                                 int bps, int br, unsigned long long* sink) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t box = 128u * 128u;
+  const uint32_t box = 128u * static_cast<uint32_t>(br);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(stages) * bps * box);
-  const int tiles = rows / 128;
+  const int tiles = rows / br;
   const int t0 = static_cast<int>(static_cast<long>(blockIdx.x) * tiles / gridDim.x);
   const int t1 = static_cast<int>(static_cast<long>(blockIdx.x + 1) * tiles / gridDim.x);
   const int nkc = cols / 64;
@@ -90,7 +93,7 @@ __global__ void __launch_bounds__(32) tma_kernel(const __grid_constant__ CUtenso
         for (int b = 0; b < nb; ++b, ++issued) {
           // adjacent K chunks of one 128-row tile first (K12's 256-B-per-row stage)
           const int tr = static_cast<int>(issued / nkc), kc = static_cast<int>(issued % nkc);
-          tma_load_2d(smem + (slot * bps + b) * box, &map, &full[slot], kc * 64, (t0 + tr) * 128, pol);
+          tma_load_2d(smem + (slot * bps + b) * box, &map, &full[slot], kc * 64, (t0 + tr) * br, pol);
         }
       }
     }
@@ -200,25 +203,32 @@ int main(int argc, char** argv) {
   cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fnp, cudaEnableDefault, &q);
   auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fnp);
-  CUtensorMap maps[kBufs];
-  for (int i = 0; i < kBufs; ++i) {
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
-    cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
-    enc(&maps[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf[i], dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  }
+  CUtensorMap maps[2][kBufs];  // box rows 128 / 32
+  for (int m = 0; m < 2; ++m)
+    for (int i = 0; i < kBufs; ++i) {
+      cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+      cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
+      cuuint32_t box[2] = {64, m == 0 ? 128u : 32u}, es[2] = {1, 1};
+      enc(&maps[m][i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf[i], dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
   cudaFuncSetAttribute(tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  const int tconf[][3] = {{4, 2, 1}, {5, 2, 1}, {6, 2, 1}, {3, 4, 1}, {2, 2, 2}, {3, 2, 2}, {2, 4, 2}, {1, 6, 2},
-                          {2, 1, 4}, {3, 1, 4}, {1, 2, 4}};
+  // {stages, boxes per stage, CTAs per SM, box rows}
+  const int tconf[][4] = {{4, 2, 1, 128}, {5, 2, 1, 128}, {6, 2, 1, 128}, {3, 4, 1, 128}, {2, 4, 1, 128},
+                          {2, 2, 2, 128}, {3, 2, 2, 128}, {2, 4, 2, 128}, {1, 6, 2, 128}, {2, 1, 4, 128},
+                          {3, 1, 4, 128}, {1, 2, 4, 128},
+                          {3, 16, 1, 32}, {2, 16, 1, 32}, {4, 8, 1, 32}, {6, 8, 1, 32}, {6, 4, 1, 32},
+                          {12, 4, 1, 32}, {2, 32, 1, 32}, {3, 8, 2, 32}};
   for (auto& c : tconf) {
-    const int stages = c[0], bps = c[1], cps = c[2];
-    const size_t smem = static_cast<size_t>(stages) * bps * 16384 + stages * 8 + 1024;
+    const int stages = c[0], bps = c[1], cps = c[2], br = c[3];
+    const size_t smem = static_cast<size_t>(stages) * bps * 128 * br + stages * 8 + 1024;
     if (smem * cps > 228 * 1024) continue;
     char name[96];
-    snprintf(name, sizeof(name), "TMA 2-D %d CTA/SM %d x %3d KB stages", cps, stages, bps * 16);
+    snprintf(name, sizeof(name), "TMA 2-D %d CTA/SM %2d x %3d KB (%3d rows x %4d B)", cps, stages, bps * br / 8, br,
+             bps * 128);
     measure(name, bytes, [&](int r) {
-      tma_kernel<<<sms * cps, 32, smem>>>(maps[r % kBufs], rows, cols, stages, bps, sink);
+      tma_kernel<<<sms * cps, 32, smem>>>(maps[br == 128 ? 0 : 1][r % kBufs], rows, cols, stages, bps, br, sink);
     });
   }
   // (3) 1-D bulk
