@@ -465,7 +465,7 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
     ev_finish(c, kPK1);
   } else {
     ev_begin(c, kPK1);
-    DI_CUDA(launch_k1(c->map_w, c->map_w8, c->map_h, a, c->k1_grid, c->k1_smem, c->stream, c->pdl));
+    DI_CUDA(launch_k1(c->map_w, c->map_w8, c->map_w32, c->map_h, a, c->k1_grid, c->k1_smem, c->stream, c->pdl));
     ev_finish(c, kPK1);
   }
   if (smooth && !c->fused) {

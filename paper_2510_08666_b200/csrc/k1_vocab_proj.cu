@@ -36,9 +36,23 @@ constexpr int kThreads = (kEpiWarps + 2) * kWarpThreads;
 // streaming at ~4.7 TB/s on B200, adjacent pairs reach ~5.6 TB/s
 // (tools/hbm_stream.cu, profiles/).
 constexpr int kChunksPerStage = 2;
-constexpr uint32_t kChunkBytes = kTileRows * 128;                 // 16 KB
-constexpr uint32_t kWStageBytes = kChunksPerStage * kChunkBytes;  // 32 KB
+// W tiles of up to kTileMax rows (N <= 128; 128 rows for larger N, whose
+// double-buffered accumulators already fill the TMEM): rows [0, 128) are one
+// UMMA, rows [128, 160) a second one over the next 128 rows of the chunk
+// space (rows past the tile are stale and ignored).  A slab is cut into
+// 32-row units (the last one may be shorter) grouped into near-equal tiles
+// of <= 5 units, so tiles are loaded as one 128-row box plus 32-row boxes
+// (8-row boxes only for the slab's last < 32 rows) -- short tail tiles of
+// 8-row boxes streamed at a fraction of the rate (K12 trace).
+constexpr int kTileMax = 160;
+constexpr uint32_t kChunkBytes = kTileMax * 128;                  // chunk space: 20 KB
+constexpr uint32_t kWStageBytes = kChunksPerStage * kChunkBytes;  // 40 KB
 constexpr int kMaxGroups = 8;                       // N <= 256
+constexpr int kUnit = 32;                           // rows per tile unit
+
+DI int unit_row(int r0, int r1, int nu, int u) { return min(r1, r0 + u * kUnit); }
+// first unit of tile t of nt tiles over nu units
+DI int tile_u(int nu, int nt, int t) { return static_cast<int>(static_cast<long>(t) * nu / nt); }
 
 __host__ __device__ inline uint32_t tmem_cols_pow2(uint32_t n) {
   uint32_t c = 32;
@@ -99,7 +113,8 @@ __host__ __device__ inline Layout make_layout(int N, int H, int stages, int h_re
 
 __global__ void __launch_bounds__(kThreads, 1)
     k1_vocab_proj(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_w8,
-                  const __grid_constant__ CUtensorMap map_h, const K1Args a) {
+                  const __grid_constant__ CUtensorMap map_w32, const __grid_constant__ CUtensorMap map_h,
+                  const K1Args a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const Layout L = make_layout(a.N, a.H, a.stages, a.h_resident, a.slab_rows_max);
@@ -135,13 +150,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     r1 = min(a.V_local, a.slab_start[blockIdx.x + 1]);
   }
   unsigned long long t_start = 0ull;  // calibration stamp: from the dependency wait (thread 0)
-  const int ntiles = (r1 - r0 + kTileRows - 1) / kTileRows;
-  const uint32_t tmem_cols = tmem_cols_pow2(2u * N);
+  const bool big = 4 * N <= 512;                        // tiles of up to 160 rows (two UMMA outputs)
+  const int umax = big ? kTileMax / kUnit : kTileRows / kUnit;
+  const int nu = (r1 - r0 + kUnit - 1) / kUnit;          // units (the last may be short)
+  const int ntiles = (nu + umax - 1) / umax;
+  const uint32_t tmem_cols = tmem_cols_pow2((big ? 4u : 2u) * N);
+  const uint32_t acc_stride = (big ? 2u : 1u) * N;       // TMEM columns per accumulator buffer
 
   if (a.trace != nullptr && threadIdx.x == 0) { a.trace[blockIdx.x * 5 + 0] = globaltimer_ns(); uint32_t sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm)); a.trace[blockIdx.x * 5 + 4] = sm; }
   if (warp == 4 && lane == 0) {
     prefetch_tmap(&map_w);
     prefetch_tmap(&map_w8);
+    prefetch_tmap(&map_w32);
     prefetch_tmap(&map_h);
     for (int i = 0; i < a.stages; ++i) {
       mbar_init(&full[i], 1);
@@ -174,8 +194,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = 0; t < ntiles; ++t) {
-        const int row0 = r0 + t * kTileRows;
-        const int rows = min(kTileRows, r1 - row0);
+        const int row0 = unit_row(r0, r1, nu, tile_u(nu, ntiles, t));
+        const int rows = unit_row(r0, r1, nu, tile_u(nu, ntiles, t + 1)) - row0;
         for (int kc0 = 0; kc0 < a.num_kc; kc0 += kChunksPerStage) {
           mbar_wait(&empty[stage], phase ^ 1u);
           // hidden chunk kc rides with W chunk kc: every stage when streamed,
@@ -188,12 +208,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < kChunksPerStage; ++j) {
             const int kc = kc0 + j;
             uint8_t* dst = w_sm + stage * kWStageBytes + j * kChunkBytes;
-            if (rows == kTileRows) {
+            // row r lands at dst + r * 128 (SW128 atoms of 8 rows): one 128-row
+            // box, 32-row boxes, 8-row boxes for the slab's last < 32 rows
+            int r = 0;
+            if (rows >= kTileRows) {
               tma_load_2d(dst, &map_w, &full[stage], kc * kKChunk, row0, pol_w);
-            } else {  // slab tail: 8-row boxes land at the same swizzled offsets
-              for (int r = 0; r < rows; r += kRowGran)
-                tma_load_2d(dst + r * 128, &map_w8, &full[stage], kc * kKChunk, row0 + r, pol_w);
+              r = kTileRows;
             }
+            for (; r + kUnit <= rows; r += kUnit)
+              tma_load_2d(dst + r * 128, &map_w32, &full[stage], kc * kKChunk, row0 + r, pol_w);
+            for (; r < rows; r += kRowGran)
+              tma_load_2d(dst + r * 128, &map_w8, &full[stage], kc * kKChunk, row0 + r, pol_w);
             if (with_h)
               tma_load_2d(h_sm + (a.h_resident ? kc : stage * kChunksPerStage + j) * hchunk, &map_h, &full[stage],
                           kc * kKChunk, 0, pol_h);
@@ -216,9 +241,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = 0; t < ntiles; ++t) {
       const int buf = t & 1;
       const uint32_t use = static_cast<uint32_t>(t >> 1);
+      const bool two = unit_row(r0, r1, nu, tile_u(nu, ntiles, t + 1)) - unit_row(r0, r1, nu, tile_u(nu, ntiles, t)) >
+                       kTileRows;
       mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
       tc_fence_after();
-      const uint32_t d = tmem_base + static_cast<uint32_t>(buf * N);
+      const uint32_t d = tmem_base + static_cast<uint32_t>(buf) * acc_stride;
       for (int kc0 = 0; kc0 < a.num_kc; kc0 += kChunksPerStage) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
@@ -229,9 +256,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < kChunksPerStage; ++j)
 #pragma unroll
-          for (int k = 0; k < kKChunk / 16; ++k)
-            mma_bf16_warp(d, sdesc_add(a0, j * kChunkBytes + k * 32), sdesc_add(b0, j * hchunk + k * 32), idesc,
-                          ((kc0 + j) | k) != 0);
+          for (int k = 0; k < kKChunk / 16; ++k) {
+            const uint64_t bd = sdesc_add(b0, j * hchunk + k * 32);
+            const uint32_t acc = ((kc0 + j) | k) != 0;
+            mma_bf16_warp(d, sdesc_add(a0, j * kChunkBytes + k * 32), bd, idesc, acc);
+            if (two) mma_bf16_warp(d + N, sdesc_add(a0, j * kChunkBytes + kTileRows * 128 + k * 32), bd, idesc, acc);
+          }
         mma_commit_warp(&empty[stage]);  // frees the smem slot when these MMAs finish
         if (++stage == a.stages) {
           stage = 0;
@@ -296,8 +326,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t use = static_cast<uint32_t>(t >> 1);
       mbar_wait(&tfull[buf], use & 1u);
       tc_fence_after();
-      const int row0 = r0 + t * kTileRows;
-      const int rows = min(kTileRows, r1 - row0);
+      const int trow0 = unit_row(r0, r1, nu, tile_u(nu, ntiles, t));
+      const int trows = unit_row(r0, r1, nu, tile_u(nu, ntiles, t + 1)) - trow0;
+      for (int u = 0; u * kTileRows < trows; ++u) {  // the tile's UMMA outputs: rows [128 u, 128 u + 128)
+      const int row0 = trow0 + u * kTileRows;
+      const int rows = min(kTileRows, trows - u * kTileRows);
       const int rit = warp * 32 + lane;
       const bool valid = rit < rows;
       const int lv = row0 + rit;
@@ -307,7 +340,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int g = 0; g < kMaxGroups; ++g) {
         if (g < ng) {
           float x[32];
-          tmem_ld32(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(buf * N + g * 32),
+          tmem_ld32(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(buf) * acc_stride +
+                        static_cast<uint32_t>(u * N + g * 32),
                     x);
           if (a.flog != nullptr && valid) {
 #pragma unroll
@@ -336,6 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           stat_combine(Rm[g], Ri[g], Rl[g], m[0], ix[0], l[0]);  // lane = column g*32+lane
         }
       }
+      }  // u
       tc_fence_before();
       mbar_arrive(&tempty[buf]);
     }
@@ -388,13 +423,13 @@ size_t k1_smem_bytes(int N, int H, int stages, int h_resident, int slab_rows_max
   return make_layout(N, H, stages, h_resident, slab_rows_max).total + 1024;
 }
 
-cudaError_t launch_k1(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
-                      const K1Args& a, int grid, size_t smem, cudaStream_t st, bool pdl) {
+cudaError_t launch_k1(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_w32,
+                      const CUtensorMap& map_h, const K1Args& a, int grid, size_t smem, cudaStream_t st, bool pdl) {
   {
     const cudaError_t e = ensure_func_smem(reinterpret_cast<const void*>(k1_vocab_proj), smem);
     if (e != cudaSuccess) return e;
   }
-  return launch_ex(k1_vocab_proj, dim3(grid), dim3(kThreads), smem, st, pdl, map_w, map_w8, map_h, a);
+  return launch_ex(k1_vocab_proj, dim3(grid), dim3(kThreads), smem, st, pdl, map_w, map_w8, map_w32, map_h, a);
 }
 
 }  // namespace dinfer

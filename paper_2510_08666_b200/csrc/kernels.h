@@ -81,8 +81,8 @@ struct K1Args {
                            //   1 no hidden loads, 2 no flog stores, 4 W evict_normal, 8 E evict_normal
 };
 size_t k1_smem_bytes(int N, int H, int stages, int h_resident, int slab_rows_max);
-cudaError_t launch_k1(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_h,
-                      const K1Args& a, int grid, size_t smem, cudaStream_t st, bool pdl);
+cudaError_t launch_k1(const CUtensorMap& map_w, const CUtensorMap& map_w8, const CUtensorMap& map_w32,
+                      const CUtensorMap& map_h, const K1Args& a, int grid, size_t smem, cudaStream_t st, bool pdl);
 
 // ---------------------------------------------------------------- K1b (M > 256)
 struct K1bArgs {
