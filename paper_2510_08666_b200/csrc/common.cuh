@@ -76,6 +76,19 @@ DI uint64_t globaltimer_ns() {
 // prefetch) while its predecessor drains; grid_dep_wait() blocks until the
 // predecessor grid has completed and its memory is visible.  Both are no-ops
 // for a normally launched kernel.
+// Ordered-uint encoding of a float (monotone: a < b  <=>  f2ord(a) < f2ord(b);
+// 0 is below every encoded value), for atomicMax over floats.
+DI unsigned f2ord(float f) {
+  const unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+DI float ord2f(unsigned u) { return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u); }
+DI unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 DI void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 DI void grid_dep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

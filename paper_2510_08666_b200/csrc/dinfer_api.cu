@@ -76,15 +76,16 @@ struct dinfer_ctx {
   size_t k1_smem = 0;
   int k2_HW = 0, k2_HS = 0, k2_VG = 0, k2_stages = 0, k2_pstages = 0, k2_nchunks = 0, k2_KV = 64;
   size_t k2_smem = 0;
-  // peer-memory exchange (world > 1): gather buffer [2 slots][world][full_words]
-  // + flags [2][world] (IPC-shared), local control words, opened peer buffers
+  // peer-memory exchange (world > 1): this rank's record, double-buffered by
+  // epoch parity [2][full_words], + flags [2][world] (IPC-shared; peers read
+  // the record in place), local control words, opened peer buffers
   float* xbuf = nullptr;
   unsigned* xctl = nullptr;
   float** d_peers = nullptr;
   float* peer_host[8] = {};
   bool p2p = false;
   bool loopback = false;  // dinfer_exchange_loopback: measurement of one rank of a G-way shard
-  long xslot = 0, xflags_off = 0;
+  long xflags_off = 0;
   // K12 (K1 + K2 fused, smoothing steps with N <= 64): the k2_* fields then
   // describe its E phase (HW, HS, VG, KV = 16) and k1_VG x k1_SPG its slabs
   bool fused = false;
@@ -104,10 +105,10 @@ struct dinfer_ctx {
   int k12_npre = 0;           // env DINFER_K12_NPRE: W stages issued before the dependency wait (0 = ring)
   int k12_x = 0;              // env DINFER_K12_X: measurement-only K12 experiments (kernels.h K1Args::xbits)
   int k12_stack = 0;          // K12 E phase: hi / lo P stacked into one MMA (K2Args::stack)
+  bool k12_rec_g1 = false;    // world 1 in K12 record mode too (env DINFER_K12_RECORD=1; measurement)
   int k12_emin = 2;           // K12 E-ring depth the smem layout is sized for (K2Args::emin)
-  bool rankfin_ok = false;    // K12 can fold the record finalize (rank_fin.cuh: <= 8 rows per CTA slice)
-  bool rankfin_g1 = false;    // world 1 also takes the record path (env DINFER_RANKFIN_G1; measurement)
-  unsigned* gbar = nullptr;   // K12 grid barrier words [count, generation]
+  unsigned* mx = nullptr;     // K12 record mode: [M] ordered-uint max of the slab maxima (self-resetting)
+  unsigned* rcnt = nullptr;   // K12 record mode: [4] W done, finish ticket, CTAs done (self-resetting)
   bool record_wdur = false;
   int f_stages = 0, f_pstages = 0;
   size_t f_smem = 0;
@@ -338,40 +339,31 @@ dinfer_status ensure_maps(dinfer_ctx* c, const uint16_t* hidden, const uint16_t*
   return DINFER_OK;
 }
 
-// K1 (+ K2, + K2r into the record when `reduce_acc`).  `rec` receives the
-// statistics part of this rank's record (and the acc part when reduce_acc).
+// K1 (+ K2, + the record finalize when `reduce_acc`), or K12.  `rec` is the
+// record this rank's step writes: the captured credited logits always; with
+// `reduce_acc` (the record leaves the rank: sharded / split-phase) also the
+// merged statistics; with K12 (smoothing steps) always the smoothing
+// accumulator (record mode: fp32, relative to the rank max, added by every CTA
+// with L2 reductions -- it must be zero at entry: the previous step's K34
+// zeroes it after use).  `rec` == xbuf: the double-buffered exchange record,
+// whose completion raises this rank's flag in every peer.
 dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W, const uint16_t* E,
                         const uint8_t* mask, const int32_t* credit_ids, const dinfer_params* p, float* rec,
-                        bool reduce_acc, const float* credit_val = nullptr) {
+                        bool reduce_acc, const float* credit_val = nullptr, bool k12_record = true) {
   const bool smooth = p->use_smooth != 0;
   dinfer_status s = ensure_maps(c, hidden, W, smooth ? E : nullptr);
   if (s != DINFER_OK) return s;
-  RecArgs r{};  // the rank record (sharded / split-phase): stats (+ acc) finalize
-  if (reduce_acc) {
-    r.M = c->M;
-    r.H = c->shp.H;
-    r.grid1 = c->k1_grid;
-    r.VG = c->k2_VG;
-    r.rec_stride = kStatWords + c->shp.K;
-    r.part1 = reinterpret_cast<const float4*>(c->part1);
-    r.part2 = smooth ? c->part2 : nullptr;
-    r.mref = c->mref;
-    r.rec = rec;
-    r.rec_acc = rec + c->stats_words;
-    r.K = c->shp.K;
-    if (c->trace != nullptr) r.trace = c->trace + 5 * (c->k1_grid + c->k2_HS * c->k2_VG + kTraceK34);
-    if (c->p2p && rec == c->rec_local) {  // dinfer_step: push the record into every rank's gather buffer
-      r.peers = c->d_peers;
-      r.world = c->shp.world;
-      r.rank = c->shp.rank;
-      r.rec_words = static_cast<long>(c->full_words);
-      r.flags_off = c->xflags_off;
-      r.ctl = c->xctl;
-      r.loopback = c->loopback ? 1 : 0;
-    }
+  const bool xrec = c->p2p && rec == c->xbuf;  // the exchange record (double-buffered, flags)
+  XArgs x{};
+  if (xrec) {
+    x.peers = c->d_peers;
+    x.world = c->shp.world;
+    x.rank = c->shp.rank;
+    x.flags_off = c->xflags_off;
+    x.ctl = c->xctl;
+    x.loopback = c->loopback ? 1 : 0;
   }
-  // K12 folds the record finalize into its tail (rank_fin.cuh) -- no extra launch
-  const bool fold = reduce_acc && smooth && c->fused && c->rankfin_ok;
+  const long par_words = xrec ? static_cast<long>(c->full_words) : 0;
   K1Args a{};
   a.M = c->M;
   a.N = c->N;
@@ -392,6 +384,8 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
   a.part = c->part1;
   a.grp_cnt = smooth ? c->grp_cnt : nullptr;  // K2 consumes the group counts
   a.rec = rec;
+  a.rec_par = par_words;
+  a.rec_ctl = c->xctl;
   a.flog = smooth ? c->flog : nullptr;
   a.mask_snap = smooth ? c->mask_snap : nullptr;
   a.credit_val = nullptr;
@@ -406,8 +400,8 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
   if (c->record_wdur) a.wdur = c->d_wdur;
   if (c->k1_balanced && !(smooth && c->fused)) a.slab_start = c->d_slab;
   if (smooth && c->fused) {
-    // K12: the vocab slab partition at 16-row chunk granularity (nchunks /
-    // chunk_rows), the E phase over the slab's vocab group
+    // K12: the vocab slab partition at 32-row chunk granularity (nchunks /
+    // chunk_rows), the E phase over the slab's vocab group, record mode
     a.stages = c->f_stages;
     a.npre = std::min(c->k12_npre, c->f_stages);
     a.xbits = c->k12_x;
@@ -442,11 +436,16 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
     b.trace = c->trace == nullptr ? nullptr : c->trace + 5 * c->k1_grid;
     b.stack = c->k12_stack;
     b.emin = c->k12_emin;
-    if (fold) {
-      b.rank_fin = 1;
-      b.gbar = c->gbar;
-      b.rf = r;
-    }
+    // record mode (sharded / split-phase; world 1 only with DINFER_K12_RECORD=1):
+    // the accumulator goes into `rec`; otherwise per-group fp16 partials (K34 merges them)
+    b.rec_acc = k12_record ? rec + c->stats_words : nullptr;
+    b.rec_stats = rec;
+    b.rec_par = par_words;
+    b.rec_stride = kStatWords + c->shp.K;
+    b.merge_stats = reduce_acc ? 1 : 0;
+    b.mx = c->mx;
+    b.rcnt = c->rcnt;
+    b.x = x;
     if (c->k12_probe) {
       if (c->probe_h == nullptr) {
         void* hp = nullptr;
@@ -463,12 +462,12 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
     DI_CUDA(launch_k12(c->map_w, c->map_w32, c->map_h, c->map_e, c->map_f, a, b, c->k1_grid, c->f_smem, c->stream,
                        c->pdl));
     ev_finish(c, kPK1);
-  } else {
-    ev_begin(c, kPK1);
-    DI_CUDA(launch_k1(c->map_w, c->map_w8, c->map_w32, c->map_h, a, c->k1_grid, c->k1_smem, c->stream, c->pdl));
-    ev_finish(c, kPK1);
+    return DINFER_OK;
   }
-  if (smooth && !c->fused) {
+  ev_begin(c, kPK1);
+  DI_CUDA(launch_k1(c->map_w, c->map_w8, c->map_w32, c->map_h, a, c->k1_grid, c->k1_smem, c->stream, c->pdl));
+  ev_finish(c, kPK1);
+  if (smooth) {
     K2Args b{};
     b.M = c->M;
     b.N = c->N;
@@ -495,7 +494,21 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
     DI_CUDA(launch_k2(c->map_e, c->map_f, b, c->k2_smem, c->stream, c->pdl));
     ev_finish(c, kPK2);
   }
-  if (reduce_acc && !fold) {  // the record finalize as its own kernel (K1 / K1 -> K2 paths)
+  if (reduce_acc) {  // the record finalize (K1 / K1 -> K2 paths): merged stats (+ acc) into `rec`
+    RecArgs r{};
+    r.M = c->M;
+    r.H = c->shp.H;
+    r.grid1 = c->k1_grid;
+    r.VG = c->k2_VG;
+    r.rec_stride = kStatWords + c->shp.K;
+    r.part1 = reinterpret_cast<const float4*>(c->part1);
+    r.part2 = smooth ? c->part2 : nullptr;
+    r.mref = c->mref;
+    r.rec = rec;
+    r.acc_off = static_cast<long>(c->stats_words);
+    r.par_words = par_words;
+    r.x = x;
+    if (!xrec) r.x.ctl = c->xctl;  // (unused without peers / par_words)
     ev_begin(c, kPK2r);
     DI_CUDA(launch_rec_finalize(r, c->stream, c->pdl));
     ev_finish(c, kPK2r);
@@ -503,10 +516,23 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
   return DINFER_OK;
 }
 
-// K3 (+ K4).  `recs` = `world` records spaced `rec_words` apart.  When
-// `acc_from_part2`, K4 sums the VG partials of this (single) rank directly.
-dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, int world, bool acc_from_part2,
-                          const uint16_t* e_mask, uint8_t* mask, int32_t* tokens, int32_t* credit_ids,
+// Where K34's smoothing blocks find the accumulator: the VG fp16 per-group
+// partials of this single rank (K1 -> K2), the `world` rank records (each
+// relative to its own merged max), or ONE record relative to the merged max
+// itself (world-1 K12 record mode).  `zero`: the record acc K34 zeroes for
+// the next step (`zero_par` > 0: the other slot of the double-buffered one).
+enum AccMode { kAccPartials, kAccRecords, kAccUnit };
+struct AccSrc {
+  AccMode mode;
+  float* zero;
+  long zero_par;
+};
+
+// K3 (+ K4).  `recs` = `world` records spaced `rec_words` apart (or the
+// exchange buffer: the peers' records read in place).  `stats_part1`: the
+// statistics are merged from this (single) rank's slab partials.
+dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, int world, bool stats_part1,
+                          AccSrc acc, const uint16_t* e_mask, uint8_t* mask, int32_t* tokens, int32_t* credit_ids,
                           float* credit_val, const dinfer_params* p, uint8_t* committed, float* smoothed,
                           float* stats, int rec_stride = -1, const uint16_t* E = nullptr, uint16_t* emb = nullptr) {
   K3Args k{};
@@ -522,7 +548,7 @@ dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, in
   k.S = c->shp.S;
   k.K = c->shp.K;
   k.world = world;
-  k.part1 = acc_from_part2 ? reinterpret_cast<const float4*>(c->part1) : nullptr;  // single-rank dinfer_step
+  k.part1 = stats_part1 ? reinterpret_cast<const float4*>(c->part1) : nullptr;  // single-rank dinfer_step
   k.grid1 = c->k1_grid;
   k.recs = recs;
   k.rec_words = static_cast<long>(rec_words);
@@ -548,16 +574,18 @@ dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, in
   k.c_gamma = p->c_gamma;
   k.pdev = c->pdev_active;
   k.err = c->err;
-  if (c->p2p && recs == c->xbuf) {
+  if (c->p2p && recs == c->xbuf) {  // the ranks' exchange records, read in place
     k.xflags = reinterpret_cast<const unsigned*>(c->xbuf + c->xflags_off);
     k.xctl = c->xctl;
-    k.xslot = c->xslot;
+    k.recs = nullptr;
+    for (int j = 0; j < 8; ++j) k.rpv[j] = c->peer_host[j];
+    k.rpar = static_cast<long>(c->full_words);
   }
   K4Args f{};
   if (p->use_smooth) {
     f.M = c->M;
     f.H = c->shp.H;
-    if (acc_from_part2) {
+    if (acc.mode == kAccPartials) {
       f.acc_h = c->part2;
       f.acc_stride = static_cast<long>(c->M) * c->shp.H;
       f.nparts = c->k2_VG;
@@ -565,12 +593,11 @@ dinfer_status run_combine(dinfer_ctx* c, const float* recs, size_t rec_words, in
       f.m_stride = c->M;
       f.m_rowstride = 1;
     } else {
-      f.acc = recs + c->stats_words;
-      f.acc_stride = static_cast<long>(rec_words);
-      f.nparts = world;
-      f.m_part = recs;
-      f.m_stride = static_cast<long>(rec_words);
-      f.m_rowstride = kStatWords + c->shp.K;
+      f.rec_mode = 1;
+      f.rec_unit = acc.mode == kAccUnit ? 1 : 0;
+      f.acc_off = static_cast<long>(c->stats_words);
+      f.zero_acc = acc.zero;
+      f.zero_par = acc.zero_par;
     }
     f.mask_start = c->mask_snap;
     f.e_mask = e_mask;
@@ -659,7 +686,7 @@ void dinfer_destroy(dinfer_ctx* c) {
 #ifdef DINFER_WITH_NCCL
   if (c->has_comm) ncclCommDestroy(c->comm);
 #endif
-  void* bufs[] = {c->part1, c->counter, c->err, c->gbar, c->rec_local, c->flog, c->part2, c->ml, c->sel, c->row_cnt, c->trace,
+  void* bufs[] = {c->part1, c->counter, c->err, c->mx, c->rcnt, c->rec_local, c->flog, c->part2, c->ml, c->sel, c->row_cnt, c->trace,
                   c->mref,
                   c->mask_snap, c->rowdone, c->cids_snap, c->cval_snap, c->xbuf, c->xctl, c->d_peers,
                   c->d_role, c->d_split, c->d_wdur, c->d_slab, c->d_gstart,
@@ -910,12 +937,8 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
   c->k12_probe = std::getenv("DINFER_K12_PROBE") != nullptr;
   if (const char* e = std::getenv("DINFER_K12_NPRE")) c->k12_npre = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("DINFER_K12_X")) c->k12_x = std::atoi(e);
-  if (c->fused) {  // rank_fin.cuh: a CTA's slice of the flat [M][H] spans <= 8 rows
-    const long per = (static_cast<long>(M) * s.H / 4 + c->k1_grid - 1) / c->k1_grid;
-    c->rankfin_ok = (per * 4) / s.H + 2 <= 8;
-    if (const char* e = std::getenv("DINFER_RANKFIN")) c->rankfin_ok = c->rankfin_ok && std::atoi(e) != 0;
-    if (const char* e = std::getenv("DINFER_RANKFIN_G1")) c->rankfin_g1 = c->rankfin_ok && std::atoi(e) != 0;
-  }
+  if (const char* e = std::getenv("DINFER_K12_RECORD")) c->k12_rec_g1 = std::atoi(e) != 0;
+
 
   // ---- workspace
   // stats part padded to a multiple of 4 words: the acc part (and every record
@@ -927,7 +950,10 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
   A(dev_alloc(&c->part1, static_cast<size_t>(c->dense ? c->kb_VG : c->k1_grid) * M * 4));
   A(dev_alloc(&c->counter, 4));
   A(dev_alloc(&c->err, 4));
-  A(dev_alloc(&c->gbar, 4));
+  if (c->fused) {
+    A(dev_alloc(&c->mx, static_cast<size_t>(M)));
+    A(dev_alloc(&c->rcnt, 4));
+  }
   A(dev_alloc(&c->rec_local, c->full_words));
   A(dev_alloc(&c->ml, static_cast<size_t>(M) * 2));
   A(dev_alloc(&c->sel, static_cast<size_t>(M)));
@@ -950,8 +976,7 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
   }
   if (s.world > 1) {
     A(dev_alloc(&c->rec_all, c->full_words * s.world));
-    c->xslot = static_cast<long>(c->full_words) * s.world;
-    c->xflags_off = 2 * c->xslot;
+    c->xflags_off = 2 * static_cast<long>(c->full_words);  // [2][full_words] record slots, then the flags
     A(dev_alloc(&c->xbuf, static_cast<size_t>(c->xflags_off) + 2 * s.world + 4));
     A(dev_alloc(&c->xctl, 4));
     A(dev_alloc(&c->d_peers, 8));
@@ -966,13 +991,14 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
     A(dev_alloc(&c->grp_pass, static_cast<size_t>(c->k2_VG)));
   }
   if (std::getenv("DINFER_TRACE") != nullptr && std::atoi(std::getenv("DINFER_TRACE")) != 0)
-    A(dev_alloc(&c->trace, static_cast<size_t>(5) * (2 * c->k1_grid + c->k2_HS * c->k2_VG + kTraceK34)));
+    A(dev_alloc(&c->trace, static_cast<size_t>(5) * (c->k1_grid + c->k2_HS * c->k2_VG + kTraceK34)));
   if (st == DINFER_OK) {
     if (c->grp_cnt != nullptr && (cudaMemset(c->grp_cnt, 0, 4 * c->k2_VG) != cudaSuccess ||
                                   cudaMemset(c->grp_pass, 0, 4 * c->k2_VG) != cudaSuccess))
       st = DINFER_ERR_CUDA;
     if (cudaMemset(c->counter, 0, 16) != cudaSuccess || cudaMemset(c->err, 0, 16) != cudaSuccess ||
-        cudaMemset(c->gbar, 0, 16) != cudaSuccess ||
+        (c->mx != nullptr && cudaMemset(c->mx, 0, 4 * static_cast<size_t>(M)) != cudaSuccess) ||
+        (c->rcnt != nullptr && cudaMemset(c->rcnt, 0, 16) != cudaSuccess) ||
         cudaMemset(c->row_cnt, 0, 4 * static_cast<size_t>(s.B)) != cudaSuccess ||
         cudaMemset(c->rowdone, 0, 4 * static_cast<size_t>(M)) != cudaSuccess ||
         (c->xbuf != nullptr && cudaMemset(c->xbuf, 0, 4 * (static_cast<size_t>(c->xflags_off) + 2 * s.world + 4)) !=
@@ -1519,35 +1545,47 @@ dinfer_status step_impl(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
     ev_begin(c, kPK1);
     DI_CUDA(launch_k1b(c->map_h, c->map_w, kb, c->kb_grid, c->kb_smem, c->stream, c->pdl));
     ev_finish(c, kPK1);
-    return run_combine(c, c->part1, static_cast<size_t>(c->M) * 4, c->kb_VG, false, e_mask, mask, tokens,
-                       credit_ids, credit_val, p, committed, smoothed, stats, /*rec_stride=*/4);
+    return run_combine(c, c->part1, static_cast<size_t>(c->M) * 4, c->kb_VG, false, AccSrc{kAccPartials, nullptr, 0},
+                       e_mask, mask, tokens, credit_ids, credit_val, p, committed, smoothed, stats, /*rec_stride=*/4);
   }
   const bool smooth = p->use_smooth != 0;
-  // world 1: K34 merges the slab / group partials itself, unless the record
-  // path is asked for (DINFER_RANKFIN_G1: K12 folds the merge into its tail)
-  const bool g1_rec = world == 1 && smooth && c->rankfin_g1 && emb == nullptr && !p->smooth_credit_fused;
-  s = run_local(c, hidden, W, E, mask, credit_ids, p, c->rec_local, /*reduce_acc=*/world > 1 || g1_rec, credit_val);
-  if (s != DINFER_OK) return s;
-  size_t words = smooth ? c->full_words : c->stats_words;
-  if (g1_rec)
-    return run_combine(c, c->rec_local, words, 1, /*acc_from_part2=*/false, e_mask, mask, tokens, credit_ids,
-                       credit_val, p, committed, smoothed, stats, -1, E, emb);
-  if (world > 1 && c->p2p) {  // the record finalize pushed every rank's record over peer memory
-    return run_combine(c, c->xbuf, c->full_words, world, /*acc_from_part2=*/false, e_mask, mask, tokens, credit_ids,
+  // K12 steps (smoothing, fused geometry) reduce the smoothing accumulator
+  // into the step's record (record mode); K34 zeroes it after use
+  const bool k12 = smooth && c->fused;
+  const size_t words = smooth ? c->full_words : c->stats_words;
+  if (world == 1) {
+    // K34 merges the slab partials (stats) itself, and the per-group fp16
+    // smoothing partials (a fixed-order merge: bitwise reproducible) -- or,
+    // with DINFER_K12_RECORD=1, reads K12's one fp32 record (L2 reductions,
+    // reproducible to rounding order only; measured no faster at world 1)
+    const bool rec1 = k12 && c->k12_rec_g1;
+    s = run_local(c, hidden, W, E, mask, credit_ids, p, c->rec_local, /*reduce_acc=*/false, credit_val, rec1);
+    if (s != DINFER_OK) return s;
+    const AccSrc acc = rec1 ? AccSrc{kAccUnit, c->rec_local + c->stats_words, 0} : AccSrc{kAccPartials, nullptr, 0};
+    return run_combine(c, c->rec_local, words, 1, /*stats_part1=*/true, acc, e_mask, mask, tokens, credit_ids,
                        credit_val, p, committed, smoothed, stats, -1, E, emb);
   }
-  if (world > 1) {
+  if (c->p2p) {  // the ranks read each other's records in place (flags raised by the producing kernel)
+    s = run_local(c, hidden, W, E, mask, credit_ids, p, c->xbuf, /*reduce_acc=*/true, credit_val);
+    if (s != DINFER_OK) return s;
+    const AccSrc acc = k12 ? AccSrc{kAccRecords, c->xbuf + c->stats_words, static_cast<long>(c->full_words)}
+                           : AccSrc{kAccRecords, nullptr, 0};
+    return run_combine(c, c->xbuf, c->full_words, world, false, acc, e_mask, mask, tokens, credit_ids, credit_val, p,
+                       committed, smoothed, stats, -1, E, emb);
+  }
 #ifdef DINFER_WITH_NCCL
-    ev_begin(c, kPC1);
-    if (ncclAllGather(c->rec_local, c->rec_all, words, ncclFloat, c->comm, c->stream) != ncclSuccess)
-      return DINFER_ERR_NCCL;
-    ev_finish(c, kPC1);
+  s = run_local(c, hidden, W, E, mask, credit_ids, p, c->rec_local, /*reduce_acc=*/true, credit_val);
+  if (s != DINFER_OK) return s;
+  ev_begin(c, kPC1);
+  if (ncclAllGather(c->rec_local, c->rec_all, words, ncclFloat, c->comm, c->stream) != ncclSuccess)
+    return DINFER_ERR_NCCL;
+  ev_finish(c, kPC1);
+  const AccSrc acc = k12 ? AccSrc{kAccRecords, c->rec_local + c->stats_words, 0} : AccSrc{kAccRecords, nullptr, 0};
+  return run_combine(c, c->rec_all, words, world, false, acc, e_mask, mask, tokens, credit_ids, credit_val, p,
+                     committed, smoothed, stats, -1, E, emb);
 #else
-    return DINFER_ERR_UNSUPPORTED;
+  return DINFER_ERR_UNSUPPORTED;
 #endif
-  }
-  return run_combine(c, c->rec_all, words, world, /*acc_from_part2=*/world == 1, e_mask, mask, tokens, credit_ids,
-                     credit_val, p, committed, smoothed, stats, -1, E, emb);
 }
 }  // namespace
 
@@ -1583,6 +1621,8 @@ dinfer_status dinfer_step_local(dinfer_ctx* c, const uint16_t* hidden, const uin
   if (p->use_credit && credit_ids == nullptr) return DINFER_ERR_ARG;
   if (p->use_smooth && (E == nullptr || !aligned(E, 16))) return DINFER_ERR_ARG;
   for (int i = 0; i < kNumPhases; ++i) c->ev_used[i] = false;
+  if (p->use_smooth && c->fused)  // K12 adds every CTA's accumulator into the record: start from zero
+    DI_CUDA(cudaMemsetAsync(record + c->stats_words, 0, static_cast<size_t>(c->M) * c->shp.H * 4, c->stream));
   return run_local(c, hidden, W, E, mask, credit_ids, p, record, /*reduce_acc=*/true);
 }
 
@@ -1606,8 +1646,8 @@ dinfer_status dinfer_step_combine(dinfer_ctx* c, const float* records, const uin
     if (p->block_start) DI_CUDA(cudaMemsetAsync(c->mask_snap, 1, c->M, c->stream));
     else DI_CUDA(cudaMemcpyAsync(c->mask_snap, mask, c->M, cudaMemcpyDeviceToDevice, c->stream));
   }
-  return run_combine(c, records, words, c->shp.world, /*acc_from_part2=*/false, e_mask, mask, tokens, credit_ids,
-                     credit_val, p, committed, smoothed, stats);
+  return run_combine(c, records, words, c->shp.world, false, AccSrc{kAccRecords, nullptr, 0}, e_mask, mask, tokens,
+                     credit_ids, credit_val, p, committed, smoothed, stats);
 }
 
 dinfer_status dinfer_step_host_async(dinfer_ctx* c, const uint16_t* hidden_h, const uint16_t* W, const uint16_t* E,
@@ -2026,7 +2066,7 @@ dinfer_status dinfer_get_timing(dinfer_ctx* c, float* ms, int32_t n) {
 
 int32_t dinfer_get_trace(dinfer_ctx* c, uint64_t* out, int32_t n) {
   if (c == nullptr || c->trace == nullptr) return 0;
-  const int total = 5 * (2 * c->k1_grid + c->k2_HS * c->k2_VG + kTraceK34);
+  const int total = 5 * (c->k1_grid + c->k2_HS * c->k2_VG + kTraceK34);
   if (out == nullptr) return total;
   cudaStreamSynchronize(c->stream);
   const int k = n < total ? n : total;

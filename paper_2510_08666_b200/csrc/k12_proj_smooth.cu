@@ -50,7 +50,6 @@
 
 #include "common.cuh"
 #include "kernels.h"
-#include "rank_fin.cuh"
 
 #include <cuda_bf16.h>
 
@@ -102,7 +101,7 @@ __host__ __device__ inline Layout make_layout(int N, int HW, int stages, int pst
   // full/empty[stages], efull/eempty[estages], tfull/tempty[2], ffull/fempty/pfull/pempty[pstages], accfull, own,
   // oth, owndone
   L.misc_off = L.bar_off + (2u * stages + 2u * L.estages + 4u + 4u * pstages + 4u) * 8u;
-  L.m_off = L.misc_off + 64u;  // tmem base, entry count, diagnostics words [4, 12)
+  L.m_off = L.misc_off + 64u;  // tmem base, entry count, diagnostics words [4, 12), first-finisher flag [12]
   L.red_off = L.m_off + static_cast<uint32_t>(4 * N) * 4u;  // m_own, m_oth, scale A, scale B
   L.total = L.red_off + static_cast<uint32_t>(kEpiWarps * N * 3) * 4u;
   return L;
@@ -533,6 +532,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ W phase: K1 epilogue
     grid_dep_wait();  // mask / credit ids of the previous step's commit visible
     if (a.wdur != nullptr && threadIdx.x == 0) t_start = globaltimer_ns();
+    // record stats rows of this step (slot (epoch & 1) of a double-buffered record)
+    float* recw = a.rec;
+    if (a.rec_par > 0) recw += (*reinterpret_cast<const volatile unsigned*>(a.rec_ctl) & 1u) * a.rec_par;
     if (a.mask_snap != nullptr && blockIdx.x == 0)
       for (int s = threadIdx.x; s < a.M; s += kEpiThreads) a.mask_snap[s] = a.block_start ? 1 : a.mask[s];
     if (a.cids_snap != nullptr && blockIdx.x == 0)
@@ -549,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (id < 0) continue;
         const int lv = id - a.v_offset;
         if (lv < 0 || lv >= a.V_local) {  // owned by another rank
-          if (blockIdx.x == 0) a.rec[s * stride + kStatWords + k] = neg_inf();
+          if (blockIdx.x == 0) recw[s * stride + kStatWords + k] = neg_inf();
           continue;
         }
         if (lv < r0 || lv >= r1) continue;
@@ -607,7 +609,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           for (int e = ent0; e >= 0; e = ent_next[e]) {
             const int s = ent_s[e] - g * 32;
-            if (s >= 0 && s < 32) a.rec[(g * 32 + s) * stride + kStatWords + ent_k[e]] = pick32(x, s);
+            if (s >= 0 && s < 32) recw[(g * 32 + s) * stride + kStatWords + ent_k[e]] = pick32(x, s);
           }
           float m[32], l[32];
           int ix[32];
@@ -651,6 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (col < a.M) {
         reinterpret_cast<float4*>(a.part)[static_cast<long>(col) * gridDim.x + role] =
             make_float4(m, __int_as_float(ix), l, 0.f);
+        if (b.rec_acc != nullptr && n_own > 0) atomicMax(b.mx + col, f2ord(m));  // -> m_rank
         m_own[col] = m;
       } else {
         m_own[col] = 0.f;
@@ -665,6 +668,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_proxy_async_global();
     named_bar_epi();
     if (threadIdx.x == 0) {
+      if (b.rec_acc != nullptr) atomicAdd(b.rcnt, 1u);  // W phases done (m_rank complete at gridDim.x)
       if (SPG > 1) {
         atomicAdd(&a.grp_cnt[grp], 1u);
         if (!has_oth) {  // waits for nobody: passes right away (after its own count)
@@ -765,7 +769,63 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     // reference rescales of the two accumulator sets (no MMA dependence)
     if (tid == 0) PROBE(4, n_all * 10000 + n_own * 10 + (has_oth ? 1 : 0));
-    for (int s = tid; s < N; s += kEpiThreads) {
+    if (b.rec_acc != nullptr) {
+      // record mode, while the MMA warp finishes the last chunks: m_rank = max
+      // of every slab's max (complete once every W phase is done -- normally
+      // long ago); the scales take the accumulator(s) from their reference
+      // (ref / m_own / m_oth) to m_rank.  The first CTA here merges the rank's
+      // statistics into the record (when the record leaves the rank).
+      if (tid == 0) {
+        uint32_t spins = 0;
+        while (ld_acquire_gpu(b.rcnt) < gridDim.x) {
+          __nanosleep(32);
+          if (++spins > (1u << 26)) __trap();
+        }
+        misc[12] = (b.merge_stats && atomicAdd(b.rcnt + 1, 1u) == 0u) ? 1u : 0u;
+      }
+      named_bar_epi();
+      for (int s = tid; s < N; s += kEpiThreads) {
+        const float mr = (s < a.M) ? ord2f(__ldcg(b.mx + s)) : 0.f;
+        if (b.stack) {
+          scA[s] = (n_all > 0 && s < a.M) ? fexp(ref[s] - mr) : 0.f;
+        } else {
+          scA[s] = (n_own > 0 && s < a.M) ? fexp(m_own[s] - mr) : 0.f;
+          scB[s] = (has_oth && s < a.M) ? fexp(m_oth[s] - mr) : 0.f;
+        }
+      }
+      if (misc[12] != 0u) {
+        // fixed-order (deterministic) merge of the slab partials: (m, v*, l, 0)
+        // rows; the captured credited logits were written there in the W phase
+        float* rs = b.rec_stats + ((b.rec_par > 0) ? (*reinterpret_cast<volatile unsigned*>(b.x.ctl) & 1u) * b.rec_par : 0);
+        for (int s = warp; s < a.M; s += kEpiWarps) {
+          float m = neg_inf(), l = 0.f;
+          int ix = INT_MAX;
+          const float4* src = reinterpret_cast<const float4*>(a.part) + static_cast<long>(s) * gridDim.x;
+          for (int j0 = 0; j0 < static_cast<int>(gridDim.x); j0 += 32 * 8) {
+            float4 p[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int j = j0 + lane + 32 * u;
+              p[u] = (j < static_cast<int>(gridDim.x)) ? __ldcg(src + j)
+                                                       : make_float4(neg_inf(), __int_as_float(INT_MAX), 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) stat_combine(m, ix, l, p[u].x, __float_as_int(p[u].y), p[u].z);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const float rm = __shfl_xor_sync(0xffffffffu, m, o);
+            const int ri = __shfl_xor_sync(0xffffffffu, ix, o);
+            const float rl = __shfl_xor_sync(0xffffffffu, l, o);
+            stat_combine(m, ix, l, rm, ri, rl);
+          }
+          if (lane == 0)
+            *reinterpret_cast<float4*>(rs + static_cast<long>(s) * b.rec_stride) =
+                make_float4(m, __int_as_float(ix), l, 0.f);
+        }
+      }
+    }
+    for (int s = tid; s < N && b.rec_acc == nullptr; s += kEpiThreads) {
       const float mo = m_own[s], mt = m_oth[s];
       const float mg = fmaxf(mo, mt);
       if (b.stack) {  // the single accumulator is relative to ref[s]
@@ -810,6 +870,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
   }
   if (threadIdx.x == 0) PROBE(5, 1);
+  const bool recmode = b.rec_acc != nullptr;
+  float* rec_acc = b.rec_acc;
+  if (recmode && b.rec_par > 0) rec_acc += (*reinterpret_cast<volatile unsigned*>(b.x.ctl) & 1u) * b.rec_par;
   {
     const int wg = warp / 4, wq = warp % 4, tg = threadIdx.x % kEpiThreads;
     const int ng = N / 32;
@@ -852,6 +915,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) x[jj] = fmaf(y[jj], scB[g * 32 + jj], x[jj]);
         }
+        if (recmode) {  // L2 reductions straight from the registers: 32 lanes = 128 contiguous bytes per row
+          float* dst = rec_acc + hbase + sub * 128 + wq * 32 + lane;
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj)
+            if (g * 32 + jj < a.M) atomicAdd(dst + static_cast<long>(g * 32 + jj) * a.H, x[jj]);
+          continue;
+        }
         float* t = tile + (((sub - sub0) * ng + g) & 1) * (32 * 128);  // two tiles: one barrier per pass
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) t[jj * 128 + wq * 32 + lane] = x[jj];
@@ -870,23 +940,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+  if (recmode) __threadfence();  // this CTA's reductions before its count below
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 5) tmem_dealloc(tmem_base, 512);
   if (a.wdur != nullptr && threadIdx.x == 0)  // whole-CTA duration (calibration objective)
     a.wdur[gridDim.x + blockIdx.x] = static_cast<unsigned>(globaltimer_ns() - t_start);
-  // the rank record (statistics + smoothing accumulator) merged across the
-  // grid and, with peers, pushed into every rank's gather buffer (rank_fin.cuh)
-  // trace: K2-slot exit = end of the partial write-out, K1-slot exit = kernel exit
+  // trace: K2-slot exit = end of the partial write-out / reductions, K1-slot exit = kernel exit
   if (tr2 != nullptr && threadIdx.x == 0) {
     tr2[0] = tr[2];
     tr2[3] = globaltimer_ns();
   }
-  if (b.rank_fin) {
-    unsigned long long* trf = (b.rf.trace != nullptr && threadIdx.x == 0) ? b.rf.trace + blockIdx.x * 5 : nullptr;
-    if (trf != nullptr && tr != nullptr) trf[4] = tr[4];
-    rank_finalize(b.rf, b.gbar, reinterpret_cast<float*>(ring), trf);
+  if (recmode && threadIdx.x == 0 && atomicAdd(b.rcnt + 2, 1u) == gridDim.x - 1) {
+    // the last CTA: every CTA has read m_rank and counted its reductions --
+    // reset the self-resetting words for the next step, then (peer exchange)
+    // raise this rank's flag in every peer
+    b.rcnt[0] = 0u;
+    b.rcnt[1] = 0u;
+    b.rcnt[2] = 0u;
+    for (int s = 0; s < a.M; ++s) b.mx[s] = 0u;
+    if (b.x.peers != nullptr) {
+      const unsigned epoch = *reinterpret_cast<volatile unsigned*>(b.x.ctl);
+      const unsigned par = epoch & 1u;
+      __threadfence_system();
+      for (int j = 0; j < b.x.world; ++j) {
+        unsigned* f = reinterpret_cast<unsigned*>(b.x.peers[j] + b.x.flags_off) + par * b.x.world +
+                      (b.x.loopback ? j : b.x.rank);
+        // relaxed: the fence above orders the record before these flags (one
+        // release per flag serialised G system-scope round trips: ~2 us each)
+        asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch + 1u) : "memory");
+      }
+    }
   }
   if (tr != nullptr && threadIdx.x == 0) tr[3] = globaltimer_ns();
 }

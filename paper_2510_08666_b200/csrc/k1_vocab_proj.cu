@@ -278,6 +278,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // are frozen (reading c7) and skipped.  Runs while the first W chunks fly.
     grid_dep_wait();  // mask / credit ids of the previous step's commit visible
     if (a.wdur != nullptr && threadIdx.x == 0) t_start = globaltimer_ns();
+    // record stats rows of this step (slot (epoch & 1) of a double-buffered record)
+    float* recw = a.rec;
+    if (a.rec_par > 0) recw += (*reinterpret_cast<const volatile unsigned*>(a.rec_ctl) & 1u) * a.rec_par;
     if (a.mask_snap != nullptr && blockIdx.x == 0)
       for (int s = threadIdx.x; s < a.M; s += kEpiWarps * kWarpThreads) a.mask_snap[s] = a.block_start ? 1 : a.mask[s];
     if (a.cids_snap != nullptr && blockIdx.x == 0)
@@ -294,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (id < 0) continue;
         const int lv = id - a.v_offset;
         if (lv < 0 || lv >= a.V_local) {  // owned by another rank
-          if (blockIdx.x == 0) a.rec[s * stride + kStatWords + k] = neg_inf();
+          if (blockIdx.x == 0) recw[s * stride + kStatWords + k] = neg_inf();
           continue;
         }
         if (lv < r0 || lv >= r1) continue;
@@ -352,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           for (int e = ent0; e >= 0; e = ent_next[e]) {
             const int s = ent_s[e] - g * 32;
-            if (s >= 0 && s < 32) a.rec[(g * 32 + s) * stride + kStatWords + ent_k[e]] = pick32(x, s);
+            if (s >= 0 && s < 32) recw[(g * 32 + s) * stride + kStatWords + ent_k[e]] = pick32(x, s);
           }
           float m[32], l[32];
           int ix[32];

@@ -322,24 +322,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 // record's (m, v*, l).  Blocks >= M (when part2): rec_acc[s, h..h+3] =
 // sum_g part2[g][s, h..] * e^{m_g - m_rank}, with m_rank recomputed from the
 // group maxima (identical to the merged m: the groups tile the shard).
-// Store one record word (or float4) locally and, with the peer exchange, into
-// every rank's gather buffer (NVLink P2P stores).
-DI long rec_slot(const RecArgs& a, int j, unsigned par) {  // loopback: see rank_fin.cuh
-  return (static_cast<long>(par) * a.world + (a.loopback ? j : a.rank)) * a.rec_words;
-}
-DI void rec_put(const RecArgs& a, long word, float v, unsigned par) {
-  if (a.peers == nullptr) return;
-  for (int j = 0; j < a.world; ++j) a.peers[j][rec_slot(a, j, par) + word] = v;
-}
-DI void rec_put4(const RecArgs& a, long word, float4 v, unsigned par) {
-  if (a.peers == nullptr) return;
-  for (int j = 0; j < a.world; ++j) *reinterpret_cast<float4*>(a.peers[j] + rec_slot(a, j, par) + word) = v;
-}
-
+// The record is written locally (slot (epoch & 1) when double-buffered);
+// with the peer exchange the last block then raises this rank's flag in every
+// peer, whose K34 reads the record in place.
 __global__ void rec_finalize_kernel(const RecArgs a) {
   grid_dep_wait();
-  const unsigned epoch = (a.peers != nullptr) ? *reinterpret_cast<volatile unsigned*>(a.ctl) : 0u;
+  const bool need_epoch = a.par_words > 0 || a.x.peers != nullptr;
+  const unsigned epoch = need_epoch ? *reinterpret_cast<volatile unsigned*>(a.x.ctl) : 0u;
   const unsigned par = epoch & 1u;
+  float* rec = a.rec + (a.par_words > 0 ? par * a.par_words : 0);
   if (static_cast<int>(blockIdx.x) < a.M) {
     if (threadIdx.x < 32) {
       const int s = blockIdx.x, lane = threadIdx.x;
@@ -356,21 +347,13 @@ __global__ void rec_finalize_kernel(const RecArgs a) {
         const float rl = __shfl_xor_sync(0xffffffffu, l, o);
         stat_combine(m, ix, l, rm, ri, rl);
       }
-      const long row = static_cast<long>(s) * a.rec_stride;
       if (lane == 0) {
-        float* r = a.rec + row;
+        float* r = rec + static_cast<long>(s) * a.rec_stride;
         r[0] = m;
         r[1] = __int_as_float(ix);
         r[2] = l;
         r[3] = 0.f;
-        rec_put(a, row, m, par);
-        rec_put(a, row + 1, __int_as_float(ix), par);
-        rec_put(a, row + 2, l, par);
-        rec_put(a, row + 3, 0.f, par);
       }
-      // the captured credited logits (K1 wrote them into the local record)
-      for (int k = lane; k < a.K && a.peers != nullptr; k += 32)
-        rec_put(a, row + kStatWords + k, __ldcg(a.rec + row + kStatWords + k), par);
     }
   } else if (a.part2 != nullptr) {
     const long t = static_cast<long>(blockIdx.x - a.M) * blockDim.x + threadIdx.x;
@@ -390,31 +373,21 @@ __global__ void rec_finalize_kernel(const RecArgs a) {
         acc.z = fmaf(v.z, sc, acc.z);
         acc.w = fmaf(v.w, sc, acc.w);
       }
-      *reinterpret_cast<float4*>(a.rec_acc + static_cast<long>(s) * a.H + h) = acc;
-      const long w = (a.rec_acc - a.rec) + static_cast<long>(s) * a.H + h;
-      if (((a.rec_acc - a.rec) | a.rec_words) % 4 == 0) {
-        rec_put4(a, w, acc, par);
-      } else {
-        rec_put(a, w, acc.x, par);
-        rec_put(a, w + 1, acc.y, par);
-        rec_put(a, w + 2, acc.z, par);
-        rec_put(a, w + 3, acc.w, par);
-      }
+      *reinterpret_cast<float4*>(rec + a.acc_off + static_cast<long>(s) * a.H + h) = acc;
     }
   }
-  if (a.peers == nullptr) return;
-  // completion: every block's peer stores are system-visible before its count;
-  // the last block raises this rank's flag on every peer (release)
+  if (a.x.peers == nullptr) return;
+  // completion: every block's record writes are visible before its count; the
+  // last block raises this rank's flag in every peer
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
-    if (atomicAdd(a.ctl + 1, 1u) == gridDim.x - 1) {
-      a.ctl[1] = 0u;
+    __threadfence();
+    if (atomicAdd(a.x.ctl + 1, 1u) == gridDim.x - 1) {
+      a.x.ctl[1] = 0u;
       __threadfence_system();
-      for (int j = 0; j < a.world; ++j) {
-        unsigned* f = reinterpret_cast<unsigned*>(a.peers[j] + a.flags_off) + par * a.world + (a.loopback ? j : a.rank);
-        // relaxed: the fence above orders every record store before these flags (one
-        // release per flag serialised G system-scope round trips: ~2 us each)
+      for (int j = 0; j < a.x.world; ++j) {
+        unsigned* f = reinterpret_cast<unsigned*>(a.x.peers[j] + a.x.flags_off) + par * a.x.world +
+                      (a.x.loopback ? j : a.x.rank);
         asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch + 1u) : "memory");
       }
     }

@@ -116,27 +116,37 @@ DI float credit_fuse_slot(float alpha, int cid, float cv, int vstar, float m, fl
 
 // Warp-collective: merged statistics (m, v*, l) of position i, from K1's
 // per-slab partials (single rank) or from the `world` records (rank order).
-// Every lane returns the identical, deterministic result.
-DI void row_stats(const K3Args& a, int i, int lane, float& m, int& vstar, float& l) {
+// Every lane returns the identical, deterministic result.  Split into the
+// loads (issued ahead, see select_block) and the merge.
+constexpr int kStatU = 5;  // slab partials per lane in one round trip (grid1 <= 160)
+struct StatIn {
+  float4 p[kStatU];
+};
+DI void stats_load(const K3Args& a, int i, int lane, StatIn& q) {
+  if (a.part1 != nullptr) {
+    const float4* src = a.part1 + static_cast<long>(i) * a.grid1;
+#pragma unroll
+    for (int u = 0; u < kStatU; ++u) {
+      const int j = lane + 32 * u;
+      q.p[u] = (j < a.grid1) ? __ldcg(src + j) : make_float4(neg_inf(), __int_as_float(INT_MAX), 0.f, 0.f);
+    }
+    return;
+  }
+  q.p[0] = (lane < a.world) ? *reinterpret_cast<const float4*>(a.rb[lane] + static_cast<long>(i) * a.rec_stride)
+                            : make_float4(neg_inf(), __int_as_float(INT_MAX), 0.f, 0.f);
+}
+DI void stats_merge(const K3Args& a, int i, int lane, const StatIn& q, float& m, int& vstar, float& l) {
   m = neg_inf();
   l = 0.f;
   vstar = INT_MAX;
   if (a.part1 != nullptr) {
     // lanes stride the slabs, then an xor butterfly (stat_combine is
-    // commutative bit for bit, so all lanes agree).  Up to 8 loads per lane
-    // are issued before the first combine (one L2 round trip, not eight).
-    constexpr int kU = 8;
-    const float4* src = a.part1 + static_cast<long>(i) * a.grid1;
-    for (int j0 = 0; j0 < a.grid1; j0 += 32 * kU) {
-      float4 p[kU];
+    // commutative bit for bit, so all lanes agree)
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int j = j0 + lane + 32 * u;
-        if (j < a.grid1) p[u] = __ldcg(src + j);
-      }
-#pragma unroll
-      for (int u = 0; u < kU; ++u)
-        if (j0 + lane + 32 * u < a.grid1) stat_combine(m, vstar, l, p[u].x, __float_as_int(p[u].y), p[u].z);
+    for (int u = 0; u < kStatU; ++u) stat_combine(m, vstar, l, q.p[u].x, __float_as_int(q.p[u].y), q.p[u].z);
+    for (int j = lane + 32 * kStatU; j < a.grid1; j += 32) {  // grid1 > 160 (not on B200)
+      const float4 p = __ldcg(a.part1 + static_cast<long>(i) * a.grid1 + j);
+      stat_combine(m, vstar, l, p.x, __float_as_int(p.y), p.z);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -147,13 +157,9 @@ DI void row_stats(const K3Args& a, int i, int lane, float& m, int& vstar, float&
     }
     return;
   }
-  const long roff = static_cast<long>(i) * a.rec_stride;
-  if (lane < a.world) {
-    const float* rr = a.recs + lane * a.rec_words + roff;
-    m = rr[0];
-    vstar = __float_as_int(rr[1]);
-    l = rr[2];
-  }
+  m = q.p[0].x;
+  vstar = __float_as_int(q.p[0].y);
+  l = q.p[0].z;
   float m0 = m, l0 = l;  // merge ranks 1..world-1 into lane 0 in rank order, then broadcast
   int v0 = vstar;
   for (int r = 1; r < a.world; ++r) {
@@ -166,20 +172,49 @@ DI void row_stats(const K3Args& a, int i, int lane, float& m, int& vstar, float&
   vstar = __shfl_sync(0xffffffffu, v0, 0);
   l = __shfl_sync(0xffffffffu, l0, 0);
 }
+DI void row_stats(const K3Args& a, int i, int lane, float& m, int& vstar, float& l) {
+  StatIn q;
+  stats_load(a, i, lane, q);
+  stats_merge(a, i, lane, q, m, vstar, l);
+}
 
-// Selection CTAs: phase 1 is spread over ceil(S / kSelPos) CTAs per batch
-// row (one warp per position: the per-position chain is latency- and
-// issue-bound, so fewer warps per SM finish sooner); each writes its
+// Per-position inputs of phase 1, loaded one position ahead of their use.
+struct PosIn {
+  StatIn st;
+  int cid;
+  float cv, fc;
+  bool und;
+};
+DI void pos_load(const K3Args& a, int i, int lane, PosIn& q) {
+  const long roff = static_cast<long>(i) * a.rec_stride;
+  const long cbase = static_cast<long>(i) * a.K;
+  q.und = a.block_start || a.mask[i] != 0;  // block start: every position undecided
+  const bool slot = a.use_credit && a.K <= 32 && lane < a.K;  // slot k in lane k, kept in registers
+  q.cid = (slot && !a.block_start) ? a.credit_ids[cbase + lane] : -1;  // block start: slots empty
+  q.cv = (slot && !a.block_start) ? a.credit_val[cbase + lane] : 0.f;
+  q.fc = 0.f;  // raw logit of the credited token (max over ranks: -inf where not owned)
+  if (slot) {
+    q.fc = a.rb[0][roff + kStatWords + lane];
+    for (int r = 1; r < a.world; ++r) q.fc = fmaxf(q.fc, a.rb[r][roff + kStatWords + lane]);
+  }
+  stats_load(a, i, lane, q.st);
+}
+
+// Selection CTAs: phase 1 covers kSelPos positions per CTA (one CTA per
+// batch row up to S = 32: no cross-CTA hand-off), each warp a strided subset
+// of them with the next position's loads issued before the current one is
+// processed (the per-position chain is latency-bound: one round trip per
+// warp instead of one per position).  With S > kSelPos each CTA writes its
 // positions' (p~, v~, undecided) to `sel`, and the last CTA of the row to
 // arrive (counter, release/acquire fences) runs phase 2 over the whole row.
-constexpr int kSelPos = 8;
+constexpr int kSelPos = 32;
 // smoothing blocks: 128 float4 columns x 4 partial groups (512 consecutive elements; one
 // wave of <= 144 blocks at the MoE shape)
 constexpr int kSmCols = 128, kSmGroups = 4, kSmBatch = 8;
 #ifndef DINFER_SM_HB
-#define DINFER_SM_HB 8
+#define DINFER_SM_HB 20
 #endif
-constexpr int kSmBatchH = DINFER_SM_HB;  // fp16 partial loads in flight per thread
+constexpr int kSmBatchH = DINFER_SM_HB;  // fp16 partial loads in flight per thread (74 partials / 4 groups in one round trip)
 DI int sel_ctas_per_row(int S) { return (S + kSelPos - 1) / kSelPos; }
 
 DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
@@ -198,28 +233,27 @@ DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
   const int b = c / cps, chunk = c - b * cps;
 
   // ------------------------------------------------------------ phase 1
-  if (warp < kSelPos && chunk * kSelPos + warp < a.S) {
-    const int s = chunk * kSelPos + warp;
+  const int s_end = min(a.S, (chunk + 1) * kSelPos);
+  PosIn nxt;
+  if (chunk * kSelPos + warp < s_end) pos_load(a, b * a.S + chunk * kSelPos + warp, lane, nxt);
+  for (int s = chunk * kSelPos + warp; s < s_end; s += nwarps) {
+    const PosIn cur = nxt;
+    if (s + nwarps < s_end) pos_load(a, b * a.S + s + nwarps, lane, nxt);  // the next position, ahead
     const int i = b * a.S + s;
     const long roff = static_cast<long>(i) * a.rec_stride;
     const long cbase = static_cast<long>(i) * a.K;
-    // state loads issued before the statistics merge (independent round trips)
-    const bool und = a.block_start || a.mask[i] != 0;  // block start: every position undecided
+    const bool und = cur.und;
     const bool fast = a.use_credit && a.K <= 32;  // slot k in lane k, kept in registers
     const bool slot = fast && lane < a.K;
-    int cid = (slot && !a.block_start) ? a.credit_ids[cbase + lane] : -1;  // block start: slots empty
-    float cv = (slot && !a.block_start) ? a.credit_val[cbase + lane] : 0.f;
+    int cid = cur.cid;
+    float cv = cur.cv;
     // device-checked precondition (SPEC: a credit entry is never negative; ids
     // index the vocabulary): sticky flag, surfaced by dinfer_sync
     if (und && slot && cid >= 0 && (cid >= a.V_total || !(cv >= 0.f))) atomicOr(a.err, kErrCreditInvalid);
-    float fc = 0.f;  // raw logit of the credited token (max over ranks: -inf where not owned)
-    if (slot) {
-      fc = a.recs[roff + kStatWords + lane];
-      for (int r = 1; r < a.world; ++r) fc = fmaxf(fc, a.recs[r * a.rec_words + roff + kStatWords + lane]);
-    }
+    const float fc = cur.fc;
     float m, l;
     int vstar;
-    row_stats(a, i, lane, m, vstar, l);
+    stats_merge(a, i, lane, cur.st, m, vstar, l);
     const float lse = m + __logf(l);
     const float pstar = __frcp_rn(l);  // == 1.0f / l (correctly rounded), no slow path
     int vt = vstar;
@@ -292,8 +326,8 @@ DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
         if (id >= 0) {
           float fk = m;
           if (id != vstar) {
-            fk = a.recs[roff + kStatWords + k];
-            for (int r = 1; r < a.world; ++r) fk = fmaxf(fk, a.recs[r * a.rec_words + roff + kStatWords + k]);
+            fk = a.rb[0][roff + kStatWords + k];
+            for (int r = 1; r < a.world; ++r) fk = fmaxf(fk, a.rb[r][roff + kStatWords + k]);
           }
           const float lc = __logf(1.f + a.credit_val[cbase + k]);
           const float ft = fk + a.c_alpha * lc;
@@ -495,6 +529,7 @@ DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
 // the running max: pacc = sum_p e^{m_p - mrun} acc_p.
 template <int kB, bool kHalf>
 DI void accumulate_parts(const K4Args& a, int s, int h, int grp, float4& pacc, float& mrun) {
+  static_assert(kHalf, "fp32 partials arrive as rank records (accumulate_recs)");
   const long base = static_cast<long>(s) * a.H + h;
   // all kB loads are issued before any use (raw fp16 words are converted in
   // the combine loop, so no conversion waits on a load between two issues)
@@ -510,8 +545,7 @@ DI void accumulate_parts(const K4Args& a, int s, int h, int grp, float4& pacc, f
       if constexpr (kHalf)
         raw[j] = ok ? ld_global_hint_v2(a.acc_h + base + p * a.acc_stride, pol) : make_uint2(0u, 0u);
       else
-        raw[j] = ok ? __ldcg(reinterpret_cast<const float4*>(a.acc + base + p * a.acc_stride))
-                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        raw[j] = make_float4(0.f, 0.f, 0.f, 0.f);
       mp[j] = ok ? a.m_part[p * a.m_stride + static_cast<long>(s) * a.m_rowstride] : neg_inf();
     }
 #pragma unroll
@@ -539,6 +573,41 @@ DI void accumulate_parts(const K4Args& a, int s, int h, int grp, float4& pacc, f
   }
 }
 
+// The world rank records in rank order (K12 record mode / sharded steps):
+// pacc = sum_r e^{m_r - mrun} acc_r with the online rescale to the running max
+// (m_r = record r's merged max); all loads issued before the first use.
+// rec_unit (world 1, K12 record mode): the one record is relative to the
+// merged m itself -- taken as is (scale 1 below).
+DI void accumulate_recs(const K3Args& a3, const K4Args& a, int s, int h, float4& pacc, float& mrun) {
+  const long off = a.acc_off + static_cast<long>(s) * a.H + h;
+  float4 v[8];
+  float mr[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    if (r < a3.world) {
+      v[r] = __ldcg(reinterpret_cast<const float4*>(a3.rb[r] + off));
+      mr[r] = a.rec_unit ? 0.f : __ldcg(a3.rb[r] + static_cast<long>(s) * a3.rec_stride);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {  // fixed summation order (rank order)
+    if (r >= a3.world) break;
+    if (mr[r] > mrun) {
+      const float q = (mrun == neg_inf()) ? 0.f : __expf(mrun - mr[r]);
+      pacc.x *= q;
+      pacc.y *= q;
+      pacc.z *= q;
+      pacc.w *= q;
+      mrun = mr[r];
+    }
+    const float sc = __expf(mr[r] - mrun);
+    pacc.x = fmaf(v[r].x, sc, pacc.x);
+    pacc.y = fmaf(v[r].y, sc, pacc.y);
+    pacc.z = fmaf(v[r].z, sc, pacc.z);
+    pacc.w = fmaf(v[r].w, sc, pacc.w);
+  }
+}
+
 DI void smooth_block(const K3Args& a3, const K4Args& a, int blk, unsigned long long* tr) {
   __shared__ float s_m[8], s_w[8];
   __shared__ float s_cw[8][32];  // credit-fused smoothing: per-slot weights w_k and ids
@@ -560,6 +629,9 @@ DI void smooth_block(const K3Args& a3, const K4Args& a, int blk, unsigned long l
   // partials, 8 loads in flight, with an online rescale to the running max
   // (pacc = sum_p e^{m_p - mrun} acc_p, fixed order), so the statistics are
   // needed only for the final scale and both latencies overlap.
+#ifdef DINFER_K34_FINE
+  if (tr != nullptr) tr[0] = globaltimer_ns();  // (fine trace) smoothing body start
+#endif
   if (warp <= s1 - s0) {
     float m, l;
     int vs;
@@ -574,7 +646,7 @@ DI void smooth_block(const K3Args& a3, const K4Args& a, int blk, unsigned long l
       const long cb = static_cast<long>(i) * a3.K;
       int cid = slot ? a.cids0[cb + lane] : -1;
       float cv = slot ? a.cval0[cb + lane] : 0.f;
-      const float fc = slot ? a3.recs[static_cast<long>(i) * a3.rec_stride + kStatWords + lane] : 0.f;
+      const float fc = slot ? a3.rb[0][static_cast<long>(i) * a3.rec_stride + kStatWords + lane] : 0.f;
       credit_update_slots(a3.c_beta, a3.c_gamma, slot, vs, __frcp_rn(l), cid, cv);
       float w = 0.f;
       if (cid >= 0) {
@@ -589,20 +661,27 @@ DI void smooth_block(const K3Args& a3, const K4Args& a, int blk, unsigned long l
       s_m[warp] = m;
       s_w[warp] = a.alpha_t / (l + extra);
     }
+#ifdef DINFER_K34_FINE
+    if (tr != nullptr) tr[4] = globaltimer_ns();  // (fine trace) row stats merged
+#endif
   }
   float4 pacc = make_float4(0.f, 0.f, 0.f, 0.f);
   float mrun = neg_inf();
-  if (active) {
-    if (a.acc_h != nullptr)  // fp16 partials
-      accumulate_parts<kSmBatchH, true>(a, s, h, grp, pacc, mrun);
-    else
-      accumulate_parts<kSmBatch, false>(a, s, h, grp, pacc, mrun);
+  if (a.rec_mode) {
+    if (active && grp == 0) accumulate_recs(a3, a, s, h, pacc, mrun);
+    // K12 record mode: the step's record accumulator is zeroed for the next
+    // step once read (same thread: the stores follow the loads of the same
+    // addresses; a double-buffered record zeroes the other slot)
+    if (a.zero_acc != nullptr && in && grp == 0)
+      *reinterpret_cast<float4*>(a.zero_acc + static_cast<long>(s) * a.H + h) = make_float4(0.f, 0.f, 0.f, 0.f);
+  } else if (active) {
+    accumulate_parts<kSmBatchH, true>(a, s, h, grp, pacc, mrun);  // fp16 per-group partials
   }
   __syncthreads();
   if (tr != nullptr) tr[2] = globaltimer_ns();
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if (active && mrun != neg_inf()) {
-    const float sc = __expf(mrun - s_m[s - s0]);
+    const float sc = a.rec_unit ? 1.f : __expf(mrun - s_m[s - s0]);
     acc = make_float4(pacc.x * sc, pacc.y * sc, pacc.z * sc, pacc.w * sc);
   }
   red[grp][cl] = acc;
@@ -663,7 +742,7 @@ DI void smooth_block(const K3Args& a3, const K4Args& a, int blk, unsigned long l
 // K3+K4 in one launch: blocks [0, B) select/commit batch rows, blocks >= B
 // (only with smoothing) write the smoothed embeddings.  Both read only what
 // K1 / K2 / the allgather produced (plus the step-start mask snapshot).
-__global__ void __launch_bounds__(kK3Threads) k34_select_smooth(const K3Args a3in, const K4Args a4in) {
+__global__ void __launch_bounds__(kK3Threads, 1) k34_select_smooth(const __grid_constant__ K3Args a3in, const __grid_constant__ K4Args a4in) {
   unsigned long long* tr =
       (a3in.trace != nullptr && threadIdx.x == 0 && blockIdx.x < kTraceK34) ? a3in.trace + blockIdx.x * 5 : nullptr;
   if (tr != nullptr) {
@@ -678,9 +757,10 @@ __global__ void __launch_bounds__(kK3Threads) k34_select_smooth(const K3Args a3i
   K3Args a3 = a3in;
   K4Args a4 = a4in;
   unsigned epoch = 0;
+  __shared__ const float* s_rb[32];  // record base of rank r (read in place; K1b: vocab group r)
   if (a3.xflags != nullptr) {
-    // peer-memory exchange: every rank's record of this epoch has landed in
-    // slot (epoch & 1) of the local gather buffer once its flag reads epoch + 1
+    // peer-memory exchange: rank r's record of this epoch is complete in slot
+    // (epoch & 1) of its exchange buffer once r's flag here reads epoch + 1
     epoch = *reinterpret_cast<volatile unsigned*>(a3.xctl);
     const unsigned par = epoch & 1u;
     if (static_cast<int>(threadIdx.x) < a3.world) {
@@ -695,10 +775,16 @@ __global__ void __launch_bounds__(kK3Threads) k34_select_smooth(const K3Args a3i
       }
     }
     __syncthreads();
-    a3.recs += par * a3.xslot;
-    a4.acc += par * a3.xslot;
-    a4.m_part += par * a3.xslot;
+    if (a4.zero_par > 0) a4.zero_acc += (par ^ 1u) * a4.zero_par;  // the slot the NEXT step's K12 fills
   }
+  if (threadIdx.x < 32) {
+    const int r = threadIdx.x;
+    s_rb[r] = (r >= a3.world) ? nullptr
+              : (a3.rpar > 0) ? a3in.rpv[r] + (epoch & 1u) * a3.rpar
+                                     : (a3.recs != nullptr ? a3.recs + r * a3.rec_words : nullptr);
+  }
+  __syncthreads();
+  a3.rb = s_rb;
   if (a3.pdev != nullptr) {  // per-step numeric parameters from device memory (graph replay)
     a3.tau = a3.pdev[0];
     a3.theta_hi = a3.pdev[1];

@@ -57,6 +57,8 @@ struct K1Args {
   float* part;             // [M][grid] float4 per-CTA (m, idx, l, 0), column-major
   unsigned* grp_cnt;       // [VG] slabs completed per group (K2 waits, resets), or nullptr
   float* rec;              // [M][4+K] rank record: only fcred (captured credited logits) is written
+  long rec_par;            // > 0: `rec` is double-buffered, slot (rec_ctl[0] & 1) at rec + slot * rec_par
+  const unsigned* rec_ctl; //      (the exchange epoch, advanced by K34)
   float* flog;             // [M][V_local] raw logits for K2, or nullptr
   uint8_t* mask_snap;      // [M] copy of the step-start mask (written by CTA 0), or nullptr
   int32_t* cids_snap;      // [M][K] copy of the step-start credit slots (f4), or nullptr
@@ -95,7 +97,20 @@ size_t k1b_smem_bytes(int stages);
 cudaError_t launch_k1b(const CUtensorMap& map_h, const CUtensorMap& map_w, const K1bArgs& a, int grid, size_t smem,
                        cudaStream_t st, bool pdl);
 
-// Rank record finalize (sharded / split-phase path):
+// Peer-memory record exchange (world > 1, dinfer_exchange_open): every rank
+// keeps its own record double-buffered by epoch parity in its exchange buffer
+// (IPC-shared); the kernel that completes it raises this rank's flag
+// (= epoch + 1) in every peer's buffer, and K34 reads the peers' records
+// in place (NVLink loads).  `peers` == nullptr: no flags to raise.
+struct XArgs {
+  float* const* peers;     // [world] device pointers to the ranks' exchange buffers, or nullptr
+  int world, rank;
+  long flags_off;          // word offset of the flags [2][world] in an exchange buffer
+  unsigned* ctl;           // local control words: [0] epoch (advanced by K34), [1] finished blocks
+  int loopback;            // measurement: peers are this GPU's own buffer, all `world` flags raised
+};
+
+// Rank record finalize (K1 / K1 -> K2 sharded and split-phase paths):
 //   stats: rec[s] = merge of K1's per-slab partials (fixed order);
 //   acc (if part2): rec_acc[s,:] = sum_g part2[g][s,:] * e^{m_g - m_rank}.
 struct RecArgs {
@@ -103,19 +118,10 @@ struct RecArgs {
   const float4* part1;
   const uint16_t* part2;   // [VG][M][H] fp16 or nullptr
   const float* mref;       // [VG][M]
-  float* rec;              // stats rows
-  float* rec_acc;          // [M][H]
-  // Peer-memory exchange (world > 1, dinfer_exchange_open): the record is ALSO
-  // written straight into every rank's gather buffer (slot [epoch & 1][rank]),
-  // then the last block raises this rank's flag (= epoch + 1) on every peer.
-  float* const* peers;     // [world] device pointers to the ranks' gather buffers, or nullptr
-  int world, rank;
-  long rec_words;          // words of one rank's record
-  long flags_off;          // word offset of the flags [2][world] in a gather buffer
-  unsigned* ctl;           // local control words: [0] epoch, [1] finished blocks of this kernel
-  int K;                   // credit slots (fcred words per stats row, copied from `rec`)
-  int loopback;            // measurement: peers are this GPU's own buffer, all `world` slots written
-  unsigned long long* trace;  // DINFER_TRACE (K12 fold): [grid][5] barrier passed, merged, stored, flag; smid
+  float* rec;              // stats rows (slot 0 when par_words > 0)
+  long acc_off;            // words from a record's start to its acc part
+  long par_words;          // > 0: double-buffered record, slot (epoch & 1) at rec + par * par_words
+  XArgs x;
 };
 
 // ---------------------------------------------------------------- K2
@@ -135,14 +141,22 @@ struct K2Args {
   uint16_t* part;          // [VG][M][H] fp16 (common.cuh: pack_half4)
   unsigned long long* trace;  // optional [grid][5]: globaltimer ns start, first E stage, MMAs done, exit; smid
   volatile int* probe;     // K12 diagnostics (env DINFER_K12_PROBE): [grid][8] progress words in mapped host memory
-  // K12 only: the rank-record finalize folded into the kernel's tail
-  // (rank_fin.cuh; grid barrier on gbar[0..1], then every CTA merges a slice
-  // of the record and, with peers, pushes it into every rank's gather buffer)
   int stack;               // K12: hi / lo P tiles stacked into one 2N-column MMA (TMEM nsub x 2N per set)
   int emin;                // K12: minimum E-ring depth (the ring is sized for it)
-  int rank_fin;
-  unsigned* gbar;
-  RecArgs rf;
+  // K12 record mode (rec_acc != nullptr): instead of per-group fp16 partials,
+  // every CTA rescales its smoothing accumulator to the rank max m_rank (the
+  // max of all slab maxima, gathered with atomicMax once every W phase is
+  // done) and adds it into ONE fp32 record [M][H] with L2 reductions
+  // (red.global.add.f32) -- the cross-CTA reduction overlaps the CTAs' finish
+  // spread, and K34 reads one record instead of VG partials.
+  float* rec_acc;          // record acc (slot 0 when rec_par > 0), relative to m_rank
+  float* rec_stats;        // record stats rows (slot 0), stride rec_stride: (m, v*, l, 0, fcred[K])
+  long rec_par;            // > 0: double-buffered by epoch parity (peer exchange), slot stride in words
+  int rec_stride;
+  int merge_stats;         // the first CTA to finish merges the slab statistics into the stats rows
+  unsigned* mx;            // [M] ordered-uint max of the slab maxima (self-resetting)
+  unsigned* rcnt;          // [4] W phases done, finish ticket, CTAs done (self-resetting)
+  XArgs x;                 // flags raised by the last CTA (peer exchange)
 };
 size_t k2_smem_bytes(int N, int HW, int KV, int stages, int pstages);
 cudaError_t launch_k2(const CUtensorMap& map_e, const CUtensorMap& map_f, const K2Args& a, size_t smem,
@@ -171,6 +185,11 @@ struct K3Args {
   int grid1;
   const float* recs;       // world records, `rec_words` apart (stats used when part1 == nullptr; fcred always)
   long rec_words;
+  // peer exchange (pull, rpar > 0): record r is at rpv[r] + (epoch & 1) * rpar (overrides recs);
+  // the pointers travel by value (no dependent load before the records)
+  float* rpv[8];
+  long rpar;
+  const float* const* rb;  // (device, set by the kernel) base of record r, r < world
   int rec_stride;          // 4 + K
   uint8_t* mask;
   int32_t* tokens;
@@ -189,13 +208,11 @@ struct K3Args {
   const uint16_t* E;       // [V_local][H] bf16 (next-input embedding of committed rows) or nullptr
   uint16_t* emb;           // [M][H] bf16 next-iteration input embedding (f2) or nullptr
   int* rowdone;            // [M] smoothing blocks done per row (phase 2 waits, then resets)
-  // Peer-memory exchange: recs / K4 acc point at slot 0 of the local gather
-  // buffer; the kernel waits until every rank's flag for this epoch is up,
-  // offsets them to slot (epoch & 1) (xslot words), and its last block
-  // advances the epoch.
-  const unsigned* xflags;  // [2][world] in the local gather buffer, or nullptr
+  // Peer-memory exchange: the kernel waits until every rank's flag for this
+  // epoch is up, reads the ranks' records of slot (epoch & 1) in place, and
+  // its last block advances the epoch.
+  const unsigned* xflags;  // [2][world] in the local exchange buffer, or nullptr
   unsigned* xctl;          // [0] epoch, [2] finished K34 blocks
-  long xslot;
   const float* pdev;       // optional device copy of the numeric params [tau, theta_hi, theta_lo,
                            // c_alpha, c_beta, c_gamma, alpha_t] (overrides the values above; lets a
                            // captured CUDA graph run with per-step schedules)
@@ -206,11 +223,18 @@ struct K3Args {
 // ---------------------------------------------------------------- K4
 struct K4Args {
   int M, H;
-  const float* acc;        // partial p at acc + p*acc_stride, [M][H] each (fp32 rank records)
-  const uint16_t* acc_h;   // or, when non-null, fp16 partials (single rank: K2 / K12 output) at acc_h + p*acc_stride
+  // smoothing accumulators: either the world rank records (rec_mode: acc at
+  // record + acc_off, relative to the record's m; rec_unit: ONE record
+  // relative to the merged m itself, scale 1 -- world-1 K12 record mode) or
+  // fp16 per-group partials (acc_h, relative to m_part)
+  int rec_mode, rec_unit;
+  long acc_off;
+  float* zero_acc;         // record acc [M][H] to zero after the step (K12 record mode), or nullptr
+  long zero_par;           // > 0: zero slot ((epoch & 1) ^ 1) of a double-buffered record instead
+  const uint16_t* acc_h;   // fp16 partials (K2 output) at acc_h + p*acc_stride
   long acc_stride;
   int nparts;
-  const float* m_part;     // m of partial p, row s at m_part[p*m_stride + s*m_rowstride]; nullptr = scale 1
+  const float* m_part;     // m of partial p, row s at m_part[p*m_stride + s*m_rowstride]
   long m_stride;
   int m_rowstride;
   const uint8_t* mask_start;  // [M] mask at step start (snapshot; the selection blocks rewrite `mask`)

@@ -386,7 +386,6 @@ class Context:
         k1 = buf[:n1].reshape(-1, 5)
         k2 = buf[n1:n1 + n2].reshape(-1, 5)
         k34 = buf[n1 + n2:n1 + n2 + 5 * 64].reshape(-1, 5)
-        self.trace_rankfin = buf[n1 + n2 + 5 * 64:].reshape(-1, 5)  # K12 record finalize stamps
         return k1, k2, k34  # K1, K2, K34 (first 64 blocks)
 
     def geometry(self) -> dict:

@@ -60,7 +60,7 @@ def main():
     g = ctx.geometry()
     print(f"shard {G}: V_local {v1 - v0}, {R} weight copies, geometry {g}")
     cols = [("start", k1[:, 0]), ("first W stage", k1[:, 1]), ("W done", k1[:, 2]), ("first E MMA", k2[:, 1]),
-            ("E MMAs done", k2[:, 2]), ("partial written", k2[:, 3]), ("exit", k1[:, 3])]
+            ("E MMAs done", k2[:, 2]), ("record added", k2[:, 3]), ("exit", k1[:, 3])]
     for n, c in cols:
         x = us(c)
         print(f"  {n:16s} min {x.min():7.1f}  p10 {np.percentile(x, 10):7.1f}  med {np.median(x):7.1f}  "
@@ -70,14 +70,8 @@ def main():
     wb = (v1 - v0) * H * 2
     print(f"  per-CTA W phase med {np.median(wph):.1f} us ({wb / np.median(wph) / 1e6:.2f} TB/s at the median), "
           f"E phase med {np.median(eph):.1f} us ({wb / np.median(eph) / 1e6:.2f} TB/s)")
-    rf = ctx.trace_rankfin
-    if G > 1 and rf is not None and rf[:, 0].any():
-        for n, j in (("rf barrier", 0), ("rf merged", 1), ("rf stored", 2), ("rf counted", 3)):
-            x = us(rf[:, j])
-            print(f"  {n:16s} min {x.min():7.1f}  p10 {np.percentile(x, 10):7.1f}  med {np.median(x):7.1f}  "
-                  f"p90 {np.percentile(x, 90):7.1f}  max {x.max():7.1f} us")
     os.makedirs("gpurun_out", exist_ok=True)
-    np.savez(f"gpurun_out/trace_k12_g{G}.npz", k1=k1, k2=k2, k34=k34, rf=rf if rf is not None else np.zeros(0), t0=t0)
+    np.savez(f"gpurun_out/trace_k12_g{G}.npz", k1=k1, k2=k2, k34=k34, t0=t0)
     x = us(k34[:, 1]), us(k34[:, 3])
     print(f"  K34: deps visible min {x[0].min():.1f} med {np.median(x[0]):.1f}; exit max {x[1].max():.1f} us "
           f"(last K12 exit {us(k1[:, 3]).max():.1f})")
