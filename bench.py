@@ -8,12 +8,15 @@ Workload (BASELINE.json metric: "denoise-step positions/sec and HBM GB/s
 fraction, LLaDA-MoE shape bs1, 1/2/4/8 B200"): configs[2], LLaDA-MoE shape
 H=2048, V=157184, block S=32, batch 1, hierarchical + credit decoding +
 iteration smoothing; for N > 1 the vocabulary is sharded over the N GPUs
-(configs[3]) and each rank's record is pushed into every peer's gather buffer
-by the producing kernel (peer-memory exchange; NCCL allgather fallback).  A
+(configs[3]) and the ranks read each other's records in place over NVLink once
+the producing kernel raises their flags (peer-memory exchange; NCCL allgather
+fallback).  A
 step = one dinfer_step on the first iteration of a block (all 32 positions
 undecided, fresh credit): K12 (vocab projection + softmax statistics +
-smoothing contraction, with the rank-record finalize folded into its tail when
-sharded) then K34 (combine, credit, selection, commit, smoothing output).
+smoothing contraction; when sharded it also builds the rank's record -- the
+accumulator added into one fp32 record with L2 reductions -- and raises the
+exchange flags) then K34 (combine, credit, selection, commit, smoothing
+output; when sharded it reads the peers' records in place).
 Synthetic seeded weights and planted hidden states (paper_2510_08666_b200.synth).
 The headline times K back-to-back steps (each a block's first iteration,
 params.block_start) under one event pair; every step reads weights the L2 does
@@ -23,9 +26,9 @@ the L2 flushed before each are reported under "l2_flushed", and the steps
 replayed from one CUDA graph under "graph_replay".
 
 --shard-sim G (N=1 only, measurement): one rank of a G-way vocab shard on one
-GPU (V_local = V/G, the record stored into all G slots of its own gather
-buffer -- dinfer_exchange_loopback), i.e. the per-rank step of configs[3]
-minus the NVLink latency; its decisions are not meaningful.
+GPU (V_local = V/G; every "peer" is its own exchange buffer, so K34 reads the
+rank's record G times -- dinfer_exchange_loopback), i.e. the per-rank step of
+configs[3] minus the NVLink latency; its decisions are not meaningful.
 
 Prints ONE JSON line on rank 0.  --impl reference times the CPU oracle (the
 reference arm of this tier) on the host cores instead.
@@ -304,8 +307,8 @@ def gpu_arm(args):
         ctx.exchange_loopback()
         exchange = "loopback"
     elif world > 1:
-        # the product's exchange: records pushed into every rank's gather buffer by
-        # the producing kernel over NVLink P2P (CUDA IPC handles shared via
+        # the product's exchange: K34 reads every rank's record in place over NVLink P2P
+        # once the producing kernel raised that rank's flag (CUDA IPC handles shared via
         # torch.distributed); the NCCL allgather stays as the fallback / --exchange nccl
         exchange = "nccl"
         if args.exchange in ("auto", "p2p"):
@@ -510,7 +513,9 @@ def gpu_arm(args):
         else:
             dom, dom_bytes, dom_ms = ("k1_vocab_proj", k1_bytes, k1_ms) if k1_ms >= k2_ms else \
                 ("k2_smooth_mix", k2_bytes, k2_ms)
-        traffic = ncu_traffic().get(f"{CFG['name']}/" + (dom if M <= 256 else "k1b_vocab_proj_dense"))
+        shards = args.shard_sim or world  # traffic captures of a vocab shard are keyed "<config>-g<G>"
+        tkey = CFG["name"] + (f"-g{shards}" if shards > 1 else "")
+        traffic = ncu_traffic().get(f"{tkey}/" + (dom if M <= 256 else "k1b_vocab_proj_dense"))
         step_bytes = k1_bytes + k2_bytes
         if M > 256:  # compute-bound regime (BASELINE configs[4]): tensor roofline of K1b
             flops = 2.0 * M * H * Vl

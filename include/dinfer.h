@@ -11,11 +11,12 @@
  *   (App. A.1) for positions still masked.
  *
  * The vocabulary may be sharded over `world` GPUs (contiguous rows of W_vocab
- * and W_emb); each rank's partial record (statistics + smoothing partial) is
- * exchanged in-kernel over peer memory (dinfer_exchange_open; the producing
- * kernel stores it into every peer's gather buffer over NVLink) or, without
- * opened peer buffers, by one NCCL allgather; every rank then runs the
- * identical combine, so decode state stays replicated and bit-identical.
+ * and W_emb); each rank builds one record (statistics + smoothing accumulator)
+ * per step inside the producing kernel and the ranks exchange records over
+ * peer memory (dinfer_exchange_open: every rank reads its peers' records in
+ * place over NVLink once their flags are up) or, without opened peer
+ * buffers, by one NCCL allgather; every rank then runs the identical combine,
+ * so decode state stays replicated and bit-identical.
  *
  * Conventions (all entry points):
  *  - Every pointer is CALLER-OWNED; the library never frees or retains it
@@ -240,23 +241,26 @@ dinfer_status dinfer_balance(dinfer_ctx* ctx, const uint16_t* hidden, const uint
 dinfer_status dinfer_balance_reset(dinfer_ctx* ctx);
 
 /* Peer-memory exchange of the per-rank records (world > 1),
- * replacing the NCCL allgather: the record finalize kernel stores this rank's
- * record straight into every rank's gather buffer over NVLink P2P (slot
- * [epoch & 1][rank], double-buffered so a rank one step ahead never
- * overwrites a slot a slower rank still reads) and raises a per-rank flag
- * (epoch + 1) on every peer; the select/commit kernel waits for all flags of
- * its epoch and advances the epoch -- no host synchronisation, graph safe.
- * dinfer_exchange_handle: this ctx's gather buffer as a 64-byte CUDA IPC
+ * replacing the NCCL allgather: each rank keeps its record in its exchange
+ * buffer, double-buffered by step parity (slot epoch & 1, so a rank one step
+ * ahead never overwrites a slot a slower rank still reads).  The kernel that
+ * completes it (K12's last CTA; the record finalize on the K1 paths) raises
+ * this rank's flag (epoch + 1) in every peer's buffer; the select/commit
+ * kernel waits for all flags of its epoch, reads the peers' records in place
+ * over NVLink, zeroes its own consumed accumulator slot and advances the
+ * epoch -- no host synchronisation, no NCCL launch, graph safe.
+ * dinfer_exchange_handle: this ctx's exchange buffer as a 64-byte CUDA IPC
  * handle.  dinfer_exchange_open: `handles` = world handles back to back in
  * rank order (all ranks); after it, dinfer_step exchanges through peer memory
  * (no communicator needed).  Errors: ARG, UNSUPPORTED (world == 1), CUDA.  */
 dinfer_status dinfer_exchange_handle(dinfer_ctx* ctx, uint8_t out_handle[64]);
 dinfer_status dinfer_exchange_open(dinfer_ctx* ctx, const uint8_t* handles);
 /* Measurement only: one rank of a `world`-way vocab shard on ONE GPU.  Every
- * "peer" is this ctx's own gather buffer and each step stores its record into
- * all `world` slots and raises all `world` flags, so the step moves the bytes
- * and runs the kernels of a real rank (minus the NVLink latency); the combined
- * results are NOT meaningful (the G records are copies of one shard's).
+ * "peer" is this ctx's own exchange buffer: each step raises all `world` flags
+ * and the combine reads this rank's record `world` times, so the step runs
+ * the kernels and moves the bytes of a real rank (minus the NVLink latency);
+ * the combined results are NOT meaningful (the G records are copies of one
+ * shard's).
  * Errors: ARG (already open), UNSUPPORTED (world == 1), CUDA.               */
 dinfer_status dinfer_exchange_loopback(dinfer_ctx* ctx);
 
@@ -282,7 +286,9 @@ dinfer_status dinfer_step_host_wait(dinfer_ctx* ctx);
  *            sum_{v in shard} exp(f_v - m), 0, fcred[K] = raw logit of each
  *            credited token if this rank owns it else -inf), padded to a
  *            multiple of 4 words (the acc part stays 16-byte aligned)
- *   + M*H    (use_smooth only) acc[s,:] = sum_{v in shard} exp(f_v - m) E[v,:].
+ *   + M*H    (use_smooth only) acc[s,:] = sum_{v in shard} exp(f_v - m) E[v,:]
+ *            (on the fused K12 path the sum over the shard's CTAs is taken with
+ *            L2 reductions: reproducible to fp32 rounding order, not bitwise).
  * dinfer_step_local writes this rank's record to `record` (device, that many
  * words).  dinfer_step_combine reads `records` = `world` records back to back
  * (rank order) and performs the combine / credit / selection / commit /
@@ -414,9 +420,9 @@ const char* dinfer_last_error(void);
 /* Instrumentation.  dinfer_set_timing(ctx, 1) brackets every kernel / the
  * collective of subsequent steps with CUDA events on the ctx stream;
  * dinfer_get_timing fills up to n floats with the last step's per-phase
- * milliseconds in the order [K1 vocab_proj (or K1b), K2 smooth_mix, record
- * finalize (sharded / split-phase), C1 allgather, K34 select_commit +
- * smooth_finalize, unused] (0 if not run); it
+ * milliseconds in the order [K1 vocab_proj (or K1b, or K12), K2 smooth_mix,
+ * record finalize (K1 paths, sharded / split-phase), C1 allgather, K34
+ * select_commit + smooth_finalize, unused] (0 if not run); it
  * synchronises the stream.  dinfer_launches_per_step: kernels the library
  * launches for one dinfer_step with these params (collectives excluded).    */
 dinfer_status dinfer_set_timing(dinfer_ctx* ctx, int32_t enable);

@@ -1898,7 +1898,7 @@ dinfer_status build_gen_graph(dinfer_ctx* c, const GenArgs& ga, const uint16_t* 
     st = dinfer_step(c, ga.hbuf, W, E, e_mask, ga.mask, ga.tokens, base->use_credit ? ga.cids : nullptr,
                      base->use_credit ? ga.cval : nullptr, base, c->g_com, base->use_smooth ? c->g_sm : nullptr,
                      nullptr);
-  if (le == cudaSuccess && st == DINFER_OK) le = launch_gen_control(ga, h, cs);
+  if (le == cudaSuccess && st == DINFER_OK) le = launch_gen_control(ga, h, cs, pdl);
   c->stream = user_stream;
   c->pdl = user_pdl;
   c->timing = user_timing;

@@ -160,6 +160,9 @@ __global__ void __launch_bounds__(kGenThreads) gen_init_kernel(const GenArgs a, 
 __global__ void __launch_bounds__(kGenThreads) gen_control_kernel(const GenArgs a, cudaGraphConditionalHandle h) {
   __shared__ int s_flag;
   extern __shared__ int s_first[];
+  // launched with PDL behind K34: resident while K34 runs, proceeds the
+  // moment K34's commit is complete (no launch gap in the loop body)
+  grid_dep_wait();
   if (threadIdx.x == 0) {
     a.st[2] += 1;  // F
     a.st[1] += 1;  // t
@@ -229,9 +232,8 @@ cudaError_t launch_gen_init(const GenArgs& a, cudaGraphConditionalHandle h, cuda
   gen_init_kernel<<<1, kGenThreads, sizeof(int) * a.B, st>>>(a, h);
   return cudaGetLastError();
 }
-cudaError_t launch_gen_control(const GenArgs& a, cudaGraphConditionalHandle h, cudaStream_t st) {
-  gen_control_kernel<<<1, kGenThreads, sizeof(int) * a.B, st>>>(a, h);
-  return cudaGetLastError();
+cudaError_t launch_gen_control(const GenArgs& a, cudaGraphConditionalHandle h, cudaStream_t st, bool pdl) {
+  return launch_ex(gen_control_kernel, dim3(1), dim3(kGenThreads), sizeof(int) * a.B, st, pdl, a, h);
 }
 cudaError_t launch_gen_hidden(const GenArgs& a, int grid, cudaStream_t st) {
   gen_hidden_kernel<<<grid, 256, 0, st>>>(a);

@@ -280,7 +280,7 @@ cudaError_t launch_stage_copy(const void* src0, void* dst0, size_t bytes0, const
                               size_t bytes1, bool in, cudaStream_t st, bool pdl);
 cudaError_t launch_block_reset(uint8_t* mask, int32_t* tokens, int32_t* cids, float* cval, int M, int K, int mask_id,
                                cudaStream_t st, bool pdl);
-cudaError_t launch_gen_control(const GenArgs& a, cudaGraphConditionalHandle h, cudaStream_t st);
+cudaError_t launch_gen_control(const GenArgs& a, cudaGraphConditionalHandle h, cudaStream_t st, bool pdl);
 cudaError_t launch_gen_hidden(const GenArgs& a, int grid, cudaStream_t st);
 
 }  // namespace dinfer

@@ -703,7 +703,10 @@ def test_combine_block_start_writes_smoothed_rows(torch_cuda):
         assert np.array_equal(got[k], want[k]), k
     still = want["mask"]
     assert still.any()
-    assert np.array_equal(got["smoothed"][still], want["smoothed"][still])
+    # bitwise on the K1 -> K2 path; the fused K12 path (DINFER_FUSED=2) adds the
+    # CTAs' accumulators with L2 reductions: equal to fp32 rounding order only
+    np.testing.assert_allclose(got["smoothed"][still], want["smoothed"][still], rtol=1e-5, atol=1e-6)
+    assert np.isfinite(got["smoothed"][still]).all()
 
 
 def test_second_host_async_is_rejected(torch_cuda):
