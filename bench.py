@@ -204,8 +204,8 @@ def bench_config(world: int, Vl: int, exchange: str, partition: str, weight_copi
                    f"vs 126 MB L2); K back-to-back block-start steps under one event pair")}
 
 
-def default_partition(no_balance: bool) -> str:
-    return ("calibrated for back-to-back steps (dinfer_balance, 4 steps)" if CFG["smooth"] and not no_balance
+def default_partition(balance: bool) -> str:
+    return ("calibrated for back-to-back steps (dinfer_balance, 4 steps)" if CFG["smooth"] and balance
             else "even")
 
 
@@ -225,7 +225,7 @@ def reference_arm(args):
     value = rows / sec
     G = args.gpus
     Vl = V // G
-    cfg = bench_config(G, Vl, "p2p" if G > 1 else "none", default_partition(args.no_balance),
+    cfg = bench_config(G, Vl, "p2p" if G > 1 else "none", default_partition(args.balance),
                        weight_copies_for(Vl * H * 2 * (2 if CFG["smooth"] else 1)))
     cfg["oracle"] = "host cores (numpy fp64 oracle, whole vocabulary)"
     line = {
@@ -364,11 +364,11 @@ def gpu_arm(args):
 
     # calibrated vocab partition (K12): measured per-SM streaming rates -> slab split
     partition = "even"
-    if not args.no_balance and smooth:
+    if args.balance and smooth:
         from paper_2510_08666_b200 import DInferError
         try:
             ctx.balance(hid, Wd[0], Ed[0], emd, p, iters=4, mode="back_to_back")
-            partition = default_partition(False)
+            partition = default_partition(True)
         except DInferError:
             pass
     # warm-up: every kernel of every timed loop runs here first (CUDA loads
@@ -589,7 +589,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--config", default="moe", choices=sorted(CONFIGS))
-    ap.add_argument("--no-balance", action="store_true", help="keep the even K12 vocab partition")
+    ap.add_argument("--balance", action="store_true",
+                    help="calibrate the K12 vocab partition first (dinfer_balance); the default even partition "
+                         "measured as fast or faster with the round-2 W tiles (214.0-215.0 vs 215.1-216.2 us)")
+    ap.add_argument("--no-balance", action="store_true", help="(default; kept for old command lines)")
     ap.add_argument("--exchange", default="auto", choices=["auto", "p2p", "nccl"],
                     help="N>1 record exchange: peer memory (auto: if every rank can open it) or NCCL allgather")
     ap.add_argument("--shard-sim", type=int, default=0, choices=[0, 2, 4, 8],
