@@ -129,6 +129,46 @@ __global__ void __launch_bounds__(32) bulk_kernel(const uint8_t* src, size_t byt
   }
 }
 
+// Column-blocked ("packed") W: the buffer viewed as [cols/64 column blocks]
+// [rows][128 B]; each CTA owns a contiguous row slab, cut into tiles of
+// `trows` rows; a stage is `cpst` adjacent column blocks of one tile, each ONE
+// contiguous trows x 128 B bulk copy (K12's W stage shape from a prepacked W).
+__global__ void __launch_bounds__(32) packed_kernel(const uint8_t* src, int rows, int cols, int stages, int cpst,
+                                                    int trows, unsigned long long* sink) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbytes = static_cast<uint32_t>(cpst) * trows * 128u;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(stages) * sbytes);
+  const int units = rows / 32;
+  const int r0 = 32 * static_cast<int>(static_cast<long>(blockIdx.x) * units / gridDim.x);
+  const int r1 = 32 * static_cast<int>(static_cast<long>(blockIdx.x + 1) * units / gridDim.x);
+  const int nkc = cols / 64;
+  const int ntile = (r1 - r0 + trows - 1) / trows;
+  const long nst = static_cast<long>(ntile) * (nkc / cpst);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < stages; ++i) mbar_init(&full[i], 1);
+    fence_mbar_init();
+    unsigned long long acc = 0;
+    for (long st = 0; st < nst + stages; ++st) {
+      if (st >= stages) {
+        const long c = st - stages;
+        mbar_wait(&full[c % stages], static_cast<uint32_t>((c / stages) & 1));
+        acc += *reinterpret_cast<volatile uint32_t*>(smem + (c % stages) * sbytes);
+      }
+      if (st < nst) {
+        const int slot = static_cast<int>(st % stages);
+        const int t = static_cast<int>(st / (nkc / cpst)), kc0 = static_cast<int>(st % (nkc / cpst)) * cpst;
+        const int row0 = r0 + t * trows, nr = min(trows, r1 - row0);
+        mbar_expect_tx(&full[slot], static_cast<uint32_t>(cpst * nr * 128));
+        for (int j = 0; j < cpst; ++j)
+          bulk_load(smem + static_cast<size_t>(slot) * sbytes + j * trows * 128,
+                    src + (static_cast<size_t>(kc0 + j) * rows + row0) * 128, nr * 128, &full[slot]);
+      }
+    }
+    if (acc == 0x12345678ull) *sink = acc;
+  }
+}
+
 struct Timer {
   cudaEvent_t e0, e1;
   Timer() {
@@ -241,6 +281,19 @@ int main(int argc, char** argv) {
     snprintf(name, sizeof(name), "bulk 1-D %d CTA/SM %d x %3d KB", cps, stages, chunk / 1024);
     measure(name, bytes, [&](int r) {
       bulk_kernel<<<sms * cps, 32, smem>>>(static_cast<const uint8_t*>(buf[r % kBufs]), bytes, stages, chunk, sink);
+    });
+  }
+  // (4) packed (column-blocked) W stages
+  cudaFuncSetAttribute(packed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  const int pconf[][3] = {{4, 2, 160}, {4, 2, 128}, {3, 2, 160}, {5, 2, 160}, {2, 4, 160}, {4, 1, 160}};
+  for (auto& c : pconf) {
+    const int stages = c[0], cpst = c[1], trows = c[2];
+    const size_t smem = static_cast<size_t>(stages) * cpst * trows * 128 + stages * 8 + 1024;
+    if (smem > 227 * 1024) continue;
+    char name[96];
+    snprintf(name, sizeof(name), "packed 1 CTA/SM %d x %2d KB (%3d rows x %d blk)", stages, cpst * trows / 8, trows, cpst);
+    measure(name, bytes, [&](int r) {
+      packed_kernel<<<sms, 32, smem>>>(static_cast<const uint8_t*>(buf[r % kBufs]), rows, cols, stages, cpst, trows, sink);
     });
   }
   return 0;
