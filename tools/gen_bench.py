@@ -1,7 +1,9 @@
 """Time the device-resident generation loop (dinfer_generate) at a BASELINE
 shape: one CUDA-graph launch runs every forward of a generation; per-forward
 time = graph time / F, compared with the same number of dinfer_step calls
-launched from the host.  Hidden states are planted (synth), not vetted --
+launched from the host (no control flow: a lower bound), and with a
+host-driven Alg. 1 loop (per forward a device->host mask read decides the
+block's end, schedules computed on the host).  Hidden states are planted (synth), not vetted --
 this measures time, not parity.
   python tools/gen_bench.py [--config moe|8b] [--blocks 8] [--reps 5]"""
 import argparse
@@ -14,6 +16,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2510_08666_b200 import Context, make_gen_config, make_params, synth  # noqa: E402
+from paper_2510_08666_b200.dinfer import alpha_schedule, tau_schedule  # noqa: E402
 
 CONFIGS = {"moe": (2048, 157184, "hierarchical", True, True), "8b": (4096, 126464, "threshold", False, False)}
 
@@ -83,10 +86,47 @@ def main():
         e1.synchronize()
         if r:
             host.append(e0.elapsed_time(e1))
-    g, h_ = float(np.median(times)), float(np.median(host))
+    # A host-driven Alg. 1 loop (what the device loop replaces): per
+    # forward the model stand-in's hidden copy, the step with the host-computed
+    # schedules (tau_t, alpha_t), then a device->host read of the mask to decide
+    # whether the block is done (host control flow needs it); at block end the
+    # block is written into X, EOS checked on the host, the next block reset.
+    hbuf = torch.empty_like(hsrc[0])
+    Xh = torch.empty_like(X)
+    alg1 = []
+    F_host = 0
+    for r in range(a.reps + 1):
+        Xh.copy_(X0.cuda())
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        n = 0
+        for blk in range(a.blocks):
+            ctx.block_reset(mask, tok, cids, cval, synth.mask_id(V))
+            t = 0
+            while True:
+                hbuf.copy_(hsrc[n % iters])
+                pt = make_params(decoder=dec, use_credit=credit, use_smooth=smooth, theta_lo=0.62,
+                                 tau=tau_schedule(0.9, t, 2), theta_hi=tau_schedule(0.9, t, 2),
+                                 alpha_t=alpha_schedule(0.1, 0.05, 0.3, t))
+                ctx.step(hbuf, Wd, Ed, em, mask, tok, cids, cval, pt, com, sm, None)
+                n += 1
+                t += 1
+                if not bool(mask.any().item()) or t >= S:  # device -> host read: the host decides
+                    break
+            Xh[:, P + blk * S:P + (blk + 1) * S] = tok.view(B, S)
+            if bool((tok == synth.eos_id(V)).any().item()):
+                break
+        e1.record(st)
+        e1.synchronize()
+        if r:
+            alg1.append(e0.elapsed_time(e1))
+            F_host = n
+    g, h_, al = float(np.median(times)), float(np.median(host)), float(np.median(alg1))
     print(json.dumps({"config": a.config, "blocks": a.blocks, "F": F, "T": int(o[0]), "tpf": o[0] / max(F, 1),
                       "loop_ms": g, "loop_us_per_forward": 1e3 * g / F,
-                      "host_steps_ms": h_, "host_us_per_step": 1e3 * h_ / F}))
+                      "host_steps_ms": h_, "host_us_per_step": 1e3 * h_ / F,
+                      "host_alg1_forwards": F_host, "host_alg1_us_per_forward": 1e3 * al / max(F_host, 1)}))
 
 
 if __name__ == "__main__":
