@@ -141,3 +141,49 @@ def test_e2e_host_async_pinned(moe):
                    vtilde=st[..., 3].copy().view(np.int32))
         compare(out, moe["res"], moe["mask"], moe["p"], where=f"e2e rep {rep}", exclude=moe["excl"])
     ctx.close()
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_shard_sim_step_equals_tiled_vocab_step(moe, G):
+    """bench.py --shard-sim G times one rank of a G-way vocab shard with the
+    loopback exchange (every "peer" record is this rank's own).  The merged
+    step is then exactly the single-rank step over a vocabulary of G copies of
+    the shard (the first copy's ids: lowest id on ties, reading c3; lse over
+    G l; e_{t+1} from G identical accumulators over G l).  Checked against that
+    single-rank step -- oracle-checked itself above -- at the LLaDA-MoE shape
+    with a hidden block planted on the shard: decisions and credit slots
+    bitwise, statistics and e_{t+1} to fp32 summation order (the single-rank
+    path sums fp16 group partials, reading c28)."""
+    import torch
+    from paper_2510_08666_b200 import Context
+    d = moe["dev"]
+    Vl = V // G
+    W, E = d["W"][:Vl], d["E"][:Vl]
+    h = to_dev_bf16(synth.planted_hidden(moe["W"][:Vl], B * S, seed=3))
+    pbs = gpu_params(moe["p"])
+    pbs.block_start, pbs.mask_id = 1, synth.mask_id(V)
+    shard = Context(B, S, H, K, V, V_local=Vl, v_offset=0, world=G, rank=0)
+    shard.exchange_loopback()
+    tiled = Context(B, S, H, K, V)
+    Wt, Et = W.repeat(G, 1).contiguous(), E.repeat(G, 1).contiguous()
+    snaps = []
+    for ctx, Wx, Ex in ((shard, W, E), (tiled, Wt, Et)):
+        st = GpuState(B, S, H, K, synth.mask_id(V))
+        for _ in range(2):  # back to back (the second step reads the other record slot)
+            ctx.step(h, Wx, Ex, d["em"], st.mask, st.tokens, st.cids, st.cval, pbs, st.committed, st.smoothed,
+                     st.stats)
+        torch.cuda.synchronize()
+        ctx.sync()
+        snaps.append(st.snapshot())
+        ctx.close()
+    a, b = snaps
+    pt = np.sort(b["ptilde"].ravel())
+    assert pt[-1] - pt[-2] > 1e-4  # the fallback's winner is not a near tie
+    for k in ("committed", "mask", "tokens", "cids", "vtilde"):
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+    np.testing.assert_allclose(a["cval"], b["cval"], rtol=1e-5, atol=1e-7)
+    np.testing.assert_allclose(a["lse"], b["lse"], rtol=1e-6, atol=1e-5)
+    np.testing.assert_allclose(a["ptilde"], b["ptilde"], rtol=1e-5, atol=1e-7)
+    x, y = a["smoothed"].reshape(-1, H).astype(np.float64), b["smoothed"].reshape(-1, H).astype(np.float64)
+    rel = np.linalg.norm(x - y, axis=-1) / np.linalg.norm(y, axis=-1)
+    assert rel.max() <= 5e-4, rel.max()
