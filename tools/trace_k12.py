@@ -75,6 +75,15 @@ def main():
     x = us(k34[:, 1]), us(k34[:, 3])
     print(f"  K34: deps visible min {x[0].min():.1f} med {np.median(x[0]):.1f}; exit max {x[1].max():.1f} us "
           f"(last K12 exit {us(k1[:, 3]).max():.1f})")
+    # K34 stamps per block: [entry, deps visible, phase mark, end, smid]; block 0 selects (mark = phase 1
+    # done), the others smooth (mark = accumulators loaded)
+    sel, smo = k34[:1], k34[1:]
+    for name, blk in (("selection", sel), ("smoothing", smo)):
+        if len(blk) == 0:
+            continue
+        e, d, m, z = (us(blk[:, j]) for j in range(4))
+        print(f"  K34 {name:9s} entry med {np.median(e):6.1f}  deps med {np.median(d):6.1f}  "
+              f"mark med {np.median(m):6.1f} max {m.max():6.1f}  end med {np.median(z):6.1f} max {z.max():6.1f} us")
     ctx.close()
 
 
