@@ -213,6 +213,7 @@ __global__ void __launch_bounds__(kAThreads) kv_attention(const AttnArgs a) {
 // out[lo + r][head*128 + c..c+3] = sum_s O_s 2^{m_s - m} / sum_s l_s 2^{m_s - m}
 // (splits merged in index order: deterministic), one float4 per thread.
 __global__ void kv_attention_merge(const AttnArgs a) {
+  grid_dep_wait();  // PDL (tcgen05 path): the key-tile partials of the attention kernel are complete
   const long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int h4 = a.H / 4;
   if (e >= static_cast<long>(a.R) * h4) return;
@@ -240,21 +241,25 @@ __global__ void kv_attention_merge(const AttnArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Tensor-core attention (tcgen05): CTA = (head, 128-query tile, 256-key tile).
-//   S = Q K^T      UMMA M=128 (queries) x N=256 (keys) x K=128 (d), both
+// Tensor-core attention (tcgen05): CTA = (head, 128-query tile, kTK-key tile).
+//   S = Q K^T      UMMA M=128 (queries) x N=kTK (keys) x K=128 (d), both
 //                  operands K-major SW128 straight from the row-major Q / cache
-//                  (TMA boxes [128|256 rows x 64 d]); S in TMEM columns 0-255
+//                  (TMA boxes [128|kTK rows x 64 d]); S in TMEM columns [0, kTK)
 //   P = exp2((S - m) log2e / sqrt(d)) per query row (thread = row, tcgen05.ld),
 //                  masked beyond L; bf16 into a K-major SW128 smem tile (the K
 //                  tile's bytes, consumed by then)
-//   O = P V        UMMA M=128 x N=128 (d) x K=256 (keys): V is the MN-major B
+//   O = P V        UMMA M=128 x N=128 (d) x K=kTK (keys): V is the MN-major B
 //                  operand taken straight from the row-major cache (boxes
-//                  [64 d x 256 keys], LBO between the two 64-d blocks)
+//                  [64 d x kTK keys], LBO between the two 64-d blocks)
 // and the (m, l, O) partial of the key tile goes to the same split merge.
 // ---------------------------------------------------------------------------
+// 256-key tiles (80 CTAs at the steady-state region, 64 queries, L = 1088):
+// 128-key tiles (144 CTAs) measured slower, 33.8 vs 32.0 us per vicinity
+// forward and 132 vs 108 us per full refresh (more Q loads, 9 partials to merge)
 constexpr int kTQ = 128, kTK = 256;
+constexpr uint32_t kTcCols = (kTK + 128 <= 256) ? 256u : 512u;  // TMEM: S [kTK] + O [d = 128] columns
 constexpr uint32_t kQBlk = kTQ * 128;    // [128 rows x 64 d] bf16 = 16 KB
-constexpr uint32_t kKBlk = kTK * 128;    // [256 rows x 64 d] bf16 = 32 KB
+constexpr uint32_t kKBlk = kTK * 128;    // [kTK rows x 64 d] bf16
 constexpr uint32_t kPBlk = kTQ * 128;    // [128 q x 64 keys] bf16 = 16 KB
 constexpr size_t kTcSmem = 2 * kQBlk + 2 * kKBlk + 2 * kKBlk + 64 + 1024;
 
@@ -287,14 +292,16 @@ __global__ void __launch_bounds__(128, 1)
     for (int i = 0; i < 3; ++i) mbar_init(&bar[i], 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc(&misc[0], 512);
+  if (warp == 0) tmem_alloc(&misc[0], kTcCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = misc[0];
-  const uint32_t tS = tmem, tO = tmem + 256;
+  const uint32_t tS = tmem, tO = tmem + kTK;
+  grid_dep_launch_dependents();  // the merge kernel may launch (it waits for this grid)
   if (threadIdx.x == 0) {
     const uint64_t pol = policy_evict_normal();
+    grid_dep_wait();  // PDL: Q and the refreshed cache rows of kv_proj_tc are complete
     mbar_expect_tx(&bar[0], 2 * kQBlk + 4 * kKBlk);
     for (int j = 0; j < 2; ++j) {
       tma_load_2d(sQ + j * kQBlk, &map_q, &bar[0], head * kD + 64 * j, q0, pol);
@@ -390,7 +397,7 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 0) tmem_dealloc(tmem, 512);
+  if (warp == 0) tmem_dealloc(tmem, kTcCols);
 }
 
 // ---------------------------------------------------------------------------
@@ -406,18 +413,24 @@ __global__ void __launch_bounds__(128, 1)
 // through distributed shared memory in rank order (deterministic), and the
 // leader writes bf16 rows of 16-B chunks into the cache / Q buffer.
 // ---------------------------------------------------------------------------
-constexpr int kPjStages = 4;
+constexpr int kPjMaxStages = 8;             // ring depth cap of the measurement override
 constexpr uint32_t kPjWBox = 128u * 128u;  // [128 rows x 64 k] bf16
 
 struct ProjArgs {
-  int H, R, lo, NT, nkc, ks;
+  int H, R, lo, NT, nkc, ks, stages, cps;  // cps: 64-wide K chunks per ring stage
   uint16_t* dst[3];   // row p of projection m at dst[m] + (p - dst_row0[m]) * H
   int dst_row0[3];
 };
 
-__host__ __device__ inline size_t kv_proj_smem(int NT) {
-  return static_cast<size_t>(kPjStages) * (kPjWBox + static_cast<uint32_t>(NT) * 128u) + 2 * kPjStages * 8 + 64 +
-         1024;
+// The ring, or (if larger) the epilogue's [NT][128] fp32 tile + bf16 rows that
+// reuse it; the barriers follow.
+__host__ __device__ inline size_t kv_proj_body(int NT, int stages, int cps) {
+  const size_t ring = static_cast<size_t>(stages) * cps * (kPjWBox + static_cast<uint32_t>(NT) * 128u);
+  const size_t epi = static_cast<size_t>(NT) * 128u * 6u;
+  return ring > epi ? ring : epi;
+}
+__host__ __device__ inline size_t kv_proj_smem(int NT, int stages, int cps) {
+  return kv_proj_body(NT, stages, cps) + 2 * stages * 8 + 64 + 1024;
 }
 
 DI uint32_t cluster_ctarank() {
@@ -444,10 +457,13 @@ __global__ void __launch_bounds__(128, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t xbox = static_cast<uint32_t>(a.NT) * 128u;
-  const uint32_t slot = kPjWBox + xbox;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPjStages * slot);
-  uint64_t* empty = full + kPjStages;
-  uint64_t* done = empty + kPjStages;
+  const int cps = a.cps;
+  const uint32_t slot = static_cast<uint32_t>(cps) * (kPjWBox + xbox);  // [cps W boxes][cps X boxes]
+  const uint32_t xoff = static_cast<uint32_t>(cps) * kPjWBox;
+  const int nst = a.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kv_proj_body(a.NT, nst, cps));
+  uint64_t* empty = full + nst;
+  uint64_t* done = empty + nst;
   uint32_t* misc = reinterpret_cast<uint32_t*>(done + 1);
   const int ftiles = a.H / 128;
   const int m = blockIdx.x / ftiles, ft = blockIdx.x - m * ftiles;
@@ -459,7 +475,7 @@ __global__ void __launch_bounds__(128, 1)
   if (threadIdx.x == 0) {
     prefetch_tmap(mw);
     prefetch_tmap(&map_x);
-    for (int i = 0; i < kPjStages; ++i) {
+    for (int i = 0; i < nst; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
@@ -467,31 +483,36 @@ __global__ void __launch_bounds__(128, 1)
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(&misc[0], 256);
+  grid_dep_launch_dependents();  // the attention kernel may launch (it waits for this grid)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = misc[0];
   if (threadIdx.x == 0) {  // TMA producer
     const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
-    for (int kc = kc0, i = 0; kc < kc1; ++kc, ++i) {
-      const int st = i % kPjStages;
-      if (i >= kPjStages) mbar_wait(&empty[st], static_cast<uint32_t>((i / kPjStages - 1) & 1));
+    for (int kc = kc0, i = 0; kc < kc1; kc += cps, ++i) {
+      const int st = i % nst, nc = min(cps, kc1 - kc);
+      if (i >= nst) mbar_wait(&empty[st], static_cast<uint32_t>((i / nst - 1) & 1));
       uint8_t* sl = smem + st * slot;
-      mbar_expect_tx(&full[st], slot);
-      tma_load_2d(sl, mw, &full[st], kc * 64, ft * 128, pol_w);
-      tma_load_2d(sl + kPjWBox, &map_x, &full[st], kc * 64, p0, pol_x);  // rows past L: zero fill
+      mbar_expect_tx(&full[st], static_cast<uint32_t>(nc) * (kPjWBox + xbox));
+      for (int j = 0; j < nc; ++j) {
+        tma_load_2d(sl + j * kPjWBox, mw, &full[st], (kc + j) * 64, ft * 128, pol_w);
+        tma_load_2d(sl + xoff + j * xbox, &map_x, &full[st], (kc + j) * 64, p0, pol_x);  // rows past L: zero fill
+      }
     }
   } else if (warp == 1) {  // MMA issuer (warp-collective issue, common.cuh mma_bf16_warp)
     const uint32_t idesc = idesc_bf16(128, a.NT, false, false);
-    for (int kc = kc0, i = 0; kc < kc1; ++kc, ++i) {
-      const int st = i % kPjStages;
-      mbar_wait(&full[st], static_cast<uint32_t>((i / kPjStages) & 1));
+    for (int kc = kc0, i = 0; kc < kc1; kc += cps, ++i) {
+      const int st = i % nst, nc = min(cps, kc1 - kc);
+      mbar_wait(&full[st], static_cast<uint32_t>((i / nst) & 1));
       tc_fence_after();
-      const uint64_t da = sdesc_sw128(smem_u32(smem + st * slot), 16, 1024);
-      const uint64_t db = sdesc_add(da, kPjWBox);
+      for (int j = 0; j < nc; ++j) {
+        const uint64_t da = sdesc_sw128(smem_u32(smem + st * slot + j * kPjWBox), 16, 1024);
+        const uint64_t db = sdesc_sw128(smem_u32(smem + st * slot + xoff + j * xbox), 16, 1024);
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        mma_bf16_warp(tmem, sdesc_add(da, k * 32), sdesc_add(db, k * 32), idesc, (i | k) != 0 ? 1u : 0u);
+        for (int k = 0; k < 4; ++k)
+          mma_bf16_warp(tmem, sdesc_add(da, k * 32), sdesc_add(db, k * 32), idesc, (i | j | k) != 0 ? 1u : 0u);
+      }
       mma_commit_warp(&empty[st]);
     }
     mma_commit_warp(done);
@@ -601,6 +622,18 @@ struct dinfer_kv {
   dinfer_kv_shape shp{};
   cudaStream_t stream = nullptr;
   int num_sms = 0;
+  size_t smem_optin = 0;  // per-block opt-in shared memory (kv_proj_tc ring depth)
+  // kv_proj_tc ring: 4 stages of one 64-wide K chunk (same-box A/B at the MoE
+  // attention shape, tools/kv_ab.sh: 33.1-33.2 us per vicinity forward vs
+  // 33.4 for 2 x 2 chunks, 33.7 for 3 x 1, 35.0 for 2 x 1, 42.0 for 3 x 2 --
+  // footprints that leave one CTA per SM strand clusters of ks CTAs in a second
+  // wave); env DINFER_KV_PJ_STAGES / DINFER_KV_PJ_CPS (measurement)
+  int pj_stages = 4;
+  int pj_nt = 0, pj_ks = 0, pj_st = 0;  // cached ring depth for (NT, ks)
+  int pj_cps = 1;  // K chunks per kv_proj_tc stage, at most
+  int pj_cur_cps = 1;
+  bool pdl = true;               // PDL between the projections, the attention and the merge (env DINFER_KV_PDL)
+  int ks_max = 4;                // kv_proj_tc cluster split of K cap (env DINFER_KV_KS, measurement)
   uint16_t* Q = nullptr;  // [L][H]
   float* opart = nullptr;
   float* mpart = nullptr;
@@ -656,8 +689,15 @@ dinfer_status dinfer_kv_create(const dinfer_kv_shape* s, void* stream, dinfer_kv
             cudaMalloc(&c->mpart, nml * 4) == cudaSuccess && cudaMalloc(&c->lpart, nml * 4) == cudaSuccess;
   const size_t ncnt = static_cast<size_t>(s->H / kD) * ((s->L + kTQ - 1) / kTQ);
   if (ok) ok = cudaMalloc(&c->cnt, ncnt * 4) == cudaSuccess && cudaMemset(c->cnt, 0, ncnt * 4) == cudaSuccess;
-  if (ok) ok = ensure_func_smem(reinterpret_cast<const void*>(kv_proj_tc), kv_proj_smem(256)) == cudaSuccess;
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  c->smem_optin = optin > 0 ? static_cast<size_t>(optin) : kv_proj_smem(256, 2, 1);
+  if (ok) ok = ensure_func_smem(reinterpret_cast<const void*>(kv_proj_tc), c->smem_optin) == cudaSuccess;
   if (const char* e = std::getenv("DINFER_KV_TC")) c->tc = std::atoi(e) != 0;
+  if (const char* e = std::getenv("DINFER_KV_PDL")) c->pdl = std::atoi(e) != 0;
+  if (const char* e = std::getenv("DINFER_KV_PJ_CPS")) c->pj_cps = std::max(1, std::min(4, std::atoi(e)));
+  if (const char* e = std::getenv("DINFER_KV_KS")) c->ks_max = std::max(1, std::min(8, std::atoi(e)));
+  if (const char* e = std::getenv("DINFER_KV_PJ_STAGES")) c->pj_stages = std::max(2, std::min(kPjMaxStages, std::atoi(e)));
   if (ok && c->tc) {
     ok = kv_map(&c->map_q, c->Q, static_cast<uint64_t>(s->H), static_cast<uint64_t>(s->L), kTQ) &&
          cudaFuncSetAttribute(kv_attention_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -723,7 +763,7 @@ dinfer_status dinfer_kv_step(dinfer_kv* c, const uint16_t* X, const uint16_t* Wq
       c->c_xnt = NT;
     }
     const int tiles = 3 * (H / 128) * ntp, nkc = H / 64;
-    const int ks = std::max(1, std::min({4, c->num_sms / tiles, nkc}));
+    const int ks = std::max(1, std::min({c->ks_max, std::max(1, c->ks_max > 4 ? 2 * c->num_sms / tiles : c->num_sms / tiles), nkc}));
     ProjArgs pa{};
     pa.H = H;
     pa.R = R;
@@ -731,6 +771,25 @@ dinfer_status dinfer_kv_step(dinfer_kv* c, const uint16_t* X, const uint16_t* Wq
     pa.NT = NT;
     pa.nkc = nkc;
     pa.ks = ks;
+    // Ring geometry: stages of cps K chunks, the deepest ring (<= pj_stages)
+    // that fits (DINFER_KV_PJ_CPS / DINFER_KV_PJ_STAGES; defaults measured,
+    // see kv_create)
+    if (c->pj_nt != NT || c->pj_ks != ks) {
+      c->pj_cur_cps = c->pj_cps;
+      c->pj_st = 0;
+      for (int cps = c->pj_cps; cps >= 1 && c->pj_st == 0; --cps)
+        for (int st = c->pj_stages; st >= 2; --st)
+          if (kv_proj_smem(NT, st, cps) <= c->smem_optin) {
+            c->pj_st = st;
+            c->pj_cur_cps = cps;
+            break;
+          }
+      if (c->pj_st == 0) return DINFER_ERR_UNSUPPORTED;
+      c->pj_nt = NT;
+      c->pj_ks = ks;
+    }
+    pa.stages = c->pj_st;
+    pa.cps = c->pj_cur_cps;
     pa.dst[0] = Kc;
     pa.dst[1] = Vc;
     pa.dst[2] = c->Q;
@@ -740,7 +799,7 @@ dinfer_status dinfer_kv_step(dinfer_kv* c, const uint16_t* X, const uint16_t* Wq
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(3 * (H / 128), ntp, ks);
     cfg.blockDim = dim3(128);
-    cfg.dynamicSmemBytes = kv_proj_smem(NT);
+    cfg.dynamicSmemBytes = kv_proj_smem(NT, pa.stages, pa.cps);
     cfg.stream = c->stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -775,7 +834,11 @@ dinfer_status dinfer_kv_step(dinfer_kv* c, const uint16_t* X, const uint16_t* Wq
     t.lpart = c->lpart;
     t.cnt = c->cnt;
     t.out = out;
-    kv_attention_tc<<<dim3(nh, nqt, nkt), 128, kTcSmem, c->stream>>>(c->map_q, c->map_k, c->map_v, t);
+    // PDL chain: the attention CTAs launch while the projections drain (setup,
+    // TMEM allocation) and wait for them before their loads; the merge likewise
+    if (launch_ex(kv_attention_tc, dim3(nh, nqt, nkt), dim3(128), kTcSmem, c->stream, c->pdl, c->map_q, c->map_k,
+                  c->map_v, t) != cudaSuccess)
+      return DINFER_ERR_CUDA;
     AttnArgs m{};
     m.L = L;
     m.H = H;
@@ -787,8 +850,9 @@ dinfer_status dinfer_kv_step(dinfer_kv* c, const uint16_t* X, const uint16_t* Wq
     m.lpart = c->lpart;
     m.out = out;
     const long n4 = static_cast<long>(R) * H / 4;
-    kv_attention_merge<<<static_cast<unsigned>((n4 + 127) / 128), 128, 0, c->stream>>>(m);
-    if (cudaGetLastError() != cudaSuccess) return DINFER_ERR_CUDA;
+    if (launch_ex(kv_attention_merge, dim3(static_cast<unsigned>((n4 + 127) / 128)), dim3(128), 0, c->stream, c->pdl,
+                  m) != cudaSuccess)
+      return DINFER_ERR_CUDA;
     return DINFER_OK;
   }
   const int nheads = H / kD, qtiles = (R + kQT - 1) / kQT;
