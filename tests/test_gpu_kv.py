@@ -105,3 +105,41 @@ def test_vicinity_llada_moe_layer(torch_cuda):
     """LLaDA-MoE attention shape: H = 2048 (16 heads of 128), L = 64 + 1024
     (prompt + gen length 1024); two blocks, attention checked on sampled rows."""
     run_blocks(torch_cuda, 1088, 2048, 64, 32, 2, 5, seed=4, check_rows=np.arange(0, 1088, 37))
+
+
+@pytest.mark.parametrize("geom", [("0", "4", "1"), ("1", "2", "2"), ("1", "3", "1")])
+def test_vicinity_launch_modes_bitwise(torch_cuda, monkeypatch, geom):
+    """The PDL chain (projections -> attention -> merge) and the projection's
+    ring geometry (stages x K chunks per stage) change scheduling only: the
+    cache rows and the attention output are bitwise those of the default
+    launch (PDL on, 4 x 1), at the LLaDA-MoE attention shape (vicinity and
+    full-refresh regions; the full refresh uses 224-position tiles whose
+    epilogue tile exceeds a shallow ring)."""
+    import torch
+    from paper_2510_08666_b200 import VicinityKV
+    L, H = 1088, 2048
+    g = torch.Generator(device="cuda").manual_seed(7)
+    W = [(torch.randn((H, H), device="cuda", generator=g) / H ** 0.5).to(torch.bfloat16) for _ in range(3)]
+    X = torch.randn((L, H), device="cuda", generator=g).to(torch.bfloat16)
+
+    def run():
+        kv = VicinityKV(L, H, 128, 16, 16, 4)
+        Kc = torch.zeros((L, H), dtype=torch.bfloat16, device="cuda")
+        Vc = torch.zeros_like(Kc)
+        out = torch.zeros((L, H), dtype=torch.float32, device="cuda")
+        res = []
+        for t, full in ((0, True), (9, False)):
+            kv.step(X, *W, Kc, Vc, 64 + 512, 64 + 544, t, out, full=full)
+            torch.cuda.synchronize()
+            res += [Kc.clone(), Vc.clone(), out.clone()]
+        kv.close()
+        return res
+
+    ref = run()
+    pdl, st, cps = geom
+    monkeypatch.setenv("DINFER_KV_PDL", pdl)
+    monkeypatch.setenv("DINFER_KV_PJ_STAGES", st)
+    monkeypatch.setenv("DINFER_KV_PJ_CPS", cps)
+    got = run()
+    for a, b in zip(ref, got):
+        assert torch.equal(a, b), geom
