@@ -220,9 +220,42 @@ __global__ void kv_attention_merge(const AttnArgs a) {
   const int r = static_cast<int>(e / h4), col = static_cast<int>(e - static_cast<long>(r) * h4) * 4;
   const int head = col / kD, nheads = a.H / kD;
   float m = neg_inf();
-  for (int s = 0; s < a.nsplit; ++s) m = fmaxf(m, __ldcg(a.mpart + (static_cast<long>(s) * nheads + head) * a.R + r));
   float den = 0.f;
   float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
+  constexpr int kMaxSplit = 8;
+  if (a.nsplit <= kMaxSplit) {
+    // every split's (m, l, O) loaded before the first use (one round trip; the
+    // two-loop form below is a dependent chain of 2 x nsplit loads); the same
+    // operations in the same order, so bitwise the same result
+    float ms[kMaxSplit], ls[kMaxSplit];
+    float4 o[kMaxSplit];
+#pragma unroll
+    for (int s = 0; s < kMaxSplit; ++s)
+      if (s < a.nsplit) {
+        const long mi = (static_cast<long>(s) * nheads + head) * a.R + r;
+        ms[s] = __ldcg(a.mpart + mi);
+        ls[s] = __ldcg(a.lpart + mi);
+        o[s] = __ldcg(reinterpret_cast<const float4*>(a.opart + (static_cast<long>(s) * a.R + r) * a.H + col));
+      }
+#pragma unroll
+    for (int s = 0; s < kMaxSplit; ++s)
+      if (s < a.nsplit) m = fmaxf(m, ms[s]);
+#pragma unroll
+    for (int s = 0; s < kMaxSplit; ++s) {
+      if (s >= a.nsplit || ms[s] == neg_inf()) continue;  // a split with no keys
+      const float w = ex2(ms[s] - m);
+      num.x = fmaf(o[s].x, w, num.x);
+      num.y = fmaf(o[s].y, w, num.y);
+      num.z = fmaf(o[s].z, w, num.z);
+      num.w = fmaf(o[s].w, w, num.w);
+      den = fmaf(ls[s], w, den);
+    }
+    const float inv = 1.f / den;
+    *reinterpret_cast<float4*>(a.out + static_cast<long>(a.lo + r) * a.H + col) =
+        make_float4(num.x * inv, num.y * inv, num.z * inv, num.w * inv);
+    return;
+  }
+  for (int s = 0; s < a.nsplit; ++s) m = fmaxf(m, __ldcg(a.mpart + (static_cast<long>(s) * nheads + head) * a.R + r));
   for (int s = 0; s < a.nsplit; ++s) {
     const long mi = (static_cast<long>(s) * nheads + head) * a.R + r;
     const float ms = __ldcg(a.mpart + mi);
@@ -525,7 +558,6 @@ __global__ void __launch_bounds__(128, 1)
   const uint32_t lrow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
   const int feat = threadIdx.x;
   const bool split = a.ks > 1;
-  const bool leader = !split || cluster_ctarank() == 0;
   for (int c0 = 0; c0 < a.NT; c0 += 32) {
     float x[32];
     tmem_ld32(lrow + c0, x);
@@ -535,53 +567,50 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_before();
   if (split) cluster_sync_all();  // every CTA's partial in its shared memory
   else __syncthreads();
-  if (leader) {
-    if (split) {  // + the other ranks' partials, in rank order; 4 x (ks - 1) loads in flight
-      float4* red4 = reinterpret_cast<float4*>(red);
-      const int nq = a.NT * 32;
-      for (int q0 = threadIdx.x; q0 < nq; q0 += 4 * 128) {
-        float4 acc[4], v[4][3];
+  // Every CTA of the cluster finishes 1/ks of the tile's positions: the ks
+  // partials summed in rank order ((p0 + p1) + p2, whichever CTA sums --
+  // bitwise the leader-only epilogue this replaces), bf16, 8-B stores of 4
+  // features (a warp covers a position's 256-B row segment).  The leader-only
+  // version left the other CTAs parked at the final cluster barrier (~45 % of
+  // the kernel's stall samples, ncu).
+  const int rank = split ? static_cast<int>(cluster_ctarank()) : 0, nr = split ? a.ks : 1;
+  const int q_lo = (rank * a.NT / nr) * 32, q_hi = ((rank + 1) * a.NT / nr) * 32;
+  uint16_t* dst = (m == 0) ? a.dst[0] : (m == 1) ? a.dst[1] : a.dst[2];  // no dynamic param indexing
+  const int row0 = (m == 0) ? a.dst_row0[0] : (m == 1) ? a.dst_row0[1] : a.dst_row0[2];
+  const float4* red4 = reinterpret_cast<const float4*>(red);
+  for (int q0 = q_lo + static_cast<int>(threadIdx.x); q0 < q_hi; q0 += 4 * 128) {
+    float4 v[4][4];  // [u][rank]: 4 x ks loads in flight
 #pragma unroll
-        for (int u = 0; u < 4; ++u) acc[u] = (q0 + u * 128 < nq) ? red4[q0 + u * 128] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int r = 1; r < 4; ++r)
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (r < a.ks && q0 + u * 128 < nq) v[u][r - 1] = ld_dsmem_v4(red4 + q0 + u * 128, r);
-#pragma unroll
-        for (int r = 1; r < 4; ++r)
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (r < a.ks && q0 + u * 128 < nq) {
-              acc[u].x += v[u][r - 1].x;
-              acc[u].y += v[u][r - 1].y;
-              acc[u].z += v[u][r - 1].z;
-              acc[u].w += v[u][r - 1].w;
-            }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (q0 + u * 128 < nq) red4[q0 + u * 128] = acc[u];
+      for (int r = 0; r < 4; ++r) {
+        const int q = q0 + u * 128;
+        if (r < nr && q < q_hi) v[u][r] = (r == rank) ? red4[q] : ld_dsmem_v4(red4 + q, static_cast<uint32_t>(r));
       }
-      __syncthreads();
-    }
-    // bf16 rows [NT positions][128 features] (256 B each) staged after the fp32 tile
-    uint16_t* ob = reinterpret_cast<uint16_t*>(red + a.NT * 128);
-    for (int c = 0; c < a.NT; ++c) {
-      const __nv_bfloat16 v = __float2bfloat16_rn(red[c * 128 + feat]);
-      ob[c * 128 + feat] = *reinterpret_cast<const uint16_t*>(&v);
-    }
-    __syncthreads();
-    uint16_t* dst = (m == 0) ? a.dst[0] : (m == 1) ? a.dst[1] : a.dst[2];  // no dynamic param indexing
-    const int row0 = (m == 0) ? a.dst_row0[0] : (m == 1) ? a.dst_row0[1] : a.dst_row0[2];
-    for (int u = threadIdx.x; u < a.NT * 16; u += 128) {
-      const int c = u / 16, q = u % 16;
-      const int pos = p0 + c;
-      if (pos < a.lo + a.R)
-        *reinterpret_cast<uint4*>(dst + static_cast<long>(pos - row0) * a.H + ft * 128 + q * 8) =
-            *reinterpret_cast<const uint4*>(ob + c * 128 + q * 8);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = q0 + u * 128;
+      if (q >= q_hi) continue;
+      float4 acc = v[u][0];
+#pragma unroll
+      for (int r = 1; r < 4; ++r)
+        if (r < nr) {
+          acc.x += v[u][r].x;
+          acc.y += v[u][r].y;
+          acc.z += v[u][r].z;
+          acc.w += v[u][r].w;
+        }
+      const int c = q / 32, f4 = q % 32, pos = p0 + c;
+      if (pos < a.lo + a.R) {
+        const __nv_bfloat162 b01 = __floats2bfloat162_rn(acc.x, acc.y), b23 = __floats2bfloat162_rn(acc.z, acc.w);
+        uint2 w;
+        w.x = *reinterpret_cast<const uint32_t*>(&b01);
+        w.y = *reinterpret_cast<const uint32_t*>(&b23);
+        *reinterpret_cast<uint2*>(dst + static_cast<long>(pos - row0) * a.H + ft * 128 + f4 * 4) = w;
+      }
     }
   }
-  if (split) cluster_sync_all();  // the peers' shared memory stays valid until the leader has read it
+  if (split) cluster_sync_all();  // every CTA's shared memory stays valid until its peers have read it
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
