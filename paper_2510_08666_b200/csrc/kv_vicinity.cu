@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(128, 1)
     prefetch_tmap(&map_q);
     prefetch_tmap(&map_k);
     prefetch_tmap(&map_v);
-    for (int i = 0; i < 3; ++i) mbar_init(&bar[i], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(&misc[0], kTcCols);
@@ -335,12 +335,15 @@ __global__ void __launch_bounds__(128, 1)
   if (threadIdx.x == 0) {
     const uint64_t pol = policy_evict_normal();
     grid_dep_wait();  // PDL: Q and the refreshed cache rows of kv_proj_tc are complete
-    mbar_expect_tx(&bar[0], 2 * kQBlk + 4 * kKBlk);
+    // Q + K on bar[0] (S = Q K^T starts when they land), V on bar[3] (needed
+    // only after the softmax)
+    mbar_expect_tx(&bar[0], 2 * kQBlk + 2 * kKBlk);
+    mbar_expect_tx(&bar[3], 2 * kKBlk);
     for (int j = 0; j < 2; ++j) {
       tma_load_2d(sQ + j * kQBlk, &map_q, &bar[0], head * kD + 64 * j, q0, pol);
       tma_load_2d(sK + j * kKBlk, &map_k, &bar[0], head * kD + 64 * j, k0, pol);
-      tma_load_2d(sV + j * kKBlk, &map_v, &bar[0], head * kD + 64 * j, k0, pol);
     }
+    for (int j = 0; j < 2; ++j) tma_load_2d(sV + j * kKBlk, &map_v, &bar[3], head * kD + 64 * j, k0, pol);
     mbar_wait(&bar[0], 0);
     tc_fence_after();
     const uint32_t idesc_s = idesc_bf16(kTQ, kTK, false, false);
@@ -399,6 +402,8 @@ __global__ void __launch_bounds__(128, 1)
     // 128-B rows of 64 d per key, 8-key atoms 1 KB apart (SBO), the two 64-d
     // blocks kKBlk apart (LBO)
     const uint32_t idesc_o = idesc_bf16(kTQ, kD, false, /*b MN-major*/ true);
+    mbar_wait(&bar[3], 0);  // V landed
+    tc_fence_after();
 #pragma unroll
     for (int kb = 0; kb < kTK / 64; ++kb)
 #pragma unroll
