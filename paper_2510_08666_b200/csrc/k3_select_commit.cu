@@ -524,47 +524,49 @@ DI void select_block(const K3Args& a, int c, unsigned long long* tr) {
 // the rows it covers itself (one warp per row), so it does not wait for the
 // selection; rows undecided at step START are written (e_{t+1} matters for
 // those still undecided after the commit).
-// Partials p = grp, grp + kSmGroups, ... of element (s, h..h+3), kB loads in
-// flight per round, accumulated in that fixed order with an online rescale to
-// the running max: pacc = sum_p e^{m_p - mrun} acc_p.
+// Partials p = grp, grp + kSmGroups, ... of element (s, h..h+3), all loads of
+// a round issued before any use, merged relative to the round's max M of the
+// partial maxima: pacc = sum_p e^{m_p - M} acc_p (fixed order; a later round,
+// only for nparts > kB * kSmGroups, rescales the running sum).  Two passes over
+// registers, no data-dependent branches: the online-rescale form this replaces
+// was ~2 K SASS instructions of K34's i-cache-bound smoothing path (ncu:
+// 35 % of K34's stall samples "no instruction").
 template <int kB, bool kHalf>
 DI void accumulate_parts(const K4Args& a, int s, int h, int grp, float4& pacc, float& mrun) {
   static_assert(kHalf, "fp32 partials arrive as rank records (accumulate_recs)");
-  const long base = static_cast<long>(s) * a.H + h;
-  // all kB loads are issued before any use (raw fp16 words are converted in
-  // the combine loop, so no conversion waits on a load between two issues)
-  using Raw = typename std::conditional<kHalf, uint2, float4>::type;
-  Raw raw[kB];
-  float mp[kB];
   const uint64_t pol = policy_evict_first();  // read once
+  const long step = static_cast<long>(kSmGroups) * a.acc_stride;
+  const uint16_t* src = a.acc_h + static_cast<long>(s) * a.H + h + grp * a.acc_stride;
+  const float* msrc = a.m_part + grp * a.m_stride + static_cast<long>(s) * a.m_rowstride;
+  const long mstep = static_cast<long>(kSmGroups) * a.m_stride;
   for (int p0 = grp; p0 < a.nparts; p0 += kB * kSmGroups) {
+    uint2 raw[kB];
+    float mp[kB];
 #pragma unroll
     for (int j = 0; j < kB; ++j) {
-      const int p = p0 + j * kSmGroups;
-      const bool ok = p < a.nparts;
-      if constexpr (kHalf)
-        raw[j] = ok ? ld_global_hint_v2(a.acc_h + base + p * a.acc_stride, pol) : make_uint2(0u, 0u);
-      else
-        raw[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-      mp[j] = ok ? a.m_part[p * a.m_stride + static_cast<long>(s) * a.m_rowstride] : neg_inf();
+      const bool ok = p0 + j * kSmGroups < a.nparts;
+      raw[j] = ok ? ld_global_hint_v2(src + j * step, pol) : make_uint2(0u, 0u);
+      mp[j] = ok ? msrc[j * mstep] : neg_inf();
     }
+    src += kB * step;
+    msrc += kB * mstep;
+    float M = mrun;
 #pragma unroll
-    for (int j = 0; j < kB; ++j) {  // fixed summation order
-      if (mp[j] == neg_inf()) continue;  // past the last partial (or an empty one)
-      float4 vj;
-      if constexpr (kHalf)
-        vj = unpack_half4(raw[j]);
-      else
-        vj = raw[j];
-      if (mp[j] > mrun) {
-        const float r = __expf(mrun - mp[j]);
-        pacc.x *= r;
-        pacc.y *= r;
-        pacc.z *= r;
-        pacc.w *= r;
-        mrun = mp[j];
-      }
-      const float sc = __expf(mp[j] - mrun);
+    for (int j = 0; j < kB; ++j) M = fmaxf(M, mp[j]);
+    if (M == neg_inf()) continue;  // no partial in this round (or all empty)
+    if (mrun != neg_inf() && M != mrun) {
+      const float r = __expf(mrun - M);
+      pacc.x *= r;
+      pacc.y *= r;
+      pacc.z *= r;
+      pacc.w *= r;
+    }
+    mrun = M;
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {  // fixed summation order; an empty partial (m = -inf) adds exactly 0
+      const bool live = mp[j] != neg_inf();
+      const float4 vj = unpack_half4(live ? raw[j] : make_uint2(0u, 0u));
+      const float sc = live ? __expf(mp[j] - M) : 0.f;
       pacc.x = fmaf(vj.x, sc, pacc.x);
       pacc.y = fmaf(vj.y, sc, pacc.y);
       pacc.z = fmaf(vj.z, sc, pacc.z);
