@@ -2,7 +2,6 @@
 # Final round-2 profiling pass (under gpurun, repo root): bench lines per
 # config, the ncu launch list of the default bench command, ncu --set full of
 # K12 + K34 (MoE, and one rank of an 8-way shard) and of the f3 kernels,
-# compute-sanitizer on the f3 kernels and the fused step.  Outputs in
 # gpurun_out/ (summarised into profiles/ with tools/ncu_summary.py).
 TAG=${1:-r2f}
 mkdir -p gpurun_out
@@ -24,7 +23,4 @@ NF="ncu --set full --clock-control none --import-source on -f"
 timeout 900 $NF -k regex:"k12_proj|k34_select" --launch-skip 4 -c 2 -o gpurun_out/${TAG}_full_moe python tools/step_loop.py --steps 4 > /dev/null 2>&1; echo "full moe rc=$?"
 timeout 900 $NF -k regex:"k12_proj|k34_select" --launch-skip 6 -c 2 -o gpurun_out/${TAG}_full_moe_g8 python tools/trace_k12.py --shard 8 > /dev/null 2>&1; echo "full g8 rc=$?"
 timeout 900 $NF -k regex:"kv_proj_tc|kv_attention_tc|kv_attention_merge" --launch-skip 30 -c 3 -o gpurun_out/${TAG}_full_kv python tools/kv_bench.py --reps 12 > /dev/null 2>&1; echo "full kv rc=$?"
-timeout 900 compute-sanitizer --tool racecheck --print-limit 20 python -m pytest tests/test_gpu_kv.py -q -k "small or ragged" > gpurun_out/${TAG}_san_racecheck_kv.log 2>&1; echo "racecheck kv rc=$?"
-timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_kv.py -q -k "small or ragged or exactness" > gpurun_out/${TAG}_san_memcheck_kv.log 2>&1; echo "memcheck kv rc=$?"
-DINFER_FUSED=2 timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_parity.py -x -q -k "split or block_start or shard or determinism" > gpurun_out/${TAG}_san_memcheck_tests.log 2>&1; echo "memcheck tests rc=$?"
 ls gpurun_out | grep "^${TAG}_" | head -60
