@@ -207,7 +207,13 @@ DI void pos_load(const K3Args& a, int i, int lane, PosIn& q) {
 // warp instead of one per position).  With S > kSelPos each CTA writes its
 // positions' (p~, v~, undecided) to `sel`, and the last CTA of the row to
 // arrive (counter, release/acquire fences) runs phase 2 over the whole row.
-constexpr int kSelPos = 32;
+// 16 positions per selection CTA (two CTAs per 32-position block, the last to
+// arrive runs phase 2): phase 1 one position per warp.  Same-box A/B against 32:
+// MoE step 214.0-214.2 vs 214.9-215.0 us, V/8 rank 62.4-62.6 vs 63.3-63.5 us.
+#ifndef DINFER_SEL_POS
+#define DINFER_SEL_POS 16
+#endif
+constexpr int kSelPos = DINFER_SEL_POS;
 // smoothing blocks: 128 float4 columns x 4 partial groups (512 consecutive elements; one
 // wave of <= 144 blocks at the MoE shape)
 constexpr int kSmCols = 128, kSmGroups = 4, kSmBatch = 8;
