@@ -2,7 +2,8 @@
 // threshold / hierarchical selection, commit.  K4 smooth_finalize -- the
 // iteration-smoothing output e_{t+1} for positions still masked.
 //
-// K3: one CTA per batch row.  Phase 1 is warp-per-position / lane-per-slot:
+// K3: kSelPos (16) positions per CTA, the last CTA of a batch row to finish
+// phase 1 runs phase 2 for the row.  Phase 1 is warp-per-position / lane-per-slot:
 //   combine   m = max_r m_r, v* = v*_r of the maximiser (lowest id on ties),
 //             l = sum_r l_r e^{m_r - m} in rank order; lse = m + ln l; p* = 1/l
 //
@@ -200,8 +201,7 @@ DI void pos_load(const K3Args& a, int i, int lane, PosIn& q) {
   stats_load(a, i, lane, q.st);
 }
 
-// Selection CTAs: phase 1 covers kSelPos positions per CTA (one CTA per
-// batch row up to S = 32: no cross-CTA hand-off), each warp a strided subset
+// Selection CTAs: phase 1 covers kSelPos positions per CTA, each warp a strided subset
 // of them with the next position's loads issued before the current one is
 // processed (the per-position chain is latency-bound: one round trip per
 // warp instead of one per position).  With S > kSelPos each CTA writes its
