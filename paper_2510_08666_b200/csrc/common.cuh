@@ -124,6 +124,16 @@ DI uint2 ld_global_hint_v2(const void* ptr, uint64_t pol) {
   return v;
 }
 // 2-D tile load global -> shared (c0 = innermost coordinate), completes on `bar`.
+// Shared -> global tensor store of a box (bulk async group), with an L2 hint
+DI void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3, %4}], [%1], %5;" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+      : "memory");
+}
+DI void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+DI void bulk_wait_group_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 DI void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, uint64_t policy) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"

@@ -183,6 +183,8 @@ struct dinfer_ctx {
   CUtensorMap mc_map_w[kMapCache]{}, mc_map_w8[kMapCache]{}, mc_map_w32[kMapCache]{}, mc_map_e[kMapCache]{};
   int mc_next_w = 0, mc_next_e = 0;
   CUtensorMap map_w{}, map_w8{}, map_w32{}, map_h{}, map_e{}, map_f{};  // W boxes of 128 / 8 / 32 rows
+  CUtensorMap map_p{};  // K12 fp16 partials [VG][M][H], boxes [1][32][128] (TMA-store epilogue)
+  int part_tma = 0;     // K12 world-1 partials stored by TMA (env DINFER_K12_PART_TMA=0: thread stores)
   // timing
   int timing = 0;
   bool pdl = true;  // programmatic dependent launch between the step's kernels
@@ -230,6 +232,20 @@ bool encode_2d_f32(CUtensorMap* m, const void* base, uint64_t inner, uint64_t ou
   cuuint32_t es[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// 3-D fp16 tensor [d2][d1][d0] row-major, no swizzle, boxes [1][b1][b0] (K12's partial stores).
+bool encode_3d_f16(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1) {
+  auto fn = tmap_encoder();
+  if (fn == nullptr) return false;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {d0 * 2, d0 * d1 * 2};
+  cuuint32_t box[3] = {b0, b1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -436,6 +452,7 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
     b.trace = c->trace == nullptr ? nullptr : c->trace + 5 * c->k1_grid;
     b.stack = c->k12_stack;
     b.emin = c->k12_emin;
+    b.part_tma = c->part_tma;
     // record mode (sharded / split-phase; world 1 only with DINFER_K12_RECORD=1):
     // the accumulator goes into `rec`; otherwise per-group fp16 partials (K34 merges them)
     b.rec_acc = k12_record ? rec + c->stats_words : nullptr;
@@ -459,7 +476,7 @@ dinfer_status run_local(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
         b.probe = static_cast<volatile int*>(dp);
     }
     ev_begin(c, kPK1);
-    DI_CUDA(launch_k12(c->map_w, c->map_w32, c->map_h, c->map_e, c->map_f, a, b, c->k1_grid, c->f_smem, c->stream,
+    DI_CUDA(launch_k12(c->map_w, c->map_w32, c->map_h, c->map_e, c->map_f, c->map_p, a, b, c->k1_grid, c->f_smem, c->stream,
                        c->pdl));
     ev_finish(c, kPK1);
     return DINFER_OK;
@@ -1011,6 +1028,13 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
       !encode_2d_f32(&c->map_f, c->flog, static_cast<uint64_t>(s.V_local), static_cast<uint64_t>(M), c->k2_KV,
                      static_cast<uint32_t>(c->N)))
     st = DINFER_ERR_CUDA;
+  if (st == DINFER_OK && c->fused && c->part2 != nullptr && c->k2_HW % 128 == 0) {
+    c->part_tma = 1;
+    if (const char* e = std::getenv("DINFER_K12_PART_TMA")) c->part_tma = std::atoi(e) != 0;
+    if (c->part_tma && !encode_3d_f16(&c->map_p, c->part2, static_cast<uint64_t>(s.H), static_cast<uint64_t>(M),
+                                      static_cast<uint64_t>(c->k2_VG), 128, 32))
+      st = DINFER_ERR_CUDA;
+  }
   for (int i = 0; i < kNumPhases && st == DINFER_OK; ++i) {
     if (cudaEventCreate(&c->ev_beg[i]) != cudaSuccess || cudaEventCreate(&c->ev_end[i]) != cudaSuccess)
       st = DINFER_ERR_CUDA;

@@ -196,7 +196,8 @@ DI void advance(int& stage, uint32_t& phase, int n) {
 __global__ void __launch_bounds__(kThreads, 1)
     k12_proj_smooth(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_w32,
                     const __grid_constant__ CUtensorMap map_h, const __grid_constant__ CUtensorMap map_e,
-                    const __grid_constant__ CUtensorMap map_f, const K1Args a, const K2Args b) {
+                    const __grid_constant__ CUtensorMap map_f, const __grid_constant__ CUtensorMap map_p,
+                    const K1Args a, const K2Args b) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const Layout L = make_layout(a.N, b.HW, a.stages, b.pstages, a.slab_rows_max, b.emin);
@@ -288,6 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&map_h);
     prefetch_tmap(&map_e);
     prefetch_tmap(&map_f);
+    if (b.part_tma) prefetch_tmap(&map_p);
     for (int i = 0; i < a.stages; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -870,6 +872,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
   }
   if (threadIdx.x == 0) PROBE(5, 1);
+  unsigned long long t_epi = 0;
+  if (tr2 != nullptr && threadIdx.x == 0) t_epi = globaltimer_ns();
   const bool recmode = b.rec_acc != nullptr;
   float* rec_acc = b.rec_acc;
   if (recmode && b.rec_par > 0) rec_acc += (*reinterpret_cast<volatile unsigned*>(b.x.ctl) & 1u) * b.rec_par;
@@ -922,6 +926,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (g * 32 + jj < a.M) atomicAdd(dst + static_cast<long>(g * 32 + jj) * a.H, x[jj]);
           continue;
         }
+        if (b.part_tma) {
+          // fp16 rows [32 s][128 h] in their own 8-KB tile (the idle ring:
+          // one tile per (sub-tile, column group) of the warpgroup, never
+          // reused, so no wait before the next pass), stored by one TMA
+          // box per pass -- the thread-store version (fp32 tile, 8 B per
+          // thread store) took ~5 us per CTA after the last E MMA
+          __half* th = reinterpret_cast<__half*>(ring) + (wg * half * ng + (sub - sub0) * ng + g) * (32 * 128);
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) th[jj * 128 + wq * 32 + lane] = __float2half_rn(x[jj]);
+          fence_proxy_async();  // generic-proxy smem writes -> the TMA store
+          if (wg == 0) {
+            asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+          } else {
+            asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads) : "memory");
+          }
+          if (tg == 0) {  // rows past M are outside the map: not written
+            tma_store_3d(&map_p, th, hbase + sub * 128, g * 32, grp, pol_part);
+            bulk_commit_group();
+          }
+          continue;
+        }
         float* t = tile + (((sub - sub0) * ng + g) & 1) * (32 * 128);  // two tiles: one barrier per pass
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) t[jj * 128 + wq * 32 + lane] = x[jj];
@@ -933,7 +958,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int u = tg; u < 32 * 32; u += kEpiThreads) {
           const int row = u >> 5, c4 = u & 31;
           const int s = g * 32 + row;
-          if (s < a.M)
+          if (s < a.M && (a.xbits & 16) == 0)  // xbits 16: measurement only, partial stores skipped
             st_global_hint_v2(b.part + (static_cast<long>(grp) * a.M + s) * a.H + hbase + sub * 128 + c4 * 4,
                               pack_half4(*reinterpret_cast<const float4*>(t + row * 128 + c4 * 4)), pol_part);
         }
@@ -941,6 +966,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   if (recmode) __threadfence();  // this CTA's reductions before its count below
+  if (!recmode && b.part_tma && threadIdx.x % kEpiThreads == 0) bulk_wait_group_all();  // partials written
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -949,7 +975,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     a.wdur[gridDim.x + blockIdx.x] = static_cast<unsigned>(globaltimer_ns() - t_start);
   // trace: K2-slot exit = end of the partial write-out / reductions, K1-slot exit = kernel exit
   if (tr2 != nullptr && threadIdx.x == 0) {
-    tr2[0] = tr[2];
+    tr2[0] = t_epi;  // (measurement) write-out start
     tr2[3] = globaltimer_ns();
   }
   if (recmode && threadIdx.x == 0 && atomicAdd(b.rcnt + 2, 1u) == gridDim.x - 1) {
@@ -998,14 +1024,14 @@ int k12_blocks_per_sm(size_t smem) {
 }
 
 cudaError_t launch_k12(const CUtensorMap& map_w, const CUtensorMap& map_w32, const CUtensorMap& map_h,
-                       const CUtensorMap& map_e, const CUtensorMap& map_f, const K1Args& a, const K2Args& b, int grid,
-                       size_t smem, cudaStream_t st, bool pdl) {
+                       const CUtensorMap& map_e, const CUtensorMap& map_f, const CUtensorMap& map_p, const K1Args& a,
+                       const K2Args& b, int grid, size_t smem, cudaStream_t st, bool pdl) {
   {
     const cudaError_t e = ensure_func_smem(reinterpret_cast<const void*>(k12_proj_smooth), smem);
     if (e != cudaSuccess) return e;
   }
-  return launch_ex(k12_proj_smooth, dim3(grid), dim3(kThreads), smem, st, pdl, map_w, map_w32, map_h, map_e, map_f, a,
-                   b);
+  return launch_ex(k12_proj_smooth, dim3(grid), dim3(kThreads), smem, st, pdl, map_w, map_w32, map_h, map_e, map_f,
+                   map_p, a, b);
 }
 
 }  // namespace dinfer

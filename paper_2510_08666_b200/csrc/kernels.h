@@ -143,6 +143,7 @@ struct K2Args {
   volatile int* probe;     // K12 diagnostics (env DINFER_K12_PROBE): [grid][8] progress words in mapped host memory
   int stack;               // K12: hi / lo P tiles stacked into one 2N-column MMA (TMEM nsub x 2N per set)
   int emin;                // K12: minimum E-ring depth (the ring is sized for it)
+  int part_tma;            // K12 world-1 epilogue: fp16 partials stored by TMA (map_p) instead of thread stores
   // K12 record mode (rec_acc != nullptr): instead of per-group fp16 partials,
   // every CTA rescales its smoothing accumulator to the rank max m_rank (the
   // max of all slab maxima, gathered with atomicMax once every W phase is
@@ -171,8 +172,8 @@ size_t k12_smem_bytes(int N, int HW, int stages, int pstages, int slab_rows_max,
 // group wait for each other's W phase, so the whole grid must be resident).
 int k12_blocks_per_sm(size_t smem);
 cudaError_t launch_k12(const CUtensorMap& map_w, const CUtensorMap& map_w32, const CUtensorMap& map_h,
-                       const CUtensorMap& map_e, const CUtensorMap& map_f, const K1Args& a, const K2Args& b, int grid,
-                       size_t smem, cudaStream_t st, bool pdl);
+                       const CUtensorMap& map_e, const CUtensorMap& map_f, const CUtensorMap& map_p, const K1Args& a,
+                       const K2Args& b, int grid, size_t smem, cudaStream_t st, bool pdl);
 
 cudaError_t launch_rec_finalize(const RecArgs& a, cudaStream_t st, bool pdl);
 

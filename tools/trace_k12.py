@@ -60,7 +60,7 @@ def main():
     g = ctx.geometry()
     print(f"shard {G}: V_local {v1 - v0}, {R} weight copies, geometry {g}")
     cols = [("start", k1[:, 0]), ("first W stage", k1[:, 1]), ("W done", k1[:, 2]), ("first E MMA", k2[:, 1]),
-            ("E MMAs done", k2[:, 2]), ("record added", k2[:, 3]), ("exit", k1[:, 3])]
+            ("E MMAs done", k2[:, 2]), ("write-out start", k2[:, 0]), ("record added", k2[:, 3]), ("exit", k1[:, 3])]
     for n, c in cols:
         x = us(c)
         print(f"  {n:16s} min {x.min():7.1f}  p10 {np.percentile(x, 10):7.1f}  med {np.median(x):7.1f}  "
