@@ -83,9 +83,11 @@ def moe():
     return dict(W=W, E=E, h=h, p=p, res=res, excl=excl, mask=mask, dev=dev)
 
 
-def test_headline_loop_block_start_calibrated(moe):
-    """Loop A: dinfer_balance(back_to_back) then block_start steps back to back
-    on garbage state; each step equals the oracle's first iteration."""
+@pytest.mark.parametrize("calibrated", [False, True])
+def test_headline_loop_block_start_calibrated(moe, calibrated):
+    """Loop A: block_start steps back to back on garbage state, with the even K12
+    partition (bench.py's default) and after dinfer_balance(back_to_back)
+    (`--balance`); each step equals the oracle's first iteration."""
     import torch
     from paper_2510_08666_b200 import Context, make_params
     d = moe["dev"]
@@ -93,8 +95,9 @@ def test_headline_loop_block_start_calibrated(moe):
     assert ctx.geometry()["fused"] == 1  # K12, the kernel the bench's roofline names
     gp = gpu_params(moe["p"])
     from paper_2510_08666_b200 import DInferError
-    try:  # bench.py calibrates when the geometry supports it (two slabs per vocab group)
-        ctx.balance(d["h"], d["W"], d["E"], d["em"], gp, iters=4, mode="back_to_back")
+    try:  # --balance calibrates when the geometry supports it (two slabs per vocab group)
+        if calibrated:
+            ctx.balance(d["h"], d["W"], d["E"], d["em"], gp, iters=4, mode="back_to_back")
     except DInferError as e:
         assert e.status == 6 and ctx.geometry()["k2_hw"] * 2 != H  # UNSUPPORTED only for HS != 2
     pbs = gpu_params(moe["p"])
