@@ -65,6 +65,8 @@ struct dinfer_ctx {
   size_t smem_optin = 0;
   cudaStream_t stream = nullptr;
   bool has_comm = false;
+  bool nccl_world1 = false;  // test hook (env DINFER_NCCL_WORLD1=1): a one-rank communicator, world-1 steps
+                             // through the sharded NCCL path (record mode, ncclAllGather, K34 over the records)
 #ifdef DINFER_WITH_NCCL
   ncclComm_t comm = nullptr;
 #endif
@@ -1046,6 +1048,16 @@ dinfer_status dinfer_create(const dinfer_shape* shape, const uint8_t* nccl_uniqu
     if (ncclCommInitRank(&c->comm, s.world, id, s.rank) != ncclSuccess) st = DINFER_ERR_NCCL;
     else c->has_comm = true;
   }
+  if (st == DINFER_OK && s.world == 1 && std::getenv("DINFER_NCCL_WORLD1") &&
+      std::atoi(std::getenv("DINFER_NCCL_WORLD1")) != 0) {
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess || ncclCommInitRank(&c->comm, 1, id, 0) != ncclSuccess) {
+      st = DINFER_ERR_NCCL;
+    } else {
+      c->has_comm = true;
+      c->nccl_world1 = true;
+    }
+  }
 #else
   (void)nccl_unique_id;
 #endif
@@ -1577,7 +1589,7 @@ dinfer_status step_impl(dinfer_ctx* c, const uint16_t* hidden, const uint16_t* W
   // into the step's record (record mode); K34 zeroes it after use
   const bool k12 = smooth && c->fused;
   const size_t words = smooth ? c->full_words : c->stats_words;
-  if (world == 1) {
+  if (world == 1 && !c->nccl_world1) {
     // K34 merges the slab partials (stats) itself, and the per-group fp16
     // smoothing partials (a fixed-order merge: bitwise reproducible) -- or,
     // with DINFER_K12_RECORD=1, reads K12's one fp32 record (L2 reductions,

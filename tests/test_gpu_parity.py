@@ -778,3 +778,29 @@ def test_k12_reference_switch_for_far_larger_partner_max(torch_cuda, monkeypatch
     ctx.sync()
     compare(st.snapshot(), res, mask, p, where="reference switch")
     ctx.close()
+
+
+def test_nccl_allgather_path_one_rank(torch_cuda, monkeypatch):
+    """The NCCL fallback exchange (BJ:5: records combined with NCCL) on a
+    one-rank communicator (the only NCCL topology one GPU allows: NCCL rejects
+    two ranks on one device): K12 in record mode, ncclAllGather of the packed
+    rank record, K34 over the gathered records -- against the oracle along a
+    vetted trajectory, and the allgather phase actually timed."""
+    from paper_2510_08666_b200 import Context
+    monkeypatch.setenv("DINFER_NCCL_WORLD1", "1")
+    run_trajectory(torch_cuda, 4096, 1024, 1, 32, 32, 8, hier_credit_smooth, True, max_iters=4)
+    run_trajectory(torch_cuda, 1000, 384, 3, 20, 24, 5, hier_credit_smooth, True, max_iters=4)
+    # the step went through the allgather
+    V, H, B, S, K = 4096, 1024, 1, 32, 32
+    W, E = weights(V, H)
+    ctx = Context(B, S, H, K, V, smooth_capable=True)
+    ctx.set_timing(True)
+    st = GpuState(B, S, H, K, synth.mask_id(V))
+    h = to_dev_bf16(synth.planted_hidden(W, B * S, seed=3))
+    p = gpu_params(hier_credit_smooth(0))
+    ctx.step(h, to_dev_bf16(W), to_dev_bf16(E), to_dev_bf16(E[synth.mask_id(V)]), st.mask, st.tokens, st.cids,
+             st.cval, p, st.committed, st.smoothed, st.stats)
+    torch_cuda.cuda.synchronize()
+    ctx.sync()
+    assert ctx.get_timing()["c1_allgather"] > 0.0
+    ctx.close()
