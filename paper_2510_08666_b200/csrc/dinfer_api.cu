@@ -141,9 +141,16 @@ struct dinfer_ctx {
   uint8_t* st_host = nullptr;   // pinned host mirror of st_block
   float* st_smoothed = nullptr;
   // dinfer_step_host replays a captured CUDA graph of its whole sequence
-  cudaGraphExec_t host_graph = nullptr;
-  uint64_t host_graph_key[12] = {};
-  bool host_graph_failed = false;
+  // dinfer_step_host graphs, keyed by everything baked into the capture; a few
+  // are kept (LRU) so callers that rotate buffers (weight copies, double-
+  // buffered inputs) do not re-capture on every call
+  static constexpr int kHostGraphs = 4;
+  cudaGraphExec_t host_graph_c[kHostGraphs] = {};
+  uint64_t host_graph_key_c[kHostGraphs][12] = {};
+  bool host_graph_failed_c[kHostGraphs] = {};
+  bool host_graph_used[kHostGraphs] = {};
+  unsigned long long host_graph_tick[kHostGraphs] = {};
+  unsigned long long host_graph_clock = 0;
   cudaStream_t cap_stream = nullptr;  // private capture stream
   const float* zc_host = nullptr;     // smoothed_h whose device mapping zc_dev was looked up
   float* zc_dev = nullptr;
@@ -717,7 +724,8 @@ void dinfer_destroy(dinfer_ctx* c) {
   if (c->rec_all != nullptr && c->rec_all != c->rec_local) cudaFree(c->rec_all);
   if (c->st_host != nullptr) cudaFreeHost(c->st_host);
   if (c->probe_h != nullptr) cudaFreeHost(c->probe_h);
-  if (c->host_graph != nullptr) cudaGraphExecDestroy(c->host_graph);
+  for (int i = 0; i < dinfer_ctx::kHostGraphs; ++i)
+    if (c->host_graph_c[i] != nullptr) cudaGraphExecDestroy(c->host_graph_c[i]);
   if (c->gen_exec != nullptr) cudaGraphExecDestroy(c->gen_exec);
   if (c->cap_stream != nullptr) cudaStreamDestroy(c->cap_stream);
   for (int i = 0; i < kNumPhases; ++i) {
@@ -1790,12 +1798,23 @@ dinfer_status dinfer_step_host_async(dinfer_ctx* c, const uint16_t* hidden_h, co
                                 8 * static_cast<uint64_t>(static_cast<uint32_t>(p->block_start ? p->mask_id : 0))};
   // timing events / NCCL: plain enqueue; a key whose capture failed (e.g. pageable
   // host buffers) also stays on the plain path
-  const bool same_key = std::memcmp(key, c->host_graph_key, sizeof(key)) == 0;
-  bool use_graph = !c->timing && c->shp.world == 1 && !(same_key && c->host_graph_failed) && c->host_graph_ok;
-  if (use_graph && (c->host_graph == nullptr || !same_key)) {
-    if (c->host_graph != nullptr) {
-      cudaGraphExecDestroy(c->host_graph);
-      c->host_graph = nullptr;
+  int slot = -1;
+  for (int i = 0; i < dinfer_ctx::kHostGraphs && slot < 0; ++i)
+    if (c->host_graph_used[i] && std::memcmp(key, c->host_graph_key_c[i], sizeof(key)) == 0) slot = i;
+  const bool same_key = slot >= 0;
+  bool use_graph = !c->timing && c->shp.world == 1 && !(same_key && c->host_graph_failed_c[slot]) && c->host_graph_ok;
+  if (use_graph && !same_key) {  // capture into an empty or the least recently used slot
+    slot = 0;
+    for (int i = 0; i < dinfer_ctx::kHostGraphs; ++i) {
+      if (!c->host_graph_used[i]) {
+        slot = i;
+        break;
+      }
+      if (c->host_graph_tick[i] < c->host_graph_tick[slot]) slot = i;
+    }
+    if (c->host_graph_c[slot] != nullptr) {
+      cudaGraphExecDestroy(c->host_graph_c[slot]);
+      c->host_graph_c[slot] = nullptr;
     }
     cudaGraph_t g = nullptr;
     // capture on a private stream (the legacy default stream cannot be
@@ -1824,18 +1843,20 @@ dinfer_status dinfer_step_host_async(dinfer_ctx* c, const uint16_t* hidden_h, co
       cudaGetLastError();
       return st;
     }
-    std::memcpy(c->host_graph_key, key, sizeof(key));
-    c->host_graph_failed = !ok || ee != cudaSuccess || g == nullptr ||
-                           cudaGraphInstantiate(&c->host_graph, g, 0) != cudaSuccess;
+    std::memcpy(c->host_graph_key_c[slot], key, sizeof(key));
+    c->host_graph_used[slot] = true;
+    c->host_graph_failed_c[slot] = !ok || ee != cudaSuccess || g == nullptr ||
+                                   cudaGraphInstantiate(&c->host_graph_c[slot], g, 0) != cudaSuccess;
     if (g != nullptr) cudaGraphDestroy(g);
-    if (c->host_graph_failed) {
-      c->host_graph = nullptr;
+    if (c->host_graph_failed_c[slot]) {
+      c->host_graph_c[slot] = nullptr;
       cudaGetLastError();
       use_graph = false;
     }
   }
   if (use_graph) {
-    DI_CUDA(cudaGraphLaunch(c->host_graph, sm));
+    c->host_graph_tick[slot] = ++c->host_graph_clock;
+    DI_CUDA(cudaGraphLaunch(c->host_graph_c[slot], sm));
   } else {
     DI_CUDA(stage_in(sm));
     s = dinfer_step(c, c->st_hidden, W, E, e_mask, d + o_mask, reinterpret_cast<int32_t*>(d + o_tok),

@@ -453,6 +453,44 @@ def test_step_host_matches_device_step(torch_cuda):
         ctx.step_host_wait()  # nothing pending
 
 
+def test_step_host_graph_cache_rotating_weights(torch_cuda):
+    """dinfer_step_host keeps a few captured graphs (LRU, keyed by the baked-in
+    pointers and flags): callers rotating buffers -- here three weight sets,
+    two of them copies of the same weights at other addresses, one different,
+    more sets than cache slots in the second round -- must get, on every call,
+    exactly the device step on the weights they passed."""
+    import torch
+    from paper_2510_08666_b200 import Context
+    V, H, B, S, K = 2048, 256, 1, 32, 8
+    sets = []
+    for seed_w in (0, 0, 5, 0, 7, 5):  # 6 buffers, 3 distinct weight sets
+        W, E = weights(V, H) if seed_w == 0 else (synth.make_W(V, H, seed_w), synth.make_E(V, H, seed_w + 1))
+        sets.append((W, to_dev_bf16(W), to_dev_bf16(E), to_dev_bf16(E[V - 1])))
+    p = gpu_params(O.Params(decoder=O.DEC_HIERARCHICAL, use_credit=True, use_smooth=True, alpha_t=0.2))
+    ctx_d, ctx_h = Context(B, S, H, K, V), Context(B, S, H, K, V)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    mask, tok = pin(np.ones((B, S), np.uint8)), pin(np.full((B, S), V - 1, np.int32))
+    cids, cval = pin(np.full((B, S, K), -1, np.int32)), pin(np.zeros((B, S, K), np.float32))
+    com, sts = pin(np.zeros((B, S), np.uint8)), pin(np.zeros((B, S, 4), np.float32))
+    sm = pin(np.full((B, S, H), np.nan, np.float32))
+    for it, i in enumerate([0, 1, 2, 0, 1, 2, 3, 4, 5, 0, 4, 2]):
+        W, Wd, Ed, emd = sets[i]
+        h = synth.planted_hidden(W, B * S, seed=60 + it)
+        hh = pin(h.view(np.int16))
+        st = GpuState(B, S, H, K, V - 1)
+        ctx_d.step(to_dev_bf16(h), Wd, Ed, emd, st.mask, st.tokens, st.cids, st.cval, p, st.committed, st.smoothed,
+                   st.stats)
+        torch.cuda.synchronize()
+        dev = st.snapshot()
+        mask.fill_(1); tok.fill_(V - 1); cids.fill_(-1); cval.zero_(); com.zero_(); sm.fill_(float("nan"))
+        ctx_h.step_host(hh, Wd, Ed, emd, mask, tok, cids, cval, p, com, sm, sts)
+        assert np.array_equal(com.numpy().astype(bool), dev["committed"]), it
+        assert np.array_equal(tok.numpy(), dev["tokens"]), it
+        assert np.array_equal(cids.numpy(), dev["cids"]) and np.array_equal(cval.numpy(), dev["cval"]), it
+        still = mask.numpy().astype(bool)
+        assert np.array_equal(sm.numpy()[still], dev["smoothed"][still]), it
+
+
 @pytest.mark.parametrize("pinned", [True, False])
 def test_step_host_graph_replay_follows_schedules(torch_cuda, pinned):
     """dinfer_step_host replays one captured CUDA graph across iterations; the
