@@ -1802,7 +1802,10 @@ dinfer_status dinfer_step_host_async(dinfer_ctx* c, const uint16_t* hidden_h, co
   for (int i = 0; i < dinfer_ctx::kHostGraphs && slot < 0; ++i)
     if (c->host_graph_used[i] && std::memcmp(key, c->host_graph_key_c[i], sizeof(key)) == 0) slot = i;
   const bool same_key = slot >= 0;
-  bool use_graph = !c->timing && c->shp.world == 1 && !(same_key && c->host_graph_failed_c[slot]) && c->host_graph_ok;
+  // world > 1: only with the peer-memory exchange (all its state lives on the
+  // device: the epoch, the flags, the peers' pointers fixed at exchange_open)
+  bool use_graph = !c->timing && (c->shp.world == 1 || c->p2p) && !(same_key && c->host_graph_failed_c[slot]) &&
+                   c->host_graph_ok;
   if (use_graph && !same_key) {  // capture into an empty or the least recently used slot
     slot = 0;
     for (int i = 0; i < dinfer_ctx::kHostGraphs; ++i) {

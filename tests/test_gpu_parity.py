@@ -842,3 +842,49 @@ def test_nccl_allgather_path_one_rank(torch_cuda, monkeypatch):
     ctx.sync()
     assert ctx.get_timing()["c1_allgather"] > 0.0
     ctx.close()
+
+
+def test_step_host_graph_sharded_loopback(torch_cuda):
+    """dinfer_step_host at world 2 with the peer-memory exchange (loopback: the
+    rank's own record stands for both) replays captured graphs too: each call
+    equals the device step of a second context -- decisions and credit slots
+    bitwise, smoothed within 1e-5 (the record's fp32 L2 reductions are
+    reproducible to rounding order only)."""
+    import torch
+    from paper_2510_08666_b200 import Context
+    V, H, B, S, K, G = 8192, 2048, 1, 32, 8, 2
+    W, E = weights(V, H)
+    Vl = V // G
+    Wd, Ed = to_dev_bf16(W[:Vl]), to_dev_bf16(E[:Vl])
+    emd = to_dev_bf16(E[V - 1])
+    p = gpu_params(O.Params(decoder=O.DEC_HIERARCHICAL, use_credit=True, use_smooth=True, alpha_t=0.2))
+    ctx_d = Context(B, S, H, K, V, V_local=Vl, v_offset=0, world=G, rank=0)
+    ctx_h = Context(B, S, H, K, V, V_local=Vl, v_offset=0, world=G, rank=0)
+    ctx_d.exchange_loopback()
+    ctx_h.exchange_loopback()
+    assert ctx_h.geometry()["fused"] == 1
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    mask, tok = pin(np.ones((B, S), np.uint8)), pin(np.full((B, S), V - 1, np.int32))
+    cids, cval = pin(np.full((B, S, K), -1, np.int32)), pin(np.zeros((B, S, K), np.float32))
+    com, sts = pin(np.zeros((B, S), np.uint8)), pin(np.zeros((B, S, 4), np.float32))
+    sm = pin(np.full((B, S, H), np.nan, np.float32))
+    for it in range(4):
+        h = synth.planted_hidden(W, B * S, seed=80 + it)
+        st = GpuState(B, S, H, K, V - 1)
+        ctx_d.step(to_dev_bf16(h), Wd, Ed, emd, st.mask, st.tokens, st.cids, st.cval, p, st.committed, st.smoothed,
+                   st.stats)
+        torch.cuda.synchronize()
+        ctx_d.sync()
+        dev = st.snapshot()
+        mask.fill_(1); tok.fill_(V - 1); cids.fill_(-1); cval.zero_(); com.zero_(); sm.fill_(float("nan"))
+        ctx_h.step_host(pin(h.view(np.int16)), Wd, Ed, emd, mask, tok, cids, cval, p, com, sm, sts)
+        ctx_h.sync()
+        assert np.array_equal(com.numpy().astype(bool), dev["committed"]), it
+        assert np.array_equal(tok.numpy(), dev["tokens"]), it
+        assert np.array_equal(cids.numpy(), dev["cids"]), it
+        assert np.allclose(cval.numpy(), dev["cval"], rtol=1e-6, atol=0), it
+        still = mask.numpy().astype(bool)
+        a, b = sm.numpy()[still], dev["smoothed"][still]
+        assert np.all(np.linalg.norm(a - b, axis=-1) <= 1e-5 * np.linalg.norm(b, axis=-1)), it
+    ctx_d.close()
+    ctx_h.close()
