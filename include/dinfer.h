@@ -191,12 +191,14 @@ dinfer_status dinfer_step_embed(dinfer_ctx* ctx, const uint16_t* hidden, const u
  * numeric params, mask, tokens, credit table) packed through one pinned
  * staging block into one H2D copy; one D2H copy of the packed state +
  * committed + stats; smoothed (M*H*4 B) directly into smoothed_h.
- * On a single-rank ctx with timing off, the whole sequence (copies and
- * kernels) is captured once into a CUDA graph and replayed; the numeric
- * params (tau, theta_*, c_*, alpha_t) are read on device from the packed
- * block, so schedules never force a re-capture. A change of any pointer
- * argument or of decoder / hier_runs_after_hi / use_credit / use_smooth /
- * stats_h nullness re-captures. Buffers the graph cannot capture (pageable
+ * On a single-rank ctx, or a sharded one whose exchange is peer memory
+ * (dinfer_exchange_open / _loopback), with timing off, the whole sequence
+ * (copies and kernels) is captured into a CUDA graph and replayed; the
+ * numeric params (tau, theta_*, c_*, alpha_t) are read on device from the
+ * packed block, so schedules never force a re-capture. The graph is keyed by
+ * every pointer argument and by decoder / hier_runs_after_hi / use_credit /
+ * use_smooth / stats_h nullness; the ctx keeps the 4 most recently used
+ * graphs, so callers rotating a few buffers replay without re-capturing. Buffers the graph cannot capture (pageable
  * host memory) run the same sequence un-captured. hidden_h and smoothed_h
  * may be pageable; pinned buffers avoid a staging copy inside the driver,
  * and a pinned smoothed_h is written by the kernel directly (zero-copy; no
