@@ -118,6 +118,12 @@ DI void st_global_hint_v2(void* ptr, uint2 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(ptr), "r"(v.x), "r"(v.y), "l"(pol)
                : "memory");
 }
+// 4-byte store with an L2 policy (the staged logits: evict_last, so they stay
+// in L2 -- and, rewritten at the same addresses every step, are never written
+// back -- instead of being evicted by the weight streams)
+DI void st_global_hint_f32(float* ptr, float v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(ptr), "f"(v), "l"(pol) : "memory");
+}
 DI uint2 ld_global_hint_v2(const void* ptr, uint64_t pol) {
   uint2 v;
   asm volatile("ld.global.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(ptr), "l"(pol));

@@ -579,6 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       Rl[g] = 0.f;
     }
     const bool up16 = lane & 16, up8 = lane & 8, up4 = lane & 4, up2 = lane & 2, up1 = lane & 1;
+    const uint64_t pol_flog = (a.xbits & 64) ? policy_evict_normal() : policy_evict_last();  // 64: old policy (A/B)
     const int stride = kStatWords + a.K;
     for (int t = 0; t < ntiles; ++t) {
       const int buf = t & 1;
@@ -606,7 +607,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const int col = g * 32 + j;
-              if (col < a.M) a.flog[static_cast<long>(col) * a.V_local + lv] = x[j];
+              if (col < a.M) st_global_hint_f32(a.flog + static_cast<long>(col) * a.V_local + lv, x[j], pol_flog);
             }
           }
           for (int e = ent0; e >= 0; e = ent_next[e]) {
